@@ -192,10 +192,11 @@ static void m2l_t(const mtab* t, const double* M, const double d[3], double* L) 
     for (int a = 0; a < t->ncoef; ++a) {
         const int* ea = t->ex[a];
         int na = ea[0] + ea[1] + ea[2];
-        for (int b = 0; b < t->ncoef; ++b) {
+        /* beta with |beta| <= P-1-|alpha| are exactly the first ncoef(P-|alpha|) entries (R11) */
+        int nbeta = ofmm_ncoef(t->P - na);
+        for (int b = 0; b < nbeta; ++b) {
             const int* eb = t->ex[b];
             int nb = eb[0] + eb[1] + eb[2];
-            if (na + nb > t->P - 1) continue;
             double sign = (nb % 2) ? -1.0 : 1.0;
             L[a] += sign * M[b] * D[t->idx[ea[0] + eb[0]][ea[1] + eb[1]][ea[2] + eb[2]]];
         }

@@ -1,0 +1,361 @@
+// capi.cu -- the extern "C" boundary of libfmm (include/fmm.h): context, build, evaluate,
+// introspection, timing.  Every step of the path runs in this library's kernels; there is
+// no CPU fallback (a missing device is an FMM_ERR_CUDA).
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+#define FMM_VERSION 1
+
+namespace {
+const char* kPhaseNames[PH_COUNT] = {"bounds", "sort", "tree", "geometry", "dtt", "lists",
+                                      "upward", "m2l", "p2p", "downward", "copy"};
+
+fmm_status check_ctx(const fmm_ctx* ctx) { return ctx ? FMM_OK : FMM_ERR_ARG; }
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+}  // namespace
+
+fmm_status buf_ensure(fmm_ctx* ctx, DevBuf& b, size_t bytes, bool keep, cudaStream_t s) {
+    if (bytes <= b.bytes) return FMM_OK;
+    void* p = nullptr;
+    size_t nb = std::max(bytes, (size_t)256);
+    cudaError_t e = cudaMalloc(&p, nb);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        ctx->err = "cudaMalloc(" + std::to_string(nb) + " B) failed: " + cudaGetErrorString(e);
+        return FMM_ERR_OOM;
+    }
+    if (keep && b.p && b.bytes) {
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(p, b.p, b.bytes, cudaMemcpyDeviceToDevice, s));
+        FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    }
+    if (b.p) cudaFree(b.p);
+    b.p = p;
+    b.bytes = nb;
+    return FMM_OK;
+}
+
+void buf_free(DevBuf& b) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+}
+
+PhaseScope::PhaseScope(fmm_ctx* c, int ph, cudaStream_t st) : ctx(c), phase(ph), s(st) {
+    if (!ctx->timing) return;
+    if (ctx->event_pool.empty()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        ctx->event_pool.push_back(e);
+    }
+    a = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
+    cudaEventRecord(a, s);
+}
+
+PhaseScope::~PhaseScope() {
+    if (!ctx->timing || !a) return;
+    cudaEvent_t b;
+    if (ctx->event_pool.empty()) cudaEventCreate(&b);
+    else {
+        b = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+    }
+    cudaEventRecord(b, s);
+    ctx->pending.push_back({phase, a, b});
+}
+
+extern "C" {
+
+int fmm_version(void) { return FMM_VERSION; }
+
+fmm_status fmm_create(int64_t n_max, int p, double theta, int ncrit, int prec, int device, fmm_ctx** out) {
+    if (!out) return FMM_ERR_ARG;
+    *out = nullptr;
+    if (n_max < 0 || n_max >= ((int64_t)1 << 32) || p < 1 || p > FMM_MAXP || !(theta > 0.0 && theta < 1.0) ||
+        ncrit < 1 || (prec != FMM_F32 && prec != FMM_F64))
+        return FMM_ERR_ARG;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return FMM_ERR_CUDA;
+    }
+    fmm_ctx* ctx = new fmm_ctx();
+    ctx->n_max = n_max;
+    ctx->P = p;
+    ctx->ncoef = ncoef_of(p);
+    ctx->theta = theta;
+    ctx->ncrit = ncrit;
+    ctx->prec = prec;
+    ctx->device = device;
+    DeviceGuard g(device);
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+        delete ctx;
+        return FMM_ERR_CUDA;
+    }
+    ctx->num_sms = prop.multiProcessorCount;
+    if (cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        delete ctx;
+        return FMM_ERR_CUDA;
+    }
+    *out = ctx;
+    return FMM_OK;
+}
+
+fmm_status fmm_destroy(fmm_ctx* ctx) {
+    if (!ctx) return FMM_ERR_ARG;
+    DeviceGuard g(ctx->device);
+    cudaDeviceSynchronize();
+    DevBuf* bufs[] = {&ctx->root, &ctx->key_a, &ctx->key_b, &ctx->idx_a, &ctx->idx_b, &ctx->sort_counts,
+                      &ctx->scan_tmp, &ctx->red_tmp, &ctx->body, &ctx->c_key, &ctx->c_level, &ctx->c_bb,
+                      &ctx->c_bc, &ctx->c_cb, &ctx->c_cc, &ctx->c_parent, &ctx->c_bmin, &ctx->c_bmax, &ctx->c_cr,
+                      &ctx->split_tmp, &ctx->split_cnt, &ctx->leaf_ids, &ctx->fr_a, &ctx->fr_b, &ctx->lst_m2l,
+                      &ctx->lst_p2p, &ctx->lst_tmp, &ctx->m2l_src, &ctx->p2p_src, &ctx->m2l_off, &ctx->p2p_off,
+                      &ctx->cnt_tmp, &ctx->dcount, &ctx->M, &ctx->L, &ctx->Mr, &ctx->near_phi, &ctx->near_grad,
+                      &ctx->h_stage};
+    for (DevBuf* b : bufs) buf_free(*b);
+    for (auto& t : ctx->pending) {
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
+    }
+    for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    if (ctx->aux) cudaStreamDestroy(ctx->aux);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    delete ctx;
+    return FMM_OK;
+}
+
+const char* fmm_last_error(const fmm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+fmm_status fmm_build(fmm_ctx* ctx, const void* pos, int64_t n, void* stream) {
+    FMM_TRY(check_ctx(ctx));
+    ctx->err.clear();
+    if (n < 0 || n > ctx->n_max) {
+        ctx->err = "fmm_build: n out of range";
+        return FMM_ERR_ARG;
+    }
+    if (n > 0 && !pos) {
+        ctx->err = "fmm_build: null pos";
+        return FMM_ERR_ARG;
+    }
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    ctx->built = false;
+    ctx->evaluated = false;
+    ctx->n = n;
+    ctx->built_pos = pos;
+    ctx->ncell = ctx->nleaf = ctx->depth = ctx->n_m2l = ctx->n_p2p = ctx->p2p_inter = 0;
+    ctx->level_begin.clear();
+    if (n > 0) {
+        FMM_TRY(build_keys(ctx, pos, n, s));
+        FMM_TRY(build_tree(ctx, s));
+        FMM_TRY(build_lists(ctx, s));
+    }
+    ctx->built = true;
+    return FMM_OK;
+}
+
+fmm_status fmm_evaluate(fmm_ctx* ctx, const void* pos, const void* q, void* phi, void* grad, void* stream) {
+    FMM_TRY(check_ctx(ctx));
+    ctx->err.clear();
+    if (!ctx->built || pos != ctx->built_pos) {
+        ctx->err = "fmm_evaluate: no matching fmm_build for these positions";
+        return FMM_ERR_STATE;
+    }
+    if (ctx->n == 0) return FMM_OK;
+    if (!q || !phi || !grad) {
+        ctx->err = "fmm_evaluate: null pointer";
+        return FMM_ERR_ARG;
+    }
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    FMM_TRY(gather_bodies_q(ctx, q, s));
+    FMM_TRY(upward_pass(ctx, s));
+    // P2P on the aux stream concurrently with M2L on the caller's stream
+    FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
+    FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+    FMM_TRY(p2p_pass(ctx, ctx->aux));
+    FMM_TRY(m2l_pass(ctx, s));
+    FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, ctx->aux));
+    FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
+    FMM_TRY(downward_pass(ctx, phi, grad, s));
+    ctx->evaluated = true;
+    return FMM_OK;
+}
+
+fmm_status fmm_solve_host(fmm_ctx* ctx, const void* pos_h, const void* q_h, int64_t n, void* phi_h, void* grad_h,
+                          void* stream) {
+    FMM_TRY(check_ctx(ctx));
+    if (n < 0 || n > ctx->n_max || (n > 0 && (!pos_h || !q_h || !phi_h || !grad_h))) return FMM_ERR_ARG;
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t es = ctx->prec == FMM_F32 ? 4 : 8;
+    const size_t bpos = (size_t)n * 3 * es, bq = (size_t)n * es;
+    // staging: pos | q | phi | grad, each 256-B aligned
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    FMM_TRY(buf_ensure(ctx, ctx->h_stage, al(bpos) * 2 + al(bq) * 2 + 1024));
+    char* base = (char*)ctx->h_stage.p;
+    void* dpos = base;
+    void* dq = base + al(bpos);
+    void* dphi = base + al(bpos) + al(bq);
+    void* dgrad = base + al(bpos) + 2 * al(bq);
+    {
+        PhaseScope ps(ctx, PH_COPY, s);
+        if (n) FMM_CUDA_TRY(ctx, cudaMemcpyAsync(dpos, pos_h, bpos, cudaMemcpyHostToDevice, s));
+        if (n) FMM_CUDA_TRY(ctx, cudaMemcpyAsync(dq, q_h, bq, cudaMemcpyHostToDevice, s));
+    }
+    FMM_TRY(fmm_build(ctx, dpos, n, stream));
+    FMM_TRY(fmm_evaluate(ctx, dpos, dq, dphi, dgrad, stream));
+    {
+        PhaseScope ps(ctx, PH_COPY, s);
+        if (n) FMM_CUDA_TRY(ctx, cudaMemcpyAsync(phi_h, dphi, bq, cudaMemcpyDeviceToHost, s));
+        if (n) FMM_CUDA_TRY(ctx, cudaMemcpyAsync(grad_h, dgrad, bpos, cudaMemcpyDeviceToHost, s));
+    }
+    FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    return FMM_OK;
+}
+
+fmm_status fmm_get_counts(const fmm_ctx* ctx, fmm_counts* out) {
+    FMM_TRY(check_ctx(ctx));
+    if (!out) return FMM_ERR_ARG;
+    out->n = ctx->n;
+    out->ncell = ctx->ncell;
+    out->nleaf = ctx->nleaf;
+    out->depth = ctx->depth;
+    out->n_m2l = ctx->n_m2l;
+    out->n_p2p = ctx->n_p2p;
+    out->p2p_interactions = ctx->p2p_inter;
+    return FMM_OK;
+}
+
+fmm_status fmm_copy_sorted(const fmm_ctx* ctx_c, uint64_t* keys, uint32_t* perm) {
+    FMM_TRY(check_ctx(ctx_c));
+    fmm_ctx* ctx = const_cast<fmm_ctx*>(ctx_c);
+    if (!ctx->built) return FMM_ERR_STATE;
+    DeviceGuard g(ctx->device);
+    FMM_CUDA_TRY(ctx, cudaDeviceSynchronize());
+    if (ctx->n == 0) return FMM_OK;
+    if (keys) FMM_CUDA_TRY(ctx, cudaMemcpy(keys, ctx->d_keys, ctx->n * 8, cudaMemcpyDeviceToHost));
+    if (perm) FMM_CUDA_TRY(ctx, cudaMemcpy(perm, ctx->d_perm, ctx->n * 4, cudaMemcpyDeviceToHost));
+    return FMM_OK;
+}
+
+fmm_status fmm_copy_cells(const fmm_ctx* ctx_c, int32_t* level, uint64_t* key, uint32_t* body_begin,
+                          uint32_t* body_count, uint32_t* child_begin, uint32_t* child_count, int32_t* parent,
+                          double* bmin, double* bmax, double* center, double* radius) {
+    FMM_TRY(check_ctx(ctx_c));
+    fmm_ctx* ctx = const_cast<fmm_ctx*>(ctx_c);
+    if (!ctx->built) return FMM_ERR_STATE;
+    DeviceGuard g(ctx->device);
+    FMM_CUDA_TRY(ctx, cudaDeviceSynchronize());
+    const int64_t nc = ctx->ncell;
+    if (nc == 0) return FMM_OK;
+    if (level) FMM_CUDA_TRY(ctx, cudaMemcpy(level, ctx->c_level.p, nc * 4, cudaMemcpyDeviceToHost));
+    if (key) FMM_CUDA_TRY(ctx, cudaMemcpy(key, ctx->c_key.p, nc * 8, cudaMemcpyDeviceToHost));
+    if (body_begin) FMM_CUDA_TRY(ctx, cudaMemcpy(body_begin, ctx->c_bb.p, nc * 4, cudaMemcpyDeviceToHost));
+    if (body_count) FMM_CUDA_TRY(ctx, cudaMemcpy(body_count, ctx->c_bc.p, nc * 4, cudaMemcpyDeviceToHost));
+    if (child_begin) FMM_CUDA_TRY(ctx, cudaMemcpy(child_begin, ctx->c_cb.p, nc * 4, cudaMemcpyDeviceToHost));
+    if (child_count) FMM_CUDA_TRY(ctx, cudaMemcpy(child_count, ctx->c_cc.p, nc * 4, cudaMemcpyDeviceToHost));
+    if (parent) FMM_CUDA_TRY(ctx, cudaMemcpy(parent, ctx->c_parent.p, nc * 4, cudaMemcpyDeviceToHost));
+    if (bmin) FMM_CUDA_TRY(ctx, cudaMemcpy(bmin, ctx->c_bmin.p, nc * 24, cudaMemcpyDeviceToHost));
+    if (bmax) FMM_CUDA_TRY(ctx, cudaMemcpy(bmax, ctx->c_bmax.p, nc * 24, cudaMemcpyDeviceToHost));
+    if (center || radius) {
+        std::vector<double> cr((size_t)nc * 4);
+        FMM_CUDA_TRY(ctx, cudaMemcpy(cr.data(), ctx->c_cr.p, nc * 32, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < nc; ++i) {
+            if (center)
+                for (int d = 0; d < 3; ++d) center[3 * i + d] = cr[4 * i + d];
+            if (radius) radius[i] = cr[4 * i + 3];
+        }
+    }
+    return FMM_OK;
+}
+
+fmm_status fmm_copy_lists(const fmm_ctx* ctx_c, uint32_t* m2l, uint32_t* p2p) {
+    FMM_TRY(check_ctx(ctx_c));
+    fmm_ctx* ctx = const_cast<fmm_ctx*>(ctx_c);
+    if (!ctx->built) return FMM_ERR_STATE;
+    DeviceGuard g(ctx->device);
+    FMM_CUDA_TRY(ctx, cudaDeviceSynchronize());
+    struct {
+        uint32_t* dst;
+        DevBuf* src;
+        int64_t n;
+    } jobs[2] = {{m2l, &ctx->lst_m2l, ctx->n_m2l}, {p2p, &ctx->lst_p2p, ctx->n_p2p}};
+    for (auto& j : jobs) {
+        if (!j.dst || j.n == 0) continue;
+        std::vector<uint64_t> tmp((size_t)j.n);
+        FMM_CUDA_TRY(ctx, cudaMemcpy(tmp.data(), j.src->p, j.n * 8, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < j.n; ++i) {
+            j.dst[2 * i] = (uint32_t)(tmp[i] >> 32);
+            j.dst[2 * i + 1] = (uint32_t)tmp[i];
+        }
+    }
+    return FMM_OK;
+}
+
+fmm_status fmm_copy_expansions(const fmm_ctx* ctx_c, double* M, double* L) {
+    FMM_TRY(check_ctx(ctx_c));
+    fmm_ctx* ctx = const_cast<fmm_ctx*>(ctx_c);
+    if (!ctx->evaluated) return FMM_ERR_STATE;
+    DeviceGuard g(ctx->device);
+    FMM_CUDA_TRY(ctx, cudaDeviceSynchronize());
+    size_t sz = (size_t)ctx->ncell * ctx->ncoef * 8;
+    if (M && sz) FMM_CUDA_TRY(ctx, cudaMemcpy(M, ctx->M.p, sz, cudaMemcpyDeviceToHost));
+    if (L && sz) FMM_CUDA_TRY(ctx, cudaMemcpy(L, ctx->L.p, sz, cudaMemcpyDeviceToHost));
+    return FMM_OK;
+}
+
+fmm_status fmm_set_timing(fmm_ctx* ctx, int enable) {
+    FMM_TRY(check_ctx(ctx));
+    ctx->timing = enable != 0;
+    return FMM_OK;
+}
+
+fmm_status fmm_phase_times(fmm_ctx* ctx, double* ms, int cap, int* n, int reset) {
+    FMM_TRY(check_ctx(ctx));
+    DeviceGuard g(ctx->device);
+    for (auto& t : ctx->pending) {
+        FMM_CUDA_TRY(ctx, cudaEventSynchronize(t.b));
+        float e = 0.f;
+        FMM_CUDA_TRY(ctx, cudaEventElapsedTime(&e, t.a, t.b));
+        ctx->phase_ms[t.phase] += e;
+        ctx->event_pool.push_back(t.a);
+        ctx->event_pool.push_back(t.b);
+    }
+    ctx->pending.clear();
+    if (ms)
+        for (int i = 0; i < cap && i < PH_COUNT; ++i) ms[i] = ctx->phase_ms[i];
+    if (n) *n = PH_COUNT;
+    if (reset)
+        for (int i = 0; i < PH_COUNT; ++i) ctx->phase_ms[i] = 0.0;
+    return FMM_OK;
+}
+
+const char* fmm_phase_name(int phase) { return (phase >= 0 && phase < PH_COUNT) ? kPhaseNames[phase] : ""; }
+
+int64_t fmm_launch_count(fmm_ctx* ctx, int reset) {
+    if (!ctx) return -1;
+    int64_t v = ctx->launches;
+    if (reset) ctx->launches = 0;
+    return v;
+}
+
+}  // extern "C"

@@ -1,0 +1,177 @@
+// common.cuh -- internal definitions shared by the libfmm translation units.
+// Product code: never includes or links anything under oracle/ (DESIGN.md §3).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/fmm.h"
+
+#define FMM_MAXP 16
+#define FMM_MAXLEVEL 21
+
+// ---- coefficient indexing (R11: degree n, then alpha_x descending, then alpha_y descending)
+__host__ __device__ __forceinline__ int ncoef_of(int P) { return P * (P + 1) * (P + 2) / 6; }
+// index of multi-index (a,b,c): ncoef(n) + m(m+1)/2 + c with n = a+b+c, m = b+c
+__host__ __device__ __forceinline__ int cidx(int a, int b, int c) {
+    int n = a + b + c, m = b + c;
+    return ncoef_of(n) + m * (m + 1) / 2 + c;
+}
+
+// inverse of cidx: coefficient index -> (a,b,c)
+__host__ __device__ __forceinline__ void decode_cidx(int k, int& a, int& b, int& c) {
+    int n = 0;
+    while (ncoef_of(n + 1) <= k) ++n;
+    int r = k - ncoef_of(n);
+    int m = 0;
+    while ((m + 1) * (m + 2) / 2 <= r) ++m;
+    c = r - m * (m + 1) / 2;
+    b = m - c;
+    a = n - m;
+}
+
+// fill a block-shared exponent table (uchar4: a, b, c, degree) for ncoef entries
+__device__ __forceinline__ void fill_ex_table(uchar4* ex, int ncoef) {
+    for (int k = threadIdx.x; k < ncoef; k += blockDim.x) {
+        int a, b, c;
+        decode_cidx(k, a, b, c);
+        ex[k] = make_uchar4((unsigned char)a, (unsigned char)b, (unsigned char)c, (unsigned char)(a + b + c));
+    }
+}
+
+// ---- phases for event timing
+enum Phase {
+    PH_BOUNDS = 0, PH_SORT, PH_TREE, PH_GEOM, PH_DTT, PH_LISTS,
+    PH_UP, PH_M2L, PH_P2P, PH_DOWN, PH_COPY, PH_COUNT
+};
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+struct TimedEvent {
+    int phase;
+    cudaEvent_t a, b;
+};
+
+struct fmm_ctx {
+    // configuration
+    int64_t n_max = 0;
+    int P = 4, ncoef = 20;
+    double theta = 0.5;
+    int ncrit = 32;
+    int prec = FMM_F64;
+    int device = 0;
+    int num_sms = 148;
+    std::string err;
+
+    // streams / events (aux stream runs P2P concurrently with M2L)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+
+    // timing
+    bool timing = false;
+    std::vector<TimedEvent> pending;
+    std::vector<cudaEvent_t> event_pool;
+    double phase_ms[PH_COUNT] = {0};
+    int64_t launches = 0;
+
+    // build state
+    const void* built_pos = nullptr;
+    int64_t n = 0;
+    bool built = false;
+    bool evaluated = false;
+
+    // root cube (device): [0..2] lo, [3..5] hi, [6..8] origin, [9] scale, [10] h
+    DevBuf root;
+    // sort buffers
+    DevBuf key_a, key_b, idx_a, idx_b, sort_counts, scan_tmp, red_tmp;
+    uint64_t* d_keys = nullptr;   // sorted keys (points into key_a or key_b)
+    uint32_t* d_perm = nullptr;   // perm (points into idx_a or idx_b)
+    DevBuf body;                  // sorted (x,y,z,q): float4 (F32) or double4-like (F64)
+
+    // cells (SoA, BFS order)
+    int64_t ncell = 0, nleaf = 0, depth = 0, cell_cap = 0;
+    std::vector<int64_t> level_begin;  // host: first cell of each level, size depth+2
+    DevBuf c_key, c_level, c_bb, c_bc, c_cb, c_cc, c_parent, c_bmin, c_bmax, c_cr;  // c_cr: double4 (cx,cy,cz,R)
+    DevBuf split_tmp, split_cnt;       // per-level temporaries
+    DevBuf leaf_ids;                   // u32 list of leaf cells
+
+    // lists (CSR by target): m2l_src[n_m2l] with m2l_off[ncell+1]; p2p likewise
+    int64_t n_m2l = 0, n_p2p = 0, p2p_inter = 0;
+    DevBuf fr_a, fr_b, lst_m2l, lst_p2p, lst_tmp, m2l_src, p2p_src, m2l_off, p2p_off, cnt_tmp, dcount;
+
+    // expansions
+    DevBuf M, L, Mr;       // fp64 [ncell][ncoef]; Mr: packed fp32 copy for the M2L kernel
+    DevBuf near_phi, near_grad;  // P2P partials in sorted order (prec type)
+    DevBuf h_stage;              // device staging for fmm_solve_host
+};
+
+// ---- error helpers
+#define FMM_CUDA_TRY(ctx, expr)                                                          \
+    do {                                                                                 \
+        cudaError_t _e = (expr);                                                         \
+        if (_e != cudaSuccess) {                                                         \
+            (ctx)->err = std::string(#expr) + ": " + cudaGetErrorString(_e);             \
+            return _e == cudaErrorMemoryAllocation ? FMM_ERR_OOM : FMM_ERR_CUDA;         \
+        }                                                                                \
+    } while (0)
+
+#define FMM_TRY(expr)                   \
+    do {                                \
+        fmm_status _s = (expr);         \
+        if (_s != FMM_OK) return _s;    \
+    } while (0)
+
+// grow a device buffer to at least `bytes` (contents discarded unless keep)
+fmm_status buf_ensure(fmm_ctx* ctx, DevBuf& b, size_t bytes, bool keep = false, cudaStream_t s = 0);
+void buf_free(DevBuf& b);
+
+template <typename T>
+__host__ __forceinline__ T* P_(DevBuf& b) { return reinterpret_cast<T*>(b.p); }
+
+// sorted body record in fp64 mode (32-B aligned for vector loads)
+struct __align__(32) dbody { double x, y, z, w; };  // w = charge
+
+template <typename Real> struct BodyT;
+template <> struct BodyT<float> { using type = float4; };
+template <> struct BodyT<double> { using type = dbody; };
+
+// timing helpers (no-ops when timing is off)
+struct PhaseScope {
+    fmm_ctx* ctx; int phase; cudaStream_t s; cudaEvent_t a = nullptr;
+    PhaseScope(fmm_ctx* c, int ph, cudaStream_t st);
+    ~PhaseScope();
+};
+
+// launch accounting
+#define FMM_LAUNCH(ctx) ((ctx)->launches++)
+
+// ---- entry points of the translation units (all enqueue on the given stream)
+// scan.cu
+fmm_status scan_exclusive_u32(fmm_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n, uint32_t* total_dev,
+                              cudaStream_t s);
+fmm_status scan_exclusive_u64(fmm_ctx* ctx, const uint64_t* in, uint64_t* out, int64_t n, uint64_t* total_dev,
+                              cudaStream_t s);
+// sort.cu: stable LSD radix sort of (key, val) over bits [bit_lo, bit_hi); result pointers returned
+fmm_status radix_sort_pairs(fmm_ctx* ctx, uint64_t* k0, uint64_t* k1, uint32_t* v0, uint32_t* v1, int64_t n,
+                            int bit_lo, int bit_hi, uint64_t** kout, uint32_t** vout, cudaStream_t s);
+fmm_status radix_sort_keys(fmm_ctx* ctx, uint64_t* k0, uint64_t* k1, int64_t n, int bit_lo, int bit_hi,
+                           uint64_t** kout, cudaStream_t s);
+// keys.cu
+fmm_status build_keys(fmm_ctx* ctx, const void* pos, int64_t n, cudaStream_t s);
+fmm_status gather_bodies_q(fmm_ctx* ctx, const void* q, cudaStream_t s);
+// tree.cu
+fmm_status build_tree(fmm_ctx* ctx, cudaStream_t s);
+// dtt.cu
+fmm_status build_lists(fmm_ctx* ctx, cudaStream_t s);
+// upward.cu / downward.cu / m2l.cu / p2p.cu
+fmm_status upward_pass(fmm_ctx* ctx, cudaStream_t s);
+fmm_status m2l_pass(fmm_ctx* ctx, cudaStream_t s);
+fmm_status p2p_pass(fmm_ctx* ctx, cudaStream_t s);
+fmm_status downward_pass(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s);

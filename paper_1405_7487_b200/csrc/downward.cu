@@ -1,0 +1,141 @@
+// downward.cu -- L2L level by level, L2P at leaves, near+far merge and un-permute (a11, a12).
+//
+// PAPER.md:151 §II-C: "a post-order traversal is performed and L2L and L2P kernels are
+// executed to cascade the information down the tree to the particles" (pre-order,
+// parent before child, realised level-synchronously).
+// R15 L2L: L_alpha(ch) += sum_{beta >= alpha} L_beta(par) s^(beta-alpha)/(beta-alpha)!, s = c_ch - c_par
+// R16 L2P: phi_i += sum_alpha L_alpha z^alpha/alpha!, (grad phi_i)_d += sum_{|g|<=P-2} L_{g+e_d} z^g/g!
+// R18: output = near (P2P) + far (L2P), scattered to the caller's order through perm.
+#include "common.cuh"
+
+namespace {
+constexpr int DN_WARPS = 4;
+constexpr int LP_WARPS = 2;
+
+__device__ __forceinline__ void pow_table(double* t, double x, int P, int lane) {
+    if (lane < P) {
+        double v = 1.0;
+        for (int i = 1; i <= lane; ++i) v = v * x / (double)i;
+        t[lane] = v;
+    }
+}
+
+// children at level l+1 receive their parent's shifted local expansion
+__global__ void __launch_bounds__(DN_WARPS * 32) k_l2l(int64_t cbeg, int64_t cend, const int32_t* __restrict__ parent,
+                                                        const double4* __restrict__ cr, int P, int ncoef,
+                                                        double* __restrict__ L) {
+    __shared__ uchar4 ex[816];
+    __shared__ double s_pow[DN_WARPS][3][FMM_MAXP];
+    fill_ex_table(ex, ncoef);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int64_t c = cbeg + (int64_t)blockIdx.x * DN_WARPS + w; c < cend; c += (int64_t)gridDim.x * DN_WARPS) {
+        int32_t par = parent[c];
+        double4 cc = cr[c], cp = cr[par];
+        const double* Lp = L + (int64_t)par * ncoef;
+        __syncwarp();
+        pow_table(s_pow[w][0], cc.x - cp.x, P, lane);
+        pow_table(s_pow[w][1], cc.y - cp.y, P, lane);
+        pow_table(s_pow[w][2], cc.z - cp.z, P, lane);
+        __syncwarp();
+        for (int k = lane; k < ncoef; k += 32) {
+            uchar4 e = ex[k];
+            int m = P - 1 - e.w;
+            double sum = 0.0;
+            for (int gx = 0; gx <= m; ++gx)
+                for (int gy = 0; gy <= m - gx; ++gy)
+                    for (int gz = 0; gz <= m - gx - gy; ++gz)
+                        sum += Lp[cidx(e.x + gx, e.y + gy, e.z + gz)] *
+                               (s_pow[w][0][gx] * s_pow[w][1][gy] * s_pow[w][2][gz]);
+            L[(int64_t)c * ncoef + k] += sum;
+        }
+    }
+}
+
+// warp per leaf, lanes over bodies; writes the final outputs in the caller's order
+template <typename Body, typename Real>
+__global__ void __launch_bounds__(LP_WARPS * 32) k_l2p(const Body* __restrict__ body, const uint32_t* __restrict__ perm,
+                                                        const uint32_t* __restrict__ leaf_ids, int64_t nleaf,
+                                                        const uint32_t* __restrict__ bb, const uint32_t* __restrict__ bc,
+                                                        const double4* __restrict__ cr, int P, int ncoef,
+                                                        const double* __restrict__ L, const Real* __restrict__ near_phi,
+                                                        const Real* __restrict__ near_grad, Real* __restrict__ phi,
+                                                        Real* __restrict__ grad) {
+    __shared__ uchar4 ex[816];
+    __shared__ double s_L[LP_WARPS][816];
+    __shared__ double s_pw[LP_WARPS][3][FMM_MAXP][32];
+    fill_ex_table(ex, ncoef);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int64_t li = (int64_t)blockIdx.x * LP_WARPS + w; li < nleaf; li += (int64_t)gridDim.x * LP_WARPS) {
+        uint32_t c = leaf_ids[li];
+        double4 ctr = cr[c];
+        __syncwarp();
+        for (int k = lane; k < ncoef; k += 32) s_L[w][k] = L[(int64_t)c * ncoef + k];
+        __syncwarp();
+        uint32_t b0 = bb[c], nb = bc[c];
+        for (uint32_t j0 = 0; j0 < nb; j0 += 32) {
+            uint32_t j = j0 + lane;
+            bool ok = j < nb;
+            double z[3] = {0, 0, 0};
+            if (ok) {
+                Body p = body[b0 + j];
+                z[0] = (double)p.x - ctr.x; z[1] = (double)p.y - ctr.y; z[2] = (double)p.z - ctr.z;
+            }
+            for (int d = 0; d < 3; ++d) {
+                double v = 1.0;
+                s_pw[w][d][0][lane] = 1.0;
+                for (int e = 1; e < P; ++e) {
+                    v = v * z[d] / (double)e;
+                    s_pw[w][d][e][lane] = v;
+                }
+            }
+            double f = 0.0, g0 = 0.0, g1 = 0.0, g2 = 0.0;
+            for (int k = 0; k < ncoef; ++k) {
+                uchar4 e = ex[k];
+                double m = s_pw[w][0][e.x][lane] * s_pw[w][1][e.y][lane] * s_pw[w][2][e.z][lane];
+                f += s_L[w][k] * m;
+                if (e.w <= P - 2) {
+                    g0 += s_L[w][cidx(e.x + 1, e.y, e.z)] * m;
+                    g1 += s_L[w][cidx(e.x, e.y + 1, e.z)] * m;
+                    g2 += s_L[w][cidx(e.x, e.y, e.z + 1)] * m;
+                }
+            }
+            if (ok) {
+                uint32_t sj = b0 + j;
+                uint32_t o = perm[sj];
+                phi[o] = (Real)(f + (double)near_phi[sj]);
+                grad[3 * (int64_t)o + 0] = (Real)(g0 + (double)near_grad[3 * (int64_t)sj + 0]);
+                grad[3 * (int64_t)o + 1] = (Real)(g1 + (double)near_grad[3 * (int64_t)sj + 1]);
+                grad[3 * (int64_t)o + 2] = (Real)(g2 + (double)near_grad[3 * (int64_t)sj + 2]);
+            }
+        }
+    }
+}
+
+template <typename Body, typename Real>
+fmm_status downward_t(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s) {
+    PhaseScope ps(ctx, PH_DOWN, s);
+    double* L = P_<double>(ctx->L);
+    for (int64_t l = 1; l <= ctx->depth; ++l) {
+        int64_t b = ctx->level_begin[l], e = ctx->level_begin[l + 1];
+        int g = (int)std::min<int64_t>((e - b + DN_WARPS - 1) / DN_WARPS, (int64_t)ctx->num_sms * 16);
+        k_l2l<<<std::max(g, 1), DN_WARPS * 32, 0, s>>>(b, e, P_<int32_t>(ctx->c_parent), P_<double4>(ctx->c_cr),
+                                                       ctx->P, ctx->ncoef, L);
+        FMM_LAUNCH(ctx);
+    }
+    int g = (int)std::min<int64_t>((ctx->nleaf + LP_WARPS - 1) / LP_WARPS, (int64_t)ctx->num_sms * 32);
+    k_l2p<Body, Real><<<std::max(g, 1), LP_WARPS * 32, 0, s>>>(
+        P_<Body>(ctx->body), ctx->d_perm, P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, P_<uint32_t>(ctx->c_bb),
+        P_<uint32_t>(ctx->c_bc), P_<double4>(ctx->c_cr), ctx->P, ctx->ncoef, L, P_<Real>(ctx->near_phi),
+        P_<Real>(ctx->near_grad), (Real*)phi, (Real*)grad);
+    FMM_LAUNCH(ctx);
+    FMM_CUDA_TRY(ctx, cudaGetLastError());
+    return FMM_OK;
+}
+}  // namespace
+
+fmm_status downward_pass(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s) {
+    if (ctx->prec == FMM_F32) return downward_t<float4, float>(ctx, phi, grad, s);
+    return downward_t<dbody, double>(ctx, phi, grad, s);
+}

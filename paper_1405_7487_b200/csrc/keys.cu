@@ -1,0 +1,183 @@
+// keys.cu -- bounds, root cube, 63-bit Morton keys, sort and body gather (a1-a3).
+//
+// R2 (root cube): lo/hi exact fp64 min/max; c0 = (lo+hi)*0.5; h = 0.5*max(hi-lo) (1 if 0);
+//     origin = c0 - h; s = 2^20/h.        (§II-C "local bounding box")
+// R3 (quantise): i = clamp(floor((x - origin)*s), 0, 2^21-1), two roundings, no FMA.
+// R4 (key): x bit -> bit 3l, y -> 3l+1, z -> 3l+2; level 1 is the top digit
+//     (§II-B "Three bits of the key are used to indicate which octant").
+// R5 (order): stable LSD radix sort of (key, original index).
+// All fp64 arithmetic uses explicit _rn intrinsics so nvcc cannot contract into FMAs:
+// the keys are bit-exact against the oracle.
+#include "common.cuh"
+
+namespace {
+
+template <typename Real>
+__global__ void k_bounds(const Real* __restrict__ pos, int64_t n, double* __restrict__ blk, int* __restrict__ bad) {
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    int nonfinite = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            double x = (double)pos[3 * i + d];
+            nonfinite |= !isfinite(x);
+            lo[d] = fmin(lo[d], x);
+            hi[d] = fmax(hi[d], x);
+        }
+    }
+#pragma unroll
+    for (int s = 16; s; s >>= 1)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], s));
+            hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], s));
+        }
+    __shared__ double s_v[32][6];
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0)
+        for (int d = 0; d < 3; ++d) { s_v[w][d] = lo[d]; s_v[w][3 + d] = hi[d]; }
+    if (nonfinite) atomicOr(bad, 1);
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        double v = s_v[0][threadIdx.x];
+        for (int k = 1; k < nw; ++k) v = threadIdx.x < 3 ? fmin(v, s_v[k][threadIdx.x]) : fmax(v, s_v[k][threadIdx.x]);
+        blk[(int64_t)blockIdx.x * 6 + threadIdx.x] = v;
+    }
+}
+
+// final reduction over blocks + R2 root cube, one thread
+__global__ void k_root_cube(const double* __restrict__ blk, int nblk, double* __restrict__ root) {
+    double lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) { lo[d] = blk[d]; hi[d] = blk[3 + d]; }
+    for (int b = 1; b < nblk; ++b)
+        for (int d = 0; d < 3; ++d) {
+            lo[d] = fmin(lo[d], blk[6 * b + d]);
+            hi[d] = fmax(hi[d], blk[6 * b + 3 + d]);
+        }
+    double c0[3], ext = 0.0;
+    for (int d = 0; d < 3; ++d) {
+        c0[d] = __dmul_rn(__dadd_rn(lo[d], hi[d]), 0.5);
+        double e = __dsub_rn(hi[d], lo[d]);
+        if (e > ext) ext = e;
+    }
+    double h = __dmul_rn(0.5, ext);
+    if (h == 0.0) h = 1.0;
+    for (int d = 0; d < 3; ++d) {
+        root[d] = lo[d];
+        root[3 + d] = hi[d];
+        root[6 + d] = __dsub_rn(c0[d], h);
+    }
+    root[9] = __ddiv_rn(1048576.0, h);
+    root[10] = h;
+}
+
+__device__ __forceinline__ uint64_t spread3(uint32_t v) {
+    uint64_t x = v & 0x1FFFFFu;
+    x = (x | (x << 32)) & 0x1F00000000FFFFull;
+    x = (x | (x << 16)) & 0x1F0000FF0000FFull;
+    x = (x | (x << 8)) & 0x100F00F00F00F00Full;
+    x = (x | (x << 4)) & 0x10C30C30C30C30C3ull;
+    x = (x | (x << 2)) & 0x1249249249249249ull;
+    return x;
+}
+
+__device__ __forceinline__ uint32_t quantise(double x, double o, double s) {
+    double t = __dmul_rn(__dsub_rn(x, o), s);
+    double f = floor(t);
+    f = fmin(fmax(f, 0.0), 2097151.0);
+    return (uint32_t)f;
+}
+
+template <typename Real>
+__global__ void k_keys(const Real* __restrict__ pos, int64_t n, const double* __restrict__ root,
+                       uint64_t* __restrict__ keys, uint32_t* __restrict__ idx) {
+    const double ox = root[6], oy = root[7], oz = root[8], s = root[9];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t ix = quantise((double)pos[3 * i], ox, s);
+        uint32_t iy = quantise((double)pos[3 * i + 1], oy, s);
+        uint32_t iz = quantise((double)pos[3 * i + 2], oz, s);
+        keys[i] = spread3(ix) | (spread3(iy) << 1) | (spread3(iz) << 2);
+        idx[i] = (uint32_t)i;
+    }
+}
+
+template <typename Real>
+__global__ void k_gather_pos(const Real* __restrict__ pos, const uint32_t* __restrict__ perm, int64_t n,
+                             typename BodyT<Real>::type* __restrict__ body) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t j = perm[k];
+        typename BodyT<Real>::type b;
+        b.x = pos[3 * (int64_t)j];
+        b.y = pos[3 * (int64_t)j + 1];
+        b.z = pos[3 * (int64_t)j + 2];
+        b.w = 0;
+        body[k] = b;
+    }
+}
+
+}  // namespace
+
+namespace {
+template <typename Real>
+__global__ void k_gather_q(const Real* __restrict__ q, const uint32_t* __restrict__ perm, int64_t n,
+                           typename BodyT<Real>::type* __restrict__ body) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        body[k].w = q[perm[k]];
+}
+
+template <typename Real>
+fmm_status build_keys_t(fmm_ctx* ctx, const Real* pos, int64_t n, cudaStream_t s) {
+    const int nblk = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 2);
+    {
+        PhaseScope ps(ctx, PH_BOUNDS, s);
+        FMM_TRY(buf_ensure(ctx, ctx->root, 16 * sizeof(double)));
+        FMM_TRY(buf_ensure(ctx, ctx->red_tmp, 64 + (size_t)nblk * 6 * sizeof(double)));
+        int* d_bad = reinterpret_cast<int*>(ctx->red_tmp.p);
+        double* d_blk = reinterpret_cast<double*>((char*)ctx->red_tmp.p + 64);
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+        k_bounds<Real><<<nblk, 256, 0, s>>>(pos, n, d_blk, d_bad);
+        k_root_cube<<<1, 1, 0, s>>>(d_blk, nblk, P_<double>(ctx->root));
+        ctx->launches += 2;
+        int bad = 0;
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+        FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+        if (bad) {
+            ctx->err = "fmm_build: non-finite position";
+            return FMM_ERR_NONFINITE;
+        }
+    }
+    PhaseScope ps(ctx, PH_SORT, s);
+    FMM_TRY(buf_ensure(ctx, ctx->key_a, (size_t)n * 8));
+    FMM_TRY(buf_ensure(ctx, ctx->key_b, (size_t)n * 8));
+    FMM_TRY(buf_ensure(ctx, ctx->idx_a, (size_t)n * 4));
+    FMM_TRY(buf_ensure(ctx, ctx->idx_b, (size_t)n * 4));
+    const int gblk = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8);
+    k_keys<Real><<<gblk, 256, 0, s>>>(pos, n, P_<double>(ctx->root), P_<uint64_t>(ctx->key_a), P_<uint32_t>(ctx->idx_a));
+    FMM_LAUNCH(ctx);
+    FMM_CUDA_TRY(ctx, cudaGetLastError());
+    FMM_TRY(radix_sort_pairs(ctx, P_<uint64_t>(ctx->key_a), P_<uint64_t>(ctx->key_b), P_<uint32_t>(ctx->idx_a),
+                             P_<uint32_t>(ctx->idx_b), n, 0, 64, &ctx->d_keys, &ctx->d_perm, s));
+    FMM_TRY(buf_ensure(ctx, ctx->body, (size_t)n * sizeof(typename BodyT<Real>::type)));
+    k_gather_pos<Real><<<gblk, 256, 0, s>>>(pos, ctx->d_perm, n, P_<typename BodyT<Real>::type>(ctx->body));
+    FMM_LAUNCH(ctx);
+    FMM_CUDA_TRY(ctx, cudaGetLastError());
+    return FMM_OK;
+}
+}  // namespace
+
+fmm_status build_keys(fmm_ctx* ctx, const void* pos, int64_t n, cudaStream_t s) {
+    if (ctx->prec == FMM_F32) return build_keys_t<float>(ctx, (const float*)pos, n, s);
+    return build_keys_t<double>(ctx, (const double*)pos, n, s);
+}
+
+fmm_status gather_bodies_q(fmm_ctx* ctx, const void* q, cudaStream_t s) {
+    int64_t n = ctx->n;
+    const int gblk = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8);
+    if (ctx->prec == FMM_F32)
+        k_gather_q<float><<<gblk, 256, 0, s>>>((const float*)q, ctx->d_perm, n, P_<float4>(ctx->body));
+    else
+        k_gather_q<double><<<gblk, 256, 0, s>>>((const double*)q, ctx->d_perm, n, P_<dbody>(ctx->body));
+    FMM_LAUNCH(ctx);
+    FMM_CUDA_TRY(ctx, cudaGetLastError());
+    return FMM_OK;
+}

@@ -1,0 +1,115 @@
+// m2l.cu -- M2L over the canonical list (a9).
+//
+// PAPER.md:58 §II-A: "The M2L (multipole-to-local) kernel ... translates them to local
+// expansions"; M2L and P2P "make up more than 90% of the total runtime".
+// R14: L_alpha(A) += sum_{|beta| <= P-1-|alpha|} (-1)^|beta| M_beta(B) D^{alpha+beta}G(c_A - c_B),
+//      D^k G via the derivative form of the R14 Taylor recurrence:
+//      n r^2 D_k = -(2n-1) sum_i k_i d_i D_{k-e_i} - (n-1) sum_i k_i (k_i-1) D_{k-2e_i}
+//      (obtained from n r^2 t_k = (2n-1) sum d_i t_{k-e_i} - (n-1) sum t_{k-2e_i} with
+//       D_k = (-1)^|k| k! t_k).
+//
+// This file holds the generic kernel (any P <= 16, Real = float or double): warp per
+// target cell over its CSR source range, D table and signed M in shared memory, lanes
+// over alpha, each pair's contribution accumulated into fp64 (R19).
+#include "common.cuh"
+
+namespace {
+constexpr int ML_WARPS = 2;
+
+template <typename Real>
+__global__ void __launch_bounds__(ML_WARPS * 32) k_m2l_generic(int64_t ncell, const uint64_t* __restrict__ lst,
+                                                                const uint64_t* __restrict__ off,
+                                                                const double4* __restrict__ cr, int P, int ncoef,
+                                                                const double* __restrict__ M, double* __restrict__ L) {
+    // dynamic shared memory: ex[ncoef] | per warp: L (double) [ncoef], D [ncoef], M [ncoef]
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uchar4* ex = reinterpret_cast<uchar4*>(smem);
+    const int ncp = (ncoef + 1) & ~1;
+    double* sLw = reinterpret_cast<double*>(smem + 4 * ncp) + (size_t)w * ncp;
+    Real* sDw = reinterpret_cast<Real*>(reinterpret_cast<double*>(smem + 4 * ncp) + (size_t)ML_WARPS * ncp) +
+                (size_t)w * 2 * ncp;
+    Real* sMw = sDw + ncp;
+    fill_ex_table(ex, ncoef);
+    __syncthreads();
+    for (int64_t a = (int64_t)blockIdx.x * ML_WARPS + w; a < ncell; a += (int64_t)gridDim.x * ML_WARPS) {
+        uint64_t p0 = off[a], p1 = off[a + 1];
+        if (p0 == p1) continue;
+        double4 ca = cr[a];
+        for (int k = lane; k < ncoef; k += 32) sLw[k] = 0.0;
+        for (uint64_t p = p0; p < p1; ++p) {
+            uint32_t b = (uint32_t)lst[p];
+            double4 cb = cr[b];
+            Real d[3] = {(Real)(ca.x - cb.x), (Real)(ca.y - cb.y), (Real)(ca.z - cb.z)};
+            Real r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+            Real inv_r2 = Real(1) / r2;
+            __syncwarp();
+            if (lane == 0) sDw[0] = Real(1) / sqrt(r2);
+            for (int k = lane; k < ncoef; k += 32) {
+                Real m = (Real)M[(int64_t)b * ncoef + k];
+                sMw[k] = (ex[k].w & 1) ? -m : m;
+            }
+            __syncwarp();
+            for (int n = 1; n < P; ++n) {
+                int kb = ncoef_of(n), ke = ncoef_of(n + 1);
+                for (int k = kb + lane; k < ke; k += 32) {
+                    uchar4 e = ex[k];
+                    int kk[3] = {e.x, e.y, e.z};
+                    Real s1 = 0, s2 = 0;
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        if (kk[i] >= 1) {
+                            int m[3] = {kk[0], kk[1], kk[2]};
+                            m[i] -= 1;
+                            s1 += Real(kk[i]) * d[i] * sDw[cidx(m[0], m[1], m[2])];
+                        }
+                        if (kk[i] >= 2) {
+                            int m[3] = {kk[0], kk[1], kk[2]};
+                            m[i] -= 2;
+                            s2 += Real(kk[i] * (kk[i] - 1)) * sDw[cidx(m[0], m[1], m[2])];
+                        }
+                    }
+                    sDw[k] = -(Real(2 * n - 1) * s1 + Real(n - 1) * s2) * inv_r2 / Real(n);
+                }
+                __syncwarp();
+            }
+            for (int k = lane; k < ncoef; k += 32) {
+                uchar4 e = ex[k];
+                int nb = ncoef_of(P - e.w);
+                Real sum = 0;
+                for (int j = 0; j < nb; ++j) {
+                    uchar4 f = ex[j];
+                    sum += sMw[j] * sDw[cidx(e.x + f.x, e.y + f.y, e.z + f.z)];
+                }
+                sLw[k] += (double)sum;
+            }
+        }
+        __syncwarp();
+        for (int k = lane; k < ncoef; k += 32) L[a * ncoef + k] = sLw[k];
+        __syncwarp();
+    }
+}
+
+template <typename Real>
+fmm_status m2l_generic(fmm_ctx* ctx, cudaStream_t s) {
+    int g = (int)std::min<int64_t>((ctx->ncell + ML_WARPS - 1) / ML_WARPS, (int64_t)ctx->num_sms * 8);
+    const int ncp = (ctx->ncoef + 1) & ~1;
+    size_t smem = (size_t)4 * ncp + (size_t)ML_WARPS * ncp * (8 + 2 * sizeof(Real));
+    k_m2l_generic<Real><<<std::max(g, 1), ML_WARPS * 32, smem, s>>>(ctx->ncell, P_<uint64_t>(ctx->lst_m2l),
+                                                                  P_<uint64_t>(ctx->m2l_off), P_<double4>(ctx->c_cr),
+                                                                  ctx->P, ctx->ncoef, P_<double>(ctx->M),
+                                                                  P_<double>(ctx->L));
+    FMM_LAUNCH(ctx);
+    FMM_CUDA_TRY(ctx, cudaGetLastError());
+    return FMM_OK;
+}
+}  // namespace
+
+fmm_status m2l_pass(fmm_ctx* ctx, cudaStream_t s) {
+    PhaseScope ps(ctx, PH_M2L, s);
+    FMM_TRY(buf_ensure(ctx, ctx->L, (size_t)ctx->ncell * ctx->ncoef * 8));
+    // cells without M2L sources still need L = 0 (the generic kernel skips them)
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->L.p, 0, (size_t)ctx->ncell * ctx->ncoef * 8, s));
+    if (ctx->prec == FMM_F32) return m2l_generic<float>(ctx, s);
+    return m2l_generic<double>(ctx, s);
+}

@@ -1,0 +1,213 @@
+"""Thin ctypes binding of libfmm.so (include/fmm.h).  Argument marshalling only: every
+step of the FMM runs in the library's CUDA kernels.  There is no CPU fallback: if the
+library or a CUDA device is missing, construction raises.
+
+PyTorch supplies device memory and the current CUDA stream; numpy is used only for the
+host-side introspection buffers and fmm_solve_host.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfmm.so")
+
+FMM_OK, FMM_ERR_ARG, FMM_ERR_STATE, FMM_ERR_NONFINITE, FMM_ERR_OOM, FMM_ERR_CUDA, FMM_ERR_NCCL = range(7)
+STATUS = {0: "FMM_OK", 1: "FMM_ERR_ARG", 2: "FMM_ERR_STATE", 3: "FMM_ERR_NONFINITE", 4: "FMM_ERR_OOM",
+          5: "FMM_ERR_CUDA", 6: "FMM_ERR_NCCL"}
+F32, F64 = 0, 1
+
+# every symbol include/fmm.h declares: (restype, argtypes)
+_p, _i, _i64, _d = C.c_void_p, C.c_int, C.c_int64, C.c_double
+SYMBOLS = {
+    "fmm_version": (_i, []),
+    "fmm_create": (_i, [_i64, _i, _d, _i, _i, _i, C.POINTER(_p)]),
+    "fmm_destroy": (_i, [_p]),
+    "fmm_last_error": (C.c_char_p, [_p]),
+    "fmm_build": (_i, [_p, _p, _i64, _p]),
+    "fmm_evaluate": (_i, [_p, _p, _p, _p, _p, _p]),
+    "fmm_solve_host": (_i, [_p, _p, _p, _i64, _p, _p, _p]),
+    "fmm_get_counts": (_i, [_p, _p]),
+    "fmm_copy_sorted": (_i, [_p, _p, _p]),
+    "fmm_copy_cells": (_i, [_p] * 12),
+    "fmm_copy_lists": (_i, [_p, _p, _p]),
+    "fmm_copy_expansions": (_i, [_p, _p, _p]),
+    "fmm_set_timing": (_i, [_p, _i]),
+    "fmm_phase_times": (_i, [_p, _p, _i, _p, _i]),
+    "fmm_phase_name": (C.c_char_p, [_i]),
+    "fmm_launch_count": (_i64, [_p, _i]),
+}
+
+_lib = None
+
+
+class FMMError(RuntimeError):
+    def __init__(self, status, msg=""):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def lib():
+    """Load libfmm.so (build it first with paper_1405_7487_b200.build.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FMMError(FMM_ERR_CUDA, f"{LIB_PATH} missing: run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SYMBOLS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+class _Counts(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in ("n", "ncell", "nleaf", "depth", "n_m2l", "n_p2p", "p2p_interactions")]
+
+
+def _np_ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+class FMM:
+    """One FMM context: fmm_create(N, P, theta, ncrit) -> build(pos) -> evaluate(pos, q)."""
+
+    def __init__(self, n_max: int, P: int, theta: float, ncrit: int, prec: str = "f32", device: int = 0):
+        self.prec = {"f32": F32, "f64": F64}[prec]
+        self.P, self.theta, self.ncrit, self.device = P, theta, ncrit, device
+        h = C.c_void_p()
+        st = lib().fmm_create(int(n_max), int(P), float(theta), int(ncrit), self.prec, int(device), C.byref(h))
+        if st != FMM_OK:
+            raise FMMError(st, "fmm_create")
+        self._h = h
+        self._pos = None
+
+    # -- lifecycle ---------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().fmm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def _check(self, st, what):
+        if st != FMM_OK:
+            msg = lib().fmm_last_error(self._h)
+            raise FMMError(st, f"{what}: {msg.decode() if msg else ''}")
+
+    @property
+    def dtype(self):
+        import torch
+        return torch.float32 if self.prec == F32 else torch.float64
+
+    @staticmethod
+    def _stream(stream):
+        import torch
+        return (stream if stream is not None else torch.cuda.current_stream()).cuda_stream
+
+    def _check_tensor(self, t, shape, name):
+        import torch
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise FMMError(FMM_ERR_ARG, f"{name} must be a CUDA tensor")
+        if t.dtype != self.dtype:
+            raise FMMError(FMM_ERR_ARG, f"{name} dtype {t.dtype} != context precision {self.dtype}")
+        if not t.is_contiguous() or tuple(t.shape) != tuple(shape):
+            raise FMMError(FMM_ERR_ARG, f"{name} must be contiguous with shape {shape}")
+
+    # -- the path ----------------------------------------------------------
+    def build(self, pos, stream=None):
+        n = pos.shape[0]
+        self._check_tensor(pos, (n, 3), "pos")
+        self._check(lib().fmm_build(self._h, C.c_void_p(pos.data_ptr()), n, C.c_void_p(self._stream(stream))),
+                    "fmm_build")
+        self._pos = pos
+        self.n = n
+        return self
+
+    def evaluate(self, pos, q, phi=None, grad=None, stream=None):
+        import torch
+        n = pos.shape[0]
+        self._check_tensor(q, (n,), "q")
+        if phi is None:
+            phi = torch.empty(n, dtype=self.dtype, device=pos.device)
+        if grad is None:
+            grad = torch.empty((n, 3), dtype=self.dtype, device=pos.device)
+        self._check_tensor(phi, (n,), "phi")
+        self._check_tensor(grad, (n, 3), "grad")
+        self._check(lib().fmm_evaluate(self._h, C.c_void_p(pos.data_ptr()), C.c_void_p(q.data_ptr()),
+                                       C.c_void_p(phi.data_ptr()), C.c_void_p(grad.data_ptr()),
+                                       C.c_void_p(self._stream(stream))), "fmm_evaluate")
+        return phi, grad
+
+    def solve(self, pos, q, phi=None, grad=None, stream=None):
+        self.build(pos, stream)
+        return self.evaluate(pos, q, phi, grad, stream)
+
+    def solve_host(self, pos: np.ndarray, q: np.ndarray, phi: np.ndarray = None, grad: np.ndarray = None,
+                   stream=None):
+        """fmm_solve_host: host arrays in, host arrays out (copies inside the library)."""
+        dt = np.float32 if self.prec == F32 else np.float64
+        pos = np.ascontiguousarray(pos, dtype=dt)
+        q = np.ascontiguousarray(q, dtype=dt)
+        n = pos.shape[0]
+        phi = np.empty(n, dt) if phi is None else phi
+        grad = np.empty((n, 3), dt) if grad is None else grad
+        s = None if stream is None else C.c_void_p(stream.cuda_stream)
+        self._check(lib().fmm_solve_host(self._h, _np_ptr(pos), _np_ptr(q), n, _np_ptr(phi), _np_ptr(grad), s),
+                    "fmm_solve_host")
+        self._pos = None
+        return phi, grad
+
+    # -- introspection -----------------------------------------------------
+    def counts(self) -> dict:
+        c = _Counts()
+        self._check(lib().fmm_get_counts(self._h, C.byref(c)), "fmm_get_counts")
+        return {k: int(getattr(c, k)) for k, _ in _Counts._fields_}
+
+    def sorted(self):
+        n = self.counts()["n"]
+        k = np.zeros(n, np.uint64); p = np.zeros(n, np.uint32)
+        self._check(lib().fmm_copy_sorted(self._h, _np_ptr(k), _np_ptr(p)), "fmm_copy_sorted")
+        return k, p
+
+    def cells(self) -> dict:
+        nc = self.counts()["ncell"]
+        out = dict(level=np.zeros(nc, np.int32), key=np.zeros(nc, np.uint64),
+                   body_begin=np.zeros(nc, np.uint32), body_count=np.zeros(nc, np.uint32),
+                   child_begin=np.zeros(nc, np.uint32), child_count=np.zeros(nc, np.uint32),
+                   parent=np.zeros(nc, np.int32), bmin=np.zeros((nc, 3)), bmax=np.zeros((nc, 3)),
+                   center=np.zeros((nc, 3)), radius=np.zeros(nc))
+        order = ["level", "key", "body_begin", "body_count", "child_begin", "child_count", "parent",
+                 "bmin", "bmax", "center", "radius"]
+        self._check(lib().fmm_copy_cells(self._h, *[_np_ptr(out[k]) for k in order]), "fmm_copy_cells")
+        return out
+
+    def lists(self):
+        c = self.counts()
+        m2l = np.zeros((c["n_m2l"], 2), np.uint32); p2p = np.zeros((c["n_p2p"], 2), np.uint32)
+        self._check(lib().fmm_copy_lists(self._h, _np_ptr(m2l), _np_ptr(p2p)), "fmm_copy_lists")
+        return m2l, p2p
+
+    def expansions(self):
+        c = self.counts()
+        nco = self.P * (self.P + 1) * (self.P + 2) // 6
+        M = np.zeros((c["ncell"], nco)); L = np.zeros((c["ncell"], nco))
+        self._check(lib().fmm_copy_expansions(self._h, _np_ptr(M), _np_ptr(L)), "fmm_copy_expansions")
+        return M, L
+
+    # -- timing ------------------------------------------------------------
+    def set_timing(self, on: bool = True):
+        self._check(lib().fmm_set_timing(self._h, int(on)), "fmm_set_timing")
+
+    def phase_times(self, reset: bool = True) -> dict:
+        ms = np.zeros(32); n = C.c_int()
+        self._check(lib().fmm_phase_times(self._h, _np_ptr(ms), 32, C.byref(n), int(reset)), "fmm_phase_times")
+        return {lib().fmm_phase_name(i).decode(): float(ms[i]) for i in range(n.value)}
+
+    def launch_count(self, reset: bool = True) -> int:
+        return int(lib().fmm_launch_count(self._h, int(reset)))

@@ -1,0 +1,181 @@
+"""GPU (libfmm, sm_100a) versus the CPU oracle, through the C-ABI.
+
+Bar (north_star): keys, permutation, cells, fp64 geometry and the canonical
+M2L/P2P lists bit-exact; phi and grad relative L2 <= 1e-12 in fp64, <= 1e-5 in fp32.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": 1e-12, "f32": 1e-5}
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1405_7487_b200 import build
+    build.build()
+    return torch
+
+
+def run_gpu(torch, pos, q, P, theta, ncrit, prec):
+    from paper_1405_7487_b200 import FMM
+    f = FMM(max(len(pos), 1), P, theta, ncrit, prec)
+    dt = torch.float32 if prec == "f32" else torch.float64
+    tp = torch.from_numpy(np.ascontiguousarray(pos)).to(dt).cuda()
+    tq = torch.from_numpy(np.ascontiguousarray(q)).to(dt).cuda()
+    phi, grad = f.solve(tp, tq)
+    torch.cuda.synchronize()
+    return f, phi.cpu().numpy().astype(np.float64), grad.cpu().numpy().astype(np.float64)
+
+
+def check_structure(f, o):
+    assert f.counts()["ncell"] == o.counts()["ncell"]
+    gk, gp = f.sorted()
+    ok, op = o.sorted()
+    np.testing.assert_array_equal(gk, ok)
+    np.testing.assert_array_equal(gp, op)
+    gc, oc = f.cells(), o.cells()
+    for k in oc:
+        np.testing.assert_array_equal(gc[k], oc[k], err_msg=k)
+    gm, gpl = f.lists()
+    om, opl = o.lists()
+    np.testing.assert_array_equal(gm, om)
+    np.testing.assert_array_equal(gpl, opl)
+    gcnt, ocnt = f.counts(), o.counts()
+    for k in ("nleaf", "depth", "n_m2l", "n_p2p", "p2p_interactions"):
+        assert gcnt[k] == ocnt[k], k
+
+
+CASES = [
+    # kind, n, P, theta, ncrit, prec
+    ("cube", 4096, 4, 0.5, 32, "f64"),       # BASELINE configs[0]
+    ("cube", 4133, 4, 0.5, 32, "f32"),       # ragged tail over several sort tiles
+    ("plummer", 3000, 6, 0.4, 16, "f64"),
+    ("plummer", 5000, 10, 0.4, 64, "f32"),
+    ("sphere", 2000, 5, 0.6, 8, "f64"),
+    ("cube", 1000, 1, 0.3, 8, "f64"),        # P = 1: monopole only, no far gradient
+    ("cube", 1000, 2, 0.7, 1, "f64"),        # ncrit = 1
+    ("cube", 700, 16, 0.5, 32, "f64"),       # maximum P
+    ("plummer", 64, 3, 0.5, 64, "f32"),      # single leaf = direct sum
+    ("cube", 7, 4, 0.5, 2, "f64"),
+]
+
+
+@pytest.mark.parametrize("kind,n,P,theta,ncrit,prec", CASES)
+def test_parity_small(torch_cuda, kind, n, P, theta, ncrit, prec):
+    pos, q = synth.generate(kind, n, 100 + n, np.float32 if prec == "f32" else np.float64)
+    f, phi, grad = run_gpu(torch_cuda, pos, q, P, theta, ncrit, prec)
+    o = oracle.FMM(pos.astype(np.float64), q.astype(np.float64), P, theta, ncrit).traverse()
+    check_structure(f, o)
+    ophi, ograd = o.evaluate()
+    assert oracle.rel_l2(phi, ophi) <= TOL[prec]
+    assert oracle.rel_l2(grad, ograd) <= TOL[prec]
+    if prec == "f64":
+        gM, gL = f.expansions()
+        oM, oL = o.expansions()
+        assert np.abs(gM - oM).max() <= 1e-12 * max(np.abs(oM).max(), 1e-300)
+        assert np.abs(gL - oL).max() <= 1e-11 * max(np.abs(oL).max(), 1e-300)
+
+
+def test_duplicates_and_coincident(torch_cuda):
+    pos, q = synth.generate("cube", 300, 5)
+    pos = np.vstack([pos, pos[:50], np.full((40, 3), 0.125)])
+    q = np.concatenate([q, q[:50], np.linspace(-1, 1, 40)])
+    f, phi, grad = run_gpu(torch_cuda, pos, q, 4, 0.5, 8, "f64")
+    o = oracle.FMM(pos, q, 4, 0.5, 8).traverse()
+    check_structure(f, o)
+    assert o.counts()["depth"] == 21
+    ophi, ograd = o.evaluate()
+    assert oracle.rel_l2(phi, ophi) <= 1e-12 and oracle.rel_l2(grad, ograd) <= 1e-12
+
+
+def test_degenerate_sizes(torch_cuda):
+    torch = torch_cuda
+    from paper_1405_7487_b200 import FMM
+    f = FMM(10, 4, 0.5, 8, "f64")
+    e = torch.zeros((0, 3), dtype=torch.float64, device="cuda")
+    f.build(e)
+    assert f.counts()["ncell"] == 0
+    phi, grad = f.evaluate(e, torch.zeros(0, dtype=torch.float64, device="cuda"))
+    assert phi.numel() == 0
+    p1 = torch.tensor([[0.3, 0.2, 0.1]], dtype=torch.float64, device="cuda")
+    phi, grad = f.solve(p1, torch.ones(1, dtype=torch.float64, device="cuda"))
+    assert phi.item() == 0 and grad.abs().max().item() == 0
+    pc = torch.full((5, 3), 0.25, dtype=torch.float64, device="cuda")
+    f = FMM(10, 4, 0.5, 2, "f64")          # ncrit < 5: a single-child chain to level 21 (R20)
+    phi, grad = f.solve(pc, torch.ones(5, dtype=torch.float64, device="cuda"))
+    assert f.counts()["depth"] == 21 and phi.abs().max().item() == 0
+
+
+def test_errors(torch_cuda):
+    torch = torch_cuda
+    from paper_1405_7487_b200 import FMM, FMMError
+    from paper_1405_7487_b200.fmm import FMM_ERR_NONFINITE, FMM_ERR_STATE, FMM_ERR_ARG
+    f = FMM(100, 4, 0.5, 8, "f64")
+    p = torch.rand((10, 3), dtype=torch.float64, device="cuda")
+    q = torch.rand(10, dtype=torch.float64, device="cuda")
+    with pytest.raises(FMMError) as ei:
+        f.evaluate(p, q)
+    assert ei.value.status == FMM_ERR_STATE
+    bad = p.clone()
+    bad[3, 1] = float("nan")
+    with pytest.raises(FMMError) as ei:
+        f.build(bad)
+    assert ei.value.status == FMM_ERR_NONFINITE
+    with pytest.raises(FMMError) as ei:
+        f.build(torch.rand((101, 3), dtype=torch.float64, device="cuda"))
+    assert ei.value.status == FMM_ERR_ARG
+    with pytest.raises(FMMError):
+        f.build(p.float())
+    f.build(p)
+    with pytest.raises(FMMError) as ei:
+        f.evaluate(p.clone(), q)   # not the built positions
+    assert ei.value.status == FMM_ERR_STATE
+
+
+def test_solve_host_matches_device(torch_cuda):
+    torch = torch_cuda
+    from paper_1405_7487_b200 import FMM
+    pos, q = synth.generate("plummer", 5000, 77, np.float32)
+    f = FMM(5000, 6, 0.5, 32, "f32")
+    phi_h, grad_h = f.solve_host(pos, q)
+    phi_d, grad_d = f.solve(torch.from_numpy(pos).cuda(), torch.from_numpy(q).cuda())
+    np.testing.assert_array_equal(phi_h, phi_d.cpu().numpy())
+    np.testing.assert_array_equal(grad_h, grad_d.cpu().numpy())
+
+
+def test_repeat_builds_reuse_context(torch_cuda):
+    # a context grows its workspace across sizes and stays exact
+    for n in (500, 5000, 800):
+        pos, q = synth.generate("cube", n, n)
+        f, phi, grad = run_gpu(torch_cuda, pos, q, 4, 0.5, 16, "f64")
+        o = oracle.FMM(pos, q, 4, 0.5, 16)
+        ophi, ograd = o.evaluate()
+        assert oracle.rel_l2(phi, ophi) <= 1e-12
+
+
+def test_c2_full_size(torch_cuda):
+    """BASELINE configs[1] at full size in the launch configuration bench.py times:
+    structure bit-exact against the oracle; phi/grad on 1000 sampled targets against the
+    oracle's sampled-target mode (<= 1e-5) and against the direct sum (reported)."""
+    cfg = synth.CONFIGS["c2"]
+    pos, q = synth.generate(cfg["kind"], cfg["n"], cfg["seed"], np.float32)
+    f, phi, grad = run_gpu(torch_cuda, pos, q, cfg["P"], cfg["theta"], cfg["ncrit"], "f32")
+    p64, q64 = pos.astype(np.float64), q.astype(np.float64)
+    o = oracle.FMM(p64, q64, cfg["P"], cfg["theta"], cfg["ncrit"]).traverse()
+    check_structure(f, o)
+    t = synth.sample_targets(cfg["n"], 1000, cfg["seed"])
+    ophi, ograd = o.evaluate(t)
+    e_phi = oracle.rel_l2(phi[t], ophi)
+    e_grad = oracle.rel_l2(grad[t], ograd)
+    dphi, dgrad = oracle.direct(p64, q64, t)
+    print(f"c2: vs oracle phi {e_phi:.2e} grad {e_grad:.2e}; vs direct phi {oracle.rel_l2(phi[t], dphi):.2e} "
+          f"grad {oracle.rel_l2(grad[t], dgrad):.2e}")
+    assert e_phi <= 1e-5 and e_grad <= 1e-5
