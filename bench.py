@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""bench.py -- FMM particles/s on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+Step = one pass of the whole hot path on one synthetic input:
+fmm_build (bounds, keys, radix sort, octree, geometry, dual tree traversal, lists) +
+fmm_evaluate (P2M/M2M, M2L, P2P, L2L/L2P, un-permute), inputs resident in HBM.
+Default workload: BASELINE.json configs[1] (N = 2^20 uniform cube, fp32, P=10, theta=0.4,
+ncrit=64).  L2 is flushed (256 MB write) before every timed step; each step is timed with
+CUDA events on the stream the library runs on.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c2|c3|c1] [--impl reference]
+
+Multi-GPU (torchrun): every rank solves its own instance (weak scaling, no collective on the
+data path: replicas until the LET exchange lands); max time over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "FMM particles/s at 1/2/4/8 B200 (P=10); P2P+M2L % of FP32 roofline"
+CONFIG_NAMES = {"c1": "configs[0]", "c2": "configs[1]", "c3": "configs[2]"}
+FP32_LANES_PER_SM = 128
+
+
+# ----------------------------------------------------------- algorithmic work
+def t2n(P):
+    return P * (P + 1) // 2
+
+
+def m2l_flops_per_pair(P: int) -> dict:
+    """Algorithmic FP work of one M2L pair in the harmonic form the kernel evaluates
+    (m2l_fast.cu; FMA = 2 flops).  Returns flops and lane-instruction counts."""
+    fma = 0
+    # contraction: S0.D0 -> L0, S0.D1 -> L1, S1.D1 -> L0, N.D0 -> L1
+    for m in range(P):                 # S0 element of degree m (m+1 of them)
+        fma += (m + 1) * (t2n(P - m) + t2n(P - 1 - m))
+    for m in range(P - 1):             # S1
+        fma += (m + 1) * t2n(P - 1 - m)
+    for m in range(2, P):              # N
+        fma += (m + 1) * t2n(P - m)
+    # recurrence: per D entry ~ (terms) multiply-adds; count exactly as the kernel forms it
+    rec_instr = 0
+    for n in range(1, P):
+        for z in range(n + 1):         # D0 entries of degree n
+            y = n - z
+            t1 = (y > 0) + (z > 0)
+            t2 = (y > 1) + (z > 1)
+            rec_instr += t1 + t2 + (2 if n > 1 else 1)
+        for z in range(n):             # D1 entries of degree n
+            y = n - 1 - z
+            t1 = 1 + (y > 0) + (z > 0)
+            t2 = (y > 1) + (z > 1)
+            rec_instr += t1 + t2 + (2 if n > 1 else 1)
+    rec_instr += 2 * (P - 1) + 3 * P + 6   # m*u tables, per-degree A/B, r2, rcp, rsqrt
+    return {"fma": fma, "rec_instr": rec_instr, "instr": fma + rec_instr, "flops": 2 * fma + 2 * rec_instr}
+
+
+P2P_FLOPS = 20      # 3 sub, |r|^2 (3 mul 2 add), rsqrt, q/r, q/r^3 (2 mul), phi add, 3 fma grad
+P2P_INSTR = 13      # FP32-pipe instructions per interaction (SASS, -ftz)
+
+
+def peaks():
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+        return json.load(f)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------ oracle (CPU) arm
+def oracle_rate(cfg: dict, n_sample: int, reps: int = 1):
+    """The CPU oracle as it stands: full FMM on a bounded sample of the workload (same
+    distribution, P, theta, ncrit; first n_sample particles of a seed-identical draw)."""
+    import oracle
+    oracle.build()
+    dt = np.float32 if cfg["prec"] == "f32" else np.float64
+    pos, q = synth.generate(cfg["kind"], n_sample, cfg["seed"], dt)
+    p64, q64 = pos.astype(np.float64), q.astype(np.float64)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        o = oracle.FMM(p64, q64, cfg["P"], cfg["theta"], cfg["ncrit"])
+        o.evaluate()
+        times.append(time.perf_counter() - t0)
+        del o
+    return n_sample, times
+
+
+def cpu_baseline(cfg):
+    n_s = 1 << 14
+    n, times = oracle_rate(cfg, n_s)
+    return {"value": n / times[0], "unit": "particles/s", "cores": 1, "kind": "oracle",
+            "sample": f"full oracle FMM (keys..L2P) on {n} particles of the {cfg['kind']} distribution with the "
+                      f"workload's P={cfg['P']}, theta={cfg['theta']}, ncrit={cfg['ncrit']}; single-threaded fp64 "
+                      f"C, {times[0]:.1f} s"}
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the oracle on the host cores, same metric/unit (rank 0 only)."""
+    if rank != 0:
+        return
+    n_s = 1 << 13
+    n, times = oracle_rate(cfg, n_s, reps=args.warmup + args.steps)
+    timed = times[args.warmup:]
+    t = sum(timed) / len(timed)
+    line = {"metric": METRIC, "impl": "reference", "value": n / t, "unit": "particles/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(cfg, args),
+            "cpu_baseline": {"value": n / t, "unit": "particles/s", "cores": 1, "kind": "oracle",
+                             "sample": f"full oracle FMM on {n} particles of the workload's distribution and "
+                                       f"parameters per step"},
+            "e2e": {"value": n / t, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg, args):
+    return {"workload": f"BASELINE.json {CONFIG_NAMES[args.config]}: 3D Laplace FMM, N={cfg['n']} {cfg['kind']}, "
+                        f"{cfg['prec']}, P={cfg['P']}, theta={cfg['theta']}, ncrit={cfg['ncrit']}",
+            "N": cfg["n"], "distribution": cfg["kind"], "P": cfg["P"], "theta": cfg["theta"], "ncrit": cfg["ncrit"],
+            "precision": cfg["prec"], "seed": cfg["seed"], "l2": "flushed (256 MB write) before every timed step",
+            "parallelism": f"{args.gpus} independent replica(s), one per GPU" if args.gpus > 1 else "1 GPU"}
+
+
+# --------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIG_NAMES))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = synth.CONFIGS[args.config]
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1405_7487_b200 import FMM, build
+    build.build()
+    dt_np = np.float32 if cfg["prec"] == "f32" else np.float64
+    dt_t = torch.float32 if cfg["prec"] == "f32" else torch.float64
+    n = cfg["n"]
+    pos, q = synth.generate(cfg["kind"], n, cfg["seed"] + rank, dt_np)
+    dpos = torch.from_numpy(pos).cuda()
+    dq = torch.from_numpy(q).cuda()
+    phi = torch.empty(n, dtype=dt_t, device="cuda")
+    grad = torch.empty((n, 3), dtype=dt_t, device="cuda")
+    fmm = FMM(n, cfg["P"], cfg["theta"], cfg["ncrit"], cfg["prec"], local)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MB > 126 MB L2
+
+    def step():
+        fmm.build(dpos, stream)
+        fmm.evaluate(dpos, dq, phi, grad, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    fmm.set_timing(True)
+    fmm.phase_times(reset=True)
+    fmm.launch_count(reset=True)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        barrier()
+    launches = fmm.launch_count(reset=True)
+    ph = fmm.phase_times(reset=True)
+    fmm.set_timing(False)
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * n / (ms_step * 1e-3)
+
+    # ---- e2e: host buffers through fmm_solve_host (H2D + D2H inside the timed region)
+    hpos = torch.from_numpy(pos).pin_memory().numpy()
+    hq = torch.from_numpy(q).pin_memory().numpy()
+    hphi = torch.empty(n, dtype=dt_t).pin_memory().numpy()
+    hgrad = torch.empty((n, 3), dtype=dt_t).pin_memory().numpy()
+    fmm.solve_host(hpos, hq, hphi, hgrad)
+    barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(3, args.steps // 2)
+    for _ in range(e2e_steps):
+        flush.fill_(0.0)
+        torch.cuda.synchronize()
+        fmm.solve_host(hpos, hq, hphi, hgrad)      # synchronous: returns after the D2H copy
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if dist is not None:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    es = 4 if cfg["prec"] == "f32" else 8
+
+    counts = fmm.counts()
+    if rank == 0:
+        pk = peaks()
+        clocks = clk.summary()
+        sm_mhz = pk["sm_max_mhz"]
+        fp32_peak_tflops = 148 * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12     # FFMA = 2 flops
+        m2l = m2l_flops_per_pair(cfg["P"])
+        m2l_ms = ph.get("m2l_kernel", 0.0) / args.steps
+        p2p_ms = ph.get("p2p_kernel", 0.0) / args.steps
+        m2l_tf = counts["n_m2l"] * m2l["flops"] / (m2l_ms * 1e-3) / 1e12 if m2l_ms else 0.0
+        p2p_tf = counts["p2p_interactions"] * P2P_FLOPS / (p2p_ms * 1e-3) / 1e12 if p2p_ms else 0.0
+        dom = "m2l" if m2l_ms >= p2p_ms else "p2p"
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tpath):
+            traffic = json.load(open(tpath)).get(f"{args.config}:{dom}")
+        roof = {"kernel": f"{dom} ({'k_m2l_fast' if dom == 'm2l' else 'k_p2p'})", "bound": "alu",
+                "achieved": round(m2l_tf if dom == "m2l" else p2p_tf, 3), "peak": round(fp32_peak_tflops, 2),
+                "unit": "TFLOP/s", "frac": round((m2l_tf if dom == "m2l" else p2p_tf) / fp32_peak_tflops, 4),
+                "traffic": traffic,
+                "peak_note": "FP32 FFMA peak = 148 SMs x 128 lanes x 2 flop x sm_max_mhz (MEASURED_PEAKS.json); "
+                             "DESIGN.md §6",
+                "per_kernel": {
+                    "m2l": {"ms": round(m2l_ms, 4), "pairs": counts["n_m2l"], "flops_per_pair": m2l["flops"],
+                            "TFLOP/s": round(m2l_tf, 3), "frac": round(m2l_tf / fp32_peak_tflops, 4),
+                            "pairs_per_s": counts["n_m2l"] / (m2l_ms * 1e-3) if m2l_ms else None},
+                    "p2p": {"ms": round(p2p_ms, 4), "interactions": counts["p2p_interactions"],
+                            "flops_per_interaction": P2P_FLOPS, "TFLOP/s": round(p2p_tf, 3),
+                            "frac": round(p2p_tf / fp32_peak_tflops, 4),
+                            "interactions_per_s": counts["p2p_interactions"] / (p2p_ms * 1e-3) if p2p_ms else None}},
+                "measured": "CUDA events recorded by libfmm on the stream each kernel runs on (M2L on the caller's "
+                            "stream, P2P on the aux stream, concurrent)"}
+        line = {"metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32" if cfg["prec"] == "f32" else "f64",
+                "data": "synthetic (seeded SplitMix64 generator, synth/)",
+                "config": workload_config(cfg, args),
+                "e2e": {"value": world * n / e2e_s, "unit": "particles/s", "h2d_bytes_per_step": n * 4 * es,
+                        "d2h_bytes_per_step": n * 4 * es, "api": "fmm_solve_host (pinned host buffers)"},
+                "gpu_launches": launches,
+                "roofline": roof,
+                "clocks": clocks,
+                "phases_ms": {k: round(v / args.steps, 4) for k, v in ph.items()},
+                "counts": counts}
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -2,6 +2,7 @@
 // introspection, timing.  Every step of the path runs in this library's kernels; there is
 // no CPU fallback (a missing device is an FMM_ERR_CUDA).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -10,7 +11,7 @@
 
 namespace {
 const char* kPhaseNames[PH_COUNT] = {"bounds", "sort", "tree", "geometry", "dtt", "lists",
-                                      "upward", "m2l", "p2p", "downward", "copy"};
+                                      "upward", "m2l", "p2p", "downward", "copy", "m2l_kernel", "p2p_kernel"};
 
 fmm_status check_ctx(const fmm_ctx* ctx) { return ctx ? FMM_OK : FMM_ERR_ARG; }
 
@@ -108,6 +109,10 @@ fmm_status fmm_create(int64_t n_max, int p, double theta, int ncrit, int prec, i
         return FMM_ERR_CUDA;
     }
     ctx->num_sms = prop.multiProcessorCount;
+    {
+        const char* g = getenv("FMM_M2L_GENERIC");
+        ctx->use_fast_m2l = !(g && g[0] == '1');
+    }
     if (cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -127,7 +132,7 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
                       &ctx->c_bc, &ctx->c_cb, &ctx->c_cc, &ctx->c_parent, &ctx->c_bmin, &ctx->c_bmax, &ctx->c_cr,
                       &ctx->split_tmp, &ctx->split_cnt, &ctx->leaf_ids, &ctx->fr_a, &ctx->fr_b, &ctx->lst_m2l,
                       &ctx->lst_p2p, &ctx->lst_tmp, &ctx->m2l_src, &ctx->p2p_src, &ctx->m2l_off, &ctx->p2p_off,
-                      &ctx->cnt_tmp, &ctx->dcount, &ctx->M, &ctx->L, &ctx->Mr, &ctx->near_phi, &ctx->near_grad,
+                      &ctx->cnt_tmp, &ctx->dcount, &ctx->M, &ctx->L, &ctx->Mr, &ctx->Lr, &ctx->near_phi, &ctx->near_grad,
                       &ctx->h_stage};
     for (DevBuf* b : bufs) buf_free(*b);
     for (auto& t : ctx->pending) {

@@ -46,7 +46,7 @@ __device__ __forceinline__ void fill_ex_table(uchar4* ex, int ncoef) {
 // ---- phases for event timing
 enum Phase {
     PH_BOUNDS = 0, PH_SORT, PH_TREE, PH_GEOM, PH_DTT, PH_LISTS,
-    PH_UP, PH_M2L, PH_P2P, PH_DOWN, PH_COPY, PH_COUNT
+    PH_UP, PH_M2L, PH_P2P, PH_DOWN, PH_COPY, PH_M2L_KERNEL, PH_P2P_KERNEL, PH_COUNT
 };
 
 struct DevBuf {
@@ -66,6 +66,7 @@ struct fmm_ctx {
     double theta = 0.5;
     int ncrit = 32;
     int prec = FMM_F64;
+    bool use_fast_m2l = true;   // register-resident M2L where instantiated (FMM_M2L_GENERIC=1 disables)
     int device = 0;
     int num_sms = 148;
     std::string err;
@@ -107,7 +108,7 @@ struct fmm_ctx {
     DevBuf fr_a, fr_b, lst_m2l, lst_p2p, lst_tmp, m2l_src, p2p_src, m2l_off, p2p_off, cnt_tmp, dcount;
 
     // expansions
-    DevBuf M, L, Mr;       // fp64 [ncell][ncoef]; Mr: packed fp32 copy for the M2L kernel
+    DevBuf M, L, Mr, Lr;   // fp64 [ncell][ncoef]; Mr: packed reduced multipoles for the M2L kernel; Lr: reduced L
     DevBuf near_phi, near_grad;  // P2P partials in sorted order (prec type)
     DevBuf h_stage;              // device staging for fmm_solve_host
 };
@@ -173,5 +174,7 @@ fmm_status build_lists(fmm_ctx* ctx, cudaStream_t s);
 // upward.cu / downward.cu / m2l.cu / p2p.cu
 fmm_status upward_pass(fmm_ctx* ctx, cudaStream_t s);
 fmm_status m2l_pass(fmm_ctx* ctx, cudaStream_t s);
+fmm_status m2l_fast(fmm_ctx* ctx, cudaStream_t s);
+bool m2l_fast_available(int P, int prec);
 fmm_status p2p_pass(fmm_ctx* ctx, cudaStream_t s);
 fmm_status downward_pass(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s);

@@ -108,8 +108,10 @@ fmm_status m2l_generic(fmm_ctx* ctx, cudaStream_t s) {
 fmm_status m2l_pass(fmm_ctx* ctx, cudaStream_t s) {
     PhaseScope ps(ctx, PH_M2L, s);
     FMM_TRY(buf_ensure(ctx, ctx->L, (size_t)ctx->ncell * ctx->ncoef * 8));
+    if (ctx->use_fast_m2l && m2l_fast_available(ctx->P, ctx->prec)) return m2l_fast(ctx, s);
     // cells without M2L sources still need L = 0 (the generic kernel skips them)
     FMM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->L.p, 0, (size_t)ctx->ncell * ctx->ncoef * 8, s));
+    PhaseScope pk(ctx, PH_M2L_KERNEL, s);
     if (ctx->prec == FMM_F32) return m2l_generic<float>(ctx, s);
     return m2l_generic<double>(ctx, s);
 }

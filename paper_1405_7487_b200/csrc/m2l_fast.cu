@@ -1,0 +1,396 @@
+// m2l_fast.cu -- register-resident M2L for P <= 10 (fp32) / P <= 6 (fp64)  (a9, the hot kernel).
+//
+// Same mathematics as R14 (L_alpha = sum_beta (-1)^|beta| M_beta D^{alpha+beta}G), evaluated
+// in the harmonic ("trace-reduced") Cartesian form, which is exact because G = 1/r is
+// harmonic (sum_i D^{gamma+2e_i}G = 0 for every gamma; pinned in tests/test_oracle.py):
+//   * D_gamma with gamma_x >= 2 is never formed: only D0 = D_(0,y,z) (|.| <= P-1) and
+//     D1 = D_(1,y,z) (|.| <= P-2) -- P^2 values instead of P(P+1)(P+2)/6;
+//   * the signed multipole S_beta = (-1)^|beta| M_beta is folded onto beta_x in {0,1} once
+//     per source cell (S_beta -> S_{beta-2e_x+2e_y}, S_{beta-2e_x+2e_z} with weight -1),
+//     which leaves every contraction with D unchanged;
+//   * only L_alpha with alpha_x in {0,1} is computed; L is harmonic to truncation order
+//     (the |beta| range depends on |alpha| only), so L_alpha for alpha_x >= 2 is rebuilt
+//     exactly as -L_{alpha-2e_x+2e_y} - L_{alpha-2e_x+2e_z} (k_l_expand).
+//   With a+b = 2 folded into N[q'] = -S1[q'-2e_y] - S1[q'-2e_z], the four products are
+//     L0[p] += S0[q] D0[p+q]   (|p|+|q| <= P-1)     L0[p] += S1[q] D1[p+q] (<= P-2)
+//     L1[p] += S0[q] D1[p+q]   (<= P-2)             L1[p] += N[q'] D0[p+q'] (<= P-1)
+//   i.e. 2275 FMA per pair at P=10 instead of 5005, and a 100-entry recurrence instead of 220.
+// Scaling (fp32 range, SURVEY §7 hard part 5): every cell has rho = 2^e (e = E - level, an
+// exact power of two near the octant width).  Stored S_hat = S / rho_B^|beta|, D is evaluated
+// at u = d / rho_A, each streamed S_hat is multiplied by (rho_B/rho_A)^|beta| (skipped when
+// the whole warp has rho_B == rho_A), and the accumulators hold L_hat = L rho_A^(|alpha|+1).
+// All scalings are exact powers of two.
+// Work layout: one warp per target cell (CSR range), ONE PAIR PER LANE; the derivative
+// table (D0, D1) and the lane's L accumulators live in registers (compile-time indices,
+// fully unrolled); S_hat of the lane's source is streamed with 16-B loads.  Lanes
+// accumulate their pairs (same target) in Real, then the warp reduces in fp64 and stores
+// the reduced L_hat (no atomics).  Targets are handed to blocks through an atomic counter.
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace {
+
+template <int B, int E, typename F>
+__device__ __forceinline__ void sfor(F&& f) {
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>{});
+        sfor<B + 1, E>(f);
+    }
+}
+
+__host__ __device__ constexpr int t2(int y, int z) { return (y + z) * (y + z + 1) / 2 + z; }
+__host__ __device__ constexpr int deg2(int e) {
+    int m = 0;
+    while ((m + 1) * (m + 2) / 2 <= e) ++m;
+    return m;
+}
+__host__ __device__ constexpr int zof(int e) { return e - deg2(e) * (deg2(e) + 1) / 2; }
+__host__ __device__ constexpr int yof(int e) { return deg2(e) - zof(e); }
+
+template <int P>
+struct RF {
+    static constexpr int N0 = P * (P + 1) / 2;   // 2D indices of degree <= P-1
+    static constexpr int N1 = (P - 1) * P / 2;   // degree <= P-2
+    static constexpr int NS = 2 * N0 + N1;       // S0 | S1 | N
+    static constexpr int NSP = (NS + 3) / 4 * 4;
+    static constexpr int NL = N0 + N1;           // L0 | L1
+};
+
+__device__ __forceinline__ float fma_(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fma_(double a, double b, double c) { return fma(a, b, c); }
+__device__ __forceinline__ float rsqrt_(float x) { return rsqrtf(x); }
+__device__ __forceinline__ double rsqrt_(double x) { return 1.0 / sqrt(x); }
+__device__ __forceinline__ float rcp_(float x) { return __frcp_rn(x); }
+__device__ __forceinline__ double rcp_(double x) { return 1.0 / x; }
+
+template <typename R> struct Vec4;
+template <> struct Vec4<float> { using type = float4; };
+template <> struct Vec4<double> { using type = double4; };
+
+// D0[t2(y,z)] = D_(0,y,z)(u), D1[t2(y,z)] = D_(1,y,z)(u): derivative form of the R14 recurrence
+//   n r^2 D_k = -(2n-1) sum_i k_i u_i D_{k-e_i} - (n-1) sum_i k_i (k_i - 1) D_{k-2e_i}
+template <int P, typename R>
+__device__ __forceinline__ void derivs(R ux, R uy, R uz, R (&D0)[RF<P>::N0], R (&D1)[RF<P>::N1]) {
+    const R r2 = ux * ux + uy * uy + uz * uz;
+    const R ir2 = rcp_(r2);
+    R yu[P], zu[P];
+#pragma unroll
+    for (int m = 1; m < P; ++m) {
+        yu[m] = R(m) * uy;
+        zu[m] = R(m) * uz;
+    }
+    D0[0] = rsqrt_(r2);
+#pragma unroll
+    for (int n = 1; n < P; ++n) {
+        const R A = R(-(2.0 * n - 1.0) / n) * ir2;
+        const R B = R(-(n - 1.0) / n) * ir2;
+#pragma unroll
+        for (int z = 0; z <= n; ++z) {
+            const int y = n - z;
+            R s1 = R(0);
+            if (y > 0) s1 = yu[y] * D0[t2(y - 1, z)];
+            if (z > 0) s1 = (y > 0) ? fma_(zu[z], D0[t2(y, z - 1)], s1) : zu[z] * D0[t2(y, z - 1)];
+            R s2 = R(0);
+            if (y > 1) s2 = R(y * (y - 1)) * D0[t2(y - 2, z)];
+            if (z > 1) s2 = fma_(R(z * (z - 1)), D0[t2(y, z - 2)], s2);
+            D0[t2(y, z)] = (n > 1) ? fma_(A, s1, B * s2) : A * s1;
+        }
+#pragma unroll
+        for (int z = 0; z <= n - 1; ++z) {
+            const int y = n - 1 - z;
+            R s1 = ux * D0[t2(y, z)];
+            if (y > 0) s1 = fma_(yu[y], D1[t2(y - 1, z)], s1);
+            if (z > 0) s1 = fma_(zu[z], D1[t2(y, z - 1)], s1);
+            R s2 = R(0);
+            if (y > 1) s2 = R(y * (y - 1)) * D1[t2(y - 2, z)];
+            if (z > 1) s2 = fma_(R(z * (z - 1)), D1[t2(y, z - 2)], s2);
+            D1[t2(y, z)] = (n > 1) ? fma_(A, s1, B * s2) : A * s1;
+        }
+    }
+}
+
+// degree |beta| of stored element E (S0: |q|, S1: |q|+1, N: |q'|-1); -1 for padding
+template <int P>
+__host__ __device__ constexpr int elem_deg(int e) {
+    return e < RF<P>::N0 ? deg2(e)
+           : e < RF<P>::N0 + RF<P>::N1 ? deg2(e - RF<P>::N0) + 1
+           : e < RF<P>::NS ? deg2(e - RF<P>::N0 - RF<P>::N1) - 1
+                           : -1;
+}
+
+// one streamed element s = S_hat[E] into the accumulators
+template <int P, int E, typename R>
+__device__ __forceinline__ void apply_elem(R s, const R (&D0)[RF<P>::N0], const R (&D1)[RF<P>::N1],
+                                           R (&L0)[RF<P>::N0], R (&L1)[RF<P>::N1]) {
+    constexpr int N0 = RF<P>::N0, N1 = RF<P>::N1;
+    if constexpr (E < N0) {
+        constexpr int qy = yof(E), qz = zof(E), m = qy + qz;
+#pragma unroll
+        for (int pm = 0; pm <= P - 1 - m; ++pm)
+#pragma unroll
+            for (int pz = 0; pz <= pm; ++pz) {
+                const int py = pm - pz;
+                L0[t2(py, pz)] = fma_(s, D0[t2(py + qy, pz + qz)], L0[t2(py, pz)]);
+            }
+#pragma unroll
+        for (int pm = 0; pm <= P - 2 - m; ++pm)
+#pragma unroll
+            for (int pz = 0; pz <= pm; ++pz) {
+                const int py = pm - pz;
+                L1[t2(py, pz)] = fma_(s, D1[t2(py + qy, pz + qz)], L1[t2(py, pz)]);
+            }
+    } else if constexpr (E < N0 + N1) {
+        constexpr int e = E - N0, qy = yof(e), qz = zof(e), m = qy + qz;
+#pragma unroll
+        for (int pm = 0; pm <= P - 2 - m; ++pm)
+#pragma unroll
+            for (int pz = 0; pz <= pm; ++pz) {
+                const int py = pm - pz;
+                L0[t2(py, pz)] = fma_(s, D1[t2(py + qy, pz + qz)], L0[t2(py, pz)]);
+            }
+    } else if constexpr (E < RF<P>::NS) {
+        constexpr int e = E - N0 - N1, qy = yof(e), qz = zof(e), m = qy + qz;
+        if constexpr (m >= 2) {
+#pragma unroll
+            for (int pm = 0; pm <= P - 1 - m; ++pm)
+#pragma unroll
+                for (int pz = 0; pz <= pm; ++pz) {
+                    const int py = pm - pz;
+                    L1[t2(py, pz)] = fma_(s, D0[t2(py + qy, pz + qz)], L1[t2(py, pz)]);
+                }
+        }
+    }
+}
+
+template <int P, typename R>
+__global__ void __launch_bounds__(128, 2)
+    k_m2l_fast(int64_t ncell, const uint64_t* __restrict__ lst, const uint64_t* __restrict__ off,
+               const double4* __restrict__ cr, const int* __restrict__ sexp,
+               const typename Vec4<R>::type* __restrict__ Sv, double* __restrict__ Lr,
+               unsigned long long* __restrict__ counter) {
+    using V4 = typename Vec4<R>::type;
+    constexpr int N0 = RF<P>::N0, N1 = RF<P>::N1, NCH = RF<P>::NSP / 4, NL = RF<P>::NL;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __shared__ long long s_base;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_base = (long long)atomicAdd(counter, 4ull);
+        __syncthreads();
+        const long long base = s_base;
+        if (base >= ncell) break;
+        const long long a = base + w;
+        if (a >= ncell) continue;
+        const uint64_t p0 = off[a], p1 = off[a + 1];
+        if (p0 == p1) continue;
+        const double4 ca = cr[a];
+        const int ea = sexp[a];
+        const double sa = exp2((double)-ea);   // 1/rho_A, exact
+        R L0[N0], L1[N1];
+#pragma unroll
+        for (int i = 0; i < N0; ++i) L0[i] = R(0);
+#pragma unroll
+        for (int i = 0; i < N1; ++i) L1[i] = R(0);
+        for (uint64_t p = p0 + lane; p < p1; p += 32) {
+            const uint32_t b = (uint32_t)lst[p];
+            const double4 cb = cr[b];
+            const int eb = sexp[b];
+            const R ux = (R)((ca.x - cb.x) * sa);
+            const R uy = (R)((ca.y - cb.y) * sa);
+            const R uz = (R)((ca.z - cb.z) * sa);
+            R D0[N0], D1[N1];
+            derivs<P, R>(ux, uy, uz, D0, D1);
+            // (rho_B / rho_A)^n per degree, exact powers of two
+            const int de = eb - ea;
+            R pw[P];
+            pw[0] = R(1);
+            pw[1] = (R)exp2((double)de);
+#pragma unroll
+            for (int n = 2; n < P; ++n) pw[n] = pw[n - 1] * pw[1];
+            const V4* sv = Sv + (size_t)b * NCH;
+            const bool same = de == 0;
+            sfor<0, NCH>([&](auto c) {
+                constexpr int C4 = decltype(c)::value;
+                const V4 v = sv[C4];
+                const R vv[4] = {v.x, v.y, v.z, v.w};
+                sfor<0, 4>([&](auto j) {
+                    constexpr int E = 4 * C4 + decltype(j)::value;
+                    constexpr int dg = elem_deg<P>(E);
+                    if constexpr (dg >= 0) {
+                        R s = vv[decltype(j)::value];
+                        if constexpr (dg > 0) s = same ? s : s * pw[dg];
+                        apply_elem<P, E, R>(s, D0, D1, L0, L1);
+                    }
+                });
+            });
+        }
+        // warp reduction in fp64, lane (k mod 32) stores entry k of the reduced L_hat
+        sfor<0, NL>([&](auto kk) {
+            constexpr int k = decltype(kk)::value;
+            double v;
+            if constexpr (k < N0) v = (double)L0[k];
+            else v = (double)L1[k - N0];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == (k & 31)) Lr[(size_t)a * NL + k] = v;
+        });
+    }
+}
+
+// per source cell: signed M -> harmonic fold onto beta_x in {0,1} -> S0 | S1 | N, scaled by
+// rho^-|beta| and rounded to R.  Also records the cell's scale exponent.
+template <typename R>
+__global__ void k_m2l_prep(int64_t ncell, int P, int ncoef, int NS, int NSP, const double* __restrict__ M,
+                           const int32_t* __restrict__ level, const double* __restrict__ root,
+                           int* __restrict__ sexp, R* __restrict__ Sv) {
+    extern __shared__ double s_S[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double* S = s_S + (size_t)w * ncoef;
+    // E: 2^E >= root cube width 2h (exact power of two)
+    int E;
+    frexp(2.0 * root[10], &E);
+    const int N0 = P * (P + 1) / 2, N1 = (P - 1) * P / 2;
+    for (int64_t c = (int64_t)blockIdx.x * nw + w; c < ncell; c += (int64_t)gridDim.x * nw) {
+        const int e = E - level[c];
+        for (int k = lane; k < ncoef; k += 32) {
+            int a, b, cc;
+            decode_cidx(k, a, b, cc);
+            double m = M[(size_t)c * ncoef + k];
+            S[k] = ((a + b + cc) & 1) ? -m : m;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            sexp[c] = e;
+            for (int bx = P - 1; bx >= 2; --bx)
+                for (int by = 0; by <= P - 1 - bx; ++by)
+                    for (int bz = 0; bz <= P - 1 - bx - by; ++bz) {
+                        double v = S[cidx(bx, by, bz)];
+                        S[cidx(bx - 2, by + 2, bz)] -= v;
+                        S[cidx(bx - 2, by, bz + 2)] -= v;
+                    }
+        }
+        __syncwarp();
+        R* out = Sv + (size_t)c * NSP;
+        for (int i = lane; i < NSP; i += 32) {
+            double v = 0.0;
+            int dg = 0;
+            if (i < N0) {
+                int m = 0;
+                while ((m + 1) * (m + 2) / 2 <= i) ++m;
+                int z = i - m * (m + 1) / 2, y = m - z;
+                v = S[cidx(0, y, z)];
+                dg = m;
+            } else if (i < N0 + N1) {
+                int ii = i - N0, m = 0;
+                while ((m + 1) * (m + 2) / 2 <= ii) ++m;
+                int z = ii - m * (m + 1) / 2, y = m - z;
+                v = S[cidx(1, y, z)];
+                dg = m + 1;
+            } else if (i < NS) {
+                int ii = i - N0 - N1, m = 0;
+                while ((m + 1) * (m + 2) / 2 <= ii) ++m;
+                int z = ii - m * (m + 1) / 2, y = m - z;
+                if (m >= 2) {
+                    if (y >= 2) v -= S[cidx(1, y - 2, z)];
+                    if (z >= 2) v -= S[cidx(1, y, z - 2)];
+                }
+                dg = m - 1;
+            }
+            out[i] = (R)ldexp(v, -e * dg);
+        }
+        __syncwarp();
+    }
+}
+
+// reduced, scaled L_hat -> full fp64 L (R11 order) by harmonicity, zero for cells without M2L
+__global__ void k_l_expand(int64_t ncell, int P, int ncoef, const uint64_t* __restrict__ off,
+                           const int* __restrict__ sexp, const double* __restrict__ Lr, double* __restrict__ L) {
+    extern __shared__ double s_L[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double* Lf = s_L + (size_t)w * ncoef;
+    const int N0 = P * (P + 1) / 2, NL = P * P;
+    for (int64_t c = (int64_t)blockIdx.x * nw + w; c < ncell; c += (int64_t)gridDim.x * nw) {
+        double* out = L + (size_t)c * ncoef;
+        if (off[c] == off[c + 1]) {
+            for (int k = lane; k < ncoef; k += 32) out[k] = 0.0;
+            continue;
+        }
+        const int e = sexp[c];
+        for (int i = lane; i < NL; i += 32) {
+            int ax = i < N0 ? 0 : 1, ii = i < N0 ? i : i - N0, m = 0;
+            while ((m + 1) * (m + 2) / 2 <= ii) ++m;
+            int z = ii - m * (m + 1) / 2, y = m - z;
+            Lf[cidx(ax, y, z)] = ldexp(Lr[(size_t)c * NL + i], -e * (ax + m + 1));
+        }
+        __syncwarp();
+        for (int ax = 2; ax < P; ++ax) {
+            int cnt = (P - ax) * (P - ax + 1) / 2;
+            for (int i = lane; i < cnt; i += 32) {
+                int m = 0;
+                while ((m + 1) * (m + 2) / 2 <= i) ++m;
+                int z = i - m * (m + 1) / 2, y = m - z;
+                Lf[cidx(ax, y, z)] = -Lf[cidx(ax - 2, y + 2, z)] - Lf[cidx(ax - 2, y, z + 2)];
+            }
+            __syncwarp();
+        }
+        for (int k = lane; k < ncoef; k += 32) out[k] = Lf[k];
+        __syncwarp();
+    }
+}
+
+template <int P, typename R>
+fmm_status m2l_fast_t(fmm_ctx* ctx, cudaStream_t s) {
+    constexpr int NSP = RF<P>::NSP, NL = RF<P>::NL;
+    const int64_t nc = ctx->ncell;
+    FMM_TRY(buf_ensure(ctx, ctx->Mr, (size_t)nc * NSP * sizeof(R) + (size_t)nc * 4 + 256));
+    FMM_TRY(buf_ensure(ctx, ctx->Lr, (size_t)nc * NL * 8));
+    FMM_TRY(buf_ensure(ctx, ctx->cnt_tmp, 64));
+    R* Sv = P_<R>(ctx->Mr);
+    int* sexp = reinterpret_cast<int*>(reinterpret_cast<char*>(ctx->Mr.p) + (size_t)nc * NSP * sizeof(R));
+    const int nw = 4;
+    int g = (int)std::min<int64_t>((nc + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
+    k_m2l_prep<R><<<std::max(g, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
+        nc, P, ctx->ncoef, RF<P>::NS, NSP, P_<double>(ctx->M), P_<int32_t>(ctx->c_level), P_<double>(ctx->root), sexp,
+        Sv);
+    FMM_LAUNCH(ctx);
+    unsigned long long* counter = P_<unsigned long long>(ctx->cnt_tmp);
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 8, s));
+    {
+        PhaseScope ps(ctx, PH_M2L_KERNEL, s);
+        k_m2l_fast<P, R><<<ctx->num_sms * 2, 128, 0, s>>>(nc, P_<uint64_t>(ctx->lst_m2l), P_<uint64_t>(ctx->m2l_off),
+                                                         P_<double4>(ctx->c_cr), sexp,
+                                                         reinterpret_cast<const typename Vec4<R>::type*>(Sv),
+                                                         P_<double>(ctx->Lr), counter);
+        FMM_LAUNCH(ctx);
+    }
+    k_l_expand<<<std::max(g, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
+        nc, P, ctx->ncoef, P_<uint64_t>(ctx->m2l_off), sexp, P_<double>(ctx->Lr), P_<double>(ctx->L));
+    FMM_LAUNCH(ctx);
+    FMM_CUDA_TRY(ctx, cudaGetLastError());
+    return FMM_OK;
+}
+}  // namespace
+
+// returns FMM_ERR_ARG (without launching) when no register kernel exists for (P, prec)
+fmm_status m2l_fast(fmm_ctx* ctx, cudaStream_t s) {
+    if (ctx->prec == FMM_F32) {
+        switch (ctx->P) {
+            case 4: return m2l_fast_t<4, float>(ctx, s);
+            case 6: return m2l_fast_t<6, float>(ctx, s);
+            case 8: return m2l_fast_t<8, float>(ctx, s);
+            case 10: return m2l_fast_t<10, float>(ctx, s);
+            default: break;
+        }
+    } else {
+        switch (ctx->P) {
+            case 4: return m2l_fast_t<4, double>(ctx, s);
+            case 6: return m2l_fast_t<6, double>(ctx, s);
+            default: break;
+        }
+    }
+    return FMM_ERR_ARG;
+}
+
+bool m2l_fast_available(int P, int prec) {
+    return prec == FMM_F32 ? (P == 4 || P == 6 || P == 8 || P == 10) : (P == 4 || P == 6);
+}

@@ -84,6 +84,7 @@ fmm_status p2p_t(fmm_ctx* ctx, cudaStream_t s) {
     PhaseScope ps(ctx, PH_P2P, s);
     FMM_TRY(buf_ensure(ctx, ctx->near_phi, (size_t)ctx->n * sizeof(Real)));
     FMM_TRY(buf_ensure(ctx, ctx->near_grad, (size_t)ctx->n * 3 * sizeof(Real)));
+    PhaseScope pk(ctx, PH_P2P_KERNEL, s);
     int g = (int)std::min<int64_t>((ctx->nleaf + PP_WARPS - 1) / PP_WARPS, (int64_t)ctx->num_sms * 16);
     k_p2p_generic<Body, Real><<<std::max(g, 1), PP_WARPS * 32, 0, s>>>(
         P_<Body>(ctx->body), P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, P_<uint64_t>(ctx->lst_p2p),
