@@ -112,6 +112,12 @@ fmm_status fmm_create(int64_t n_max, int p, double theta, int ncrit, int prec, i
     {
         const char* g = getenv("FMM_M2L_GENERIC");
         ctx->use_fast_m2l = !(g && g[0] == '1');
+        const char* g2 = getenv("FMM_P2P_GENERIC");
+        ctx->use_fast_p2p = !(g2 && g2[0] == '1');
+        const char* g3 = getenv("FMM_P2P_VARIANT");
+        ctx->p2p_variant = g3 ? atoi(g3) : 0;
+        const char* g4 = getenv("FMM_OVERLAP");
+        ctx->serial_nearfar = !(g4 && g4[0] == '1');
     }
     if (cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -132,7 +138,8 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
                       &ctx->c_bc, &ctx->c_cb, &ctx->c_cc, &ctx->c_parent, &ctx->c_bmin, &ctx->c_bmax, &ctx->c_cr,
                       &ctx->split_tmp, &ctx->split_cnt, &ctx->leaf_ids, &ctx->fr_a, &ctx->fr_b, &ctx->lst_m2l,
                       &ctx->lst_p2p, &ctx->lst_tmp, &ctx->m2l_src, &ctx->p2p_src, &ctx->m2l_off, &ctx->p2p_off,
-                      &ctx->cnt_tmp, &ctx->dcount, &ctx->M, &ctx->L, &ctx->Mr, &ctx->Lr, &ctx->near_phi, &ctx->near_grad,
+                      &ctx->cnt_tmp, &ctx->cnt_tmp2, &ctx->dcount, &ctx->runs, &ctx->run_off, &ctx->run_tmp, &ctx->run_pre,
+                      &ctx->run_len64, &ctx->dcount2, &ctx->M, &ctx->L, &ctx->Mr, &ctx->Lr, &ctx->near_phi, &ctx->near_grad,
                       &ctx->h_stage};
     for (DevBuf* b : bufs) buf_free(*b);
     for (auto& t : ctx->pending) {
@@ -193,13 +200,19 @@ fmm_status fmm_evaluate(fmm_ctx* ctx, const void* pos, const void* q, void* phi,
     cudaStream_t s = (cudaStream_t)stream;
     FMM_TRY(gather_bodies_q(ctx, q, s));
     FMM_TRY(upward_pass(ctx, s));
-    // P2P on the aux stream concurrently with M2L on the caller's stream
-    FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
-    FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
-    FMM_TRY(p2p_pass(ctx, ctx->aux));
-    FMM_TRY(m2l_pass(ctx, s));
-    FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, ctx->aux));
-    FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
+    if (ctx->serial_nearfar) {
+        // both persistent kernels fill the GPU on their own: run them back to back
+        FMM_TRY(p2p_pass(ctx, s));
+        FMM_TRY(m2l_pass(ctx, s));
+    } else {
+        // P2P on the aux stream concurrently with M2L on the caller's stream
+        FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
+        FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+        FMM_TRY(p2p_pass(ctx, ctx->aux));
+        FMM_TRY(m2l_pass(ctx, s));
+        FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, ctx->aux));
+        FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
+    }
     FMM_TRY(downward_pass(ctx, phi, grad, s));
     ctx->evaluated = true;
     return FMM_OK;

@@ -12,43 +12,61 @@ namespace {
 constexpr int DN_WARPS = 4;
 constexpr int LP_WARPS = 2;
 
-__device__ __forceinline__ void pow_table(double* t, double x, int P, int lane) {
-    if (lane < P) {
-        double v = 1.0;
-        for (int i = 1; i <= lane; ++i) v = v * x / (double)i;
-        t[lane] = v;
+__constant__ double c_inv[FMM_MAXP + 1] = {0.0,       1.0,        1.0 / 2,  1.0 / 3,  1.0 / 4,  1.0 / 5,
+                                           1.0 / 6,   1.0 / 7,    1.0 / 8,  1.0 / 9,  1.0 / 10, 1.0 / 11,
+                                           1.0 / 12,  1.0 / 13,   1.0 / 14, 1.0 / 15, 1.0 / 16};
+
+// separable 1D "down" shift along axis ax: out_alpha = sum_{k <= P-1-|alpha|} in_{alpha + k e_ax} t[k]
+__device__ __forceinline__ void shift_pass_down(const uchar4* __restrict__ ex, int ncoef, int P, int ax,
+                                                const double* in, double* out, const double* t, int lane) {
+    for (int kk = lane; kk < ncoef; kk += 32) {
+        const uchar4 e = ex[kk];
+        int a[3] = {e.x, e.y, e.z};
+        const int base = a[ax], top = P - 1 - e.w;
+        double s = 0.0;
+        for (int k = 0; k <= top; ++k) {
+            a[ax] = base + k;
+            s += in[cidx(a[0], a[1], a[2])] * t[k];
+        }
+        out[kk] = s;
     }
 }
 
-// children at level l+1 receive their parent's shifted local expansion
+// children at level l+1 receive their parent's shifted local expansion: R15 grouped as three
+// 1D passes (the shift operator s^g/g! is separable per axis)
 __global__ void __launch_bounds__(DN_WARPS * 32) k_l2l(int64_t cbeg, int64_t cend, const int32_t* __restrict__ parent,
                                                         const double4* __restrict__ cr, int P, int ncoef,
                                                         double* __restrict__ L) {
+    extern __shared__ double s_dyn[];
     __shared__ uchar4 ex[816];
-    __shared__ double s_pow[DN_WARPS][3][FMM_MAXP];
+    __shared__ double s_t[DN_WARPS][3][FMM_MAXP];
     fill_ex_table(ex, ncoef);
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double* A = s_dyn + (size_t)w * 2 * ncoef;
+    double* B = A + ncoef;
     for (int64_t c = cbeg + (int64_t)blockIdx.x * DN_WARPS + w; c < cend; c += (int64_t)gridDim.x * DN_WARPS) {
-        int32_t par = parent[c];
-        double4 cc = cr[c], cp = cr[par];
-        const double* Lp = L + (int64_t)par * ncoef;
+        const int32_t par = parent[c];
+        const double4 cc = cr[c], cp = cr[par];
         __syncwarp();
-        pow_table(s_pow[w][0], cc.x - cp.x, P, lane);
-        pow_table(s_pow[w][1], cc.y - cp.y, P, lane);
-        pow_table(s_pow[w][2], cc.z - cp.z, P, lane);
-        __syncwarp();
-        for (int k = lane; k < ncoef; k += 32) {
-            uchar4 e = ex[k];
-            int m = P - 1 - e.w;
-            double sum = 0.0;
-            for (int gx = 0; gx <= m; ++gx)
-                for (int gy = 0; gy <= m - gx; ++gy)
-                    for (int gz = 0; gz <= m - gx - gy; ++gz)
-                        sum += Lp[cidx(e.x + gx, e.y + gy, e.z + gz)] *
-                               (s_pow[w][0][gx] * s_pow[w][1][gy] * s_pow[w][2][gz]);
-            L[(int64_t)c * ncoef + k] += sum;
+        for (int i = lane; i < ncoef; i += 32) A[i] = L[(int64_t)par * ncoef + i];
+        if (lane < 3) {
+            const double sh = lane == 0 ? cc.x - cp.x : lane == 1 ? cc.y - cp.y : cc.z - cp.z;
+            double v = 1.0;
+            s_t[w][lane][0] = 1.0;
+            for (int e = 1; e < P; ++e) {
+                v = v * sh * c_inv[e];
+                s_t[w][lane][e] = v;
+            }
         }
+        __syncwarp();
+        shift_pass_down(ex, ncoef, P, 0, A, B, s_t[w][0], lane);
+        __syncwarp();
+        shift_pass_down(ex, ncoef, P, 1, B, A, s_t[w][1], lane);
+        __syncwarp();
+        shift_pass_down(ex, ncoef, P, 2, A, B, s_t[w][2], lane);
+        __syncwarp();
+        for (int i = lane; i < ncoef; i += 32) L[(int64_t)c * ncoef + i] += B[i];
     }
 }
 
@@ -86,7 +104,7 @@ __global__ void __launch_bounds__(LP_WARPS * 32) k_l2p(const Body* __restrict__ 
                 double v = 1.0;
                 s_pw[w][d][0][lane] = 1.0;
                 for (int e = 1; e < P; ++e) {
-                    v = v * z[d] / (double)e;
+                    v = v * z[d] * c_inv[e];
                     s_pw[w][d][e][lane] = v;
                 }
             }
@@ -117,10 +135,12 @@ template <typename Body, typename Real>
 fmm_status downward_t(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s) {
     PhaseScope ps(ctx, PH_DOWN, s);
     double* L = P_<double>(ctx->L);
+    const size_t smem = (size_t)DN_WARPS * 2 * ctx->ncoef * 8;
+    if (smem > 48 * 1024) FMM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_l2l, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     for (int64_t l = 1; l <= ctx->depth; ++l) {
         int64_t b = ctx->level_begin[l], e = ctx->level_begin[l + 1];
         int g = (int)std::min<int64_t>((e - b + DN_WARPS - 1) / DN_WARPS, (int64_t)ctx->num_sms * 16);
-        k_l2l<<<std::max(g, 1), DN_WARPS * 32, 0, s>>>(b, e, P_<int32_t>(ctx->c_parent), P_<double4>(ctx->c_cr),
+        k_l2l<<<std::max(g, 1), DN_WARPS * 32, smem, s>>>(b, e, P_<int32_t>(ctx->c_parent), P_<double4>(ctx->c_cr),
                                                        ctx->P, ctx->ncoef, L);
         FMM_LAUNCH(ctx);
     }

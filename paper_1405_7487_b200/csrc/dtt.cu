@@ -151,6 +151,119 @@ fmm_status sort_and_index(fmm_ctx* ctx, DevBuf& lst, int64_t n, DevBuf& off, cud
     return FMM_OK;
 }
 
+__global__ void k_widen(const uint32_t* __restrict__ in, int64_t n, uint64_t* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = in[i];
+}
+
+// ---- P2P source runs: consecutive list entries of one target whose body ranges are
+// contiguous (Morton-adjacent leaves) merge into one run {start body, flat offset in the
+// target's source stream}; rtot[t] = total sources of target t.  Used by the P2P kernel to
+// stream a target's sources as full fixed-size chunks.
+__global__ void k_run_flags(const uint64_t* __restrict__ lst, int64_t n, const uint32_t* __restrict__ bb,
+                            const uint32_t* __restrict__ bc, uint32_t* __restrict__ flag) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t cur = lst[i];
+    uint32_t f = 1;
+    if (i > 0) {
+        const uint64_t prv = lst[i - 1];
+        const uint32_t sp = (uint32_t)prv, sc = (uint32_t)cur;
+        f = ((prv >> 32) != (cur >> 32)) || (bb[sp] + bc[sp] != bb[sc]);
+    }
+    flag[i] = f;
+}
+
+__global__ void k_run_emit(const uint64_t* __restrict__ lst, int64_t n, const uint32_t* __restrict__ bb,
+                           const uint32_t* __restrict__ bc, const uint32_t* __restrict__ flag,
+                           const uint32_t* __restrict__ rid, uint32_t* __restrict__ rstart, uint32_t* __restrict__ rlen,
+                           uint32_t* __restrict__ rtarget) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t cur = lst[i];
+    const uint32_t sc = (uint32_t)cur, r = rid[i] + flag[i] - 1;   // run containing entry i
+    if (flag[i]) {
+        rstart[r] = bb[sc];
+        rtarget[r] = (uint32_t)(cur >> 32);
+    }
+    if (i + 1 == n || flag[i + 1]) rlen[r] = bb[sc] + bc[sc];   // end body; converted to length below
+}
+
+__global__ void k_run_len(int64_t nr, const uint32_t* __restrict__ rstart, uint32_t* __restrict__ rlen) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < nr) rlen[r] -= rstart[r];
+}
+
+// per target: roff (first run), then each run's flat offset within its target and the total
+__global__ void k_run_csr(const uint32_t* __restrict__ rtarget, int64_t nr, int64_t ncell, uint32_t* __restrict__ roff) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c > ncell) return;
+    int64_t lo = 0, hi = nr;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (rtarget[mid] < (uint32_t)c) lo = mid + 1;
+        else hi = mid;
+    }
+    roff[c] = (uint32_t)lo;
+}
+
+__global__ void k_run_flat(int64_t nr, int64_t ncell, const uint32_t* __restrict__ rtarget,
+                           const uint32_t* __restrict__ roff, const uint32_t* __restrict__ rstart,
+                           const uint64_t* __restrict__ gpre, const uint32_t* __restrict__ rlen,
+                           uint2* __restrict__ runs, uint32_t* __restrict__ rtot) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < nr) {
+        const uint32_t t = rtarget[r];
+        runs[r] = make_uint2(rstart[r], (uint32_t)(gpre[r] - gpre[roff[t]]));
+    }
+    if (r < ncell) {
+        const uint32_t a = roff[r], b = roff[r + 1];
+        rtot[r] = (a == b) ? 0u : (uint32_t)(gpre[b - 1] + rlen[b - 1] - gpre[a]);
+    }
+}
+
+fmm_status build_runs(fmm_ctx* ctx, cudaStream_t s) {
+    const int64_t n = ctx->n_p2p, nc = ctx->ncell;
+    FMM_TRY(buf_ensure(ctx, ctx->run_tmp, (size_t)std::max<int64_t>(n, 1) * 4 * 5 + 64));
+    uint32_t* flag = P_<uint32_t>(ctx->run_tmp);
+    uint32_t* rid = flag + n;
+    uint32_t* rstart = rid + n;
+    uint32_t* rlen = rstart + n;
+    uint32_t* rtarget = rlen + n;
+    FMM_TRY(buf_ensure(ctx, ctx->dcount2, 64));
+    uint32_t* d_nr = P_<uint32_t>(ctx->dcount2);
+    const unsigned g = (unsigned)((n + 255) / 256);
+    k_run_flags<<<g, 256, 0, s>>>(P_<uint64_t>(ctx->lst_p2p), n, P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), flag);
+    FMM_LAUNCH(ctx);
+    FMM_TRY(scan_exclusive_u32(ctx, flag, rid, n, d_nr, s));
+    k_run_emit<<<g, 256, 0, s>>>(P_<uint64_t>(ctx->lst_p2p), n, P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc),
+                                 flag, rid, rstart, rlen, rtarget);
+    FMM_LAUNCH(ctx);
+    uint32_t nr = 0;
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&nr, d_nr, 4, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    ctx->n_runs = nr;
+    k_run_len<<<(unsigned)((nr + 255) / 256), 256, 0, s>>>(nr, rstart, rlen);
+    FMM_LAUNCH(ctx);
+    FMM_TRY(buf_ensure(ctx, ctx->run_off, (size_t)(nc + 2) * 4));
+    FMM_TRY(buf_ensure(ctx, ctx->runs, (size_t)std::max<int64_t>(nr, 1) * 8 + (size_t)(nc + 1) * 4 + 64));
+    FMM_TRY(buf_ensure(ctx, ctx->run_pre, (size_t)std::max<int64_t>(nr, 1) * 8));
+    k_run_csr<<<(unsigned)((nc + 1 + 255) / 256), 256, 0, s>>>(rtarget, nr, nc, P_<uint32_t>(ctx->run_off));
+    FMM_LAUNCH(ctx);
+    // 64-bit exclusive scan of the run lengths (widen on the fly)
+    FMM_TRY(buf_ensure(ctx, ctx->run_len64, (size_t)std::max<int64_t>(nr, 1) * 8));
+    k_widen<<<(unsigned)((nr + 255) / 256), 256, 0, s>>>(rlen, nr, P_<uint64_t>(ctx->run_len64));
+    FMM_LAUNCH(ctx);
+    FMM_TRY(scan_exclusive_u64(ctx, P_<uint64_t>(ctx->run_len64), P_<uint64_t>(ctx->run_pre), nr, nullptr, s));
+    uint2* runs = P_<uint2>(ctx->runs);
+    uint32_t* rtot = reinterpret_cast<uint32_t*>(runs + std::max<int64_t>(nr, 1));
+    k_run_flat<<<(unsigned)((std::max<int64_t>(nr, nc) + 255) / 256), 256, 0, s>>>(
+        nr, nc, rtarget, P_<uint32_t>(ctx->run_off), rstart, P_<uint64_t>(ctx->run_pre), rlen, runs, rtot);
+    FMM_LAUNCH(ctx);
+    FMM_CUDA_TRY(ctx, cudaGetLastError());
+    return FMM_OK;
+}
+
 }  // namespace
 
 fmm_status build_lists(fmm_ctx* ctx, cudaStream_t s) {
@@ -205,5 +318,5 @@ fmm_status build_lists(fmm_ctx* ctx, cudaStream_t s) {
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&inter, P_<unsigned long long>(ctx->dcount) + 7, 8, cudaMemcpyDeviceToHost, s));
     FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
     ctx->p2p_inter = (int64_t)inter;
-    return FMM_OK;
+    return build_runs(ctx, s);
 }

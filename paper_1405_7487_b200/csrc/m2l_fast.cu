@@ -17,14 +17,14 @@
 //   i.e. 2275 FMA per pair at P=10 instead of 5005, and a 100-entry recurrence instead of 220.
 // Scaling (fp32 range, SURVEY §7 hard part 5): every cell has rho = 2^e (e = E - level, an
 // exact power of two near the octant width).  Stored S_hat = S / rho_B^|beta|, D is evaluated
-// at u = d / rho_A, each streamed S_hat is multiplied by (rho_B/rho_A)^|beta| (skipped when
-// the whole warp has rho_B == rho_A), and the accumulators hold L_hat = L rho_A^(|alpha|+1).
+// at u = d / rho_A, each streamed S_hat is multiplied by (rho_B/rho_A)^|beta|, and the
+// accumulators hold L_hat = L rho_A^(|alpha|+1).
 // All scalings are exact powers of two.
 // Work layout: one warp per target cell (CSR range), ONE PAIR PER LANE; the derivative
 // table (D0, D1) and the lane's L accumulators live in registers (compile-time indices,
 // fully unrolled); S_hat of the lane's source is streamed with 16-B loads.  Lanes
 // accumulate their pairs (same target) in Real, then the warp reduces in fp64 and stores
-// the reduced L_hat (no atomics).  Targets are handed to blocks through an atomic counter.
+// the reduced L_hat (no atomics).  Targets are handed to warps through an atomic counter.
 #include <type_traits>
 
 #include "common.cuh"
@@ -172,15 +172,12 @@ __global__ void __launch_bounds__(128, 2)
     using V4 = typename Vec4<R>::type;
     constexpr int N0 = RF<P>::N0, N1 = RF<P>::N1, NCH = RF<P>::NSP / 4, NL = RF<P>::NL;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    __shared__ long long s_base;
+    (void)w;
     for (;;) {
-        __syncthreads();
-        if (threadIdx.x == 0) s_base = (long long)atomicAdd(counter, 4ull);
-        __syncthreads();
-        const long long base = s_base;
-        if (base >= ncell) break;
-        const long long a = base + w;
-        if (a >= ncell) continue;
+        unsigned long long an = 0;
+        if (lane == 0) an = atomicAdd(counter, 1ull);
+        const long long a = (long long)__shfl_sync(0xffffffffu, an, 0);
+        if (a >= ncell) break;
         const uint64_t p0 = off[a], p1 = off[a + 1];
         if (p0 == p1) continue;
         const double4 ca = cr[a];
@@ -208,7 +205,6 @@ __global__ void __launch_bounds__(128, 2)
 #pragma unroll
             for (int n = 2; n < P; ++n) pw[n] = pw[n - 1] * pw[1];
             const V4* sv = Sv + (size_t)b * NCH;
-            const bool same = de == 0;
             sfor<0, NCH>([&](auto c) {
                 constexpr int C4 = decltype(c)::value;
                 const V4 v = sv[C4];
@@ -218,7 +214,7 @@ __global__ void __launch_bounds__(128, 2)
                     constexpr int dg = elem_deg<P>(E);
                     if constexpr (dg >= 0) {
                         R s = vv[decltype(j)::value];
-                        if constexpr (dg > 0) s = same ? s : s * pw[dg];
+                        if constexpr (dg > 0) s *= pw[dg];
                         apply_elem<P, E, R>(s, D0, D1, L0, L1);
                     }
                 });

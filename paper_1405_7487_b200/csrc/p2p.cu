@@ -8,6 +8,8 @@
 //
 // Generic kernel: warp per target leaf, 2 targets per lane (64 per pass), sources of each
 // list entry staged through a per-warp shared-memory tile and read as broadcasts.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace {
@@ -79,12 +81,322 @@ __global__ void __launch_bounds__(PP_WARPS * 32) k_p2p_generic(const Body* __res
     }
 }
 
+
+// ---------------------------------------------------------------- fp32 fast path
+// Warp per target leaf (dynamic: per-warp atomic counter).  The leaf's nt targets are
+// spread over lpg = ceil(nt/T) lanes with T = 4 targets per lane; the warp's 32 lanes form
+// G = 32/lpg groups that split the source stream (group g takes sources g, g+G, ...), so
+// small leaves still fill the warp.  Source leaves are streamed through a per-warp
+// double-buffered shared-memory tile with cp.async (16 B per body); in the inner loop the
+// G groups read G consecutive float4 (one wavefront).  Non-self pairs skip the r^2 > 0
+// test (coincident points share a key and hence a leaf, so r^2 = 0 only occurs in the
+// self pair A<-A, which takes the checked loop).  Group partials are summed in shared memory.
+constexpr int PF_WARPS = 8;
+constexpr int PF_T = 4;
+constexpr int PF_TILE = 64;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+template <bool CHECK>
+__device__ __forceinline__ void p2p_body(const float4 s, const float (&x)[PF_T], const float (&y)[PF_T],
+                                         const float (&z)[PF_T], float (&f)[PF_T], float (&gx)[PF_T],
+                                         float (&gy)[PF_T], float (&gz)[PF_T]) {
+#pragma unroll
+    for (int k = 0; k < PF_T; ++k) {
+        const float dx = s.x - x[k], dy = s.y - y[k], dz = s.z - z[k];
+        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        float inv = rsqrtf(r2);
+        if (CHECK) inv = r2 > 0.f ? inv : 0.f;
+        const float qi = s.w * inv;
+        const float qi3 = qi * (inv * inv);
+        f[k] += qi;
+        gx[k] = fmaf(qi3, dx, gx[k]);
+        gy[k] = fmaf(qi3, dy, gy[k]);
+        gz[k] = fmaf(qi3, dz, gz[k]);
+    }
+}
+
+__global__ void __launch_bounds__(PF_WARPS * 32) k_p2p_f32(const float4* __restrict__ body,
+                                                           const uint32_t* __restrict__ leaf_ids, int64_t nleaf,
+                                                           const uint64_t* __restrict__ lst,
+                                                           const uint64_t* __restrict__ off,
+                                                           const uint32_t* __restrict__ bb,
+                                                           const uint32_t* __restrict__ bc, float* __restrict__ near_phi,
+                                                           float* __restrict__ near_grad,
+                                                           unsigned long long* __restrict__ counter) {
+    __shared__ __align__(16) float4 s_tile[PF_WARPS][2][PF_TILE];
+    __shared__ float4 s_red[PF_WARPS][32 * PF_T];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    float4 (*tile)[PF_TILE] = s_tile[w];
+    for (;;) {
+        unsigned long long li = 0;
+        if (lane == 0) li = atomicAdd(counter, 1ull);
+        li = __shfl_sync(0xffffffffu, li, 0);
+        if (li >= (unsigned long long)nleaf) break;
+        const uint32_t a = leaf_ids[li];
+        const uint32_t tb = bb[a], nt_all = bc[a];
+        const uint64_t p0 = off[a], p1 = off[a + 1];
+        for (uint32_t t0 = 0; t0 < nt_all; t0 += 32 * PF_T) {
+            const uint32_t nt = min(nt_all - t0, (uint32_t)(32 * PF_T));
+            const int lpg = (int)((nt + PF_T - 1) / PF_T);
+            const int G = min(32 / lpg, 16);
+            const int g = lane / lpg, j = lane - g * lpg;
+            const bool active = g < G;
+            float x[PF_T], y[PF_T], z[PF_T], f[PF_T], gx[PF_T], gy[PF_T], gz[PF_T];
+#pragma unroll
+            for (int k = 0; k < PF_T; ++k) {
+                const uint32_t t = (uint32_t)(j + k * lpg);
+                const float4 p = body[tb + t0 + (t < nt ? t : 0)];
+                // unused slots sit far away so they never produce r^2 = 0
+                x[k] = t < nt ? p.x : 1e30f; y[k] = p.y; z[k] = p.z;
+                f[k] = gx[k] = gy[k] = gz[k] = 0.f;
+            }
+            // chunk iterator over (list entry, offset in source leaf)
+            uint64_t cp_ = p0;
+            uint32_t cs = 0;
+            auto chunk = [&](uint64_t pp, uint32_t s0, uint32_t& src, uint32_t& m, bool& self) {
+                const uint32_t b = (uint32_t)lst[pp];
+                src = bb[b] + s0;
+                m = min((uint32_t)PF_TILE, bc[b] - s0);
+                self = b == a;
+            };
+            auto advance = [&](uint64_t& pp, uint32_t& s0) {
+                const uint32_t b = (uint32_t)lst[pp];
+                s0 += PF_TILE;
+                if (s0 >= bc[b]) { ++pp; s0 = 0; }
+            };
+            int buf = 0;
+            uint32_t src_c = 0, m_c = 0;
+            bool self_c = false;
+            if (cp_ < p1) {
+                chunk(cp_, cs, src_c, m_c, self_c);
+                for (uint32_t i = lane; i < m_c; i += 32) cp_async16(&tile[0][i], body + src_c + i);
+            }
+            cp_async_commit();
+            while (cp_ < p1) {
+                // prefetch the next chunk into the other buffer
+                uint64_t np_ = cp_;
+                uint32_t ns_ = cs;
+                advance(np_, ns_);
+                uint32_t src_n = 0, m_n = 0;
+                bool self_n = false;
+                if (np_ < p1) {
+                    chunk(np_, ns_, src_n, m_n, self_n);
+                    for (uint32_t i = lane; i < m_n; i += 32) cp_async16(&tile[buf ^ 1][i], body + src_n + i);
+                }
+                cp_async_commit();
+                cp_async_wait_1();
+                __syncwarp();
+                if (active) {
+                    const float4* tl = tile[buf];
+                    if (self_c) {
+                        for (uint32_t i = g; i < m_c; i += G) p2p_body<true>(tl[i], x, y, z, f, gx, gy, gz);
+                    } else {
+                        for (uint32_t i = g; i < m_c; i += G) p2p_body<false>(tl[i], x, y, z, f, gx, gy, gz);
+                    }
+                }
+                __syncwarp();
+                cp_ = np_;
+                cs = ns_;
+                m_c = m_n;
+                self_c = self_n;
+                buf ^= 1;
+            }
+            cp_async_wait_0();
+            // sum the G group partials per target
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < PF_T; ++k) s_red[w][lane * PF_T + k] = make_float4(f[k], gx[k], gy[k], gz[k]);
+            __syncwarp();
+            if (g == 0) {
+#pragma unroll
+                for (int k = 0; k < PF_T; ++k) {
+                    const uint32_t t = (uint32_t)(j + k * lpg);
+                    if (t < nt) {
+                        float4 acc = s_red[w][lane * PF_T + k];
+                        for (int gg = 1; gg < G; ++gg) {
+                            const float4 v = s_red[w][(gg * lpg + j) * PF_T + k];
+                            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+                        }
+                        const int64_t o = (int64_t)tb + t0 + t;
+                        near_phi[o] = acc.x;
+                        near_grad[3 * o] = acc.y;
+                        near_grad[3 * o + 1] = acc.z;
+                        near_grad[3 * o + 2] = acc.w;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+
+// ------------------------------------------------------- fp32 CTA-per-leaf path
+// One CTA (128 threads) per target leaf, taken from an atomic counter in leaf order.  The
+// leaf's nt targets occupy lpg = ceil(nt/4) threads x 4 registers; the CTA's 128 threads form
+// G = 128/lpg groups that split the target's source stream (512 slots per CTA keeps the
+// slot use ~90-100% for the ragged occupancies around ncrit/2).  The source stream is the
+// target's P2P list flattened into Morton-contiguous body runs (build_runs); it is cut into
+// chunks of CH = G*floor(256/G) bodies, loaded with cp.async into a double-buffered shared
+// tile (thread i fetches flat indices i and i+128, locating its run with a forward cursor),
+// and group g consumes entries g, g+G, ... (G consecutive float4 per step).  Only chunks
+// that overlap the target's own leaf take the r^2 > 0 test.
+constexpr int PC_THREADS = 128;
+constexpr int PC_TILE = 256;
+
+__global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict__ body,
+                                                         const uint32_t* __restrict__ leaf_ids, int64_t nleaf,
+                                                         const uint2* __restrict__ runs,
+                                                         const uint32_t* __restrict__ roff,
+                                                         const uint32_t* __restrict__ rtot,
+                                                         const uint32_t* __restrict__ bb, const uint32_t* __restrict__ bc,
+                                                         float* __restrict__ near_phi, float* __restrict__ near_grad,
+                                                         unsigned long long* __restrict__ counter) {
+    __shared__ __align__(16) float4 s_tile[2][PC_TILE];
+    __shared__ float4 s_red[PC_THREADS * PF_T];
+    __shared__ unsigned long long s_leaf;
+    __shared__ uint32_t s_self;
+    const int tid = threadIdx.x;
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) s_leaf = atomicAdd(counter, 1ull);
+        __syncthreads();
+        const unsigned long long li = s_leaf;
+        if (li >= (unsigned long long)nleaf) break;
+        const uint32_t a = leaf_ids[li];
+        const uint32_t tb = bb[a], nt_all = bc[a];
+        const uint32_t r0 = roff[a], r1 = roff[a + 1], ns = rtot[a];
+        // flat offset of the target's own bodies in its source stream
+        for (uint32_t r = r0 + tid; r < r1; r += PC_THREADS) {
+            const uint2 ru = runs[r];
+            const uint32_t end = (r + 1 < r1) ? runs[r + 1].y : ns;
+            if (ru.x <= tb && tb < ru.x + (end - ru.y)) s_self = ru.y + (tb - ru.x);
+        }
+        __syncthreads();
+        const uint32_t selfF = s_self;
+        for (uint32_t t0 = 0; t0 < nt_all; t0 += PC_THREADS * PF_T) {
+            const uint32_t nt = min(nt_all - t0, (uint32_t)(PC_THREADS * PF_T));
+            const int lpg = (int)((nt + PF_T - 1) / PF_T);
+            const int G = min(PC_THREADS / lpg, 64);
+            const int g = tid / lpg, j = tid - g * lpg;
+            const bool active = g < G;
+            const uint32_t CH = (uint32_t)(G * (PC_TILE / G));
+            float x[PF_T], y[PF_T], z[PF_T], f[PF_T], gx[PF_T], gy[PF_T], gz[PF_T];
+#pragma unroll
+            for (int k = 0; k < PF_T; ++k) {
+                const uint32_t t = (uint32_t)(j + k * lpg);
+                const float4 p = body[tb + t0 + (t < nt ? t : 0)];
+                x[k] = t < nt ? p.x : 1e30f; y[k] = p.y; z[k] = p.z;
+                f[k] = gx[k] = gy[k] = gz[k] = 0.f;
+            }
+            // loader cursors for flat indices tid and tid + 128 of every chunk
+            uint32_t cur0 = r0, cur1 = r0;
+            auto load_chunk = [&](uint32_t k, int buf) {
+                const uint32_t f0 = k * CH;
+                const uint32_t len = min(CH, ns - f0);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t i = (uint32_t)tid + (uint32_t)h * PC_THREADS;
+                    if (i < len) {
+                        const uint32_t fl = f0 + i;
+                        uint32_t& cur = h ? cur1 : cur0;
+                        while (cur + 1 < r1 && runs[cur + 1].y <= fl) ++cur;
+                        const uint2 ru = runs[cur];
+                        cp_async16(&s_tile[buf][i], body + ru.x + (fl - ru.y));
+                    }
+                }
+            };
+            const uint32_t nch = (ns + CH - 1) / CH;
+            if (nch > 0) load_chunk(0, 0);
+            cp_async_commit();
+            for (uint32_t k = 0; k < nch; ++k) {
+                if (k + 1 < nch) load_chunk(k + 1, (k + 1) & 1);
+                cp_async_commit();
+                cp_async_wait_1();
+                __syncthreads();
+                const uint32_t f0 = k * CH;
+                const uint32_t len = min(CH, ns - f0);
+                if (active) {
+                    const float4* tl = s_tile[k & 1];
+                    const bool self = f0 < selfF + nt_all && selfF < f0 + len;
+                    if (self) {
+                        for (uint32_t i = g; i < len; i += G) p2p_body<true>(tl[i], x, y, z, f, gx, gy, gz);
+                    } else {
+                        for (uint32_t i = g; i < len; i += G) p2p_body<false>(tl[i], x, y, z, f, gx, gy, gz);
+                    }
+                }
+                __syncthreads();
+            }
+            cp_async_wait_0();
+#pragma unroll
+            for (int k = 0; k < PF_T; ++k) s_red[tid * PF_T + k] = make_float4(f[k], gx[k], gy[k], gz[k]);
+            __syncthreads();
+            if (g == 0) {
+#pragma unroll
+                for (int k = 0; k < PF_T; ++k) {
+                    const uint32_t t = (uint32_t)(j + k * lpg);
+                    if (t < nt) {
+                        float4 acc = s_red[tid * PF_T + k];
+                        for (int gg = 1; gg < G; ++gg) {
+                            const float4 v = s_red[(gg * lpg + j) * PF_T + k];
+                            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+                        }
+                        const int64_t o = (int64_t)tb + t0 + t;
+                        near_phi[o] = acc.x;
+                        near_grad[3 * o] = acc.y;
+                        near_grad[3 * o + 1] = acc.z;
+                        near_grad[3 * o + 2] = acc.w;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
 template <typename Body, typename Real>
 fmm_status p2p_t(fmm_ctx* ctx, cudaStream_t s) {
     PhaseScope ps(ctx, PH_P2P, s);
     FMM_TRY(buf_ensure(ctx, ctx->near_phi, (size_t)ctx->n * sizeof(Real)));
     FMM_TRY(buf_ensure(ctx, ctx->near_grad, (size_t)ctx->n * 3 * sizeof(Real)));
     PhaseScope pk(ctx, PH_P2P_KERNEL, s);
+    if (std::is_same<Real, float>::value && ctx->use_fast_p2p && ctx->p2p_variant == 0) {
+        FMM_TRY(buf_ensure(ctx, ctx->cnt_tmp2, 64));
+        unsigned long long* counter = P_<unsigned long long>(ctx->cnt_tmp2);
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 8, s));
+        int nb = 0;
+        FMM_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_p2p_cta, PC_THREADS, 0));
+        const uint2* runs = P_<uint2>(ctx->runs);
+        const uint32_t* rtot = reinterpret_cast<const uint32_t*>(runs + std::max<int64_t>(ctx->n_runs, 1));
+        k_p2p_cta<<<ctx->num_sms * std::max(nb, 1), PC_THREADS, 0, s>>>(
+            P_<float4>(ctx->body), P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, runs, P_<uint32_t>(ctx->run_off), rtot,
+            P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), (float*)ctx->near_phi.p, (float*)ctx->near_grad.p,
+            counter);
+        FMM_LAUNCH(ctx);
+        FMM_CUDA_TRY(ctx, cudaGetLastError());
+        return FMM_OK;
+    }
+    if (std::is_same<Real, float>::value && ctx->use_fast_p2p) {
+        FMM_TRY(buf_ensure(ctx, ctx->cnt_tmp2, 64));
+        unsigned long long* counter = P_<unsigned long long>(ctx->cnt_tmp2);
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 8, s));
+        int nb = 0;
+        FMM_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_p2p_f32, PF_WARPS * 32, 0));
+        k_p2p_f32<<<ctx->num_sms * std::max(nb, 1), PF_WARPS * 32, 0, s>>>(
+            P_<float4>(ctx->body), P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, P_<uint64_t>(ctx->lst_p2p),
+            P_<uint64_t>(ctx->p2p_off), P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), (float*)ctx->near_phi.p,
+            (float*)ctx->near_grad.p, counter);
+        FMM_LAUNCH(ctx);
+        FMM_CUDA_TRY(ctx, cudaGetLastError());
+        return FMM_OK;
+    }
     int g = (int)std::min<int64_t>((ctx->nleaf + PP_WARPS - 1) / PP_WARPS, (int64_t)ctx->num_sms * 16);
     k_p2p_generic<Body, Real><<<std::max(g, 1), PP_WARPS * 32, 0, s>>>(
         P_<Body>(ctx->body), P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, P_<uint64_t>(ctx->lst_p2p),

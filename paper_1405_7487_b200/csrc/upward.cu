@@ -5,102 +5,147 @@
 // kernel ... translates the multipole expansions from its children's centers to its center."
 // R12 P2M: M_beta(C) = sum_j q_j (x_j - c_C)^beta / beta!
 // R13 M2M: M_alpha(par) += sum_{beta <= alpha} M_beta(ch) s^(alpha-beta)/(alpha-beta)!, s = c_ch - c_par
-// Post-order is realised level-synchronously: all cells of level l+1 are final before
-// level l is formed.  Warp per cell, lanes over coefficients, per-warp power tables
-// x^e/e! in shared memory, accumulators in shared memory (runtime P <= 16).
+// Post-order is realised level-synchronously (all cells of level l+1 final before level l).
+//
+// P2M: warp per leaf; 32 bodies at a time, each lane builds its body's x^e/e! tables in
+// shared memory, then lanes over coefficients accumulate the 32 bodies in order.
+// M2M: warp per parent; the shift operator is separable, s^(a-b)/(a-b)! = prod_i
+// s_i^(a_i-b_i)/(a_i-b_i)!, so each child's expansion is shifted by three 1D passes
+// (x, then y, then z) through shared memory -- the same sum as R13, grouped per axis.
 #include "common.cuh"
 
 namespace {
 constexpr int UP_WARPS = 4;
+constexpr int P2M_WARPS = 2;
 
-// lanes 0..P-1 of the warp fill t[e] = x^e / e! (product of x/i; same value as the
-// definition up to rounding order)
-__device__ __forceinline__ void pow_table(double* t, double x, int P, int lane) {
-    if (lane < P) {
-        double v = 1.0;
-        for (int i = 1; i <= lane; ++i) v = v * x / (double)i;
-        t[lane] = v;
-    }
-}
+__constant__ double c_inv[FMM_MAXP + 1] = {0.0,       1.0,        1.0 / 2,  1.0 / 3,  1.0 / 4,  1.0 / 5,
+                                           1.0 / 6,   1.0 / 7,    1.0 / 8,  1.0 / 9,  1.0 / 10, 1.0 / 11,
+                                           1.0 / 12,  1.0 / 13,   1.0 / 14, 1.0 / 15, 1.0 / 16};
 
 template <typename Body>
-__global__ void __launch_bounds__(UP_WARPS * 32) k_p2m(const Body* __restrict__ body, const uint32_t* __restrict__ leaf_ids,
+__global__ void __launch_bounds__(P2M_WARPS * 32) k_p2m(const Body* __restrict__ body, const uint32_t* __restrict__ leaf_ids,
                                                         int64_t nleaf, const uint32_t* __restrict__ bb,
                                                         const uint32_t* __restrict__ bc, const double4* __restrict__ cr,
                                                         int P, int ncoef, double* __restrict__ M) {
     __shared__ uchar4 ex[816];
-    __shared__ double s_pow[UP_WARPS][3][FMM_MAXP];
-    __shared__ double s_acc[UP_WARPS][816];
+    __shared__ double s_pw[P2M_WARPS][3][FMM_MAXP][33];
+    __shared__ double s_q[P2M_WARPS][32];
     fill_ex_table(ex, ncoef);
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int64_t li = (int64_t)blockIdx.x * UP_WARPS + w; li < nleaf; li += (int64_t)gridDim.x * UP_WARPS) {
-        uint32_t c = leaf_ids[li];
-        double4 ctr = cr[c];
-        for (int k = lane; k < ncoef; k += 32) s_acc[w][k] = 0.0;
-        uint32_t b0 = bb[c], nb = bc[c];
-        for (uint32_t j = 0; j < nb; ++j) {
-            Body p = body[b0 + j];
-            double q = (double)p.w;
+    for (int64_t li = (int64_t)blockIdx.x * P2M_WARPS + w; li < nleaf; li += (int64_t)gridDim.x * P2M_WARPS) {
+        const uint32_t c = leaf_ids[li];
+        const double4 ctr = cr[c];
+        double acc[26];
+#pragma unroll
+        for (int i = 0; i < 26; ++i) acc[i] = 0.0;
+        const uint32_t b0 = bb[c], nb = bc[c];
+        for (uint32_t j0 = 0; j0 < nb; j0 += 32) {
+            const uint32_t m = min(32u, nb - j0);
             __syncwarp();
-            pow_table(s_pow[w][0], (double)p.x - ctr.x, P, lane);
-            pow_table(s_pow[w][1], (double)p.y - ctr.y, P, lane);
-            pow_table(s_pow[w][2], (double)p.z - ctr.z, P, lane);
+            if ((uint32_t)lane < m) {
+                const Body p = body[b0 + j0 + lane];
+                const double d[3] = {(double)p.x - ctr.x, (double)p.y - ctr.y, (double)p.z - ctr.z};
+                s_q[w][lane] = (double)p.w;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    double v = 1.0;
+                    s_pw[w][a][0][lane] = 1.0;
+                    for (int e = 1; e < P; ++e) {
+                        v = v * d[a] * c_inv[e];
+                        s_pw[w][a][e][lane] = v;
+                    }
+                }
+            }
             __syncwarp();
-            for (int k = lane; k < ncoef; k += 32) {
-                uchar4 e = ex[k];
-                s_acc[w][k] += q * (s_pow[w][0][e.x] * s_pow[w][1][e.y] * s_pow[w][2][e.z]);
+#pragma unroll
+            for (int i = 0; i < 26; ++i) {
+                const int k = lane + 32 * i;
+                if (k < ncoef) {
+                    const uchar4 e = ex[k];
+                    double sacc = acc[i];
+                    for (uint32_t j = 0; j < m; ++j)
+                        sacc += s_q[w][j] * (s_pw[w][0][e.x][j] * s_pw[w][1][e.y][j] * s_pw[w][2][e.z][j]);
+                    acc[i] = sacc;
+                }
             }
         }
-        __syncwarp();
-        for (int k = lane; k < ncoef; k += 32) M[(int64_t)c * ncoef + k] = s_acc[w][k];
-        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 26; ++i) {
+            const int k = lane + 32 * i;
+            if (k < ncoef) M[(int64_t)c * ncoef + k] = acc[i];
+        }
+    }
+}
+
+// one separable 1D shift pass along axis `ax`: out_alpha = sum_{b <= a_ax} in_{alpha with a_ax -> b} t[a_ax - b]
+__device__ __forceinline__ void shift_pass_up(const uchar4* __restrict__ ex, int ncoef, int ax, const double* in,
+                                              double* out, const double* t, int lane) {
+    for (int k = lane; k < ncoef; k += 32) {
+        const uchar4 e = ex[k];
+        int a[3] = {e.x, e.y, e.z};
+        const int top = a[ax];
+        double s = 0.0;
+        for (int b = 0; b <= top; ++b) {
+            a[ax] = b;
+            s += in[cidx(a[0], a[1], a[2])] * t[top - b];
+        }
+        out[k] = s;
     }
 }
 
 __global__ void __launch_bounds__(UP_WARPS * 32) k_m2m(int64_t cbeg, int64_t cend, const uint32_t* __restrict__ cb,
                                                         const uint32_t* __restrict__ cc, const double4* __restrict__ cr,
                                                         int P, int ncoef, double* __restrict__ M) {
+    extern __shared__ double s_dyn[];
     __shared__ uchar4 ex[816];
-    __shared__ double s_pow[UP_WARPS][3][FMM_MAXP];
+    __shared__ double s_t[UP_WARPS][3][FMM_MAXP];
     fill_ex_table(ex, ncoef);
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double* A = s_dyn + (size_t)w * 2 * ncoef;
+    double* B = A + ncoef;
     for (int64_t c = cbeg + (int64_t)blockIdx.x * UP_WARPS + w; c < cend; c += (int64_t)gridDim.x * UP_WARPS) {
-        uint32_t nk = cc[c];
-        if (nk == 0) continue;  // leaf: P2M already wrote it
-        double4 cp = cr[c];
+        const uint32_t nk = cc[c];
+        if (nk == 0) continue;  // leaf: written by P2M
+        const double4 cp = cr[c];
         double acc[26];
 #pragma unroll
         for (int i = 0; i < 26; ++i) acc[i] = 0.0;
         for (uint32_t k = 0; k < nk; ++k) {
-            uint32_t ch = cb[c] + k;
-            double4 cc4 = cr[ch];
-            const double* Mc = M + (int64_t)ch * ncoef;
+            const uint32_t ch = cb[c] + k;
+            const double4 q = cr[ch];
             __syncwarp();
-            pow_table(s_pow[w][0], cc4.x - cp.x, P, lane);
-            pow_table(s_pow[w][1], cc4.y - cp.y, P, lane);
-            pow_table(s_pow[w][2], cc4.z - cp.z, P, lane);
+            for (int i = lane; i < ncoef; i += 32) A[i] = M[(int64_t)ch * ncoef + i];
+            if (lane < 3) {
+                const double s = lane == 0 ? q.x - cp.x : lane == 1 ? q.y - cp.y : q.z - cp.z;
+                double v = 1.0;
+                s_t[w][lane][0] = 1.0;
+                for (int e = 1; e < P; ++e) {
+                    v = v * s * c_inv[e];
+                    s_t[w][lane][e] = v;
+                }
+            }
+            __syncwarp();
+            shift_pass_up(ex, ncoef, 0, A, B, s_t[w][0], lane);
+            __syncwarp();
+            shift_pass_up(ex, ncoef, 1, B, A, s_t[w][1], lane);
             __syncwarp();
 #pragma unroll
             for (int i = 0; i < 26; ++i) {
-                int kk = lane + 32 * i;
-                if (kk >= ncoef) break;
-                uchar4 e = ex[kk];
-                double sum = 0.0;
-                for (int bx = 0; bx <= e.x; ++bx)
-                    for (int by = 0; by <= e.y; ++by)
-                        for (int bz = 0; bz <= e.z; ++bz)
-                            sum += Mc[cidx(bx, by, bz)] *
-                                   (s_pow[w][0][e.x - bx] * s_pow[w][1][e.y - by] * s_pow[w][2][e.z - bz]);
-                acc[i] += sum;
+                const int kk = lane + 32 * i;
+                if (kk < ncoef) {
+                    const uchar4 e = ex[kk];
+                    double s = 0.0;
+                    for (int b = 0; b <= e.z; ++b) s += A[cidx(e.x, e.y, b)] * s_t[w][2][e.z - b];
+                    acc[i] += s;
+                }
             }
         }
 #pragma unroll
         for (int i = 0; i < 26; ++i) {
-            int kk = lane + 32 * i;
-            if (kk >= ncoef) break;
-            M[(int64_t)c * ncoef + kk] = acc[i];
+            const int kk = lane + 32 * i;
+            if (kk < ncoef) M[(int64_t)c * ncoef + kk] = acc[i];
         }
     }
 }
@@ -111,16 +156,18 @@ fmm_status upward_t(fmm_ctx* ctx, cudaStream_t s) {
     const int64_t nc = ctx->ncell;
     FMM_TRY(buf_ensure(ctx, ctx->M, (size_t)nc * ctx->ncoef * 8));
     double* M = P_<double>(ctx->M);
-    int g = (int)std::min<int64_t>((ctx->nleaf + UP_WARPS - 1) / UP_WARPS, (int64_t)ctx->num_sms * 16);
-    k_p2m<Body><<<std::max(g, 1), UP_WARPS * 32, 0, s>>>(P_<Body>(ctx->body), P_<uint32_t>(ctx->leaf_ids), ctx->nleaf,
+    int g = (int)std::min<int64_t>((ctx->nleaf + P2M_WARPS - 1) / P2M_WARPS, (int64_t)ctx->num_sms * 32);
+    k_p2m<Body><<<std::max(g, 1), P2M_WARPS * 32, 0, s>>>(P_<Body>(ctx->body), P_<uint32_t>(ctx->leaf_ids), ctx->nleaf,
                                                          P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc),
                                                          P_<double4>(ctx->c_cr), ctx->P, ctx->ncoef, M);
     FMM_LAUNCH(ctx);
+    const size_t smem = (size_t)UP_WARPS * 2 * ctx->ncoef * 8;
+    if (smem > 48 * 1024) FMM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_m2m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     for (int64_t l = ctx->depth - 1; l >= 0; --l) {
         int64_t b = ctx->level_begin[l], e = ctx->level_begin[l + 1];
         int gg = (int)std::min<int64_t>((e - b + UP_WARPS - 1) / UP_WARPS, (int64_t)ctx->num_sms * 16);
-        k_m2m<<<std::max(gg, 1), UP_WARPS * 32, 0, s>>>(b, e, P_<uint32_t>(ctx->c_cb), P_<uint32_t>(ctx->c_cc),
-                                                        P_<double4>(ctx->c_cr), ctx->P, ctx->ncoef, M);
+        k_m2m<<<std::max(gg, 1), UP_WARPS * 32, smem, s>>>(b, e, P_<uint32_t>(ctx->c_cb), P_<uint32_t>(ctx->c_cc),
+                                                           P_<double4>(ctx->c_cr), ctx->P, ctx->ncoef, M);
         FMM_LAUNCH(ctx);
     }
     FMM_CUDA_TRY(ctx, cudaGetLastError());
