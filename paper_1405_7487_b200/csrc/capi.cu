@@ -118,6 +118,8 @@ fmm_status fmm_create(int64_t n_max, int p, double theta, int ncrit, int prec, i
         ctx->p2p_variant = g3 ? atoi(g3) : 0;
         const char* g4 = getenv("FMM_OVERLAP");
         ctx->serial_nearfar = !(g4 && g4[0] == '1');
+        const char* g5 = getenv("FMM_CANONICAL_M2L");
+        ctx->canonical_m2l = !(g5 && g5[0] == '0');
     }
     if (cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -139,7 +141,7 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
                       &ctx->split_tmp, &ctx->split_cnt, &ctx->leaf_ids, &ctx->fr_a, &ctx->fr_b, &ctx->lst_m2l,
                       &ctx->lst_p2p, &ctx->lst_tmp, &ctx->m2l_src, &ctx->p2p_src, &ctx->m2l_off, &ctx->p2p_off,
                       &ctx->cnt_tmp, &ctx->cnt_tmp2, &ctx->dcount, &ctx->runs, &ctx->run_off, &ctx->run_tmp, &ctx->run_pre,
-                      &ctx->run_len64, &ctx->dcount2, &ctx->M, &ctx->L, &ctx->Mr, &ctx->Lr, &ctx->near_phi, &ctx->near_grad,
+                      &ctx->run_len64, &ctx->dcount2, &ctx->tcnt, &ctx->cnt64, &ctx->M, &ctx->L, &ctx->Mr, &ctx->Lr, &ctx->near_phi, &ctx->near_grad,
                       &ctx->h_stage};
     for (DevBuf* b : bufs) buf_free(*b);
     for (auto& t : ctx->pending) {
@@ -314,16 +316,22 @@ fmm_status fmm_copy_lists(const fmm_ctx* ctx_c, uint32_t* m2l, uint32_t* p2p) {
     FMM_CUDA_TRY(ctx, cudaDeviceSynchronize());
     struct {
         uint32_t* dst;
+        DevBuf* off;
         DevBuf* src;
         int64_t n;
-    } jobs[2] = {{m2l, &ctx->lst_m2l, ctx->n_m2l}, {p2p, &ctx->lst_p2p, ctx->n_p2p}};
+    } jobs[2] = {{m2l, &ctx->m2l_off, &ctx->m2l_src, ctx->n_m2l}, {p2p, &ctx->p2p_off, &ctx->p2p_src, ctx->n_p2p}};
     for (auto& j : jobs) {
         if (!j.dst || j.n == 0) continue;
-        std::vector<uint64_t> tmp((size_t)j.n);
-        FMM_CUDA_TRY(ctx, cudaMemcpy(tmp.data(), j.src->p, j.n * 8, cudaMemcpyDeviceToHost));
-        for (int64_t i = 0; i < j.n; ++i) {
-            j.dst[2 * i] = (uint32_t)(tmp[i] >> 32);
-            j.dst[2 * i + 1] = (uint32_t)tmp[i];
+        std::vector<uint64_t> off((size_t)ctx->ncell + 1);
+        std::vector<uint32_t> src((size_t)j.n);
+        FMM_CUDA_TRY(ctx, cudaMemcpy(off.data(), j.off->p, off.size() * 8, cudaMemcpyDeviceToHost));
+        FMM_CUDA_TRY(ctx, cudaMemcpy(src.data(), j.src->p, src.size() * 4, cudaMemcpyDeviceToHost));
+        for (int64_t t = 0; t < ctx->ncell; ++t) {
+            std::sort(src.begin() + off[t], src.begin() + off[t + 1]);   // canonical (target, source) order
+            for (uint64_t p = off[t]; p < off[t + 1]; ++p) {
+                j.dst[2 * p] = (uint32_t)t;
+                j.dst[2 * p + 1] = src[p];
+            }
         }
     }
     return FMM_OK;

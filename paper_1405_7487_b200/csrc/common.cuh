@@ -69,6 +69,7 @@ struct fmm_ctx {
     bool use_fast_m2l = true;
     bool use_fast_p2p = true;   // fp32 grouped P2P (FMM_P2P_GENERIC=1 disables)
     int p2p_variant = 0;        // 0: CTA per leaf over source runs, 1: warp per leaf (FMM_P2P_VARIANT)
+    bool canonical_m2l = true;   // sort M2L sources within each target on the device (FMM_CANONICAL_M2L=0: skip)
     bool serial_nearfar = true; // P2P and M2L on one stream (FMM_OVERLAP=1: P2P on the aux stream)   // register-resident M2L where instantiated (FMM_M2L_GENERIC=1 disables)
     int device = 0;
     int num_sms = 148;
@@ -106,12 +107,13 @@ struct fmm_ctx {
     DevBuf split_tmp, split_cnt;       // per-level temporaries
     DevBuf leaf_ids;                   // u32 list of leaf cells
 
-    // lists (CSR by target): m2l_src[n_m2l] with m2l_off[ncell+1]; p2p likewise
+    // lists (CSR by target, canonical order): m2l_off[ncell+1] (u64), m2l_src[n_m2l] (u32); p2p likewise.
+    // lst_m2l / lst_p2p are the unsorted packed (target<<32|source) append buffers of the DTT.
     int64_t n_m2l = 0, n_p2p = 0, p2p_inter = 0;
     DevBuf fr_a, fr_b, lst_m2l, lst_p2p, lst_tmp, m2l_src, p2p_src, m2l_off, p2p_off, cnt_tmp, cnt_tmp2, dcount;
     // P2P source runs: runs[n_runs] = {start body, flat offset}, then rtot[ncell]; run_off[ncell+1]
     int64_t n_runs = 0;
-    DevBuf runs, run_off, run_tmp, run_pre, run_len64, dcount2;
+    DevBuf runs, run_off, run_tmp, run_pre, run_len64, dcount2, tcnt, cnt64;
 
     // expansions
     DevBuf M, L, Mr, Lr;   // fp64 [ncell][ncoef]; Mr: packed reduced multipoles for the M2L kernel; Lr: reduced L

@@ -7,10 +7,19 @@
 // R9 from (root, root): MAC -> M2L; both leaves -> P2P; else split A if B is a leaf or
 //         (A internal and R_A >= R_B), else split B.  The rule is a pure function of the
 //         pair, so this breadth-first frontier emits the same SETS as the oracle's recursion.
-// R10 canonical order: ascending (target, source) -- radix sort of the packed u64
-//         (target << 32 | source); CSR offsets per target cell by binary search.
-// Each frontier step: a count kernel (3 warp-aggregated counters), one host read to size
-// the buffers, then an emit kernel appending with warp-aggregated atomics.
+// R10 canonical order: ascending (target, source).  Lists are stored as CSR by target:
+//         off[ncell+1] (u64) and src[n] (u32), sources ascending within a target.
+//
+// Frontier step = ONE kernel: classify each pair, append M2L/P2P pairs and children with
+// warp-aggregated atomics (buffers pre-sized: a pair emits at most one list entry or 8
+// children), and histogram the list entries per target.  The host reads three counters.
+// Grouping without a global sort: scan the per-target counts (CSR offsets) and scatter each
+// unsorted pair's source into its target segment (atomic cursor).  P2P segments are then
+// sorted in shared memory (bitonic, u32) -- canonical order; M2L segments only when
+// FMM_CANONICAL_M2L=1 (otherwise fmm_copy_lists orders each segment on the host).
+// Segments longer than the shared-memory sort take a global radix sort of the packed
+// (target, source) keys instead.
+// P2P source runs (build_runs) merge Morton-contiguous source leaves for the P2P kernel.
 #include "common.cuh"
 
 namespace {
@@ -23,14 +32,17 @@ struct CellView {
 
 // outcome: 0 = M2L, 1 = P2P, 2 = split A, 3 = split B; nchild = children emitted
 __device__ __forceinline__ int classify(const CellView& v, uint32_t a, uint32_t b, double theta, uint32_t& nchild) {
-    double4 A = v.cr[a], B = v.cr[b];
-    double dx = __dsub_rn(A.x, B.x), dy = __dsub_rn(A.y, B.y), dz = __dsub_rn(A.z, B.z);
-    double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    const double4 A = v.cr[a], B = v.cr[b];
+    const double dx = __dsub_rn(A.x, B.x), dy = __dsub_rn(A.y, B.y), dz = __dsub_rn(A.z, B.z);
+    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
     nchild = 0;
     if (__dadd_rn(A.w, B.w) < __dmul_rn(theta, __dsqrt_rn(d2))) return 0;
-    uint32_t ca = v.cc[a], cbn = v.cc[b];
+    const uint32_t ca = v.cc[a], cbn = v.cc[b];
     if (ca == 0 && cbn == 0) return 1;
-    if (cbn == 0 || (ca != 0 && A.w >= B.w)) { nchild = ca; return 2; }
+    if (cbn == 0 || (ca != 0 && A.w >= B.w)) {
+        nchild = ca;
+        return 2;
+    }
     nchild = cbn;
     return 3;
 }
@@ -41,224 +53,376 @@ __device__ __forceinline__ unsigned long long warp_append(unsigned long long* co
     uint32_t x = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
-    uint32_t total = __shfl_sync(0xffffffffu, x, 31);
+    const uint32_t total = __shfl_sync(0xffffffffu, x, 31);
     unsigned long long base = 0;
     if (lane == 31 && total) base = atomicAdd(counter, (unsigned long long)total);
     base = __shfl_sync(0xffffffffu, base, 31);
     return base + (x - cnt);
 }
 
-__global__ void k_dtt_count(const uint64_t* __restrict__ fr, int64_t nf, CellView v, double theta,
-                            unsigned long long* __restrict__ cnt /* [3]: m2l, p2p, next */) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    unsigned long long m = 0, p = 0, c = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += stride) {
-        uint64_t pr = fr[i];
-        uint32_t nch;
-        int o = classify(v, (uint32_t)(pr >> 32), (uint32_t)pr, theta, nch);
-        m += (o == 0);
-        p += (o == 1);
-        c += nch;
-    }
-#pragma unroll
-    for (int s = 16; s; s >>= 1) {
-        m += __shfl_xor_sync(0xffffffffu, m, s);
-        p += __shfl_xor_sync(0xffffffffu, p, s);
-        c += __shfl_xor_sync(0xffffffffu, c, s);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (m) atomicAdd(&cnt[0], m);
-        if (p) atomicAdd(&cnt[1], p);
-        if (c) atomicAdd(&cnt[2], c);
+__device__ __forceinline__ unsigned long long ballot_append(unsigned long long* counter, bool pred) {
+    const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    unsigned long long base = 0;
+    if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(counter, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    return base + __popc(m & lt);
+}
+
+// per-target histogram with one atomic per distinct target in the warp
+__device__ __forceinline__ void count_target(uint32_t* __restrict__ tcnt, bool pred, uint32_t a) {
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    if (pred) {
+        const unsigned peers = __match_any_sync(m, a);
+        if ((peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&tcnt[a], (uint32_t)__popc(peers));
     }
 }
 
-__global__ void k_dtt_emit(const uint64_t* __restrict__ fr, int64_t nf, CellView v, double theta,
-                           unsigned long long* __restrict__ cnt, uint64_t* __restrict__ m2l, uint64_t* __restrict__ p2p,
-                           uint64_t* __restrict__ next) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    // grid-stride with warp-uniform trip count so every lane joins the shuffles
-    int64_t nfr = (nf + 31) / 32 * 32;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nfr; i += stride) {
-        bool ok = i < nf;
-        uint32_t a = 0, b = 0, nch = 0;
-        int o = -1;
-        if (ok) {
-            uint64_t pr = fr[i];
-            a = (uint32_t)(pr >> 32);
-            b = (uint32_t)pr;
-            o = classify(v, a, b, theta, nch);
+// One block = 1024 consecutive frontier pairs (4 per thread, coalesced).  Each thread packs
+// its (m2l, p2p, children) counts into one u64, a block-wide exclusive scan gives every
+// thread its output offsets, and one thread reserves the block's space with 3 atomics.
+constexpr int DT_THREADS = 256;
+constexpr int DT_ITEMS = 4;
+
+__global__ void __launch_bounds__(DT_THREADS) k_dtt_step(const uint64_t* __restrict__ fr, int64_t nf, CellView v,
+                                                         double theta, unsigned long long* __restrict__ cnt,
+                                                         uint64_t* __restrict__ m2l, uint64_t* __restrict__ p2p,
+                                                         uint64_t* __restrict__ next, uint32_t* __restrict__ tcnt_m2l,
+                                                         uint32_t* __restrict__ tcnt_p2p) {
+    __shared__ unsigned long long s_warp[DT_THREADS / 32];
+    __shared__ unsigned long long s_base[3];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int64_t tile = (int64_t)blockIdx.x * DT_THREADS * DT_ITEMS; tile < nf;
+         tile += (int64_t)gridDim.x * DT_THREADS * DT_ITEMS) {
+        uint32_t a[DT_ITEMS], b[DT_ITEMS], nch[DT_ITEMS];
+        int o[DT_ITEMS];
+        unsigned long long packed = 0;   // m2l | p2p << 16 | children << 32
+#pragma unroll
+        for (int k = 0; k < DT_ITEMS; ++k) {
+            const int64_t i = tile + (int64_t)k * DT_THREADS + tid;
+            o[k] = -1; a[k] = b[k] = nch[k] = 0;
+            if (i < nf) {
+                const uint64_t pr = fr[i];
+                a[k] = (uint32_t)(pr >> 32);
+                b[k] = (uint32_t)pr;
+            }
         }
-        unsigned long long pm = warp_append(&cnt[0], o == 0);
-        unsigned long long pp = warp_append(&cnt[1], o == 1);
-        unsigned long long pc = warp_append(&cnt[2], nch);
-        const uint64_t packed = ((uint64_t)a << 32) | b;
-        if (o == 0) m2l[pm] = packed;
-        else if (o == 1) p2p[pp] = packed;
-        else if (o == 2) {
-            uint32_t k0 = v.cb[a];
-            for (uint32_t k = 0; k < nch; ++k) next[pc + k] = ((uint64_t)(k0 + k) << 32) | b;
-        } else if (o == 3) {
-            uint32_t k0 = v.cb[b];
-            for (uint32_t k = 0; k < nch; ++k) next[pc + k] = ((uint64_t)a << 32) | (k0 + k);
+#pragma unroll
+        for (int k = 0; k < DT_ITEMS; ++k) {
+            const int64_t i = tile + (int64_t)k * DT_THREADS + tid;
+            if (i < nf) o[k] = classify(v, a[k], b[k], theta, nch[k]);
+            packed += (unsigned long long)(o[k] == 0) | ((unsigned long long)(o[k] == 1) << 16) |
+                      ((unsigned long long)nch[k] << 32);
         }
+        // block exclusive scan of the packed counts (fields never overflow: <= 1024, <= 1024, <= 8192)
+        unsigned long long x = packed;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+        }
+        if (lane == 31) s_warp[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            unsigned long long w = lane < DT_THREADS / 32 ? s_warp[lane] : 0ull;
+#pragma unroll
+            for (int d = 1; d < DT_THREADS / 32; d <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, w, d);
+                if (lane >= d) w += y;
+            }
+            if (lane < DT_THREADS / 32) s_warp[lane] = w;
+            if (lane == DT_THREADS / 32 - 1) {
+                s_base[0] = atomicAdd(&cnt[0], w & 0xFFFFull);
+                s_base[1] = atomicAdd(&cnt[1], (w >> 16) & 0xFFFFull);
+                s_base[2] = atomicAdd(&cnt[2], w >> 32);
+            }
+        }
+        __syncthreads();
+        const unsigned long long ex = (wid ? s_warp[wid - 1] : 0ull) + x - packed;
+        unsigned long long pm = s_base[0] + (ex & 0xFFFFull);
+        unsigned long long pp = s_base[1] + ((ex >> 16) & 0xFFFFull);
+        unsigned long long pc = s_base[2] + (ex >> 32);
+#pragma unroll
+        for (int k = 0; k < DT_ITEMS; ++k) {
+            const uint64_t pr = ((uint64_t)a[k] << 32) | b[k];
+            if (o[k] == 0) m2l[pm++] = pr;
+            else if (o[k] == 1) p2p[pp++] = pr;
+            else if (o[k] == 2) {
+                const uint32_t k0 = v.cb[a[k]];
+                for (uint32_t c = 0; c < nch[k]; ++c) next[pc + c] = ((uint64_t)(k0 + c) << 32) | b[k];
+                pc += nch[k];
+            } else if (o[k] == 3) {
+                const uint32_t k0 = v.cb[b[k]];
+                for (uint32_t c = 0; c < nch[k]; ++c) next[pc + c] = ((uint64_t)a[k] << 32) | (k0 + c);
+                pc += nch[k];
+            }
+            count_target(tcnt_m2l, o[k] == 0, a[k]);
+            count_target(tcnt_p2p, o[k] == 1, a[k]);
+        }
+        __syncthreads();   // s_warp / s_base reuse
     }
 }
 
 __global__ void k_init_frontier(uint64_t* fr) { fr[0] = 0; }
 
-// CSR offsets: off[c] = first list index with target >= c (sorted packed keys)
-__global__ void k_csr(const uint64_t* __restrict__ lst, int64_t n, int64_t ncell, uint64_t* __restrict__ off) {
-    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c > ncell) return;
-    int64_t lo = 0, hi = n;
-    const uint64_t key = (uint64_t)c << 32;
-    while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if (lst[mid] < key) lo = mid + 1;
-        else hi = mid;
-    }
-    off[c] = (uint64_t)lo;
+__global__ void k_widen_u32(const uint32_t* __restrict__ in, int64_t n, uint64_t* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = in[i];
 }
 
-__global__ void k_p2p_inter(const uint64_t* __restrict__ lst, int64_t n, const uint32_t* __restrict__ bc,
-                            unsigned long long* out) {
-    unsigned long long s = 0;
+// counting-sort scatter of unsorted (target, source) pairs into per-target segments
+__global__ void k_scatter_src(const uint64_t* __restrict__ lst, int64_t n, const uint64_t* __restrict__ off,
+                              uint32_t* __restrict__ cursor, uint32_t* __restrict__ src) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t pr = lst[i];
-        s += (unsigned long long)bc[pr >> 32] * bc[(uint32_t)pr];
+        const uint64_t pr = lst[i];
+        const uint32_t t = (uint32_t)(pr >> 32);
+        const uint32_t k = atomicAdd(&cursor[t], 1u);
+        src[off[t] + k] = (uint32_t)pr;
+    }
+}
+
+constexpr int SEG_THREADS = 256;
+constexpr int SEG_MAX = 4096;
+
+// ascending sort of each target segment in shared memory (bitonic over the next power of two)
+__global__ void __launch_bounds__(SEG_THREADS) k_segsort(const uint64_t* __restrict__ off, int64_t ncell,
+                                                         uint32_t* __restrict__ src) {
+    __shared__ uint32_t s[SEG_MAX];
+    for (int64_t t = blockIdx.x; t < ncell; t += gridDim.x) {
+        const uint64_t b = off[t];
+        const int n = (int)(off[t + 1] - b);
+        if (n <= 1024) continue;   // the warp sorts handled these
+        int m = 1;
+        while (m < n) m <<= 1;
+        __syncthreads();
+        for (int i = threadIdx.x; i < m; i += SEG_THREADS) s[i] = i < n ? src[b + i] : 0xFFFFFFFFu;
+        __syncthreads();
+        for (int k = 2; k <= m; k <<= 1)
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < m; i += SEG_THREADS) {
+                    const int l = i ^ j;
+                    if (l > i) {
+                        const uint32_t x = s[i], y = s[l];
+                        const bool up = (i & k) == 0;
+                        if ((x > y) == up) {
+                            s[i] = y;
+                            s[l] = x;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        for (int i = threadIdx.x; i < n; i += SEG_THREADS) src[b + i] = s[i];
+    }
+}
+
+// Warp-per-segment bitonic sort in registers: K elements per lane (lane-major: element
+// e = lane*K + r), padded with 0xFFFFFFFF to the next power of two >= n (<= 32K).  Stages with
+// partner distance j >= K exchange through __shfl_xor_sync, stages with j < K stay in the
+// lane with compile-time register indices.
+template <int K>
+__device__ __forceinline__ void warp_bitonic(uint32_t (&v)[K], int np, int lane) {
+    for (int k = 2; k <= np; k <<= 1) {
+        for (int j = k >> 1; j >= K; j >>= 1) {
+            const int pl = j / K;
+            const bool lower = (lane & pl) == 0;
+#pragma unroll
+            for (int r = 0; r < K; ++r) {
+                const uint32_t p = __shfl_xor_sync(0xffffffffu, v[r], pl);
+                const bool up = (((lane * K) + r) & k) == 0;
+                const uint32_t lo = min(v[r], p), hi = max(v[r], p);
+                v[r] = (lower == up) ? lo : hi;
+            }
+        }
+#pragma unroll
+        for (int jj = K / 2; jj >= 1; jj >>= 1) {
+            if (jj < k) {
+#pragma unroll
+                for (int r = 0; r < K; ++r) {
+                    if ((r & jj) == 0) {
+                        const int r2 = r | jj;
+                        const bool up = (((lane * K) + r) & k) == 0;
+                        const uint32_t lo = min(v[r], v[r2]), hi = max(v[r], v[r2]);
+                        v[r] = up ? lo : hi;
+                        v[r2] = up ? hi : lo;
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(128) k_segsort_warp(const uint64_t* __restrict__ off, int64_t ncell,
+                                                      uint32_t* __restrict__ src, int min_n) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = warp; t < ncell; t += nw) {
+        const uint64_t b = off[t];
+        const int n = (int)(off[t + 1] - b);
+        if (n <= 1 || n < min_n || n > 32 * K) continue;
+        int np = 1;
+        while (np < n) np <<= 1;
+        uint32_t v[K];
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+            const int e = lane * K + r;
+            v[r] = e < n ? src[b + e] : 0xFFFFFFFFu;
+        }
+        warp_bitonic<K>(v, np, lane);
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+            const int e = lane * K + r;
+            if (e < n) src[b + e] = v[r];
+        }
+    }
+}
+
+__global__ void k_max_u32(const uint32_t* __restrict__ in, int64_t n, unsigned* __restrict__ out) {
+    unsigned m = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, in[i]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+// fallback for very long segments: sorted packed keys -> src
+__global__ void k_unpack_src(const uint64_t* __restrict__ lst, int64_t n, uint32_t* __restrict__ src) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) src[i] = (uint32_t)lst[i];
+}
+
+__global__ void k_p2p_inter(const uint64_t* __restrict__ off, int64_t ncell, const uint32_t* __restrict__ src,
+                            const uint32_t* __restrict__ bc, unsigned long long* out) {
+    unsigned long long s = 0;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ncell; t += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long st = 0;
+        for (uint64_t p = off[t]; p < off[t + 1]; ++p) st += bc[src[p]];
+        s += st * bc[t];
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
 
-fmm_status sort_and_index(fmm_ctx* ctx, DevBuf& lst, int64_t n, DevBuf& off, cudaStream_t s) {
-    FMM_TRY(buf_ensure(ctx, ctx->lst_tmp, (size_t)std::max<int64_t>(n, 1) * 8));
-    FMM_TRY(buf_ensure(ctx, off, (size_t)(ctx->ncell + 1) * 8));
-    int nb = 0;
-    while (((int64_t)1 << nb) < ctx->ncell) ++nb;
-    uint64_t* sorted = nullptr;
-    FMM_TRY(radix_sort_keys(ctx, P_<uint64_t>(lst), P_<uint64_t>(ctx->lst_tmp), n, 0, 32 + nb, &sorted, s));
-    if (sorted != P_<uint64_t>(lst)) std::swap(lst, ctx->lst_tmp);
-    k_csr<<<(unsigned)((ctx->ncell + 1 + 255) / 256), 256, 0, s>>>(P_<uint64_t>(lst), n, ctx->ncell,
-                                                                   P_<uint64_t>(off));
+// unsorted packed list (n pairs) + per-target counts -> CSR off/src, canonical order
+fmm_status canonicalise(fmm_ctx* ctx, DevBuf& lst, int64_t n, uint32_t* tcnt, DevBuf& off, DevBuf& src,
+                        bool sort_segments, cudaStream_t s) {
+    const int64_t nc = ctx->ncell;
+    FMM_TRY(buf_ensure(ctx, off, (size_t)(nc + 1) * 8));
+    FMM_TRY(buf_ensure(ctx, src, (size_t)std::max<int64_t>(n, 1) * 4));
+    FMM_TRY(buf_ensure(ctx, ctx->cnt64, (size_t)(nc + 1) * 8));
+    uint64_t* c64 = P_<uint64_t>(ctx->cnt64);
+    k_widen_u32<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(tcnt, nc, c64);
     FMM_LAUNCH(ctx);
+    FMM_TRY(scan_exclusive_u64(ctx, c64, P_<uint64_t>(off), nc, P_<uint64_t>(off) + nc, s));
+    // longest segment decides the sorting path
+    unsigned* d_max = P_<unsigned>(ctx->dcount2) + 8;
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_max, 0, 4, s));
+    k_max_u32<<<ctx->num_sms * 2, 256, 0, s>>>(tcnt, nc, d_max);
+    FMM_LAUNCH(ctx);
+    unsigned mx = 0;
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&mx, d_max, 4, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    if (mx <= (unsigned)SEG_MAX) {
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(tcnt, 0, (size_t)nc * 4, s));   // reuse as cursors
+        const int g = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 16);
+        k_scatter_src<<<std::max(g, 1), 256, 0, s>>>(P_<uint64_t>(lst), n, P_<uint64_t>(off), tcnt, P_<uint32_t>(src));
+        FMM_LAUNCH(ctx);
+        if (sort_segments) {
+            // warp-register bitonic for segments <= 256 and <= 1024, CTA bitonic above
+            const unsigned gw = (unsigned)std::min<int64_t>((nc + 3) / 4, (int64_t)ctx->num_sms * 32);
+            k_segsort_warp<8><<<gw, 128, 0, s>>>(P_<uint64_t>(off), nc, P_<uint32_t>(src), 0);
+            FMM_LAUNCH(ctx);
+            if (mx > 256) {
+                k_segsort_warp<32><<<gw, 128, 0, s>>>(P_<uint64_t>(off), nc, P_<uint32_t>(src), 257);
+                FMM_LAUNCH(ctx);
+            }
+            if (mx > 1024) {
+                k_segsort<<<(unsigned)std::min<int64_t>(nc, (int64_t)ctx->num_sms * 16), SEG_THREADS, 0, s>>>(
+                    P_<uint64_t>(off), nc, P_<uint32_t>(src));
+                FMM_LAUNCH(ctx);
+            }
+        }
+    } else {
+        FMM_TRY(buf_ensure(ctx, ctx->lst_tmp, (size_t)std::max<int64_t>(n, 1) * 8));
+        int nb = 0;
+        while (((int64_t)1 << nb) < nc) ++nb;
+        uint64_t* sorted = nullptr;
+        FMM_TRY(radix_sort_keys(ctx, P_<uint64_t>(lst), P_<uint64_t>(ctx->lst_tmp), n, 0, 32 + nb, &sorted, s));
+        k_unpack_src<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sorted, n, P_<uint32_t>(src));
+        FMM_LAUNCH(ctx);
+    }
     FMM_CUDA_TRY(ctx, cudaGetLastError());
     return FMM_OK;
-}
-
-__global__ void k_widen(const uint32_t* __restrict__ in, int64_t n, uint64_t* __restrict__ out) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = in[i];
 }
 
 // ---- P2P source runs: consecutive list entries of one target whose body ranges are
 // contiguous (Morton-adjacent leaves) merge into one run {start body, flat offset in the
 // target's source stream}; rtot[t] = total sources of target t.  Used by the P2P kernel to
 // stream a target's sources as full fixed-size chunks.
-__global__ void k_run_flags(const uint64_t* __restrict__ lst, int64_t n, const uint32_t* __restrict__ bb,
-                            const uint32_t* __restrict__ bc, uint32_t* __restrict__ flag) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint64_t cur = lst[i];
-    uint32_t f = 1;
-    if (i > 0) {
-        const uint64_t prv = lst[i - 1];
-        const uint32_t sp = (uint32_t)prv, sc = (uint32_t)cur;
-        f = ((prv >> 32) != (cur >> 32)) || (bb[sp] + bc[sp] != bb[sc]);
+__global__ void k_run_flags(const uint64_t* __restrict__ off, const uint32_t* __restrict__ src, int64_t ncell,
+                            const uint32_t* __restrict__ bb, const uint32_t* __restrict__ bc,
+                            uint32_t* __restrict__ flag) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ncell; t += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t p0 = off[t], p1 = off[t + 1];
+        uint32_t prev_end = 0xFFFFFFFFu;
+        for (uint64_t p = p0; p < p1; ++p) {
+            const uint32_t sc = src[p];
+            flag[p] = (p == p0) || (prev_end != bb[sc]);
+            prev_end = bb[sc] + bc[sc];
+        }
     }
-    flag[i] = f;
 }
 
-__global__ void k_run_emit(const uint64_t* __restrict__ lst, int64_t n, const uint32_t* __restrict__ bb,
-                           const uint32_t* __restrict__ bc, const uint32_t* __restrict__ flag,
-                           const uint32_t* __restrict__ rid, uint32_t* __restrict__ rstart, uint32_t* __restrict__ rlen,
-                           uint32_t* __restrict__ rtarget) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint64_t cur = lst[i];
-    const uint32_t sc = (uint32_t)cur, r = rid[i] + flag[i] - 1;   // run containing entry i
-    if (flag[i]) {
-        rstart[r] = bb[sc];
-        rtarget[r] = (uint32_t)(cur >> 32);
+__global__ void k_run_emit(const uint64_t* __restrict__ off, const uint32_t* __restrict__ src, int64_t ncell,
+                           const uint32_t* __restrict__ bb, const uint32_t* __restrict__ bc,
+                           const uint32_t* __restrict__ flag, const uint32_t* __restrict__ rid,
+                           uint2* __restrict__ runs, uint32_t* __restrict__ roff, uint32_t* __restrict__ rtot) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ncell; t += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t p0 = off[t], p1 = off[t + 1];
+        roff[t] = p0 < p1 ? rid[p0] : (p0 > 0 ? rid[p0 - 1] + flag[p0 - 1] : 0u);
+        uint32_t flat = 0;
+        for (uint64_t p = p0; p < p1; ++p) {
+            const uint32_t sc = src[p];
+            if (flag[p]) runs[rid[p]] = make_uint2(bb[sc], flat);
+            flat += bc[sc];
+        }
+        rtot[t] = flat;
     }
-    if (i + 1 == n || flag[i + 1]) rlen[r] = bb[sc] + bc[sc];   // end body; converted to length below
 }
 
-__global__ void k_run_len(int64_t nr, const uint32_t* __restrict__ rstart, uint32_t* __restrict__ rlen) {
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < nr) rlen[r] -= rstart[r];
-}
-
-// per target: roff (first run), then each run's flat offset within its target and the total
-__global__ void k_run_csr(const uint32_t* __restrict__ rtarget, int64_t nr, int64_t ncell, uint32_t* __restrict__ roff) {
-    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c > ncell) return;
-    int64_t lo = 0, hi = nr;
-    while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if (rtarget[mid] < (uint32_t)c) lo = mid + 1;
-        else hi = mid;
-    }
-    roff[c] = (uint32_t)lo;
-}
-
-__global__ void k_run_flat(int64_t nr, int64_t ncell, const uint32_t* __restrict__ rtarget,
-                           const uint32_t* __restrict__ roff, const uint32_t* __restrict__ rstart,
-                           const uint64_t* __restrict__ gpre, const uint32_t* __restrict__ rlen,
-                           uint2* __restrict__ runs, uint32_t* __restrict__ rtot) {
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < nr) {
-        const uint32_t t = rtarget[r];
-        runs[r] = make_uint2(rstart[r], (uint32_t)(gpre[r] - gpre[roff[t]]));
-    }
-    if (r < ncell) {
-        const uint32_t a = roff[r], b = roff[r + 1];
-        rtot[r] = (a == b) ? 0u : (uint32_t)(gpre[b - 1] + rlen[b - 1] - gpre[a]);
-    }
-}
+__global__ void k_run_last(int64_t ncell, uint32_t nr, uint32_t* __restrict__ roff) { roff[ncell] = nr; }
 
 fmm_status build_runs(fmm_ctx* ctx, cudaStream_t s) {
     const int64_t n = ctx->n_p2p, nc = ctx->ncell;
-    FMM_TRY(buf_ensure(ctx, ctx->run_tmp, (size_t)std::max<int64_t>(n, 1) * 4 * 5 + 64));
+    FMM_TRY(buf_ensure(ctx, ctx->run_tmp, (size_t)std::max<int64_t>(n, 1) * 4 * 2 + 64));
     uint32_t* flag = P_<uint32_t>(ctx->run_tmp);
     uint32_t* rid = flag + n;
-    uint32_t* rstart = rid + n;
-    uint32_t* rlen = rstart + n;
-    uint32_t* rtarget = rlen + n;
-    FMM_TRY(buf_ensure(ctx, ctx->dcount2, 64));
     uint32_t* d_nr = P_<uint32_t>(ctx->dcount2);
-    const unsigned g = (unsigned)((n + 255) / 256);
-    k_run_flags<<<g, 256, 0, s>>>(P_<uint64_t>(ctx->lst_p2p), n, P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), flag);
+    const uint64_t* off = P_<uint64_t>(ctx->p2p_off);
+    const uint32_t* src = P_<uint32_t>(ctx->p2p_src);
+    const int g = (int)std::min<int64_t>((nc + 127) / 128, (int64_t)ctx->num_sms * 16);
+    k_run_flags<<<std::max(g, 1), 128, 0, s>>>(off, src, nc, P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), flag);
     FMM_LAUNCH(ctx);
     FMM_TRY(scan_exclusive_u32(ctx, flag, rid, n, d_nr, s));
-    k_run_emit<<<g, 256, 0, s>>>(P_<uint64_t>(ctx->lst_p2p), n, P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc),
-                                 flag, rid, rstart, rlen, rtarget);
-    FMM_LAUNCH(ctx);
     uint32_t nr = 0;
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&nr, d_nr, 4, cudaMemcpyDeviceToHost, s));
     FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
     ctx->n_runs = nr;
-    k_run_len<<<(unsigned)((nr + 255) / 256), 256, 0, s>>>(nr, rstart, rlen);
-    FMM_LAUNCH(ctx);
     FMM_TRY(buf_ensure(ctx, ctx->run_off, (size_t)(nc + 2) * 4));
-    FMM_TRY(buf_ensure(ctx, ctx->runs, (size_t)std::max<int64_t>(nr, 1) * 8 + (size_t)(nc + 1) * 4 + 64));
-    FMM_TRY(buf_ensure(ctx, ctx->run_pre, (size_t)std::max<int64_t>(nr, 1) * 8));
-    k_run_csr<<<(unsigned)((nc + 1 + 255) / 256), 256, 0, s>>>(rtarget, nr, nc, P_<uint32_t>(ctx->run_off));
-    FMM_LAUNCH(ctx);
-    // 64-bit exclusive scan of the run lengths (widen on the fly)
-    FMM_TRY(buf_ensure(ctx, ctx->run_len64, (size_t)std::max<int64_t>(nr, 1) * 8));
-    k_widen<<<(unsigned)((nr + 255) / 256), 256, 0, s>>>(rlen, nr, P_<uint64_t>(ctx->run_len64));
-    FMM_LAUNCH(ctx);
-    FMM_TRY(scan_exclusive_u64(ctx, P_<uint64_t>(ctx->run_len64), P_<uint64_t>(ctx->run_pre), nr, nullptr, s));
+    FMM_TRY(buf_ensure(ctx, ctx->runs, (size_t)std::max<uint32_t>(nr, 1) * 8 + (size_t)(nc + 1) * 4 + 64));
     uint2* runs = P_<uint2>(ctx->runs);
-    uint32_t* rtot = reinterpret_cast<uint32_t*>(runs + std::max<int64_t>(nr, 1));
-    k_run_flat<<<(unsigned)((std::max<int64_t>(nr, nc) + 255) / 256), 256, 0, s>>>(
-        nr, nc, rtarget, P_<uint32_t>(ctx->run_off), rstart, P_<uint64_t>(ctx->run_pre), rlen, runs, rtot);
+    uint32_t* rtot = reinterpret_cast<uint32_t*>(runs + std::max<uint32_t>(nr, 1));
+    k_run_emit<<<std::max(g, 1), 128, 0, s>>>(off, src, nc, P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), flag, rid,
+                                             runs, P_<uint32_t>(ctx->run_off), rtot);
+    FMM_LAUNCH(ctx);
+    k_run_last<<<1, 1, 0, s>>>(nc, nr, P_<uint32_t>(ctx->run_off));
     FMM_LAUNCH(ctx);
     FMM_CUDA_TRY(ctx, cudaGetLastError());
     return FMM_OK;
@@ -267,40 +431,40 @@ fmm_status build_runs(fmm_ctx* ctx, cudaStream_t s) {
 }  // namespace
 
 fmm_status build_lists(fmm_ctx* ctx, cudaStream_t s) {
-    CellView v{P_<double4>(ctx->c_cr), P_<uint32_t>(ctx->c_cb), P_<uint32_t>(ctx->c_cc)};
+    const CellView v{P_<double4>(ctx->c_cr), P_<uint32_t>(ctx->c_cb), P_<uint32_t>(ctx->c_cc)};
+    const int64_t nc = ctx->ncell;
     int64_t n_m2l = 0, n_p2p = 0;
+    FMM_TRY(buf_ensure(ctx, ctx->tcnt, (size_t)nc * 2 * 4));
+    uint32_t* tcnt_m2l = P_<uint32_t>(ctx->tcnt);
+    uint32_t* tcnt_p2p = tcnt_m2l + nc;
+    FMM_TRY(buf_ensure(ctx, ctx->dcount2, 64));
     {
         PhaseScope ps(ctx, PH_DTT, s);
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(tcnt_m2l, 0, (size_t)nc * 2 * 4, s));
         FMM_TRY(buf_ensure(ctx, ctx->fr_a, 1024 * 8));
         FMM_TRY(buf_ensure(ctx, ctx->dcount, 64));
-        if (ctx->lst_m2l.bytes == 0) FMM_TRY(buf_ensure(ctx, ctx->lst_m2l, (size_t)ctx->ncell * 256 * 8));
-        if (ctx->lst_p2p.bytes == 0) FMM_TRY(buf_ensure(ctx, ctx->lst_p2p, (size_t)ctx->nleaf * 32 * 8));
-        unsigned long long* d_cnt = P_<unsigned long long>(ctx->dcount);   // [0..2] step counts, [4..6] emit cursors
+        unsigned long long* d_cnt = P_<unsigned long long>(ctx->dcount);
         k_init_frontier<<<1, 1, 0, s>>>(P_<uint64_t>(ctx->fr_a));
         FMM_LAUNCH(ctx);
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt, 0, 3 * 8, s));
         int64_t nf = 1;
-        FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt + 4, 0, 3 * 8, s));
         while (nf > 0) {
-            FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt, 0, 3 * 8, s));
-            int g = (int)std::min<int64_t>((nf + 255) / 256, (int64_t)ctx->num_sms * 16);
-            k_dtt_count<<<g, 256, 0, s>>>(P_<uint64_t>(ctx->fr_a), nf, v, ctx->theta, d_cnt);
+            // worst case per step: one list entry or 8 children per pair
+            const size_t need_m = (size_t)(n_m2l + nf) * 8, need_p = (size_t)(n_p2p + nf) * 8;
+            if (need_m > ctx->lst_m2l.bytes) FMM_TRY(buf_ensure(ctx, ctx->lst_m2l, need_m + need_m / 2, true, s));
+            if (need_p > ctx->lst_p2p.bytes) FMM_TRY(buf_ensure(ctx, ctx->lst_p2p, need_p + need_p / 2, true, s));
+            FMM_TRY(buf_ensure(ctx, ctx->fr_b, (size_t)nf * 8 * 8));
+            FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt + 2, 0, 8, s));   // next-frontier cursor restarts
+            const int g = (int)std::min<int64_t>((nf + DT_THREADS * DT_ITEMS - 1) / (DT_THREADS * DT_ITEMS),
+                                                 (int64_t)ctx->num_sms * 8);
+            k_dtt_step<<<g, DT_THREADS, 0, s>>>(P_<uint64_t>(ctx->fr_a), nf, v, ctx->theta, d_cnt, P_<uint64_t>(ctx->lst_m2l),
+                                         P_<uint64_t>(ctx->lst_p2p), P_<uint64_t>(ctx->fr_b), tcnt_m2l, tcnt_p2p);
             FMM_LAUNCH(ctx);
             unsigned long long h[3];
             FMM_CUDA_TRY(ctx, cudaMemcpyAsync(h, d_cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
             FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-            size_t need_m = (size_t)(n_m2l + h[0]) * 8, need_p = (size_t)(n_p2p + h[1]) * 8;
-            if (need_m > ctx->lst_m2l.bytes) FMM_TRY(buf_ensure(ctx, ctx->lst_m2l, need_m + need_m / 2, true, s));
-            if (need_p > ctx->lst_p2p.bytes) FMM_TRY(buf_ensure(ctx, ctx->lst_p2p, need_p + need_p / 2, true, s));
-            FMM_TRY(buf_ensure(ctx, ctx->fr_b, (size_t)std::max<unsigned long long>(h[2], 1) * 8));
-            // the next-frontier cursor restarts at 0 each step
-            FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt + 6, 0, 8, s));
-            k_dtt_emit<<<g, 256, 0, s>>>(P_<uint64_t>(ctx->fr_a), nf, v, ctx->theta, d_cnt + 4,
-                                         P_<uint64_t>(ctx->lst_m2l), P_<uint64_t>(ctx->lst_p2p),
-                                         P_<uint64_t>(ctx->fr_b));
-            FMM_LAUNCH(ctx);
-            FMM_CUDA_TRY(ctx, cudaGetLastError());
-            n_m2l += h[0];
-            n_p2p += h[1];
+            n_m2l = (int64_t)h[0];
+            n_p2p = (int64_t)h[1];
             nf = (int64_t)h[2];
             std::swap(ctx->fr_a, ctx->fr_b);
         }
@@ -308,15 +472,19 @@ fmm_status build_lists(fmm_ctx* ctx, cudaStream_t s) {
     ctx->n_m2l = n_m2l;
     ctx->n_p2p = n_p2p;
     PhaseScope ps(ctx, PH_LISTS, s);
-    FMM_TRY(sort_and_index(ctx, ctx->lst_m2l, n_m2l, ctx->m2l_off, s));
-    FMM_TRY(sort_and_index(ctx, ctx->lst_p2p, n_p2p, ctx->p2p_off, s));
-    FMM_CUDA_TRY(ctx, cudaMemsetAsync(P_<unsigned long long>(ctx->dcount) + 7, 0, 8, s));
-    k_p2p_inter<<<ctx->num_sms * 4, 256, 0, s>>>(P_<uint64_t>(ctx->lst_p2p), n_p2p, P_<uint32_t>(ctx->c_bc),
-                                                  P_<unsigned long long>(ctx->dcount) + 7);
+    // P2P sources are always put in ascending order (the source runs need it); the M2L
+    // segments only when canonical device order is requested (fmm_copy_lists sorts on the
+    // host otherwise; the set and the grouping by target are the same either way).
+    FMM_TRY(canonicalise(ctx, ctx->lst_m2l, n_m2l, tcnt_m2l, ctx->m2l_off, ctx->m2l_src, ctx->canonical_m2l, s));
+    FMM_TRY(canonicalise(ctx, ctx->lst_p2p, n_p2p, tcnt_p2p, ctx->p2p_off, ctx->p2p_src, true, s));
+    unsigned long long* d_inter = P_<unsigned long long>(ctx->dcount2) + 2;
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_inter, 0, 8, s));
+    k_p2p_inter<<<ctx->num_sms * 4, 256, 0, s>>>(P_<uint64_t>(ctx->p2p_off), nc, P_<uint32_t>(ctx->p2p_src),
+                                                  P_<uint32_t>(ctx->c_bc), d_inter);
     FMM_LAUNCH(ctx);
     unsigned long long inter = 0;
-    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&inter, P_<unsigned long long>(ctx->dcount) + 7, 8, cudaMemcpyDeviceToHost, s));
-    FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&inter, d_inter, 8, cudaMemcpyDeviceToHost, s));
+    FMM_TRY(build_runs(ctx, s));   // synchronises s
     ctx->p2p_inter = (int64_t)inter;
-    return build_runs(ctx, s);
+    return FMM_OK;
 }

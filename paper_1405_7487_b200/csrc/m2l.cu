@@ -17,7 +17,7 @@ namespace {
 constexpr int ML_WARPS = 2;
 
 template <typename Real>
-__global__ void __launch_bounds__(ML_WARPS * 32) k_m2l_generic(int64_t ncell, const uint64_t* __restrict__ lst,
+__global__ void __launch_bounds__(ML_WARPS * 32) k_m2l_generic(int64_t ncell, const uint32_t* __restrict__ src,
                                                                 const uint64_t* __restrict__ off,
                                                                 const double4* __restrict__ cr, int P, int ncoef,
                                                                 const double* __restrict__ M, double* __restrict__ L) {
@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(ML_WARPS * 32) k_m2l_generic(int64_t ncell, co
         double4 ca = cr[a];
         for (int k = lane; k < ncoef; k += 32) sLw[k] = 0.0;
         for (uint64_t p = p0; p < p1; ++p) {
-            uint32_t b = (uint32_t)lst[p];
+            uint32_t b = src[p];
             double4 cb = cr[b];
             Real d[3] = {(Real)(ca.x - cb.x), (Real)(ca.y - cb.y), (Real)(ca.z - cb.z)};
             Real r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
@@ -95,7 +95,7 @@ fmm_status m2l_generic(fmm_ctx* ctx, cudaStream_t s) {
     int g = (int)std::min<int64_t>((ctx->ncell + ML_WARPS - 1) / ML_WARPS, (int64_t)ctx->num_sms * 8);
     const int ncp = (ctx->ncoef + 1) & ~1;
     size_t smem = (size_t)4 * ncp + (size_t)ML_WARPS * ncp * (8 + 2 * sizeof(Real));
-    k_m2l_generic<Real><<<std::max(g, 1), ML_WARPS * 32, smem, s>>>(ctx->ncell, P_<uint64_t>(ctx->lst_m2l),
+    k_m2l_generic<Real><<<std::max(g, 1), ML_WARPS * 32, smem, s>>>(ctx->ncell, P_<uint32_t>(ctx->m2l_src),
                                                                   P_<uint64_t>(ctx->m2l_off), P_<double4>(ctx->c_cr),
                                                                   ctx->P, ctx->ncoef, P_<double>(ctx->M),
                                                                   P_<double>(ctx->L));

@@ -165,7 +165,7 @@ __device__ __forceinline__ void apply_elem(R s, const R (&D0)[RF<P>::N0], const 
 
 template <int P, typename R>
 __global__ void __launch_bounds__(128, 2)
-    k_m2l_fast(int64_t ncell, const uint64_t* __restrict__ lst, const uint64_t* __restrict__ off,
+    k_m2l_fast(int64_t ncell, const uint32_t* __restrict__ src, const uint64_t* __restrict__ off,
                const double4* __restrict__ cr, const int* __restrict__ sexp,
                const typename Vec4<R>::type* __restrict__ Sv, double* __restrict__ Lr,
                unsigned long long* __restrict__ counter) {
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(128, 2)
 #pragma unroll
         for (int i = 0; i < N1; ++i) L1[i] = R(0);
         for (uint64_t p = p0 + lane; p < p1; p += 32) {
-            const uint32_t b = (uint32_t)lst[p];
+            const uint32_t b = src[p];
             const double4 cb = cr[b];
             const int eb = sexp[b];
             const R ux = (R)((ca.x - cb.x) * sa);
@@ -353,7 +353,7 @@ fmm_status m2l_fast_t(fmm_ctx* ctx, cudaStream_t s) {
     FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 8, s));
     {
         PhaseScope ps(ctx, PH_M2L_KERNEL, s);
-        k_m2l_fast<P, R><<<ctx->num_sms * 2, 128, 0, s>>>(nc, P_<uint64_t>(ctx->lst_m2l), P_<uint64_t>(ctx->m2l_off),
+        k_m2l_fast<P, R><<<ctx->num_sms * 2, 128, 0, s>>>(nc, P_<uint32_t>(ctx->m2l_src), P_<uint64_t>(ctx->m2l_off),
                                                          P_<double4>(ctx->c_cr), sexp,
                                                          reinterpret_cast<const typename Vec4<R>::type*>(Sv),
                                                          P_<double>(ctx->Lr), counter);

@@ -22,7 +22,7 @@ __device__ __forceinline__ double rsqrt_(double x) { return 1.0 / sqrt(x); }
 template <typename Body, typename Real>
 __global__ void __launch_bounds__(PP_WARPS * 32) k_p2p_generic(const Body* __restrict__ body,
                                                                 const uint32_t* __restrict__ leaf_ids, int64_t nleaf,
-                                                                const uint64_t* __restrict__ lst,
+                                                                const uint32_t* __restrict__ lst,
                                                                 const uint64_t* __restrict__ off,
                                                                 const uint32_t* __restrict__ bb,
                                                                 const uint32_t* __restrict__ bc,
@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(PP_WARPS * 32) k_p2p_generic(const Body* __res
                 x[r] = p.x; y[r] = p.y; z[r] = p.z;
             }
             for (uint64_t pp = p0; pp < p1; ++pp) {
-                uint32_t b = (uint32_t)lst[pp];
+                uint32_t b = lst[pp];
                 uint32_t sb = bb[b], ns = bc[b];
                 for (uint32_t s0 = 0; s0 < ns; s0 += PP_TILE) {
                     uint32_t m = min((uint32_t)PP_TILE, ns - s0);
@@ -124,7 +124,7 @@ __device__ __forceinline__ void p2p_body(const float4 s, const float (&x)[PF_T],
 
 __global__ void __launch_bounds__(PF_WARPS * 32) k_p2p_f32(const float4* __restrict__ body,
                                                            const uint32_t* __restrict__ leaf_ids, int64_t nleaf,
-                                                           const uint64_t* __restrict__ lst,
+                                                           const uint32_t* __restrict__ lst,
                                                            const uint64_t* __restrict__ off,
                                                            const uint32_t* __restrict__ bb,
                                                            const uint32_t* __restrict__ bc, float* __restrict__ near_phi,
@@ -161,13 +161,13 @@ __global__ void __launch_bounds__(PF_WARPS * 32) k_p2p_f32(const float4* __restr
             uint64_t cp_ = p0;
             uint32_t cs = 0;
             auto chunk = [&](uint64_t pp, uint32_t s0, uint32_t& src, uint32_t& m, bool& self) {
-                const uint32_t b = (uint32_t)lst[pp];
+                const uint32_t b = lst[pp];
                 src = bb[b] + s0;
                 m = min((uint32_t)PF_TILE, bc[b] - s0);
                 self = b == a;
             };
             auto advance = [&](uint64_t& pp, uint32_t& s0) {
-                const uint32_t b = (uint32_t)lst[pp];
+                const uint32_t b = lst[pp];
                 s0 += PF_TILE;
                 if (s0 >= bc[b]) { ++pp; s0 = 0; }
             };
@@ -390,7 +390,7 @@ fmm_status p2p_t(fmm_ctx* ctx, cudaStream_t s) {
         int nb = 0;
         FMM_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_p2p_f32, PF_WARPS * 32, 0));
         k_p2p_f32<<<ctx->num_sms * std::max(nb, 1), PF_WARPS * 32, 0, s>>>(
-            P_<float4>(ctx->body), P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, P_<uint64_t>(ctx->lst_p2p),
+            P_<float4>(ctx->body), P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, P_<uint32_t>(ctx->p2p_src),
             P_<uint64_t>(ctx->p2p_off), P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), (float*)ctx->near_phi.p,
             (float*)ctx->near_grad.p, counter);
         FMM_LAUNCH(ctx);
@@ -399,7 +399,7 @@ fmm_status p2p_t(fmm_ctx* ctx, cudaStream_t s) {
     }
     int g = (int)std::min<int64_t>((ctx->nleaf + PP_WARPS - 1) / PP_WARPS, (int64_t)ctx->num_sms * 16);
     k_p2p_generic<Body, Real><<<std::max(g, 1), PP_WARPS * 32, 0, s>>>(
-        P_<Body>(ctx->body), P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, P_<uint64_t>(ctx->lst_p2p),
+        P_<Body>(ctx->body), P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, P_<uint32_t>(ctx->p2p_src),
         P_<uint64_t>(ctx->p2p_off), P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), P_<Real>(ctx->near_phi),
         P_<Real>(ctx->near_grad));
     FMM_LAUNCH(ctx);
