@@ -141,7 +141,7 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
                       &ctx->split_tmp, &ctx->split_cnt, &ctx->leaf_ids, &ctx->fr_a, &ctx->fr_b, &ctx->lst_m2l,
                       &ctx->lst_p2p, &ctx->lst_tmp, &ctx->m2l_src, &ctx->p2p_src, &ctx->m2l_off, &ctx->p2p_off,
                       &ctx->cnt_tmp, &ctx->cnt_tmp2, &ctx->dcount, &ctx->runs, &ctx->run_off, &ctx->run_tmp, &ctx->run_pre,
-                      &ctx->run_len64, &ctx->dcount2, &ctx->tcnt, &ctx->cnt64, &ctx->M, &ctx->L, &ctx->Mr, &ctx->Lr, &ctx->near_phi, &ctx->near_grad,
+                      &ctx->run_len64, &ctx->dcount2, &ctx->tcnt, &ctx->cnt64, &ctx->big_off, &ctx->M, &ctx->L, &ctx->Mr, &ctx->Lr, &ctx->near_phi, &ctx->near_grad,
                       &ctx->h_stage};
     for (DevBuf* b : bufs) buf_free(*b);
     for (auto& t : ctx->pending) {

@@ -10,7 +10,8 @@
 
 namespace {
 constexpr int DN_WARPS = 4;
-constexpr int LP_WARPS = 2;
+constexpr int LP_WARPS = 4;   // P-specialised L2P
+constexpr int LPG_WARPS = 2;  // generic L2P (shared power tables)
 
 __constant__ double c_inv[FMM_MAXP + 1] = {0.0,       1.0,        1.0 / 2,  1.0 / 3,  1.0 / 4,  1.0 / 5,
                                            1.0 / 6,   1.0 / 7,    1.0 / 8,  1.0 / 9,  1.0 / 10, 1.0 / 11,
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_l2l(int64_t cbeg, int64_t cen
 
 // warp per leaf, lanes over bodies; writes the final outputs in the caller's order
 template <typename Body, typename Real>
-__global__ void __launch_bounds__(LP_WARPS * 32) k_l2p(const Body* __restrict__ body, const uint32_t* __restrict__ perm,
+__global__ void __launch_bounds__(LPG_WARPS * 32) k_l2p(const Body* __restrict__ body, const uint32_t* __restrict__ perm,
                                                         const uint32_t* __restrict__ leaf_ids, int64_t nleaf,
                                                         const uint32_t* __restrict__ bb, const uint32_t* __restrict__ bc,
                                                         const double4* __restrict__ cr, int P, int ncoef,
@@ -80,12 +81,12 @@ __global__ void __launch_bounds__(LP_WARPS * 32) k_l2p(const Body* __restrict__ 
                                                         const Real* __restrict__ near_grad, Real* __restrict__ phi,
                                                         Real* __restrict__ grad) {
     __shared__ uchar4 ex[816];
-    __shared__ double s_L[LP_WARPS][816];
-    __shared__ double s_pw[LP_WARPS][3][FMM_MAXP][32];
+    __shared__ double s_L[LPG_WARPS][816];
+    __shared__ double s_pw[LPG_WARPS][3][FMM_MAXP][32];
     fill_ex_table(ex, ncoef);
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int64_t li = (int64_t)blockIdx.x * LP_WARPS + w; li < nleaf; li += (int64_t)gridDim.x * LP_WARPS) {
+    for (int64_t li = (int64_t)blockIdx.x * LPG_WARPS + w; li < nleaf; li += (int64_t)gridDim.x * LPG_WARPS) {
         uint32_t c = leaf_ids[li];
         double4 ctr = cr[c];
         __syncwarp();
@@ -131,6 +132,90 @@ __global__ void __launch_bounds__(LP_WARPS * 32) k_l2p(const Body* __restrict__ 
     }
 }
 
+// P-specialised L2P: one lane per body, z^e/e! per axis in registers, L from a per-warp
+// shared copy (broadcast reads); R16 evaluated as nested sums over (a, b, c) with
+// compile-time indices.  phi uses all |alpha| <= P-1, grad_d uses L_{g+e_d}, |g| <= P-2.
+template <int P>
+struct InvFact {
+    double v[P];
+    __host__ __device__ constexpr InvFact() : v() {
+        double f = 1.0;
+        for (int i = 0; i < P; ++i) {
+            if (i > 0) f *= (double)i;
+            v[i] = 1.0 / f;
+        }
+    }
+};
+
+template <int P, typename Body, typename Real>
+__global__ void __launch_bounds__(LP_WARPS * 32) k_l2p_t(const Body* __restrict__ body, const uint32_t* __restrict__ perm,
+                                                          const uint32_t* __restrict__ leaf_ids, int64_t nleaf,
+                                                          const uint32_t* __restrict__ bb,
+                                                          const uint32_t* __restrict__ bc,
+                                                          const double4* __restrict__ cr, const double* __restrict__ L,
+                                                          const Real* __restrict__ near_phi,
+                                                          const Real* __restrict__ near_grad, Real* __restrict__ phi,
+                                                          Real* __restrict__ grad) {
+    constexpr int NC = P * (P + 1) * (P + 2) / 6;
+    __shared__ double s_L[LP_WARPS][NC];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int64_t li = (int64_t)blockIdx.x * LP_WARPS + w; li < nleaf; li += (int64_t)gridDim.x * LP_WARPS) {
+        const uint32_t c = leaf_ids[li];
+        const double4 ctr = cr[c];
+        __syncwarp();
+        for (int k = lane; k < NC; k += 32) s_L[w][k] = L[(int64_t)c * NC + k];
+        __syncwarp();
+        const double* Ls = s_L[w];
+        const uint32_t b0 = bb[c], nb = bc[c];
+        for (uint32_t j0 = 0; j0 < nb; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            if (j >= nb) continue;
+            const Body p = body[b0 + j];
+            const double z[3] = {(double)p.x - ctr.x, (double)p.y - ctr.y, (double)p.z - ctr.z};
+            constexpr InvFact<P> F{};
+            double pw[3][P];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                double v = 1.0;
+#pragma unroll
+                for (int e = 0; e < P; ++e) {
+                    pw[d][e] = v * F.v[e];
+                    v *= z[d];
+                }
+            }
+            double f = 0.0, g[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+            for (int a = 0; a < P; ++a) {
+                double fa = 0.0, ga[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+                for (int bq = 0; bq < P - a; ++bq) {
+                    double fb = 0.0, gb[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+                    for (int cq = 0; cq < P - a - bq; ++cq) {
+                        fb = fma(Ls[cidx(a, bq, cq)], pw[2][cq], fb);
+                        if (a + bq + cq <= P - 2) {
+                            gb[0] = fma(Ls[cidx(a + 1, bq, cq)], pw[2][cq], gb[0]);
+                            gb[1] = fma(Ls[cidx(a, bq + 1, cq)], pw[2][cq], gb[1]);
+                            gb[2] = fma(Ls[cidx(a, bq, cq + 1)], pw[2][cq], gb[2]);
+                        }
+                    }
+                    fa = fma(fb, pw[1][bq], fa);
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) ga[d] = fma(gb[d], pw[1][bq], ga[d]);
+                }
+                f = fma(fa, pw[0][a], f);
+#pragma unroll
+                for (int d = 0; d < 3; ++d) g[d] = fma(ga[d], pw[0][a], g[d]);
+            }
+            const uint32_t sj = b0 + j;
+            const uint32_t o = perm[sj];
+            phi[o] = (Real)(f + (double)near_phi[sj]);
+#pragma unroll
+            for (int d = 0; d < 3; ++d) grad[3 * (int64_t)o + d] = (Real)(g[d] + (double)near_grad[3 * (int64_t)sj + d]);
+        }
+    }
+}
+
 template <typename Body, typename Real>
 fmm_status downward_t(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s) {
     PhaseScope ps(ctx, PH_DOWN, s);
@@ -145,7 +230,23 @@ fmm_status downward_t(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s) {
         FMM_LAUNCH(ctx);
     }
     int g = (int)std::min<int64_t>((ctx->nleaf + LP_WARPS - 1) / LP_WARPS, (int64_t)ctx->num_sms * 32);
-    k_l2p<Body, Real><<<std::max(g, 1), LP_WARPS * 32, 0, s>>>(
+#define FMM_L2P_T(PP)                                                                                              \
+    if (ctx->P == PP) {                                                                                            \
+        k_l2p_t<PP, Body, Real><<<std::max(g, 1), LP_WARPS * 32, 0, s>>>(                                          \
+            P_<Body>(ctx->body), ctx->d_perm, P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, P_<uint32_t>(ctx->c_bb),    \
+            P_<uint32_t>(ctx->c_bc), P_<double4>(ctx->c_cr), L, P_<Real>(ctx->near_phi), P_<Real>(ctx->near_grad), \
+            (Real*)phi, (Real*)grad);                                                                              \
+        FMM_LAUNCH(ctx);                                                                                           \
+        FMM_CUDA_TRY(ctx, cudaGetLastError());                                                                     \
+        return FMM_OK;                                                                                             \
+    }
+    FMM_L2P_T(4)
+    FMM_L2P_T(6)
+    FMM_L2P_T(8)
+    FMM_L2P_T(10)
+#undef FMM_L2P_T
+    g = (int)std::min<int64_t>((ctx->nleaf + LPG_WARPS - 1) / LPG_WARPS, (int64_t)ctx->num_sms * 32);
+    k_l2p<Body, Real><<<std::max(g, 1), LPG_WARPS * 32, 0, s>>>(
         P_<Body>(ctx->body), ctx->d_perm, P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, P_<uint32_t>(ctx->c_bb),
         P_<uint32_t>(ctx->c_bc), P_<double4>(ctx->c_cr), ctx->P, ctx->ncoef, L, P_<Real>(ctx->near_phi),
         P_<Real>(ctx->near_grad), (Real*)phi, (Real*)grad);

@@ -17,8 +17,8 @@
 // unsorted pair's source into its target segment (atomic cursor).  P2P segments are then
 // sorted in shared memory (bitonic, u32) -- canonical order; M2L segments only when
 // FMM_CANONICAL_M2L=1 (otherwise fmm_copy_lists orders each segment on the host).
-// Segments longer than the shared-memory sort take a global radix sort of the packed
-// (target, source) keys instead.
+// Segments longer than the shared-memory sort are gathered and radix-sorted as packed
+// (target, source) keys.
 // P2P source runs (build_runs) merge Morton-contiguous source leaves for the P2P kernel.
 #include "common.cuh"
 
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(SEG_THREADS) k_segsort(const uint64_t* __restr
     for (int64_t t = blockIdx.x; t < ncell; t += gridDim.x) {
         const uint64_t b = off[t];
         const int n = (int)(off[t + 1] - b);
-        if (n <= 1024) continue;   // the warp sorts handled these
+        if (n <= 2048 || n > SEG_MAX) continue;   // warp sorts / big-segment path handle these
         int m = 1;
         while (m < n) m <<= 1;
         __syncthreads();
@@ -310,6 +310,35 @@ __global__ void k_p2p_inter(const uint64_t* __restrict__ off, int64_t ncell, con
     if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
 
+// segments longer than SEG_MAX: gather them as packed (target, source) keys, radix-sort that
+// (small) array, write the sources back in place
+__global__ void k_big_flags(const uint64_t* __restrict__ off, int64_t ncell, uint64_t* __restrict__ sz) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < ncell) {
+        const uint64_t n = off[t + 1] - off[t];
+        sz[t] = n > (uint64_t)SEG_MAX ? n : 0ull;
+    }
+}
+
+__global__ void k_big_gather(const uint64_t* __restrict__ off, const uint64_t* __restrict__ boff, int64_t ncell,
+                             const uint32_t* __restrict__ src, uint64_t* __restrict__ tmp) {
+    for (int64_t t = blockIdx.x; t < ncell; t += gridDim.x) {
+        const uint64_t n = off[t + 1] - off[t];
+        if (n <= (uint64_t)SEG_MAX) continue;
+        for (uint64_t i = threadIdx.x; i < n; i += blockDim.x)
+            tmp[boff[t] + i] = ((uint64_t)t << 32) | src[off[t] + i];
+    }
+}
+
+__global__ void k_big_scatter(const uint64_t* __restrict__ off, const uint64_t* __restrict__ boff, int64_t ncell,
+                              const uint64_t* __restrict__ tmp, uint32_t* __restrict__ src) {
+    for (int64_t t = blockIdx.x; t < ncell; t += gridDim.x) {
+        const uint64_t n = off[t + 1] - off[t];
+        if (n <= (uint64_t)SEG_MAX) continue;
+        for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) src[off[t] + i] = (uint32_t)tmp[boff[t] + i];
+    }
+}
+
 // unsorted packed list (n pairs) + per-target counts -> CSR off/src, canonical order
 fmm_status canonicalise(fmm_ctx* ctx, DevBuf& lst, int64_t n, uint32_t* tcnt, DevBuf& off, DevBuf& src,
                         bool sort_segments, cudaStream_t s) {
@@ -329,34 +358,52 @@ fmm_status canonicalise(fmm_ctx* ctx, DevBuf& lst, int64_t n, uint32_t* tcnt, De
     unsigned mx = 0;
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&mx, d_max, 4, cudaMemcpyDeviceToHost, s));
     FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-    if (mx <= (unsigned)SEG_MAX) {
-        FMM_CUDA_TRY(ctx, cudaMemsetAsync(tcnt, 0, (size_t)nc * 4, s));   // reuse as cursors
-        const int g = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 16);
-        k_scatter_src<<<std::max(g, 1), 256, 0, s>>>(P_<uint64_t>(lst), n, P_<uint64_t>(off), tcnt, P_<uint32_t>(src));
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(tcnt, 0, (size_t)nc * 4, s));   // reuse as cursors
+    const int g = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 16);
+    k_scatter_src<<<std::max(g, 1), 256, 0, s>>>(P_<uint64_t>(lst), n, P_<uint64_t>(off), tcnt, P_<uint32_t>(src));
+    FMM_LAUNCH(ctx);
+    if (sort_segments) {
+        // warp-register bitonic for segments <= 256 and <= 1024, CTA bitonic <= SEG_MAX
+        const unsigned gw = (unsigned)std::min<int64_t>((nc + 3) / 4, (int64_t)ctx->num_sms * 32);
+        k_segsort_warp<8><<<gw, 128, 0, s>>>(P_<uint64_t>(off), nc, P_<uint32_t>(src), 0);
         FMM_LAUNCH(ctx);
-        if (sort_segments) {
-            // warp-register bitonic for segments <= 256 and <= 1024, CTA bitonic above
-            const unsigned gw = (unsigned)std::min<int64_t>((nc + 3) / 4, (int64_t)ctx->num_sms * 32);
-            k_segsort_warp<8><<<gw, 128, 0, s>>>(P_<uint64_t>(off), nc, P_<uint32_t>(src), 0);
+        if (mx > 256) {
+            k_segsort_warp<32><<<gw, 128, 0, s>>>(P_<uint64_t>(off), nc, P_<uint32_t>(src), 257);
             FMM_LAUNCH(ctx);
-            if (mx > 256) {
-                k_segsort_warp<32><<<gw, 128, 0, s>>>(P_<uint64_t>(off), nc, P_<uint32_t>(src), 257);
-                FMM_LAUNCH(ctx);
-            }
-            if (mx > 1024) {
-                k_segsort<<<(unsigned)std::min<int64_t>(nc, (int64_t)ctx->num_sms * 16), SEG_THREADS, 0, s>>>(
-                    P_<uint64_t>(off), nc, P_<uint32_t>(src));
-                FMM_LAUNCH(ctx);
-            }
         }
-    } else {
-        FMM_TRY(buf_ensure(ctx, ctx->lst_tmp, (size_t)std::max<int64_t>(n, 1) * 8));
-        int nb = 0;
-        while (((int64_t)1 << nb) < nc) ++nb;
-        uint64_t* sorted = nullptr;
-        FMM_TRY(radix_sort_keys(ctx, P_<uint64_t>(lst), P_<uint64_t>(ctx->lst_tmp), n, 0, 32 + nb, &sorted, s));
-        k_unpack_src<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sorted, n, P_<uint32_t>(src));
-        FMM_LAUNCH(ctx);
+        if (mx > 1024) {
+            k_segsort_warp<64><<<gw, 128, 0, s>>>(P_<uint64_t>(off), nc, P_<uint32_t>(src), 1025);
+            FMM_LAUNCH(ctx);
+        }
+        if (mx > 2048) {
+            k_segsort<<<(unsigned)std::min<int64_t>(nc, (int64_t)ctx->num_sms * 16), SEG_THREADS, 0, s>>>(
+                P_<uint64_t>(off), nc, P_<uint32_t>(src));
+            FMM_LAUNCH(ctx);
+        }
+        if (mx > (unsigned)SEG_MAX) {
+            // c64 (count widening buffer, nc+1 entries) is free again: reuse it for the sizes
+            uint64_t* bsz = c64;
+            FMM_TRY(buf_ensure(ctx, ctx->big_off, (size_t)(nc + 1) * 8));
+            uint64_t* boff = P_<uint64_t>(ctx->big_off);
+            k_big_flags<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(P_<uint64_t>(off), nc, bsz);
+            FMM_LAUNCH(ctx);
+            FMM_TRY(scan_exclusive_u64(ctx, bsz, boff, nc, boff + nc, s));
+            uint64_t nbig = 0;
+            FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&nbig, boff + nc, 8, cudaMemcpyDeviceToHost, s));
+            FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+            FMM_TRY(buf_ensure(ctx, ctx->lst_tmp, (size_t)nbig * 16 + 16));
+            uint64_t* t0 = P_<uint64_t>(ctx->lst_tmp);
+            uint64_t* t1 = t0 + nbig;
+            const unsigned gb = (unsigned)std::min<int64_t>(nc, (int64_t)ctx->num_sms * 8);
+            k_big_gather<<<gb, 256, 0, s>>>(P_<uint64_t>(off), boff, nc, P_<uint32_t>(src), t0);
+            FMM_LAUNCH(ctx);
+            int nb = 0;
+            while (((int64_t)1 << nb) < nc) ++nb;
+            uint64_t* sorted = nullptr;
+            FMM_TRY(radix_sort_keys(ctx, t0, t1, (int64_t)nbig, 0, 32 + nb, &sorted, s));
+            k_big_scatter<<<gb, 256, 0, s>>>(P_<uint64_t>(off), boff, nc, sorted, P_<uint32_t>(src));
+            FMM_LAUNCH(ctx);
+        }
     }
     FMM_CUDA_TRY(ctx, cudaGetLastError());
     return FMM_OK;

@@ -233,6 +233,23 @@ __global__ void __launch_bounds__(128, 2)
     }
 }
 
+// harmonic fold in closed form: repeatedly moving S_beta (beta_x >= 2) onto
+// beta - 2e_x + 2e_y and beta - 2e_x + 2e_z with weight -1 gives
+//   S~(b,y,z) = sum_k (-1)^k sum_{j<=k} C(k,j) S(b+2k, y-2j, z-2(k-j))
+__device__ __forceinline__ double fold_pull(const double* S, int b, int y, int z) {
+    double acc = 0.0;
+    for (int k = 0; 2 * k <= y + z; ++k) {
+        double binom = 1.0, part = 0.0;
+        for (int j = 0; j <= k; ++j) {
+            if (j > 0) binom = binom * (double)(k - j + 1) / (double)j;
+            const int yy = y - 2 * j, zz = z - 2 * (k - j);
+            if (yy >= 0 && zz >= 0) part += binom * S[cidx(b + 2 * k, yy, zz)];
+        }
+        acc += (k & 1) ? -part : part;
+    }
+    return acc;
+}
+
 // per source cell: signed M -> harmonic fold onto beta_x in {0,1} -> S0 | S1 | N, scaled by
 // rho^-|beta| and rounded to R.  Also records the cell's scale exponent.
 template <typename R>
@@ -254,17 +271,7 @@ __global__ void k_m2l_prep(int64_t ncell, int P, int ncoef, int NS, int NSP, con
             double m = M[(size_t)c * ncoef + k];
             S[k] = ((a + b + cc) & 1) ? -m : m;
         }
-        __syncwarp();
-        if (lane == 0) {
-            sexp[c] = e;
-            for (int bx = P - 1; bx >= 2; --bx)
-                for (int by = 0; by <= P - 1 - bx; ++by)
-                    for (int bz = 0; bz <= P - 1 - bx - by; ++bz) {
-                        double v = S[cidx(bx, by, bz)];
-                        S[cidx(bx - 2, by + 2, bz)] -= v;
-                        S[cidx(bx - 2, by, bz + 2)] -= v;
-                    }
-        }
+        if (lane == 0) sexp[c] = e;
         __syncwarp();
         R* out = Sv + (size_t)c * NSP;
         for (int i = lane; i < NSP; i += 32) {
@@ -274,21 +281,21 @@ __global__ void k_m2l_prep(int64_t ncell, int P, int ncoef, int NS, int NSP, con
                 int m = 0;
                 while ((m + 1) * (m + 2) / 2 <= i) ++m;
                 int z = i - m * (m + 1) / 2, y = m - z;
-                v = S[cidx(0, y, z)];
+                v = fold_pull(S, 0, y, z);
                 dg = m;
             } else if (i < N0 + N1) {
                 int ii = i - N0, m = 0;
                 while ((m + 1) * (m + 2) / 2 <= ii) ++m;
                 int z = ii - m * (m + 1) / 2, y = m - z;
-                v = S[cidx(1, y, z)];
+                v = fold_pull(S, 1, y, z);
                 dg = m + 1;
             } else if (i < NS) {
                 int ii = i - N0 - N1, m = 0;
                 while ((m + 1) * (m + 2) / 2 <= ii) ++m;
                 int z = ii - m * (m + 1) / 2, y = m - z;
                 if (m >= 2) {
-                    if (y >= 2) v -= S[cidx(1, y - 2, z)];
-                    if (z >= 2) v -= S[cidx(1, y, z - 2)];
+                    if (y >= 2) v -= fold_pull(S, 1, y - 2, z);
+                    if (z >= 2) v -= fold_pull(S, 1, y, z - 2);
                 }
                 dg = m - 1;
             }

@@ -84,6 +84,21 @@ def test_parity_small(torch_cuda, kind, n, P, theta, ncrit, prec):
         assert np.abs(gL - oL).max() <= 1e-11 * max(np.abs(oL).max(), 1e-300)
 
 
+@pytest.mark.parametrize("prec,P", [("f64", 2), ("f32", 4)])
+def test_long_list_segments(torch_cuda, prec, P):
+    # tiny theta and ncrit on a Plummer cloud: M2L segments of ~8.8k sources and a P2P segment
+    # of ~23.7k source leaves exercise the big-segment sort path (> 4096 per target)
+    pos, q = synth.generate("plummer", 30000, 7, np.float32 if prec == "f32" else np.float64)
+    f, phi, grad = run_gpu(torch_cuda, pos, q, P, 0.2, 2, prec)
+    o = oracle.FMM(pos.astype(np.float64), q.astype(np.float64), P, 0.2, 2).traverse()
+    check_structure(f, o)
+    m, p2 = o.lists()
+    assert np.bincount(m[:, 0]).max() > 4096 and np.bincount(p2[:, 0]).max() > 4096
+    t = synth.sample_targets(30000, 300, 7)
+    ophi, ograd = o.evaluate(t)
+    assert oracle.rel_l2(phi[t], ophi) <= TOL[prec] and oracle.rel_l2(grad[t], ograd) <= TOL[prec]
+
+
 def test_duplicates_and_coincident(torch_cuda):
     pos, q = synth.generate("cube", 300, 5)
     pos = np.vstack([pos, pos[:50], np.full((40, 3), 0.125)])
