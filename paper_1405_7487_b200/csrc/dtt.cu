@@ -282,6 +282,83 @@ __global__ void __launch_bounds__(128) k_segsort_warp(const uint64_t* __restrict
     }
 }
 
+// Warp-per-segment stable LSD radix sort in shared memory for 257..2048 keys: RBITS-bit
+// digits; ranking row by row (32 keys) with __match_any_sync and a per-warp running
+// histogram, exclusive scan of the bins, scatter to the other buffer.  ~25 instr/key/pass.
+constexpr int WR_WARPS = 4;
+constexpr int WR_MAX = 2048;
+constexpr int WR_BITS = 10;
+constexpr int WR_BINS = 1 << WR_BITS;
+
+__global__ void __launch_bounds__(WR_WARPS * 32) k_segsort_wradix(const uint64_t* __restrict__ off, int64_t ncell,
+                                                                  uint32_t* __restrict__ src, int nbits, int min_n) {
+    extern __shared__ uint32_t wr_smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t* A = wr_smem + (size_t)w * (2 * WR_MAX + WR_MAX / 2 + WR_BINS);
+    uint32_t* B = A + WR_MAX;
+    uint16_t* pos = reinterpret_cast<uint16_t*>(B + WR_MAX);
+    uint32_t* hist = B + WR_MAX + WR_MAX / 2;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t warp = (int64_t)blockIdx.x * WR_WARPS + w;
+    const int64_t nw = (int64_t)gridDim.x * WR_WARPS;
+    for (int64_t t = warp; t < ncell; t += nw) {
+        const uint64_t b0 = off[t];
+        const int n = (int)(off[t + 1] - b0);
+        if (n < min_n || n > WR_MAX) continue;
+        for (int i = lane; i < n; i += 32) A[i] = src[b0 + i];
+        uint32_t* in = A;
+        uint32_t* out = B;
+        for (int shift = 0; shift < nbits; shift += WR_BITS) {
+            for (int i = lane; i < WR_BINS; i += 32) hist[i] = 0;
+            __syncwarp();
+            for (int r = 0; r < n; r += 32) {
+                const int i = r + lane;
+                const bool ok = i < n;
+                const uint32_t d = ok ? (in[i] >> shift) & (WR_BINS - 1) : 0xFFFFFFFFu;
+                const unsigned peers = __match_any_sync(0xffffffffu, d);
+                uint32_t before = 0;
+                if (ok) before = hist[d];
+                __syncwarp();
+                if (ok) {
+                    pos[i] = (uint16_t)(before + __popc(peers & lt));
+                    if ((peers & lt) == 0) hist[d] = before + __popc(peers);
+                }
+                __syncwarp();
+            }
+            // exclusive scan of the bins (WR_BINS / 32 per lane)
+            constexpr int PER = WR_BINS / 32;
+            uint32_t loc = 0;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) loc += hist[lane * PER + k];
+            uint32_t x = loc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            uint32_t run = x - loc;
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const uint32_t c = hist[lane * PER + k];
+                hist[lane * PER + k] = run;
+                run += c;
+            }
+            __syncwarp();
+            for (int i = lane; i < n; i += 32) {
+                const uint32_t v = in[i];
+                out[hist[(v >> shift) & (WR_BINS - 1)] + pos[i]] = v;
+            }
+            __syncwarp();
+            uint32_t* tmp = in;
+            in = out;
+            out = tmp;
+        }
+        for (int i = lane; i < n; i += 32) src[b0 + i] = in[i];
+        __syncwarp();
+    }
+}
+
 __global__ void k_max_u32(const uint32_t* __restrict__ in, int64_t n, unsigned* __restrict__ out) {
     unsigned m = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -368,11 +445,17 @@ fmm_status canonicalise(fmm_ctx* ctx, DevBuf& lst, int64_t n, uint32_t* tcnt, De
         k_segsort_warp<8><<<gw, 128, 0, s>>>(P_<uint64_t>(off), nc, P_<uint32_t>(src), 0);
         FMM_LAUNCH(ctx);
         if (mx > 256) {
-            k_segsort_warp<32><<<gw, 128, 0, s>>>(P_<uint64_t>(off), nc, P_<uint32_t>(src), 257);
-            FMM_LAUNCH(ctx);
-        }
-        if (mx > 1024) {
-            k_segsort_warp<64><<<gw, 128, 0, s>>>(P_<uint64_t>(off), nc, P_<uint32_t>(src), 1025);
+            int nbits = 1;
+            while (((int64_t)1 << nbits) < nc) ++nbits;
+            const size_t smem = (size_t)WR_WARPS * (2 * WR_MAX + WR_MAX / 2 + WR_BINS) * 4;
+            static bool attr = false;
+            if (!attr) {
+                FMM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_segsort_wradix, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)smem));
+                attr = true;
+            }
+            const unsigned gr = (unsigned)std::min<int64_t>((nc + WR_WARPS - 1) / WR_WARPS, (int64_t)ctx->num_sms * 8);
+            k_segsort_wradix<<<gr, WR_WARPS * 32, smem, s>>>(P_<uint64_t>(off), nc, P_<uint32_t>(src), nbits, 257);
             FMM_LAUNCH(ctx);
         }
         if (mx > 2048) {
