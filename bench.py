@@ -292,7 +292,7 @@ def main():
         tpath = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tpath):
             traffic = json.load(open(tpath)).get(f"{args.config}:{dom}")
-        roof = {"kernel": f"{dom} ({'k_m2l_fast' if dom == 'm2l' else 'k_p2p'})", "bound": "alu",
+        roof = {"kernel": f"{dom} ({'k_m2l_fast' if dom == 'm2l' else 'k_p2p_cta'})", "bound": "alu",
                 "achieved": round(m2l_tf if dom == "m2l" else p2p_tf, 3), "peak": round(fp32_peak_tflops, 2),
                 "unit": "TFLOP/s", "frac": round((m2l_tf if dom == "m2l" else p2p_tf) / fp32_peak_tflops, 4),
                 "traffic": traffic,
@@ -306,8 +306,9 @@ def main():
                             "flops_per_interaction": P2P_FLOPS, "TFLOP/s": round(p2p_tf, 3),
                             "frac": round(p2p_tf / fp32_peak_tflops, 4),
                             "interactions_per_s": counts["p2p_interactions"] / (p2p_ms * 1e-3) if p2p_ms else None}},
-                "measured": "CUDA events recorded by libfmm on the stream each kernel runs on (M2L on the caller's "
-                            "stream, P2P on the aux stream, concurrent)"}
+                "measured": "CUDA events recorded by libfmm around each kernel on the stream it runs on (P2P then "
+                            "M2L, back to back on the caller's stream); per-launch average over the timed steps",
+                "traffic_note": "dram read+write bytes per launch from one ncu --set full capture (profiles/traffic.json)"}
         line = {"metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32" if cfg["prec"] == "f32" else "f64",
