@@ -58,6 +58,10 @@ def lib():
             "ofmm_cells": (None, [p] * 12),
             "ofmm_lists": (None, [p, p, p]),
             "ofmm_expansions": (None, [p, p, p]),
+            "ofmm_traverse_pair": (p, [p, p]),
+            "ofmm_pairlists_get": (None, [p, p, p, p]),
+            "ofmm_pairlists_free": (None, [p]),
+            "ofmm_evaluate_multi": (i32, [p, p, i32, p, p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -231,6 +235,29 @@ class FMM:
         M = np.zeros((nc, ncoef(self.P))); L = np.zeros((nc, ncoef(self.P)))
         lib().ofmm_expansions(self._h, _ptr(M), _ptr(L))
         return M, L
+
+
+def traverse_pair(T: "FMM", S: "FMM"):
+    """Per-partition mode: canonical (target in T, source in S) M2L and P2P lists."""
+    h = lib().ofmm_traverse_pair(T._h, S._h)
+    c = np.zeros(2, dtype=np.int64)
+    lib().ofmm_pairlists_get(h, _ptr(c), None, None)
+    m2l = np.zeros((c[0], 2), dtype=np.uint32); p2p = np.zeros((c[1], 2), dtype=np.uint32)
+    lib().ofmm_pairlists_get(h, _ptr(c), _ptr(m2l), _ptr(p2p))
+    lib().ofmm_pairlists_free(h)
+    return m2l, p2p
+
+
+def evaluate_multi(T: "FMM", sources):
+    """phi/grad of T's particles (T's input order) with sources T and every tree in `sources`."""
+    if not T._traversed:
+        T.traverse()
+    arr = (C.c_void_p * max(len(sources), 1))(*[s._h for s in sources])
+    phi = np.zeros(T.n); grad = np.zeros((T.n, 3))
+    rc = lib().ofmm_evaluate_multi(T._h, arr, len(sources), _ptr(phi), _ptr(grad))
+    if rc != 0:
+        raise RuntimeError(f"oracle evaluate_multi failed ({rc})")
+    return phi, grad
 
 
 def rel_l2(a, b) -> float:

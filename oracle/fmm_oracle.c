@@ -618,6 +618,101 @@ int ofmm_evaluate(ofmm* o, const int64_t* targets, int64_t nt, double* phi, doub
     return 0;
 }
 
+
+/* ------------------------------------------------- per-partition mode (§8e) --- */
+/* The targets of tree T traversed against the FULL local tree S of another partition, from
+ * (root_T, root_S), by the same R8/R9 rules (A from T, B from S).  This is what every rank's
+ * remote traversal must reproduce when the LET is sufficient. */
+struct ofmm_pairlists { pairvec m2l, p2p; };
+
+static void dtt2(const ofmm* T, const ofmm* S, ofmm_pairlists* out, uint32_t a, uint32_t b) {
+    const cell_t* A = &T->cells[a];
+    const cell_t* B = &S->cells[b];
+    int leafA = A->child_count == 0, leafB = B->child_count == 0;
+    if (mac(T, A, B)) {
+        push_pair(&out->m2l, a, b);
+    } else if (leafA && leafB) {
+        push_pair(&out->p2p, a, b);
+    } else if (leafB || (!leafA && A->R >= B->R)) {
+        for (uint32_t k = 0; k < A->child_count; ++k) dtt2(T, S, out, A->child_begin + k, b);
+    } else {
+        for (uint32_t k = 0; k < B->child_count; ++k) dtt2(T, S, out, a, B->child_begin + k);
+    }
+}
+
+ofmm_pairlists* ofmm_traverse_pair(const ofmm* T, const ofmm* S) {
+    ofmm_pairlists* pl = calloc(1, sizeof(ofmm_pairlists));
+    if (T->ncell > 0 && S->ncell > 0) dtt2(T, S, pl, 0, 0);
+    if (pl->m2l.n) qsort(pl->m2l.v, (size_t)pl->m2l.n, 2 * sizeof(uint32_t), cmp_pair);
+    if (pl->p2p.n) qsort(pl->p2p.v, (size_t)pl->p2p.n, 2 * sizeof(uint32_t), cmp_pair);
+    return pl;
+}
+
+void ofmm_pairlists_get(const ofmm_pairlists* pl, int64_t counts[2], uint32_t* m2l, uint32_t* p2p) {
+    counts[0] = pl->m2l.n; counts[1] = pl->p2p.n;
+    if (m2l && pl->m2l.n) memcpy(m2l, pl->m2l.v, (size_t)pl->m2l.n * 2 * sizeof(uint32_t));
+    if (p2p && pl->p2p.n) memcpy(p2p, pl->p2p.v, (size_t)pl->p2p.n * 2 * sizeof(uint32_t));
+}
+
+void ofmm_pairlists_free(ofmm_pairlists* pl) {
+    if (!pl) return;
+    free(pl->m2l.v); free(pl->p2p.v); free(pl);
+}
+
+/* phi/grad (caller order of T's particles) with sources = T itself and every S[k]: local
+ * lists of T, remote lists (T, S[k]); M of each S[k] from its own upward pass; L2L/L2P in T. */
+int ofmm_evaluate_multi(ofmm* T, ofmm* const* S, int nsrc, double* phi, double* grad) {
+    int64_t n = T->n;
+    for (int64_t k = 0; k < n; ++k) { phi[k] = 0.0; grad[3 * k] = grad[3 * k + 1] = grad[3 * k + 2] = 0.0; }
+    if (n == 0) return 0;
+    if (!T->traversed && ofmm_traverse(T) != 0) return -1;
+    int nc = T->t->ncoef;
+    free(T->M); free(T->L);
+    T->M = calloc((size_t)T->ncell * nc, sizeof(double));
+    T->L = calloc((size_t)T->ncell * nc, sizeof(double));
+    upward(T, 0);
+    for (int k = 0; k < nsrc; ++k)
+        if (S[k]->ncell > 0) {
+            free(S[k]->M);
+            S[k]->M = calloc((size_t)S[k]->ncell * nc, sizeof(double));
+            upward(S[k], 0);
+        }
+    double* phi_s = calloc((size_t)n, sizeof(double));
+    double* grad_s = calloc((size_t)3 * n, sizeof(double));
+    for (int k = -1; k < nsrc; ++k) {
+        const ofmm* src = k < 0 ? T : S[k];
+        ofmm_pairlists* pl = NULL;
+        const pairvec* m2l = &T->m2l;
+        const pairvec* p2p = &T->p2p;
+        if (k >= 0) {
+            pl = ofmm_traverse_pair(T, src);
+            m2l = &pl->m2l; p2p = &pl->p2p;
+        }
+        for (int64_t i = 0; i < m2l->n; ++i) {
+            const cell_t* A = &T->cells[m2l->v[2 * i]];
+            const cell_t* B = &src->cells[m2l->v[2 * i + 1]];
+            double d[3] = {A->c[0] - B->c[0], A->c[1] - B->c[1], A->c[2] - B->c[2]};
+            m2l_t(T->t, src->M + (size_t)m2l->v[2 * i + 1] * nc, d, T->L + (size_t)m2l->v[2 * i] * nc);
+        }
+        for (int64_t i = 0; i < p2p->n; ++i) {
+            const cell_t* A = &T->cells[p2p->v[2 * i]];
+            const cell_t* B = &src->cells[p2p->v[2 * i + 1]];
+            for (uint32_t j = A->body_begin; j < A->body_begin + A->body_count; ++j)
+                p2p_one(T->pos + 3 * (size_t)j, B->body_count, src->pos + 3 * (size_t)B->body_begin,
+                        src->q + B->body_begin, phi_s + j, grad_s + 3 * (size_t)j);
+        }
+        ofmm_pairlists_free(pl);
+    }
+    downward(T, 0, NULL, NULL, phi_s, grad_s);
+    for (int64_t i = 0; i < n; ++i) {
+        uint32_t j = T->perm[i];
+        phi[j] = phi_s[i];
+        for (int d = 0; d < 3; ++d) grad[3 * (size_t)j + d] = grad_s[3 * (size_t)i + d];
+    }
+    free(phi_s); free(grad_s);
+    return 0;
+}
+
 /* -------------------------------------------------------- introspection --- */
 void ofmm_counts(const ofmm* o, int64_t c[6]) {
     int64_t nleaf = 0, depth = 0, inter = 0;

@@ -69,6 +69,16 @@ void ofmm_cells(const ofmm*, int32_t* level, uint64_t* key, uint32_t* body_begin
 void ofmm_lists(const ofmm*, uint32_t* m2l /* [n_m2l][2] */, uint32_t* p2p /* [n_p2p][2] */);
 void ofmm_expansions(const ofmm*, double* M, double* L);   /* [ncell][ncoef] each; NULL to skip */
 
+/* Per-partition mode: the targets of tree T against the full local tree S
+ * of another partition, from (root_T, root_S) under R8-R10; and phi/grad of T's particles with
+ * sources T and S[0..nsrc).  Each tree is built from its own particles (local root cube,
+ * PAPER.md:118 §II-C "completely local construction of the octree using the local bounding box"). */
+typedef struct ofmm_pairlists ofmm_pairlists;
+ofmm_pairlists* ofmm_traverse_pair(const ofmm* T, const ofmm* S);
+void ofmm_pairlists_get(const ofmm_pairlists*, int64_t counts[2], uint32_t* m2l, uint32_t* p2p);
+void ofmm_pairlists_free(ofmm_pairlists*);
+int  ofmm_evaluate_multi(ofmm* T, ofmm* const* S, int nsrc, double* phi, double* grad);
+
 #ifdef __cplusplus
 }
 #endif

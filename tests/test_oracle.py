@@ -519,3 +519,56 @@ def test_generator_determinism_and_plummer_median():
     assert np.all((c[0] >= 0) & (c[0] < 1)) and np.all((c[1] >= -1) & (c[1] < 1))
     f32 = synth.generate("cube", 100, 1, np.float32)[0]
     np.testing.assert_array_equal(f32, c[0].astype(np.float32))
+
+
+# ------------------------------------------------------ per-partition mode (§8e) --
+def _partitions(pos, k):
+    return np.array_split(np.argsort(pos[:, 0], kind="stable"), k)
+
+
+def test_partition_tiny_theta_equals_direct():
+    # theta -> 0: every cross-partition pair is P2P, so the multi-tree sum is the direct sum
+    pos, q = synth.generate("plummer", 900, 31)
+    parts = _partitions(pos, 3)
+    trees = [oracle.FMM(pos[p], q[p], 3, 1e-3, 8) for p in parts]
+    dp, dg = oracle.direct(pos, q)
+    for k, p in enumerate(parts):
+        phi, g = oracle.evaluate_multi(trees[k], [t for j, t in enumerate(trees) if j != k])
+        assert oracle.rel_l2(phi, dp[p]) <= 1e-13 and oracle.rel_l2(g, dg[p]) <= 1e-13
+
+
+def test_partition_exactly_once_coverage():
+    # local lists of tree k plus its remote lists against every other tree cover each
+    # (target body, source body) pair of the whole system exactly once
+    pos, q = synth.generate("cube", 600, 32)
+    parts = _partitions(pos, 3)
+    trees = [oracle.FMM(pos[p], q[p], 3, 0.5, 8).traverse() for p in parts]
+    for k in range(3):
+        T = trees[k]
+        cT = T.cells()
+        _, permT = T.sorted()
+        cov = np.zeros((len(parts[k]), len(pos)), dtype=np.int32)
+        for j in range(3):
+            S = trees[j]
+            cS = S.cells()
+            _, permS = S.sorted()
+            m2l, p2p = T.lists() if j == k else oracle.traverse_pair(T, S)
+            for a, b in np.vstack([m2l, p2p]):
+                ta = permT[cT["body_begin"][a]:cT["body_begin"][a] + cT["body_count"][a]]
+                sb = parts[j][permS[cS["body_begin"][b]:cS["body_begin"][b] + cS["body_count"][b]]]
+                cov[np.ix_(ta, sb)] += 1
+            if j != k:
+                for a, b in m2l:   # remote M2L pairs satisfy the MAC strictly
+                    d = np.linalg.norm(cT["center"][a] - cS["center"][b])
+                    assert cT["radius"][a] + cS["radius"][b] < 0.5 * d
+        assert np.all(cov == 1)
+
+
+def test_partition_single_tree_equals_evaluate():
+    pos, q = synth.generate("cube", 800, 33)
+    a = oracle.FMM(pos, q, 5, 0.5, 16)
+    b = oracle.FMM(pos, q, 5, 0.5, 16)
+    phi1, g1 = a.evaluate()
+    phi2, g2 = oracle.evaluate_multi(b, [])
+    np.testing.assert_array_equal(phi1, phi2)
+    np.testing.assert_array_equal(g1, g2)
