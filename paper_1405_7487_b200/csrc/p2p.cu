@@ -238,6 +238,35 @@ __global__ void __launch_bounds__(PF_WARPS * 32) k_p2p_f32(const float4* __restr
 }
 
 
+// Packed form of p2p_body for the CTA path: the thread's 4 targets are held as 2 float2 pairs
+// (positions stored NEGATED so dx = s.x + (-x) is one FADD2 with a broadcast operand), and
+// every FP32 step is an f32x2 instruction (FADD2/FMUL2/FFMA2, sm_100): the FMA pipe does the
+// same 13 lane-ops per interaction, but the issue slots they take halve, which leaves room
+// for the LDS, MUFU.RSQ and loop instructions (the scalar form was issue-bound).
+template <bool CHECK>
+__device__ __forceinline__ void p2p_body2(const float4 s, const float2 (&nx)[2], const float2 (&ny)[2],
+                                          const float2 (&nz)[2], float2 (&f)[2], float2 (&gx)[2],
+                                          float2 (&gy)[2], float2 (&gz)[2]) {
+    const float2 sx = make_float2(s.x, s.x), sy = make_float2(s.y, s.y), sz = make_float2(s.z, s.z);
+    const float2 sq = make_float2(s.w, s.w);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const float2 dx = __fadd2_rn(sx, nx[k]), dy = __fadd2_rn(sy, ny[k]), dz = __fadd2_rn(sz, nz[k]);
+        const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+        float2 inv = make_float2(rsqrtf(r2.x), rsqrtf(r2.y));
+        if (CHECK) {
+            inv.x = r2.x > 0.f ? inv.x : 0.f;
+            inv.y = r2.y > 0.f ? inv.y : 0.f;
+        }
+        const float2 qi = __fmul2_rn(sq, inv);
+        const float2 qi3 = __fmul2_rn(qi, __fmul2_rn(inv, inv));
+        f[k] = __fadd2_rn(f[k], qi);
+        gx[k] = __ffma2_rn(qi3, dx, gx[k]);
+        gy[k] = __ffma2_rn(qi3, dy, gy[k]);
+        gz[k] = __ffma2_rn(qi3, dz, gz[k]);
+    }
+}
+
 // ------------------------------------------------------- fp32 CTA-per-leaf path
 // One CTA (128 threads) per target leaf, taken from an atomic counter in leaf order.  The
 // leaf's nt targets occupy lpg = ceil(nt/4) threads x 4 registers; the CTA's 128 threads form
@@ -249,8 +278,7 @@ __global__ void __launch_bounds__(PF_WARPS * 32) k_p2p_f32(const float4* __restr
 // and group g consumes entries g, g+G, ... (G consecutive float4 per step).  Only chunks
 // that overlap the target's own leaf take the r^2 > 0 test.
 constexpr int PC_THREADS = 128;
-constexpr int PC_TILE = 256;
-
+template <int PC_TILE>
 __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict__ body,
                                                          const uint32_t* __restrict__ leaf_ids, int64_t nleaf,
                                                          const uint2* __restrict__ runs,
@@ -288,27 +316,37 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict
             const int g = tid / lpg, j = tid - g * lpg;
             const bool active = g < G;
             const uint32_t CH = (uint32_t)(G * (PC_TILE / G));
-            float x[PF_T], y[PF_T], z[PF_T], f[PF_T], gx[PF_T], gy[PF_T], gz[PF_T];
+            // target slot k of this thread is t = j + k*lpg; slots (0,1) and (2,3) form the pairs
+            float2 nx[2], ny[2], nz[2], f[2], gx[2], gy[2], gz[2];
 #pragma unroll
-            for (int k = 0; k < PF_T; ++k) {
-                const uint32_t t = (uint32_t)(j + k * lpg);
-                const float4 p = body[tb + t0 + (t < nt ? t : 0)];
-                x[k] = t < nt ? p.x : 1e30f; y[k] = p.y; z[k] = p.z;
-                f[k] = gx[k] = gy[k] = gz[k] = 0.f;
+            for (int h = 0; h < 2; ++h) {
+                float px[2], py[2], pz[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const uint32_t t = (uint32_t)(j + (2 * h + e) * lpg);
+                    const float4 p = body[tb + t0 + (t < nt ? t : 0)];
+                    // unused slots sit far away so they never produce r^2 = 0
+                    px[e] = t < nt ? -p.x : -1e30f; py[e] = -p.y; pz[e] = -p.z;
+                }
+                nx[h] = make_float2(px[0], px[1]); ny[h] = make_float2(py[0], py[1]);
+                nz[h] = make_float2(pz[0], pz[1]);
+                f[h] = gx[h] = gy[h] = gz[h] = make_float2(0.f, 0.f);
             }
             // loader cursors for flat indices tid and tid + 128 of every chunk
-            uint32_t cur0 = r0, cur1 = r0;
+            constexpr int NH = PC_TILE / PC_THREADS;
+            uint32_t cur[NH];
+#pragma unroll
+            for (int h = 0; h < NH; ++h) cur[h] = r0;
             auto load_chunk = [&](uint32_t k, int buf) {
                 const uint32_t f0 = k * CH;
                 const uint32_t len = min(CH, ns - f0);
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < NH; ++h) {
                     const uint32_t i = (uint32_t)tid + (uint32_t)h * PC_THREADS;
                     if (i < len) {
                         const uint32_t fl = f0 + i;
-                        uint32_t& cur = h ? cur1 : cur0;
-                        while (cur + 1 < r1 && runs[cur + 1].y <= fl) ++cur;
-                        const uint2 ru = runs[cur];
+                        while (cur[h] + 1 < r1 && runs[cur[h] + 1].y <= fl) ++cur[h];
+                        const uint2 ru = runs[cur[h]];
                         cp_async16(&s_tile[buf][i], body + ru.x + (fl - ru.y));
                     }
                 }
@@ -327,16 +365,19 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict
                     const float4* tl = s_tile[k & 1];
                     const bool self = f0 < selfF + nt_all && selfF < f0 + len;
                     if (self) {
-                        for (uint32_t i = g; i < len; i += G) p2p_body<true>(tl[i], x, y, z, f, gx, gy, gz);
+                        for (uint32_t i = g; i < len; i += G) p2p_body2<true>(tl[i], nx, ny, nz, f, gx, gy, gz);
                     } else {
-                        for (uint32_t i = g; i < len; i += G) p2p_body<false>(tl[i], x, y, z, f, gx, gy, gz);
+                        for (uint32_t i = g; i < len; i += G) p2p_body2<false>(tl[i], nx, ny, nz, f, gx, gy, gz);
                     }
                 }
                 __syncthreads();
             }
             cp_async_wait_0();
 #pragma unroll
-            for (int k = 0; k < PF_T; ++k) s_red[tid * PF_T + k] = make_float4(f[k], gx[k], gy[k], gz[k]);
+            for (int h = 0; h < 2; ++h) {
+                s_red[tid * PF_T + 2 * h] = make_float4(f[h].x, gx[h].x, gy[h].x, gz[h].x);
+                s_red[tid * PF_T + 2 * h + 1] = make_float4(f[h].y, gx[h].y, gy[h].y, gz[h].y);
+            }
             __syncthreads();
             if (g == 0) {
 #pragma unroll
@@ -372,10 +413,11 @@ fmm_status p2p_t(fmm_ctx* ctx, cudaStream_t s) {
         unsigned long long* counter = P_<unsigned long long>(ctx->cnt_tmp2);
         FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 8, s));
         int nb = 0;
-        FMM_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_p2p_cta, PC_THREADS, 0));
+        auto kern = k_p2p_cta<256>;
+        FMM_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, PC_THREADS, 0));
         const uint2* runs = P_<uint2>(ctx->runs);
         const uint32_t* rtot = reinterpret_cast<const uint32_t*>(runs + std::max<int64_t>(ctx->n_runs, 1));
-        k_p2p_cta<<<ctx->num_sms * std::max(nb, 1), PC_THREADS, 0, s>>>(
+        kern<<<ctx->num_sms * std::max(nb, 1), PC_THREADS, 0, s>>>(
             P_<float4>(ctx->body), P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, runs, P_<uint32_t>(ctx->run_off), rtot,
             P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), (float*)ctx->near_phi.p, (float*)ctx->near_grad.p,
             counter);
