@@ -72,6 +72,31 @@ const char* fmm_last_error(const fmm_ctx* ctx);
  * FMM_OK no-op (R20).  The positions must stay unchanged until fmm_evaluate. */
 fmm_status fmm_build(fmm_ctx* ctx, const void* pos, int64_t n, void* stream);
 
+/* The two halves of fmm_build, for the multi-GPU path, where remote LET
+ * cells are grafted between the tree and the traversal:
+ * fmm_build_tree: R2-R7 only (keys, sort, tree, geometry); synchronises `stream`.  Discards
+ *   grafted LETs and lists of an earlier build.
+ * fmm_dtt: dual tree traversal (R8-R10, §II-C).  remote == 0: from (root,
+ *   root), replacing earlier lists; remote != 0: from (root, r) for the root r of every LET
+ *   grafted by fmm_let_graft, appended to the lists of the last fmm_dtt.  Synchronises.
+ *   FMM_ERR_STATE if the traversal needs children of a remote cell that were not exported.
+ * fmm_lists: groups the traversal's pairs into canonical CSR lists (R10; sources of a
+ *   target ascending: local cells, then LET 0, LET 1, ... in their sender's order).
+ * fmm_build(pos, n) == fmm_build_tree + fmm_dtt(0) + fmm_lists. */
+fmm_status fmm_build_tree(fmm_ctx* ctx, const void* pos, int64_t n, void* stream);
+fmm_status fmm_dtt(fmm_ctx* ctx, int remote, void* stream);
+fmm_status fmm_lists(fmm_ctx* ctx, void* stream);
+
+/* The two halves of fmm_evaluate:
+ * fmm_upward: gathers q (device [n]) into the sorted bodies and runs P2M/M2M (R12, R13)
+ *   over the local tree; pos must be the pointer of the last build.
+ * fmm_interact: M2L (R14) and P2P (R17) over the lists -- including grafted LET sources,
+ *   whose data must have arrived by fmm_let_unpack -- then L2L/L2P (R15, R16) and the
+ *   output scatter (R18).  phi [n], grad [n][3] device, caller order.  Asynchronous.
+ * fmm_evaluate(pos, q, phi, grad) == fmm_upward + fmm_interact. */
+fmm_status fmm_upward(fmm_ctx* ctx, const void* pos, const void* q, void* stream);
+fmm_status fmm_interact(fmm_ctx* ctx, void* phi, void* grad, void* stream);
+
 /* fmm_evaluate: potentials and gradients for the last build (R12-R18).
  *   pos  the same device pointer passed to the last fmm_build (else FMM_ERR_STATE)
  *   q    device [n] charges;  phi device [n];  grad device [n][3] (grad = +grad(phi), R1)
@@ -98,6 +123,62 @@ fmm_status fmm_copy_cells(const fmm_ctx* ctx, int32_t* level, uint64_t* key, uin
 fmm_status fmm_copy_lists(const fmm_ctx* ctx, uint32_t* m2l, uint32_t* p2p);
 /* fp64 expansions [ncell][ncoef] after fmm_evaluate (R11 order); either may be NULL */
 fmm_status fmm_copy_expansions(const fmm_ctx* ctx, double* M, double* L);
+
+/* ---- multi-GPU: Morton-range partition (§II-B,
+ * Eq. (1)).  The collectives between these calls are the caller's (the
+ * Python layer uses torch.distributed over NCCL); every step on the data runs here.
+ * fmm_bounds: exact fp64 min/max of pos (device [n][3], ctx precision) into out (HOST [6]:
+ *   lo xyz, hi xyz; +inf/-inf when n == 0).  Synchronises.  FMM_ERR_NONFINITE on NaN/Inf.
+ * fmm_part_keys: 63-bit Morton keys (R3, R4) of pos under the root cube (R2) of the given
+ *   GLOBAL bounds (HOST [6], the all-reduce of every rank's fmm_bounds); keys device [n].
+ * fmm_part_histogram: hist (device [2^bits] fp64, overwritten): every key whose top
+ *   prefix_bits bits equal prefix adds w[i] (device [n] fp32, NULL = 1) at the bin of its
+ *   next `bits` bits; prefix_bits = 0 takes every key.  1 <= bits <= 24, prefix_bits + bits
+ *   <= 63.  The caller all-reduces it and refines the splitters bin by bin.
+ * fmm_part_pack: destination rank of particle i = number of splitters (HOST [nranks-1]
+ *   ascending keys) <= key[i]; writes the particles grouped by destination, stable within a
+ *   group, to out_pos [n][3] / out_q [n] (device, ctx precision) with global ids
+ *   out_gid [n] = gid_base + i (device int64), and counts (HOST [nranks]) per destination.
+ *   Synchronises.  1 <= nranks <= 256. */
+fmm_status fmm_bounds(fmm_ctx* ctx, const void* pos, int64_t n, double* out, void* stream);
+fmm_status fmm_part_keys(fmm_ctx* ctx, const void* pos, int64_t n, const double* bounds, uint64_t* keys, void* stream);
+fmm_status fmm_part_histogram(fmm_ctx* ctx, const uint64_t* keys, const float* w, int64_t n, uint64_t prefix,
+                              int prefix_bits, int bits, double* hist, void* stream);
+fmm_status fmm_part_pack(fmm_ctx* ctx, const void* pos, const void* q, const uint64_t* keys, int64_t n,
+                         const uint64_t* splitters, int nranks, int64_t gid_base, void* out_pos, void* out_q,
+                         int64_t* out_gid, int64_t* counts, void* stream);
+
+/* ---- multi-GPU: local essential tree (§II-C).
+ * Sender-initiated: every rank publishes a cover of its local tree, every sender exports to
+ * each receiver the part of its tree the receiver's traversal can need (let.cu states the
+ * rule), the receiver grafts the parts after its local cells and traverses them.
+ * fmm_let_cover: the cover of this rank's tree into cover (HOST [FMM_LET_MAX_COVER][8]:
+ *   kind (0 summary, 1 guard), radius, box lo xyz, box hi xyz) and its entry count.
+ *   Needs fmm_build_tree.  Synchronises.
+ * fmm_let_plan: which cells and bodies go to `peer` (any id >= 0 the caller chooses) given
+ *   that peer's cover; returns the byte sizes of its structure and data messages.  Needs
+ *   fmm_build_tree.  Synchronises.
+ * fmm_let_pack_struct: writes the structure message for `peer` (geometry, child/body
+ *   counts, sender cell ids, body positions) to dst (device, struct_bytes, 16-B aligned).
+ * fmm_let_pack_data: writes the data message (fp64 multipoles, body charges) to dst
+ *   (device, data_bytes); needs fmm_upward.
+ * fmm_let_graft: appends the npeers received structure messages (device pointers src[k] of
+ *   bytes[k] bytes, HOST arrays) after the local cells and bodies, replacing earlier
+ *   grafts; then fmm_dtt(remote = 1) and fmm_lists.  Synchronises.
+ * fmm_let_unpack: writes the received data messages (same order as the graft) into the
+ *   grafted cells and bodies; call after fmm_upward, before fmm_interact.
+ * fmm_let_remote: grafted LET k: first cell index, cell and body counts, and (HOST [ncell],
+ *   may be NULL) the sender's cell index of each grafted cell (parity tests). */
+#define FMM_LET_MAX_COVER 73
+#define FMM_LET_ABSENT 0xFFFFFFFFu
+fmm_status fmm_let_cover(fmm_ctx* ctx, double* cover, int* ncover, void* stream);
+fmm_status fmm_let_plan(fmm_ctx* ctx, int peer, const double* cover, int ncover, int64_t* struct_bytes,
+                        int64_t* data_bytes, void* stream);
+fmm_status fmm_let_pack_struct(fmm_ctx* ctx, int peer, void* dst, void* stream);
+fmm_status fmm_let_pack_data(fmm_ctx* ctx, int peer, void* dst, void* stream);
+fmm_status fmm_let_graft(fmm_ctx* ctx, int npeers, const void* const* src, const int64_t* bytes, void* stream);
+fmm_status fmm_let_unpack(fmm_ctx* ctx, int npeers, const void* const* src, const int64_t* bytes, void* stream);
+fmm_status fmm_let_remote(const fmm_ctx* ctx, int k, int64_t* base, int64_t* ncell, int64_t* nbody, uint32_t* orig);
 
 /* ---- timing (bench): per-phase device time from CUDA events recorded on the stream
  * each phase runs on.  enable != 0 turns recording on (small overhead).

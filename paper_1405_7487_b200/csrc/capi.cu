@@ -144,6 +144,12 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
                       &ctx->run_len64, &ctx->dcount2, &ctx->tcnt, &ctx->cnt64, &ctx->big_off, &ctx->M, &ctx->L, &ctx->Mr, &ctx->Lr, &ctx->near_phi, &ctx->near_grad,
                       &ctx->h_stage};
     for (DevBuf* b : bufs) buf_free(*b);
+    DevBuf* lbufs[] = {&ctx->let_tmp, &ctx->let_cov, &ctx->c_orig, &ctx->part_tmp};
+    for (DevBuf* b : lbufs) buf_free(*b);
+    for (auto& lp : ctx->let_peers) {
+        DevBuf* pb[] = {&lp.opened, &lp.eflag, &lp.eidx, &lp.bflag, &lp.boff};
+        for (DevBuf* b : pb) buf_free(*b);
+    }
     for (auto& t : ctx->pending) {
         cudaEventDestroy(t.a);
         cudaEventDestroy(t.b);
@@ -158,7 +164,7 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
 
 const char* fmm_last_error(const fmm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
-fmm_status fmm_build(fmm_ctx* ctx, const void* pos, int64_t n, void* stream) {
+fmm_status fmm_build_tree(fmm_ctx* ctx, const void* pos, int64_t n, void* stream) {
     FMM_TRY(check_ctx(ctx));
     ctx->err.clear();
     if (n < 0 || n > ctx->n_max) {
@@ -171,37 +177,102 @@ fmm_status fmm_build(fmm_ctx* ctx, const void* pos, int64_t n, void* stream) {
     }
     DeviceGuard g(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
-    ctx->built = false;
-    ctx->evaluated = false;
+    ctx->built = ctx->tree_built = false;
+    ctx->evaluated = ctx->upward_done = false;
     ctx->n = n;
     ctx->built_pos = pos;
     ctx->ncell = ctx->nleaf = ctx->depth = ctx->n_m2l = ctx->n_p2p = ctx->p2p_inter = 0;
+    ctx->nrem = ctx->nrem_body = 0;
+    ctx->let_remote.clear();
+    for (auto& lp : ctx->let_peers) lp.planned = false;
     ctx->level_begin.clear();
     if (n > 0) {
         FMM_TRY(build_keys(ctx, pos, n, s));
         FMM_TRY(build_tree(ctx, s));
-        FMM_TRY(build_lists(ctx, s));
     }
+    ctx->tree_built = true;
+    return FMM_OK;
+}
+
+fmm_status fmm_dtt(fmm_ctx* ctx, int remote, void* stream) {
+    FMM_TRY(check_ctx(ctx));
+    ctx->err.clear();
+    if (!ctx->tree_built) {
+        ctx->err = "fmm_dtt: no tree (fmm_build_tree first)";
+        return FMM_ERR_STATE;
+    }
+    ctx->built = ctx->evaluated = false;
+    if (ctx->n == 0) return FMM_OK;
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!remote) {
+        const uint64_t root_pair = 0;
+        return dtt_pass(ctx, &root_pair, 1, false, s);
+    }
+    std::vector<uint64_t> seeds;
+    for (const auto& r : ctx->let_remote)
+        if (r.ncell > 0) seeds.push_back((uint64_t)r.base);   // (local root 0, remote root)
+    if (seeds.empty()) return FMM_OK;
+    return dtt_pass(ctx, seeds.data(), (int)seeds.size(), true, s);
+}
+
+fmm_status fmm_lists(fmm_ctx* ctx, void* stream) {
+    FMM_TRY(check_ctx(ctx));
+    ctx->err.clear();
+    if (!ctx->tree_built) {
+        ctx->err = "fmm_lists: no tree (fmm_build_tree first)";
+        return FMM_ERR_STATE;
+    }
+    DeviceGuard g(ctx->device);
+    if (ctx->n > 0) FMM_TRY(lists_pass(ctx, (cudaStream_t)stream));
     ctx->built = true;
     return FMM_OK;
 }
 
-fmm_status fmm_evaluate(fmm_ctx* ctx, const void* pos, const void* q, void* phi, void* grad, void* stream) {
+fmm_status fmm_build(fmm_ctx* ctx, const void* pos, int64_t n, void* stream) {
+    FMM_TRY(fmm_build_tree(ctx, pos, n, stream));
+    FMM_TRY(fmm_dtt(ctx, 0, stream));
+    return fmm_lists(ctx, stream);
+}
+
+fmm_status fmm_upward(fmm_ctx* ctx, const void* pos, const void* q, void* stream) {
     FMM_TRY(check_ctx(ctx));
     ctx->err.clear();
-    if (!ctx->built || pos != ctx->built_pos) {
-        ctx->err = "fmm_evaluate: no matching fmm_build for these positions";
+    if (!ctx->tree_built || pos != ctx->built_pos) {
+        ctx->err = "fmm_upward: no matching fmm_build for these positions";
         return FMM_ERR_STATE;
     }
-    if (ctx->n == 0) return FMM_OK;
-    if (!q || !phi || !grad) {
-        ctx->err = "fmm_evaluate: null pointer";
+    ctx->evaluated = false;
+    if (ctx->n == 0) {
+        ctx->upward_done = true;
+        return FMM_OK;
+    }
+    if (!q) {
+        ctx->err = "fmm_upward: null pointer";
         return FMM_ERR_ARG;
     }
     DeviceGuard g(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
     FMM_TRY(gather_bodies_q(ctx, q, s));
     FMM_TRY(upward_pass(ctx, s));
+    ctx->upward_done = true;
+    return FMM_OK;
+}
+
+fmm_status fmm_interact(fmm_ctx* ctx, void* phi, void* grad, void* stream) {
+    FMM_TRY(check_ctx(ctx));
+    ctx->err.clear();
+    if (!ctx->built || !ctx->upward_done) {
+        ctx->err = "fmm_interact: needs fmm_lists and fmm_upward first";
+        return FMM_ERR_STATE;
+    }
+    if (ctx->n == 0) return FMM_OK;
+    if (!phi || !grad) {
+        ctx->err = "fmm_interact: null pointer";
+        return FMM_ERR_ARG;
+    }
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
     if (ctx->serial_nearfar) {
         // both persistent kernels fill the GPU on their own: run them back to back
         FMM_TRY(p2p_pass(ctx, s));
@@ -217,6 +288,101 @@ fmm_status fmm_evaluate(fmm_ctx* ctx, const void* pos, const void* q, void* phi,
     }
     FMM_TRY(downward_pass(ctx, phi, grad, s));
     ctx->evaluated = true;
+    return FMM_OK;
+}
+
+fmm_status fmm_evaluate(fmm_ctx* ctx, const void* pos, const void* q, void* phi, void* grad, void* stream) {
+    FMM_TRY(check_ctx(ctx));
+    if (!ctx->built || pos != ctx->built_pos) {
+        ctx->err = "fmm_evaluate: no matching fmm_build for these positions";
+        return FMM_ERR_STATE;
+    }
+    if (ctx->n > 0 && (!q || !phi || !grad)) {
+        ctx->err = "fmm_evaluate: null pointer";
+        return FMM_ERR_ARG;
+    }
+    FMM_TRY(fmm_upward(ctx, pos, q, stream));
+    return fmm_interact(ctx, phi, grad, stream);
+}
+
+// ---- multi-GPU: LET (let.cu)
+fmm_status fmm_let_cover(fmm_ctx* ctx, double* cover, int* ncover, void* stream) {
+    FMM_TRY(check_ctx(ctx));
+    ctx->err.clear();
+    if (!cover || !ncover) return FMM_ERR_ARG;
+    if (!ctx->tree_built) return FMM_ERR_STATE;
+    DeviceGuard g(ctx->device);
+    return let_cover(ctx, cover, ncover, (cudaStream_t)stream);
+}
+
+fmm_status fmm_let_plan(fmm_ctx* ctx, int peer, const double* cover, int ncover, int64_t* struct_bytes,
+                        int64_t* data_bytes, void* stream) {
+    FMM_TRY(check_ctx(ctx));
+    ctx->err.clear();
+    if (peer < 0 || ncover < 0 || ncover > FMM_LET_MAX_COVER || (ncover > 0 && !cover) || !struct_bytes ||
+        !data_bytes)
+        return FMM_ERR_ARG;
+    if (!ctx->tree_built) return FMM_ERR_STATE;
+    DeviceGuard g(ctx->device);
+    if (ctx->n == 0) {
+        if ((int)ctx->let_peers.size() <= peer) ctx->let_peers.resize(peer + 1);
+        ctx->let_peers[peer].ncell = ctx->let_peers[peer].nbody = 0;
+        ctx->let_peers[peer].planned = false;
+        *struct_bytes = *data_bytes = 0;
+        return FMM_OK;
+    }
+    return let_plan(ctx, peer, cover, ncover, struct_bytes, data_bytes, (cudaStream_t)stream);
+}
+
+fmm_status fmm_let_pack_struct(fmm_ctx* ctx, int peer, void* dst, void* stream) {
+    FMM_TRY(check_ctx(ctx));
+    ctx->err.clear();
+    if (!dst) return FMM_ERR_ARG;
+    DeviceGuard g(ctx->device);
+    return let_pack(ctx, peer, 0, dst, (cudaStream_t)stream);
+}
+
+fmm_status fmm_let_pack_data(fmm_ctx* ctx, int peer, void* dst, void* stream) {
+    FMM_TRY(check_ctx(ctx));
+    ctx->err.clear();
+    if (!dst) return FMM_ERR_ARG;
+    DeviceGuard g(ctx->device);
+    return let_pack(ctx, peer, 1, dst, (cudaStream_t)stream);
+}
+
+fmm_status fmm_let_graft(fmm_ctx* ctx, int npeers, const void* const* src, const int64_t* bytes, void* stream) {
+    FMM_TRY(check_ctx(ctx));
+    ctx->err.clear();
+    if (npeers < 0 || (npeers > 0 && (!src || !bytes))) return FMM_ERR_ARG;
+    if (!ctx->tree_built) return FMM_ERR_STATE;
+    if (ctx->n == 0) return FMM_OK;
+    DeviceGuard g(ctx->device);
+    ctx->built = ctx->evaluated = false;
+    return let_graft(ctx, npeers, src, bytes, (cudaStream_t)stream);
+}
+
+fmm_status fmm_let_unpack(fmm_ctx* ctx, int npeers, const void* const* src, const int64_t* bytes, void* stream) {
+    FMM_TRY(check_ctx(ctx));
+    ctx->err.clear();
+    if (npeers < 0 || (npeers > 0 && (!src || !bytes))) return FMM_ERR_ARG;
+    if (ctx->n == 0) return FMM_OK;
+    DeviceGuard g(ctx->device);
+    return let_unpack(ctx, npeers, src, bytes, (cudaStream_t)stream);
+}
+
+fmm_status fmm_let_remote(const fmm_ctx* ctx_c, int k, int64_t* base, int64_t* ncell, int64_t* nbody, uint32_t* orig) {
+    FMM_TRY(check_ctx(ctx_c));
+    fmm_ctx* ctx = const_cast<fmm_ctx*>(ctx_c);
+    if (k < 0 || k >= (int)ctx->let_remote.size()) return FMM_ERR_ARG;
+    const LetRemote& r = ctx->let_remote[k];
+    if (base) *base = r.base;
+    if (ncell) *ncell = r.ncell;
+    if (nbody) *nbody = r.nbody;
+    if (orig && r.ncell) {
+        DeviceGuard g(ctx->device);
+        FMM_CUDA_TRY(ctx, cudaDeviceSynchronize());
+        FMM_CUDA_TRY(ctx, cudaMemcpy(orig, P_<uint32_t>(ctx->c_orig) + r.base, r.ncell * 4, cudaMemcpyDeviceToHost));
+    }
     return FMM_OK;
 }
 

@@ -54,6 +54,17 @@ struct DevBuf {
     size_t bytes = 0;
 };
 
+// per-peer LET export plan (let.cu): opened / exported flags, compacted cell and body offsets
+struct LetPeer {
+    DevBuf opened, eflag, eidx, bflag, boff;
+    int64_t ncell = 0, nbody = 0;
+    bool planned = false;
+};
+// one grafted remote LET: cells [base, base + ncell), bodies [bbase, bbase + nbody)
+struct LetRemote {
+    int64_t base, ncell, bbase, nbody;
+};
+
 struct TimedEvent {
     int phase;
     cudaEvent_t a, b;
@@ -89,7 +100,8 @@ struct fmm_ctx {
     // build state
     const void* built_pos = nullptr;
     int64_t n = 0;
-    bool built = false;
+    bool built = false;        // lists ready (fmm_lists)
+    bool tree_built = false;   // keys, tree and geometry ready (fmm_build_tree)
     bool evaluated = false;
 
     // root cube (device): [0..2] lo, [3..5] hi, [6..8] origin, [9] scale, [10] h
@@ -118,6 +130,14 @@ struct fmm_ctx {
     // expansions
     DevBuf M, L, Mr, Lr;   // fp64 [ncell][ncoef]; Mr: packed reduced multipoles for the M2L kernel; Lr: reduced L
     DevBuf near_phi, near_grad;  // P2P partials in sorted order (prec type)
+    bool upward_done = false;
+
+    // multi-GPU (let.cu, part.cu): remote LET cells live at [ncell, ncell + nrem) of every
+    // cell array the traversal and the M2L/P2P kernels read, remote bodies at [n, n + nrem_body)
+    int64_t nrem = 0, nrem_body = 0;
+    std::vector<LetPeer> let_peers;
+    std::vector<LetRemote> let_remote;
+    DevBuf let_tmp, let_cov, c_orig, part_tmp;
     DevBuf h_stage;              // device staging for fmm_solve_host
 };
 
@@ -177,8 +197,18 @@ fmm_status build_keys(fmm_ctx* ctx, const void* pos, int64_t n, cudaStream_t s);
 fmm_status gather_bodies_q(fmm_ctx* ctx, const void* q, cudaStream_t s);
 // tree.cu
 fmm_status build_tree(fmm_ctx* ctx, cudaStream_t s);
-// dtt.cu
+// dtt.cu: traversal from the given seed pairs (target << 32 | source), appended to the
+// unsorted lists when append; lists_pass groups them into canonical CSR lists + P2P runs
+fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append, cudaStream_t s);
+fmm_status lists_pass(fmm_ctx* ctx, cudaStream_t s);
 fmm_status build_lists(fmm_ctx* ctx, cudaStream_t s);
+// let.cu
+fmm_status let_cover(fmm_ctx* ctx, double* cover, int* ncover, cudaStream_t s);
+fmm_status let_plan(fmm_ctx* ctx, int peer, const double* cover, int ncover, int64_t* sbytes, int64_t* dbytes,
+                    cudaStream_t s);
+fmm_status let_pack(fmm_ctx* ctx, int peer, int part, void* dst, cudaStream_t s);
+fmm_status let_graft(fmm_ctx* ctx, int npeers, const void* const* src, const int64_t* bytes, cudaStream_t s);
+fmm_status let_unpack(fmm_ctx* ctx, int npeers, const void* const* src, const int64_t* bytes, cudaStream_t s);
 // upward.cu / downward.cu / m2l.cu / p2p.cu
 fmm_status upward_pass(fmm_ctx* ctx, cudaStream_t s);
 fmm_status m2l_pass(fmm_ctx* ctx, cudaStream_t s);

@@ -156,7 +156,11 @@ __global__ void __launch_bounds__(DT_THREADS) k_dtt_step(const uint64_t* __restr
                 pc += nch[k];
             } else if (o[k] == 3) {
                 const uint32_t k0 = v.cb[b[k]];
-                for (uint32_t c = 0; c < nch[k]; ++c) next[pc + c] = ((uint64_t)a[k] << 32) | (k0 + c);
+                // a grafted LET cell whose children were not exported (let.cu): the cover was
+                // insufficient; flag it instead of reading past the LET
+                if (k0 == FMM_LET_ABSENT) atomicOr(&cnt[3], 1ull);
+                for (uint32_t c = 0; c < nch[k]; ++c)
+                    next[pc + c] = ((uint64_t)a[k] << 32) | (k0 == FMM_LET_ABSENT ? b[k] : k0 + c);
                 pc += nch[k];
             }
             count_target(tcnt_m2l, o[k] == 0, a[k]);
@@ -166,7 +170,6 @@ __global__ void __launch_bounds__(DT_THREADS) k_dtt_step(const uint64_t* __restr
     }
 }
 
-__global__ void k_init_frontier(uint64_t* fr) { fr[0] = 0; }
 
 __global__ void k_widen_u32(const uint32_t* __restrict__ in, int64_t n, uint64_t* __restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -446,7 +449,7 @@ fmm_status canonicalise(fmm_ctx* ctx, DevBuf& lst, int64_t n, uint32_t* tcnt, De
         FMM_LAUNCH(ctx);
         if (mx > 256) {
             int nbits = 1;
-            while (((int64_t)1 << nbits) < nc) ++nbits;
+            while (((int64_t)1 << nbits) < nc + ctx->nrem) ++nbits;
             const size_t smem = (size_t)WR_WARPS * (2 * WR_MAX + WR_MAX / 2 + WR_BINS) * 4;
             static bool attr = false;
             if (!attr) {
@@ -481,7 +484,7 @@ fmm_status canonicalise(fmm_ctx* ctx, DevBuf& lst, int64_t n, uint32_t* tcnt, De
             k_big_gather<<<gb, 256, 0, s>>>(P_<uint64_t>(off), boff, nc, P_<uint32_t>(src), t0);
             FMM_LAUNCH(ctx);
             int nb = 0;
-            while (((int64_t)1 << nb) < nc) ++nb;
+            while (((int64_t)1 << nb) < nc + ctx->nrem) ++nb;
             uint64_t* sorted = nullptr;
             FMM_TRY(radix_sort_keys(ctx, t0, t1, (int64_t)nbig, 0, 32 + nb, &sorted, s));
             k_big_scatter<<<gb, 256, 0, s>>>(P_<uint64_t>(off), boff, nc, sorted, P_<uint32_t>(src));
@@ -560,53 +563,63 @@ fmm_status build_runs(fmm_ctx* ctx, cudaStream_t s) {
 
 }  // namespace
 
-fmm_status build_lists(fmm_ctx* ctx, cudaStream_t s) {
+fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append, cudaStream_t s) {
     const CellView v{P_<double4>(ctx->c_cr), P_<uint32_t>(ctx->c_cb), P_<uint32_t>(ctx->c_cc)};
     const int64_t nc = ctx->ncell;
-    int64_t n_m2l = 0, n_p2p = 0;
+    int64_t n_m2l = append ? ctx->n_m2l : 0, n_p2p = append ? ctx->n_p2p : 0;
     FMM_TRY(buf_ensure(ctx, ctx->tcnt, (size_t)nc * 2 * 4));
     uint32_t* tcnt_m2l = P_<uint32_t>(ctx->tcnt);
     uint32_t* tcnt_p2p = tcnt_m2l + nc;
     FMM_TRY(buf_ensure(ctx, ctx->dcount2, 64));
-    {
-        PhaseScope ps(ctx, PH_DTT, s);
+    PhaseScope ps(ctx, PH_DTT, s);
+    FMM_TRY(buf_ensure(ctx, ctx->fr_a, (size_t)std::max(nseeds, 128) * 8));
+    FMM_TRY(buf_ensure(ctx, ctx->dcount, 64));
+    unsigned long long* d_cnt = P_<unsigned long long>(ctx->dcount);
+    if (!append) {
         FMM_CUDA_TRY(ctx, cudaMemsetAsync(tcnt_m2l, 0, (size_t)nc * 2 * 4, s));
-        FMM_TRY(buf_ensure(ctx, ctx->fr_a, 1024 * 8));
-        FMM_TRY(buf_ensure(ctx, ctx->dcount, 64));
-        unsigned long long* d_cnt = P_<unsigned long long>(ctx->dcount);
-        k_init_frontier<<<1, 1, 0, s>>>(P_<uint64_t>(ctx->fr_a));
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt, 0, 4 * 8, s));
+    }
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->fr_a.p, seeds, (size_t)nseeds * 8, cudaMemcpyHostToDevice, s));
+    int64_t nf = nseeds;
+    while (nf > 0) {
+        // worst case per step: one list entry or 8 children per pair
+        const size_t need_m = (size_t)(n_m2l + nf) * 8, need_p = (size_t)(n_p2p + nf) * 8;
+        if (need_m > ctx->lst_m2l.bytes) FMM_TRY(buf_ensure(ctx, ctx->lst_m2l, need_m + need_m / 2, true, s));
+        if (need_p > ctx->lst_p2p.bytes) FMM_TRY(buf_ensure(ctx, ctx->lst_p2p, need_p + need_p / 2, true, s));
+        FMM_TRY(buf_ensure(ctx, ctx->fr_b, (size_t)nf * 8 * 8));
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt + 2, 0, 8, s));   // next-frontier cursor restarts
+        const int g = (int)std::min<int64_t>((nf + DT_THREADS * DT_ITEMS - 1) / (DT_THREADS * DT_ITEMS),
+                                             (int64_t)ctx->num_sms * 8);
+        k_dtt_step<<<g, DT_THREADS, 0, s>>>(P_<uint64_t>(ctx->fr_a), nf, v, ctx->theta, d_cnt, P_<uint64_t>(ctx->lst_m2l),
+                                            P_<uint64_t>(ctx->lst_p2p), P_<uint64_t>(ctx->fr_b), tcnt_m2l, tcnt_p2p);
         FMM_LAUNCH(ctx);
-        FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt, 0, 3 * 8, s));
-        int64_t nf = 1;
-        while (nf > 0) {
-            // worst case per step: one list entry or 8 children per pair
-            const size_t need_m = (size_t)(n_m2l + nf) * 8, need_p = (size_t)(n_p2p + nf) * 8;
-            if (need_m > ctx->lst_m2l.bytes) FMM_TRY(buf_ensure(ctx, ctx->lst_m2l, need_m + need_m / 2, true, s));
-            if (need_p > ctx->lst_p2p.bytes) FMM_TRY(buf_ensure(ctx, ctx->lst_p2p, need_p + need_p / 2, true, s));
-            FMM_TRY(buf_ensure(ctx, ctx->fr_b, (size_t)nf * 8 * 8));
-            FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt + 2, 0, 8, s));   // next-frontier cursor restarts
-            const int g = (int)std::min<int64_t>((nf + DT_THREADS * DT_ITEMS - 1) / (DT_THREADS * DT_ITEMS),
-                                                 (int64_t)ctx->num_sms * 8);
-            k_dtt_step<<<g, DT_THREADS, 0, s>>>(P_<uint64_t>(ctx->fr_a), nf, v, ctx->theta, d_cnt, P_<uint64_t>(ctx->lst_m2l),
-                                         P_<uint64_t>(ctx->lst_p2p), P_<uint64_t>(ctx->fr_b), tcnt_m2l, tcnt_p2p);
-            FMM_LAUNCH(ctx);
-            unsigned long long h[3];
-            FMM_CUDA_TRY(ctx, cudaMemcpyAsync(h, d_cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
-            FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-            n_m2l = (int64_t)h[0];
-            n_p2p = (int64_t)h[1];
-            nf = (int64_t)h[2];
-            std::swap(ctx->fr_a, ctx->fr_b);
+        unsigned long long h[4];
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(h, d_cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+        FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+        if (h[3]) {
+            ctx->err = "dual tree traversal needed children of a remote LET cell that were not exported";
+            return FMM_ERR_STATE;
         }
+        n_m2l = (int64_t)h[0];
+        n_p2p = (int64_t)h[1];
+        nf = (int64_t)h[2];
+        std::swap(ctx->fr_a, ctx->fr_b);
     }
     ctx->n_m2l = n_m2l;
     ctx->n_p2p = n_p2p;
+    return FMM_OK;
+}
+
+fmm_status lists_pass(fmm_ctx* ctx, cudaStream_t s) {
+    const int64_t nc = ctx->ncell;
+    uint32_t* tcnt_m2l = P_<uint32_t>(ctx->tcnt);
+    uint32_t* tcnt_p2p = tcnt_m2l + nc;
     PhaseScope ps(ctx, PH_LISTS, s);
     // P2P sources are always put in ascending order (the source runs need it); the M2L
     // segments only when canonical device order is requested (fmm_copy_lists sorts on the
     // host otherwise; the set and the grouping by target are the same either way).
-    FMM_TRY(canonicalise(ctx, ctx->lst_m2l, n_m2l, tcnt_m2l, ctx->m2l_off, ctx->m2l_src, ctx->canonical_m2l, s));
-    FMM_TRY(canonicalise(ctx, ctx->lst_p2p, n_p2p, tcnt_p2p, ctx->p2p_off, ctx->p2p_src, true, s));
+    FMM_TRY(canonicalise(ctx, ctx->lst_m2l, ctx->n_m2l, tcnt_m2l, ctx->m2l_off, ctx->m2l_src, ctx->canonical_m2l, s));
+    FMM_TRY(canonicalise(ctx, ctx->lst_p2p, ctx->n_p2p, tcnt_p2p, ctx->p2p_off, ctx->p2p_src, true, s));
     unsigned long long* d_inter = P_<unsigned long long>(ctx->dcount2) + 2;
     FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_inter, 0, 8, s));
     k_p2p_inter<<<ctx->num_sms * 4, 256, 0, s>>>(P_<uint64_t>(ctx->p2p_off), nc, P_<uint32_t>(ctx->p2p_src),
@@ -617,4 +630,10 @@ fmm_status build_lists(fmm_ctx* ctx, cudaStream_t s) {
     FMM_TRY(build_runs(ctx, s));   // synchronises s
     ctx->p2p_inter = (int64_t)inter;
     return FMM_OK;
+}
+
+fmm_status build_lists(fmm_ctx* ctx, cudaStream_t s) {
+    const uint64_t root_pair = 0;
+    FMM_TRY(dtt_pass(ctx, &root_pair, 1, false, s));
+    return lists_pass(ctx, s);
 }

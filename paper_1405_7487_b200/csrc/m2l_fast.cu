@@ -345,15 +345,17 @@ template <int P, typename R>
 fmm_status m2l_fast_t(fmm_ctx* ctx, cudaStream_t s) {
     constexpr int NSP = RF<P>::NSP, NL = RF<P>::NL;
     const int64_t nc = ctx->ncell;
-    FMM_TRY(buf_ensure(ctx, ctx->Mr, (size_t)nc * NSP * sizeof(R) + (size_t)nc * 4 + 256));
+    const int64_t nct = ctx->ncell + ctx->nrem;   // sources include grafted LET cells
+    FMM_TRY(buf_ensure(ctx, ctx->Mr, (size_t)nct * NSP * sizeof(R) + (size_t)nct * 4 + 256));
     FMM_TRY(buf_ensure(ctx, ctx->Lr, (size_t)nc * NL * 8));
     FMM_TRY(buf_ensure(ctx, ctx->cnt_tmp, 64));
     R* Sv = P_<R>(ctx->Mr);
-    int* sexp = reinterpret_cast<int*>(reinterpret_cast<char*>(ctx->Mr.p) + (size_t)nc * NSP * sizeof(R));
+    int* sexp = reinterpret_cast<int*>(reinterpret_cast<char*>(ctx->Mr.p) + (size_t)nct * NSP * sizeof(R));
     const int nw = 4;
     int g = (int)std::min<int64_t>((nc + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
-    k_m2l_prep<R><<<std::max(g, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
-        nc, P, ctx->ncoef, RF<P>::NS, NSP, P_<double>(ctx->M), P_<int32_t>(ctx->c_level), P_<double>(ctx->root), sexp,
+    const int gp = (int)std::min<int64_t>((nct + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
+    k_m2l_prep<R><<<std::max(gp, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
+        nct, P, ctx->ncoef, RF<P>::NS, NSP, P_<double>(ctx->M), P_<int32_t>(ctx->c_level), P_<double>(ctx->root), sexp,
         Sv);
     FMM_LAUNCH(ctx);
     unsigned long long* counter = P_<unsigned long long>(ctx->cnt_tmp);

@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(UP_WARPS * 32) k_m2m(int64_t cbeg, int64_t cen
 template <typename Body>
 fmm_status upward_t(fmm_ctx* ctx, cudaStream_t s) {
     PhaseScope ps(ctx, PH_UP, s);
-    const int64_t nc = ctx->ncell;
+    // remote LET cells (let.cu) take [ncell, ncell + nrem); their M arrives by fmm_let_unpack
+    const int64_t nc = ctx->ncell + ctx->nrem;
     FMM_TRY(buf_ensure(ctx, ctx->M, (size_t)nc * ctx->ncoef * 8));
     double* M = P_<double>(ctx->M);
     int g = (int)std::min<int64_t>((ctx->nleaf + P2M_WARPS - 1) / P2M_WARPS, (int64_t)ctx->num_sms * 32);

@@ -1,0 +1,325 @@
+"""Multi-GPU FMM: Morton-range partition + local essential tree (LET) exchange.
+
+One process per GPU.  Every step on the particle and tree data runs in libfmm's kernels
+(part.cu, let.cu and the single-GPU path); this module only sequences the calls and moves
+the byte messages between ranks through a `Comm`:
+
+* `TorchComm`     -- torch.distributed (NCCL on B200s: all_to_all_single with uneven splits is
+                     NCCL grouped send/recv; gloo for the CPU plumbing tests);
+* `LoopbackComm`  -- K ranks driven by ONE process on one device (single-GPU parity tests):
+                     the ranks run one after another, messages are handed over in memory.
+                     Nothing waits on another rank's kernels, so this is safe on one GPU.
+
+Collectives take and return one entry per rank this process drives.
+
+The step (§II-B/C):
+  1. global bounds = all-reduce of fmm_bounds; keys under the global root cube (R2-R4);
+  2. weighted key histogram (Eq. (1) weights; 1 at the first step),
+     all-reduced; rank j takes the bins whose cumulative weight falls in [j/K, (j+1)/K);
+  3. particles exchanged to their ranks (fmm_part_pack + all-to-all);
+  4. local tree from the LOCAL bounds; covers all-gathered; each rank packs
+     for every peer the part of its tree that peer can need (fmm_let_plan/pack_struct);
+  5. structure all-to-all in flight WHILE the local dual tree traversal runs
+     (communication overlapped with local work); graft, remote traversal
+     from (local root, remote root), canonical lists;
+  6. upward pass, multipole/charge all-to-all, unpack, M2L + P2P + downward;
+  7. results returned to the particles' owners in their original order.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .fmm import FMM
+
+HIST_BITS = 16
+
+
+# ------------------------------------------------------------------ communication
+class Comm:
+    world: int
+    ranks: list   # global ranks driven by this process
+
+    def allreduce(self, xs, op):   # op in {"sum", "min", "max"}
+        raise NotImplementedError
+
+    def allgather(self, xs):       # -> per local rank, list over all ranks
+        raise NotImplementedError
+
+    def alltoallv(self, sends, async_op=False):
+        """sends[i][j]: 1-D tensor from local rank i to global rank j.  Returns recv with
+        recv[i][j] from global rank j (or a handle whose wait() returns it)."""
+        raise NotImplementedError
+
+    def barrier(self):
+        pass
+
+
+class _Done:
+    def __init__(self, v):
+        self.v = v
+
+    def wait(self):
+        return self.v
+
+
+class LoopbackComm(Comm):
+    def __init__(self, world: int):
+        self.world = world
+        self.ranks = list(range(world))
+
+    def allreduce(self, xs, op):
+        st = torch.stack(xs)
+        r = {"sum": st.sum(0), "min": st.min(0).values, "max": st.max(0).values}[op]
+        return [r.clone() for _ in xs]
+
+    def allgather(self, xs):
+        return [list(xs) for _ in xs]
+
+    def alltoallv(self, sends, async_op=False):
+        recv = [[sends[j][i] for j in range(self.world)] for i in range(self.world)]
+        return _Done(recv) if async_op else recv
+
+
+class _A2AWork:
+    def __init__(self, work, out, sizes):
+        self.work, self.out, self.sizes = work, out, sizes
+
+    def wait(self):
+        if self.work is not None:
+            self.work.wait()
+        return [list(self.out.split(self.sizes))]
+
+
+class TorchComm(Comm):
+    """One rank per process over an initialised torch.distributed process group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.world = dist.get_world_size(group)
+        self.ranks = [dist.get_rank(group)]
+
+    def allreduce(self, xs, op):
+        d = self.dist
+        t = xs[0].clone()
+        d.all_reduce(t, op={"sum": d.ReduceOp.SUM, "min": d.ReduceOp.MIN, "max": d.ReduceOp.MAX}[op], group=self.group)
+        return [t]
+
+    def allgather(self, xs):
+        out = [torch.empty_like(xs[0]) for _ in range(self.world)]
+        self.dist.all_gather(out, xs[0].contiguous(), group=self.group)
+        return [out]
+
+    def alltoallv(self, sends, async_op=False):
+        s = sends[0]
+        dev = s[0].device
+        in_sizes = [int(t.numel()) for t in s]
+        out_sz = torch.empty(self.world, dtype=torch.int64, device=dev)
+        self.dist.all_to_all_single(out_sz, torch.tensor(in_sizes, dtype=torch.int64, device=dev), group=self.group)
+        sizes = [int(v) for v in out_sz.tolist()]
+        inp = torch.cat([t.reshape(-1) for t in s])
+        out = torch.empty(sum(sizes), dtype=s[0].dtype, device=dev)
+        work = self.dist.all_to_all_single(out, inp, output_split_sizes=sizes, input_split_sizes=in_sizes,
+                                           group=self.group, async_op=async_op)
+        h = _A2AWork(work if async_op else None, out, sizes)
+        return h if async_op else h.wait()
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+
+# ------------------------------------------------------------------ host logic
+def choose_bins(hist: np.ndarray, targets: np.ndarray):
+    """For each target weight t (measured from the start of this histogram): the bin where
+    the inclusive cumulative weight first reaches t, and the weight still needed inside it."""
+    c = np.cumsum(np.asarray(hist, dtype=np.float64))
+    b = np.minimum(np.searchsorted(c, targets, side="left"), len(c) - 1)
+    before = np.where(b > 0, c[np.maximum(b - 1, 0)], 0.0)
+    return b.astype(np.int64), np.asarray(targets, dtype=np.float64) - before
+
+
+def partition_splitters(hist_fn, nranks: int, bits: int = HIST_BITS, tol: float = 1.0 / 512):
+    """Morton-range splitters by histogram refinement ("HOT is analogous to radix
+    sort, where each bit of the key is examined at each step"; Eq. (1) weights).
+
+    hist_fn(prefixes, prefix_bits, bits) -> [len(prefixes), 2^bits] GLOBAL (all-reduced)
+    weights of the keys under each prefix.  Splitter j (1 <= j < K) is refined, `bits` key
+    bits per round, down to the bin where the cumulative weight crosses j/K of the total,
+    until that bin holds <= tol * total / K or the key is exhausted; rank j takes the keys
+    >= splitter j.  Returns the K-1 splitter keys (uint64, non-decreasing)."""
+    K = nranks
+    if K <= 1:
+        return np.zeros(0, dtype=np.uint64)
+    h0 = np.asarray(hist_fn([0], 0, bits))[0]
+    total = float(h0.sum())
+    if total <= 0:
+        return np.zeros(K - 1, dtype=np.uint64)
+    b, resid = choose_bins(h0, total * np.arange(1, K) / K)
+    prefix = [int(x) for x in b]
+    weight = h0[b]
+    pbits = bits
+    while pbits < 63 and np.any(weight > tol * total / K):
+        nb = min(bits, 63 - pbits)
+        hs = np.asarray(hist_fn(prefix, pbits, nb))
+        for j in range(K - 1):
+            bj, rj = choose_bins(hs[j], resid[j:j + 1])
+            prefix[j] = (prefix[j] << nb) | int(bj[0])
+            resid[j] = rj[0]
+            weight[j] = hs[j][bj[0]]
+        pbits += nb
+    out = np.array([p << (63 - pbits) for p in prefix], dtype=np.uint64)
+    return np.maximum.accumulate(out)
+
+
+# ------------------------------------------------------------------ driver
+class DistFMM:
+    """The FMM on `comm.world` ranks; this process drives the ranks `comm.ranks`.
+
+    solve(pos[i], q[i], gid_base[i], w[i]) for every local rank i (device tensors of the
+    contexts' precision) returns phi[i], grad[i] in the caller's particle order."""
+
+    def __init__(self, comm: Comm, n_max: int, P: int, theta: float, ncrit: int, prec: str = "f32",
+                 device: int = 0, hist_bits: int = HIST_BITS):
+        self.comm, self.K = comm, comm.world
+        self.fmm = [FMM(n_max, P, theta, ncrit, prec, device) for _ in comm.ranks]
+        self.hist_bits = hist_bits
+        self.stats = {}
+
+    def close(self):
+        for f in self.fmm:
+            f.close()
+
+    # 1-3: partition
+    def partition(self, pos, q, gid_base, w=None):
+        cm, K, F = self.comm, self.K, self.fmm
+        nl = len(F)
+        b = [torch.from_numpy(f.bounds(p)) for f, p in zip(F, pos)]
+        lo = cm.allreduce([x[:3].clone() for x in b], "min")
+        hi = cm.allreduce([x[3:].clone() for x in b], "max")
+        gb = [torch.cat([lo[i], hi[i]]).numpy() for i in range(nl)]
+        keys = [F[i].part_keys(pos[i], gb[i]) for i in range(nl)]
+
+        def hist_fn(prefixes, pbits, bits):
+            loc = []
+            for i in range(nl):
+                h = torch.empty((len(prefixes), 1 << bits), dtype=torch.float64, device=keys[i].device)
+                for r, pre in enumerate(prefixes):
+                    F[i].part_histogram(keys[i], None if w is None else w[i], bits, pre, pbits, out=h[r])
+                loc.append(h)
+            return cm.allreduce(loc, "sum")[0].cpu().numpy()
+
+        s = partition_splitters(hist_fn, K, self.hist_bits)
+        spl = [s for _ in range(nl)]
+        packed = [F[i].part_pack(pos[i], q[i], keys[i], spl[i], K, gid_base[i]) for i in range(nl)]
+        cnt = [p[3] for p in packed]
+        sp = cm.alltoallv([list(packed[i][0].reshape(-1).split((cnt[i] * 3).tolist())) for i in range(nl)])
+        sq = cm.alltoallv([list(packed[i][1].split(cnt[i].tolist())) for i in range(nl)])
+        sg = cm.alltoallv([list(packed[i][2].split(cnt[i].tolist())) for i in range(nl)])
+        lpos = [torch.cat(sp[i]).reshape(-1, 3).contiguous() for i in range(nl)]
+        lq = [torch.cat(sq[i]).contiguous() for i in range(nl)]
+        lgid = [torch.cat(sg[i]) for i in range(nl)]
+        back = [[int(t.numel()) for t in sq[i]] for i in range(nl)]   # segment sizes per source rank
+        return lpos, lq, lgid, back, packed, cnt
+
+    # 4-5: local trees, LET structure, traversal
+    def build(self, lpos):
+        cm, K, F = self.comm, self.K, self.fmm
+        nl = len(F)
+        dev = lpos[0].device
+        for f, p in zip(F, lpos):
+            f.build_tree(p)
+        cov = []
+        for f in F:
+            c = f.let_cover()
+            t = torch.zeros(1 + 8 * 73, dtype=torch.float64)
+            t[0] = len(c)
+            t[1:1 + c.size] = torch.from_numpy(c.reshape(-1))
+            cov.append(t.to(dev))
+        allcov = cm.allgather(cov)
+        self._dbytes = []
+        sends = []
+        for i, f in enumerate(F):
+            me = cm.ranks[i]
+            row, db = [], []
+            for j in range(K):
+                if j == me:
+                    row.append(torch.empty(0, dtype=torch.uint8, device=dev))
+                    db.append(0)
+                    continue
+                cj = allcov[i][j].cpu().numpy()
+                sb, d = f.let_plan(j, cj[1:1 + 8 * int(cj[0])].reshape(-1, 8))
+                buf = torch.empty(sb, dtype=torch.uint8, device=dev)
+                if sb:
+                    f.let_pack_struct(j, buf)
+                row.append(buf)
+                db.append(d)
+            sends.append(row)
+            self._dbytes.append(db)
+        h = cm.alltoallv(sends, async_op=True)
+        for f in F:                       # local traversal overlaps the LET structure exchange
+            f.dtt(remote=False)
+        recv = h.wait()
+        self._peers = []
+        for i, f in enumerate(F):
+            me = cm.ranks[i]
+            peers = [j for j in range(K) if j != me and recv[i][j].numel() > 0]
+            self._peers.append(peers)
+            f.let_graft([recv[i][j] for j in peers])
+            f.dtt(remote=True)
+            f.make_lists()
+        self.stats["let_struct_bytes"] = sum(int(t.numel()) for row in sends for t in row)
+
+    # 6: upward, LET data, interactions
+    def evaluate(self, lpos, lq):
+        cm, K, F = self.comm, self.K, self.fmm
+        dev = lpos[0].device
+        sends = []
+        for i, f in enumerate(F):
+            f.upward(lpos[i], lq[i])
+            me = cm.ranks[i]
+            row = []
+            for j in range(K):
+                d = self._dbytes[i][j]
+                buf = torch.empty(d, dtype=torch.uint8, device=dev)
+                if d and j != me:
+                    f.let_pack_data(j, buf)
+                row.append(buf)
+            sends.append(row)
+        recv = cm.alltoallv(sends)
+        out = []
+        for i, f in enumerate(F):
+            f.let_unpack([recv[i][j] for j in self._peers[i]])
+            n = lpos[i].shape[0]
+            phi = torch.empty(n, dtype=f.dtype, device=dev)
+            grad = torch.empty((n, 3), dtype=f.dtype, device=dev)
+            f.interact(phi, grad)
+            out.append((phi, grad))
+        self.stats["let_data_bytes"] = sum(int(t.numel()) for row in sends for t in row)
+        return out
+
+    # 7: results back to the owners, original order
+    def gather_back(self, res, back, packed, cnt, gid_base, n_in):
+        cm = self.comm
+        nl = len(self.fmm)
+        sends = []
+        for i in range(nl):
+            phi, grad = res[i]
+            v = torch.cat([phi.reshape(-1, 1), grad], dim=1)   # [n, 4]
+            sends.append(list(v.reshape(-1).split([4 * s for s in back[i]])))
+        recv = cm.alltoallv(sends)
+        out = []
+        for i in range(nl):
+            v = torch.cat(recv[i]).reshape(-1, 4)              # in this rank's packed order
+            idx = packed[i][2] - gid_base[i]                    # original local index
+            r = torch.empty((n_in[i], 4), dtype=v.dtype, device=v.device)
+            r[idx] = v
+            out.append((r[:, 0].contiguous(), r[:, 1:].contiguous()))
+        return out
+
+    def solve(self, pos, q, gid_base, w=None):
+        lpos, lq, lgid, back, packed, cnt = self.partition(pos, q, gid_base, w)
+        self.build(lpos)
+        res = self.evaluate(lpos, lq)
+        self.local = (lpos, lq, lgid)
+        return self.gather_back(res, back, packed, cnt, gid_base, [p.shape[0] for p in pos])

@@ -39,7 +39,24 @@ SYMBOLS = {
     "fmm_phase_times": (_i, [_p, _p, _i, _p, _i]),
     "fmm_phase_name": (C.c_char_p, [_i]),
     "fmm_launch_count": (_i64, [_p, _i]),
+    "fmm_build_tree": (_i, [_p, _p, _i64, _p]),
+    "fmm_dtt": (_i, [_p, _i, _p]),
+    "fmm_lists": (_i, [_p, _p]),
+    "fmm_upward": (_i, [_p, _p, _p, _p]),
+    "fmm_interact": (_i, [_p, _p, _p, _p]),
+    "fmm_bounds": (_i, [_p, _p, _i64, _p, _p]),
+    "fmm_part_keys": (_i, [_p, _p, _i64, _p, _p, _p]),
+    "fmm_part_histogram": (_i, [_p, _p, _p, _i64, C.c_uint64, _i, _i, _p, _p]),
+    "fmm_part_pack": (_i, [_p, _p, _p, _p, _i64, _p, _i, _i64, _p, _p, _p, _p, _p]),
+    "fmm_let_cover": (_i, [_p, _p, _p, _p]),
+    "fmm_let_plan": (_i, [_p, _i, _p, _i, _p, _p, _p]),
+    "fmm_let_pack_struct": (_i, [_p, _i, _p, _p]),
+    "fmm_let_pack_data": (_i, [_p, _i, _p, _p]),
+    "fmm_let_graft": (_i, [_p, _i, _p, _p, _p]),
+    "fmm_let_unpack": (_i, [_p, _i, _p, _p, _p]),
+    "fmm_let_remote": (_i, [_p, _i, _p, _p, _p, _p]),
 }
+LET_MAX_COVER = 73
 
 _lib = None
 
@@ -162,6 +179,130 @@ class FMM:
                     "fmm_solve_host")
         self._pos = None
         return phi, grad
+
+    # -- the path in halves (multi-GPU: LET grafted between tree and traversal) --
+    def build_tree(self, pos, stream=None):
+        n = pos.shape[0]
+        self._check_tensor(pos, (n, 3), "pos")
+        self._check(lib().fmm_build_tree(self._h, C.c_void_p(pos.data_ptr()), n, C.c_void_p(self._stream(stream))),
+                    "fmm_build_tree")
+        self._pos = pos
+        self.n = n
+        return self
+
+    def dtt(self, remote: bool = False, stream=None):
+        self._check(lib().fmm_dtt(self._h, int(remote), C.c_void_p(self._stream(stream))), "fmm_dtt")
+
+    def make_lists(self, stream=None):
+        self._check(lib().fmm_lists(self._h, C.c_void_p(self._stream(stream))), "fmm_lists")
+
+    def upward(self, pos, q, stream=None):
+        n = pos.shape[0]
+        self._check_tensor(q, (n,), "q")
+        self._check(lib().fmm_upward(self._h, C.c_void_p(pos.data_ptr()), C.c_void_p(q.data_ptr()),
+                                     C.c_void_p(self._stream(stream))), "fmm_upward")
+
+    def interact(self, phi, grad, stream=None):
+        n = phi.shape[0]
+        self._check_tensor(phi, (n,), "phi")
+        self._check_tensor(grad, (n, 3), "grad")
+        self._check(lib().fmm_interact(self._h, C.c_void_p(phi.data_ptr()), C.c_void_p(grad.data_ptr()),
+                                       C.c_void_p(self._stream(stream))), "fmm_interact")
+        return phi, grad
+
+    # -- multi-GPU: partition (part.cu) --------------------------------------
+    def bounds(self, pos, stream=None) -> np.ndarray:
+        n = pos.shape[0]
+        self._check_tensor(pos, (n, 3), "pos")
+        out = np.zeros(6)
+        self._check(lib().fmm_bounds(self._h, C.c_void_p(pos.data_ptr()), n, _np_ptr(out),
+                                     C.c_void_p(self._stream(stream))), "fmm_bounds")
+        return out
+
+    def part_keys(self, pos, bounds: np.ndarray, stream=None):
+        """Morton keys under the root cube of the global bounds (int64 tensor holding u64 bits)."""
+        import torch
+        n = pos.shape[0]
+        self._check_tensor(pos, (n, 3), "pos")
+        b = np.ascontiguousarray(bounds, dtype=np.float64)
+        keys = torch.empty(n, dtype=torch.int64, device=pos.device)
+        self._check(lib().fmm_part_keys(self._h, C.c_void_p(pos.data_ptr()), n, _np_ptr(b), C.c_void_p(keys.data_ptr()),
+                                        C.c_void_p(self._stream(stream))), "fmm_part_keys")
+        return keys
+
+    def part_histogram(self, keys, w=None, bits: int = 16, prefix: int = 0, prefix_bits: int = 0, out=None,
+                       stream=None):
+        import torch
+        hist = torch.empty(1 << bits, dtype=torch.float64, device=keys.device) if out is None else out
+        wp = None if w is None else C.c_void_p(w.data_ptr())
+        self._check(lib().fmm_part_histogram(self._h, C.c_void_p(keys.data_ptr()), wp, keys.shape[0], int(prefix),
+                                             int(prefix_bits), bits, C.c_void_p(hist.data_ptr()),
+                                             C.c_void_p(self._stream(stream))), "fmm_part_histogram")
+        return hist
+
+    def part_pack(self, pos, q, keys, splitters: np.ndarray, nranks: int, gid_base: int, stream=None):
+        import torch
+        n = pos.shape[0]
+        self._check_tensor(pos, (n, 3), "pos")
+        self._check_tensor(q, (n,), "q")
+        spl = np.ascontiguousarray(splitters, dtype=np.uint64)
+        opos = torch.empty_like(pos); oq = torch.empty_like(q)
+        gid = torch.empty(n, dtype=torch.int64, device=pos.device)
+        counts = np.zeros(nranks, np.int64)
+        self._check(lib().fmm_part_pack(self._h, C.c_void_p(pos.data_ptr()), C.c_void_p(q.data_ptr()),
+                                        C.c_void_p(keys.data_ptr()), n, _np_ptr(spl), int(nranks), int(gid_base),
+                                        C.c_void_p(opos.data_ptr()), C.c_void_p(oq.data_ptr()),
+                                        C.c_void_p(gid.data_ptr()), _np_ptr(counts), C.c_void_p(self._stream(stream))),
+                    "fmm_part_pack")
+        return opos, oq, gid, counts
+
+    # -- multi-GPU: local essential tree (let.cu) -------------------------------
+    def let_cover(self, stream=None) -> np.ndarray:
+        cov = np.zeros((LET_MAX_COVER, 8)); k = C.c_int()
+        self._check(lib().fmm_let_cover(self._h, _np_ptr(cov), C.byref(k), C.c_void_p(self._stream(stream))),
+                    "fmm_let_cover")
+        return cov[:k.value].copy()
+
+    def let_plan(self, peer: int, cover: np.ndarray, stream=None):
+        cov = np.ascontiguousarray(cover, dtype=np.float64).reshape(-1, 8)
+        sb, db = C.c_int64(), C.c_int64()
+        self._check(lib().fmm_let_plan(self._h, int(peer), _np_ptr(cov) if len(cov) else None, len(cov),
+                                       C.byref(sb), C.byref(db), C.c_void_p(self._stream(stream))), "fmm_let_plan")
+        return int(sb.value), int(db.value)
+
+    def let_pack_struct(self, peer: int, dst, stream=None):
+        self._check(lib().fmm_let_pack_struct(self._h, int(peer), C.c_void_p(dst.data_ptr()),
+                                              C.c_void_p(self._stream(stream))), "fmm_let_pack_struct")
+
+    def let_pack_data(self, peer: int, dst, stream=None):
+        self._check(lib().fmm_let_pack_data(self._h, int(peer), C.c_void_p(dst.data_ptr()),
+                                            C.c_void_p(self._stream(stream))), "fmm_let_pack_data")
+
+    @staticmethod
+    def _buf_arrays(bufs):
+        ptrs = (C.c_void_p * max(len(bufs), 1))(*[b.data_ptr() for b in bufs])
+        sizes = (C.c_int64 * max(len(bufs), 1))(*[b.numel() * b.element_size() for b in bufs])
+        return ptrs, sizes
+
+    def let_graft(self, bufs, stream=None):
+        ptrs, sizes = self._buf_arrays(bufs)
+        self._check(lib().fmm_let_graft(self._h, len(bufs), ptrs, sizes, C.c_void_p(self._stream(stream))),
+                    "fmm_let_graft")
+
+    def let_unpack(self, bufs, stream=None):
+        ptrs, sizes = self._buf_arrays(bufs)
+        self._check(lib().fmm_let_unpack(self._h, len(bufs), ptrs, sizes, C.c_void_p(self._stream(stream))),
+                    "fmm_let_unpack")
+
+    def let_remote(self, k: int, with_orig: bool = True):
+        base, nc, nb = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(lib().fmm_let_remote(self._h, int(k), C.byref(base), C.byref(nc), C.byref(nb), None),
+                    "fmm_let_remote")
+        orig = None
+        if with_orig:
+            orig = np.zeros(nc.value, np.uint32)
+            self._check(lib().fmm_let_remote(self._h, int(k), None, None, None, _np_ptr(orig)), "fmm_let_remote")
+        return int(base.value), int(nc.value), int(nb.value), orig
 
     # -- introspection -----------------------------------------------------
     def counts(self) -> dict:

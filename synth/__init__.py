@@ -40,18 +40,22 @@ def uniform01(seed: int, counters: np.ndarray) -> np.ndarray:
     return (splitmix64(seed, counters) >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
 
 
-def _draws(n: int, seed: int) -> np.ndarray:
-    c = np.arange(4 * n, dtype=np.uint64)
+def _draws(n: int, seed: int, start: int = 0) -> np.ndarray:
+    c = np.arange(4 * start, 4 * (start + n), dtype=np.uint64)
     return uniform01(seed, c).reshape(n, 4)
 
 
-def generate(kind: str, n: int, seed: int, dtype=np.float64):
-    """Return (pos[n,3], q[n]) as C-contiguous arrays of `dtype` (float64 or float32)."""
+def generate(kind: str, n: int, seed: int, dtype=np.float64, start: int = 0, n_total: int = None):
+    """Return (pos[n,3], q[n]) as C-contiguous arrays of `dtype` (float64 or float32).
+
+    Particles start .. start+n-1 of an n_total-particle set (default: the whole set of n),
+    so that ranks of a multi-GPU run can each draw their own slice of one global set."""
     if kind not in KINDS:
         raise ValueError(f"unknown distribution {kind!r}; expected one of {KINDS}")
-    if n < 0:
-        raise ValueError("n must be >= 0")
-    u = _draws(n, seed)
+    if n < 0 or start < 0:
+        raise ValueError("n and start must be >= 0")
+    n_total = n if n_total is None else n_total
+    u = _draws(n, seed, start)
     if kind == "cube":
         pos = u[:, :3].copy()
         q = 2.0 * u[:, 3] - 1.0
@@ -68,7 +72,7 @@ def generate(kind: str, n: int, seed: int, dtype=np.float64):
             m = u[:, 0] * mmax
             with np.errstate(divide="ignore"):
                 r = np.where(m > 0.0, 1.0 / np.sqrt(np.maximum(m, 1e-300) ** (-2.0 / 3.0) - 1.0), 0.0)
-            q = np.full(n, 1.0 / max(n, 1))
+            q = np.full(n, 1.0 / max(n_total, 1))
         pos = np.stack([r * sth * np.cos(ph), r * sth * np.sin(ph), r * cth], axis=1)
     pos = np.ascontiguousarray(pos.astype(dtype))
     q = np.ascontiguousarray(q.astype(dtype))

@@ -1,0 +1,129 @@
+"""Host-side logic of the multi-GPU path on CPU (no GPU): the splitter rule, and the
+TorchComm collectives over a world_size-2 gloo group -- the same calls the NCCL run makes
+(all_reduce, all_gather, all_to_all_single with uneven splits) -- checked against the
+in-process LoopbackComm the single-GPU tests use.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+from paper_1405_7487_b200.dist import LoopbackComm, TorchComm, choose_bins, partition_splitters
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _host_hist_fn(keys, w=None):
+    """numpy stand-in for the all-reduced device histogram (same binning as fmm_part_histogram)."""
+    w = np.ones(len(keys)) if w is None else w
+
+    def fn(prefixes, pbits, bits):
+        out = np.zeros((len(prefixes), 1 << bits))
+        lo = np.uint64(63 - pbits - bits)
+        for r, pre in enumerate(prefixes):
+            sel = np.ones(len(keys), bool) if pbits == 0 else (keys >> np.uint64(63 - pbits)) == np.uint64(pre)
+            b = ((keys[sel] >> lo) & np.uint64((1 << bits) - 1)).astype(np.int64)
+            out[r] = np.bincount(b, weights=w[sel], minlength=1 << bits)
+        return out
+    return fn
+
+
+def test_choose_bins():
+    b, r = choose_bins(np.array([1.0, 0.0, 3.0, 2.0]), np.array([0.5, 1.0, 2.5, 6.0]))
+    np.testing.assert_array_equal(b, [0, 0, 2, 3])
+    np.testing.assert_array_equal(r, [0.5, 1.0, 1.5, 2.0])
+
+
+@pytest.mark.parametrize("kind", ["cube", "plummer"])
+def test_partition_gives_balanced_morton_ranges(kind):
+    # Plummer: the top 16 key bits put most particles in a few bins; refinement splits them
+    pos, _ = synth.generate(kind, 20000, 5)
+    k = oracle.keys(pos)
+    order = np.argsort(k, kind="stable")
+    for K in (1, 2, 3, 4, 8):
+        spl = partition_splitters(_host_hist_fn(k), K)
+        assert len(spl) == K - 1 and np.all(np.diff(spl.astype(np.float64)) >= 0)
+        dest = np.searchsorted(spl, k, side="right")     # = number of splitters <= key
+        assert np.all(np.diff(dest[order]) >= 0)           # contiguous along the Morton curve
+        cnt = np.bincount(dest, minlength=K)
+        assert np.abs(cnt - len(pos) / K).max() <= 0.01 * len(pos) / K + 1, cnt
+
+
+def test_partition_weighted():
+    # Eq. (1): weights move the cuts -- heavy particles get ranks of their own
+    pos, _ = synth.generate("cube", 4000, 6)
+    k = oracle.keys(pos)
+    w = np.where(pos[:, 0] < 0.25, 9.0, 1.0)
+    spl = partition_splitters(_host_hist_fn(k, w), 4)
+    dest = np.searchsorted(spl, k, side="right")
+    share = np.array([w[dest == j].sum() for j in range(4)]) / w.sum()
+    assert np.abs(share - 0.25).max() < 0.01, share
+
+
+def test_partition_degenerate():
+    k = np.full(100, np.uint64(12345), dtype=np.uint64)   # coincident particles: one key
+    spl = partition_splitters(_host_hist_fn(k), 4)
+    dest = np.searchsorted(spl, k, side="right")
+    assert len(np.unique(dest)) == 1                        # equal keys never split
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cm = TorchComm()
+        x = torch.tensor([1.0 + rank, -2.0 * rank, 5.0])
+        s = cm.allreduce([x], "sum")[0].tolist()
+        mn = cm.allreduce([x], "min")[0].tolist()
+        mx = cm.allreduce([x], "max")[0].tolist()
+        g = [t.tolist() for t in cm.allgather([torch.arange(3, dtype=torch.float64) + 10 * rank])[0]]
+        # uneven byte messages: rank r sends r*3 + j + 1 bytes to rank j, valued 16*r + j
+        sends = [torch.full((rank * 3 + j + 1,), 16 * rank + j, dtype=torch.uint8) for j in range(world)]
+        recv = [t.tolist() for t in cm.alltoallv([sends])[0]]
+        h = cm.alltoallv([sends], async_op=True)
+        recv2 = [t.tolist() for t in h.wait()[0]]
+        q.put((rank, s, mn, mx, g, recv, recv2))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_torchcomm_gloo_matches_loopback():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r = q.get(timeout=120)
+        res[r[0]] = r
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # the same collectives in-process
+    lb = LoopbackComm(world)
+    xs = [torch.tensor([1.0 + r, -2.0 * r, 5.0]) for r in range(world)]
+    sends = [[torch.full((r * 3 + j + 1,), 16 * r + j, dtype=torch.uint8) for j in range(world)] for r in range(world)]
+    ls = lb.allreduce(xs, "sum"); lmn = lb.allreduce(xs, "min"); lmx = lb.allreduce(xs, "max")
+    lg = lb.allgather([torch.arange(3, dtype=torch.float64) + 10 * r for r in range(world)])
+    lr = lb.alltoallv(sends)
+    for r in range(world):
+        _, s, mn, mx, g, recv, recv2 = res[r]
+        assert s == ls[r].tolist() and mn == lmn[r].tolist() and mx == lmx[r].tolist()
+        assert g == [t.tolist() for t in lg[r]]
+        assert recv == [t.tolist() for t in lr[r]] == recv2
+        assert recv[1 - r] == [16 * (1 - r) + r] * ((1 - r) * 3 + r + 1)

@@ -1,0 +1,137 @@
+"""Multi-GPU path on ONE GPU: K ranks driven by one process (LoopbackComm),
+checked against the oracle's per-partition mode (oracle.traverse_pair / evaluate_multi).
+
+Bar: rank i's lists over (local tree + grafted LETs) equal the oracle's
+lists of T_i against every full local tree S_j, bit-exact (remote sources mapped back to the
+sender's cell ids); phi / grad against evaluate_multi at the §8(c) tolerances.  The ranks
+run one after another: no kernel waits on another rank's kernel.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": 1e-12, "f32": 1e-5}
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1405_7487_b200 import build
+    build.build()
+    return torch
+
+
+def run_dist(torch, kind, n, K, P, theta, ncrit, prec, seed):
+    from paper_1405_7487_b200.dist import DistFMM, LoopbackComm
+    dt = np.float32 if prec == "f32" else np.float64
+    tdt = torch.float32 if prec == "f32" else torch.float64
+    pos, q = synth.generate(kind, n, seed, dt)
+    # initial ownership: contiguous index slices (not spatial), as a user would hold them
+    cuts = np.linspace(0, n, K + 1).astype(int)
+    P_in = [torch.from_numpy(pos[cuts[r]:cuts[r + 1]]).cuda() for r in range(K)]
+    Q_in = [torch.from_numpy(q[cuts[r]:cuts[r + 1]]).cuda() for r in range(K)]
+    D = DistFMM(LoopbackComm(K), n, P, theta, ncrit, prec)
+    out = D.solve(P_in, Q_in, [int(c) for c in cuts[:-1]])
+    torch.cuda.synchronize()
+    phi = np.concatenate([o[0].cpu().numpy() for o in out]).astype(np.float64)
+    grad = np.concatenate([o[1].cpu().numpy() for o in out]).astype(np.float64)
+    return D, pos, q, phi, grad
+
+
+CASES = [
+    # kind, n, K, P, theta, ncrit, prec
+    ("cube", 6000, 2, 4, 0.5, 32, "f64"),
+    ("cube", 9000, 3, 6, 0.4, 16, "f64"),
+    ("plummer", 8000, 4, 5, 0.5, 16, "f64"),
+    ("cube", 20000, 4, 10, 0.4, 64, "f32"),
+    ("plummer", 12000, 3, 10, 0.4, 64, "f32"),
+    ("sphere", 5000, 2, 4, 0.6, 8, "f32"),
+]
+
+
+@pytest.mark.parametrize("kind,n,K,P,theta,ncrit,prec", CASES)
+def test_dist_lists_and_fields(torch_cuda, kind, n, K, P, theta, ncrit, prec):
+    D, pos, q, phi, grad = run_dist(torch_cuda, kind, n, K, P, theta, ncrit, prec, 500 + n + K)
+    lpos, lq, lgid = D.local
+    gids = [g.cpu().numpy() for g in lgid]
+    # every particle lands on exactly one rank, and the ranks are Morton ranges of similar size
+    allg = np.sort(np.concatenate(gids))
+    np.testing.assert_array_equal(allg, np.arange(n))
+    sizes = np.array([len(g) for g in gids])
+    assert sizes.min() >= 0.5 * n / K, sizes
+    # oracle trees of every rank, built from the rank's particles in the order the rank holds them
+    O = [oracle.FMM(pos[g].astype(np.float64), q[g].astype(np.float64), P, theta, ncrit) for g in gids]
+    for i in range(K):
+        f = D.fmm[i]
+        m2l, p2p = f.lists()
+        nci = f.counts()["ncell"]
+        peers = D._peers[i]
+        regions = [f.let_remote(k) for k in range(len(peers))]
+
+        def split(lst):
+            loc = lst[lst[:, 1] < nci]
+            rem = {}
+            for k, j in enumerate(peers):
+                base, ncl, _, orig = regions[k]
+                sel = (lst[:, 1] >= base) & (lst[:, 1] < base + ncl)
+                r = lst[sel].copy()
+                r[:, 1] = orig[r[:, 1] - base]
+                rem[j] = r
+            assert len(loc) + sum(len(r) for r in rem.values()) == len(lst)
+            return loc, rem
+
+        lm, rm = split(m2l)
+        lp_, rp = split(p2p)
+        om, op = O[i].traverse().lists()
+        np.testing.assert_array_equal(lm, om)
+        np.testing.assert_array_equal(lp_, op)
+        for j in range(K):
+            if j == i:
+                continue
+            tm, tp = oracle.traverse_pair(O[i], O[j])
+            gm = rm.get(j, np.zeros((0, 2), np.uint32))
+            gp = rp.get(j, np.zeros((0, 2), np.uint32))
+            np.testing.assert_array_equal(gm, tm, err_msg=f"M2L rank {i} <- {j}")
+            np.testing.assert_array_equal(gp, tp, err_msg=f"P2P rank {i} <- {j}")
+    # fields: rank-local results against the oracle's multi-tree evaluation, and the gathered
+    # (original-order) results against the same numbers
+    ref_phi = np.zeros(n); ref_grad = np.zeros((n, 3))
+    for i in range(K):
+        o_phi, o_grad = oracle.evaluate_multi(O[i], [O[j] for j in range(K) if j != i])
+        ref_phi[gids[i]] = o_phi
+        ref_grad[gids[i]] = o_grad
+    assert oracle.rel_l2(phi, ref_phi) <= TOL[prec]
+    assert oracle.rel_l2(grad, ref_grad) <= TOL[prec]
+    # and the whole-system FMM is an approximation of the direct sum
+    t = synth.sample_targets(n, 200, 7)
+    dp, dg = oracle.direct(pos.astype(np.float64), q.astype(np.float64), t)
+    assert oracle.rel_l2(phi[t], dp) <= 1e-2 and oracle.rel_l2(grad[t], dg) <= 5e-2
+
+
+def test_dist_single_rank_equals_single_gpu(torch_cuda):
+    """K = 1: partition + LET machinery reduce to the single-GPU path, bit for bit."""
+    import torch
+    from paper_1405_7487_b200 import FMM
+    D, pos, q, phi, grad = run_dist(torch, "cube", 5000, 1, 6, 0.5, 32, "f64", 11)
+    f = FMM(5000, 6, 0.5, 32, "f64")
+    p1, g1 = f.solve(torch.from_numpy(pos).cuda(), torch.from_numpy(q).cuda())
+    np.testing.assert_array_equal(phi, p1.cpu().numpy())
+    np.testing.assert_array_equal(grad, g1.cpu().numpy())
+
+
+def test_let_needs_subset_of_remote_tree(torch_cuda):
+    """The LET a rank receives is a strict subset of the sender's tree (far cells are cut)."""
+    D, pos, q, phi, grad = run_dist(torch_cuda, "cube", 30000, 4, 4, 0.5, 16, "f64", 21)
+    for i in range(4):
+        f = D.fmm[i]
+        for k, j in enumerate(D._peers[i]):
+            _, ncl, nbd, orig = f.let_remote(k)
+            assert ncl < D.fmm[j].counts()["ncell"]
+            assert nbd < D.fmm[j].counts()["n"]
+            assert np.all(np.diff(orig.astype(np.int64)) > 0)   # sender order kept
