@@ -10,8 +10,11 @@ CUDA events on the stream the library runs on.
 
   python bench.py [--gpus N --steps K --warmup W] [--config c2|c3|c1] [--impl reference]
 
-Multi-GPU (torchrun): every rank solves its own instance (weak scaling, no collective on the
-data path: replicas until the LET exchange lands); max time over ranks.
+Multi-GPU (torchrun, --gpus N > 1): ONE FMM over N x 2^20 particles (weak scaling: each rank
+starts with its 2^20-particle slice of one global cube set), solved by the distributed path
+(paper_1405_7487_b200/dist.py over NCCL): Morton-range partition, local trees, LET exchange
+overlapped with the local traversal, remote traversal, M2L/P2P, results back to the owners.
+Step time = max over ranks of the CUDA-event time around the whole distributed solve.
 """
 from __future__ import annotations
 
@@ -162,7 +165,7 @@ def run_reference(args, cfg, rank, world):
     line = {"metric": METRIC, "impl": "reference", "value": n / t, "unit": "particles/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(cfg, args),
+            "config": workload_config(cfg, args, world),
             "cpu_baseline": {"value": n / t, "unit": "particles/s", "cores": 1, "kind": "oracle",
                              "sample": f"full oracle FMM on {n} particles of the workload's distribution and "
                                        f"parameters per step"},
@@ -170,12 +173,141 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(cfg, args):
-    return {"workload": f"BASELINE.json {CONFIG_NAMES[args.config]}: 3D Laplace FMM, N={cfg['n']} {cfg['kind']}, "
-                        f"{cfg['prec']}, P={cfg['P']}, theta={cfg['theta']}, ncrit={cfg['ncrit']}",
-            "N": cfg["n"], "distribution": cfg["kind"], "P": cfg["P"], "theta": cfg["theta"], "ncrit": cfg["ncrit"],
-            "precision": cfg["prec"], "seed": cfg["seed"], "l2": "flushed (256 MB write) before every timed step",
-            "parallelism": f"{args.gpus} independent replica(s), one per GPU" if args.gpus > 1 else "1 GPU"}
+def workload_config(cfg, args, world=1):
+    n = cfg["n"] * world
+    d = {"workload": f"BASELINE.json {CONFIG_NAMES[args.config]}: 3D Laplace FMM, N={n} {cfg['kind']}, "
+                     f"{cfg['prec']}, P={cfg['P']}, theta={cfg['theta']}, ncrit={cfg['ncrit']}",
+         "N": n, "distribution": cfg["kind"], "P": cfg["P"], "theta": cfg["theta"], "ncrit": cfg["ncrit"],
+         "precision": cfg["prec"], "seed": cfg["seed"], "l2": "flushed (256 MB write) before every timed step",
+         "parallelism": "1 GPU"}
+    if world > 1:
+        d["parallelism"] = (f"{world} GPUs, one FMM: Morton-range partition + LET exchange over NCCL "
+                            f"(weak scaling, {cfg['n']} particles per GPU)")
+        d["workload"] = ("BASELINE.json configs[3] (weak scaling, per-GPU size of " + CONFIG_NAMES[args.config] +
+                         f"): 3D Laplace FMM, N={n} {cfg['kind']}, {cfg['prec']}, P={cfg['P']}, theta={cfg['theta']}, "
+                         f"ncrit={cfg['ncrit']}")
+    return d
+
+
+def roofline_block(args, cfg, counts, ph):
+    pk = peaks()
+    sm_mhz = pk["sm_max_mhz"]
+    fp32_peak_tflops = 148 * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12     # FFMA = 2 flops
+    m2l = m2l_flops_per_pair(cfg["P"])
+    m2l_ms = ph.get("m2l_kernel", 0.0) / args.steps
+    p2p_ms = ph.get("p2p_kernel", 0.0) / args.steps
+    m2l_tf = counts["n_m2l"] * m2l["flops"] / (m2l_ms * 1e-3) / 1e12 if m2l_ms else 0.0
+    p2p_tf = counts["p2p_interactions"] * P2P_FLOPS / (p2p_ms * 1e-3) / 1e12 if p2p_ms else 0.0
+    dom = "m2l" if m2l_ms >= p2p_ms else "p2p"
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(f"{args.config}:{dom}")
+    return {"kernel": f"{dom} ({'k_m2l_fast' if dom == 'm2l' else 'k_p2p_cta'})", "bound": "alu",
+            "achieved": round(m2l_tf if dom == "m2l" else p2p_tf, 3), "peak": round(fp32_peak_tflops, 2),
+            "unit": "TFLOP/s", "frac": round((m2l_tf if dom == "m2l" else p2p_tf) / fp32_peak_tflops, 4),
+            "traffic": traffic,
+            "peak_note": "FP32 FFMA peak = 148 SMs x 128 lanes x 2 flop x sm_max_mhz (MEASURED_PEAKS.json); "
+                         "DESIGN.md §6",
+            "per_kernel": {
+                "m2l": {"ms": round(m2l_ms, 4), "pairs": counts["n_m2l"], "flops_per_pair": m2l["flops"],
+                        "TFLOP/s": round(m2l_tf, 3), "frac": round(m2l_tf / fp32_peak_tflops, 4),
+                        "pairs_per_s": counts["n_m2l"] / (m2l_ms * 1e-3) if m2l_ms else None},
+                "p2p": {"ms": round(p2p_ms, 4), "interactions": counts["p2p_interactions"],
+                        "flops_per_interaction": P2P_FLOPS, "TFLOP/s": round(p2p_tf, 3),
+                        "frac": round(p2p_tf / fp32_peak_tflops, 4),
+                        "fp32_issue_frac": round(counts["p2p_interactions"] * P2P_INSTR / (p2p_ms * 1e-3) /
+                                                 (148 * FP32_LANES_PER_SM * sm_mhz * 1e6), 4) if p2p_ms else None,
+                        "interactions_per_s": counts["p2p_interactions"] / (p2p_ms * 1e-3) if p2p_ms else None}},
+            "measured": "CUDA events recorded by libfmm around each kernel on the stream it runs on (P2P then "
+                        "M2L, back to back on the caller's stream); per-launch average over the timed steps",
+            "traffic_note": "dram read+write bytes per launch from one ncu --set full capture (profiles/traffic.json)"}
+
+
+def run_dist(args, cfg, rank, world, local):
+    """--gpus N > 1 under torchrun: the distributed FMM (dist.py) over NCCL."""
+    import torch
+    import torch.distributed as tdist
+    from paper_1405_7487_b200.dist import DistFMM, TorchComm
+    dt_np = np.float32 if cfg["prec"] == "f32" else np.float64
+    dt_t = torch.float32 if cfg["prec"] == "f32" else torch.float64
+    n = cfg["n"]
+    N = n * world
+    pos, q = synth.generate(cfg["kind"], n, cfg["seed"], dt_np, start=rank * n, n_total=N)
+    dpos = torch.from_numpy(pos).cuda()
+    dq = torch.from_numpy(q).cuda()
+    D = DistFMM(TorchComm(), N, cfg["P"], cfg["theta"], cfg["ncrit"], cfg["prec"], local)
+    f = D.fmm[0]
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+
+    def step():
+        return D.solve([dpos], [dq], [rank * n])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    f.set_timing(True)
+    f.phase_times(reset=True)
+    f.launch_count(reset=True)
+    tdist.barrier()
+    torch.cuda.synchronize()
+    ms = 0.0
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step()
+            b.record(stream)
+            b.synchronize()
+            ms += a.elapsed_time(b)
+        tdist.barrier()
+        torch.cuda.synchronize()
+    launches = f.launch_count(reset=True)
+    ph = f.phase_times(reset=True)
+    f.set_timing(False)
+    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    # e2e: pinned host buffers in, host results out, copies inside the timed region
+    hpos = torch.from_numpy(pos).pin_memory()
+    hq = torch.from_numpy(q).pin_memory()
+    hphi = torch.empty(n, dtype=dt_t).pin_memory()
+    hgrad = torch.empty((n, 3), dtype=dt_t).pin_memory()
+    tdist.barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(3, args.steps // 2)
+    for _ in range(e2e_steps):
+        gp = hpos.to("cuda", non_blocking=True)
+        gq = hq.to("cuda", non_blocking=True)
+        (phi, grad), = D.solve([gp], [gq], [rank * n])
+        hphi.copy_(phi, non_blocking=True)
+        hgrad.copy_(grad, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    counts = f.counts()
+    es = 4 if cfg["prec"] == "f32" else 8
+    if rank == 0:
+        line = {"metric": METRIC, "value": N / (ms_step * 1e-3), "unit": "particles/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32" if cfg["prec"] == "f32" else "f64",
+                "data": "synthetic (seeded SplitMix64 generator, synth/; each rank draws its slice)",
+                "config": workload_config(cfg, args, world),
+                "e2e": {"value": N / e2e_s, "unit": "particles/s", "h2d_bytes_per_step": n * 4 * es,
+                        "d2h_bytes_per_step": n * 4 * es, "api": "DistFMM.solve (pinned host buffers, per rank)"},
+                "gpu_launches": launches,
+                "roofline": roofline_block(args, cfg, counts, ph),
+                "clocks": clk.summary(),
+                "phases_ms": {k: round(v / args.steps, 4) for k, v in ph.items()},
+                "counts_rank0": counts,
+                "let_bytes_rank0": dict(D.stats)}
+        print(json.dumps(line), flush=True)
+    tdist.barrier()
+    D.close()
 
 
 # --------------------------------------------------------------------- main
@@ -187,6 +319,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIG_NAMES))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true", help="use the distributed path even on 1 GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = synth.CONFIGS[args.config]
@@ -201,13 +334,17 @@ def main():
 
     import torch
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
     from paper_1405_7487_b200 import FMM, build
     build.build()
+    dist = None
+    if world > 1 or args.dist:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
+        run_dist(args, cfg, rank, world, local)
+        dist.destroy_process_group()
+        return
     dt_np = np.float32 if cfg["prec"] == "f32" else np.float64
     dt_t = torch.float32 if cfg["prec"] == "f32" else torch.float64
     n = cfg["n"]
@@ -278,37 +415,8 @@ def main():
 
     counts = fmm.counts()
     if rank == 0:
-        pk = peaks()
         clocks = clk.summary()
-        sm_mhz = pk["sm_max_mhz"]
-        fp32_peak_tflops = 148 * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12     # FFMA = 2 flops
-        m2l = m2l_flops_per_pair(cfg["P"])
-        m2l_ms = ph.get("m2l_kernel", 0.0) / args.steps
-        p2p_ms = ph.get("p2p_kernel", 0.0) / args.steps
-        m2l_tf = counts["n_m2l"] * m2l["flops"] / (m2l_ms * 1e-3) / 1e12 if m2l_ms else 0.0
-        p2p_tf = counts["p2p_interactions"] * P2P_FLOPS / (p2p_ms * 1e-3) / 1e12 if p2p_ms else 0.0
-        dom = "m2l" if m2l_ms >= p2p_ms else "p2p"
-        traffic = None
-        tpath = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tpath):
-            traffic = json.load(open(tpath)).get(f"{args.config}:{dom}")
-        roof = {"kernel": f"{dom} ({'k_m2l_fast' if dom == 'm2l' else 'k_p2p_cta'})", "bound": "alu",
-                "achieved": round(m2l_tf if dom == "m2l" else p2p_tf, 3), "peak": round(fp32_peak_tflops, 2),
-                "unit": "TFLOP/s", "frac": round((m2l_tf if dom == "m2l" else p2p_tf) / fp32_peak_tflops, 4),
-                "traffic": traffic,
-                "peak_note": "FP32 FFMA peak = 148 SMs x 128 lanes x 2 flop x sm_max_mhz (MEASURED_PEAKS.json); "
-                             "DESIGN.md §6",
-                "per_kernel": {
-                    "m2l": {"ms": round(m2l_ms, 4), "pairs": counts["n_m2l"], "flops_per_pair": m2l["flops"],
-                            "TFLOP/s": round(m2l_tf, 3), "frac": round(m2l_tf / fp32_peak_tflops, 4),
-                            "pairs_per_s": counts["n_m2l"] / (m2l_ms * 1e-3) if m2l_ms else None},
-                    "p2p": {"ms": round(p2p_ms, 4), "interactions": counts["p2p_interactions"],
-                            "flops_per_interaction": P2P_FLOPS, "TFLOP/s": round(p2p_tf, 3),
-                            "frac": round(p2p_tf / fp32_peak_tflops, 4),
-                            "interactions_per_s": counts["p2p_interactions"] / (p2p_ms * 1e-3) if p2p_ms else None}},
-                "measured": "CUDA events recorded by libfmm around each kernel on the stream it runs on (P2P then "
-                            "M2L, back to back on the caller's stream); per-launch average over the timed steps",
-                "traffic_note": "dram read+write bytes per launch from one ncu --set full capture (profiles/traffic.json)"}
+        roof = roofline_block(args, cfg, counts, ph)
         line = {"metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32" if cfg["prec"] == "f32" else "f64",

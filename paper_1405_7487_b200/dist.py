@@ -194,10 +194,10 @@ class DistFMM:
     def partition(self, pos, q, gid_base, w=None):
         cm, K, F = self.comm, self.K, self.fmm
         nl = len(F)
-        b = [torch.from_numpy(f.bounds(p)) for f, p in zip(F, pos)]
+        b = [torch.from_numpy(f.bounds(p)).to(p.device) for f, p in zip(F, pos)]
         lo = cm.allreduce([x[:3].clone() for x in b], "min")
         hi = cm.allreduce([x[3:].clone() for x in b], "max")
-        gb = [torch.cat([lo[i], hi[i]]).numpy() for i in range(nl)]
+        gb = [torch.cat([lo[i], hi[i]]).cpu().numpy() for i in range(nl)]
         keys = [F[i].part_keys(pos[i], gb[i]) for i in range(nl)]
 
         def hist_fn(prefixes, pbits, bits):
