@@ -125,7 +125,7 @@ struct fmm_ctx {
     DevBuf fr_a, fr_b, lst_m2l, lst_p2p, lst_tmp, m2l_src, p2p_src, m2l_off, p2p_off, cnt_tmp, cnt_tmp2, dcount;
     // P2P source runs: runs[n_runs] = {start body, flat offset}, then rtot[ncell]; run_off[ncell+1]
     int64_t n_runs = 0;
-    DevBuf runs, run_off, run_tmp, run_pre, run_len64, dcount2, tcnt, cnt64, big_off;
+    DevBuf runs, run_off, run_tmp, run_pre, run_len64, dcount2, tcnt, cnt64, big_off, seg_lists;
 
     // expansions
     DevBuf M, L, Mr, Lr;   // fp64 [ncell][ncoef]; Mr: packed reduced multipoles for the M2L kernel; Lr: reduced L

@@ -176,14 +176,26 @@ __global__ void k_widen_u32(const uint32_t* __restrict__ in, int64_t n, uint64_t
     if (i < n) out[i] = in[i];
 }
 
-// counting-sort scatter of unsorted (target, source) pairs into per-target segments
+// counting-sort scatter of unsorted (target, source) pairs into per-target segments; the
+// traversal emits the pairs of one target in runs (children of a split source are adjacent),
+// so lanes of a warp with the same target share one atomic (__match_any_sync)
 __global__ void k_scatter_src(const uint64_t* __restrict__ lst, int64_t n, const uint64_t* __restrict__ off,
                               uint32_t* __restrict__ cursor, uint32_t* __restrict__ src) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t pr = lst[i];
+    const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+        const int64_t i = i0 + threadIdx.x;
+        const bool ok = i < n;
+        const uint64_t pr = ok ? lst[i] : ~0ull;
         const uint32_t t = (uint32_t)(pr >> 32);
-        const uint32_t k = atomicAdd(&cursor[t], 1u);
-        src[off[t] + k] = (uint32_t)pr;
+        const unsigned act = __ballot_sync(0xffffffffu, ok);
+        if (!ok) continue;
+        const unsigned peers = __match_any_sync(act, t);
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if ((peers & lt) == 0) base = atomicAdd(&cursor[t], (uint32_t)__popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        src[off[t] + base + __popc(peers & lt)] = (uint32_t)pr;
     }
 }
 
@@ -191,13 +203,13 @@ constexpr int SEG_THREADS = 256;
 constexpr int SEG_MAX = 4096;
 
 // ascending sort of each target segment in shared memory (bitonic over the next power of two)
-__global__ void __launch_bounds__(SEG_THREADS) k_segsort(const uint64_t* __restrict__ off, int64_t ncell,
-                                                         uint32_t* __restrict__ src) {
+__global__ void __launch_bounds__(SEG_THREADS) k_segsort(const uint64_t* __restrict__ off, const uint32_t* __restrict__ tl,
+                                                         int64_t nt, uint32_t* __restrict__ src) {
     __shared__ uint32_t s[SEG_MAX];
-    for (int64_t t = blockIdx.x; t < ncell; t += gridDim.x) {
+    for (int64_t ti = blockIdx.x; ti < nt; ti += gridDim.x) {
+        const uint32_t t = tl[ti];
         const uint64_t b = off[t];
         const int n = (int)(off[t + 1] - b);
-        if (n <= 2048 || n > SEG_MAX) continue;   // warp sorts / big-segment path handle these
         int m = 1;
         while (m < n) m <<= 1;
         __syncthreads();
@@ -259,15 +271,15 @@ __device__ __forceinline__ void warp_bitonic(uint32_t (&v)[K], int np, int lane)
 }
 
 template <int K>
-__global__ void __launch_bounds__(128) k_segsort_warp(const uint64_t* __restrict__ off, int64_t ncell,
-                                                      uint32_t* __restrict__ src, int min_n) {
+__global__ void __launch_bounds__(128) k_segsort_warp(const uint64_t* __restrict__ off, const uint32_t* __restrict__ tl,
+                                                      int64_t nt, uint32_t* __restrict__ src) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t t = warp; t < ncell; t += nw) {
+    for (int64_t ti = warp; ti < nt; ti += nw) {
+        const uint32_t t = tl[ti];
         const uint64_t b = off[t];
         const int n = (int)(off[t + 1] - b);
-        if (n <= 1 || n < min_n || n > 32 * K) continue;
         int np = 1;
         while (np < n) np <<= 1;
         uint32_t v[K];
@@ -285,39 +297,43 @@ __global__ void __launch_bounds__(128) k_segsort_warp(const uint64_t* __restrict
     }
 }
 
-// Warp-per-segment stable LSD radix sort in shared memory for 257..2048 keys: RBITS-bit
+// Warp-per-segment stable LSD radix sort in shared memory for up to MAXN keys: BITS-bit
 // digits; ranking row by row (32 keys) with __match_any_sync and a per-warp running
 // histogram, exclusive scan of the bins, scatter to the other buffer.  ~25 instr/key/pass.
+// <1024, 8>: 11 KB of shared memory per warp (20 warps/SM); <2048, 10>: 24 KB.
 constexpr int WR_WARPS = 4;
-constexpr int WR_MAX = 2048;
-constexpr int WR_BITS = 10;
-constexpr int WR_BINS = 1 << WR_BITS;
 
-__global__ void __launch_bounds__(WR_WARPS * 32) k_segsort_wradix(const uint64_t* __restrict__ off, int64_t ncell,
-                                                                  uint32_t* __restrict__ src, int nbits, int min_n) {
+template <int MAXN, int BITS>
+constexpr size_t wradix_smem() { return (size_t)WR_WARPS * (2 * MAXN + MAXN / 2 + (1 << BITS)) * 4; }
+
+template <int MAXN, int BITS>
+__global__ void __launch_bounds__(WR_WARPS * 32) k_segsort_wradix(const uint64_t* __restrict__ off,
+                                                                  const uint32_t* __restrict__ tl, int64_t nt,
+                                                                  uint32_t* __restrict__ src, int nbits) {
+    constexpr int BINS = 1 << BITS;
     extern __shared__ uint32_t wr_smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint32_t* A = wr_smem + (size_t)w * (2 * WR_MAX + WR_MAX / 2 + WR_BINS);
-    uint32_t* B = A + WR_MAX;
-    uint16_t* pos = reinterpret_cast<uint16_t*>(B + WR_MAX);
-    uint32_t* hist = B + WR_MAX + WR_MAX / 2;
+    uint32_t* A = wr_smem + (size_t)w * (2 * MAXN + MAXN / 2 + BINS);
+    uint32_t* B = A + MAXN;
+    uint16_t* pos = reinterpret_cast<uint16_t*>(B + MAXN);
+    uint32_t* hist = B + MAXN + MAXN / 2;
     const unsigned lt = (1u << lane) - 1u;
     const int64_t warp = (int64_t)blockIdx.x * WR_WARPS + w;
     const int64_t nw = (int64_t)gridDim.x * WR_WARPS;
-    for (int64_t t = warp; t < ncell; t += nw) {
+    for (int64_t ti = warp; ti < nt; ti += nw) {
+        const uint32_t t = tl[ti];
         const uint64_t b0 = off[t];
         const int n = (int)(off[t + 1] - b0);
-        if (n < min_n || n > WR_MAX) continue;
         for (int i = lane; i < n; i += 32) A[i] = src[b0 + i];
         uint32_t* in = A;
         uint32_t* out = B;
-        for (int shift = 0; shift < nbits; shift += WR_BITS) {
-            for (int i = lane; i < WR_BINS; i += 32) hist[i] = 0;
+        for (int shift = 0; shift < nbits; shift += BITS) {
+            for (int i = lane; i < BINS; i += 32) hist[i] = 0;
             __syncwarp();
             for (int r = 0; r < n; r += 32) {
                 const int i = r + lane;
                 const bool ok = i < n;
-                const uint32_t d = ok ? (in[i] >> shift) & (WR_BINS - 1) : 0xFFFFFFFFu;
+                const uint32_t d = ok ? (in[i] >> shift) & (BINS - 1) : 0xFFFFFFFFu;
                 const unsigned peers = __match_any_sync(0xffffffffu, d);
                 uint32_t before = 0;
                 if (ok) before = hist[d];
@@ -328,8 +344,8 @@ __global__ void __launch_bounds__(WR_WARPS * 32) k_segsort_wradix(const uint64_t
                 }
                 __syncwarp();
             }
-            // exclusive scan of the bins (WR_BINS / 32 per lane)
-            constexpr int PER = WR_BINS / 32;
+            // exclusive scan of the bins (BINS / 32 per lane)
+            constexpr int PER = BINS / 32;
             uint32_t loc = 0;
 #pragma unroll
             for (int k = 0; k < PER; ++k) loc += hist[lane * PER + k];
@@ -350,7 +366,7 @@ __global__ void __launch_bounds__(WR_WARPS * 32) k_segsort_wradix(const uint64_t
             __syncwarp();
             for (int i = lane; i < n; i += 32) {
                 const uint32_t v = in[i];
-                out[hist[(v >> shift) & (WR_BINS - 1)] + pos[i]] = v;
+                out[hist[(v >> shift) & (BINS - 1)] + pos[i]] = v;
             }
             __syncwarp();
             uint32_t* tmp = in;
@@ -359,6 +375,27 @@ __global__ void __launch_bounds__(WR_WARPS * 32) k_segsort_wradix(const uint64_t
         }
         for (int i = lane; i < n; i += 32) src[b0 + i] = in[i];
         __syncwarp();
+    }
+}
+
+// segment size classes for the sorts: 0: 2..256 (warp bitonic), 1: 257..1024 (radix<1024,8>),
+// 2: 1025..2048 (radix<2048,10>), 3: 2049..SEG_MAX (CTA bitonic), 4: longer (global radix)
+constexpr int NSEGCLS = 5;
+__device__ __forceinline__ int seg_class(uint64_t n) {
+    return n <= 1 ? -1 : n <= 256 ? 0 : n <= 1024 ? 1 : n <= 2048 ? 2 : n <= (uint64_t)SEG_MAX ? 3 : 4;
+}
+
+__global__ void k_seg_classify(const uint64_t* __restrict__ off, int64_t nc, uint32_t* __restrict__ lists,
+                               unsigned* __restrict__ counts) {
+    const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+    for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x; t0 < nc; t0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = t0 + threadIdx.x;
+        const int c = t < nc ? seg_class(off[t + 1] - off[t]) : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, c);
+        unsigned base = 0;
+        if (c >= 0 && (peers & lt) == 0) base = atomicAdd(&counts[c], (unsigned)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, __ffs(peers) - 1);
+        if (c >= 0) lists[(size_t)c * nc + base + __popc(peers & lt)] = (uint32_t)t;
     }
 }
 
@@ -430,42 +467,62 @@ fmm_status canonicalise(fmm_ctx* ctx, DevBuf& lst, int64_t n, uint32_t* tcnt, De
     k_widen_u32<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(tcnt, nc, c64);
     FMM_LAUNCH(ctx);
     FMM_TRY(scan_exclusive_u64(ctx, c64, P_<uint64_t>(off), nc, P_<uint64_t>(off) + nc, s));
-    // longest segment decides the sorting path
-    unsigned* d_max = P_<unsigned>(ctx->dcount2) + 8;
-    FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_max, 0, 4, s));
-    k_max_u32<<<ctx->num_sms * 2, 256, 0, s>>>(tcnt, nc, d_max);
-    FMM_LAUNCH(ctx);
-    unsigned mx = 0;
-    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&mx, d_max, 4, cudaMemcpyDeviceToHost, s));
-    FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
     FMM_CUDA_TRY(ctx, cudaMemsetAsync(tcnt, 0, (size_t)nc * 4, s));   // reuse as cursors
     const int g = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 16);
     k_scatter_src<<<std::max(g, 1), 256, 0, s>>>(P_<uint64_t>(lst), n, P_<uint64_t>(off), tcnt, P_<uint32_t>(src));
     FMM_LAUNCH(ctx);
     if (sort_segments) {
-        // warp-register bitonic for segments <= 256 and <= 1024, CTA bitonic <= SEG_MAX
-        const unsigned gw = (unsigned)std::min<int64_t>((nc + 3) / 4, (int64_t)ctx->num_sms * 32);
-        k_segsort_warp<8><<<gw, 128, 0, s>>>(P_<uint64_t>(off), nc, P_<uint32_t>(src), 0);
+        // segments grouped by size class (one list of targets per class), each class sorted by
+        // the kernel that fits it; only the classes that occur are launched
+        FMM_TRY(buf_ensure(ctx, ctx->seg_lists, (size_t)NSEGCLS * nc * 4 + 64));
+        uint32_t* lists = P_<uint32_t>(ctx->seg_lists);
+        unsigned* d_ccnt = P_<unsigned>(ctx->dcount2) + 8;
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_ccnt, 0, NSEGCLS * 4, s));
+        k_seg_classify<<<(unsigned)std::min<int64_t>((nc + 255) / 256, (int64_t)ctx->num_sms * 8), 256, 0, s>>>(
+            P_<uint64_t>(off), nc, lists, d_ccnt);
         FMM_LAUNCH(ctx);
-        if (mx > 256) {
-            int nbits = 1;
-            while (((int64_t)1 << nbits) < nc + ctx->nrem) ++nbits;
-            const size_t smem = (size_t)WR_WARPS * (2 * WR_MAX + WR_MAX / 2 + WR_BINS) * 4;
-            static bool attr = false;
-            if (!attr) {
-                FMM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_segsort_wradix, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       (int)smem));
-                attr = true;
+        unsigned cc[NSEGCLS];
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(cc, d_ccnt, sizeof(cc), cudaMemcpyDeviceToHost, s));
+        FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+        int nbits = 1;
+        while (((int64_t)1 << nbits) < nc + ctx->nrem) ++nbits;
+        auto gwarps = [&](unsigned cnt, int wpb) {
+            return (unsigned)std::max<int64_t>(std::min<int64_t>(((int64_t)cnt + wpb - 1) / wpb, (int64_t)ctx->num_sms * 32), 1);
+        };
+        if (cc[0]) {
+            k_segsort_warp<8><<<gwarps(cc[0], 4), 128, 0, s>>>(P_<uint64_t>(off), lists, cc[0], P_<uint32_t>(src));
+            FMM_LAUNCH(ctx);
+        }
+        if (cc[1]) {
+            constexpr size_t sm = wradix_smem<1024, 8>();
+            static bool attr1 = false;
+            if (!attr1) {
+                FMM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_segsort_wradix<1024, 8>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                attr1 = true;
             }
-            const unsigned gr = (unsigned)std::min<int64_t>((nc + WR_WARPS - 1) / WR_WARPS, (int64_t)ctx->num_sms * 8);
-            k_segsort_wradix<<<gr, WR_WARPS * 32, smem, s>>>(P_<uint64_t>(off), nc, P_<uint32_t>(src), nbits, 257);
+            k_segsort_wradix<1024, 8><<<gwarps(cc[1], WR_WARPS), WR_WARPS * 32, sm, s>>>(
+                P_<uint64_t>(off), lists + (size_t)nc, cc[1], P_<uint32_t>(src), nbits);
             FMM_LAUNCH(ctx);
         }
-        if (mx > 2048) {
-            k_segsort<<<(unsigned)std::min<int64_t>(nc, (int64_t)ctx->num_sms * 16), SEG_THREADS, 0, s>>>(
-                P_<uint64_t>(off), nc, P_<uint32_t>(src));
+        if (cc[2]) {
+            constexpr size_t sm = wradix_smem<2048, 10>();
+            static bool attr2 = false;
+            if (!attr2) {
+                FMM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_segsort_wradix<2048, 10>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                attr2 = true;
+            }
+            k_segsort_wradix<2048, 10><<<gwarps(cc[2], WR_WARPS), WR_WARPS * 32, sm, s>>>(
+                P_<uint64_t>(off), lists + 2 * (size_t)nc, cc[2], P_<uint32_t>(src), nbits);
             FMM_LAUNCH(ctx);
         }
+        if (cc[3]) {
+            k_segsort<<<(unsigned)std::min<int64_t>(cc[3], (int64_t)ctx->num_sms * 16), SEG_THREADS, 0, s>>>(
+                P_<uint64_t>(off), lists + 3 * (size_t)nc, cc[3], P_<uint32_t>(src));
+            FMM_LAUNCH(ctx);
+        }
+        const unsigned mx = cc[4] ? (unsigned)SEG_MAX + 1 : 0u;
         if (mx > (unsigned)SEG_MAX) {
             // c64 (count widening buffer, nc+1 entries) is free again: reuse it for the sizes
             uint64_t* bsz = c64;
@@ -499,34 +556,53 @@ fmm_status canonicalise(fmm_ctx* ctx, DevBuf& lst, int64_t n, uint32_t* tcnt, De
 // contiguous (Morton-adjacent leaves) merge into one run {start body, flat offset in the
 // target's source stream}; rtot[t] = total sources of target t.  Used by the P2P kernel to
 // stream a target's sources as full fixed-size chunks.
+// warp per target: a list entry starts a new run unless its body range begins where the
+// previous entry's ends
 __global__ void k_run_flags(const uint64_t* __restrict__ off, const uint32_t* __restrict__ src, int64_t ncell,
                             const uint32_t* __restrict__ bb, const uint32_t* __restrict__ bc,
                             uint32_t* __restrict__ flag) {
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ncell; t += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = w0; t < ncell; t += nw) {
         const uint64_t p0 = off[t], p1 = off[t + 1];
-        uint32_t prev_end = 0xFFFFFFFFu;
-        for (uint64_t p = p0; p < p1; ++p) {
+        for (uint64_t p = p0 + lane; p < p1; p += 32) {
             const uint32_t sc = src[p];
-            flag[p] = (p == p0) || (prev_end != bb[sc]);
-            prev_end = bb[sc] + bc[sc];
+            uint32_t f = 1;
+            if (p > p0) {
+                const uint32_t pv = src[p - 1];
+                f = bb[pv] + bc[pv] != bb[sc];
+            }
+            flag[p] = f;
         }
     }
 }
 
+// warp per target: flat source offsets are a warp scan of the body counts
 __global__ void k_run_emit(const uint64_t* __restrict__ off, const uint32_t* __restrict__ src, int64_t ncell,
                            const uint32_t* __restrict__ bb, const uint32_t* __restrict__ bc,
                            const uint32_t* __restrict__ flag, const uint32_t* __restrict__ rid,
                            uint2* __restrict__ runs, uint32_t* __restrict__ roff, uint32_t* __restrict__ rtot) {
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ncell; t += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = w0; t < ncell; t += nw) {
         const uint64_t p0 = off[t], p1 = off[t + 1];
-        roff[t] = p0 < p1 ? rid[p0] : (p0 > 0 ? rid[p0 - 1] + flag[p0 - 1] : 0u);
-        uint32_t flat = 0;
-        for (uint64_t p = p0; p < p1; ++p) {
-            const uint32_t sc = src[p];
-            if (flag[p]) runs[rid[p]] = make_uint2(bb[sc], flat);
-            flat += bc[sc];
+        if (lane == 0) roff[t] = p0 < p1 ? rid[p0] : (p0 > 0 ? rid[p0 - 1] + flag[p0 - 1] : 0u);
+        uint32_t carry = 0;
+        for (uint64_t q0 = p0; q0 < p1; q0 += 32) {
+            const uint64_t p = q0 + lane;
+            const bool ok = p < p1;
+            const uint32_t sc = ok ? src[p] : 0u;
+            const uint32_t c = ok ? bc[sc] : 0u;
+            uint32_t x = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (ok && flag[p]) runs[rid[p]] = make_uint2(bb[sc], carry + x - c);
+            carry += __shfl_sync(0xffffffffu, x, 31);
         }
-        rtot[t] = flat;
+        if (lane == 0) rtot[t] = carry;
     }
 }
 
@@ -540,7 +616,7 @@ fmm_status build_runs(fmm_ctx* ctx, cudaStream_t s) {
     uint32_t* d_nr = P_<uint32_t>(ctx->dcount2);
     const uint64_t* off = P_<uint64_t>(ctx->p2p_off);
     const uint32_t* src = P_<uint32_t>(ctx->p2p_src);
-    const int g = (int)std::min<int64_t>((nc + 127) / 128, (int64_t)ctx->num_sms * 16);
+    const int g = (int)std::min<int64_t>((nc + 3) / 4, (int64_t)ctx->num_sms * 16);
     k_run_flags<<<std::max(g, 1), 128, 0, s>>>(off, src, nc, P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), flag);
     FMM_LAUNCH(ctx);
     FMM_TRY(scan_exclusive_u32(ctx, flag, rid, n, d_nr, s));
