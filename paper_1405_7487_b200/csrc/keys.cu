@@ -45,15 +45,20 @@ __global__ void k_bounds(const Real* __restrict__ pos, int64_t n, double* __rest
     }
 }
 
-// final reduction over blocks + R2 root cube, one thread
+// final reduction over blocks (one warp; min/max are exact in any order) + R2 root cube
 __global__ void k_root_cube(const double* __restrict__ blk, int nblk, double* __restrict__ root) {
-    double lo[3], hi[3];
-    for (int d = 0; d < 3; ++d) { lo[d] = blk[d]; hi[d] = blk[3 + d]; }
-    for (int b = 1; b < nblk; ++b)
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int b = threadIdx.x; b < nblk; b += 32)
         for (int d = 0; d < 3; ++d) {
             lo[d] = fmin(lo[d], blk[6 * b + d]);
             hi[d] = fmax(hi[d], blk[6 * b + 3 + d]);
         }
+    for (int o = 16; o; o >>= 1)
+        for (int d = 0; d < 3; ++d) {
+            lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+            hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+        }
+    if (threadIdx.x != 0) return;
     double c0[3], ext = 0.0;
     for (int d = 0; d < 3; ++d) {
         c0[d] = __dmul_rn(__dadd_rn(lo[d], hi[d]), 0.5);
@@ -136,7 +141,7 @@ fmm_status build_keys_t(fmm_ctx* ctx, const Real* pos, int64_t n, cudaStream_t s
         double* d_blk = reinterpret_cast<double*>((char*)ctx->red_tmp.p + 64);
         FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_bad, 0, sizeof(int), s));
         k_bounds<Real><<<nblk, 256, 0, s>>>(pos, n, d_blk, d_bad);
-        k_root_cube<<<1, 1, 0, s>>>(d_blk, nblk, P_<double>(ctx->root));
+        k_root_cube<<<1, 32, 0, s>>>(d_blk, nblk, P_<double>(ctx->root));
         ctx->launches += 2;
         int bad = 0;
         FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -9,13 +9,12 @@
 //
 // P2M: warp per leaf; 32 bodies at a time, each lane builds its body's x^e/e! tables in
 // shared memory, then lanes over coefficients accumulate the 32 bodies in order.
-// M2M: warp per parent; the shift operator is separable, s^(a-b)/(a-b)! = prod_i
-// s_i^(a_i-b_i)/(a_i-b_i)!, so each child's expansion is shifted by three 1D passes
+// M2M: block per parent, warp per child; the shift operator is separable, s^(a-b)/(a-b)! =
+// prod_i s_i^(a_i-b_i)/(a_i-b_i)!, so each child's expansion is shifted by three 1D passes
 // (x, then y, then z) through shared memory -- the same sum as R13, grouped per axis.
 #include "common.cuh"
 
 namespace {
-constexpr int UP_WARPS = 4;
 constexpr int P2M_WARPS = 2;
 
 __constant__ double c_inv[FMM_MAXP + 1] = {0.0,       1.0,        1.0 / 2,  1.0 / 3,  1.0 / 4,  1.0 / 5,
@@ -94,35 +93,35 @@ __device__ __forceinline__ void shift_pass_up(const uchar4* __restrict__ ex, int
     }
 }
 
-__global__ void __launch_bounds__(UP_WARPS * 32) k_m2m(int64_t cbeg, int64_t cend, const uint32_t* __restrict__ cb,
-                                                        const uint32_t* __restrict__ cc, const double4* __restrict__ cr,
-                                                        int P, int ncoef, double* __restrict__ M) {
+// One block per parent, one warp per child (up to 8): each warp shifts its child's
+// expansion with the three separable passes into its own shared buffers, then the block
+// sums the (up to) 8 shifted expansions in child order (the same order as R13's loop).
+constexpr int M2M_THREADS = 256;
+__global__ void __launch_bounds__(M2M_THREADS) k_m2m(int64_t cbeg, int64_t cend, const uint32_t* __restrict__ cb,
+                                                     const uint32_t* __restrict__ cc, const double4* __restrict__ cr,
+                                                     int P, int ncoef, double* __restrict__ M) {
     extern __shared__ double s_dyn[];
     __shared__ uchar4 ex[816];
-    __shared__ double s_t[UP_WARPS][3][FMM_MAXP];
+    __shared__ double s_t[8][3][FMM_MAXP];
     fill_ex_table(ex, ncoef);
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double* A = s_dyn + (size_t)w * 2 * ncoef;
     double* B = A + ncoef;
-    for (int64_t c = cbeg + (int64_t)blockIdx.x * UP_WARPS + w; c < cend; c += (int64_t)gridDim.x * UP_WARPS) {
+    for (int64_t c = cbeg + blockIdx.x; c < cend; c += gridDim.x) {
         const uint32_t nk = cc[c];
-        if (nk == 0) continue;  // leaf: written by P2M
+        if (nk == 0) continue;  // leaf: written by P2M (uniform over the block)
         const double4 cp = cr[c];
-        double acc[26];
-#pragma unroll
-        for (int i = 0; i < 26; ++i) acc[i] = 0.0;
-        for (uint32_t k = 0; k < nk; ++k) {
-            const uint32_t ch = cb[c] + k;
+        if ((uint32_t)w < nk) {
+            const uint32_t ch = cb[c] + w;
             const double4 q = cr[ch];
-            __syncwarp();
             for (int i = lane; i < ncoef; i += 32) A[i] = M[(int64_t)ch * ncoef + i];
             if (lane < 3) {
-                const double s = lane == 0 ? q.x - cp.x : lane == 1 ? q.y - cp.y : q.z - cp.z;
+                const double sh = lane == 0 ? q.x - cp.x : lane == 1 ? q.y - cp.y : q.z - cp.z;
                 double v = 1.0;
                 s_t[w][lane][0] = 1.0;
                 for (int e = 1; e < P; ++e) {
-                    v = v * s * c_inv[e];
+                    v = v * sh * c_inv[e];
                     s_t[w][lane][e] = v;
                 }
             }
@@ -131,22 +130,15 @@ __global__ void __launch_bounds__(UP_WARPS * 32) k_m2m(int64_t cbeg, int64_t cen
             __syncwarp();
             shift_pass_up(ex, ncoef, 1, B, A, s_t[w][1], lane);
             __syncwarp();
-#pragma unroll
-            for (int i = 0; i < 26; ++i) {
-                const int kk = lane + 32 * i;
-                if (kk < ncoef) {
-                    const uchar4 e = ex[kk];
-                    double s = 0.0;
-                    for (int b = 0; b <= e.z; ++b) s += A[cidx(e.x, e.y, b)] * s_t[w][2][e.z - b];
-                    acc[i] += s;
-                }
-            }
+            shift_pass_up(ex, ncoef, 2, A, B, s_t[w][2], lane);
         }
-#pragma unroll
-        for (int i = 0; i < 26; ++i) {
-            const int kk = lane + 32 * i;
-            if (kk < ncoef) M[(int64_t)c * ncoef + kk] = acc[i];
+        __syncthreads();
+        for (int k = threadIdx.x; k < ncoef; k += M2M_THREADS) {
+            double acc = 0.0;
+            for (uint32_t j = 0; j < nk; ++j) acc += s_dyn[(size_t)j * 2 * ncoef + ncoef + k];
+            M[(int64_t)c * ncoef + k] = acc;
         }
+        __syncthreads();
     }
 }
 
@@ -162,13 +154,13 @@ fmm_status upward_t(fmm_ctx* ctx, cudaStream_t s) {
                                                          P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc),
                                                          P_<double4>(ctx->c_cr), ctx->P, ctx->ncoef, M);
     FMM_LAUNCH(ctx);
-    const size_t smem = (size_t)UP_WARPS * 2 * ctx->ncoef * 8;
+    const size_t smem = (size_t)8 * 2 * ctx->ncoef * 8;
     if (smem > 48 * 1024) FMM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_m2m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     for (int64_t l = ctx->depth - 1; l >= 0; --l) {
         int64_t b = ctx->level_begin[l], e = ctx->level_begin[l + 1];
-        int gg = (int)std::min<int64_t>((e - b + UP_WARPS - 1) / UP_WARPS, (int64_t)ctx->num_sms * 16);
-        k_m2m<<<std::max(gg, 1), UP_WARPS * 32, smem, s>>>(b, e, P_<uint32_t>(ctx->c_cb), P_<uint32_t>(ctx->c_cc),
-                                                           P_<double4>(ctx->c_cr), ctx->P, ctx->ncoef, M);
+        int gg = (int)std::min<int64_t>(e - b, (int64_t)ctx->num_sms * 16);
+        k_m2m<<<std::max(gg, 1), M2M_THREADS, smem, s>>>(b, e, P_<uint32_t>(ctx->c_cb), P_<uint32_t>(ctx->c_cc),
+                                                         P_<double4>(ctx->c_cr), ctx->P, ctx->ncoef, M);
         FMM_LAUNCH(ctx);
     }
     FMM_CUDA_TRY(ctx, cudaGetLastError());
