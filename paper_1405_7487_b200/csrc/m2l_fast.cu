@@ -199,6 +199,9 @@ __global__ void __launch_bounds__(128, 2)
             derivs<P, R>(ux, uy, uz, D0, D1);
             // (rho_B / rho_A)^n per degree, exact powers of two
             const int de = eb - ea;
+            // (rho_B/rho_A)^n: all pairs of a uniform tree have de = 0; the scaling runs only
+            // in chunks of pairs where some lane of the warp needs it (warp-uniform branch)
+            const bool need = __any_sync(__activemask(), de != 0);
             R pw[P];
             pw[0] = R(1);
             pw[1] = (R)exp2((double)de);
@@ -208,15 +211,17 @@ __global__ void __launch_bounds__(128, 2)
             sfor<0, NCH>([&](auto c) {
                 constexpr int C4 = decltype(c)::value;
                 const V4 v = sv[C4];
-                const R vv[4] = {v.x, v.y, v.z, v.w};
+                R vv[4] = {v.x, v.y, v.z, v.w};
+                if (need) {
+                    sfor<0, 4>([&](auto j) {
+                        constexpr int dg = elem_deg<P>(4 * C4 + decltype(j)::value);
+                        if constexpr (dg > 0) vv[decltype(j)::value] *= pw[dg];
+                    });
+                }
                 sfor<0, 4>([&](auto j) {
                     constexpr int E = 4 * C4 + decltype(j)::value;
                     constexpr int dg = elem_deg<P>(E);
-                    if constexpr (dg >= 0) {
-                        R s = vv[decltype(j)::value];
-                        if constexpr (dg > 0) s *= pw[dg];
-                        apply_elem<P, E, R>(s, D0, D1, L0, L1);
-                    }
+                    if constexpr (dg >= 0) apply_elem<P, E, R>(vv[decltype(j)::value], D0, D1, L0, L1);
                 });
             });
         }
