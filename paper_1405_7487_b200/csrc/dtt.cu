@@ -91,7 +91,8 @@ __global__ void __launch_bounds__(DT_THREADS) k_dtt_step(const uint64_t* __restr
                                                          double theta, unsigned long long* __restrict__ cnt,
                                                          uint64_t* __restrict__ m2l, uint64_t* __restrict__ p2p,
                                                          uint64_t* __restrict__ next, uint32_t* __restrict__ tcnt_m2l,
-                                                         uint32_t* __restrict__ tcnt_p2p) {
+                                                         uint32_t* __restrict__ tcnt_p2p, uint64_t cap_next,
+                                                         int children_only) {
     __shared__ unsigned long long s_warp[DT_THREADS / 32];
     __shared__ unsigned long long s_base[3];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -135,8 +136,8 @@ __global__ void __launch_bounds__(DT_THREADS) k_dtt_step(const uint64_t* __restr
             }
             if (lane < DT_THREADS / 32) s_warp[lane] = w;
             if (lane == DT_THREADS / 32 - 1) {
-                s_base[0] = atomicAdd(&cnt[0], w & 0xFFFFull);
-                s_base[1] = atomicAdd(&cnt[1], (w >> 16) & 0xFFFFull);
+                s_base[0] = children_only ? 0ull : atomicAdd(&cnt[0], w & 0xFFFFull);
+                s_base[1] = children_only ? 0ull : atomicAdd(&cnt[1], (w >> 16) & 0xFFFFull);
                 s_base[2] = atomicAdd(&cnt[2], w >> 32);
             }
         }
@@ -148,9 +149,16 @@ __global__ void __launch_bounds__(DT_THREADS) k_dtt_step(const uint64_t* __restr
 #pragma unroll
         for (int k = 0; k < DT_ITEMS; ++k) {
             const uint64_t pr = ((uint64_t)a[k] << 32) | b[k];
-            if (o[k] == 0) m2l[pm++] = pr;
-            else if (o[k] == 1) p2p[pp++] = pr;
-            else if (o[k] == 2) {
+            if (nch[k] && pc + nch[k] > cap_next) {
+                // next frontier larger than its buffer: the host grows it to the exact size
+                // (the cursor still advances) and re-runs the step for the children only
+                atomicOr(&cnt[3], 2ull);
+                pc += nch[k];
+            } else if (o[k] == 0) {
+                if (!children_only) m2l[pm++] = pr;
+            } else if (o[k] == 1) {
+                if (!children_only) p2p[pp++] = pr;
+            } else if (o[k] == 2) {
                 const uint32_t k0 = v.cb[a[k]];
                 for (uint32_t c = 0; c < nch[k]; ++c) next[pc + c] = ((uint64_t)(k0 + c) << 32) | b[k];
                 pc += nch[k];
@@ -163,8 +171,10 @@ __global__ void __launch_bounds__(DT_THREADS) k_dtt_step(const uint64_t* __restr
                     next[pc + c] = ((uint64_t)a[k] << 32) | (k0 == FMM_LET_ABSENT ? b[k] : k0 + c);
                 pc += nch[k];
             }
-            count_target(tcnt_m2l, o[k] == 0, a[k]);
-            count_target(tcnt_p2p, o[k] == 1, a[k]);
+            if (!children_only) {
+                count_target(tcnt_m2l, o[k] == 0, a[k]);
+                count_target(tcnt_p2p, o[k] == 1, a[k]);
+            }
         }
         __syncthreads();   // s_warp / s_base reuse
     }
@@ -662,16 +672,30 @@ fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append
         const size_t need_m = (size_t)(n_m2l + nf) * 8, need_p = (size_t)(n_p2p + nf) * 8;
         if (need_m > ctx->lst_m2l.bytes) FMM_TRY(buf_ensure(ctx, ctx->lst_m2l, need_m + need_m / 2, true, s));
         if (need_p > ctx->lst_p2p.bytes) FMM_TRY(buf_ensure(ctx, ctx->lst_p2p, need_p + need_p / 2, true, s));
-        FMM_TRY(buf_ensure(ctx, ctx->fr_b, (size_t)nf * 8 * 8));
+        // next frontier: at most 8 children per pair; large frontiers start from 3x and grow
+        // to the exact size on overflow (keeps deep traversals of 2^24+ particles in HBM)
+        const uint64_t cap = nf <= (1 << 20) ? (uint64_t)nf * 8 : (uint64_t)nf * 3;
+        FMM_TRY(buf_ensure(ctx, ctx->fr_b, (size_t)cap * 8));
         FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt + 2, 0, 8, s));   // next-frontier cursor restarts
         const int g = (int)std::min<int64_t>((nf + DT_THREADS * DT_ITEMS - 1) / (DT_THREADS * DT_ITEMS),
                                              (int64_t)ctx->num_sms * 8);
         k_dtt_step<<<g, DT_THREADS, 0, s>>>(P_<uint64_t>(ctx->fr_a), nf, v, ctx->theta, d_cnt, P_<uint64_t>(ctx->lst_m2l),
-                                            P_<uint64_t>(ctx->lst_p2p), P_<uint64_t>(ctx->fr_b), tcnt_m2l, tcnt_p2p);
+                                            P_<uint64_t>(ctx->lst_p2p), P_<uint64_t>(ctx->fr_b), tcnt_m2l, tcnt_p2p,
+                                            ctx->fr_b.bytes / 8, 0);
         FMM_LAUNCH(ctx);
         unsigned long long h[4];
         FMM_CUDA_TRY(ctx, cudaMemcpyAsync(h, d_cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
         FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+        if (h[3] & 2ull) {
+            FMM_TRY(buf_ensure(ctx, ctx->fr_b, (size_t)h[2] * 8));
+            FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt + 2, 0, 16, s));
+            k_dtt_step<<<g, DT_THREADS, 0, s>>>(P_<uint64_t>(ctx->fr_a), nf, v, ctx->theta, d_cnt,
+                                                P_<uint64_t>(ctx->lst_m2l), P_<uint64_t>(ctx->lst_p2p),
+                                                P_<uint64_t>(ctx->fr_b), tcnt_m2l, tcnt_p2p, ctx->fr_b.bytes / 8, 1);
+            FMM_LAUNCH(ctx);
+            FMM_CUDA_TRY(ctx, cudaMemcpyAsync(h, d_cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+            FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+        }
         if (h[3]) {
             ctx->err = "dual tree traversal needed children of a remote LET cell that were not exported";
             return FMM_ERR_STATE;
