@@ -14,7 +14,8 @@ Multi-GPU (torchrun, --gpus N > 1): ONE FMM over N x 2^20 particles (weak scalin
 starts with its 2^20-particle slice of one global cube set), solved by the distributed path
 (paper_1405_7487_b200/dist.py over NCCL): Morton-range partition, local trees, LET exchange
 overlapped with the local traversal, remote traversal, M2L/P2P, results back to the owners.
-Step time = max over ranks of the CUDA-event time around the whole distributed solve.
+Step time = max over ranks of the CUDA-event time around the whole distributed solve; every
+step partitions with the Eq. (1) weights measured in the previous step.
 """
 from __future__ import annotations
 
@@ -41,36 +42,7 @@ FP32_LANES_PER_SM = 128
 
 
 # ----------------------------------------------------------- algorithmic work
-def t2n(P):
-    return P * (P + 1) // 2
-
-
-def m2l_flops_per_pair(P: int) -> dict:
-    """Algorithmic FP work of one M2L pair in the harmonic form the kernel evaluates
-    (m2l_fast.cu; FMA = 2 flops).  Returns flops and lane-instruction counts."""
-    fma = 0
-    # contraction: S0.D0 -> L0, S0.D1 -> L1, S1.D1 -> L0, N.D0 -> L1 (DESIGN.md §5)
-    for m in range(P):                 # S0 element of degree m (m+1 of them)
-        fma += (m + 1) * (t2n(P - m) + t2n(P - 1 - m))
-    for m in range(P - 1):             # S1
-        fma += (m + 1) * t2n(P - 1 - m)
-    for m in range(2, P):              # N
-        fma += (m + 1) * t2n(P - m)
-    # recurrence: per D entry ~ (terms) multiply-adds; count exactly as the kernel forms it
-    rec_instr = 0
-    for n in range(1, P):
-        for z in range(n + 1):         # D0 entries of degree n
-            y = n - z
-            t1 = (y > 0) + (z > 0)
-            t2 = (y > 1) + (z > 1)
-            rec_instr += t1 + t2 + (2 if n > 1 else 1)
-        for z in range(n):             # D1 entries of degree n
-            y = n - 1 - z
-            t1 = 1 + (y > 0) + (z > 0)
-            t2 = (y > 1) + (z > 1)
-            rec_instr += t1 + t2 + (2 if n > 1 else 1)
-    rec_instr += 2 * (P - 1) + 3 * P + 6   # m*u tables, per-degree A/B, r2, rcp, rsqrt
-    return {"fma": fma, "rec_instr": rec_instr, "instr": fma + rec_instr, "flops": 2 * fma + 2 * rec_instr}
+from paper_1405_7487_b200.costs import m2l_flops_per_pair, t2n  # noqa: E402,F401
 
 
 P2P_FLOPS = 20      # 3 sub, |r|^2 (3 mul 2 add), rsqrt, q/r, q/r^3 (2 mul), phi add, 3 fma grad
@@ -242,7 +214,8 @@ def run_dist(args, cfg, rank, world, local):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 
     def step():
-        return D.solve([dpos], [dq], [rank * n])
+        # every step after the first partitions with the previous step's Eq. (1) weights
+        return D.solve([dpos], [dq], [rank * n], reuse_weights=True)
 
     for _ in range(args.warmup):
         step()
@@ -281,7 +254,7 @@ def run_dist(args, cfg, rank, world, local):
     for _ in range(e2e_steps):
         gp = hpos.to("cuda", non_blocking=True)
         gq = hq.to("cuda", non_blocking=True)
-        (phi, grad), = D.solve([gp], [gq], [rank * n])
+        (phi, grad), = D.solve([gp], [gq], [rank * n], reuse_weights=True)
         hphi.copy_(phi, non_blocking=True)
         hgrad.copy_(grad, non_blocking=True)
         torch.cuda.synchronize()

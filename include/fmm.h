@@ -180,6 +180,14 @@ fmm_status fmm_let_graft(fmm_ctx* ctx, int npeers, const void* const* src, const
 fmm_status fmm_let_unpack(fmm_ctx* ctx, int npeers, const void* const* src, const int64_t* bytes, void* stream);
 fmm_status fmm_let_remote(const fmm_ctx* ctx, int k, int64_t* base, int64_t* ncell, int64_t* nbody, uint32_t* orig);
 
+/* fmm_work: Eq. (1) weights of the last build for the next partition,
+ *   w[i] = l_i + alpha * r_i into w (device [n] fp32, caller order), where l_i / r_i count the
+ *   work of particle i's interaction lists with local / grafted-LET sources: 1 per P2P source
+ *   body of its leaf, c_m2l / |C| per M2L pair of its leaf or any ancestor C (c_m2l = cost of
+ *   one M2L pair in P2P interactions).  lr_sums (HOST [2], may be NULL): sum of l and of r;
+ *   synchronises when given.  Needs fmm_lists. */
+fmm_status fmm_work(fmm_ctx* ctx, double c_m2l, float alpha, float* w, double* lr_sums, void* stream);
+
 /* ---- timing (bench): per-phase device time from CUDA events recorded on the stream
  * each phase runs on.  enable != 0 turns recording on (small overhead).
  * fmm_phase_times fills up to `cap` entries of ms accumulated since the last reset and

@@ -456,3 +456,96 @@ fmm_status let_unpack(fmm_ctx* ctx, int npeers, const void* const* src, const in
     FMM_CUDA_TRY(ctx, cudaGetLastError());
     return FMM_OK;
 }
+
+// ---------------------------------------------------------------- Eq. (1) work weights
+// PAPER.md:108-115 Eq. (1): w_i = l_i + alpha * r_i, l_i / r_i the local / remote interaction
+// list sizes of particle i.  Here a list entry is weighted by its work:
+//   P2P: every source body of i's leaf counts 1 (one interaction);
+//   M2L: every pair (C <- B) of i's leaf or any ancestor C counts c_m2l / |C| (the pair's work,
+//        in P2P-interaction units, shared by the |C| particles below C);
+// local: sources of this rank's tree, remote: sources in grafted LETs (index >= ncell).
+namespace {
+__global__ void k_work_cells(int64_t nc, const uint64_t* __restrict__ off, const uint32_t* __restrict__ src,
+                             const uint32_t* __restrict__ bc, double c_m2l, double2* __restrict__ share) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    const uint64_t p0 = off[c], p1 = off[c + 1];
+    uint64_t nl = 0;
+    for (uint64_t p = p0; p < p1; ++p) nl += src[p] < (uint32_t)nc;
+    const double inv = bc[c] ? c_m2l / (double)bc[c] : 0.0;
+    share[c] = make_double2(inv * (double)nl, inv * (double)(p1 - p0 - nl));
+}
+
+template <typename Real>
+__global__ void k_work_leaves(int64_t nc, const uint32_t* __restrict__ leaf_ids, int64_t nleaf,
+                              const uint64_t* __restrict__ poff, const uint32_t* __restrict__ psrc,
+                              const uint32_t* __restrict__ bb, const uint32_t* __restrict__ bc,
+                              const int32_t* __restrict__ parent, const double2* __restrict__ share,
+                              const uint32_t* __restrict__ perm, float alpha, float* __restrict__ w,
+                              double* __restrict__ sums) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double sl = 0.0, sr = 0.0;
+    for (int64_t li = w0; li < nleaf; li += nw) {
+        const uint32_t a = leaf_ids[li];
+        double pl = 0.0, pr = 0.0;
+        for (uint64_t p = poff[a] + lane; p < poff[a + 1]; p += 32) {
+            const uint32_t b = psrc[p];
+            if (b < (uint32_t)nc) pl += bc[b];
+            else pr += bc[b];
+        }
+        for (int o = 16; o; o >>= 1) {
+            pl += __shfl_xor_sync(0xffffffffu, pl, o);
+            pr += __shfl_xor_sync(0xffffffffu, pr, o);
+        }
+        double ml = 0.0, mr = 0.0;
+        for (int32_t c = (int32_t)a; c >= 0; c = parent[c]) {
+            const double2 s = share[c];
+            ml += s.x;
+            mr += s.y;
+        }
+        const double l = pl + ml, r = pr + mr;
+        const uint32_t b0 = bb[a], m = bc[a];
+        for (uint32_t k = lane; k < m; k += 32) w[perm[b0 + k]] = (float)(l + (double)alpha * r);
+        if (lane == 0) {
+            sl += l * m;
+            sr += r * m;
+        }
+    }
+    if (lane == 0 && (sl != 0.0 || sr != 0.0)) {
+        atomicAdd(&sums[0], sl);
+        atomicAdd(&sums[1], sr);
+    }
+}
+}  // namespace
+
+extern "C" fmm_status fmm_work(fmm_ctx* ctx, double c_m2l, float alpha, float* w, double* lr_sums, void* stream) {
+    if (!ctx || !w || c_m2l < 0) return FMM_ERR_ARG;
+    if (!ctx->built) {
+        ctx->err = "fmm_work: needs the lists of a build";
+        return FMM_ERR_STATE;
+    }
+    if (lr_sums) lr_sums[0] = lr_sums[1] = 0.0;
+    if (ctx->n == 0) return FMM_OK;
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nc = ctx->ncell;
+    FMM_TRY(buf_ensure(ctx, ctx->let_tmp, (size_t)nc * 16 + 64));
+    double2* share = P_<double2>(ctx->let_tmp);
+    double* sums = reinterpret_cast<double*>(share + nc);
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(sums, 0, 16, s));
+    k_work_cells<<<blocks_for(nc, 256), 256, 0, s>>>(nc, P_<uint64_t>(ctx->m2l_off), P_<uint32_t>(ctx->m2l_src),
+                                                     P_<uint32_t>(ctx->c_bc), c_m2l, share);
+    const unsigned g = (unsigned)std::min<int64_t>((ctx->nleaf + 3) / 4, (int64_t)ctx->num_sms * 16);
+    k_work_leaves<float><<<std::max(g, 1u), 128, 0, s>>>(nc, P_<uint32_t>(ctx->leaf_ids), ctx->nleaf,
+                                                        P_<uint64_t>(ctx->p2p_off), P_<uint32_t>(ctx->p2p_src),
+                                                        P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc),
+                                                        P_<int32_t>(ctx->c_parent), share, ctx->d_perm, alpha, w, sums);
+    ctx->launches += 2;
+    FMM_CUDA_TRY(ctx, cudaGetLastError());
+    if (lr_sums) {
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(lr_sums, sums, 16, cudaMemcpyDeviceToHost, s));
+        FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    }
+    return FMM_OK;
+}

@@ -30,6 +30,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
+from .costs import m2l_cost_ratio
 from .fmm import FMM
 
 HIST_BITS = 16
@@ -180,11 +181,14 @@ class DistFMM:
     contexts' precision) returns phi[i], grad[i] in the caller's particle order."""
 
     def __init__(self, comm: Comm, n_max: int, P: int, theta: float, ncrit: int, prec: str = "f32",
-                 device: int = 0, hist_bits: int = HIST_BITS):
+                 device: int = 0, hist_bits: int = HIST_BITS, alpha: float = 1.0, c_m2l: float = None):
         self.comm, self.K = comm, comm.world
         self.fmm = [FMM(n_max, P, theta, ncrit, prec, device) for _ in comm.ranks]
         self.hist_bits = hist_bits
+        self.alpha = alpha                                        # Eq. (1)
+        self.c_m2l = m2l_cost_ratio(P) if c_m2l is None else c_m2l
         self.stats = {}
+        self.weights = None                                       # per local rank, owner order
 
     def close(self):
         for f in self.fmm:
@@ -298,28 +302,41 @@ class DistFMM:
         self.stats["let_data_bytes"] = sum(int(t.numel()) for row in sends for t in row)
         return out
 
-    # 7: results back to the owners, original order
-    def gather_back(self, res, back, packed, cnt, gid_base, n_in):
+    # 7: results (and the Eq. (1) weights of this step) back to the owners, original order
+    def gather_back(self, res, wts, back, packed, cnt, gid_base, n_in):
         cm = self.comm
         nl = len(self.fmm)
         sends = []
         for i in range(nl):
             phi, grad = res[i]
-            v = torch.cat([phi.reshape(-1, 1), grad], dim=1)   # [n, 4]
-            sends.append(list(v.reshape(-1).split([4 * s for s in back[i]])))
+            v = torch.cat([phi.reshape(-1, 1), grad, wts[i].to(phi.dtype).reshape(-1, 1)], dim=1)   # [n, 5]
+            sends.append(list(v.reshape(-1).split([5 * s for s in back[i]])))
         recv = cm.alltoallv(sends)
-        out = []
+        out, wout = [], []
         for i in range(nl):
-            v = torch.cat(recv[i]).reshape(-1, 4)              # in this rank's packed order
+            v = torch.cat(recv[i]).reshape(-1, 5)              # in this rank's packed order
             idx = packed[i][2] - gid_base[i]                    # original local index
-            r = torch.empty((n_in[i], 4), dtype=v.dtype, device=v.device)
+            r = torch.empty((n_in[i], 5), dtype=v.dtype, device=v.device)
             r[idx] = v
-            out.append((r[:, 0].contiguous(), r[:, 1:].contiguous()))
-        return out
+            out.append((r[:, 0].contiguous(), r[:, 1:4].contiguous()))
+            wout.append(r[:, 4].float().contiguous())
+        return out, wout
 
-    def solve(self, pos, q, gid_base, w=None):
+    def solve(self, pos, q, gid_base, w=None, reuse_weights=False):
+        """One distributed FMM step.  w: per-rank particle weights for the partition (None:
+        1, or with reuse_weights the Eq. (1) weights this object measured at its last step)."""
+        if w is None and reuse_weights and self.weights is not None:
+            w = self.weights
         lpos, lq, lgid, back, packed, cnt = self.partition(pos, q, gid_base, w)
         self.build(lpos)
         res = self.evaluate(lpos, lq)
+        wts = []
+        lr = np.zeros(2)
+        for f in self.fmm:
+            wi, s = f.work(self.c_m2l, self.alpha)
+            wts.append(wi)
+            lr += s
+        self.stats["work_local"], self.stats["work_remote"] = float(lr[0]), float(lr[1])
         self.local = (lpos, lq, lgid)
-        return self.gather_back(res, back, packed, cnt, gid_base, [p.shape[0] for p in pos])
+        out, self.weights = self.gather_back(res, wts, back, packed, cnt, gid_base, [p.shape[0] for p in pos])
+        return out

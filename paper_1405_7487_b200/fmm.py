@@ -55,6 +55,7 @@ SYMBOLS = {
     "fmm_let_graft": (_i, [_p, _i, _p, _p, _p]),
     "fmm_let_unpack": (_i, [_p, _i, _p, _p, _p]),
     "fmm_let_remote": (_i, [_p, _i, _p, _p, _p, _p]),
+    "fmm_work": (_i, [_p, _d, C.c_float, _p, _p, _p]),
 }
 LET_MAX_COVER = 73
 
@@ -303,6 +304,15 @@ class FMM:
             orig = np.zeros(nc.value, np.uint32)
             self._check(lib().fmm_let_remote(self._h, int(k), None, None, None, _np_ptr(orig)), "fmm_let_remote")
         return int(base.value), int(nc.value), int(nb.value), orig
+
+    def work(self, c_m2l: float, alpha: float = 1.0, out=None, stream=None):
+        """Eq. (1) weights of the last build (caller order) and the sums of l and r."""
+        import torch
+        w = torch.empty(self.n, dtype=torch.float32, device="cuda") if out is None else out
+        lr = np.zeros(2)
+        self._check(lib().fmm_work(self._h, float(c_m2l), float(alpha), C.c_void_p(w.data_ptr()), _np_ptr(lr),
+                                   C.c_void_p(self._stream(stream))), "fmm_work")
+        return w, lr
 
     # -- introspection -----------------------------------------------------
     def counts(self) -> dict:

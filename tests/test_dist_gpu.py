@@ -135,3 +135,79 @@ def test_let_needs_subset_of_remote_tree(torch_cuda):
             assert ncl < D.fmm[j].counts()["ncell"]
             assert nbd < D.fmm[j].counts()["n"]
             assert np.all(np.diff(orig.astype(np.int64)) > 0)   # sender order kept
+
+
+def _host_work(D, i, c, alpha):
+    """Eq. (1) weights of rank i recomputed on the host from its lists and cells."""
+    f = D.fmm[i]
+    cells = f.cells()
+    nci = len(cells["level"])
+    bc = cells["body_count"].astype(np.float64)
+    m2l, p2p = f.lists()
+    # body counts of every source index (local cells, then each grafted LET)
+    src_bc = {}
+    for k, j in enumerate(D._peers[i]):
+        base, ncl, _, orig = f.let_remote(k)
+        rb = D.fmm[j].cells()["body_count"].astype(np.float64)[orig]
+        for t in range(ncl):
+            src_bc[base + t] = rb[t]
+    def bcount(s):
+        return bc[s] if s < nci else src_bc[s]
+    ml = np.zeros(nci); mr = np.zeros(nci)
+    for a, b in m2l:
+        if b < nci:
+            ml[a] += c / bc[a]
+        else:
+            mr[a] += c / bc[a]
+    pl = np.zeros(nci); pr = np.zeros(nci)
+    for a, b in p2p:
+        if b < nci:
+            pl[a] += bcount(b)
+        else:
+            pr[a] += bcount(b)
+    _, perm = f.sorted()
+    w = np.zeros(f.counts()["n"])
+    for a in np.nonzero(cells["child_count"] == 0)[0]:
+        l, r = pl[a], pr[a]
+        x = a
+        while x >= 0:
+            l += ml[x]; r += mr[x]
+            x = cells["parent"][x]
+        b0, m = cells["body_begin"][a], cells["body_count"][a]
+        w[perm[b0:b0 + m]] = l + alpha * r
+    return w
+
+
+@pytest.mark.parametrize("K", [1, 3])
+def test_work_weights_eq1(torch_cuda, K):
+    """fmm_work (Eq. (1)) against the same weights recomputed from the lists."""
+    D, pos, q, phi, grad = run_dist(torch_cuda, "plummer", 6000, K, 4, 0.5, 16, "f64", 41 + K)
+    for i in range(K):
+        c, alpha = 37.5, 0.25
+        w, lr = D.fmm[i].work(c, alpha)
+        ref = _host_work(D, i, c, alpha)
+        np.testing.assert_allclose(w.cpu().numpy(), ref, rtol=2e-6)
+        if K == 1:
+            assert lr[1] == 0.0   # no remote sources on one rank
+
+
+def test_weighted_partition_balances_work(torch_cuda):
+    """Second step partitions with the first step's Eq. (1) weights: the ranks' shares of the
+    (first-step) work are balanced, where the unweighted split by particle count is not."""
+    import torch
+    from paper_1405_7487_b200.dist import DistFMM, LoopbackComm
+    n, K = 20000, 4
+    pos, q = synth.generate("plummer", n, 77, np.float64)
+    cuts = np.linspace(0, n, K + 1).astype(int)
+    P_in = [torch.from_numpy(pos[cuts[r]:cuts[r + 1]]).cuda() for r in range(K)]
+    Q_in = [torch.from_numpy(q[cuts[r]:cuts[r + 1]]).cuda() for r in range(K)]
+    D = DistFMM(LoopbackComm(K), n, 4, 0.5, 16, "f64")
+    D.solve(P_in, Q_in, [int(c) for c in cuts[:-1]])
+    w1 = np.concatenate([w.cpu().numpy() for w in D.weights]).astype(np.float64)   # owner order = global order
+    g1 = [g.cpu().numpy() for g in D.local[2]]
+    share1 = np.array([w1[g].sum() for g in g1]) / w1.sum()
+    D.solve(P_in, Q_in, [int(c) for c in cuts[:-1]], reuse_weights=True)
+    g2 = [g.cpu().numpy() for g in D.local[2]]
+    share2 = np.array([w1[g].sum() for g in g2]) / w1.sum()
+    assert np.abs(share2 - 1.0 / K).max() < 0.01, share2
+    assert np.abs(share1 - 1.0 / K).max() > np.abs(share2 - 1.0 / K).max(), (share1, share2)
