@@ -153,8 +153,9 @@ def workload_config(cfg, args, world=1):
          "precision": cfg["prec"], "seed": cfg["seed"], "l2": "flushed (256 MB write) before every timed step",
          "parallelism": "1 GPU"}
     if world > 1:
-        d["parallelism"] = (f"{world} GPUs, one FMM: Morton-range partition + LET exchange over NCCL "
-                            f"(weak scaling, {cfg['n']} particles per GPU)")
+        part = "ORB multisection" if getattr(args, "partitioner", "morton") == "orb" else "Morton-range"
+        d["parallelism"] = (f"{world} GPUs, one FMM: {part} partition with Eq. (1) weights + LET exchange over "
+                            f"NCCL (weak scaling, {cfg['n']} particles per GPU)")
         d["workload"] = ("BASELINE.json configs[3] (weak scaling, per-GPU size of " + CONFIG_NAMES[args.config] +
                          f"): 3D Laplace FMM, N={n} {cfg['kind']}, {cfg['prec']}, P={cfg['P']}, theta={cfg['theta']}, "
                          f"ncrit={cfg['ncrit']}")
@@ -208,7 +209,8 @@ def run_dist(args, cfg, rank, world, local):
     pos, q = synth.generate(cfg["kind"], n, cfg["seed"], dt_np, start=rank * n, n_total=N)
     dpos = torch.from_numpy(pos).cuda()
     dq = torch.from_numpy(q).cuda()
-    D = DistFMM(TorchComm(), N, cfg["P"], cfg["theta"], cfg["ncrit"], cfg["prec"], local)
+    D = DistFMM(TorchComm(), N, cfg["P"], cfg["theta"], cfg["ncrit"], cfg["prec"], local,
+                partitioner=args.partitioner)
     f = D.fmm[0]
     stream = torch.cuda.current_stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
@@ -293,6 +295,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist", action="store_true", help="use the distributed path even on 1 GPU")
+    ap.add_argument("--partitioner", default="morton", choices=["morton", "orb"],
+                    help="multi-GPU partition: Morton ranges (north_star) or ORB multisection (SURVEY 8f f3)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = synth.CONFIGS[args.config]

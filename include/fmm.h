@@ -148,6 +148,26 @@ fmm_status fmm_part_pack(fmm_ctx* ctx, const void* pos, const void* q, const uin
                          const uint64_t* splitters, int nranks, int64_t gid_base, void* out_pos, void* out_q,
                          int64_t* out_gid, int64_t* counts, void* stream);
 
+/* ORB multisection: particles carry a group id (device
+ * int32 [n], the rank range they will be split into); coordinates are the R3 21-bit
+ * quantised coordinates recovered from keys (fmm_part_keys).
+ * fmm_orb_histogram: hist (device [ngroups][2^bits] fp64, overwritten) += w (NULL = 1) of every
+ *   particle of group g with axis[g] >= 0 whose coordinate along axis[g] (0 x, 1 y, 2 z) has
+ *   its top prefix_bits bits equal to prefix[g], at the bin of its next `bits` bits
+ *   (HOST arrays axis, prefix [ngroups]; 1 <= bits <= 16, prefix_bits + bits <= 21).
+ * fmm_orb_split: particles of group g with axis[g] >= 0 and coordinate >= cut[g] move to
+ *   group right[g] (HOST arrays [ngroups]).
+ * fmm_part_pack_dest: as fmm_part_pack with the destination rank given per particle
+ *   (dest, device int32 [n], values < nranks).  All three synchronise. */
+fmm_status fmm_orb_histogram(fmm_ctx* ctx, const uint64_t* keys, const float* w, const int32_t* group, int64_t n,
+                             int ngroups, const int32_t* axis, const uint32_t* prefix, int prefix_bits, int bits,
+                             double* hist, void* stream);
+fmm_status fmm_orb_split(fmm_ctx* ctx, const uint64_t* keys, int32_t* group, int64_t n, int ngroups,
+                         const int32_t* axis, const uint32_t* cut, const int32_t* right, void* stream);
+fmm_status fmm_part_pack_dest(fmm_ctx* ctx, const void* pos, const void* q, const int32_t* dest, int64_t n,
+                              int nranks, int64_t gid_base, void* out_pos, void* out_q, int64_t* out_gid,
+                              int64_t* counts, void* stream);
+
 /* ---- multi-GPU: local essential tree (§II-C).
  * Sender-initiated: every rank publishes a cover of its local tree, every sender exports to
  * each receiver the part of its tree the receiver's traversal can need (let.cu states the

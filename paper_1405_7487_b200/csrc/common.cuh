@@ -137,7 +137,7 @@ struct fmm_ctx {
     int64_t nrem = 0, nrem_body = 0;
     std::vector<LetPeer> let_peers;
     std::vector<LetRemote> let_remote;
-    DevBuf let_tmp, let_cov, c_orig, part_tmp;
+    DevBuf let_tmp, let_cov, c_orig, part_tmp, orb_tmp;
     DevBuf h_stage;              // device staging for fmm_solve_host
 };
 

@@ -239,3 +239,151 @@ fmm_status fmm_part_pack(fmm_ctx* ctx, const void* pos, const void* q, const uin
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- ORB multisection (§8f f3)
+// PAPER.md:81, 94 §II-B: orthogonal recursive bisection along the longest axis with weighted
+// cuts, generalised to any rank count: a group of K ranks is cut at the
+// coordinate where the weight fraction reaches floor(K/2)/K.  Coordinates are the R3 21-bit
+// quantised coordinates of the global root cube, recovered from the Morton keys, so a cut is
+// exact and equal positions never separate.
+namespace {
+__device__ __forceinline__ uint32_t compact3(uint64_t x) {
+    x &= 0x1249249249249249ull;
+    x = (x | (x >> 2)) & 0x10C30C30C30C30C3ull;
+    x = (x | (x >> 4)) & 0x100F00F00F00F00Full;
+    x = (x | (x >> 8)) & 0x1F0000FF0000FFull;
+    x = (x | (x >> 16)) & 0x1F00000000FFFFull;
+    x = (x | (x >> 32)) & 0x1FFFFFull;
+    return (uint32_t)x;
+}
+
+__global__ void k_orb_hist(const uint64_t* __restrict__ keys, const float* __restrict__ w,
+                           const int32_t* __restrict__ grp, int64_t n, const int32_t* __restrict__ axis,
+                           const uint32_t* __restrict__ prefix, int pbits, int bits, double* __restrict__ hist) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t g = grp[i];
+        const int a = axis[g];
+        if (a < 0) continue;
+        const uint32_t c = compact3(keys[i] >> a);
+        if (pbits > 0 && (c >> (21 - pbits)) != prefix[g]) continue;
+        const uint32_t bin = (c >> (21 - pbits - bits)) & ((1u << bits) - 1);
+        atomicAdd(&hist[((size_t)g << bits) + bin], w ? (double)w[i] : 1.0);
+    }
+}
+
+__global__ void k_orb_split(const uint64_t* __restrict__ keys, int32_t* __restrict__ grp, int64_t n,
+                            const int32_t* __restrict__ axis, const uint32_t* __restrict__ cut,
+                            const int32_t* __restrict__ right) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t g = grp[i];
+        const int a = axis[g];
+        if (a < 0) continue;
+        if (compact3(keys[i] >> a) >= cut[g]) grp[i] = right[g];
+    }
+}
+
+template <typename Real>
+__global__ void k_part_gather_dest(const Real* __restrict__ pos, const Real* __restrict__ q,
+                                   const uint32_t* __restrict__ order, int64_t n, int64_t gid_base,
+                                   Real* __restrict__ opos, Real* __restrict__ oq, int64_t* __restrict__ ogid) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = order[k];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) opos[3 * k + d] = pos[3 * (int64_t)i + d];
+        oq[k] = q[i];
+        ogid[k] = gid_base + i;
+    }
+}
+
+__global__ void k_dest_keys(const int32_t* __restrict__ dest, int64_t n, uint64_t* __restrict__ dkey,
+                            uint32_t* __restrict__ idx, unsigned long long* counts) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        dkey[i] = (uint64_t)dest[i];
+        idx[i] = (uint32_t)i;
+        atomicAdd(&counts[dest[i]], 1ull);
+    }
+}
+}  // namespace
+
+extern "C" {
+
+fmm_status fmm_orb_histogram(fmm_ctx* ctx, const uint64_t* keys, const float* w, const int32_t* group, int64_t n,
+                             int ngroups, const int32_t* axis, const uint32_t* prefix, int prefix_bits, int bits,
+                             double* hist, void* stream) {
+    if (!ctx || ngroups < 1 || ngroups > 256 || !axis || !prefix || !hist || bits < 1 || bits > 16 ||
+        prefix_bits < 0 || prefix_bits + bits > 21 || n < 0 || (n > 0 && (!keys || !group)))
+        return FMM_ERR_ARG;
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    FMM_TRY(buf_ensure(ctx, ctx->orb_tmp, (size_t)256 * 12 + 64));
+    int32_t* dax = P_<int32_t>(ctx->orb_tmp);
+    uint32_t* dpre = reinterpret_cast<uint32_t*>(dax + 256);
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(dax, axis, (size_t)ngroups * 4, cudaMemcpyHostToDevice, s));
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(dpre, prefix, (size_t)ngroups * 4, cudaMemcpyHostToDevice, s));
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(hist, 0, ((size_t)ngroups << bits) * 8, s));
+    if (n > 0) {
+        k_orb_hist<<<grid_for(ctx, n), 256, 0, s>>>(keys, w, group, n, dax, dpre, prefix_bits, bits, hist);
+        FMM_LAUNCH(ctx);
+    }
+    FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));   // host arrays may be reused at return
+    return FMM_OK;
+}
+
+fmm_status fmm_orb_split(fmm_ctx* ctx, const uint64_t* keys, int32_t* group, int64_t n, int ngroups,
+                         const int32_t* axis, const uint32_t* cut, const int32_t* right, void* stream) {
+    if (!ctx || ngroups < 1 || ngroups > 256 || !axis || !cut || !right || n < 0 || (n > 0 && (!keys || !group)))
+        return FMM_ERR_ARG;
+    if (n == 0) return FMM_OK;
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    FMM_TRY(buf_ensure(ctx, ctx->orb_tmp, (size_t)256 * 12 + 64));
+    int32_t* dax = P_<int32_t>(ctx->orb_tmp);
+    uint32_t* dcut = reinterpret_cast<uint32_t*>(dax + 256);
+    int32_t* drt = reinterpret_cast<int32_t*>(dcut + 256);
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(dax, axis, (size_t)ngroups * 4, cudaMemcpyHostToDevice, s));
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(dcut, cut, (size_t)ngroups * 4, cudaMemcpyHostToDevice, s));
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(drt, right, (size_t)ngroups * 4, cudaMemcpyHostToDevice, s));
+    k_orb_split<<<grid_for(ctx, n), 256, 0, s>>>(keys, group, n, dax, dcut, drt);
+    FMM_LAUNCH(ctx);
+    FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    return FMM_OK;
+}
+
+fmm_status fmm_part_pack_dest(fmm_ctx* ctx, const void* pos, const void* q, const int32_t* dest, int64_t n,
+                              int nranks, int64_t gid_base, void* out_pos, void* out_q, int64_t* out_gid,
+                              int64_t* counts, void* stream) {
+    if (!ctx || nranks < 1 || nranks > 256 || !counts || n < 0 ||
+        (n > 0 && (!pos || !q || !dest || !out_pos || !out_q || !out_gid)))
+        return FMM_ERR_ARG;
+    for (int r = 0; r < nranks; ++r) counts[r] = 0;
+    if (n == 0) return FMM_OK;
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t need = (size_t)n * 24 + 256 * 8 + 64;
+    FMM_TRY(buf_ensure(ctx, ctx->part_tmp, need));
+    uint64_t* k0 = P_<uint64_t>(ctx->part_tmp);
+    uint64_t* k1 = k0 + n;
+    uint32_t* v0 = reinterpret_cast<uint32_t*>(k1 + n);
+    uint32_t* v1 = v0 + n;
+    unsigned long long* dcnt = reinterpret_cast<unsigned long long*>(v1 + n);   // byte offset 24n
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(dcnt, 0, (size_t)nranks * 8, s));
+    k_dest_keys<<<grid_for(ctx, n), 256, 0, s>>>(dest, n, k0, v0, dcnt);
+    FMM_LAUNCH(ctx);
+    uint64_t* kout = nullptr;
+    uint32_t* order = nullptr;
+    FMM_TRY(radix_sort_pairs(ctx, k0, k1, v0, v1, n, 0, 8, &kout, &order, s));
+    if (ctx->prec == FMM_F32)
+        k_part_gather_dest<float><<<grid_for(ctx, n), 256, 0, s>>>((const float*)pos, (const float*)q, order, n,
+                                                                  gid_base, (float*)out_pos, (float*)out_q, out_gid);
+    else
+        k_part_gather_dest<double><<<grid_for(ctx, n), 256, 0, s>>>((const double*)pos, (const double*)q, order, n,
+                                                                   gid_base, (double*)out_pos, (double*)out_q, out_gid);
+    FMM_LAUNCH(ctx);
+    std::vector<unsigned long long> hc(nranks);
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(hc.data(), dcnt, (size_t)nranks * 8, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    for (int r = 0; r < nranks; ++r) counts[r] = (int64_t)hc[r];
+    return FMM_OK;
+}
+
+}  // extern "C"

@@ -173,6 +173,70 @@ def partition_splitters(hist_fn, nranks: int, bits: int = HIST_BITS, tol: float 
     return np.maximum.accumulate(out)
 
 
+COORD_BITS = 21   # R3 quantised coordinates
+
+
+def orb_plan(hist_fn, split_fn, nranks: int, bits: int = 16):
+    """ORB multisection for any rank count.
+
+    Group ids are the first rank of the group's rank range, so after the last round a
+    particle's group is its rank.  Every round, each group of Kg > 1 ranks is cut along the
+    longest axis of its box (quantised coordinates, ties to the lower axis) where the global
+    weight fraction reaches floor(Kg/2)/Kg; the cut coordinate is refined `bits` then the
+    remaining bits (the same histogram refinement as partition_splitters) and particles with
+    coordinate >= cut take the right half's id.
+      hist_fn(axis[K], prefix[K], prefix_bits, bits) -> [K, 2^bits] global weights
+      split_fn(axis[K], cut[K], right[K])
+    Returns the list of groups {r0, r1, lo, hi} (boxes in quantised coordinates)."""
+    K = nranks
+    full = 1 << COORD_BITS
+    groups = {0: dict(r0=0, r1=K, lo=[0, 0, 0], hi=[full, full, full])}
+    while any(g["r1"] - g["r0"] > 1 for g in groups.values()):
+        axis = np.full(K, -1, np.int32)
+        frac = np.zeros(K)
+        for gid, g in groups.items():
+            if g["r1"] - g["r0"] > 1:
+                ext = [g["hi"][a] - g["lo"][a] for a in range(3)]
+                axis[gid] = int(np.argmax(ext))
+                frac[gid] = ((g["r1"] - g["r0"]) // 2) / (g["r1"] - g["r0"])
+        prefix = np.zeros(K, np.uint32)
+        h = np.asarray(hist_fn(axis, prefix, 0, bits))
+        total = h.sum(axis=1)
+        resid = total * frac
+        for gid in groups:
+            if axis[gid] >= 0:
+                b, r = choose_bins(h[gid], resid[gid:gid + 1]) if total[gid] > 0 else (np.array([0]), np.array([0.0]))
+                prefix[gid] = int(b[0])
+                resid[gid] = r[0]
+        nb = COORD_BITS - bits
+        h2 = np.asarray(hist_fn(axis, prefix, bits, nb))
+        cut = np.zeros(K, np.uint32)
+        right = np.zeros(K, np.int32)
+        new = {}
+        for gid, g in list(groups.items()):
+            if axis[gid] < 0:
+                new[gid] = g
+                continue
+            a = int(axis[gid])
+            if total[gid] > 0:
+                b2, _ = choose_bins(h2[gid], resid[gid:gid + 1])
+                c = (int(prefix[gid]) << nb) | int(b2[0])
+            else:
+                c = (g["lo"][a] + g["hi"][a]) // 2
+            c = min(max(c, g["lo"][a]), g["hi"][a])
+            kl = (g["r1"] - g["r0"]) // 2
+            rid = g["r0"] + kl
+            cut[gid], right[gid] = c, rid
+            lo_r, hi_l = list(g["lo"]), list(g["hi"])
+            hi_l[a] = c
+            lo_r[a] = c
+            new[gid] = dict(r0=g["r0"], r1=rid, lo=g["lo"], hi=hi_l)
+            new[rid] = dict(r0=rid, r1=g["r1"], lo=lo_r, hi=g["hi"])
+        split_fn(axis, cut, right)
+        groups = new
+    return groups
+
+
 # ------------------------------------------------------------------ driver
 class DistFMM:
     """The FMM on `comm.world` ranks; this process drives the ranks `comm.ranks`.
@@ -181,7 +245,11 @@ class DistFMM:
     contexts' precision) returns phi[i], grad[i] in the caller's particle order."""
 
     def __init__(self, comm: Comm, n_max: int, P: int, theta: float, ncrit: int, prec: str = "f32",
-                 device: int = 0, hist_bits: int = HIST_BITS, alpha: float = 1.0, c_m2l: float = None):
+                 device: int = 0, hist_bits: int = HIST_BITS, alpha: float = 1.0, c_m2l: float = None,
+                 partitioner: str = "morton"):
+        if partitioner not in ("morton", "orb"):
+            raise ValueError("partitioner must be 'morton' (Morton ranges) or 'orb' (multisection)")
+        self.partitioner = partitioner
         self.comm, self.K = comm, comm.world
         self.fmm = [FMM(n_max, P, theta, ncrit, prec, device) for _ in comm.ranks]
         self.hist_bits = hist_bits
@@ -213,9 +281,23 @@ class DistFMM:
                 loc.append(h)
             return cm.allreduce(loc, "sum")[0].cpu().numpy()
 
-        s = partition_splitters(hist_fn, K, self.hist_bits)
-        spl = [s for _ in range(nl)]
-        packed = [F[i].part_pack(pos[i], q[i], keys[i], spl[i], K, gid_base[i]) for i in range(nl)]
+        if self.partitioner == "morton":
+            s = partition_splitters(hist_fn, K, self.hist_bits)
+            packed = [F[i].part_pack(pos[i], q[i], keys[i], s, K, gid_base[i]) for i in range(nl)]
+        else:
+            grp = [torch.zeros(keys[i].shape[0], dtype=torch.int32, device=keys[i].device) for i in range(nl)]
+
+            def orb_hist(axis, prefix, pbits, bits):
+                loc = [F[i].orb_histogram(keys[i], grp[i], axis, prefix, pbits, bits,
+                                          None if w is None else w[i]) for i in range(nl)]
+                return cm.allreduce(loc, "sum")[0].cpu().numpy()
+
+            def orb_split(axis, cut, right):
+                for i in range(nl):
+                    F[i].orb_split(keys[i], grp[i], axis, cut, right)
+
+            self.orb_groups = orb_plan(orb_hist, orb_split, K, self.hist_bits)
+            packed = [F[i].part_pack_dest(pos[i], q[i], grp[i], K, gid_base[i]) for i in range(nl)]
         cnt = [p[3] for p in packed]
         sp = cm.alltoallv([list(packed[i][0].reshape(-1).split((cnt[i] * 3).tolist())) for i in range(nl)])
         sq = cm.alltoallv([list(packed[i][1].split(cnt[i].tolist())) for i in range(nl)])

@@ -56,6 +56,9 @@ SYMBOLS = {
     "fmm_let_unpack": (_i, [_p, _i, _p, _p, _p]),
     "fmm_let_remote": (_i, [_p, _i, _p, _p, _p, _p]),
     "fmm_work": (_i, [_p, _d, C.c_float, _p, _p, _p]),
+    "fmm_orb_histogram": (_i, [_p, _p, _p, _p, _i64, _i, _p, _p, _i, _i, _p, _p]),
+    "fmm_orb_split": (_i, [_p, _p, _p, _i64, _i, _p, _p, _p, _p]),
+    "fmm_part_pack_dest": (_i, [_p, _p, _p, _p, _i64, _i, _i64, _p, _p, _p, _p, _p]),
 }
 LET_MAX_COVER = 73
 
@@ -255,6 +258,40 @@ class FMM:
                                         C.c_void_p(opos.data_ptr()), C.c_void_p(oq.data_ptr()),
                                         C.c_void_p(gid.data_ptr()), _np_ptr(counts), C.c_void_p(self._stream(stream))),
                     "fmm_part_pack")
+        return opos, oq, gid, counts
+
+    def orb_histogram(self, keys, group, axis, prefix, prefix_bits, bits, w=None, stream=None):
+        import torch
+        ng = len(axis)
+        ax = np.ascontiguousarray(axis, dtype=np.int32); pre = np.ascontiguousarray(prefix, dtype=np.uint32)
+        hist = torch.empty((ng, 1 << bits), dtype=torch.float64, device=keys.device)
+        wp = None if w is None else C.c_void_p(w.data_ptr())
+        self._check(lib().fmm_orb_histogram(self._h, C.c_void_p(keys.data_ptr()), wp, C.c_void_p(group.data_ptr()),
+                                            keys.shape[0], ng, _np_ptr(ax), _np_ptr(pre), int(prefix_bits), int(bits),
+                                            C.c_void_p(hist.data_ptr()), C.c_void_p(self._stream(stream))),
+                    "fmm_orb_histogram")
+        return hist
+
+    def orb_split(self, keys, group, axis, cut, right, stream=None):
+        ax = np.ascontiguousarray(axis, dtype=np.int32); ct = np.ascontiguousarray(cut, dtype=np.uint32)
+        rt = np.ascontiguousarray(right, dtype=np.int32)
+        self._check(lib().fmm_orb_split(self._h, C.c_void_p(keys.data_ptr()), C.c_void_p(group.data_ptr()),
+                                        keys.shape[0], len(ax), _np_ptr(ax), _np_ptr(ct), _np_ptr(rt),
+                                        C.c_void_p(self._stream(stream))), "fmm_orb_split")
+
+    def part_pack_dest(self, pos, q, dest, nranks: int, gid_base: int, stream=None):
+        import torch
+        n = pos.shape[0]
+        self._check_tensor(pos, (n, 3), "pos")
+        self._check_tensor(q, (n,), "q")
+        opos = torch.empty_like(pos); oq = torch.empty_like(q)
+        gid = torch.empty(n, dtype=torch.int64, device=pos.device)
+        counts = np.zeros(nranks, np.int64)
+        self._check(lib().fmm_part_pack_dest(self._h, C.c_void_p(pos.data_ptr()), C.c_void_p(q.data_ptr()),
+                                             C.c_void_p(dest.data_ptr()), n, int(nranks), int(gid_base),
+                                             C.c_void_p(opos.data_ptr()), C.c_void_p(oq.data_ptr()),
+                                             C.c_void_p(gid.data_ptr()), _np_ptr(counts),
+                                             C.c_void_p(self._stream(stream))), "fmm_part_pack_dest")
         return opos, oq, gid, counts
 
     # -- multi-GPU: local essential tree (let.cu) -------------------------------

@@ -127,3 +127,51 @@ def test_torchcomm_gloo_matches_loopback():
         assert g == [t.tolist() for t in lg[r]]
         assert recv == [t.tolist() for t in lr[r]] == recv2
         assert recv[1 - r] == [16 * (1 - r) + r] * ((1 - r) * 3 + r + 1)
+
+
+def _coords(keys):
+    """R3 quantised coordinates from 63-bit Morton keys (x -> bit 0 of each octal digit)."""
+    out = np.zeros((len(keys), 3), dtype=np.int64)
+    for a in range(3):
+        c = np.zeros(len(keys), dtype=np.int64)
+        for l in range(21):
+            c |= (((keys >> np.uint64(3 * l + a)) & np.uint64(1)).astype(np.int64)) << l
+        out[:, a] = c
+    return out
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("kind", ["cube", "plummer"])
+def test_orb_plan_balanced_boxes(K, kind):
+    from paper_1405_7487_b200.dist import orb_plan
+    pos, _ = synth.generate(kind, 12000, 9)
+    xyz = _coords(oracle.keys(pos))
+    w = 1.0 + (pos[:, 0] > np.median(pos[:, 0]))          # uneven weights
+    grp = np.zeros(len(pos), dtype=np.int64)
+
+    def hist_fn(axis, prefix, pbits, bits):
+        out = np.zeros((K, 1 << bits))
+        for g in range(K):
+            if axis[g] < 0:
+                continue
+            c = xyz[:, axis[g]]
+            sel = grp == g
+            if pbits:
+                sel &= (c >> (21 - pbits)) == prefix[g]
+            b = (c[sel] >> (21 - pbits - bits)) & ((1 << bits) - 1)
+            out[g] = np.bincount(b, weights=w[sel], minlength=1 << bits)
+        return out
+
+    def split_fn(axis, cut, right):
+        for g in range(K):
+            if axis[g] >= 0:
+                m = (grp == g) & (xyz[:, axis[g]] >= cut[g])
+                grp[m] = right[g]
+
+    groups = orb_plan(hist_fn, split_fn, K)
+    assert sorted(groups) == list(range(K))
+    share = np.array([w[grp == r].sum() for r in range(K)]) / w.sum()
+    assert np.abs(share - 1.0 / K).max() < 0.01, share
+    for r, g in groups.items():               # every particle lies in its rank's box
+        m = grp == r
+        assert np.all((xyz[m] >= np.array(g["lo"])) & (xyz[m] < np.array(g["hi"])))

@@ -27,7 +27,7 @@ def torch_cuda():
     return torch
 
 
-def run_dist(torch, kind, n, K, P, theta, ncrit, prec, seed):
+def run_dist(torch, kind, n, K, P, theta, ncrit, prec, seed, part="morton"):
     from paper_1405_7487_b200.dist import DistFMM, LoopbackComm
     dt = np.float32 if prec == "f32" else np.float64
     tdt = torch.float32 if prec == "f32" else torch.float64
@@ -36,7 +36,7 @@ def run_dist(torch, kind, n, K, P, theta, ncrit, prec, seed):
     cuts = np.linspace(0, n, K + 1).astype(int)
     P_in = [torch.from_numpy(pos[cuts[r]:cuts[r + 1]]).cuda() for r in range(K)]
     Q_in = [torch.from_numpy(q[cuts[r]:cuts[r + 1]]).cuda() for r in range(K)]
-    D = DistFMM(LoopbackComm(K), n, P, theta, ncrit, prec)
+    D = DistFMM(LoopbackComm(K), n, P, theta, ncrit, prec, partitioner=part)
     out = D.solve(P_in, Q_in, [int(c) for c in cuts[:-1]])
     torch.cuda.synchronize()
     phi = np.concatenate([o[0].cpu().numpy() for o in out]).astype(np.float64)
@@ -45,19 +45,23 @@ def run_dist(torch, kind, n, K, P, theta, ncrit, prec, seed):
 
 
 CASES = [
-    # kind, n, K, P, theta, ncrit, prec
-    ("cube", 6000, 2, 4, 0.5, 32, "f64"),
-    ("cube", 9000, 3, 6, 0.4, 16, "f64"),
-    ("plummer", 8000, 4, 5, 0.5, 16, "f64"),
-    ("cube", 20000, 4, 10, 0.4, 64, "f32"),
-    ("plummer", 12000, 3, 10, 0.4, 64, "f32"),
-    ("sphere", 5000, 2, 4, 0.6, 8, "f32"),
+    # kind, n, K, P, theta, ncrit, prec, partitioner
+    ("cube", 6000, 2, 4, 0.5, 32, "f64", "morton"),
+    ("cube", 9000, 3, 6, 0.4, 16, "f64", "morton"),
+    ("plummer", 8000, 4, 5, 0.5, 16, "f64", "morton"),
+    ("cube", 20000, 4, 10, 0.4, 64, "f32", "morton"),
+    ("plummer", 12000, 3, 10, 0.4, 64, "f32", "morton"),
+    ("sphere", 5000, 2, 4, 0.6, 8, "f32", "morton"),
+    # ORB multisection, including non-power-of-two rank counts
+    ("cube", 9000, 3, 6, 0.4, 16, "f64", "orb"),
+    ("plummer", 12000, 5, 10, 0.4, 64, "f32", "orb"),
+    ("sphere", 6000, 4, 4, 0.6, 8, "f64", "orb"),
 ]
 
 
-@pytest.mark.parametrize("kind,n,K,P,theta,ncrit,prec", CASES)
-def test_dist_lists_and_fields(torch_cuda, kind, n, K, P, theta, ncrit, prec):
-    D, pos, q, phi, grad = run_dist(torch_cuda, kind, n, K, P, theta, ncrit, prec, 500 + n + K)
+@pytest.mark.parametrize("kind,n,K,P,theta,ncrit,prec,part", CASES)
+def test_dist_lists_and_fields(torch_cuda, kind, n, K, P, theta, ncrit, prec, part):
+    D, pos, q, phi, grad = run_dist(torch_cuda, kind, n, K, P, theta, ncrit, prec, 500 + n + K, part)
     lpos, lq, lgid = D.local
     gids = [g.cpu().numpy() for g in lgid]
     # every particle lands on exactly one rank, and the ranks are Morton ranges of similar size
@@ -65,6 +69,16 @@ def test_dist_lists_and_fields(torch_cuda, kind, n, K, P, theta, ncrit, prec):
     np.testing.assert_array_equal(allg, np.arange(n))
     sizes = np.array([len(g) for g in gids])
     assert sizes.min() >= 0.5 * n / K, sizes
+    if part == "orb":   # ORB boxes are axis-aligned and disjoint: each rank's particles lie in its box
+        from oracle import keys as okeys
+        k = okeys(pos.astype(np.float64))
+        for r, g in D.orb_groups.items():
+            kk = k[gids[r]]
+            for a in range(3):
+                c = np.zeros(len(kk), dtype=np.int64)
+                for l in range(21):
+                    c |= (((kk >> np.uint64(3 * l + a)) & np.uint64(1)).astype(np.int64)) << l
+                assert np.all((c >= g["lo"][a]) & (c < g["hi"][a]))
     # oracle trees of every rank, built from the rank's particles in the order the rank holds them
     O = [oracle.FMM(pos[g].astype(np.float64), q[g].astype(np.float64), P, theta, ncrit) for g in gids]
     for i in range(K):
