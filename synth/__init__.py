@@ -102,4 +102,6 @@ CONFIGS = {
     "c1": dict(kind="cube", n=4096, P=4, theta=0.5, ncrit=32, prec="f64", seed=1),
     "c2": dict(kind="cube", n=1 << 20, P=10, theta=0.4, ncrit=64, prec="f32", seed=2),
     "c3": dict(kind="plummer", n=10_000_000, P=10, theta=0.4, ncrit=64, prec="f32", seed=3),
+    # Table I case 2: sphere surface, P=10, theta=0.4, ncrit=512
+    "sph": dict(kind="sphere", n=1 << 22, P=10, theta=0.4, ncrit=512, prec="f32", seed=5),
 }

@@ -65,6 +65,7 @@ CASES = [
     ("cube", 700, 16, 0.5, 32, "f64"),       # maximum P
     ("plummer", 64, 3, 0.5, 64, "f32"),      # single leaf = direct sum
     ("cube", 7, 4, 0.5, 2, "f64"),
+    ("sphere", 30000, 10, 0.4, 512, "f32"),  # Table I case 2 parameters (ncrit 512 leaves)
 ]
 
 
