@@ -84,6 +84,12 @@ fmm_status fmm_build(fmm_ctx* ctx, const void* pos, int64_t n, void* stream);
  *   target ascending: local cells, then LET 0, LET 1, ... in their sender's order).
  * fmm_build(pos, n) == fmm_build_tree + fmm_dtt(0) + fmm_lists. */
 fmm_status fmm_build_tree(fmm_ctx* ctx, const void* pos, int64_t n, void* stream);
+/* fmm_set_root_bounds: later builds take the R2 root cube from these bounds (HOST [6]: lo xyz,
+ *   hi xyz) instead of the particles' own min/max -- for a Morton-range partition, the global
+ *   box, so every rank's local tree is a subtree of one global octree (HOT, PAPER.md:83-92;
+ *   DESIGN.md §2 reading 9).  NULL restores the default.  A build whose particles lie outside
+ *   the bounds returns FMM_ERR_ARG. */
+fmm_status fmm_set_root_bounds(fmm_ctx* ctx, const double* bounds);
 fmm_status fmm_dtt(fmm_ctx* ctx, int remote, void* stream);
 fmm_status fmm_lists(fmm_ctx* ctx, void* stream);
 
@@ -183,10 +189,12 @@ fmm_status fmm_part_pack_dest(fmm_ctx* ctx, const void* pos, const void* q, cons
  * fmm_let_pack_data: writes the data message (fp64 multipoles, body charges) to dst
  *   (device, data_bytes); needs fmm_upward.
  * fmm_let_graft: appends the npeers received structure messages (device pointers src[k] of
- *   bytes[k] bytes, HOST arrays) after the local cells and bodies, replacing earlier
- *   grafts; then fmm_dtt(remote = 1) and fmm_lists.  Synchronises.
- * fmm_let_unpack: writes the received data messages (same order as the graft) into the
- *   grafted cells and bodies; call after fmm_upward, before fmm_interact.
+ *   bytes[k] bytes, HOST arrays) after the local cells, bodies and the LETs grafted earlier
+ *   in this build (fragments may arrive one by one: PAPER.md:129-149, the per-message `when`);
+ *   then fmm_dtt(remote = 1), which traverses the LETs grafted since its last call, and
+ *   fmm_lists once all have arrived.  Synchronises.
+ * fmm_let_unpack: writes npeers received data messages into grafted LETs first ..
+ *   first + npeers - 1 (graft order); call after fmm_upward, before fmm_interact.
  * fmm_let_remote: grafted LET k: first cell index, cell and body counts, and (HOST [ncell],
  *   may be NULL) the sender's cell index of each grafted cell (parity tests). */
 #define FMM_LET_MAX_COVER 73
@@ -197,7 +205,8 @@ fmm_status fmm_let_plan(fmm_ctx* ctx, int peer, const double* cover, int ncover,
 fmm_status fmm_let_pack_struct(fmm_ctx* ctx, int peer, void* dst, void* stream);
 fmm_status fmm_let_pack_data(fmm_ctx* ctx, int peer, void* dst, void* stream);
 fmm_status fmm_let_graft(fmm_ctx* ctx, int npeers, const void* const* src, const int64_t* bytes, void* stream);
-fmm_status fmm_let_unpack(fmm_ctx* ctx, int npeers, const void* const* src, const int64_t* bytes, void* stream);
+fmm_status fmm_let_unpack(fmm_ctx* ctx, int first, int npeers, const void* const* src, const int64_t* bytes,
+                          void* stream);
 fmm_status fmm_let_remote(const fmm_ctx* ctx, int k, int64_t* base, int64_t* ncell, int64_t* nbody, uint32_t* orig);
 
 /* fmm_work: Eq. (1) weights of the last build for the next partition,

@@ -50,6 +50,7 @@ def lib():
             "ofmm_p2p": (None, [i64, p, i64, p, p, p, p]),
             "ofmm_direct": (None, [i64, p, p, p, i64, p, p]),
             "ofmm_create": (p, [i64, p, p, i32, dbl, i32]),
+            "ofmm_create_in": (p, [i64, p, p, i32, dbl, i32, p]),
             "ofmm_destroy": (None, [p]),
             "ofmm_traverse": (i32, [p]),
             "ofmm_evaluate": (i32, [p, p, i64, p, p]),
@@ -170,10 +171,14 @@ def direct(pos, q, targets=None):
 class FMM:
     """The whole method on one set of particles: create (R2-R7), traverse (R8-R10), evaluate (R12-R18)."""
 
-    def __init__(self, pos, q, P: int, theta: float, ncrit: int):
+    def __init__(self, pos, q, P: int, theta: float, ncrit: int, bounds=None):
+        """bounds (lo xyz, hi xyz): the box the R2 root cube is taken from (default: the
+        particles' own min/max)."""
         self.pos, self.q = _d(pos).reshape(-1, 3), _d(q).reshape(-1)
         self.n, self.P = self.pos.shape[0], P
-        self._h = lib().ofmm_create(self.n, _ptr(self.pos), _ptr(self.q), P, float(theta), ncrit)
+        self._bounds = None if bounds is None else _d(bounds).reshape(6)
+        self._h = lib().ofmm_create_in(self.n, _ptr(self.pos), _ptr(self.q), P, float(theta), ncrit,
+                                       None if self._bounds is None else _ptr(self._bounds))
         if not self._h:
             raise ValueError("oracle rejected arguments")
         self._traversed = False

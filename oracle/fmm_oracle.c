@@ -83,10 +83,12 @@ static void bounds(int64_t n, const double* pos, double lo[3], double hi[3]) {
         }
 }
 
-/* R2: c0 = (lo+hi)*0.5, h = 0.5*max_d(hi_d-lo_d) (1 if 0), origin = c0 - h, s = 2^20/h. */
-void ofmm_root_cube(int64_t n, const double* pos, double o[3], double* scale, double* hout) {
-    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, c0[3];
-    if (n > 0) bounds(n, pos, lo, hi);
+/* R2: c0 = (lo+hi)*0.5, h = 0.5*max_d(hi_d-lo_d) (1 if 0), origin = c0 - h, s = 2^20/h,
+ * where lo/hi are the particles' own min/max, or given bounds (the GLOBAL box, so that the
+ * local trees of a Morton-range partition are subtrees of one global octree; DESIGN.md §2
+ * reading 9). */
+static void root_cube_of(const double lo[3], const double hi[3], double o[3], double* scale, double* hout) {
+    double c0[3];
     double ext = 0.0;
     for (int d = 0; d < 3; ++d) {
         c0[d] = (lo[d] + hi[d]) * 0.5;
@@ -98,6 +100,12 @@ void ofmm_root_cube(int64_t n, const double* pos, double o[3], double* scale, do
     for (int d = 0; d < 3; ++d) o[d] = c0[d] - h;
     *scale = 1048576.0 / h;
     *hout = h;
+}
+
+void ofmm_root_cube(int64_t n, const double* pos, double o[3], double* scale, double* hout) {
+    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    if (n > 0) bounds(n, pos, lo, hi);
+    root_cube_of(lo, hi, o, scale, hout);
 }
 
 /* R3: i_d = clamp(floor((x_d - o_d) * s), 0, 2^21 - 1). */
@@ -122,13 +130,17 @@ static uint64_t interleave(uint32_t ix, uint32_t iy, uint32_t iz) {
     return key;
 }
 
-void ofmm_keys(int64_t n, const double* pos, uint64_t* keys) {
+/* keys under the root cube of `root` (lo xyz, hi xyz) or, when NULL, of the particles' own bounds */
+static void keys_in(int64_t n, const double* pos, const double* root, uint64_t* keys) {
     double o[3], s, h;
-    ofmm_root_cube(n, pos, o, &s, &h);
+    if (root) root_cube_of(root, root + 3, o, &s, &h);
+    else ofmm_root_cube(n, pos, o, &s, &h);
     for (int64_t i = 0; i < n; ++i)
         keys[i] = interleave(quantise(pos[3 * i], o[0], s), quantise(pos[3 * i + 1], o[1], s),
                              quantise(pos[3 * i + 2], o[2], s));
 }
+
+void ofmm_keys(int64_t n, const double* pos, uint64_t* keys) { keys_in(n, pos, NULL, keys); }
 
 /* -------------------------------------------------------------- R12-R17 ---- */
 /* R12: M_beta(C) += sum_j q_j (x_j - c)^beta / beta! */
@@ -363,7 +375,16 @@ static int cmp_lvlkey(const void* a, const void* b) {
 }
 
 ofmm* ofmm_create(int64_t n, const double* pos, const double* q, int P, double theta, int ncrit) {
+    return ofmm_create_in(n, pos, q, P, theta, ncrit, NULL);
+}
+
+ofmm* ofmm_create_in(int64_t n, const double* pos, const double* q, int P, double theta, int ncrit,
+                     const double* root) {
     if (n < 0 || P < 1 || P > OFMM_MAXP || !(theta > 0.0 && theta < 1.0) || ncrit < 1) return NULL;
+    if (root)
+        for (int64_t i = 0; i < n; ++i)
+            for (int d = 0; d < 3; ++d)
+                if (pos[3 * i + d] < root[d] || pos[3 * i + d] > root[3 + d]) return NULL;   /* outside */
     ofmm* o = calloc(1, sizeof(ofmm));
     o->n = n; o->P = P; o->theta = theta; o->ncrit = ncrit;
     o->t = malloc(sizeof(mtab));
@@ -376,7 +397,7 @@ ofmm* ofmm_create(int64_t n, const double* pos, const double* q, int P, double t
 
     /* R2-R4 keys, R5 stable sort (ties by original index) */
     uint64_t* k0 = malloc((size_t)n * sizeof(uint64_t));
-    ofmm_keys(n, pos, k0);
+    keys_in(n, pos, root, k0);
     keyidx* ki = malloc((size_t)n * sizeof(keyidx));
     for (int64_t i = 0; i < n; ++i) { ki[i].key = k0[i]; ki[i].idx = (uint32_t)i; }
     qsort(ki, (size_t)n, sizeof(keyidx), cmp_keyidx);

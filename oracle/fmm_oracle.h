@@ -50,6 +50,10 @@ void ofmm_direct(int64_t n, const double* pos, const double* q, const int64_t* t
 /* Whole method.  create: keys, stable sort, recursive tree, geometry (R2-R7).
  * Returns NULL on bad arguments (P outside 1..16, theta outside (0,1), ncrit < 1, n < 0). */
 ofmm* ofmm_create(int64_t n, const double* pos, const double* q, int P, double theta, int ncrit);
+/* the same with the R2 root cube taken from given bounds root[6] = lo xyz, hi xyz (NULL: the
+ * particles' own bounds); NULL result if a particle lies outside them */
+ofmm* ofmm_create_in(int64_t n, const double* pos, const double* q, int P, double theta, int ncrit,
+                     const double* root);
 void  ofmm_destroy(ofmm*);
 /* R8-R10: recursive dual tree traversal from (root, root); lists in canonical order. */
 int   ofmm_traverse(ofmm*);

@@ -5,6 +5,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cmath>
+
 #include "common.cuh"
 
 #define FMM_VERSION 1
@@ -144,7 +146,7 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
                       &ctx->run_len64, &ctx->dcount2, &ctx->tcnt, &ctx->cnt64, &ctx->big_off, &ctx->M, &ctx->L, &ctx->Mr, &ctx->Lr, &ctx->near_phi, &ctx->near_grad,
                       &ctx->h_stage};
     for (DevBuf* b : bufs) buf_free(*b);
-    DevBuf* lbufs[] = {&ctx->let_tmp, &ctx->let_cov, &ctx->c_orig, &ctx->part_tmp, &ctx->seg_lists, &ctx->orb_tmp};
+    DevBuf* lbufs[] = {&ctx->let_tmp, &ctx->let_cov, &ctx->c_orig, &ctx->part_tmp, &ctx->seg_lists, &ctx->orb_tmp, &ctx->root_given};
     for (DevBuf* b : lbufs) buf_free(*b);
     for (auto& lp : ctx->let_peers) {
         DevBuf* pb[] = {&lp.opened, &lp.eflag, &lp.eidx, &lp.bflag, &lp.boff};
@@ -184,6 +186,7 @@ fmm_status fmm_build_tree(fmm_ctx* ctx, const void* pos, int64_t n, void* stream
     ctx->ncell = ctx->nleaf = ctx->depth = ctx->n_m2l = ctx->n_p2p = ctx->p2p_inter = 0;
     ctx->nrem = ctx->nrem_body = 0;
     ctx->let_remote.clear();
+    ctx->let_traversed = 0;
     for (auto& lp : ctx->let_peers) lp.planned = false;
     ctx->level_begin.clear();
     if (n > 0) {
@@ -191,6 +194,19 @@ fmm_status fmm_build_tree(fmm_ctx* ctx, const void* pos, int64_t n, void* stream
         FMM_TRY(build_tree(ctx, s));
     }
     ctx->tree_built = true;
+    return FMM_OK;
+}
+
+fmm_status fmm_set_root_bounds(fmm_ctx* ctx, const double* bounds) {
+    FMM_TRY(check_ctx(ctx));
+    if (!bounds) {
+        ctx->has_root_bounds = false;
+        return FMM_OK;
+    }
+    for (int d = 0; d < 3; ++d)
+        if (!std::isfinite(bounds[d]) || !std::isfinite(bounds[3 + d]) || bounds[d] > bounds[3 + d]) return FMM_ERR_ARG;
+    for (int d = 0; d < 6; ++d) ctx->root_bounds[d] = bounds[d];
+    ctx->has_root_bounds = true;
     return FMM_OK;
 }
 
@@ -209,9 +225,11 @@ fmm_status fmm_dtt(fmm_ctx* ctx, int remote, void* stream) {
         const uint64_t root_pair = 0;
         return dtt_pass(ctx, &root_pair, 1, false, s);
     }
+    // (local root 0, remote root) of every LET grafted since the last remote traversal
     std::vector<uint64_t> seeds;
-    for (const auto& r : ctx->let_remote)
-        if (r.ncell > 0) seeds.push_back((uint64_t)r.base);   // (local root 0, remote root)
+    for (size_t k = ctx->let_traversed; k < ctx->let_remote.size(); ++k)
+        if (ctx->let_remote[k].ncell > 0) seeds.push_back((uint64_t)ctx->let_remote[k].base);
+    ctx->let_traversed = ctx->let_remote.size();
     if (seeds.empty()) return FMM_OK;
     return dtt_pass(ctx, seeds.data(), (int)seeds.size(), true, s);
 }
@@ -361,13 +379,14 @@ fmm_status fmm_let_graft(fmm_ctx* ctx, int npeers, const void* const* src, const
     return let_graft(ctx, npeers, src, bytes, (cudaStream_t)stream);
 }
 
-fmm_status fmm_let_unpack(fmm_ctx* ctx, int npeers, const void* const* src, const int64_t* bytes, void* stream) {
+fmm_status fmm_let_unpack(fmm_ctx* ctx, int first, int npeers, const void* const* src, const int64_t* bytes,
+                          void* stream) {
     FMM_TRY(check_ctx(ctx));
     ctx->err.clear();
-    if (npeers < 0 || (npeers > 0 && (!src || !bytes))) return FMM_ERR_ARG;
+    if (first < 0 || npeers < 0 || (npeers > 0 && (!src || !bytes))) return FMM_ERR_ARG;
     if (ctx->n == 0) return FMM_OK;
     DeviceGuard g(ctx->device);
-    return let_unpack(ctx, npeers, src, bytes, (cudaStream_t)stream);
+    return let_unpack(ctx, first, npeers, src, bytes, (cudaStream_t)stream);
 }
 
 fmm_status fmm_let_remote(const fmm_ctx* ctx_c, int k, int64_t* base, int64_t* ncell, int64_t* nbody, uint32_t* orig) {

@@ -105,7 +105,9 @@ struct fmm_ctx {
     bool evaluated = false;
 
     // root cube (device): [0..2] lo, [3..5] hi, [6..8] origin, [9] scale, [10] h
-    DevBuf root;
+    DevBuf root, root_given;
+    bool has_root_bounds = false;   // fmm_set_root_bounds: R2 from these bounds, not the particles'
+    double root_bounds[6] = {0, 0, 0, 0, 0, 0};
     // sort buffers
     DevBuf key_a, key_b, idx_a, idx_b, sort_counts, scan_tmp, red_tmp;
     uint64_t* d_keys = nullptr;   // sorted keys (points into key_a or key_b)
@@ -137,6 +139,7 @@ struct fmm_ctx {
     int64_t nrem = 0, nrem_body = 0;
     std::vector<LetPeer> let_peers;
     std::vector<LetRemote> let_remote;
+    size_t let_traversed = 0;   // grafted LETs already seeded into the traversal
     DevBuf let_tmp, let_cov, c_orig, part_tmp, orb_tmp;
     DevBuf h_stage;              // device staging for fmm_solve_host
 };
@@ -208,7 +211,8 @@ fmm_status let_plan(fmm_ctx* ctx, int peer, const double* cover, int ncover, int
                     cudaStream_t s);
 fmm_status let_pack(fmm_ctx* ctx, int peer, int part, void* dst, cudaStream_t s);
 fmm_status let_graft(fmm_ctx* ctx, int npeers, const void* const* src, const int64_t* bytes, cudaStream_t s);
-fmm_status let_unpack(fmm_ctx* ctx, int npeers, const void* const* src, const int64_t* bytes, cudaStream_t s);
+fmm_status let_unpack(fmm_ctx* ctx, int first, int npeers, const void* const* src, const int64_t* bytes,
+                      cudaStream_t s);
 // upward.cu / downward.cu / m2l.cu / p2p.cu
 fmm_status upward_pass(fmm_ctx* ctx, cudaStream_t s);
 fmm_status m2l_pass(fmm_ctx* ctx, cudaStream_t s);

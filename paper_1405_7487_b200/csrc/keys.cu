@@ -45,8 +45,10 @@ __global__ void k_bounds(const Real* __restrict__ pos, int64_t n, double* __rest
     }
 }
 
-// final reduction over blocks (one warp; min/max are exact in any order) + R2 root cube
-__global__ void k_root_cube(const double* __restrict__ blk, int nblk, double* __restrict__ root) {
+// final reduction over blocks (one warp; min/max are exact in any order) + R2 root cube, from
+// the particles' own bounds or from given bounds (which must contain them: *bad |= 2 if not)
+__global__ void k_root_cube(const double* __restrict__ blk, int nblk, double* __restrict__ root,
+                            const double* __restrict__ given, int* __restrict__ bad) {
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int b = threadIdx.x; b < nblk; b += 32)
         for (int d = 0; d < 3; ++d) {
@@ -59,6 +61,14 @@ __global__ void k_root_cube(const double* __restrict__ blk, int nblk, double* __
             hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
         }
     if (threadIdx.x != 0) return;
+    if (given) {
+        for (int d = 0; d < 3; ++d)
+            if (lo[d] < given[d] || hi[d] > given[3 + d]) *bad |= 2;
+        for (int d = 0; d < 3; ++d) {
+            lo[d] = given[d];
+            hi[d] = given[3 + d];
+        }
+    }
     double c0[3], ext = 0.0;
     for (int d = 0; d < 3; ++d) {
         c0[d] = __dmul_rn(__dadd_rn(lo[d], hi[d]), 0.5);
@@ -141,14 +151,25 @@ fmm_status build_keys_t(fmm_ctx* ctx, const Real* pos, int64_t n, cudaStream_t s
         double* d_blk = reinterpret_cast<double*>((char*)ctx->red_tmp.p + 64);
         FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_bad, 0, sizeof(int), s));
         k_bounds<Real><<<nblk, 256, 0, s>>>(pos, n, d_blk, d_bad);
-        k_root_cube<<<1, 32, 0, s>>>(d_blk, nblk, P_<double>(ctx->root));
+        const double* given = nullptr;
+        if (ctx->has_root_bounds) {
+            FMM_TRY(buf_ensure(ctx, ctx->root_given, 6 * sizeof(double)));
+            FMM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->root_given.p, ctx->root_bounds, 6 * sizeof(double),
+                                              cudaMemcpyHostToDevice, s));
+            given = P_<double>(ctx->root_given);
+        }
+        k_root_cube<<<1, 32, 0, s>>>(d_blk, nblk, P_<double>(ctx->root), given, d_bad);
         ctx->launches += 2;
         int bad = 0;
         FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
         FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-        if (bad) {
+        if (bad & 1) {
             ctx->err = "fmm_build: non-finite position";
             return FMM_ERR_NONFINITE;
+        }
+        if (bad & 2) {
+            ctx->err = "fmm_build: a position lies outside the root bounds set by fmm_set_root_bounds";
+            return FMM_ERR_ARG;
         }
     }
     PhaseScope ps(ctx, PH_SORT, s);

@@ -376,7 +376,8 @@ fmm_status let_graft(fmm_ctx* ctx, int npeers, const void* const* src, const int
         add_c += h.ncell;
         add_b += h.nbody;
     }
-    const int64_t ctot = nc + add_c, btot = n + add_b;
+    // grafts append after the LETs already grafted in this build (one fragment at a time)
+    const int64_t ctot = nc + ctx->nrem + add_c, btot = n + ctx->nrem_body + add_b;
     if (ctot >= (int64_t)FMM_LET_ABSENT || btot >= (int64_t)FMM_LET_ABSENT) {
         ctx->err = "fmm_let_graft: more than 2^32-1 cells or bodies";
         return FMM_ERR_ARG;
@@ -390,8 +391,7 @@ fmm_status let_graft(fmm_ctx* ctx, int npeers, const void* const* src, const int
     FMM_TRY(buf_ensure(ctx, ctx->c_cr, (size_t)ctot * 32, true, s));
     FMM_TRY(buf_ensure(ctx, ctx->c_orig, (size_t)std::max<int64_t>(ctot, 1) * 4, true, s));
     FMM_TRY(buf_ensure(ctx, ctx->body, (size_t)btot * bs, true, s));
-    ctx->let_remote.clear();
-    int64_t cbase = nc, bbase = n;
+    int64_t cbase = nc + ctx->nrem, bbase = n + ctx->nrem_body;
     for (int k = 0; k < npeers; ++k) {
         const LetHeader& h = hs[k];
         const char* p = (const char*)src[k] + sizeof(LetHeader);
@@ -417,21 +417,22 @@ fmm_status let_graft(fmm_ctx* ctx, int npeers, const void* const* src, const int
         cbase += h.ncell;
         bbase += h.nbody;
     }
-    ctx->nrem = add_c;
-    ctx->nrem_body = add_b;
+    ctx->nrem += add_c;
+    ctx->nrem_body += add_b;
     FMM_CUDA_TRY(ctx, cudaGetLastError());
     return FMM_OK;
 }
 
-fmm_status let_unpack(fmm_ctx* ctx, int npeers, const void* const* src, const int64_t* bytes, cudaStream_t s) {
-    if (npeers != (int)ctx->let_remote.size()) {
-        ctx->err = "fmm_let_unpack: peer count differs from fmm_let_graft";
+fmm_status let_unpack(fmm_ctx* ctx, int first, int npeers, const void* const* src, const int64_t* bytes,
+                      cudaStream_t s) {
+    if (first < 0 || first + npeers > (int)ctx->let_remote.size()) {
+        ctx->err = "fmm_let_unpack: more data messages than grafted LETs";
         return FMM_ERR_STATE;
     }
     const int64_t ctot = ctx->ncell + ctx->nrem;
     FMM_TRY(buf_ensure(ctx, ctx->M, (size_t)ctot * ctx->ncoef * 8, true, s));
     for (int k = 0; k < npeers; ++k) {
-        const LetRemote& r = ctx->let_remote[k];
+        const LetRemote& r = ctx->let_remote[first + k];
         const size_t need = sizeof(LetHeader) + let_round16((size_t)r.ncell * ctx->ncoef * 8) +
                             (size_t)r.nbody * (ctx->prec == FMM_F32 ? 4 : 8);
         if (!src[k] || bytes[k] < (int64_t)need) {

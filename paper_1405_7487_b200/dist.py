@@ -19,9 +19,10 @@ The step (§II-B/C):
   3. particles exchanged to their ranks (fmm_part_pack + all-to-all);
   4. local tree from the LOCAL bounds; covers all-gathered; each rank packs
      for every peer the part of its tree that peer can need (fmm_let_plan/pack_struct);
-  5. structure all-to-all in flight WHILE the local dual tree traversal runs
-     (communication overlapped with local work); graft, remote traversal
-     from (local root, remote root), canonical lists;
+  5. LET structure sent in K-1 ring rounds of grouped send/recv: the local dual tree traversal
+     overlaps round 1 and every received fragment is grafted and traversed from (local root,
+     remote root) while the next round is in flight; then the
+     canonical lists;
   6. upward pass, multipole/charge all-to-all, unpack, M2L + P2P + downward;
   7. results returned to the particles' owners in their original order.
 """
@@ -52,6 +53,11 @@ class Comm:
         recv[i][j] from global rank j (or a handle whose wait() returns it)."""
         raise NotImplementedError
 
+    def sendrecv(self, sends, dst, src, recv_sizes, async_op=False):
+        """Point-to-point round: local rank i sends sends[i] to global rank dst[i] and receives
+        recv_sizes[i] elements from global rank src[i] (grouped send/recv, deadlock-free)."""
+        raise NotImplementedError
+
     def barrier(self):
         pass
 
@@ -80,6 +86,22 @@ class LoopbackComm(Comm):
     def alltoallv(self, sends, async_op=False):
         recv = [[sends[j][i] for j in range(self.world)] for i in range(self.world)]
         return _Done(recv) if async_op else recv
+
+    def sendrecv(self, sends, dst, src, recv_sizes, async_op=False):
+        by_dst = {dst[j]: j for j in range(self.world)}
+        recv = [sends[by_dst[i]] for i in range(self.world)]
+        assert all(src[i] == by_dst[i] and recv[i].numel() == recv_sizes[i] for i in range(self.world))
+        return _Done(recv) if async_op else recv
+
+
+class _P2PWork:
+    def __init__(self, works, out):
+        self.works, self.out = works, out
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+        return [self.out]
 
 
 class _A2AWork:
@@ -124,6 +146,19 @@ class TorchComm(Comm):
         work = self.dist.all_to_all_single(out, inp, output_split_sizes=sizes, input_split_sizes=in_sizes,
                                            group=self.group, async_op=async_op)
         h = _A2AWork(work if async_op else None, out, sizes)
+        return h if async_op else h.wait()
+
+    def sendrecv(self, sends, dst, src, recv_sizes, async_op=False):
+        d = self.dist
+        t = sends[0]
+        out = torch.empty(int(recv_sizes[0]), dtype=t.dtype, device=t.device)
+        ops = []
+        if t.numel():
+            ops.append(d.P2POp(d.isend, t, dst[0], group=self.group))
+        if out.numel():
+            ops.append(d.P2POp(d.irecv, out, src[0], group=self.group))
+        works = d.batch_isend_irecv(ops) if ops else []
+        h = _P2PWork(works, out)
         return h if async_op else h.wait()
 
     def barrier(self):
@@ -270,6 +305,7 @@ class DistFMM:
         lo = cm.allreduce([x[:3].clone() for x in b], "min")
         hi = cm.allreduce([x[3:].clone() for x in b], "max")
         gb = [torch.cat([lo[i], hi[i]]).cpu().numpy() for i in range(nl)]
+        self.global_bounds = gb[0]
         keys = [F[i].part_keys(pos[i], gb[i]) for i in range(nl)]
 
         def hist_fn(prefixes, pbits, bits):
@@ -314,6 +350,10 @@ class DistFMM:
         nl = len(F)
         dev = lpos[0].device
         for f, p in zip(F, lpos):
+            # Morton ranges are pieces of the global curve: build each local tree on the global
+            # root cube so it is a subtree of the global octree (no slivers at the range ends);
+            # ORB boxes are compact: local bounding box
+            f.set_root_bounds(self.global_bounds if self.partitioner == "morton" else None)
             f.build_tree(p)
         cov = []
         for f in F:
@@ -342,17 +382,36 @@ class DistFMM:
                 db.append(d)
             sends.append(row)
             self._dbytes.append(db)
-        h = cm.alltoallv(sends, async_op=True)
-        for f in F:                       # local traversal overlaps the LET structure exchange
+        # sizes first (one small all-to-all), then K-1 ring rounds: in round s every rank sends
+        # its LET to rank me+s and receives rank me-s's.  Round s+1 is in flight while round
+        # s's fragment is grafted and traversed (each message processed as it
+        # lands); the local traversal overlaps round 1.
+        szs = cm.alltoallv([[torch.tensor([t.numel()], dtype=torch.int64, device=dev) for t in row]
+                            for row in sends])
+        rsz = [[int(x) for x in torch.cat(szs[i]).tolist()] for i in range(nl)]
+        me = cm.ranks
+
+        def start(sr):
+            dst = [(me[i] + sr) % K for i in range(nl)]
+            src = [(me[i] - sr) % K for i in range(nl)]
+            return cm.sendrecv([sends[i][dst[i]] for i in range(nl)], dst, src,
+                               [rsz[i][src[i]] for i in range(nl)], async_op=True), src
+
+        self._peers = [[] for _ in range(nl)]
+        h = start(1) if K > 1 else None
+        for f in F:                       # local traversal overlaps the first LET round
             f.dtt(remote=False)
-        recv = h.wait()
-        self._peers = []
-        for i, f in enumerate(F):
-            me = cm.ranks[i]
-            peers = [j for j in range(K) if j != me and recv[i][j].numel() > 0]
-            self._peers.append(peers)
-            f.let_graft([recv[i][j] for j in peers])
-            f.dtt(remote=True)
+        for sr in range(1, K):
+            hh, src = h
+            recv = hh.wait()
+            if sr + 1 < K:
+                h = start(sr + 1)
+            for i, f in enumerate(F):
+                if recv[i].numel() > 0:
+                    f.let_graft([recv[i]])
+                    f.dtt(remote=True)    # traverses only the fragment just grafted
+                    self._peers[i].append(src[i])
+        for f in F:
             f.make_lists()
         self.stats["let_struct_bytes"] = sum(int(t.numel()) for row in sends for t in row)
 
@@ -375,7 +434,7 @@ class DistFMM:
         recv = cm.alltoallv(sends)
         out = []
         for i, f in enumerate(F):
-            f.let_unpack([recv[i][j] for j in self._peers[i]])
+            f.let_unpack([recv[i][j] for j in self._peers[i]])    # graft (ring) order
             n = lpos[i].shape[0]
             phi = torch.empty(n, dtype=f.dtype, device=dev)
             grad = torch.empty((n, 3), dtype=f.dtype, device=dev)

@@ -40,6 +40,7 @@ SYMBOLS = {
     "fmm_phase_name": (C.c_char_p, [_i]),
     "fmm_launch_count": (_i64, [_p, _i]),
     "fmm_build_tree": (_i, [_p, _p, _i64, _p]),
+    "fmm_set_root_bounds": (_i, [_p, _p]),
     "fmm_dtt": (_i, [_p, _i, _p]),
     "fmm_lists": (_i, [_p, _p]),
     "fmm_upward": (_i, [_p, _p, _p, _p]),
@@ -53,7 +54,7 @@ SYMBOLS = {
     "fmm_let_pack_struct": (_i, [_p, _i, _p, _p]),
     "fmm_let_pack_data": (_i, [_p, _i, _p, _p]),
     "fmm_let_graft": (_i, [_p, _i, _p, _p, _p]),
-    "fmm_let_unpack": (_i, [_p, _i, _p, _p, _p]),
+    "fmm_let_unpack": (_i, [_p, _i, _i, _p, _p, _p]),
     "fmm_let_remote": (_i, [_p, _i, _p, _p, _p, _p]),
     "fmm_work": (_i, [_p, _d, C.c_float, _p, _p, _p]),
     "fmm_orb_histogram": (_i, [_p, _p, _p, _p, _i64, _i, _p, _p, _i, _i, _p, _p]),
@@ -194,6 +195,11 @@ class FMM:
         self.n = n
         return self
 
+    def set_root_bounds(self, bounds=None):
+        """R2 root cube of later builds from these bounds (lo xyz, hi xyz); None: own bounds."""
+        self._root_bounds = None if bounds is None else np.ascontiguousarray(bounds, dtype=np.float64).reshape(6)
+        self._check(lib().fmm_set_root_bounds(self._h, _np_ptr(self._root_bounds)), "fmm_set_root_bounds")
+
     def dtt(self, remote: bool = False, stream=None):
         self._check(lib().fmm_dtt(self._h, int(remote), C.c_void_p(self._stream(stream))), "fmm_dtt")
 
@@ -327,10 +333,10 @@ class FMM:
         self._check(lib().fmm_let_graft(self._h, len(bufs), ptrs, sizes, C.c_void_p(self._stream(stream))),
                     "fmm_let_graft")
 
-    def let_unpack(self, bufs, stream=None):
+    def let_unpack(self, bufs, first: int = 0, stream=None):
         ptrs, sizes = self._buf_arrays(bufs)
-        self._check(lib().fmm_let_unpack(self._h, len(bufs), ptrs, sizes, C.c_void_p(self._stream(stream))),
-                    "fmm_let_unpack")
+        self._check(lib().fmm_let_unpack(self._h, int(first), len(bufs), ptrs, sizes,
+                                         C.c_void_p(self._stream(stream))), "fmm_let_unpack")
 
     def let_remote(self, k: int, with_orig: bool = True):
         base, nc, nb = C.c_int64(), C.c_int64(), C.c_int64()

@@ -94,7 +94,11 @@ def _worker(rank, world, port, q):
         recv = [t.tolist() for t in cm.alltoallv([sends])[0]]
         h = cm.alltoallv([sends], async_op=True)
         recv2 = [t.tolist() for t in h.wait()[0]]
-        q.put((rank, s, mn, mx, g, recv, recv2))
+        # ring round 1: send to rank+1, receive from rank-1 (sizes known in advance)
+        dst, src = (rank + 1) % world, (rank - 1) % world
+        msg = torch.full((3 + rank,), 7 * rank + 1, dtype=torch.uint8)
+        ring = cm.sendrecv([msg], [dst], [src], [3 + src], async_op=True).wait()[0].tolist()
+        q.put((rank, s, mn, mx, g, recv, recv2, ring))
     finally:
         dist.destroy_process_group()
 
@@ -121,8 +125,12 @@ def test_torchcomm_gloo_matches_loopback():
     ls = lb.allreduce(xs, "sum"); lmn = lb.allreduce(xs, "min"); lmx = lb.allreduce(xs, "max")
     lg = lb.allgather([torch.arange(3, dtype=torch.float64) + 10 * r for r in range(world)])
     lr = lb.alltoallv(sends)
+    lring = lb.sendrecv([torch.full((3 + r,), 7 * r + 1, dtype=torch.uint8) for r in range(world)],
+                        [(r + 1) % world for r in range(world)], [(r - 1) % world for r in range(world)],
+                        [3 + (r - 1) % world for r in range(world)])
     for r in range(world):
-        _, s, mn, mx, g, recv, recv2 = res[r]
+        _, s, mn, mx, g, recv, recv2, ring = res[r]
+        assert ring == lring[r].tolist() == [7 * ((r - 1) % world) + 1] * (3 + (r - 1) % world)
         assert s == ls[r].tolist() and mn == lmn[r].tolist() and mx == lmx[r].tolist()
         assert g == [t.tolist() for t in lg[r]]
         assert recv == [t.tolist() for t in lr[r]] == recv2

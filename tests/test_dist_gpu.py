@@ -80,7 +80,8 @@ def test_dist_lists_and_fields(torch_cuda, kind, n, K, P, theta, ncrit, prec, pa
                     c |= (((kk >> np.uint64(3 * l + a)) & np.uint64(1)).astype(np.int64)) << l
                 assert np.all((c >= g["lo"][a]) & (c < g["hi"][a]))
     # oracle trees of every rank, built from the rank's particles in the order the rank holds them
-    O = [oracle.FMM(pos[g].astype(np.float64), q[g].astype(np.float64), P, theta, ncrit) for g in gids]
+    rb = D.global_bounds if part == "morton" else None   # the root cube the ranks built on
+    O = [oracle.FMM(pos[g].astype(np.float64), q[g].astype(np.float64), P, theta, ncrit, bounds=rb) for g in gids]
     for i in range(K):
         f = D.fmm[i]
         m2l, p2p = f.lists()

@@ -195,3 +195,27 @@ def test_c2_full_size(torch_cuda):
     print(f"c2: vs oracle phi {e_phi:.2e} grad {e_grad:.2e}; vs direct phi {oracle.rel_l2(phi[t], dphi):.2e} "
           f"grad {oracle.rel_l2(grad[t], dgrad):.2e}")
     assert e_phi <= 1e-5 and e_grad <= 1e-5
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_root_bounds_matches_oracle(torch_cuda, prec):
+    """fmm_set_root_bounds (global root cube of a Morton-range part) against the oracle built on
+    the same bounds: structure bit-exact, fields at tolerance; outside bounds rejected."""
+    from paper_1405_7487_b200 import FMM, FMMError
+    dt = np.float32 if prec == "f32" else np.float64
+    pos, q = synth.generate("plummer", 6000, 61, dt)
+    b = np.array([-30.0, -20.0, -25.0, 40.0, 35.0, 30.0])
+    sel = np.all((pos >= b[:3]) & (pos <= b[3:]), axis=1)
+    pos, q = np.ascontiguousarray(pos[sel]), np.ascontiguousarray(q[sel])
+    f = FMM(len(pos), 6, 0.5, 16, prec)
+    f.set_root_bounds(b)
+    tp = torch_cuda.from_numpy(pos).cuda()
+    phi, grad = f.solve(tp, torch_cuda.from_numpy(q).cuda())
+    o = oracle.FMM(pos.astype(np.float64), q.astype(np.float64), 6, 0.5, 16, bounds=b).traverse()
+    check_structure(f, o)
+    ophi, ograd = o.evaluate()
+    assert oracle.rel_l2(phi.cpu().numpy().astype(np.float64), ophi) <= TOL[prec]
+    assert oracle.rel_l2(grad.cpu().numpy().astype(np.float64), ograd) <= TOL[prec]
+    f.set_root_bounds(np.array([0.0, 0.0, 0.0, 1.0, 1.0, 1.0]))
+    with pytest.raises(FMMError):
+        f.build(tp)

@@ -526,23 +526,31 @@ def _partitions(pos, k):
     return np.array_split(np.argsort(pos[:, 0], kind="stable"), k)
 
 
-def test_partition_tiny_theta_equals_direct():
+def _global_bounds(pos):
+    return np.concatenate([pos.min(0), pos.max(0)])
+
+
+@pytest.mark.parametrize("glob", [False, True])
+def test_partition_tiny_theta_equals_direct(glob):
     # theta -> 0: every cross-partition pair is P2P, so the multi-tree sum is the direct sum
     pos, q = synth.generate("plummer", 900, 31)
     parts = _partitions(pos, 3)
-    trees = [oracle.FMM(pos[p], q[p], 3, 1e-3, 8) for p in parts]
+    b = _global_bounds(pos) if glob else None
+    trees = [oracle.FMM(pos[p], q[p], 3, 1e-3, 8, bounds=b) for p in parts]
     dp, dg = oracle.direct(pos, q)
     for k, p in enumerate(parts):
         phi, g = oracle.evaluate_multi(trees[k], [t for j, t in enumerate(trees) if j != k])
         assert oracle.rel_l2(phi, dp[p]) <= 1e-13 and oracle.rel_l2(g, dg[p]) <= 1e-13
 
 
-def test_partition_exactly_once_coverage():
+@pytest.mark.parametrize("glob", [False, True])
+def test_partition_exactly_once_coverage(glob):
     # local lists of tree k plus its remote lists against every other tree cover each
     # (target body, source body) pair of the whole system exactly once
     pos, q = synth.generate("cube", 600, 32)
     parts = _partitions(pos, 3)
-    trees = [oracle.FMM(pos[p], q[p], 3, 0.5, 8).traverse() for p in parts]
+    b = _global_bounds(pos) if glob else None
+    trees = [oracle.FMM(pos[p], q[p], 3, 0.5, 8, bounds=b).traverse() for p in parts]
     for k in range(3):
         T = trees[k]
         cT = T.cells()
@@ -572,3 +580,38 @@ def test_partition_single_tree_equals_evaluate():
     phi2, g2 = oracle.evaluate_multi(b, [])
     np.testing.assert_array_equal(phi1, phi2)
     np.testing.assert_array_equal(g1, g2)
+
+
+def test_root_bounds_own_box_is_default():
+    pos, q = synth.generate("plummer", 700, 34)
+    a = oracle.FMM(pos, q, 4, 0.5, 16)
+    b = oracle.FMM(pos, q, 4, 0.5, 16, bounds=_global_bounds(pos))
+    for x, y in zip(a.sorted(), b.sorted()):
+        np.testing.assert_array_equal(x, y)
+    for k, v in a.cells().items():
+        np.testing.assert_array_equal(v, b.cells()[k])
+    np.testing.assert_array_equal(a.evaluate()[0], b.evaluate()[0])
+
+
+def test_root_bounds_global_keys_are_subtree_keys():
+    # HOT reading (DESIGN.md §2 reading 9): a Morton-range part built on the global root cube
+    # has exactly the global keys, and every one of its cells is a cell of the global octree
+    pos, q = synth.generate("cube", 3000, 35)
+    gk = oracle.keys(pos)
+    b = _global_bounds(pos)
+    order = np.argsort(gk, kind="stable")
+    part = np.sort(order[1000:2000])              # one Morton range of the global curve
+    t = oracle.FMM(pos[part], q[part], 4, 0.5, 16, bounds=b)
+    k, perm = t.sorted()
+    np.testing.assert_array_equal(k, gk[part][perm])
+    c = t.cells()
+    lo = c["body_begin"]; lv = c["level"]
+    for i in range(len(lv)):                     # cell key = common level-l prefix of its bodies
+        pre = k[lo[i]] >> np.uint64(3 * (21 - lv[i]))
+        assert c["key"][i] == pre
+
+
+def test_root_bounds_reject_outside():
+    pos, q = synth.generate("cube", 10, 36)
+    with pytest.raises(ValueError):
+        oracle.FMM(pos, q, 3, 0.5, 4, bounds=np.array([0.1, 0.1, 0.1, 0.9, 0.9, 0.9]))
