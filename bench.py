@@ -155,7 +155,8 @@ def workload_config(cfg, args, world=1):
     if world > 1:
         part = "ORB multisection" if getattr(args, "partitioner", "morton") == "orb" else "Morton-range"
         d["parallelism"] = (f"{world} GPUs, one FMM: {part} partition with Eq. (1) weights + LET exchange over "
-                            f"NCCL (weak scaling, {cfg['n']} particles per GPU)")
+                            f"NCCL (weak scaling at constant density, {cfg['n']} particles per GPU, rank r's "
+                            f"slice in unit cube r of a 2x2x2 Morton block pattern)")
         d["workload"] = ("BASELINE.json configs[3] (weak scaling, per-GPU size of " + CONFIG_NAMES[args.config] +
                          f"): 3D Laplace FMM, N={n} {cfg['kind']}, {cfg['prec']}, P={cfg['P']}, theta={cfg['theta']}, "
                          f"ncrit={cfg['ncrit']}")
@@ -197,6 +198,16 @@ def roofline_block(args, cfg, counts, ph):
             "traffic_note": "dram read+write bytes per launch from one ncu --set full capture (profiles/traffic.json)"}
 
 
+def weak_offset(r: int) -> np.ndarray:
+    """Weak scaling at constant density: rank r's 2^20 particles fill unit cube r of a block
+    pattern in Morton order (r bits -> x, y, z, x, ...; 2 GPUs: 2x1x1, 4: 2x2x1, 8: 2x2x2), so
+    every GPU's particles have the same spacing and its tree the same leaf occupancy as c2."""
+    o = np.zeros(3)
+    for b in range(max(r.bit_length(), 1)):
+        o[b % 3] += ((r >> b) & 1) << (b // 3)
+    return o
+
+
 def run_dist(args, cfg, rank, world, local):
     """--gpus N > 1 under torchrun: the distributed FMM (dist.py) over NCCL."""
     import torch
@@ -207,6 +218,7 @@ def run_dist(args, cfg, rank, world, local):
     n = cfg["n"]
     N = n * world
     pos, q = synth.generate(cfg["kind"], n, cfg["seed"], dt_np, start=rank * n, n_total=N)
+    pos = (pos + weak_offset(rank)).astype(dt_np)      # constant density: rank r's unit cube
     dpos = torch.from_numpy(pos).cuda()
     dq = torch.from_numpy(q).cuda()
     D = DistFMM(TorchComm(), N, cfg["P"], cfg["theta"], cfg["ncrit"], cfg["prec"], local,

@@ -7,7 +7,11 @@ from paper_1405_7487_b200.dist import DistFMM, LoopbackComm
 
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 n = 1 << 20
+from bench import weak_offset
 pos, q = synth.generate("cube", n * K, 2, np.float32)
+if len(sys.argv) > 2 and sys.argv[2] == "weak":
+    for r in range(K):
+        pos[r * n:(r + 1) * n] += weak_offset(r).astype(np.float32)
 P_in = [torch.from_numpy(pos[r * n:(r + 1) * n]).cuda() for r in range(K)]
 Q_in = [torch.from_numpy(q[r * n:(r + 1) * n]).cuda() for r in range(K)]
 D = DistFMM(LoopbackComm(K), n * K, 10, 0.4, 64, "f32")
