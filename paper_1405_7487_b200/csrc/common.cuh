@@ -130,7 +130,9 @@ struct fmm_ctx {
     DevBuf runs, run_off, run_tmp, run_pre, run_len64, dcount2, tcnt, cnt64, big_off, seg_lists;
 
     // expansions
-    DevBuf M, L, Mr, Lr;   // fp64 [ncell][ncoef]; Mr: packed reduced multipoles for the M2L kernel; Lr: reduced L
+    DevBuf M, L, Mr, Lr, fold_tab;
+    int fold_P = -1;              // P of the fold table in fold_tab (m2l_fast.cu)
+    int64_t fold_nt = 0;   // fp64 [ncell][ncoef]; Mr: packed reduced multipoles for the M2L kernel; Lr: reduced L
     DevBuf near_phi, near_grad;  // P2P partials in sorted order (prec type)
     bool upward_done = false;
 

@@ -238,73 +238,100 @@ __global__ void __launch_bounds__(128, 2)
     }
 }
 
-// harmonic fold in closed form: repeatedly moving S_beta (beta_x >= 2) onto
-// beta - 2e_x + 2e_y and beta - 2e_x + 2e_z with weight -1 gives
-//   S~(b,y,z) = sum_k (-1)^k sum_{j<=k} C(k,j) S(b+2k, y-2j, z-2(k-j))
-__device__ __forceinline__ double fold_pull(const double* S, int b, int y, int z) {
-    double acc = 0.0;
+// Harmonic fold in closed form (operand preparation, per source cell): repeatedly moving
+// S_beta (beta_x >= 2) onto beta - 2e_x + 2e_y and beta - 2e_x + 2e_z with weight -1 gives
+//   S~(b,y,z) = sum_k (-1)^k sum_{j<=k} C(k,j) S(b+2k, y-2j, z-2(k-j)),  S = (-1)^|beta| M;
+// the streamed operand is S0 = S~(0,.,.) | S1 = S~(1,.,.) | N[q] = -S1[q-2e_y] - S1[q-2e_z]
+// (|q| >= 2), each scaled by rho^-|beta| (exact powers of two) and rounded to R.
+// The preparation is a sparse linear map built once per P from the rules above: output
+// element i = sum over table entries (k, w) of w * M[k] (the sign (-1)^|beta| and the fold's
+// binomial weights in w), then scaled by rho^(-e dg_i).  The kernel is a warp per cell with M
+// staged in shared memory and lanes over outputs (the per-element decode-and-recurse version
+// took 0.26 ms at c2 and 4.1 ms at c3; profiles/r01_c3 launch list).
+struct FoldTable {
+    std::vector<int> off;      // [NSP + 1]
+    std::vector<int> k;        // coefficient index (R11 order)
+    std::vector<double> w;     // weight
+    std::vector<int> dg;       // [NSP] degree |beta| for the rho scaling, -1 for padding
+};
+
+void fold_terms_host(int b, int y, int z, double sgn, std::vector<std::pair<int, double>>& out) {
+    // S~(b,y,z) = sum_k (-1)^k sum_{j<=k} C(k,j) S(b+2k, y-2j, z-2(k-j)), S = (-1)^|beta| M
     for (int k = 0; 2 * k <= y + z; ++k) {
-        double binom = 1.0, part = 0.0;
+        double binom = 1.0;
         for (int j = 0; j <= k; ++j) {
             if (j > 0) binom = binom * (double)(k - j + 1) / (double)j;
             const int yy = y - 2 * j, zz = z - 2 * (k - j);
-            if (yy >= 0 && zz >= 0) part += binom * S[cidx(b + 2 * k, yy, zz)];
+            if (yy >= 0 && zz >= 0) {
+                const int a = b + 2 * k;
+                const double sM = ((a + yy + zz) & 1) ? -1.0 : 1.0;
+                out.push_back({cidx(a, yy, zz), sgn * ((k & 1) ? -binom : binom) * sM});
+            }
         }
-        acc += (k & 1) ? -part : part;
     }
-    return acc;
 }
 
-// per source cell: signed M -> harmonic fold onto beta_x in {0,1} -> S0 | S1 | N, scaled by
-// rho^-|beta| and rounded to R.  Also records the cell's scale exponent.
+FoldTable build_fold_table(int P, int NS, int NSP) {
+    FoldTable t;
+    const int N0 = P * (P + 1) / 2, N1 = (P - 1) * P / 2;
+    t.off.assign(NSP + 1, 0);
+    t.dg.assign(NSP, -1);
+    auto decode = [](int ii, int& m, int& y, int& z) {
+        m = 0;
+        while ((m + 1) * (m + 2) / 2 <= ii) ++m;
+        z = ii - m * (m + 1) / 2;
+        y = m - z;
+    };
+    for (int i = 0; i < NSP; ++i) {
+        std::vector<std::pair<int, double>> e;
+        int m, y, z;
+        if (i < N0) {            // S0: S~(0, q)
+            decode(i, m, y, z);
+            fold_terms_host(0, y, z, 1.0, e);
+            t.dg[i] = m;
+        } else if (i < N0 + N1) {   // S1: S~(1, q)
+            decode(i - N0, m, y, z);
+            fold_terms_host(1, y, z, 1.0, e);
+            t.dg[i] = m + 1;
+        } else if (i < NS) {        // N[q] = -S1[q - 2e_y] - S1[q - 2e_z]
+            decode(i - N0 - N1, m, y, z);
+            if (m >= 2) {
+                if (y >= 2) fold_terms_host(1, y - 2, z, -1.0, e);
+                if (z >= 2) fold_terms_host(1, y, z - 2, -1.0, e);
+            }
+            t.dg[i] = m - 1;
+        }
+        for (auto& x : e) {
+            t.k.push_back(x.first);
+            t.w.push_back(x.second);
+        }
+        t.off[i + 1] = (int)t.k.size();
+    }
+    return t;
+}
+
 template <typename R>
-__global__ void k_m2l_prep(int64_t ncell, int P, int ncoef, int NS, int NSP, const double* __restrict__ M,
-                           const int32_t* __restrict__ level, const double* __restrict__ root,
-                           int* __restrict__ sexp, R* __restrict__ Sv) {
-    extern __shared__ double s_S[];
+__global__ void k_m2l_prep_table(int64_t ncell, int ncoef, int NSP, const int* __restrict__ toff,
+                                 const int* __restrict__ tk, const double* __restrict__ tw,
+                                 const int* __restrict__ tdg, const double* __restrict__ M,
+                                 const int32_t* __restrict__ level, const double* __restrict__ root,
+                                 int* __restrict__ sexp, R* __restrict__ Sv) {
+    extern __shared__ double s_M[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    double* S = s_S + (size_t)w * ncoef;
-    // E: 2^E >= root cube width 2h (exact power of two)
+    double* Mw = s_M + (size_t)w * ncoef;
     int E;
     frexp(2.0 * root[10], &E);
-    const int N0 = P * (P + 1) / 2, N1 = (P - 1) * P / 2;
     for (int64_t c = (int64_t)blockIdx.x * nw + w; c < ncell; c += (int64_t)gridDim.x * nw) {
         const int e = E - level[c];
-        for (int k = lane; k < ncoef; k += 32) {
-            int a, b, cc;
-            decode_cidx(k, a, b, cc);
-            double m = M[(size_t)c * ncoef + k];
-            S[k] = ((a + b + cc) & 1) ? -m : m;
-        }
+        for (int k = lane; k < ncoef; k += 32) Mw[k] = M[(size_t)c * ncoef + k];
         if (lane == 0) sexp[c] = e;
         __syncwarp();
         R* out = Sv + (size_t)c * NSP;
         for (int i = lane; i < NSP; i += 32) {
             double v = 0.0;
-            int dg = 0;
-            if (i < N0) {
-                int m = 0;
-                while ((m + 1) * (m + 2) / 2 <= i) ++m;
-                int z = i - m * (m + 1) / 2, y = m - z;
-                v = fold_pull(S, 0, y, z);
-                dg = m;
-            } else if (i < N0 + N1) {
-                int ii = i - N0, m = 0;
-                while ((m + 1) * (m + 2) / 2 <= ii) ++m;
-                int z = ii - m * (m + 1) / 2, y = m - z;
-                v = fold_pull(S, 1, y, z);
-                dg = m + 1;
-            } else if (i < NS) {
-                int ii = i - N0 - N1, m = 0;
-                while ((m + 1) * (m + 2) / 2 <= ii) ++m;
-                int z = ii - m * (m + 1) / 2, y = m - z;
-                if (m >= 2) {
-                    if (y >= 2) v -= fold_pull(S, 1, y - 2, z);
-                    if (z >= 2) v -= fold_pull(S, 1, y, z - 2);
-                }
-                dg = m - 1;
-            }
-            out[i] = (R)ldexp(v, -e * dg);
+            for (int t = toff[i]; t < toff[i + 1]; ++t) v += tw[t] * Mw[tk[t]];
+            const int dg = tdg[i];
+            out[i] = dg < 0 ? R(0) : (R)ldexp(v, -e * dg);
         }
         __syncwarp();
     }
@@ -359,9 +386,27 @@ fmm_status m2l_fast_t(fmm_ctx* ctx, cudaStream_t s) {
     const int nw = 4;
     int g = (int)std::min<int64_t>((nc + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
     const int gp = (int)std::min<int64_t>((nct + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
-    k_m2l_prep<R><<<std::max(gp, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
-        nct, P, ctx->ncoef, RF<P>::NS, NSP, P_<double>(ctx->M), P_<int32_t>(ctx->c_level), P_<double>(ctx->root), sexp,
-        Sv);
+    if (ctx->fold_P != P) {
+        const FoldTable t = build_fold_table(P, RF<P>::NS, NSP);
+        const size_t nt = t.k.size();
+        FMM_TRY(buf_ensure(ctx, ctx->fold_tab, (NSP + 1) * 4 + NSP * 4 + nt * 4 + nt * 8 + 64));
+        char* b = (char*)ctx->fold_tab.p;
+        FMM_CUDA_TRY(ctx, cudaMemcpy(b, t.w.data(), nt * 8, cudaMemcpyHostToDevice));
+        FMM_CUDA_TRY(ctx, cudaMemcpy(b + nt * 8, t.off.data(), (NSP + 1) * 4, cudaMemcpyHostToDevice));
+        FMM_CUDA_TRY(ctx, cudaMemcpy(b + nt * 8 + (NSP + 1) * 4, t.dg.data(), NSP * 4, cudaMemcpyHostToDevice));
+        FMM_CUDA_TRY(ctx, cudaMemcpy(b + nt * 8 + (2 * NSP + 1) * 4, t.k.data(), nt * 4, cudaMemcpyHostToDevice));
+        ctx->fold_P = P;
+        ctx->fold_nt = (int64_t)nt;
+    }
+    {
+        char* b = (char*)ctx->fold_tab.p;
+        const size_t nt = (size_t)ctx->fold_nt;
+        k_m2l_prep_table<R><<<std::max(gp, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
+            nct, ctx->ncoef, NSP, reinterpret_cast<const int*>(b + nt * 8),
+            reinterpret_cast<const int*>(b + nt * 8 + (2 * NSP + 1) * 4), reinterpret_cast<const double*>(b),
+            reinterpret_cast<const int*>(b + nt * 8 + (NSP + 1) * 4), P_<double>(ctx->M), P_<int32_t>(ctx->c_level),
+            P_<double>(ctx->root), sexp, Sv);
+    }
     FMM_LAUNCH(ctx);
     unsigned long long* counter = P_<unsigned long long>(ctx->cnt_tmp);
     FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 8, s));
