@@ -521,7 +521,7 @@ __global__ void k_work_leaves(int64_t nc, const uint32_t* __restrict__ leaf_ids,
 }  // namespace
 
 extern "C" fmm_status fmm_work(fmm_ctx* ctx, double c_m2l, float alpha, float* w, double* lr_sums, void* stream) {
-    if (!ctx || !w || c_m2l < 0) return FMM_ERR_ARG;
+    if (!ctx || c_m2l < 0 || (ctx->n > 0 && !w)) return FMM_ERR_ARG;
     if (!ctx->built) {
         ctx->err = "fmm_work: needs the lists of a build";
         return FMM_ERR_STATE;

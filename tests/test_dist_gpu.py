@@ -226,3 +226,26 @@ def test_weighted_partition_balances_work(torch_cuda):
     share2 = np.array([w1[g].sum() for g in g2]) / w1.sum()
     assert np.abs(share2 - 1.0 / K).max() < 0.01, share2
     assert np.abs(share1 - 1.0 / K).max() > np.abs(share2 - 1.0 / K).max(), (share1, share2)
+
+
+@pytest.mark.parametrize("part", ["morton", "orb"])
+def test_dist_degenerate(torch_cuda, part):
+    """Ranks left empty by the partition (3 particles on 4 ranks; all particles coincident):
+    the distributed path still returns the direct sum."""
+    import torch
+    from paper_1405_7487_b200.dist import DistFMM, LoopbackComm
+    for pos in (np.array([[0.1, 0.2, 0.3], [0.9, 0.8, 0.7], [0.5, 0.5, 0.1]]),
+                np.tile(np.array([[0.25, 0.5, 0.75]]), (40, 1))):
+        n, K = len(pos), 4
+        q = np.linspace(-1.0, 1.0, n)
+        cuts = np.linspace(0, n, K + 1).astype(int)
+        P_in = [torch.from_numpy(np.ascontiguousarray(pos[cuts[r]:cuts[r + 1]])).cuda() for r in range(K)]
+        Q_in = [torch.from_numpy(np.ascontiguousarray(q[cuts[r]:cuts[r + 1]])).cuda() for r in range(K)]
+        D = DistFMM(LoopbackComm(K), n, 4, 0.5, 2, "f64", partitioner=part)
+        out = D.solve(P_in, Q_in, [int(c) for c in cuts[:-1]])
+        phi = np.concatenate([o[0].cpu().numpy() for o in out])
+        grad = np.concatenate([o[1].cpu().numpy() for o in out])
+        dp, dg = oracle.direct(pos, q)
+        np.testing.assert_allclose(phi, dp, rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(grad, dg, rtol=1e-12, atol=1e-12)
+        D.close()
