@@ -13,6 +13,7 @@
 
 #define FMM_MAXP 16
 #define FMM_MAXLEVEL 21
+#define P2P_BIG_LEAF 128u   // leaves with at least this many bodies take the 4-pairs-per-thread P2P
 
 // ---- coefficient indexing (R11: degree n, then alpha_x descending, then alpha_y descending)
 __host__ __device__ __forceinline__ int ncoef_of(int P) { return P * (P + 1) * (P + 2) / 6; }
@@ -79,7 +80,8 @@ struct fmm_ctx {
     int prec = FMM_F64;
     bool use_fast_m2l = true;
     bool use_fast_p2p = true;   // fp32 grouped P2P (FMM_P2P_GENERIC=1 disables)
-    int p2p_variant = 0;        // 0: CTA per leaf over source runs, 1: warp per leaf (FMM_P2P_VARIANT)
+    int p2p_variant = 0;
+    int p2p_np = 2;             // CTA P2P: target pairs per thread (FMM_P2P_NP = 1, 2, 4)        // 0: CTA per leaf over source runs, 1: warp per leaf (FMM_P2P_VARIANT)
     bool canonical_m2l = true;   // sort M2L sources within each target on the device (FMM_CANONICAL_M2L=0: skip)
     bool serial_nearfar = true; // P2P and M2L on one stream (FMM_OVERLAP=1: P2P on the aux stream)   // register-resident M2L where instantiated (FMM_M2L_GENERIC=1 disables)
     int device = 0;
@@ -128,6 +130,8 @@ struct fmm_ctx {
     // P2P source runs: runs[n_runs] = {start body, flat offset}, then rtot[ncell]; run_off[ncell+1]
     int64_t n_runs = 0;
     DevBuf runs, run_off, run_tmp, run_pre, run_len64, dcount2, tcnt, cnt64, big_off, seg_lists;
+    DevBuf leaf_cls;                    // leaves by P2P size class: [0, nleaf) small, [nleaf, 2 nleaf) big
+    int64_t n_leaf_cls[2] = {0, 0};
 
     // expansions
     DevBuf M, L, Mr, Lr, fold_tab;

@@ -618,6 +618,22 @@ __global__ void k_run_emit(const uint64_t* __restrict__ off, const uint32_t* __r
 
 __global__ void k_run_last(int64_t ncell, uint32_t nr, uint32_t* __restrict__ roff) { roff[ncell] = nr; }
 
+// leaves split by size for the P2P kernel: big leaves (>= P2P_BIG_LEAF targets) go to the
+// variant with 4 target pairs per thread (more reuse of each staged source), the rest to 2
+__global__ void k_leaf_split(const uint32_t* __restrict__ leaf_ids, int64_t nleaf, const uint32_t* __restrict__ bc,
+                             uint32_t big, uint32_t* __restrict__ out, unsigned* __restrict__ counts) {
+    const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < nleaf; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        const int c = i < nleaf ? (bc[leaf_ids[i]] >= big ? 1 : 0) : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, c);
+        unsigned base = 0;
+        if (c >= 0 && (peers & lt) == 0) base = atomicAdd(&counts[c], (unsigned)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, __ffs(peers) - 1);
+        if (c >= 0) out[(size_t)c * nleaf + base + __popc(peers & lt)] = leaf_ids[i];
+    }
+}
+
 fmm_status build_runs(fmm_ctx* ctx, cudaStream_t s) {
     const int64_t n = ctx->n_p2p, nc = ctx->ncell;
     FMM_TRY(buf_ensure(ctx, ctx->run_tmp, (size_t)std::max<int64_t>(n, 1) * 4 * 2 + 64));
@@ -630,9 +646,23 @@ fmm_status build_runs(fmm_ctx* ctx, cudaStream_t s) {
     k_run_flags<<<std::max(g, 1), 128, 0, s>>>(off, src, nc, P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), flag);
     FMM_LAUNCH(ctx);
     FMM_TRY(scan_exclusive_u32(ctx, flag, rid, n, d_nr, s));
-    uint32_t nr = 0;
-    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&nr, d_nr, 4, cudaMemcpyDeviceToHost, s));
+    // P2P leaf classes (see k_leaf_split); the counts ride on the same host round trip
+    FMM_TRY(buf_ensure(ctx, ctx->leaf_cls, (size_t)2 * std::max<int64_t>(ctx->nleaf, 1) * 4));
+    unsigned* d_lc = P_<unsigned>(ctx->dcount2) + 14;   // u32 14..15 (0: runs, 4..5: inter, 8..12: classes)
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_lc, 0, 8, s));
+    if (ctx->nleaf > 0) {
+        k_leaf_split<<<(unsigned)std::min<int64_t>((ctx->nleaf + 255) / 256, (int64_t)ctx->num_sms * 8), 256, 0, s>>>(
+            P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, P_<uint32_t>(ctx->c_bc), P2P_BIG_LEAF, P_<uint32_t>(ctx->leaf_cls),
+            d_lc);
+        FMM_LAUNCH(ctx);
+    }
+    uint32_t hr[3] = {0, 0, 0};
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&hr[0], d_nr, 4, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&hr[1], d_lc, 8, cudaMemcpyDeviceToHost, s));
     FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    const uint32_t nr = hr[0];
+    ctx->n_leaf_cls[0] = hr[1];
+    ctx->n_leaf_cls[1] = hr[2];
     ctx->n_runs = nr;
     FMM_TRY(buf_ensure(ctx, ctx->run_off, (size_t)(nc + 2) * 4));
     FMM_TRY(buf_ensure(ctx, ctx->runs, (size_t)std::max<uint32_t>(nr, 1) * 8 + (size_t)(nc + 1) * 4 + 64));

@@ -243,14 +243,14 @@ __global__ void __launch_bounds__(PF_WARPS * 32) k_p2p_f32(const float4* __restr
 // every FP32 step is an f32x2 instruction (FADD2/FMUL2/FFMA2, sm_100): the FMA pipe does the
 // same 13 lane-ops per interaction, but the issue slots they take halve, which leaves room
 // for the LDS, MUFU.RSQ and loop instructions (the scalar form was issue-bound).
-template <bool CHECK>
-__device__ __forceinline__ void p2p_body2(const float4 s, const float2 (&nx)[2], const float2 (&ny)[2],
-                                          const float2 (&nz)[2], float2 (&f)[2], float2 (&gx)[2],
-                                          float2 (&gy)[2], float2 (&gz)[2]) {
+template <bool CHECK, int NP>
+__device__ __forceinline__ void p2p_body2(const float4 s, const float2 (&nx)[NP], const float2 (&ny)[NP],
+                                          const float2 (&nz)[NP], float2 (&f)[NP], float2 (&gx)[NP],
+                                          float2 (&gy)[NP], float2 (&gz)[NP]) {
     const float2 sx = make_float2(s.x, s.x), sy = make_float2(s.y, s.y), sz = make_float2(s.z, s.z);
     const float2 sq = make_float2(s.w, s.w);
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < NP; ++k) {
         const float2 dx = __fadd2_rn(sx, nx[k]), dy = __fadd2_rn(sy, ny[k]), dz = __fadd2_rn(sz, nz[k]);
         const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
         float2 inv = make_float2(rsqrtf(r2.x), rsqrtf(r2.y));
@@ -278,7 +278,7 @@ __device__ __forceinline__ void p2p_body2(const float4 s, const float2 (&nx)[2],
 // and group g consumes entries g, g+G, ... (G consecutive float4 per step).  Only chunks
 // that overlap the target's own leaf take the r^2 > 0 test.
 constexpr int PC_THREADS = 128;
-template <int PC_TILE>
+template <int PC_TILE, int NP>
 __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict__ body,
                                                          const uint32_t* __restrict__ leaf_ids, int64_t nleaf,
                                                          const uint2* __restrict__ runs,
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict
                                                          float* __restrict__ near_phi, float* __restrict__ near_grad,
                                                          unsigned long long* __restrict__ counter) {
     __shared__ __align__(16) float4 s_tile[2][PC_TILE];
-    __shared__ float4 s_red[PC_THREADS * PF_T];
+    __shared__ float4 s_red[PC_THREADS * (2 * NP)];
     __shared__ unsigned long long s_leaf;
     __shared__ uint32_t s_self;
     const int tid = threadIdx.x;
@@ -309,17 +309,17 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict
         }
         __syncthreads();
         const uint32_t selfF = s_self;
-        for (uint32_t t0 = 0; t0 < nt_all; t0 += PC_THREADS * PF_T) {
-            const uint32_t nt = min(nt_all - t0, (uint32_t)(PC_THREADS * PF_T));
-            const int lpg = (int)((nt + PF_T - 1) / PF_T);
+        for (uint32_t t0 = 0; t0 < nt_all; t0 += PC_THREADS * (2 * NP)) {
+            const uint32_t nt = min(nt_all - t0, (uint32_t)(PC_THREADS * (2 * NP)));
+            const int lpg = (int)((nt + (2 * NP) - 1) / (2 * NP));
             const int G = min(PC_THREADS / lpg, 64);
             const int g = tid / lpg, j = tid - g * lpg;
             const bool active = g < G;
             const uint32_t CH = (uint32_t)(G * (PC_TILE / G));
             // target slot k of this thread is t = j + k*lpg; slots (0,1) and (2,3) form the pairs
-            float2 nx[2], ny[2], nz[2], f[2], gx[2], gy[2], gz[2];
+            float2 nx[NP], ny[NP], nz[NP], f[NP], gx[NP], gy[NP], gz[NP];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < NP; ++h) {
                 float px[2], py[2], pz[2];
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
@@ -365,28 +365,28 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict
                     const float4* tl = s_tile[k & 1];
                     const bool self = f0 < selfF + nt_all && selfF < f0 + len;
                     if (self) {
-                        for (uint32_t i = g; i < len; i += G) p2p_body2<true>(tl[i], nx, ny, nz, f, gx, gy, gz);
+                        for (uint32_t i = g; i < len; i += G) p2p_body2<true, NP>(tl[i], nx, ny, nz, f, gx, gy, gz);
                     } else {
-                        for (uint32_t i = g; i < len; i += G) p2p_body2<false>(tl[i], nx, ny, nz, f, gx, gy, gz);
+                        for (uint32_t i = g; i < len; i += G) p2p_body2<false, NP>(tl[i], nx, ny, nz, f, gx, gy, gz);
                     }
                 }
                 __syncthreads();
             }
             cp_async_wait_0();
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                s_red[tid * PF_T + 2 * h] = make_float4(f[h].x, gx[h].x, gy[h].x, gz[h].x);
-                s_red[tid * PF_T + 2 * h + 1] = make_float4(f[h].y, gx[h].y, gy[h].y, gz[h].y);
+            for (int h = 0; h < NP; ++h) {
+                s_red[tid * (2 * NP) + 2 * h] = make_float4(f[h].x, gx[h].x, gy[h].x, gz[h].x);
+                s_red[tid * (2 * NP) + 2 * h + 1] = make_float4(f[h].y, gx[h].y, gy[h].y, gz[h].y);
             }
             __syncthreads();
             if (g == 0) {
 #pragma unroll
-                for (int k = 0; k < PF_T; ++k) {
+                for (int k = 0; k < (2 * NP); ++k) {
                     const uint32_t t = (uint32_t)(j + k * lpg);
                     if (t < nt) {
-                        float4 acc = s_red[tid * PF_T + k];
+                        float4 acc = s_red[tid * (2 * NP) + k];
                         for (int gg = 1; gg < G; ++gg) {
-                            const float4 v = s_red[(gg * lpg + j) * PF_T + k];
+                            const float4 v = s_red[(gg * lpg + j) * (2 * NP) + k];
                             acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
                         }
                         const int64_t o = (int64_t)tb + t0 + t;
@@ -409,19 +409,27 @@ fmm_status p2p_t(fmm_ctx* ctx, cudaStream_t s) {
     FMM_TRY(buf_ensure(ctx, ctx->near_grad, (size_t)ctx->n * 3 * sizeof(Real)));
     PhaseScope pk(ctx, PH_P2P_KERNEL, s);
     if (std::is_same<Real, float>::value && ctx->use_fast_p2p && ctx->p2p_variant == 0) {
+        // small leaves: 2 target pairs per thread; big leaves (>= P2P_BIG_LEAF): 4 pairs per
+        // thread (measured: c2 leaves of ~32 run best with 2, sphere leaves of ~234 with 4)
         FMM_TRY(buf_ensure(ctx, ctx->cnt_tmp2, 64));
         unsigned long long* counter = P_<unsigned long long>(ctx->cnt_tmp2);
-        FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 8, s));
-        int nb = 0;
-        auto kern = k_p2p_cta<256>;
-        FMM_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, PC_THREADS, 0));
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 16, s));
         const uint2* runs = P_<uint2>(ctx->runs);
         const uint32_t* rtot = reinterpret_cast<const uint32_t*>(runs + std::max<int64_t>(ctx->n_runs, 1));
-        kern<<<ctx->num_sms * std::max(nb, 1), PC_THREADS, 0, s>>>(
-            P_<float4>(ctx->body), P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, runs, P_<uint32_t>(ctx->run_off), rtot,
-            P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), (float*)ctx->near_phi.p, (float*)ctx->near_grad.p,
-            counter);
-        FMM_LAUNCH(ctx);
+        const uint32_t* lists = P_<uint32_t>(ctx->leaf_cls);
+        auto launch = [&](auto kern, const uint32_t* ids, int64_t cnt, unsigned long long* ctr) -> fmm_status {
+            if (cnt == 0) return FMM_OK;
+            int nb = 0;
+            FMM_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, PC_THREADS, 0));
+            const int64_t g = std::min<int64_t>((int64_t)ctx->num_sms * std::max(nb, 1), cnt);
+            kern<<<(unsigned)g, PC_THREADS, 0, s>>>(P_<float4>(ctx->body), ids, cnt, runs, P_<uint32_t>(ctx->run_off),
+                                                   rtot, P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc),
+                                                   (float*)ctx->near_phi.p, (float*)ctx->near_grad.p, ctr);
+            FMM_LAUNCH(ctx);
+            return FMM_OK;
+        };
+        FMM_TRY(launch(k_p2p_cta<256, 2>, lists, ctx->n_leaf_cls[0], counter));
+        FMM_TRY(launch(k_p2p_cta<256, 4>, lists + ctx->nleaf, ctx->n_leaf_cls[1], counter + 1));
         FMM_CUDA_TRY(ctx, cudaGetLastError());
         return FMM_OK;
     }
