@@ -14,6 +14,7 @@
 #define FMM_MAXP 16
 #define FMM_MAXLEVEL 21
 #define P2P_BIG_LEAF 128u   // leaves with at least this many bodies take the 4-pairs-per-thread P2P
+#define P2P_TINY_LEAF 16u   // leaves with at most this many bodies take the warp-per-leaf P2P
 
 // ---- coefficient indexing (R11: degree n, then alpha_x descending, then alpha_y descending)
 __host__ __device__ __forceinline__ int ncoef_of(int P) { return P * (P + 1) * (P + 2) / 6; }
@@ -130,8 +131,8 @@ struct fmm_ctx {
     // P2P source runs: runs[n_runs] = {start body, flat offset}, then rtot[ncell]; run_off[ncell+1]
     int64_t n_runs = 0;
     DevBuf runs, run_off, run_tmp, run_pre, run_len64, dcount2, tcnt, cnt64, big_off, seg_lists;
-    DevBuf leaf_cls;                    // leaves by P2P size class: [0, nleaf) small, [nleaf, 2 nleaf) big
-    int64_t n_leaf_cls[2] = {0, 0};
+    DevBuf leaf_cls;                    // leaves by P2P size class c at [c nleaf, (c+1) nleaf): tiny, mid, big
+    int64_t n_leaf_cls[3] = {0, 0, 0};
 
     // expansions
     DevBuf M, L, Mr, Lr, fold_tab;

@@ -618,14 +618,33 @@ __global__ void k_run_emit(const uint64_t* __restrict__ off, const uint32_t* __r
 
 __global__ void k_run_last(int64_t ncell, uint32_t nr, uint32_t* __restrict__ roff) { roff[ncell] = nr; }
 
-// leaves split by size for the P2P kernel: big leaves (>= P2P_BIG_LEAF targets) go to the
-// variant with 4 target pairs per thread (more reuse of each staged source), the rest to 2
+// leaves split by size for the P2P kernel: tiny leaves (<= P2P_TINY_LEAF bodies) to a warp per
+// leaf, mid-size to a 128-thread CTA with 2 target pairs per thread, big leaves
+// (>= P2P_BIG_LEAF) to a CTA with 4 pairs per thread (more reuse of each staged source).  The
+// tiny class is used only when it holds >= 1/16 of the leaves (else its leaves join the mid
+// class): decided from this build's counts, so the kernel -- and the fp32 summation order --
+// of every leaf is a function of the input alone.
+__global__ void k_leaf_count(const uint32_t* __restrict__ leaf_ids, int64_t nleaf, const uint32_t* __restrict__ bc,
+                             unsigned* __restrict__ counts) {
+    unsigned c0 = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nleaf; i += (int64_t)gridDim.x * blockDim.x)
+        c0 += bc[leaf_ids[i]] <= P2P_TINY_LEAF;
+    for (int o = 16; o; o >>= 1) c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+    if ((threadIdx.x & 31) == 0 && c0) atomicAdd(&counts[3], c0);
+}
+
 __global__ void k_leaf_split(const uint32_t* __restrict__ leaf_ids, int64_t nleaf, const uint32_t* __restrict__ bc,
-                             uint32_t big, uint32_t* __restrict__ out, unsigned* __restrict__ counts) {
+                             const unsigned* __restrict__ tiny_count, uint32_t* __restrict__ out,
+                             unsigned* __restrict__ counts) {
     const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+    const bool tiny_on = (int64_t)(*tiny_count) * 16 >= nleaf;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < nleaf; i0 += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = i0 + threadIdx.x;
-        const int c = i < nleaf ? (bc[leaf_ids[i]] >= big ? 1 : 0) : -1;
+        int c = -1;
+        if (i < nleaf) {
+            const uint32_t m = bc[leaf_ids[i]];
+            c = (tiny_on && m <= P2P_TINY_LEAF) ? 0 : (m >= P2P_BIG_LEAF ? 2 : 1);
+        }
         const unsigned peers = __match_any_sync(0xffffffffu, c);
         unsigned base = 0;
         if (c >= 0 && (peers & lt) == 0) base = atomicAdd(&counts[c], (unsigned)__popc(peers));
@@ -647,22 +666,22 @@ fmm_status build_runs(fmm_ctx* ctx, cudaStream_t s) {
     FMM_LAUNCH(ctx);
     FMM_TRY(scan_exclusive_u32(ctx, flag, rid, n, d_nr, s));
     // P2P leaf classes (see k_leaf_split); the counts ride on the same host round trip
-    FMM_TRY(buf_ensure(ctx, ctx->leaf_cls, (size_t)2 * std::max<int64_t>(ctx->nleaf, 1) * 4));
-    unsigned* d_lc = P_<unsigned>(ctx->dcount2) + 14;   // u32 14..15 (0: runs, 4..5: inter, 8..12: classes)
-    FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_lc, 0, 8, s));
+    FMM_TRY(buf_ensure(ctx, ctx->leaf_cls, (size_t)3 * std::max<int64_t>(ctx->nleaf, 1) * 4));
+    unsigned* d_lc = P_<unsigned>(ctx->dcount2) + 16;   // u32 16..19 (0: runs, 4..5: inter, 8..12: classes)
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_lc, 0, 16, s));
     if (ctx->nleaf > 0) {
-        k_leaf_split<<<(unsigned)std::min<int64_t>((ctx->nleaf + 255) / 256, (int64_t)ctx->num_sms * 8), 256, 0, s>>>(
-            P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, P_<uint32_t>(ctx->c_bc), P2P_BIG_LEAF, P_<uint32_t>(ctx->leaf_cls),
-            d_lc);
-        FMM_LAUNCH(ctx);
+        const unsigned gl = (unsigned)std::min<int64_t>((ctx->nleaf + 255) / 256, (int64_t)ctx->num_sms * 8);
+        k_leaf_count<<<gl, 256, 0, s>>>(P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, P_<uint32_t>(ctx->c_bc), d_lc);
+        k_leaf_split<<<gl, 256, 0, s>>>(P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, P_<uint32_t>(ctx->c_bc), d_lc + 3,
+                                        P_<uint32_t>(ctx->leaf_cls), d_lc);
+        ctx->launches += 2;
     }
-    uint32_t hr[3] = {0, 0, 0};
+    uint32_t hr[4] = {0, 0, 0, 0};
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&hr[0], d_nr, 4, cudaMemcpyDeviceToHost, s));
-    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&hr[1], d_lc, 8, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&hr[1], d_lc, 12, cudaMemcpyDeviceToHost, s));
     FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
     const uint32_t nr = hr[0];
-    ctx->n_leaf_cls[0] = hr[1];
-    ctx->n_leaf_cls[1] = hr[2];
+    for (int c = 0; c < 3; ++c) ctx->n_leaf_cls[c] = hr[1 + c];
     ctx->n_runs = nr;
     FMM_TRY(buf_ensure(ctx, ctx->run_off, (size_t)(nc + 2) * 4));
     FMM_TRY(buf_ensure(ctx, ctx->runs, (size_t)std::max<uint32_t>(nr, 1) * 8 + (size_t)(nc + 1) * 4 + 64));
@@ -686,7 +705,7 @@ fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append
     FMM_TRY(buf_ensure(ctx, ctx->tcnt, (size_t)nc * 2 * 4));
     uint32_t* tcnt_m2l = P_<uint32_t>(ctx->tcnt);
     uint32_t* tcnt_p2p = tcnt_m2l + nc;
-    FMM_TRY(buf_ensure(ctx, ctx->dcount2, 64));
+    FMM_TRY(buf_ensure(ctx, ctx->dcount2, 128));
     PhaseScope ps(ctx, PH_DTT, s);
     FMM_TRY(buf_ensure(ctx, ctx->fr_a, (size_t)std::max(nseeds, 128) * 8));
     FMM_TRY(buf_ensure(ctx, ctx->dcount, 64));

@@ -278,7 +278,10 @@ __device__ __forceinline__ void p2p_body2(const float4 s, const float2 (&nx)[NP]
 // and group g consumes entries g, g+G, ... (G consecutive float4 per step).  Only chunks
 // that overlap the target's own leaf take the r^2 > 0 test.
 constexpr int PC_THREADS = 128;
-template <int PC_TILE, int NP>
+// GT threads ("team") per target leaf; a block of PC_THREADS holds PC_THREADS/GT teams that
+// work independently (GT = 32: a warp per leaf for small leaves, synchronised with
+// __syncwarp; GT = 128: the whole block).
+template <int GT, int PC_TILE, int NP>
 __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict__ body,
                                                          const uint32_t* __restrict__ leaf_ids, int64_t nleaf,
                                                          const uint2* __restrict__ runs,
@@ -287,36 +290,45 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict
                                                          const uint32_t* __restrict__ bb, const uint32_t* __restrict__ bc,
                                                          float* __restrict__ near_phi, float* __restrict__ near_grad,
                                                          unsigned long long* __restrict__ counter) {
-    __shared__ __align__(16) float4 s_tile[2][PC_TILE];
-    __shared__ float4 s_red[PC_THREADS * (2 * NP)];
-    __shared__ unsigned long long s_leaf;
-    __shared__ uint32_t s_self;
-    const int tid = threadIdx.x;
+    constexpr int TEAMS = PC_THREADS / GT;
+    __shared__ __align__(16) float4 s_tile_all[TEAMS][2][PC_TILE];
+    __shared__ float4 s_red_all[TEAMS][GT * (2 * NP)];
+    __shared__ unsigned long long s_leaf_all[TEAMS];
+    __shared__ uint32_t s_self_all[TEAMS];
+    const int team = threadIdx.x / GT, tid = threadIdx.x - team * GT;
+    float4 (*s_tile)[PC_TILE] = s_tile_all[team];
+    float4* s_red = s_red_all[team];
+    unsigned long long& s_leaf = s_leaf_all[team];
+    uint32_t& s_self = s_self_all[team];
+    auto team_sync = [] {
+        if constexpr (GT == 32) __syncwarp();
+        else __syncthreads();
+    };
     for (;;) {
-        __syncthreads();
+        team_sync();
         if (tid == 0) s_leaf = atomicAdd(counter, 1ull);
-        __syncthreads();
+        team_sync();
         const unsigned long long li = s_leaf;
         if (li >= (unsigned long long)nleaf) break;
         const uint32_t a = leaf_ids[li];
         const uint32_t tb = bb[a], nt_all = bc[a];
         const uint32_t r0 = roff[a], r1 = roff[a + 1], ns = rtot[a];
         // flat offset of the target's own bodies in its source stream
-        for (uint32_t r = r0 + tid; r < r1; r += PC_THREADS) {
+        for (uint32_t r = r0 + tid; r < r1; r += GT) {
             const uint2 ru = runs[r];
             const uint32_t end = (r + 1 < r1) ? runs[r + 1].y : ns;
             if (ru.x <= tb && tb < ru.x + (end - ru.y)) s_self = ru.y + (tb - ru.x);
         }
-        __syncthreads();
+        team_sync();
         const uint32_t selfF = s_self;
-        for (uint32_t t0 = 0; t0 < nt_all; t0 += PC_THREADS * (2 * NP)) {
-            const uint32_t nt = min(nt_all - t0, (uint32_t)(PC_THREADS * (2 * NP)));
+        for (uint32_t t0 = 0; t0 < nt_all; t0 += GT * (2 * NP)) {
+            const uint32_t nt = min(nt_all - t0, (uint32_t)(GT * (2 * NP)));
             const int lpg = (int)((nt + (2 * NP) - 1) / (2 * NP));
-            const int G = min(PC_THREADS / lpg, 64);
+            const int G = min(GT / lpg, 64);
             const int g = tid / lpg, j = tid - g * lpg;
             const bool active = g < G;
             const uint32_t CH = (uint32_t)(G * (PC_TILE / G));
-            // target slot k of this thread is t = j + k*lpg; slots (0,1) and (2,3) form the pairs
+            // target slot k of this thread is t = j + k*lpg; slots (2h, 2h+1) form pair h
             float2 nx[NP], ny[NP], nz[NP], f[NP], gx[NP], gy[NP], gz[NP];
 #pragma unroll
             for (int h = 0; h < NP; ++h) {
@@ -332,8 +344,8 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict
                 nz[h] = make_float2(pz[0], pz[1]);
                 f[h] = gx[h] = gy[h] = gz[h] = make_float2(0.f, 0.f);
             }
-            // loader cursors for flat indices tid and tid + 128 of every chunk
-            constexpr int NH = PC_TILE / PC_THREADS;
+            // loader cursors for flat indices tid, tid + GT, ... of every chunk
+            constexpr int NH = PC_TILE / GT;
             uint32_t cur[NH];
 #pragma unroll
             for (int h = 0; h < NH; ++h) cur[h] = r0;
@@ -342,7 +354,7 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict
                 const uint32_t len = min(CH, ns - f0);
 #pragma unroll
                 for (int h = 0; h < NH; ++h) {
-                    const uint32_t i = (uint32_t)tid + (uint32_t)h * PC_THREADS;
+                    const uint32_t i = (uint32_t)tid + (uint32_t)h * GT;
                     if (i < len) {
                         const uint32_t fl = f0 + i;
                         while (cur[h] + 1 < r1 && runs[cur[h] + 1].y <= fl) ++cur[h];
@@ -358,7 +370,7 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict
                 if (k + 1 < nch) load_chunk(k + 1, (k + 1) & 1);
                 cp_async_commit();
                 cp_async_wait_1();
-                __syncthreads();
+                team_sync();
                 const uint32_t f0 = k * CH;
                 const uint32_t len = min(CH, ns - f0);
                 if (active) {
@@ -370,7 +382,7 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict
                         for (uint32_t i = g; i < len; i += G) p2p_body2<false, NP>(tl[i], nx, ny, nz, f, gx, gy, gz);
                     }
                 }
-                __syncthreads();
+                team_sync();
             }
             cp_async_wait_0();
 #pragma unroll
@@ -378,7 +390,7 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict
                 s_red[tid * (2 * NP) + 2 * h] = make_float4(f[h].x, gx[h].x, gy[h].x, gz[h].x);
                 s_red[tid * (2 * NP) + 2 * h + 1] = make_float4(f[h].y, gx[h].y, gy[h].y, gz[h].y);
             }
-            __syncthreads();
+            team_sync();
             if (g == 0) {
 #pragma unroll
                 for (int k = 0; k < (2 * NP); ++k) {
@@ -397,7 +409,7 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict
                     }
                 }
             }
-            __syncthreads();
+            team_sync();
         }
     }
 }
@@ -409,11 +421,12 @@ fmm_status p2p_t(fmm_ctx* ctx, cudaStream_t s) {
     FMM_TRY(buf_ensure(ctx, ctx->near_grad, (size_t)ctx->n * 3 * sizeof(Real)));
     PhaseScope pk(ctx, PH_P2P_KERNEL, s);
     if (std::is_same<Real, float>::value && ctx->use_fast_p2p && ctx->p2p_variant == 0) {
-        // small leaves: 2 target pairs per thread; big leaves (>= P2P_BIG_LEAF): 4 pairs per
-        // thread (measured: c2 leaves of ~32 run best with 2, sphere leaves of ~234 with 4)
+        // three leaf classes (k_leaf_split): tiny (<= P2P_TINY_LEAF) a warp per leaf, mid a CTA with
+        // 2 target pairs per thread, big (>= P2P_BIG_LEAF) a CTA with 4 (measured: mean-8 leaves
+        // 1.9x faster per warp than per CTA; c2's ~32-body leaves best at 2 pairs, sphere's ~234 at 4)
         FMM_TRY(buf_ensure(ctx, ctx->cnt_tmp2, 64));
         unsigned long long* counter = P_<unsigned long long>(ctx->cnt_tmp2);
-        FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 16, s));
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 24, s));
         const uint2* runs = P_<uint2>(ctx->runs);
         const uint32_t* rtot = reinterpret_cast<const uint32_t*>(runs + std::max<int64_t>(ctx->n_runs, 1));
         const uint32_t* lists = P_<uint32_t>(ctx->leaf_cls);
@@ -421,15 +434,16 @@ fmm_status p2p_t(fmm_ctx* ctx, cudaStream_t s) {
             if (cnt == 0) return FMM_OK;
             int nb = 0;
             FMM_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, PC_THREADS, 0));
-            const int64_t g = std::min<int64_t>((int64_t)ctx->num_sms * std::max(nb, 1), cnt);
+            const int64_t g = std::min<int64_t>((int64_t)ctx->num_sms * std::max(nb, 1), (cnt + 3) / 4 * 4);
             kern<<<(unsigned)g, PC_THREADS, 0, s>>>(P_<float4>(ctx->body), ids, cnt, runs, P_<uint32_t>(ctx->run_off),
                                                    rtot, P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc),
                                                    (float*)ctx->near_phi.p, (float*)ctx->near_grad.p, ctr);
             FMM_LAUNCH(ctx);
             return FMM_OK;
         };
-        FMM_TRY(launch(k_p2p_cta<256, 2>, lists, ctx->n_leaf_cls[0], counter));
-        FMM_TRY(launch(k_p2p_cta<256, 4>, lists + ctx->nleaf, ctx->n_leaf_cls[1], counter + 1));
+        FMM_TRY(launch(k_p2p_cta<32, 64, 1>, lists, ctx->n_leaf_cls[0], counter));
+        FMM_TRY(launch(k_p2p_cta<128, 256, 2>, lists + ctx->nleaf, ctx->n_leaf_cls[1], counter + 1));
+        FMM_TRY(launch(k_p2p_cta<128, 256, 4>, lists + 2 * ctx->nleaf, ctx->n_leaf_cls[2], counter + 2));
         FMM_CUDA_TRY(ctx, cudaGetLastError());
         return FMM_OK;
     }
