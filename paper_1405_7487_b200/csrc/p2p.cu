@@ -300,9 +300,10 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict
     float4* s_red = s_red_all[team];
     unsigned long long& s_leaf = s_leaf_all[team];
     uint32_t& s_self = s_self_all[team];
-    auto team_sync = [] {
+    auto team_sync = [team] {
         if constexpr (GT == 32) __syncwarp();
-        else __syncthreads();
+        else if constexpr (GT == PC_THREADS) __syncthreads();
+        else asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(GT) : "memory");   // named barrier per team
     };
     for (;;) {
         team_sync();
