@@ -122,6 +122,8 @@ fmm_status fmm_create(int64_t n_max, int p, double theta, int ncrit, int prec, i
         ctx->serial_nearfar = !(g4 && g4[0] == '1');
         const char* g5 = getenv("FMM_CANONICAL_M2L");
         ctx->canonical_m2l = !(g5 && g5[0] == '0');
+        const char* g6 = getenv("FMM_M2L_VARIANT");
+        ctx->m2l_variant = g6 ? atoi(g6) : 0;
     }
     if (cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||

@@ -82,6 +82,7 @@ struct fmm_ctx {
     bool use_fast_m2l = true;
     bool use_fast_p2p = true;   // fp32 grouped P2P (FMM_P2P_GENERIC=1 disables)
     int p2p_variant = 0;
+    int m2l_variant = 0;        // fp32 register M2L: 0 mirror-paired f32x2, 1 scalar (FMM_M2L_VARIANT)
     int p2p_np = 2;             // CTA P2P: target pairs per thread (FMM_P2P_NP = 1, 2, 4)        // 0: CTA per leaf over source runs, 1: warp per leaf (FMM_P2P_VARIANT)
     bool canonical_m2l = true;   // sort M2L sources within each target on the device (FMM_CANONICAL_M2L=0: skip)
     bool serial_nearfar = true; // P2P and M2L on one stream (FMM_OVERLAP=1: P2P on the aux stream)   // register-resident M2L where instantiated (FMM_M2L_GENERIC=1 disables)

@@ -386,7 +386,7 @@ fmm_status m2l_fast_t(fmm_ctx* ctx, cudaStream_t s) {
     const int nw = 4;
     int g = (int)std::min<int64_t>((nc + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
     const int gp = (int)std::min<int64_t>((nct + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
-    if (ctx->fold_P != P) {
+    if (ctx->fold_P != P) {   // scalar layout table (the mirror kernel keys its own as 1000 + P)
         const FoldTable t = build_fold_table(P, RF<P>::NS, NSP);
         const size_t nt = t.k.size();
         FMM_TRY(buf_ensure(ctx, ctx->fold_tab, (NSP + 1) * 4 + NSP * 4 + nt * 4 + nt * 8 + 64));
@@ -424,11 +424,440 @@ fmm_status m2l_fast_t(fmm_ctx* ctx, cudaStream_t s) {
     FMM_CUDA_TRY(ctx, cudaGetLastError());
     return FMM_OK;
 }
+
+// ================================================================ mirror-paired M2L (fp32)
+// The harmonic 2D correlations are symmetric under the y <-> z mirror M(y,z) = (z,y): the
+// recurrence gives D at M(k) from the recurrence at k with u_y and u_z exchanged, and
+// M(p) + M(q) = M(p+q).  So every off-diagonal canonical index (y > z) holds the PAIR
+// {X[y,z], X[z,y]} of D0, D1, L0, L1 and of the streamed S0, S1, N, and one f32x2 instruction
+// (FFMA2/FMUL2, sm_100) does the work for an index and its mirror:
+//   recurrence:  DP[y,z] = A ({y uy, y uz} * DP(y-1,z) + {z uz, z uy} * DP(y,z-1)) + B (...)
+//   contraction: LP[p] += SP[q] * DP(p+q)  (element q)   and   LP[p] += swap(SP[q]) * DP(p+Mq)
+//                (element Mq); DP(k) of a non-canonical k is swap(DP[Mk]); diagonal indices
+//                (y == z) are scalars used through the .F32 broadcast operand.
+// All swaps and broadcasts are FFMA2 operand modifiers (no extra instructions).  The pair body is
+// ~1,500 instructions at P=10 (the scalar kernel: ~3,100), within the 32 KB L1.5 I-cache.
+namespace mir {
+__host__ __device__ constexpr int t2m(int y, int z) { return (y + z) * (y + z + 1) / 2 + z; }
+// off-diagonal canonical (y > z) slots of degree <= D, in t2 order of (y, z)
+__host__ __device__ constexpr int noff(int D) {
+    int c = 0;
+    for (int n = 0; n <= D; ++n) c += (n + 1) / 2;
+    return c;
+}
+__host__ __device__ constexpr int ndia(int D) { return D / 2 + 1; }
+__host__ __device__ constexpr int off(int y, int z) {   // y > z
+    int c = noff(y + z - 1);
+    for (int zz = 0; zz < z; ++zz)
+        if (y + z - zz > zz) ++c;
+    return c;
+}
+
+template <int P>
+struct L {
+    static constexpr int D0 = P - 1, D1 = P - 2;
+    static constexpr int O0 = noff(D0), O1 = noff(D1 < 0 ? 0 : D1), G0 = ndia(D0), G1 = ndia(D1 < 0 ? 0 : D1);
+    // stream (floats): S0 pairs | S1 pairs | N pairs | S0 diag | S1 diag | N diag
+    static constexpr int BS0 = 0, BS1 = 2 * O0, BN = BS1 + 2 * O1, BD0 = BN + 2 * O0, BD1 = BD0 + G0,
+                         BDN = BD1 + G1, NS = BDN + G0, NSP = (NS + 3) / 4 * 4, NCH = NSP / 4;
+    static constexpr int NL = P * (P + 1) / 2 + (P - 1) * P / 2;   // reduced L: L0 | L1 (t2 order)
+};
+
+template <int P>
+struct Regs {
+    using K = L<P>;
+    float2 D0p[K::O0];
+    float D0d[K::G0];
+    float2 D1p[K::O1 > 0 ? K::O1 : 1];
+    float D1d[K::G1];
+    float2 L0p[K::O0];
+    float L0d[K::G0];
+    float2 L1p[K::O1 > 0 ? K::O1 : 1];
+    float L1d[K::G1];
+};
+
+__device__ __forceinline__ float2 sw(float2 v) { return make_float2(v.y, v.x); }
+__device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
+
+// {X[y,z], X[z,y]} of a paired array for any (y, z)
+template <int Y, int Z>
+__device__ __forceinline__ float2 pr(const float2* p, const float* d) {
+    if constexpr (Y > Z) return p[off(Y, Z)];
+    else if constexpr (Y < Z) return sw(p[off(Z, Y)]);
+    else return bc(d[Y]);
+}
+
+template <int P>
+__device__ __forceinline__ void derivs_mir(float ux, float uy, float uz, Regs<P>& R) {
+    const float r2 = ux * ux + uy * uy + uz * uz;
+    const float ir2 = __frcp_rn(r2);
+    float2 YU[P];   // {m uy, m uz}
+#pragma unroll
+    for (int m = 1; m < P; ++m) YU[m] = make_float2(float(m) * uy, float(m) * uz);
+    R.D0d[0] = rsqrtf(r2);
+    sfor<1, P>([&](auto nn) {
+        constexpr int n = decltype(nn)::value;
+        const float A = float(-(2.0 * n - 1.0) / n) * ir2;
+        const float B = float(-(n - 1.0) / n) * ir2;
+        // D0, degree n: canonical (y >= z), y + z = n
+        sfor<0, n / 2 + 1>([&](auto zz) {
+            constexpr int z = decltype(zz)::value, y = n - z;
+            if constexpr (y > z) {
+                float2 s1;
+                if constexpr (z > 0)
+                    s1 = __ffma2_rn(sw(YU[z]), pr<y, z - 1>(R.D0p, R.D0d), __fmul2_rn(YU[y], pr<y - 1, z>(R.D0p, R.D0d)));
+                else
+                    s1 = __fmul2_rn(YU[y], pr<y - 1, z>(R.D0p, R.D0d));
+                float2 v;
+                if constexpr (n > 1) {
+                    float2 s2 = make_float2(0.f, 0.f);
+                    if constexpr (y > 1) s2 = __fmul2_rn(bc(float(y * (y - 1))), pr<y - 2, z>(R.D0p, R.D0d));
+                    if constexpr (z > 1) s2 = __ffma2_rn(bc(float(z * (z - 1))), pr<y, z - 2>(R.D0p, R.D0d), s2);
+                    v = __ffma2_rn(bc(A), s1, __fmul2_rn(bc(B), s2));
+                } else {
+                    v = __fmul2_rn(bc(A), s1);
+                }
+                R.D0p[off(y, z)] = v;
+            } else {   // diagonal: D0[y,y] = A y (uy D0[y-1,y] + uz D0[y,y-1]) + B y(y-1) (D0[y-2,y] + D0[y,y-2])
+                const float2 q1 = R.D0p[off(y, y - 1)];
+                const float s1 = fmaf(YU[y].y, q1.x, YU[y].x * q1.y);
+                float v;
+                if constexpr (y > 1) {
+                    const float2 q2 = R.D0p[off(y, y - 2)];
+                    v = fmaf(A, s1, B * (float(y * (y - 1)) * (q2.x + q2.y)));
+                } else {
+                    v = A * s1;
+                }
+                R.D0d[y] = v;
+            }
+        });
+        // D1, total degree n: canonical (y >= z), y + z = n - 1
+        sfor<0, (n - 1) / 2 + 1>([&](auto zz) {
+            constexpr int z = decltype(zz)::value, y = n - 1 - z;
+            if constexpr (y > z) {
+                float2 s1 = __fmul2_rn(bc(ux), pr<y, z>(R.D0p, R.D0d));
+                if constexpr (y > 0) s1 = __ffma2_rn(YU[y], pr<y - 1, z>(R.D1p, R.D1d), s1);
+                if constexpr (z > 0) s1 = __ffma2_rn(sw(YU[z]), pr<y, z - 1>(R.D1p, R.D1d), s1);
+                float2 v;
+                if constexpr (n > 1) {
+                    float2 s2 = make_float2(0.f, 0.f);
+                    if constexpr (y > 1) s2 = __fmul2_rn(bc(float(y * (y - 1))), pr<y - 2, z>(R.D1p, R.D1d));
+                    if constexpr (z > 1) s2 = __ffma2_rn(bc(float(z * (z - 1))), pr<y, z - 2>(R.D1p, R.D1d), s2);
+                    v = __ffma2_rn(bc(A), s1, __fmul2_rn(bc(B), s2));
+                } else {
+                    v = __fmul2_rn(bc(A), s1);
+                }
+                R.D1p[off(y, z)] = v;
+            } else {   // diagonal y == z
+                float s1 = ux * R.D0d[y];
+                if constexpr (y > 0) {
+                    const float2 q1 = R.D1p[off(y, y - 1)];
+                    s1 = fmaf(YU[y].x, q1.y, s1);
+                    s1 = fmaf(YU[y].y, q1.x, s1);
+                }
+                float v;
+                if constexpr (y > 1) {
+                    const float2 q2 = R.D1p[off(y, y - 2)];
+                    v = fmaf(A, s1, B * (float(y * (y - 1)) * (q2.x + q2.y)));
+                } else if constexpr (n > 1) {
+                    v = A * s1;
+                } else {
+                    v = A * s1;
+                }
+                R.D1d[y] = v;
+            }
+        });
+    });
+}
+
+// element pair {S[q], S[Mq]} (q = (QY, QZ), QY > QZ) into L += S (x) D for |p| + |q| <= DMAX
+template <int DMAX, int QY, int QZ, int NO, int NG, int DO, int DG>
+__device__ __forceinline__ void corr_pair(float2 sp, float2 (&Lp)[NO], float (&Ld)[NG], const float2 (&Dp)[DO],
+                                          const float (&Dd)[DG]) {
+    constexpr int m = QY + QZ;
+    sfor<0, DMAX - m + 1>([&](auto pp) {
+        constexpr int pn = decltype(pp)::value;
+        sfor<0, pn / 2 + 1>([&](auto zz) {
+            constexpr int pz = decltype(zz)::value, py = pn - pz;
+            if constexpr (py > pz) {
+                Lp[off(py, pz)] = __ffma2_rn(sp, pr<py + QY, pz + QZ>(Dp, Dd), Lp[off(py, pz)]);
+                Lp[off(py, pz)] = __ffma2_rn(sw(sp), pr<py + QZ, pz + QY>(Dp, Dd), Lp[off(py, pz)]);
+            } else {   // diagonal p: k = p + q is canonical off-diagonal; elements q and Mq
+                const float2 dk = Dp[off(py + QY, pz + QZ)];
+                Ld[py] = fmaf(sp.x, dk.x, Ld[py]);
+                Ld[py] = fmaf(sp.y, dk.y, Ld[py]);
+            }
+        });
+    });
+}
+
+// diagonal element S[q] (q = (Q, Q)) into L += S (x) D for |p| + |q| <= DMAX
+template <int DMAX, int Q, int NO, int NG, int DO, int DG>
+__device__ __forceinline__ void corr_diag(float s, float2 (&Lp)[NO], float (&Ld)[NG], const float2 (&Dp)[DO],
+                                          const float (&Dd)[DG]) {
+    constexpr int m = 2 * Q;
+    sfor<0, DMAX - m + 1>([&](auto pp) {
+        constexpr int pn = decltype(pp)::value;
+        sfor<0, pn / 2 + 1>([&](auto zz) {
+            constexpr int pz = decltype(zz)::value, py = pn - pz;
+            if constexpr (py > pz) Lp[off(py, pz)] = __ffma2_rn(bc(s), pr<py + Q, pz + Q>(Dp, Dd), Lp[off(py, pz)]);
+            else Ld[py] = fmaf(s, Dd[py + Q], Ld[py]);
+        });
+    });
+}
+
+// canonical off-diagonal slot index j of degree <= D -> (y, z)
+__host__ __device__ constexpr int slot_y(int j) {
+    for (int n = 0;; ++n)
+        for (int z = 0; 2 * z < n; ++z)
+            if (j-- == 0) return n - z;
+}
+__host__ __device__ constexpr int slot_z(int j) {
+    for (int n = 0;; ++n)
+        for (int z = 0; 2 * z < n; ++z)
+            if (j-- == 0) return z;
+}
+
+template <int P>
+__global__ void __launch_bounds__(128, 2)
+    k_m2l_mir(int64_t ncell, const uint32_t* __restrict__ src, const uint64_t* __restrict__ offs,
+              const double4* __restrict__ cr, const int* __restrict__ sexp, const float4* __restrict__ Sv,
+              double* __restrict__ Lr, unsigned long long* __restrict__ counter) {
+    using K = L<P>;
+    constexpr int NCH = K::NCH;
+    const int lane = threadIdx.x & 31;
+    // next pair's source centre, fetched with cp.async one pair ahead (ncu: the src -> cr load
+    // chain at every pair start was the top long-scoreboard stall)
+    __shared__ __align__(16) double4 s_cb[128];
+    double4* my_cb = s_cb + threadIdx.x;
+    auto fetch_cb = [&](uint32_t bn) {
+        const unsigned sa_ = (unsigned)__cvta_generic_to_shared(my_cb);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa_), "l"(cr + bn) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa_ + 16), "l"(reinterpret_cast<const char*>(cr + bn) + 16) : "memory");
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    for (;;) {
+        unsigned long long an = 0;
+        if (lane == 0) an = atomicAdd(counter, 1ull);
+        const long long a = (long long)__shfl_sync(0xffffffffu, an, 0);
+        if (a >= ncell) break;
+        const uint64_t p0 = offs[a], p1 = offs[a + 1];
+        if (p0 == p1) continue;
+        const double4 ca = cr[a];
+        const int ea = sexp[a];
+        const double sa = exp2((double)-ea);   // 1/rho_A, exact
+        Regs<P> R;
+#pragma unroll
+        for (int i = 0; i < K::O0; ++i) R.L0p[i] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < K::G0; ++i) R.L0d[i] = 0.f;
+#pragma unroll
+        for (int i = 0; i < K::O1; ++i) R.L1p[i] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < K::G1; ++i) R.L1d[i] = 0.f;
+        uint32_t bnext = 0;
+        if (p0 + lane < p1) {
+            bnext = src[p0 + lane];
+            fetch_cb(bnext);
+        }
+        for (uint64_t p = p0 + lane; p < p1; p += 32) {
+            const uint32_t b = bnext;
+            bnext = p + 32 < p1 ? src[p + 32] : b;
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
+            const double4 cb = *my_cb;
+            const int de = sexp[b] - ea;
+            const float ux = (float)((ca.x - cb.x) * sa);
+            const float uy = (float)((ca.y - cb.y) * sa);
+            const float uz = (float)((ca.z - cb.z) * sa);
+            derivs_mir<P>(ux, uy, uz, R);
+            if (p + 32 < p1) fetch_cb(bnext);   // after the recurrence: bnext has landed
+            // (rho_B/rho_A)^n: only in warps where some lane needs it (uniform trees: never)
+            const bool need = __any_sync(__activemask(), de != 0);
+            auto pw = [&](int n) { return __int_as_float((127 + de * n) << 23); };
+            const float4* sv = Sv + (size_t)b * NCH;
+            sfor<0, NCH>([&](auto cc) {
+                constexpr int C = decltype(cc)::value;
+                const float4 v = sv[C];
+                const float vv[4] = {v.x, v.y, v.z, v.w};
+                sfor<0, 4>([&](auto jj) {
+                    constexpr int F = 4 * C + decltype(jj)::value;
+                    if constexpr (F < K::BD0) {
+                        if constexpr (F % 2 == 0) {
+                            constexpr int kind = F < K::BS1 ? 0 : (F < K::BN ? 1 : 2);
+                            constexpr int j = (F - (kind == 0 ? K::BS0 : kind == 1 ? K::BS1 : K::BN)) / 2;
+                            constexpr int qy = slot_y(j), qz = slot_z(j), m = qy + qz;
+                            float2 sp = make_float2(vv[F % 4], vv[F % 4 + 1]);
+                            if constexpr (kind == 0) {          // S0: L0 += S0 D0 (<= P-1), L1 += S0 D1 (<= P-2)
+                                if constexpr (m > 0) {
+                                    if (need) sp = __fmul2_rn(bc(pw(m)), sp);
+                                }
+                                corr_pair<P - 1, qy, qz>(sp, R.L0p, R.L0d, R.D0p, R.D0d);
+                                if constexpr (m <= P - 2) corr_pair<P - 2, qy, qz>(sp, R.L1p, R.L1d, R.D1p, R.D1d);
+                            } else if constexpr (kind == 1) {   // S1 (degree m+1): L0 += S1 D1 (<= P-2)
+                                if (need) sp = __fmul2_rn(bc(pw(m + 1)), sp);
+                                corr_pair<P - 2, qy, qz>(sp, R.L0p, R.L0d, R.D1p, R.D1d);
+                            } else if constexpr (m >= 2) {      // N (degree m-1): L1 += N D0 (<= P-1)
+                                if (need) sp = __fmul2_rn(bc(pw(m - 1)), sp);
+                                corr_pair<P - 1, qy, qz>(sp, R.L1p, R.L1d, R.D0p, R.D0d);
+                            }
+                        }
+                    } else if constexpr (F < K::NS) {
+                        constexpr int kind = F < K::BD1 ? 0 : (F < K::BDN ? 1 : 2);
+                        constexpr int Q = F - (kind == 0 ? K::BD0 : kind == 1 ? K::BD1 : K::BDN);
+                        float sd = vv[F % 4];
+                        if constexpr (kind == 0) {
+                            if constexpr (Q > 0) {
+                                if (need) sd *= pw(2 * Q);
+                            }
+                            corr_diag<P - 1, Q>(sd, R.L0p, R.L0d, R.D0p, R.D0d);
+                            if constexpr (2 * Q <= P - 2) corr_diag<P - 2, Q>(sd, R.L1p, R.L1d, R.D1p, R.D1d);
+                        } else if constexpr (kind == 1) {
+                            if (need) sd *= pw(2 * Q + 1);
+                            corr_diag<P - 2, Q>(sd, R.L0p, R.L0d, R.D1p, R.D1d);
+                        } else if constexpr (2 * Q >= 2) {
+                            if (need) sd *= pw(2 * Q - 1);
+                            corr_diag<P - 1, Q>(sd, R.L1p, R.L1d, R.D0p, R.D0d);
+                        }
+                    }
+                });
+            });
+        }
+        // warp reduction in fp64; reduced L_hat in (L0 | L1) t2 order for k_l_expand
+        constexpr int N0 = P * (P + 1) / 2;
+        sfor<0, K::NL>([&](auto kk) {
+            constexpr int k = decltype(kk)::value;
+            constexpr int x1 = k >= N0, e = x1 ? k - N0 : k;
+            constexpr int n = deg2(e), z = zof(e), y = n - z;
+            float f;
+            if constexpr (!x1) {
+                if constexpr (y > z) f = R.L0p[off(y, z)].x;
+                else if constexpr (y < z) f = R.L0p[off(z, y)].y;
+                else f = R.L0d[y];
+            } else {
+                if constexpr (y > z) f = R.L1p[off(y, z)].x;
+                else if constexpr (y < z) f = R.L1p[off(z, y)].y;
+                else f = R.L1d[y];
+            }
+            double v = (double)f;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == (k & 31)) Lr[(size_t)a * K::NL + k] = v;
+        });
+    }
+}
+
+// operand layout of the mirror kernel as a fold table: output float i -> (kind, 2D index, degree)
+FoldTable build_fold_table_mir(int P, int NS, int NSP) {
+    const int O0 = noff(P - 1), O1 = noff(P - 2 < 0 ? 0 : P - 2), G0 = ndia(P - 1), G1 = ndia(P - 2 < 0 ? 0 : P - 2);
+    const int BS1 = 2 * O0, BN = BS1 + 2 * O1, BD0 = BN + 2 * O0, BD1 = BD0 + G0, BDN = BD1 + G1;
+    FoldTable t;
+    t.off.assign(NSP + 1, 0);
+    t.dg.assign(NSP, -1);
+    for (int i = 0; i < NSP; ++i) {
+        std::vector<std::pair<int, double>> e;
+        int kind = -1, y = 0, z = 0;
+        if (i < BD0) {
+            const int base = i < BS1 ? 0 : (i < BN ? BS1 : BN);
+            kind = i < BS1 ? 0 : (i < BN ? 1 : 2);
+            const int j = (i - base) / 2;
+            y = slot_y(j);
+            z = slot_z(j);
+            if ((i - base) & 1) std::swap(y, z);   // .y of the pair: the mirror element
+        } else if (i < NS) {
+            kind = i < BD1 ? 0 : (i < BDN ? 1 : 2);
+            const int Q = i - (kind == 0 ? BD0 : kind == 1 ? BD1 : BDN);
+            y = z = Q;
+        }
+        const int m = y + z;
+        if (kind == 0) {
+            fold_terms_host(0, y, z, 1.0, e);
+            t.dg[i] = m;
+        } else if (kind == 1) {
+            fold_terms_host(1, y, z, 1.0, e);
+            t.dg[i] = m + 1;
+        } else if (kind == 2) {
+            if (m >= 2) {
+                if (y >= 2) fold_terms_host(1, y - 2, z, -1.0, e);
+                if (z >= 2) fold_terms_host(1, y, z - 2, -1.0, e);
+            }
+            t.dg[i] = m - 1;
+        }
+        for (auto& x : e) {
+            t.k.push_back(x.first);
+            t.w.push_back(x.second);
+        }
+        t.off[i + 1] = (int)t.k.size();
+    }
+    return t;
+}
+}  // namespace mir
+
+template <int P>
+fmm_status m2l_mir_t(fmm_ctx* ctx, cudaStream_t s) {
+    using K = mir::L<P>;
+    constexpr int NSP = K::NSP, NL = K::NL;
+    const int64_t nc = ctx->ncell;
+    const int64_t nct = ctx->ncell + ctx->nrem;   // sources include grafted LET cells
+    FMM_TRY(buf_ensure(ctx, ctx->Mr, (size_t)nct * NSP * 4 + (size_t)nct * 4 + 256));
+    FMM_TRY(buf_ensure(ctx, ctx->Lr, (size_t)nc * NL * 8));
+    FMM_TRY(buf_ensure(ctx, ctx->cnt_tmp, 64));
+    float* Sv = P_<float>(ctx->Mr);
+    int* sexp = reinterpret_cast<int*>(reinterpret_cast<char*>(ctx->Mr.p) + (size_t)nct * NSP * 4);
+    const int nw = 4;
+    const int g = (int)std::min<int64_t>((nc + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
+    const int gp = (int)std::min<int64_t>((nct + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
+    if (ctx->fold_P != 1000 + P) {
+        const FoldTable t = mir::build_fold_table_mir(P, K::NS, NSP);
+        const size_t nt = t.k.size();
+        FMM_TRY(buf_ensure(ctx, ctx->fold_tab, (NSP + 1) * 4 + NSP * 4 + nt * 4 + nt * 8 + 64));
+        char* b = (char*)ctx->fold_tab.p;
+        FMM_CUDA_TRY(ctx, cudaMemcpy(b, t.w.data(), nt * 8, cudaMemcpyHostToDevice));
+        FMM_CUDA_TRY(ctx, cudaMemcpy(b + nt * 8, t.off.data(), (NSP + 1) * 4, cudaMemcpyHostToDevice));
+        FMM_CUDA_TRY(ctx, cudaMemcpy(b + nt * 8 + (NSP + 1) * 4, t.dg.data(), NSP * 4, cudaMemcpyHostToDevice));
+        FMM_CUDA_TRY(ctx, cudaMemcpy(b + nt * 8 + (2 * NSP + 1) * 4, t.k.data(), nt * 4, cudaMemcpyHostToDevice));
+        ctx->fold_P = 1000 + P;
+        ctx->fold_nt = (int64_t)nt;
+    }
+    {
+        char* b = (char*)ctx->fold_tab.p;
+        const size_t nt = (size_t)ctx->fold_nt;
+        k_m2l_prep_table<float><<<std::max(gp, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
+            nct, ctx->ncoef, NSP, reinterpret_cast<const int*>(b + nt * 8),
+            reinterpret_cast<const int*>(b + nt * 8 + (2 * NSP + 1) * 4), reinterpret_cast<const double*>(b),
+            reinterpret_cast<const int*>(b + nt * 8 + (NSP + 1) * 4), P_<double>(ctx->M), P_<int32_t>(ctx->c_level),
+            P_<double>(ctx->root), sexp, Sv);
+        FMM_LAUNCH(ctx);
+    }
+    unsigned long long* counter = P_<unsigned long long>(ctx->cnt_tmp);
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 8, s));
+    {
+        PhaseScope ps(ctx, PH_M2L_KERNEL, s);
+        mir::k_m2l_mir<P><<<ctx->num_sms * 2, 128, 0, s>>>(nc, P_<uint32_t>(ctx->m2l_src), P_<uint64_t>(ctx->m2l_off),
+                                                          P_<double4>(ctx->c_cr), sexp,
+                                                          reinterpret_cast<const float4*>(Sv), P_<double>(ctx->Lr),
+                                                          counter);
+        FMM_LAUNCH(ctx);
+    }
+    k_l_expand<<<std::max(g, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
+        nc, P, ctx->ncoef, P_<uint64_t>(ctx->m2l_off), sexp, P_<double>(ctx->Lr), P_<double>(ctx->L));
+    FMM_LAUNCH(ctx);
+    FMM_CUDA_TRY(ctx, cudaGetLastError());
+    return FMM_OK;
+}
 }  // namespace
 
 // returns FMM_ERR_ARG (without launching) when no register kernel exists for (P, prec)
 fmm_status m2l_fast(fmm_ctx* ctx, cudaStream_t s) {
     if (ctx->prec == FMM_F32) {
+        if (ctx->m2l_variant == 0) {
+            switch (ctx->P) {
+                case 4: return m2l_mir_t<4>(ctx, s);
+                case 6: return m2l_mir_t<6>(ctx, s);
+                case 8: return m2l_mir_t<8>(ctx, s);
+                case 10: return m2l_mir_t<10>(ctx, s);
+                default: break;
+            }
+        }
         switch (ctx->P) {
             case 4: return m2l_fast_t<4, float>(ctx, s);
             case 6: return m2l_fast_t<6, float>(ctx, s);
