@@ -471,9 +471,9 @@ struct Regs {
     float2 D1p[K::O1 > 0 ? K::O1 : 1];
     float D1d[K::G1];
     float2 L0p[K::O0];
-    float L0d[K::G0];
+    float2 L0d[K::G0];   // diagonal outputs as two partial sums (one FFMA2 per element pair)
     float2 L1p[K::O1 > 0 ? K::O1 : 1];
-    float L1d[K::G1];
+    float2 L1d[K::G1];
 };
 
 __device__ __forceinline__ float2 sw(float2 v) { return make_float2(v.y, v.x); }
@@ -572,28 +572,35 @@ __device__ __forceinline__ void derivs_mir(float ux, float uy, float uz, Regs<P>
 
 // element pair {S[q], S[Mq]} (q = (QY, QZ), QY > QZ) into L += S (x) D for |p| + |q| <= DMAX
 template <int DMAX, int QY, int QZ, int NO, int NG, int DO, int DG>
-__device__ __forceinline__ void corr_pair(float2 sp, float2 (&Lp)[NO], float (&Ld)[NG], const float2 (&Dp)[DO],
+__device__ __forceinline__ void corr_pair(float2 sp, float2 (&Lp)[NO], float2 (&Ld)[NG], const float2 (&Dp)[DO],
                                           const float (&Dd)[DG]) {
     constexpr int m = QY + QZ;
+    // element q (and the diagonal outputs), then element Mq: the two updates of one accumulator
+    // are a whole sweep apart (no back-to-back dependent FFMA2)
     sfor<0, DMAX - m + 1>([&](auto pp) {
         constexpr int pn = decltype(pp)::value;
         sfor<0, pn / 2 + 1>([&](auto zz) {
             constexpr int pz = decltype(zz)::value, py = pn - pz;
             if constexpr (py > pz) {
                 Lp[off(py, pz)] = __ffma2_rn(sp, pr<py + QY, pz + QZ>(Dp, Dd), Lp[off(py, pz)]);
-                Lp[off(py, pz)] = __ffma2_rn(sw(sp), pr<py + QZ, pz + QY>(Dp, Dd), Lp[off(py, pz)]);
-            } else {   // diagonal p: k = p + q is canonical off-diagonal; elements q and Mq
-                const float2 dk = Dp[off(py + QY, pz + QZ)];
-                Ld[py] = fmaf(sp.x, dk.x, Ld[py]);
-                Ld[py] = fmaf(sp.y, dk.y, Ld[py]);
+            } else {   // diagonal p: k = p + q is canonical off-diagonal; .x element q, .y element Mq
+                Ld[py] = __ffma2_rn(sp, Dp[off(py + QY, pz + QZ)], Ld[py]);
             }
+        });
+    });
+    sfor<0, DMAX - m + 1>([&](auto pp) {
+        constexpr int pn = decltype(pp)::value;
+        sfor<0, pn / 2 + 1>([&](auto zz) {
+            constexpr int pz = decltype(zz)::value, py = pn - pz;
+            if constexpr (py > pz)
+                Lp[off(py, pz)] = __ffma2_rn(sw(sp), pr<py + QZ, pz + QY>(Dp, Dd), Lp[off(py, pz)]);
         });
     });
 }
 
 // diagonal element S[q] (q = (Q, Q)) into L += S (x) D for |p| + |q| <= DMAX
 template <int DMAX, int Q, int NO, int NG, int DO, int DG>
-__device__ __forceinline__ void corr_diag(float s, float2 (&Lp)[NO], float (&Ld)[NG], const float2 (&Dp)[DO],
+__device__ __forceinline__ void corr_diag(float s, float2 (&Lp)[NO], float2 (&Ld)[NG], const float2 (&Dp)[DO],
                                           const float (&Dd)[DG]) {
     constexpr int m = 2 * Q;
     sfor<0, DMAX - m + 1>([&](auto pp) {
@@ -601,7 +608,7 @@ __device__ __forceinline__ void corr_diag(float s, float2 (&Lp)[NO], float (&Ld)
         sfor<0, pn / 2 + 1>([&](auto zz) {
             constexpr int pz = decltype(zz)::value, py = pn - pz;
             if constexpr (py > pz) Lp[off(py, pz)] = __ffma2_rn(bc(s), pr<py + Q, pz + Q>(Dp, Dd), Lp[off(py, pz)]);
-            else Ld[py] = fmaf(s, Dd[py + Q], Ld[py]);
+            else Ld[py].x = fmaf(s, Dd[py + Q], Ld[py].x);
         });
     });
 }
@@ -629,11 +636,15 @@ __global__ void __launch_bounds__(128, 2)
     // next pair's source centre, fetched with cp.async one pair ahead (ncu: the src -> cr load
     // chain at every pair start was the top long-scoreboard stall)
     __shared__ __align__(16) double4 s_cb[128];
+    __shared__ int s_eb[128];
     double4* my_cb = s_cb + threadIdx.x;
+    int* my_eb = s_eb + threadIdx.x;
     auto fetch_cb = [&](uint32_t bn) {
         const unsigned sa_ = (unsigned)__cvta_generic_to_shared(my_cb);
+        const unsigned se_ = (unsigned)__cvta_generic_to_shared(my_eb);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa_), "l"(cr + bn) : "memory");
         asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa_ + 16), "l"(reinterpret_cast<const char*>(cr + bn) + 16) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(se_), "l"(sexp + bn) : "memory");
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
     for (;;) {
@@ -650,11 +661,11 @@ __global__ void __launch_bounds__(128, 2)
 #pragma unroll
         for (int i = 0; i < K::O0; ++i) R.L0p[i] = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int i = 0; i < K::G0; ++i) R.L0d[i] = 0.f;
+        for (int i = 0; i < K::G0; ++i) R.L0d[i] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int i = 0; i < K::O1; ++i) R.L1p[i] = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int i = 0; i < K::G1; ++i) R.L1d[i] = 0.f;
+        for (int i = 0; i < K::G1; ++i) R.L1d[i] = make_float2(0.f, 0.f);
         uint32_t bnext = 0;
         if (p0 + lane < p1) {
             bnext = src[p0 + lane];
@@ -665,7 +676,7 @@ __global__ void __launch_bounds__(128, 2)
             bnext = p + 32 < p1 ? src[p + 32] : b;
             asm volatile("cp.async.wait_all;\n" ::: "memory");
             const double4 cb = *my_cb;
-            const int de = sexp[b] - ea;
+            const int de = *my_eb - ea;
             const float ux = (float)((ca.x - cb.x) * sa);
             const float uy = (float)((ca.y - cb.y) * sa);
             const float uz = (float)((ca.z - cb.z) * sa);
@@ -732,11 +743,11 @@ __global__ void __launch_bounds__(128, 2)
             if constexpr (!x1) {
                 if constexpr (y > z) f = R.L0p[off(y, z)].x;
                 else if constexpr (y < z) f = R.L0p[off(z, y)].y;
-                else f = R.L0d[y];
+                else f = R.L0d[y].x + R.L0d[y].y;
             } else {
                 if constexpr (y > z) f = R.L1p[off(y, z)].x;
                 else if constexpr (y < z) f = R.L1p[off(z, y)].y;
-                else f = R.L1d[y];
+                else f = R.L1d[y].x + R.L1d[y].y;
             }
             double v = (double)f;
 #pragma unroll
