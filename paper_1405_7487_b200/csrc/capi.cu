@@ -148,7 +148,7 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
                       &ctx->run_len64, &ctx->dcount2, &ctx->tcnt, &ctx->cnt64, &ctx->big_off, &ctx->M, &ctx->L, &ctx->Mr, &ctx->Lr, &ctx->near_phi, &ctx->near_grad,
                       &ctx->h_stage};
     for (DevBuf* b : bufs) buf_free(*b);
-    DevBuf* lbufs[] = {&ctx->let_tmp, &ctx->let_cov, &ctx->c_orig, &ctx->part_tmp, &ctx->seg_lists, &ctx->orb_tmp, &ctx->root_given, &ctx->fold_tab, &ctx->leaf_cls};
+    DevBuf* lbufs[] = {&ctx->let_tmp, &ctx->let_cov, &ctx->c_orig, &ctx->part_tmp, &ctx->seg_lists, &ctx->orb_tmp, &ctx->root_given, &ctx->fold_tab, &ctx->leaf_cls, &ctx->dtt_lvl};
     for (DevBuf* b : lbufs) buf_free(*b);
     for (auto& lp : ctx->let_peers) {
         DevBuf* pb[] = {&lp.opened, &lp.eflag, &lp.eidx, &lp.bflag, &lp.boff};

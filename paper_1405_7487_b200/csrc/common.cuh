@@ -129,6 +129,8 @@ struct fmm_ctx {
     // lst_m2l / lst_p2p are the unsorted packed (target<<32|source) append buffers of the DTT.
     int64_t n_m2l = 0, n_p2p = 0, p2p_inter = 0;
     DevBuf fr_a, fr_b, lst_m2l, lst_p2p, lst_tmp, m2l_src, p2p_src, m2l_off, p2p_off, cnt_tmp, cnt_tmp2, dcount;
+    DevBuf dtt_lvl;                                          // per-level frontier sizes (dtt.cu fast path)
+    int64_t dtt_est_front = 0, dtt_est_m2l = 0, dtt_est_p2p = 0;   // buffer sizes learnt from the last build
     // P2P source runs: runs[n_runs] = {start body, flat offset}, then rtot[ncell]; run_off[ncell+1]
     int64_t n_runs = 0;
     DevBuf runs, run_off, run_tmp, run_pre, run_len64, dcount2, tcnt, cnt64, big_off, seg_lists;

@@ -87,15 +87,27 @@ __device__ __forceinline__ void count_target(uint32_t* __restrict__ tcnt, bool p
 constexpr int DT_THREADS = 256;
 constexpr int DT_ITEMS = 4;
 
-__global__ void __launch_bounds__(DT_THREADS) k_dtt_step(const uint64_t* __restrict__ fr, int64_t nf, CellView v,
+// cnt[0], cnt[1]: M2L / P2P list cursors; next_count: next-frontier cursor; cnt[3]: flags
+// (1: absent LET children, 2: next frontier over cap_next, 4: a list over its capacity).  With
+// nf_dev the frontier size is read on the device (levels launched back to back, no host sync).
+__global__ void __launch_bounds__(DT_THREADS) k_dtt_step(const uint64_t* __restrict__ fr, int64_t nf_host,
+                                                         const unsigned long long* __restrict__ nf_dev, CellView v,
                                                          double theta, unsigned long long* __restrict__ cnt,
+                                                         unsigned long long* __restrict__ next_count,
                                                          uint64_t* __restrict__ m2l, uint64_t* __restrict__ p2p,
                                                          uint64_t* __restrict__ next, uint32_t* __restrict__ tcnt_m2l,
                                                          uint32_t* __restrict__ tcnt_p2p, uint64_t cap_next,
-                                                         int children_only) {
+                                                         uint64_t cap_m2l, uint64_t cap_p2p, int children_only) {
     __shared__ unsigned long long s_warp[DT_THREADS / 32];
     __shared__ unsigned long long s_base[3];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    int64_t nf = nf_host;
+    if (nf_dev) {
+        // back-to-back levels: after an overflow in an earlier level the frontier in memory is
+        // incomplete -- every later level is a no-op and the host re-runs synchronously
+        if (*reinterpret_cast<volatile unsigned long long*>(&cnt[3]) & 6ull) return;
+        nf = (int64_t)min(*nf_dev, (unsigned long long)cap_next);
+    }
     for (int64_t tile = (int64_t)blockIdx.x * DT_THREADS * DT_ITEMS; tile < nf;
          tile += (int64_t)gridDim.x * DT_THREADS * DT_ITEMS) {
         uint32_t a[DT_ITEMS], b[DT_ITEMS], nch[DT_ITEMS];
@@ -138,7 +150,7 @@ __global__ void __launch_bounds__(DT_THREADS) k_dtt_step(const uint64_t* __restr
             if (lane == DT_THREADS / 32 - 1) {
                 s_base[0] = children_only ? 0ull : atomicAdd(&cnt[0], w & 0xFFFFull);
                 s_base[1] = children_only ? 0ull : atomicAdd(&cnt[1], (w >> 16) & 0xFFFFull);
-                s_base[2] = atomicAdd(&cnt[2], w >> 32);
+                s_base[2] = atomicAdd(next_count, w >> 32);
             }
         }
         __syncthreads();
@@ -155,9 +167,17 @@ __global__ void __launch_bounds__(DT_THREADS) k_dtt_step(const uint64_t* __restr
                 atomicOr(&cnt[3], 2ull);
                 pc += nch[k];
             } else if (o[k] == 0) {
-                if (!children_only) m2l[pm++] = pr;
+                if (!children_only) {
+                    if (pm < cap_m2l) m2l[pm] = pr;
+                    else atomicOr(&cnt[3], 4ull);
+                    ++pm;
+                }
             } else if (o[k] == 1) {
-                if (!children_only) p2p[pp++] = pr;
+                if (!children_only) {
+                    if (pp < cap_p2p) p2p[pp] = pr;
+                    else atomicOr(&cnt[3], 4ull);
+                    ++pp;
+                }
             } else if (o[k] == 2) {
                 const uint32_t k0 = v.cb[a[k]];
                 for (uint32_t c = 0; c < nch[k]; ++c) next[pc + c] = ((uint64_t)(k0 + c) << 32) | b[k];
@@ -698,25 +718,82 @@ fmm_status build_runs(fmm_ctx* ctx, cudaStream_t s) {
 
 }  // namespace
 
+// Level-by-level traversal.  Fast path (a fresh traversal whose buffer sizes are known from an
+// earlier build of similar size): all 2*depth+1 levels are launched back to back, each reading its
+// frontier size on the device, with one host round trip at the end; on any overflow (or a deeper
+// traversal) it falls back to the synchronous loop, which grows the buffers to the exact sizes.
 fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append, cudaStream_t s) {
     const CellView v{P_<double4>(ctx->c_cr), P_<uint32_t>(ctx->c_cb), P_<uint32_t>(ctx->c_cc)};
     const int64_t nc = ctx->ncell;
-    int64_t n_m2l = append ? ctx->n_m2l : 0, n_p2p = append ? ctx->n_p2p : 0;
     FMM_TRY(buf_ensure(ctx, ctx->tcnt, (size_t)nc * 2 * 4));
     uint32_t* tcnt_m2l = P_<uint32_t>(ctx->tcnt);
     uint32_t* tcnt_p2p = tcnt_m2l + nc;
     FMM_TRY(buf_ensure(ctx, ctx->dcount2, 128));
     PhaseScope ps(ctx, PH_DTT, s);
-    FMM_TRY(buf_ensure(ctx, ctx->fr_a, (size_t)std::max(nseeds, 128) * 8));
     FMM_TRY(buf_ensure(ctx, ctx->dcount, 64));
     unsigned long long* d_cnt = P_<unsigned long long>(ctx->dcount);
-    if (!append) {
-        FMM_CUDA_TRY(ctx, cudaMemsetAsync(tcnt_m2l, 0, (size_t)nc * 2 * 4, s));
-        FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt, 0, 4 * 8, s));
+    const int64_t m2l0 = append ? ctx->n_m2l : 0, p2p0 = append ? ctx->n_p2p : 0;
+    auto reset = [&]() -> fmm_status {
+        if (!append) {
+            FMM_CUDA_TRY(ctx, cudaMemsetAsync(tcnt_m2l, 0, (size_t)nc * 2 * 4, s));
+            FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt, 0, 4 * 8, s));
+        }
+        return FMM_OK;
+    };
+    const int g_max = ctx->num_sms * 8;
+    int64_t peak = nseeds;
+
+    if (!append && ctx->dtt_est_front > 0) {
+        const int L = 2 * (int)ctx->depth + 1;
+        const uint64_t capf = (uint64_t)ctx->dtt_est_front;
+        const uint64_t capm = (uint64_t)ctx->dtt_est_m2l, capp = (uint64_t)ctx->dtt_est_p2p;
+        FMM_TRY(buf_ensure(ctx, ctx->fr_a, (size_t)std::max<uint64_t>(capf, (uint64_t)nseeds) * 8));
+        FMM_TRY(buf_ensure(ctx, ctx->fr_b, (size_t)capf * 8));
+        FMM_TRY(buf_ensure(ctx, ctx->lst_m2l, (size_t)capm * 8));
+        FMM_TRY(buf_ensure(ctx, ctx->lst_p2p, (size_t)capp * 8));
+        FMM_TRY(buf_ensure(ctx, ctx->dtt_lvl, (size_t)(L + 2) * 8));
+        unsigned long long* lvl = P_<unsigned long long>(ctx->dtt_lvl);
+        FMM_TRY(reset());
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(lvl, 0, (size_t)(L + 2) * 8, s));
+        const unsigned long long ns = (unsigned long long)nseeds;
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(lvl, &ns, 8, cudaMemcpyHostToDevice, s));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->fr_a.p, seeds, (size_t)nseeds * 8, cudaMemcpyHostToDevice, s));
+        for (int l = 0; l < L; ++l) {
+            DevBuf& in = (l & 1) ? ctx->fr_b : ctx->fr_a;
+            DevBuf& out = (l & 1) ? ctx->fr_a : ctx->fr_b;
+            k_dtt_step<<<g_max, DT_THREADS, 0, s>>>(P_<uint64_t>(in), 0, lvl + l, v, ctx->theta, d_cnt, lvl + l + 1,
+                                                    P_<uint64_t>(ctx->lst_m2l), P_<uint64_t>(ctx->lst_p2p),
+                                                    P_<uint64_t>(out), tcnt_m2l, tcnt_p2p, capf, capm, capp, 0);
+            FMM_LAUNCH(ctx);
+        }
+        unsigned long long h[4];
+        std::vector<unsigned long long> hl(L + 1);
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(h, d_cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(hl.data(), lvl, (size_t)(L + 1) * 8, cudaMemcpyDeviceToHost, s));
+        FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+        if (h[3] & 1ull) {
+            ctx->err = "dual tree traversal needed children of a remote LET cell that were not exported";
+            return FMM_ERR_STATE;
+        }
+        for (int l = 0; l <= L; ++l) peak = std::max<int64_t>(peak, (int64_t)hl[l]);
+        if (!(h[3] & 6ull) && hl[L] == 0) {
+            ctx->n_m2l = (int64_t)h[0];
+            ctx->n_p2p = (int64_t)h[1];
+            ctx->dtt_est_front = peak + peak / 8 + 1024;
+            ctx->dtt_est_m2l = ctx->n_m2l + ctx->n_m2l / 8 + 1024;
+            ctx->dtt_est_p2p = ctx->n_p2p + ctx->n_p2p / 8 + 1024;
+            return FMM_OK;
+        }
+        // overflow or deeper than 2*depth+1: redo synchronously (exact sizes)
     }
+
+    int64_t n_m2l = m2l0, n_p2p = p2p0;
+    FMM_TRY(buf_ensure(ctx, ctx->fr_a, (size_t)std::max(nseeds, 128) * 8));
+    FMM_TRY(reset());
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->fr_a.p, seeds, (size_t)nseeds * 8, cudaMemcpyHostToDevice, s));
     int64_t nf = nseeds;
     while (nf > 0) {
+        peak = std::max(peak, nf);
         // worst case per step: one list entry or 8 children per pair
         const size_t need_m = (size_t)(n_m2l + nf) * 8, need_p = (size_t)(n_p2p + nf) * 8;
         if (need_m > ctx->lst_m2l.bytes) FMM_TRY(buf_ensure(ctx, ctx->lst_m2l, need_m + need_m / 2, true, s));
@@ -726,11 +803,12 @@ fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append
         const uint64_t cap = nf <= (1 << 20) ? (uint64_t)nf * 8 : (uint64_t)nf * 3;
         FMM_TRY(buf_ensure(ctx, ctx->fr_b, (size_t)cap * 8));
         FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt + 2, 0, 8, s));   // next-frontier cursor restarts
-        const int g = (int)std::min<int64_t>((nf + DT_THREADS * DT_ITEMS - 1) / (DT_THREADS * DT_ITEMS),
-                                             (int64_t)ctx->num_sms * 8);
-        k_dtt_step<<<g, DT_THREADS, 0, s>>>(P_<uint64_t>(ctx->fr_a), nf, v, ctx->theta, d_cnt, P_<uint64_t>(ctx->lst_m2l),
-                                            P_<uint64_t>(ctx->lst_p2p), P_<uint64_t>(ctx->fr_b), tcnt_m2l, tcnt_p2p,
-                                            ctx->fr_b.bytes / 8, 0);
+        const int g = (int)std::min<int64_t>((nf + DT_THREADS * DT_ITEMS - 1) / (DT_THREADS * DT_ITEMS), g_max);
+        const uint64_t capm = ctx->lst_m2l.bytes / 8, capp = ctx->lst_p2p.bytes / 8;
+        k_dtt_step<<<g, DT_THREADS, 0, s>>>(P_<uint64_t>(ctx->fr_a), nf, nullptr, v, ctx->theta, d_cnt, d_cnt + 2,
+                                            P_<uint64_t>(ctx->lst_m2l), P_<uint64_t>(ctx->lst_p2p),
+                                            P_<uint64_t>(ctx->fr_b), tcnt_m2l, tcnt_p2p, ctx->fr_b.bytes / 8, capm,
+                                            capp, 0);
         FMM_LAUNCH(ctx);
         unsigned long long h[4];
         FMM_CUDA_TRY(ctx, cudaMemcpyAsync(h, d_cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -738,9 +816,10 @@ fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append
         if (h[3] & 2ull) {
             FMM_TRY(buf_ensure(ctx, ctx->fr_b, (size_t)h[2] * 8));
             FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt + 2, 0, 16, s));
-            k_dtt_step<<<g, DT_THREADS, 0, s>>>(P_<uint64_t>(ctx->fr_a), nf, v, ctx->theta, d_cnt,
+            k_dtt_step<<<g, DT_THREADS, 0, s>>>(P_<uint64_t>(ctx->fr_a), nf, nullptr, v, ctx->theta, d_cnt, d_cnt + 2,
                                                 P_<uint64_t>(ctx->lst_m2l), P_<uint64_t>(ctx->lst_p2p),
-                                                P_<uint64_t>(ctx->fr_b), tcnt_m2l, tcnt_p2p, ctx->fr_b.bytes / 8, 1);
+                                                P_<uint64_t>(ctx->fr_b), tcnt_m2l, tcnt_p2p, ctx->fr_b.bytes / 8, capm,
+                                                capp, 1);
             FMM_LAUNCH(ctx);
             FMM_CUDA_TRY(ctx, cudaMemcpyAsync(h, d_cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
             FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
@@ -756,6 +835,11 @@ fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append
     }
     ctx->n_m2l = n_m2l;
     ctx->n_p2p = n_p2p;
+    if (!append) {   // sizes for the back-to-back path of the next build
+        ctx->dtt_est_front = peak + peak / 8 + 1024;
+        ctx->dtt_est_m2l = n_m2l + n_m2l / 8 + 1024;
+        ctx->dtt_est_p2p = n_p2p + n_p2p / 8 + 1024;
+    }
     return FMM_OK;
 }
 

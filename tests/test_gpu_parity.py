@@ -168,13 +168,19 @@ def test_solve_host_matches_device(torch_cuda):
 
 
 def test_repeat_builds_reuse_context(torch_cuda):
-    # a context grows its workspace across sizes and stays exact
-    for n in (500, 5000, 800):
-        pos, q = synth.generate("cube", n, n)
-        f, phi, grad = run_gpu(torch_cuda, pos, q, 4, 0.5, 16, "f64")
-        o = oracle.FMM(pos, q, 4, 0.5, 16)
+    # ONE context across sizes and distributions: workspace growth, and the back-to-back
+    # traversal sized from the previous build (smaller, larger -> overflow fallback, deeper)
+    from paper_1405_7487_b200 import FMM
+    f = FMM(20000, 4, 0.5, 16, "f64")
+    for kind, n in (("cube", 500), ("cube", 5000), ("cube", 5000), ("cube", 800), ("plummer", 20000),
+                    ("plummer", 20000), ("cube", 3000)):
+        pos, q = synth.generate(kind, n, n)
+        tp = torch_cuda.from_numpy(pos).cuda()
+        phi, grad = f.solve(tp, torch_cuda.from_numpy(q).cuda())
+        o = oracle.FMM(pos, q, 4, 0.5, 16).traverse()
+        check_structure(f, o)
         ophi, ograd = o.evaluate()
-        assert oracle.rel_l2(phi, ophi) <= 1e-12
+        assert oracle.rel_l2(phi.cpu().numpy(), ophi) <= 1e-12
 
 
 def test_c2_full_size(torch_cuda):
