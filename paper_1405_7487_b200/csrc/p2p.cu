@@ -415,6 +415,164 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_cta(const float4* __restrict
     }
 }
 
+// ---------------------------------------------------------------- TMA bulk-copy variant
+// Same work layout as k_p2p_cta<128, TILE, NP>, but the source chunks are staged with 1D bulk
+// copies (cp.async.bulk, the TMA engine) of whole Morton runs issued by one thread, with
+// mbarrier completion: consumers wait on the chunk's "full" barrier (transaction bytes), each
+// warp arrives on the buffer's "empty" barrier when done, and the issuing thread waits on that
+// before refilling -- no CTA-wide barrier per chunk (ncu: ~10% barrier stalls).
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(b);
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                     "r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+                 "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+
+template <int PC_TILE, int NP>
+__global__ void __launch_bounds__(PC_THREADS) k_p2p_tma(const float4* __restrict__ body,
+                                                         const uint32_t* __restrict__ leaf_ids, int64_t nleaf,
+                                                         const uint2* __restrict__ runs,
+                                                         const uint32_t* __restrict__ roff,
+                                                         const uint32_t* __restrict__ rtot,
+                                                         const uint32_t* __restrict__ bb, const uint32_t* __restrict__ bc,
+                                                         float* __restrict__ near_phi, float* __restrict__ near_grad,
+                                                         unsigned long long* __restrict__ counter) {
+    constexpr int NW = PC_THREADS / 32;
+    __shared__ __align__(128) float4 s_tile[2][PC_TILE];
+    __shared__ float4 s_red[PC_THREADS * (2 * NP)];
+    __shared__ __align__(8) uint64_t full[2], empty[2];
+    __shared__ unsigned long long s_leaf;
+    __shared__ uint32_t s_self;
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid == 0) {
+        mbar_init(&full[0], 1); mbar_init(&full[1], 1);
+        mbar_init(&empty[0], NW); mbar_init(&empty[1], NW);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t kk = 0;   // chunks issued by this CTA so far (buffer kk & 1, use parity (kk >> 1) & 1)
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) s_leaf = atomicAdd(counter, 1ull);
+        __syncthreads();
+        const unsigned long long li = s_leaf;
+        if (li >= (unsigned long long)nleaf) break;
+        const uint32_t a = leaf_ids[li];
+        const uint32_t tb = bb[a], nt_all = bc[a];
+        const uint32_t r0 = roff[a], r1 = roff[a + 1], ns = rtot[a];
+        for (uint32_t r = r0 + tid; r < r1; r += PC_THREADS) {
+            const uint2 ru = runs[r];
+            const uint32_t end = (r + 1 < r1) ? runs[r + 1].y : ns;
+            if (ru.x <= tb && tb < ru.x + (end - ru.y)) s_self = ru.y + (tb - ru.x);
+        }
+        __syncthreads();
+        const uint32_t selfF = s_self;
+        for (uint32_t t0 = 0; t0 < nt_all; t0 += PC_THREADS * (2 * NP)) {
+            const uint32_t nt = min(nt_all - t0, (uint32_t)(PC_THREADS * (2 * NP)));
+            const int lpg = (int)((nt + (2 * NP) - 1) / (2 * NP));
+            const int G = min(PC_THREADS / lpg, 64);
+            const int g = tid / lpg, j = tid - g * lpg;
+            const bool active = g < G;
+            const uint32_t CH = (uint32_t)(G * (PC_TILE / G));
+            float2 nx[NP], ny[NP], nz[NP], f[NP], gx[NP], gy[NP], gz[NP];
+#pragma unroll
+            for (int h = 0; h < NP; ++h) {
+                float px[2], py[2], pz[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const uint32_t t = (uint32_t)(j + (2 * h + e) * lpg);
+                    const float4 p = body[tb + t0 + (t < nt ? t : 0)];
+                    px[e] = t < nt ? -p.x : -1e30f; py[e] = -p.y; pz[e] = -p.z;
+                }
+                nx[h] = make_float2(px[0], px[1]); ny[h] = make_float2(py[0], py[1]);
+                nz[h] = make_float2(pz[0], pz[1]);
+                f[h] = gx[h] = gy[h] = gz[h] = make_float2(0.f, 0.f);
+            }
+            const uint32_t nch = (ns + CH - 1) / CH;
+            uint32_t cur = r0;   // thread 0's run cursor
+            // thread 0 issues chunk c (global number kk0 + c) as bulk copies of its run pieces
+            const uint32_t kk0 = kk;
+            auto issue = [&](uint32_t c) {
+                const uint32_t q = kk0 + c, buf = q & 1;
+                if (q >= 2) mbar_wait(&empty[buf], ((q >> 1) - 1) & 1);   // chunk q-2 consumed
+                const uint32_t f0 = c * CH, len = min(CH, ns - f0);
+                mbar_expect_tx(&full[buf], len * 16u);
+                uint32_t fl = f0, dst = 0;
+                while (dst < len) {
+                    while (cur + 1 < r1 && runs[cur + 1].y <= fl) ++cur;
+                    const uint2 ru = runs[cur];
+                    const uint32_t end = (cur + 1 < r1) ? runs[cur + 1].y : ns;
+                    const uint32_t m = min(end - fl, len - dst);
+                    bulk_g2s(&s_tile[buf][dst], body + ru.x + (fl - ru.y), m * 16u, &full[buf]);
+                    fl += m;
+                    dst += m;
+                }
+            };
+            if (tid == 0 && nch > 0) issue(0);
+            for (uint32_t c = 0; c < nch; ++c) {
+                const uint32_t q = kk0 + c, buf = q & 1;
+                if (tid == 0 && c + 1 < nch) issue(c + 1);
+                mbar_wait(&full[buf], (q >> 1) & 1);
+                const uint32_t f0 = c * CH;
+                const uint32_t len = min(CH, ns - f0);
+                if (active) {
+                    const float4* tl = s_tile[buf];
+                    const bool self = f0 < selfF + nt_all && selfF < f0 + len;
+                    if (self) {
+                        for (uint32_t i = g; i < len; i += G) p2p_body2<true, NP>(tl[i], nx, ny, nz, f, gx, gy, gz);
+                    } else {
+                        for (uint32_t i = g; i < len; i += G) p2p_body2<false, NP>(tl[i], nx, ny, nz, f, gx, gy, gz);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[buf]);
+            }
+            kk += nch;
+#pragma unroll
+            for (int h = 0; h < NP; ++h) {
+                s_red[tid * (2 * NP) + 2 * h] = make_float4(f[h].x, gx[h].x, gy[h].x, gz[h].x);
+                s_red[tid * (2 * NP) + 2 * h + 1] = make_float4(f[h].y, gx[h].y, gy[h].y, gz[h].y);
+            }
+            __syncthreads();
+            if (g == 0) {
+#pragma unroll
+                for (int k = 0; k < (2 * NP); ++k) {
+                    const uint32_t t = (uint32_t)(j + k * lpg);
+                    if (t < nt) {
+                        float4 acc = s_red[tid * (2 * NP) + k];
+                        for (int gg = 1; gg < G; ++gg) {
+                            const float4 v = s_red[(gg * lpg + j) * (2 * NP) + k];
+                            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+                        }
+                        const int64_t o = (int64_t)tb + t0 + t;
+                        near_phi[o] = acc.x;
+                        near_grad[3 * o] = acc.y;
+                        near_grad[3 * o + 1] = acc.z;
+                        near_grad[3 * o + 2] = acc.w;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
 template <typename Body, typename Real>
 fmm_status p2p_t(fmm_ctx* ctx, cudaStream_t s) {
     PhaseScope ps(ctx, PH_P2P, s);
@@ -443,7 +601,9 @@ fmm_status p2p_t(fmm_ctx* ctx, cudaStream_t s) {
             return FMM_OK;
         };
         FMM_TRY(launch(k_p2p_cta<32, 64, 1>, lists, ctx->n_leaf_cls[0], counter));
-        FMM_TRY(launch(k_p2p_cta<128, 256, 2>, lists + ctx->nleaf, ctx->n_leaf_cls[1], counter + 1));
+        // mid leaves: TMA bulk-copy staging (measured 3% faster at c2/c3); big leaves: cp.async
+        // (bulk copies measured 3% slower for the sphere's ~234-body leaves)
+        FMM_TRY(launch(k_p2p_tma<256, 2>, lists + ctx->nleaf, ctx->n_leaf_cls[1], counter + 1));
         FMM_TRY(launch(k_p2p_cta<128, 256, 4>, lists + 2 * ctx->nleaf, ctx->n_leaf_cls[2], counter + 2));
         FMM_CUDA_TRY(ctx, cudaGetLastError());
         return FMM_OK;
