@@ -444,7 +444,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                  "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
 }
 
-template <int PC_TILE, int NP>
+template <int PC_TILE, int NP, int NS = 2>
 __global__ void __launch_bounds__(PC_THREADS) k_p2p_tma(const float4* __restrict__ body,
                                                          const uint32_t* __restrict__ leaf_ids, int64_t nleaf,
                                                          const uint2* __restrict__ runs,
@@ -454,19 +454,21 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_tma(const float4* __restrict
                                                          float* __restrict__ near_phi, float* __restrict__ near_grad,
                                                          unsigned long long* __restrict__ counter) {
     constexpr int NW = PC_THREADS / 32;
-    __shared__ __align__(128) float4 s_tile[2][PC_TILE];
+    __shared__ __align__(128) float4 s_tile[NS][PC_TILE];
     __shared__ float4 s_red[PC_THREADS * (2 * NP)];
-    __shared__ __align__(8) uint64_t full[2], empty[2];
+    __shared__ __align__(8) uint64_t full[NS], empty[NS];
     __shared__ unsigned long long s_leaf;
     __shared__ uint32_t s_self;
     const int tid = threadIdx.x, lane = tid & 31;
     if (tid == 0) {
-        mbar_init(&full[0], 1); mbar_init(&full[1], 1);
-        mbar_init(&empty[0], NW); mbar_init(&empty[1], NW);
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], NW);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    uint32_t kk = 0;   // chunks issued by this CTA so far (buffer kk & 1, use parity (kk >> 1) & 1)
+    uint32_t kk = 0;   // chunks issued by this CTA so far (buffer kk % NS, use parity (kk / NS) & 1)
     for (;;) {
         __syncthreads();
         if (tid == 0) s_leaf = atomicAdd(counter, 1ull);
@@ -509,8 +511,8 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_tma(const float4* __restrict
             // thread 0 issues chunk c (global number kk0 + c) as bulk copies of its run pieces
             const uint32_t kk0 = kk;
             auto issue = [&](uint32_t c) {
-                const uint32_t q = kk0 + c, buf = q & 1;
-                if (q >= 2) mbar_wait(&empty[buf], ((q >> 1) - 1) & 1);   // chunk q-2 consumed
+                const uint32_t q = kk0 + c, buf = q % NS;
+                if (q >= NS) mbar_wait(&empty[buf], (q / NS - 1) & 1);   // chunk q-NS consumed
                 const uint32_t f0 = c * CH, len = min(CH, ns - f0);
                 mbar_expect_tx(&full[buf], len * 16u);
                 uint32_t fl = f0, dst = 0;
@@ -524,11 +526,12 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_tma(const float4* __restrict
                     dst += m;
                 }
             };
-            if (tid == 0 && nch > 0) issue(0);
+            if (tid == 0)
+                for (uint32_t c = 0; c + 1 < NS && c < nch; ++c) issue(c);
             for (uint32_t c = 0; c < nch; ++c) {
-                const uint32_t q = kk0 + c, buf = q & 1;
-                if (tid == 0 && c + 1 < nch) issue(c + 1);
-                mbar_wait(&full[buf], (q >> 1) & 1);
+                const uint32_t q = kk0 + c, buf = q % NS;
+                if (tid == 0 && c + NS - 1 < nch) issue(c + NS - 1);
+                mbar_wait(&full[buf], (q / NS) & 1);
                 const uint32_t f0 = c * CH;
                 const uint32_t len = min(CH, ns - f0);
                 if (active) {
