@@ -177,7 +177,7 @@ def roofline_block(args, cfg, counts, ph):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(f"{args.config}:{dom}")
-    return {"kernel": f"{dom} ({'k_m2l_mir' if dom == 'm2l' else 'k_p2p_cta'})", "bound": "alu",
+    return {"kernel": f"{dom} ({'k_m2l_mir' if dom == 'm2l' else 'k_p2p_tma + k_p2p_cta (leaf classes)'})", "bound": "alu",
             "achieved": round(m2l_tf if dom == "m2l" else p2p_tf, 3), "peak": round(fp32_peak_tflops, 2),
             "unit": "TFLOP/s", "frac": round((m2l_tf if dom == "m2l" else p2p_tf) / fp32_peak_tflops, 4),
             "traffic": traffic,
