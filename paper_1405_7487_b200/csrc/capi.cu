@@ -225,15 +225,19 @@ fmm_status fmm_dtt(fmm_ctx* ctx, int remote, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (!remote) {
         const uint64_t root_pair = 0;
-        return dtt_pass(ctx, &root_pair, 1, false, s);
+        return dtt_pass(ctx, &root_pair, 1, false, s, -1);
     }
     // (local root 0, remote root) of every LET grafted since the last remote traversal
     std::vector<uint64_t> seeds;
+    int dmax = 0;
     for (size_t k = ctx->let_traversed; k < ctx->let_remote.size(); ++k)
-        if (ctx->let_remote[k].ncell > 0) seeds.push_back((uint64_t)ctx->let_remote[k].base);
+        if (ctx->let_remote[k].ncell > 0) {
+            seeds.push_back((uint64_t)ctx->let_remote[k].base);
+            dmax = std::max(dmax, ctx->let_remote[k].depth);
+        }
     ctx->let_traversed = ctx->let_remote.size();
     if (seeds.empty()) return FMM_OK;
-    return dtt_pass(ctx, seeds.data(), (int)seeds.size(), true, s);
+    return dtt_pass(ctx, seeds.data(), (int)seeds.size(), true, s, dmax);
 }
 
 fmm_status fmm_lists(fmm_ctx* ctx, void* stream) {

@@ -65,6 +65,7 @@ struct LetPeer {
 // one grafted remote LET: cells [base, base + ncell), bodies [bbase, bbase + nbody)
 struct LetRemote {
     int64_t base, ncell, bbase, nbody;
+    int depth;   // deepest level of the sender's tree (bounds the traversal's level count)
 };
 
 struct TimedEvent {
@@ -212,7 +213,9 @@ fmm_status gather_bodies_q(fmm_ctx* ctx, const void* q, cudaStream_t s);
 fmm_status build_tree(fmm_ctx* ctx, cudaStream_t s);
 // dtt.cu: traversal from the given seed pairs (target << 32 | source), appended to the
 // unsorted lists when append; lists_pass groups them into canonical CSR lists + P2P runs
-fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append, cudaStream_t s);
+// max_depth_src: deepest source tree among the seeds (-1 unknown: synchronous levels for append)
+fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append, cudaStream_t s,
+                    int max_depth_src = -1);
 fmm_status lists_pass(fmm_ctx* ctx, cudaStream_t s);
 fmm_status build_lists(fmm_ctx* ctx, cudaStream_t s);
 // let.cu

@@ -95,8 +95,7 @@ __global__ void __launch_bounds__(DT_THREADS) k_dtt_step(const uint64_t* __restr
                                                          double theta, unsigned long long* __restrict__ cnt,
                                                          unsigned long long* __restrict__ next_count,
                                                          uint64_t* __restrict__ m2l, uint64_t* __restrict__ p2p,
-                                                         uint64_t* __restrict__ next, uint32_t* __restrict__ tcnt_m2l,
-                                                         uint32_t* __restrict__ tcnt_p2p, uint64_t cap_next,
+                                                         uint64_t* __restrict__ next, uint64_t cap_next,
                                                          uint64_t cap_m2l, uint64_t cap_p2p, int children_only) {
     __shared__ unsigned long long s_warp[DT_THREADS / 32];
     __shared__ unsigned long long s_base[3];
@@ -191,10 +190,6 @@ __global__ void __launch_bounds__(DT_THREADS) k_dtt_step(const uint64_t* __restr
                     next[pc + c] = ((uint64_t)a[k] << 32) | (k0 == FMM_LET_ABSENT ? b[k] : k0 + c);
                 pc += nch[k];
             }
-            if (!children_only) {
-                count_target(tcnt_m2l, o[k] == 0, a[k]);
-                count_target(tcnt_p2p, o[k] == 1, a[k]);
-            }
         }
         __syncthreads();   // s_warp / s_base reuse
     }
@@ -204,6 +199,18 @@ __global__ void __launch_bounds__(DT_THREADS) k_dtt_step(const uint64_t* __restr
 __global__ void k_widen_u32(const uint32_t* __restrict__ in, int64_t n, uint64_t* __restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = in[i];
+}
+
+// per-target counts of an unsorted (target, source) list (warp-aggregated atomics; the traversal
+// emits the pairs of one target in runs)
+__global__ void k_count_targets(const uint64_t* __restrict__ lst, int64_t n, uint32_t* __restrict__ tcnt) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+        const int64_t i = i0 + threadIdx.x;
+        const bool ok = i < n;
+        const uint32_t t = ok ? (uint32_t)(lst[i] >> 32) : 0u;
+        count_target(tcnt, ok, t);
+    }
 }
 
 // counting-sort scatter of unsorted (target, source) pairs into per-target segments; the
@@ -490,6 +497,12 @@ __global__ void k_big_scatter(const uint64_t* __restrict__ off, const uint64_t* 
 fmm_status canonicalise(fmm_ctx* ctx, DevBuf& lst, int64_t n, uint32_t* tcnt, DevBuf& off, DevBuf& src,
                         bool sort_segments, cudaStream_t s) {
     const int64_t nc = ctx->ncell;
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(tcnt, 0, (size_t)nc * 4, s));
+    if (n > 0) {
+        k_count_targets<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 16), 256, 0, s>>>(
+            P_<uint64_t>(lst), n, tcnt);
+        FMM_LAUNCH(ctx);
+    }
     FMM_TRY(buf_ensure(ctx, off, (size_t)(nc + 1) * 8));
     FMM_TRY(buf_ensure(ctx, src, (size_t)std::max<int64_t>(n, 1) * 4));
     FMM_TRY(buf_ensure(ctx, ctx->cnt64, (size_t)(nc + 1) * 8));
@@ -722,7 +735,8 @@ fmm_status build_runs(fmm_ctx* ctx, cudaStream_t s) {
 // earlier build of similar size): all 2*depth+1 levels are launched back to back, each reading its
 // frontier size on the device, with one host round trip at the end; on any overflow (or a deeper
 // traversal) it falls back to the synchronous loop, which grows the buffers to the exact sizes.
-fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append, cudaStream_t s) {
+fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append, cudaStream_t s,
+                    int max_depth_src) {
     const CellView v{P_<double4>(ctx->c_cr), P_<uint32_t>(ctx->c_cb), P_<uint32_t>(ctx->c_cc)};
     const int64_t nc = ctx->ncell;
     FMM_TRY(buf_ensure(ctx, ctx->tcnt, (size_t)nc * 2 * 4));
@@ -733,24 +747,27 @@ fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append
     FMM_TRY(buf_ensure(ctx, ctx->dcount, 64));
     unsigned long long* d_cnt = P_<unsigned long long>(ctx->dcount);
     const int64_t m2l0 = append ? ctx->n_m2l : 0, p2p0 = append ? ctx->n_p2p : 0;
+    // list cursors restart at the entries kept from an earlier traversal (append: the local
+    // lists stay, a failed fast attempt's remote entries are overwritten)
     auto reset = [&]() -> fmm_status {
-        if (!append) {
-            FMM_CUDA_TRY(ctx, cudaMemsetAsync(tcnt_m2l, 0, (size_t)nc * 2 * 4, s));
-            FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt, 0, 4 * 8, s));
-        }
+        const unsigned long long c0[4] = {(unsigned long long)m2l0, (unsigned long long)p2p0, 0ull, 0ull};
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(d_cnt, c0, sizeof(c0), cudaMemcpyHostToDevice, s));
         return FMM_OK;
     };
     const int g_max = ctx->num_sms * 8;
     int64_t peak = nseeds;
 
-    if (!append && ctx->dtt_est_front > 0) {
-        const int L = 2 * (int)ctx->depth + 1;
+    if (ctx->dtt_est_front > 0 && (!append || max_depth_src >= 0)) {
+        const int L = (int)ctx->depth + (append ? max_depth_src : (int)ctx->depth) + 1;
         const uint64_t capf = (uint64_t)ctx->dtt_est_front;
-        const uint64_t capm = (uint64_t)ctx->dtt_est_m2l, capp = (uint64_t)ctx->dtt_est_p2p;
+        const uint64_t capm = append ? std::max<uint64_t>(ctx->lst_m2l.bytes / 8, (uint64_t)ctx->dtt_est_m2l)
+                                     : (uint64_t)ctx->dtt_est_m2l;
+        const uint64_t capp = append ? std::max<uint64_t>(ctx->lst_p2p.bytes / 8, (uint64_t)ctx->dtt_est_p2p)
+                                     : (uint64_t)ctx->dtt_est_p2p;
         FMM_TRY(buf_ensure(ctx, ctx->fr_a, (size_t)std::max<uint64_t>(capf, (uint64_t)nseeds) * 8));
         FMM_TRY(buf_ensure(ctx, ctx->fr_b, (size_t)capf * 8));
-        FMM_TRY(buf_ensure(ctx, ctx->lst_m2l, (size_t)capm * 8));
-        FMM_TRY(buf_ensure(ctx, ctx->lst_p2p, (size_t)capp * 8));
+        FMM_TRY(buf_ensure(ctx, ctx->lst_m2l, (size_t)capm * 8, append, s));
+        FMM_TRY(buf_ensure(ctx, ctx->lst_p2p, (size_t)capp * 8, append, s));
         FMM_TRY(buf_ensure(ctx, ctx->dtt_lvl, (size_t)(L + 2) * 8));
         unsigned long long* lvl = P_<unsigned long long>(ctx->dtt_lvl);
         FMM_TRY(reset());
@@ -763,7 +780,7 @@ fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append
             DevBuf& out = (l & 1) ? ctx->fr_a : ctx->fr_b;
             k_dtt_step<<<g_max, DT_THREADS, 0, s>>>(P_<uint64_t>(in), 0, lvl + l, v, ctx->theta, d_cnt, lvl + l + 1,
                                                     P_<uint64_t>(ctx->lst_m2l), P_<uint64_t>(ctx->lst_p2p),
-                                                    P_<uint64_t>(out), tcnt_m2l, tcnt_p2p, capf, capm, capp, 0);
+                                                    P_<uint64_t>(out), capf, capm, capp, 0);
             FMM_LAUNCH(ctx);
         }
         unsigned long long h[4];
@@ -779,9 +796,11 @@ fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append
         if (!(h[3] & 6ull) && hl[L] == 0) {
             ctx->n_m2l = (int64_t)h[0];
             ctx->n_p2p = (int64_t)h[1];
-            ctx->dtt_est_front = peak + peak / 8 + 1024;
-            ctx->dtt_est_m2l = ctx->n_m2l + ctx->n_m2l / 8 + 1024;
-            ctx->dtt_est_p2p = ctx->n_p2p + ctx->n_p2p / 8 + 1024;
+            if (!append) {
+                ctx->dtt_est_front = peak + peak / 8 + 1024;
+                ctx->dtt_est_m2l = ctx->n_m2l + ctx->n_m2l / 8 + 1024;
+                ctx->dtt_est_p2p = ctx->n_p2p + ctx->n_p2p / 8 + 1024;
+            }
             return FMM_OK;
         }
         // overflow or deeper than 2*depth+1: redo synchronously (exact sizes)
@@ -807,7 +826,7 @@ fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append
         const uint64_t capm = ctx->lst_m2l.bytes / 8, capp = ctx->lst_p2p.bytes / 8;
         k_dtt_step<<<g, DT_THREADS, 0, s>>>(P_<uint64_t>(ctx->fr_a), nf, nullptr, v, ctx->theta, d_cnt, d_cnt + 2,
                                             P_<uint64_t>(ctx->lst_m2l), P_<uint64_t>(ctx->lst_p2p),
-                                            P_<uint64_t>(ctx->fr_b), tcnt_m2l, tcnt_p2p, ctx->fr_b.bytes / 8, capm,
+                                            P_<uint64_t>(ctx->fr_b), ctx->fr_b.bytes / 8, capm,
                                             capp, 0);
         FMM_LAUNCH(ctx);
         unsigned long long h[4];
@@ -818,7 +837,7 @@ fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append
             FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_cnt + 2, 0, 16, s));
             k_dtt_step<<<g, DT_THREADS, 0, s>>>(P_<uint64_t>(ctx->fr_a), nf, nullptr, v, ctx->theta, d_cnt, d_cnt + 2,
                                                 P_<uint64_t>(ctx->lst_m2l), P_<uint64_t>(ctx->lst_p2p),
-                                                P_<uint64_t>(ctx->fr_b), tcnt_m2l, tcnt_p2p, ctx->fr_b.bytes / 8, capm,
+                                                P_<uint64_t>(ctx->fr_b), ctx->fr_b.bytes / 8, capm,
                                                 capp, 1);
             FMM_LAUNCH(ctx);
             FMM_CUDA_TRY(ctx, cudaMemcpyAsync(h, d_cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -867,6 +886,6 @@ fmm_status lists_pass(fmm_ctx* ctx, cudaStream_t s) {
 
 fmm_status build_lists(fmm_ctx* ctx, cudaStream_t s) {
     const uint64_t root_pair = 0;
-    FMM_TRY(dtt_pass(ctx, &root_pair, 1, false, s));
+    FMM_TRY(dtt_pass(ctx, &root_pair, 1, false, s, -1));
     return lists_pass(ctx, s);
 }

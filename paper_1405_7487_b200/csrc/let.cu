@@ -38,7 +38,7 @@ struct __align__(16) LetCell {
 static_assert(sizeof(LetCell) == 64, "LetCell is 64 B");
 
 struct LetHeader {
-    int64_t ncell, nbody, ncoef, prec, magic, pad[3];
+    int64_t ncell, nbody, ncoef, prec, magic, depth, pad[2];   // depth: sender's deepest level
 };
 static_assert(sizeof(LetHeader) == 64, "LetHeader is 64 B");
 constexpr int64_t LET_MAGIC = 0x4c45543031ll;   // "LET01"
@@ -318,6 +318,7 @@ fmm_status let_pack(fmm_ctx* ctx, int peer, int part, void* dst, cudaStream_t s)
     h.ncoef = ctx->ncoef;
     h.prec = ctx->prec;
     h.magic = LET_MAGIC + part;
+    h.depth = ctx->depth;
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(dst, &h, sizeof(h), cudaMemcpyHostToDevice, s));
     char* p = (char*)dst + sizeof(LetHeader);
     const unsigned gw = (unsigned)std::min<int64_t>((nc + 7) / 8, (int64_t)ctx->num_sms * 16);
@@ -413,7 +414,7 @@ fmm_status let_graft(fmm_ctx* ctx, int npeers, const void* const* src, const int
                     h.nbody, (const dbody*)p, P_<dbody>(ctx->body) + bbase);
             FMM_LAUNCH(ctx);
         }
-        ctx->let_remote.push_back({cbase, h.ncell, bbase, h.nbody});
+        ctx->let_remote.push_back({cbase, h.ncell, bbase, h.nbody, (int)h.depth});
         cbase += h.ncell;
         bbase += h.nbody;
     }
