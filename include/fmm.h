@@ -109,6 +109,16 @@ fmm_status fmm_interact(fmm_ctx* ctx, void* phi, void* grad, void* stream);
  * Outputs are in the caller's original particle order.  Asynchronous on `stream`. */
 fmm_status fmm_evaluate(fmm_ctx* ctx, const void* pos, const void* q, void* phi, void* grad, void* stream);
 
+/* fmm_solve: fmm_build followed by fmm_evaluate on the same device buffers, in one call, so
+ * the library can overlap independent passes: P2M/M2M (R12, R13; they need the tree and q
+ * only) run on the library's aux stream while the dual tree traversal and the list grouping
+ * (R9, R10) run on `stream`; L2L/L2P run on the aux stream while P2P runs on `stream`.  The
+ * results are identical to fmm_build + fmm_evaluate.  pos device [n][3], q device [n],
+ * phi device [n], grad device [n][3] (prec type, caller order); n as in fmm_build.
+ * Synchronises `stream` once (the build's host round trips); the evaluation is enqueued
+ * asynchronously and joined back into `stream`.  Errors as fmm_build / fmm_evaluate. */
+fmm_status fmm_solve(fmm_ctx* ctx, const void* pos, const void* q, int64_t n, void* phi, void* grad, void* stream);
+
 /* fmm_solve_host: build + evaluate on HOST buffers (pos[n][3], q[n] in; phi[n],
  * grad[n][3] out), host<->device copies included; synchronous.  Pinned host memory is
  * recommended for copy speed but not required. */

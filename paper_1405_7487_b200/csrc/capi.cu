@@ -119,15 +119,18 @@ fmm_status fmm_create(int64_t n_max, int p, double theta, int ncrit, int prec, i
         const char* g3 = getenv("FMM_P2P_VARIANT");
         ctx->p2p_variant = g3 ? atoi(g3) : 0;
         const char* g4 = getenv("FMM_OVERLAP");
-        ctx->serial_nearfar = !(g4 && g4[0] == '1');
+        ctx->overlap = !(g4 && g4[0] == '0');
         const char* g5 = getenv("FMM_CANONICAL_M2L");
         ctx->canonical_m2l = !(g5 && g5[0] == '0');
+        const char* g7 = getenv("FMM_LIST_SORT");
+        ctx->list_sort = g7 ? atoi(g7) : 0;
         const char* g6 = getenv("FMM_M2L_VARIANT");
         ctx->m2l_variant = g6 ? atoi(g6) : 0;
     }
     if (cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_up, cudaEventDisableTiming) != cudaSuccess) {
         delete ctx;
         return FMM_ERR_CUDA;
     }
@@ -146,7 +149,7 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
                       &ctx->lst_p2p, &ctx->lst_tmp, &ctx->m2l_src, &ctx->p2p_src, &ctx->m2l_off, &ctx->p2p_off,
                       &ctx->cnt_tmp, &ctx->cnt_tmp2, &ctx->dcount, &ctx->runs, &ctx->run_off, &ctx->run_tmp, &ctx->run_pre,
                       &ctx->run_len64, &ctx->dcount2, &ctx->tcnt, &ctx->cnt64, &ctx->big_off, &ctx->M, &ctx->L, &ctx->Mr, &ctx->Lr, &ctx->near_phi, &ctx->near_grad,
-                      &ctx->h_stage};
+                      &ctx->far, &ctx->h_stage};
     for (DevBuf* b : bufs) buf_free(*b);
     DevBuf* lbufs[] = {&ctx->let_tmp, &ctx->let_cov, &ctx->c_orig, &ctx->part_tmp, &ctx->seg_lists, &ctx->orb_tmp, &ctx->root_given, &ctx->fold_tab, &ctx->leaf_cls, &ctx->dtt_lvl};
     for (DevBuf* b : lbufs) buf_free(*b);
@@ -162,6 +165,7 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->ev_up) cudaEventDestroy(ctx->ev_up);
     delete ctx;
     return FMM_OK;
 }
@@ -297,20 +301,21 @@ fmm_status fmm_interact(fmm_ctx* ctx, void* phi, void* grad, void* stream) {
     }
     DeviceGuard g(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
-    if (ctx->serial_nearfar) {
-        // both persistent kernels fill the GPU on their own: run them back to back
+    FMM_TRY(m2l_pass(ctx, s));
+    if (!ctx->overlap) {
         FMM_TRY(p2p_pass(ctx, s));
-        FMM_TRY(m2l_pass(ctx, s));
+        FMM_TRY(downward_pass(ctx, phi, grad, s));
     } else {
-        // P2P on the aux stream concurrently with M2L on the caller's stream
+        // L2L/L2P (level-synchronous, latency-bound) on the aux stream while P2P fills the GPU;
+        // the far field waits in ctx->far and the merge adds the P2P partials
         FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
         FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
-        FMM_TRY(p2p_pass(ctx, ctx->aux));
-        FMM_TRY(m2l_pass(ctx, s));
+        FMM_TRY(downward_far(ctx, ctx->aux));
         FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, ctx->aux));
+        FMM_TRY(p2p_pass(ctx, s));
         FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
+        FMM_TRY(merge_nearfar(ctx, phi, grad, s));
     }
-    FMM_TRY(downward_pass(ctx, phi, grad, s));
     ctx->evaluated = true;
     return FMM_OK;
 }
@@ -326,6 +331,34 @@ fmm_status fmm_evaluate(fmm_ctx* ctx, const void* pos, const void* q, void* phi,
         return FMM_ERR_ARG;
     }
     FMM_TRY(fmm_upward(ctx, pos, q, stream));
+    return fmm_interact(ctx, phi, grad, stream);
+}
+
+fmm_status fmm_solve(fmm_ctx* ctx, const void* pos, const void* q, int64_t n, void* phi, void* grad, void* stream) {
+    FMM_TRY(check_ctx(ctx));
+    if (n > 0 && (!q || !phi || !grad)) {
+        ctx->err = "fmm_solve: null pointer";
+        return FMM_ERR_ARG;
+    }
+    FMM_TRY(fmm_build_tree(ctx, pos, n, stream));
+    if (n == 0 || !ctx->overlap) {
+        FMM_TRY(fmm_dtt(ctx, 0, stream));
+        FMM_TRY(fmm_lists(ctx, stream));
+        return fmm_evaluate(ctx, pos, q, phi, grad, stream);
+    }
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    // P2M/M2M need the tree and q only: on the aux stream while the traversal and the list
+    // grouping (latency-bound, with host round trips) run on the caller's stream
+    FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
+    FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+    FMM_TRY(gather_bodies_q(ctx, q, ctx->aux));
+    FMM_TRY(upward_pass(ctx, ctx->aux));
+    FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_up, ctx->aux));
+    FMM_TRY(fmm_dtt(ctx, 0, stream));
+    FMM_TRY(fmm_lists(ctx, stream));
+    FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_up, 0));
+    ctx->upward_done = true;
     return fmm_interact(ctx, phi, grad, stream);
 }
 
@@ -432,8 +465,7 @@ fmm_status fmm_solve_host(fmm_ctx* ctx, const void* pos_h, const void* q_h, int6
         if (n) FMM_CUDA_TRY(ctx, cudaMemcpyAsync(dpos, pos_h, bpos, cudaMemcpyHostToDevice, s));
         if (n) FMM_CUDA_TRY(ctx, cudaMemcpyAsync(dq, q_h, bq, cudaMemcpyHostToDevice, s));
     }
-    FMM_TRY(fmm_build(ctx, dpos, n, stream));
-    FMM_TRY(fmm_evaluate(ctx, dpos, dq, dphi, dgrad, stream));
+    FMM_TRY(fmm_solve(ctx, dpos, dq, n, dphi, dgrad, stream));
     {
         PhaseScope ps(ctx, PH_COPY, s);
         if (n) FMM_CUDA_TRY(ctx, cudaMemcpyAsync(phi_h, dphi, bq, cudaMemcpyDeviceToHost, s));

@@ -85,15 +85,19 @@ struct fmm_ctx {
     int p2p_variant = 0;
     int m2l_variant = 0;        // fp32 register M2L: 0 mirror-paired f32x2, 1 scalar (FMM_M2L_VARIANT)
     int p2p_np = 2;             // CTA P2P: target pairs per thread (FMM_P2P_NP = 1, 2, 4)        // 0: CTA per leaf over source runs, 1: warp per leaf (FMM_P2P_VARIANT)
+    int list_sort = 0;           // list grouping: 0 counting scatter + per-segment sorts, 1 one radix sort of the packed pairs (FMM_LIST_SORT)
     bool canonical_m2l = true;   // sort M2L sources within each target on the device (FMM_CANONICAL_M2L=0: skip)
-    bool serial_nearfar = true; // P2P and M2L on one stream (FMM_OVERLAP=1: P2P on the aux stream)   // register-resident M2L where instantiated (FMM_M2L_GENERIC=1 disables)
+    // aux-stream overlap of the latency-bound passes (FMM_OVERLAP=0: everything on the caller's
+    // stream): L2L/L2P run concurrently with P2P; in fmm_solve P2M/M2M also run concurrently with
+    // the traversal and list grouping
+    bool overlap = true;
     int device = 0;
     int num_sms = 148;
     std::string err;
 
-    // streams / events (aux stream runs P2P concurrently with M2L)
+    // aux stream and the events that order it against the caller's stream
     cudaStream_t aux = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_up = nullptr;
 
     // timing
     bool timing = false;
@@ -143,6 +147,7 @@ struct fmm_ctx {
     int fold_P = -1;              // P of the fold table in fold_tab (m2l_fast.cu)
     int64_t fold_nt = 0;   // fp64 [ncell][ncoef]; Mr: packed reduced multipoles for the M2L kernel; Lr: reduced L
     DevBuf near_phi, near_grad;  // P2P partials in sorted order (prec type)
+    DevBuf far;                  // L2P far field in sorted order, double4 (phi, grad) (overlap mode)
     bool upward_done = false;
 
     // multi-GPU (let.cu, part.cu): remote LET cells live at [ncell, ncell + nrem) of every
@@ -201,11 +206,13 @@ fmm_status scan_exclusive_u32(fmm_ctx* ctx, const uint32_t* in, uint32_t* out, i
                               cudaStream_t s);
 fmm_status scan_exclusive_u64(fmm_ctx* ctx, const uint64_t* in, uint64_t* out, int64_t n, uint64_t* total_dev,
                               cudaStream_t s);
-// sort.cu: stable LSD radix sort of (key, val) over bits [bit_lo, bit_hi); result pointers returned
+// sort.cu: stable LSD radix sort of (key, val) over the 8-bit digits of [bit_lo, bit_hi) that
+// `vary` touches (0: find the varying digits on the device, one host read); result pointers returned
 fmm_status radix_sort_pairs(fmm_ctx* ctx, uint64_t* k0, uint64_t* k1, uint32_t* v0, uint32_t* v1, int64_t n,
-                            int bit_lo, int bit_hi, uint64_t** kout, uint32_t** vout, cudaStream_t s);
+                            int bit_lo, int bit_hi, uint64_t** kout, uint32_t** vout, cudaStream_t s,
+                            uint64_t vary = 0);
 fmm_status radix_sort_keys(fmm_ctx* ctx, uint64_t* k0, uint64_t* k1, int64_t n, int bit_lo, int bit_hi,
-                           uint64_t** kout, cudaStream_t s);
+                           uint64_t** kout, cudaStream_t s, uint64_t vary = 0);
 // keys.cu
 fmm_status build_keys(fmm_ctx* ctx, const void* pos, int64_t n, cudaStream_t s);
 fmm_status gather_bodies_q(fmm_ctx* ctx, const void* q, cudaStream_t s);
@@ -233,3 +240,6 @@ fmm_status m2l_fast(fmm_ctx* ctx, cudaStream_t s);
 bool m2l_fast_available(int P, int prec);
 fmm_status p2p_pass(fmm_ctx* ctx, cudaStream_t s);
 fmm_status downward_pass(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s);
+// L2L + L2P writing the far field to ctx->far (sorted order); merge_nearfar adds P2P and un-permutes
+fmm_status downward_far(fmm_ctx* ctx, cudaStream_t s);
+fmm_status merge_nearfar(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s);

@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(LPG_WARPS * 32) k_l2p(const Body* __restrict__
                                                         const double4* __restrict__ cr, int P, int ncoef,
                                                         const double* __restrict__ L, const Real* __restrict__ near_phi,
                                                         const Real* __restrict__ near_grad, Real* __restrict__ phi,
-                                                        Real* __restrict__ grad) {
+                                                        Real* __restrict__ grad, double4* __restrict__ far) {
     __shared__ uchar4 ex[816];
     __shared__ double s_L[LPG_WARPS][816];
     __shared__ double s_pw[LPG_WARPS][3][FMM_MAXP][32];
@@ -120,7 +120,9 @@ __global__ void __launch_bounds__(LPG_WARPS * 32) k_l2p(const Body* __restrict__
                     g2 += s_L[w][cidx(e.x, e.y, e.z + 1)] * m;
                 }
             }
-            if (ok) {
+            if (ok && far) {
+                far[b0 + j] = make_double4(f, g0, g1, g2);
+            } else if (ok) {
                 uint32_t sj = b0 + j;
                 uint32_t o = perm[sj];
                 phi[o] = (Real)(f + (double)near_phi[sj]);
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(LP_WARPS * 32) k_l2p_t(const Body* __restrict_
                                                           const double4* __restrict__ cr, const double* __restrict__ L,
                                                           const Real* __restrict__ near_phi,
                                                           const Real* __restrict__ near_grad, Real* __restrict__ phi,
-                                                          Real* __restrict__ grad) {
+                                                          Real* __restrict__ grad, double4* __restrict__ far) {
     constexpr int NC = P * (P + 1) * (P + 2) / 6;
     __shared__ double s_L[LP_WARPS][NC];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -208,6 +210,10 @@ __global__ void __launch_bounds__(LP_WARPS * 32) k_l2p_t(const Body* __restrict_
                 for (int d = 0; d < 3; ++d) g[d] = fma(ga[d], pw[0][a], g[d]);
             }
             const uint32_t sj = b0 + j;
+            if (far) {
+                far[sj] = make_double4(f, g[0], g[1], g[2]);
+                continue;
+            }
             const uint32_t o = perm[sj];
             phi[o] = (Real)(f + (double)near_phi[sj]);
 #pragma unroll
@@ -216,8 +222,25 @@ __global__ void __launch_bounds__(LP_WARPS * 32) k_l2p_t(const Body* __restrict_
     }
 }
 
+// R18 with the far field kept separately (L2P ran concurrently with P2P): the same sums as the
+// fused L2P epilogue, (Real)(far + (double)near), scattered to the caller's order
+template <typename Real>
+__global__ void k_merge_nearfar(int64_t n, const uint32_t* __restrict__ perm, const double4* __restrict__ far,
+                                const Real* __restrict__ near_phi, const Real* __restrict__ near_grad,
+                                Real* __restrict__ phi, Real* __restrict__ grad) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double4 f = far[i];
+        const uint32_t o = perm[i];
+        phi[o] = (Real)(f.x + (double)near_phi[i]);
+        grad[3 * (int64_t)o + 0] = (Real)(f.y + (double)near_grad[3 * i + 0]);
+        grad[3 * (int64_t)o + 1] = (Real)(f.z + (double)near_grad[3 * i + 1]);
+        grad[3 * (int64_t)o + 2] = (Real)(f.w + (double)near_grad[3 * i + 2]);
+    }
+}
+
 template <typename Body, typename Real>
-fmm_status downward_t(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s) {
+fmm_status downward_t(fmm_ctx* ctx, void* phi, void* grad, double4* far, cudaStream_t s) {
     PhaseScope ps(ctx, PH_DOWN, s);
     double* L = P_<double>(ctx->L);
     const size_t smem = (size_t)DN_WARPS * 2 * ctx->ncoef * 8;
@@ -235,7 +258,7 @@ fmm_status downward_t(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s) {
         k_l2p_t<PP, Body, Real><<<std::max(g, 1), LP_WARPS * 32, 0, s>>>(                                          \
             P_<Body>(ctx->body), ctx->d_perm, P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, P_<uint32_t>(ctx->c_bb),    \
             P_<uint32_t>(ctx->c_bc), P_<double4>(ctx->c_cr), L, P_<Real>(ctx->near_phi), P_<Real>(ctx->near_grad), \
-            (Real*)phi, (Real*)grad);                                                                              \
+            (Real*)phi, (Real*)grad, far);                                                                         \
         FMM_LAUNCH(ctx);                                                                                           \
         FMM_CUDA_TRY(ctx, cudaGetLastError());                                                                     \
         return FMM_OK;                                                                                             \
@@ -249,7 +272,19 @@ fmm_status downward_t(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s) {
     k_l2p<Body, Real><<<std::max(g, 1), LPG_WARPS * 32, 0, s>>>(
         P_<Body>(ctx->body), ctx->d_perm, P_<uint32_t>(ctx->leaf_ids), ctx->nleaf, P_<uint32_t>(ctx->c_bb),
         P_<uint32_t>(ctx->c_bc), P_<double4>(ctx->c_cr), ctx->P, ctx->ncoef, L, P_<Real>(ctx->near_phi),
-        P_<Real>(ctx->near_grad), (Real*)phi, (Real*)grad);
+        P_<Real>(ctx->near_grad), (Real*)phi, (Real*)grad, far);
+    FMM_LAUNCH(ctx);
+    FMM_CUDA_TRY(ctx, cudaGetLastError());
+    return FMM_OK;
+}
+
+template <typename Real>
+fmm_status merge_t(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s) {
+    PhaseScope ps(ctx, PH_DOWN, s);
+    const int g = (int)std::min<int64_t>((ctx->n + 255) / 256, (int64_t)ctx->num_sms * 8);
+    k_merge_nearfar<Real><<<std::max(g, 1), 256, 0, s>>>(ctx->n, ctx->d_perm, P_<double4>(ctx->far),
+                                                         P_<Real>(ctx->near_phi), P_<Real>(ctx->near_grad),
+                                                         (Real*)phi, (Real*)grad);
     FMM_LAUNCH(ctx);
     FMM_CUDA_TRY(ctx, cudaGetLastError());
     return FMM_OK;
@@ -257,6 +292,18 @@ fmm_status downward_t(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s) {
 }  // namespace
 
 fmm_status downward_pass(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s) {
-    if (ctx->prec == FMM_F32) return downward_t<float4, float>(ctx, phi, grad, s);
-    return downward_t<dbody, double>(ctx, phi, grad, s);
+    if (ctx->prec == FMM_F32) return downward_t<float4, float>(ctx, phi, grad, nullptr, s);
+    return downward_t<dbody, double>(ctx, phi, grad, nullptr, s);
+}
+
+fmm_status downward_far(fmm_ctx* ctx, cudaStream_t s) {
+    FMM_TRY(buf_ensure(ctx, ctx->far, (size_t)ctx->n * sizeof(double4)));
+    double4* far = P_<double4>(ctx->far);
+    if (ctx->prec == FMM_F32) return downward_t<float4, float>(ctx, nullptr, nullptr, far, s);
+    return downward_t<dbody, double>(ctx, nullptr, nullptr, far, s);
+}
+
+fmm_status merge_nearfar(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s) {
+    if (ctx->prec == FMM_F32) return merge_t<float>(ctx, phi, grad, s);
+    return merge_t<double>(ctx, phi, grad, s);
 }

@@ -493,6 +493,48 @@ __global__ void k_big_scatter(const uint64_t* __restrict__ off, const uint64_t* 
     }
 }
 
+// sorted packed (target << 32 | source) list -> CSR: src[i] = low word; off[t] = first entry of
+// target t (filled for every target between two consecutive distinct targets), off[nc] = n
+__global__ void k_list_csr(const uint64_t* __restrict__ lst, int64_t n, int64_t nc, uint64_t* __restrict__ off,
+                           uint32_t* __restrict__ src) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint64_t x = lst[i];
+        const int64_t t = (int64_t)(x >> 32);
+        src[i] = (uint32_t)x;
+        const int64_t tp = i == 0 ? -1 : (int64_t)(lst[i - 1] >> 32);
+        for (int64_t u = tp + 1; u <= t; ++u) off[u] = (uint64_t)i;
+        if (i == n - 1)
+            for (int64_t u = t + 1; u <= nc; ++u) off[u] = (uint64_t)n;
+    }
+}
+
+// canonical R10 order by one stable radix sort of the packed (target, source) words over the
+// digits that can vary (source bits [0, nb_src), target bits [32, 32 + nb_tgt)), then CSR.
+// FMM_LIST_SORT=1 only: at c2 the four onesweep passes over the 2.7e7 M2L words (~120 Gkeys/s
+// per pass) cost 2x the counting scatter + per-segment sorts of canonicalise (measured round 1)
+fmm_status canonicalise_sorted(fmm_ctx* ctx, DevBuf& lst, int64_t n, DevBuf& off, DevBuf& src, cudaStream_t s) {
+    const int64_t nc = ctx->ncell;
+    FMM_TRY(buf_ensure(ctx, off, (size_t)(nc + 1) * 8));
+    FMM_TRY(buf_ensure(ctx, src, (size_t)std::max<int64_t>(n, 1) * 4));
+    if (n == 0) {
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(off.p, 0, (size_t)(nc + 1) * 8, s));
+        return FMM_OK;
+    }
+    int nbs = 1, nbt = 1;
+    while (((int64_t)1 << nbs) < nc + ctx->nrem) ++nbs;
+    while (((int64_t)1 << nbt) < nc) ++nbt;
+    const uint64_t vary = (((uint64_t)1 << nbs) - 1) | ((((uint64_t)1 << nbt) - 1) << 32);
+    FMM_TRY(buf_ensure(ctx, ctx->lst_tmp, (size_t)n * 8));
+    uint64_t* sorted = nullptr;
+    FMM_TRY(radix_sort_keys(ctx, P_<uint64_t>(lst), P_<uint64_t>(ctx->lst_tmp), n, 0, 64, &sorted, s, vary));
+    const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 16);
+    k_list_csr<<<g, 256, 0, s>>>(sorted, n, nc, P_<uint64_t>(off), P_<uint32_t>(src));
+    FMM_LAUNCH(ctx);
+    FMM_CUDA_TRY(ctx, cudaGetLastError());
+    return FMM_OK;
+}
+
 // unsorted packed list (n pairs) + per-target counts -> CSR off/src, canonical order
 fmm_status canonicalise(fmm_ctx* ctx, DevBuf& lst, int64_t n, uint32_t* tcnt, DevBuf& off, DevBuf& src,
                         bool sort_segments, cudaStream_t s) {
@@ -870,8 +912,13 @@ fmm_status lists_pass(fmm_ctx* ctx, cudaStream_t s) {
     // P2P sources are always put in ascending order (the source runs need it); the M2L
     // segments only when canonical device order is requested (fmm_copy_lists sorts on the
     // host otherwise; the set and the grouping by target are the same either way).
-    FMM_TRY(canonicalise(ctx, ctx->lst_m2l, ctx->n_m2l, tcnt_m2l, ctx->m2l_off, ctx->m2l_src, ctx->canonical_m2l, s));
-    FMM_TRY(canonicalise(ctx, ctx->lst_p2p, ctx->n_p2p, tcnt_p2p, ctx->p2p_off, ctx->p2p_src, true, s));
+    if (ctx->list_sort == 1 && ctx->canonical_m2l) {
+        FMM_TRY(canonicalise_sorted(ctx, ctx->lst_m2l, ctx->n_m2l, ctx->m2l_off, ctx->m2l_src, s));
+        FMM_TRY(canonicalise_sorted(ctx, ctx->lst_p2p, ctx->n_p2p, ctx->p2p_off, ctx->p2p_src, s));
+    } else {
+        FMM_TRY(canonicalise(ctx, ctx->lst_m2l, ctx->n_m2l, tcnt_m2l, ctx->m2l_off, ctx->m2l_src, ctx->canonical_m2l, s));
+        FMM_TRY(canonicalise(ctx, ctx->lst_p2p, ctx->n_p2p, tcnt_p2p, ctx->p2p_off, ctx->p2p_src, true, s));
+    }
     unsigned long long* d_inter = P_<unsigned long long>(ctx->dcount2) + 2;
     FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_inter, 0, 8, s));
     k_p2p_inter<<<ctx->num_sms * 4, 256, 0, s>>>(P_<uint64_t>(ctx->p2p_off), nc, P_<uint32_t>(ctx->p2p_src),

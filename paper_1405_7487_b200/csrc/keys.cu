@@ -182,7 +182,7 @@ fmm_status build_keys_t(fmm_ctx* ctx, const Real* pos, int64_t n, cudaStream_t s
     FMM_LAUNCH(ctx);
     FMM_CUDA_TRY(ctx, cudaGetLastError());
     FMM_TRY(radix_sort_pairs(ctx, P_<uint64_t>(ctx->key_a), P_<uint64_t>(ctx->key_b), P_<uint32_t>(ctx->idx_a),
-                             P_<uint32_t>(ctx->idx_b), n, 0, 64, &ctx->d_keys, &ctx->d_perm, s));
+                             P_<uint32_t>(ctx->idx_b), n, 0, 64, &ctx->d_keys, &ctx->d_perm, s, ~0ull));
     FMM_TRY(buf_ensure(ctx, ctx->body, (size_t)n * sizeof(typename BodyT<Real>::type)));
     k_gather_pos<Real><<<gblk, 256, 0, s>>>(pos, ctx->d_perm, n, P_<typename BodyT<Real>::type>(ctx->body));
     FMM_LAUNCH(ctx);

@@ -21,7 +21,7 @@ __constant__ double c_inv[FMM_MAXP + 1] = {0.0,       1.0,        1.0 / 2,  1.0 
                                            1.0 / 6,   1.0 / 7,    1.0 / 8,  1.0 / 9,  1.0 / 10, 1.0 / 11,
                                            1.0 / 12,  1.0 / 13,   1.0 / 14, 1.0 / 15, 1.0 / 16};
 
-template <typename Body>
+template <typename Body, int NI>
 __global__ void __launch_bounds__(P2M_WARPS * 32) k_p2m(const Body* __restrict__ body, const uint32_t* __restrict__ leaf_ids,
                                                         int64_t nleaf, const uint32_t* __restrict__ bb,
                                                         const uint32_t* __restrict__ bc, const double4* __restrict__ cr,
@@ -35,9 +35,13 @@ __global__ void __launch_bounds__(P2M_WARPS * 32) k_p2m(const Body* __restrict__
     for (int64_t li = (int64_t)blockIdx.x * P2M_WARPS + w; li < nleaf; li += (int64_t)gridDim.x * P2M_WARPS) {
         const uint32_t c = leaf_ids[li];
         const double4 ctr = cr[c];
-        double acc[26];
+        double acc[NI];
+        uchar4 ek[NI];
 #pragma unroll
-        for (int i = 0; i < 26; ++i) acc[i] = 0.0;
+        for (int i = 0; i < NI; ++i) {
+            acc[i] = 0.0;
+            ek[i] = ex[min(lane + 32 * i, ncoef - 1)];
+        }
         const uint32_t b0 = bb[c], nb = bc[c];
         for (uint32_t j0 = 0; j0 < nb; j0 += 32) {
             const uint32_t m = min(32u, nb - j0);
@@ -57,20 +61,21 @@ __global__ void __launch_bounds__(P2M_WARPS * 32) k_p2m(const Body* __restrict__
                 }
             }
             __syncwarp();
+            // bodies outer, coefficients inner: the NI accumulators are independent chains
+            // (each coefficient still sums its bodies in order)
+            for (uint32_t j = 0; j < m; ++j) {
+                const double qj = s_q[w][j];
 #pragma unroll
-            for (int i = 0; i < 26; ++i) {
-                const int k = lane + 32 * i;
-                if (k < ncoef) {
-                    const uchar4 e = ex[k];
-                    double sacc = acc[i];
-                    for (uint32_t j = 0; j < m; ++j)
-                        sacc += s_q[w][j] * (s_pw[w][0][e.x][j] * s_pw[w][1][e.y][j] * s_pw[w][2][e.z][j]);
-                    acc[i] = sacc;
+                for (int i = 0; i < NI; ++i) {
+                    if (lane + 32 * i < ncoef) {
+                        const uchar4 e = ek[i];
+                        acc[i] += qj * (s_pw[w][0][e.x][j] * s_pw[w][1][e.y][j] * s_pw[w][2][e.z][j]);
+                    }
                 }
             }
         }
 #pragma unroll
-        for (int i = 0; i < 26; ++i) {
+        for (int i = 0; i < NI; ++i) {
             const int k = lane + 32 * i;
             if (k < ncoef) M[(int64_t)c * ncoef + k] = acc[i];
         }
@@ -150,9 +155,21 @@ fmm_status upward_t(fmm_ctx* ctx, cudaStream_t s) {
     FMM_TRY(buf_ensure(ctx, ctx->M, (size_t)nc * ctx->ncoef * 8));
     double* M = P_<double>(ctx->M);
     int g = (int)std::min<int64_t>((ctx->nleaf + P2M_WARPS - 1) / P2M_WARPS, (int64_t)ctx->num_sms * 32);
-    k_p2m<Body><<<std::max(g, 1), P2M_WARPS * 32, 0, s>>>(P_<Body>(ctx->body), P_<uint32_t>(ctx->leaf_ids), ctx->nleaf,
-                                                         P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc),
-                                                         P_<double4>(ctx->c_cr), ctx->P, ctx->ncoef, M);
+    const int ni = (ctx->ncoef + 31) / 32;
+    auto p2m = [&](auto tag) {
+        constexpr int NI = decltype(tag)::value;
+        k_p2m<Body, NI><<<std::max(g, 1), P2M_WARPS * 32, 0, s>>>(P_<Body>(ctx->body), P_<uint32_t>(ctx->leaf_ids),
+                                                                 ctx->nleaf, P_<uint32_t>(ctx->c_bb),
+                                                                 P_<uint32_t>(ctx->c_bc), P_<double4>(ctx->c_cr),
+                                                                 ctx->P, ctx->ncoef, M);
+    };
+    if (ni <= 1) p2m(std::integral_constant<int, 1>());
+    else if (ni <= 2) p2m(std::integral_constant<int, 2>());
+    else if (ni <= 4) p2m(std::integral_constant<int, 4>());
+    else if (ni <= 7) p2m(std::integral_constant<int, 7>());
+    else if (ni <= 12) p2m(std::integral_constant<int, 12>());
+    else if (ni <= 18) p2m(std::integral_constant<int, 18>());
+    else p2m(std::integral_constant<int, 26>());
     FMM_LAUNCH(ctx);
     const size_t smem = (size_t)8 * 2 * ctx->ncoef * 8;
     if (smem > 48 * 1024) FMM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_m2m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

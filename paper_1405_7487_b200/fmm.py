@@ -29,6 +29,7 @@ SYMBOLS = {
     "fmm_last_error": (C.c_char_p, [_p]),
     "fmm_build": (_i, [_p, _p, _i64, _p]),
     "fmm_evaluate": (_i, [_p, _p, _p, _p, _p, _p]),
+    "fmm_solve": (_i, [_p, _p, _p, _i64, _p, _p, _p]),
     "fmm_solve_host": (_i, [_p, _p, _p, _i64, _p, _p, _p]),
     "fmm_get_counts": (_i, [_p, _p]),
     "fmm_copy_sorted": (_i, [_p, _p, _p]),
@@ -167,8 +168,23 @@ class FMM:
         return phi, grad
 
     def solve(self, pos, q, phi=None, grad=None, stream=None):
-        self.build(pos, stream)
-        return self.evaluate(pos, q, phi, grad, stream)
+        """fmm_solve: build + evaluate in one call (the library overlaps independent passes)."""
+        import torch
+        n = pos.shape[0]
+        self._check_tensor(pos, (n, 3), "pos")
+        self._check_tensor(q, (n,), "q")
+        if phi is None:
+            phi = torch.empty(n, dtype=self.dtype, device=pos.device)
+        if grad is None:
+            grad = torch.empty((n, 3), dtype=self.dtype, device=pos.device)
+        self._check_tensor(phi, (n,), "phi")
+        self._check_tensor(grad, (n, 3), "grad")
+        self._check(lib().fmm_solve(self._h, C.c_void_p(pos.data_ptr()), C.c_void_p(q.data_ptr()), n,
+                                    C.c_void_p(phi.data_ptr()), C.c_void_p(grad.data_ptr()),
+                                    C.c_void_p(self._stream(stream))), "fmm_solve")
+        self._pos = pos
+        self.n = n
+        return phi, grad
 
     def solve_host(self, pos: np.ndarray, q: np.ndarray, phi: np.ndarray = None, grad: np.ndarray = None,
                    stream=None):

@@ -167,6 +167,35 @@ def test_solve_host_matches_device(torch_cuda):
     np.testing.assert_array_equal(grad_h, grad_d.cpu().numpy())
 
 
+@pytest.mark.parametrize("prec,kind", [("f32", "cube"), ("f64", "plummer")])
+def test_solve_equals_build_evaluate(torch_cuda, prec, kind, monkeypatch):
+    """fmm_solve (P2M/M2M on the aux stream during the traversal, L2L/L2P during P2P, far field
+    merged afterwards) gives bit-identical outputs to fmm_build + fmm_evaluate and to a context
+    with every pass on the caller's stream (FMM_OVERLAP=0)."""
+    torch = torch_cuda
+    from paper_1405_7487_b200 import FMM
+    dt = np.float32 if prec == "f32" else np.float64
+    pos, q = synth.generate(kind, 30000, 91, dt)
+    tp, tq = torch.from_numpy(pos).cuda(), torch.from_numpy(q).cuda()
+    f = FMM(30000, 10 if prec == "f32" else 6, 0.4, 64 if prec == "f32" else 32, prec)
+    phi_s, grad_s = f.solve(tp, tq)
+    f.build(tp)
+    phi_e, grad_e = f.evaluate(tp, tq)
+    monkeypatch.setenv("FMM_OVERLAP", "0")
+    g = FMM(30000, 10 if prec == "f32" else 6, 0.4, 64 if prec == "f32" else 32, prec)
+    phi_0, grad_0 = g.solve(tp, tq)
+    # the other list grouping (one radix sort of the packed pairs) gives the same lists
+    monkeypatch.setenv("FMM_LIST_SORT", "1")
+    h = FMM(30000, 10 if prec == "f32" else 6, 0.4, 64 if prec == "f32" else 32, prec)
+    phi_1, grad_1 = h.solve(tp, tq)
+    torch.cuda.synchronize()
+    for a, b in ((phi_s, phi_e), (grad_s, grad_e), (phi_s, phi_0), (grad_s, grad_0), (phi_s, phi_1),
+                 (grad_s, grad_1)):
+        np.testing.assert_array_equal(a.cpu().numpy(), b.cpu().numpy())
+    for a, b in zip(f.lists(), h.lists()):
+        np.testing.assert_array_equal(a, b)
+
+
 def test_repeat_builds_reuse_context(torch_cuda):
     # ONE context across sizes and distributions: workspace growth, and the back-to-back
     # traversal sized from the previous build (smaller, larger -> overflow fallback, deeper)
