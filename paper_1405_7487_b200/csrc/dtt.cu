@@ -72,16 +72,7 @@ __device__ __forceinline__ unsigned long long ballot_append(unsigned long long* 
     return base + __popc(m & lt);
 }
 
-// per-target histogram with one atomic per distinct target in the warp
-__device__ __forceinline__ void count_target(uint32_t* __restrict__ tcnt, bool pred, uint32_t a) {
-    const unsigned m = __ballot_sync(0xffffffffu, pred);
-    if (pred) {
-        const unsigned peers = __match_any_sync(m, a);
-        if ((peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&tcnt[a], (uint32_t)__popc(peers));
-    }
-}
-
-// One block = 1024 consecutive frontier pairs (4 per thread, coalesced).  Each thread packs
+// One block = 1024 consecutive frontier pairs (4 consecutive per thread, one 32-B load).  Each thread packs
 // its (m2l, p2p, children) counts into one u64, a block-wide exclusive scan gives every
 // thread its output offsets, and one thread reserves the block's space with 3 atomics.
 constexpr int DT_THREADS = 256;
@@ -112,19 +103,34 @@ __global__ void __launch_bounds__(DT_THREADS) k_dtt_step(const uint64_t* __restr
         uint32_t a[DT_ITEMS], b[DT_ITEMS], nch[DT_ITEMS];
         int o[DT_ITEMS];
         unsigned long long packed = 0;   // m2l | p2p << 16 | children << 32
+        // thread tid owns frontier entries i0 .. i0+3: the outputs (block scan in thread order)
+        // keep the frontier order, so the children of a split source stay adjacent downstream
+        const int64_t i0 = tile + (int64_t)tid * DT_ITEMS;
+        if (i0 + DT_ITEMS <= nf) {
+            const ulonglong2 u0 = *reinterpret_cast<const ulonglong2*>(fr + i0);
+            const ulonglong2 u1 = *reinterpret_cast<const ulonglong2*>(fr + i0 + 2);
+            const uint64_t pr[4] = {u0.x, u0.y, u1.x, u1.y};
 #pragma unroll
-        for (int k = 0; k < DT_ITEMS; ++k) {
-            const int64_t i = tile + (int64_t)k * DT_THREADS + tid;
-            o[k] = -1; a[k] = b[k] = nch[k] = 0;
-            if (i < nf) {
-                const uint64_t pr = fr[i];
-                a[k] = (uint32_t)(pr >> 32);
-                b[k] = (uint32_t)pr;
+            for (int k = 0; k < DT_ITEMS; ++k) {
+                o[k] = -1; nch[k] = 0;
+                a[k] = (uint32_t)(pr[k] >> 32);
+                b[k] = (uint32_t)pr[k];
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < DT_ITEMS; ++k) {
+                const int64_t i = i0 + k;
+                o[k] = -1; a[k] = b[k] = nch[k] = 0;
+                if (i < nf) {
+                    const uint64_t pr = fr[i];
+                    a[k] = (uint32_t)(pr >> 32);
+                    b[k] = (uint32_t)pr;
+                }
             }
         }
 #pragma unroll
         for (int k = 0; k < DT_ITEMS; ++k) {
-            const int64_t i = tile + (int64_t)k * DT_THREADS + tid;
+            const int64_t i = i0 + k;
             if (i < nf) o[k] = classify(v, a[k], b[k], theta, nch[k]);
             packed += (unsigned long long)(o[k] == 0) | ((unsigned long long)(o[k] == 1) << 16) |
                       ((unsigned long long)nch[k] << 32);
@@ -201,15 +207,31 @@ __global__ void k_widen_u32(const uint32_t* __restrict__ in, int64_t n, uint64_t
     if (i < n) out[i] = in[i];
 }
 
-// per-target counts of an unsorted (target, source) list (warp-aggregated atomics; the traversal
-// emits the pairs of one target in runs)
+// Runs of equal targets in adjacent lanes (the valid lanes are a prefix of the warp): the run's
+// first lane (head) and its length.  Replaces __match_any_sync (ncu: MATCH.ANY was the top
+// stall of the count and scatter kernels); the traversal keeps a split source's children adjacent.
+__device__ __forceinline__ void lane_runs(uint32_t t, bool ok, int& head, int& len) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, t, 1);
+    const unsigned valid = __ballot_sync(0xffffffffu, ok);
+    const unsigned heads = __ballot_sync(0xffffffffu, ok && (lane == 0 || prev != t));
+    const unsigned upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+    head = 31 - __clz(heads & upto);
+    const unsigned above = heads & ~(head == 31 ? 0xffffffffu : ((2u << head) - 1u));
+    const int end = above ? __ffs(above) - 1 : __popc(valid);
+    len = end - head;
+}
+
+// per-target counts of an unsorted (target, source) list: one atomic per run of equal targets
 __global__ void k_count_targets(const uint64_t* __restrict__ lst, int64_t n, uint32_t* __restrict__ tcnt) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
         const int64_t i = i0 + threadIdx.x;
         const bool ok = i < n;
-        const uint32_t t = ok ? (uint32_t)(lst[i] >> 32) : 0u;
-        count_target(tcnt, ok, t);
+        const uint32_t t = ok ? (uint32_t)(lst[i] >> 32) : 0xffffffffu;
+        int head, len;
+        lane_runs(t, ok, head, len);
+        if (ok && (int)(threadIdx.x & 31) == head) atomicAdd(&tcnt[t], (uint32_t)len);
     }
 }
 
@@ -218,21 +240,19 @@ __global__ void k_count_targets(const uint64_t* __restrict__ lst, int64_t n, uin
 // so lanes of a warp with the same target share one atomic (__match_any_sync)
 __global__ void k_scatter_src(const uint64_t* __restrict__ lst, int64_t n, const uint64_t* __restrict__ off,
                               uint32_t* __restrict__ cursor, uint32_t* __restrict__ src) {
-    const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
         const int64_t i = i0 + threadIdx.x;
         const bool ok = i < n;
         const uint64_t pr = ok ? lst[i] : ~0ull;
         const uint32_t t = (uint32_t)(pr >> 32);
-        const unsigned act = __ballot_sync(0xffffffffu, ok);
-        if (!ok) continue;
-        const unsigned peers = __match_any_sync(act, t);
-        const int leader = __ffs(peers) - 1;
+        int head, len;
+        lane_runs(t, ok, head, len);
+        const int lane = threadIdx.x & 31;
         uint32_t base = 0;
-        if ((peers & lt) == 0) base = atomicAdd(&cursor[t], (uint32_t)__popc(peers));
-        base = __shfl_sync(peers, base, leader);
-        src[off[t] + base + __popc(peers & lt)] = (uint32_t)pr;
+        if (ok && lane == head) base = atomicAdd(&cursor[t], (uint32_t)len);
+        base = __shfl_sync(0xffffffffu, base, head);
+        if (ok) src[off[t] + base + (uint32_t)(lane - head)] = (uint32_t)pr;
     }
 }
 
