@@ -130,9 +130,17 @@ fmm_status fmm_create(int64_t n_max, int p, double theta, int ncrit, int prec, i
     if (cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_up, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&ctx->ev_up, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_done, cudaEventDisableTiming) != cudaSuccess) {
         delete ctx;
         return FMM_ERR_CUDA;
+    }
+    {
+        const char* g11 = getenv("FMM_PRIO");
+        int lo = 0, hi = 0;
+        if (!(g11 && g11[0] == '0') && cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess && hi < lo) {
+            if (cudaStreamCreateWithPriority(&ctx->hp, cudaStreamNonBlocking, hi) != cudaSuccess) ctx->hp = nullptr;
+        }
     }
     *out = ctx;
     return FMM_OK;
@@ -166,6 +174,8 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->ev_up) cudaEventDestroy(ctx->ev_up);
+    if (ctx->ev_done) cudaEventDestroy(ctx->ev_done);
+    if (ctx->hp) cudaStreamDestroy(ctx->hp);
     delete ctx;
     return FMM_OK;
 }
@@ -340,26 +350,40 @@ fmm_status fmm_solve(fmm_ctx* ctx, const void* pos, const void* q, int64_t n, vo
         ctx->err = "fmm_solve: null pointer";
         return FMM_ERR_ARG;
     }
-    FMM_TRY(fmm_build_tree(ctx, pos, n, stream));
     if (n == 0 || !ctx->overlap) {
+        FMM_TRY(fmm_build_tree(ctx, pos, n, stream));
         FMM_TRY(fmm_dtt(ctx, 0, stream));
         FMM_TRY(fmm_lists(ctx, stream));
         return fmm_evaluate(ctx, pos, q, phi, grad, stream);
     }
     DeviceGuard g(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
+    // the critical path runs on the library's high-priority stream (joined back into `stream`
+    // at the end), the aux stream has the lowest priority: its blocks only take SM slots the
+    // critical path leaves free
+    cudaStream_t m = ctx->hp ? ctx->hp : s;
+    if (m != s) {
+        FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
+        FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(m, ctx->ev_fork, 0));
+    }
+    FMM_TRY(fmm_build_tree(ctx, pos, n, m));
     // P2M/M2M need the tree and q only: on the aux stream while the traversal and the list
-    // grouping (latency-bound, with host round trips) run on the caller's stream
-    FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
+    // grouping (latency-bound, with host round trips) run on the critical-path stream
+    FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, m));
     FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
     FMM_TRY(gather_bodies_q(ctx, q, ctx->aux));
     FMM_TRY(upward_pass(ctx, ctx->aux));
     FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_up, ctx->aux));
-    FMM_TRY(fmm_dtt(ctx, 0, stream));
-    FMM_TRY(fmm_lists(ctx, stream));
-    FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_up, 0));
+    FMM_TRY(fmm_dtt(ctx, 0, m));
+    FMM_TRY(fmm_lists(ctx, m));
+    FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(m, ctx->ev_up, 0));
     ctx->upward_done = true;
-    return fmm_interact(ctx, phi, grad, stream);
+    FMM_TRY(fmm_interact(ctx, phi, grad, m));
+    if (m != s) {
+        FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_done, m));
+        FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_done, 0));
+    }
+    return FMM_OK;
 }
 
 // ---- multi-GPU: LET (let.cu)

@@ -97,7 +97,8 @@ struct fmm_ctx {
 
     // aux stream and the events that order it against the caller's stream
     cudaStream_t aux = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_up = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_up = nullptr, ev_done = nullptr;
+    cudaStream_t hp = nullptr;   // high-priority stream for fmm_solve's critical path (FMM_PRIO=0: none)
 
     // timing
     bool timing = false;
