@@ -231,6 +231,13 @@ def run_dist(args, cfg, rank, world, local):
         # every step after the first partitions with the previous step's Eq. (1) weights
         return D.solve([dpos], [dq], [rank * n], reuse_weights=True)
 
+    if args.tune_alpha > 0:
+        # Eq. (1) alpha optimised over time steps before the measured run, then frozen
+        D.enable_alpha_tuning()
+        for _ in range(args.tune_alpha):
+            step()
+        D.alpha = D.tuner.best
+        D.tuner = None
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -293,7 +300,8 @@ def run_dist(args, cfg, rank, world, local):
                 "phases_note": "per-phase CUDA-event spans; upward overlaps dtt/lists and downward overlaps p2p "
                                "(aux stream), so the spans sum to more than ms_per_step",
                 "counts_rank0": counts,
-                "let_bytes_rank0": dict(D.stats)}
+                "let_bytes_rank0": dict(D.stats),
+                "alpha": D.alpha, "alpha_tuned_steps": args.tune_alpha}
         print(json.dumps(line), flush=True)
     tdist.barrier()
     D.close()
@@ -309,6 +317,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist", action="store_true", help="use the distributed path even on 1 GPU")
+    ap.add_argument("--tune-alpha", type=int, default=0,
+                    help="distributed path: optimise Eq. (1)'s alpha over this many steps before the warm-up")
     ap.add_argument("--partitioner", default="morton", choices=["morton", "orb"],
                     help="multi-GPU partition: Morton ranges (north_star) or ORB multisection (SURVEY 8f f3)")
     args = ap.parse_args()

@@ -28,6 +28,8 @@ The step (§II-B/C):
 """
 from __future__ import annotations
 
+import time
+
 import numpy as np
 import torch
 
@@ -272,6 +274,79 @@ def orb_plan(hist_fn, split_fn, nranks: int, bits: int = 16):
     return groups
 
 
+# ------------------------------------------------------------------ Eq. (1) alpha over time steps
+class AlphaTuner:
+    """alpha of Eq. (1) w_i = l_i + alpha r_i, "a constant that is optimized over the time steps to
+    minimize the total runtime" (§II-B; the paper names no method).  Reading: a
+    golden-section search on log(alpha) over [lo, hi], one measured step runtime per probe, until
+    the bracket is narrower than `tol` (in log alpha); then alpha stays at the fastest probe.
+
+    The weights a step computes with alpha only shape the NEXT step's partition, so a probe is
+    set for two consecutive steps and scored by the runtime of the second (the first step that
+    ran on a partition made with it): next_alpha() before each step's weights, report(t) after
+    each step."""
+
+    GR = (np.sqrt(5.0) - 1.0) / 2.0
+
+    def __init__(self, lo: float = 1.0 / 16, hi: float = 16.0, tol: float = 0.1):
+        if not (0 < lo < hi):
+            raise ValueError("need 0 < lo < hi")
+        self.a, self.b, self.tol = float(np.log(lo)), float(np.log(hi)), tol
+        self.c = self.b - self.GR * (self.b - self.a)
+        self.d = self.a + self.GR * (self.b - self.a)
+        self.fc = self.fd = None
+        self.history = []            # (alpha, runtime) per scored probe
+        self._probe = self.c         # log alpha being evaluated
+        self._age = 0                # steps the current probe has been set for
+
+    @property
+    def converged(self) -> bool:
+        return self.b - self.a < self.tol
+
+    @property
+    def best(self) -> float:
+        if not self.history:
+            return float(np.exp(self._probe))
+        return min(self.history, key=lambda h: h[1])[0]
+
+    def next_alpha(self) -> float:
+        if self.converged:
+            return self.best
+        return float(np.exp(self._probe))
+
+    def report(self, runtime: float) -> None:
+        """runtime of the step just finished (its partition used the weights of the step before)."""
+        if self.converged:
+            return
+        self._age += 1
+        if self._age < 2:            # the probe's weights have not partitioned a step yet
+            return
+        self.history.append((float(np.exp(self._probe)), float(runtime)))
+        if self._probe == self.c:
+            self.fc = float(runtime)
+        else:
+            self.fd = float(runtime)
+        if self.fc is None:
+            self._probe = self.c
+        elif self.fd is None:
+            self._probe = self.d
+        else:
+            self._shrink()
+        self._age = 0
+
+    def _shrink(self) -> None:
+        if self.fc < self.fd:        # minimum in [a, d]
+            self.b, self.d, self.fd = self.d, self.c, self.fc
+            self.c = self.b - self.GR * (self.b - self.a)
+            self.fc = None
+            self._probe = self.c
+        else:                        # minimum in [c, b]
+            self.a, self.c, self.fc = self.c, self.d, self.fd
+            self.d = self.a + self.GR * (self.b - self.a)
+            self.fd = None
+            self._probe = self.d
+
+
 # ------------------------------------------------------------------ driver
 class DistFMM:
     """The FMM on `comm.world` ranks; this process drives the ranks `comm.ranks`.
@@ -292,6 +367,13 @@ class DistFMM:
         self.c_m2l = m2l_cost_ratio(P) if c_m2l is None else c_m2l
         self.stats = {}
         self.weights = None                                       # per local rank, owner order
+        self.tuner = None                                         # AlphaTuner (enable_alpha_tuning)
+
+    def enable_alpha_tuning(self, lo: float = 1.0 / 16, hi: float = 16.0, tol: float = 0.1):
+        """Optimise Eq. (1)'s alpha over the following solve(reuse_weights=True) steps by their
+        measured runtime (max over ranks); see AlphaTuner."""
+        self.tuner = AlphaTuner(lo, hi, tol)
+        return self.tuner
 
     def close(self):
         for f in self.fmm:
@@ -468,6 +550,12 @@ class DistFMM:
         1, or with reuse_weights the Eq. (1) weights this object measured at its last step)."""
         if w is None and reuse_weights and self.weights is not None:
             w = self.weights
+        if self.tuner is not None:
+            dev = pos[0].device
+            if dev.type == "cuda":
+                torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            self.alpha = self.tuner.next_alpha()                 # for this step's weights
         lpos, lq, lgid, back, packed, cnt = self.partition(pos, q, gid_base, w)
         self.build(lpos)
         res = self.evaluate(lpos, lq)
@@ -480,4 +568,11 @@ class DistFMM:
         self.stats["work_local"], self.stats["work_remote"] = float(lr[0]), float(lr[1])
         self.local = (lpos, lq, lgid)
         out, self.weights = self.gather_back(res, wts, back, packed, cnt, gid_base, [p.shape[0] for p in pos])
+        if self.tuner is not None:
+            if dev.type == "cuda":
+                torch.cuda.synchronize(dev)
+            t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+            t = self.comm.allreduce([t] * len(self.fmm), "max")[0]
+            self.tuner.report(float(t.item()))
+            self.stats["alpha"] = self.alpha
         return out

@@ -183,3 +183,49 @@ def test_orb_plan_balanced_boxes(K, kind):
     for r, g in groups.items():               # every particle lies in its rank's box
         m = grp == r
         assert np.all((xyz[m] >= np.array(g["lo"])) & (xyz[m] < np.array(g["hi"])))
+
+
+def _run_tuner(cost, steps, **kw):
+    """Drive AlphaTuner the way DistFMM.solve does: alpha_k is set before step k's weights, and
+    step k's runtime reflects the partition made with alpha_{k-1}."""
+    from paper_1405_7487_b200.dist import AlphaTuner
+    tu = AlphaTuner(**kw)
+    prev = None
+    for _ in range(steps):
+        a = tu.next_alpha()
+        tu.report(cost(prev if prev is not None else 1.0))
+        prev = a
+    return tu
+
+
+@pytest.mark.parametrize("amin", [0.08, 0.3, 1.0, 6.0])
+def test_alpha_tuner_finds_minimum(amin):
+    """Golden-section over log(alpha) ("optimized over the time steps to minimize the
+    total runtime"): on a unimodal runtime with its minimum at amin it converges to amin, scoring
+    each probe by the step after the one that set it."""
+    cost = lambda a: 1.0 + (np.log(a) - np.log(amin)) ** 2
+    tu = _run_tuner(cost, 80, lo=1.0 / 16, hi=16.0, tol=0.05)
+    assert tu.converged
+    assert abs(np.log(tu.best) - np.log(amin)) < 0.1, (tu.best, amin, tu.history)
+    # every scored probe's runtime is the cost of the alpha it was scored for (no lag mix-up)
+    for a, t in tu.history:
+        assert t == pytest.approx(cost(a))
+    # golden-section: ~log(range/tol)/log(1/0.618) probes, two steps each
+    assert len(tu.history) <= 16
+
+
+def test_alpha_tuner_edges():
+    from paper_1405_7487_b200.dist import AlphaTuner
+    with pytest.raises(ValueError):
+        AlphaTuner(lo=2.0, hi=1.0)
+    with pytest.raises(ValueError):
+        AlphaTuner(lo=0.0, hi=1.0)
+    # monotone runtime: converges to the bracket end
+    tu = _run_tuner(lambda a: a, 80, lo=0.1, hi=10.0, tol=0.05)
+    assert tu.converged and tu.best < 0.13
+    tu = _run_tuner(lambda a: -a, 80, lo=0.1, hi=10.0, tol=0.05)
+    assert tu.converged and tu.best > 7.5
+    # after convergence alpha is frozen at the best probe
+    a = tu.next_alpha()
+    tu.report(123.0)
+    assert tu.next_alpha() == a

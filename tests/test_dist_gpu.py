@@ -249,3 +249,35 @@ def test_dist_degenerate(torch_cuda, part):
         np.testing.assert_allclose(phi, dp, rtol=1e-12, atol=1e-12)
         np.testing.assert_allclose(grad, dg, rtol=1e-12, atol=1e-12)
         D.close()
+
+
+def test_alpha_tuning_steps(torch_cuda):
+    """Eq. (1) alpha optimised over time steps: a tuned multi-step run changes
+    alpha between steps (probes of the golden-section search), and every step still returns the
+    direct sum within the FMM error of a single-rank solve."""
+    import torch
+    from paper_1405_7487_b200 import FMM
+    from paper_1405_7487_b200.dist import DistFMM, LoopbackComm
+    n, K = 12000, 3
+    pos, q = synth.generate("plummer", n, 5, np.float64)
+    cuts = np.linspace(0, n, K + 1).astype(int)
+    P_in = [torch.from_numpy(pos[cuts[r]:cuts[r + 1]]).cuda() for r in range(K)]
+    Q_in = [torch.from_numpy(q[cuts[r]:cuts[r + 1]]).cuda() for r in range(K)]
+    D = DistFMM(LoopbackComm(K), n, 6, 0.5, 16, "f64")
+    tu = D.enable_alpha_tuning(lo=0.25, hi=4.0, tol=0.2)
+    t = synth.sample_targets(n, 300, 5)
+    dphi, dgrad = oracle.direct(pos, q, t)
+    f1 = FMM(n, 6, 0.5, 16, "f64")
+    p1, _ = f1.solve(torch.from_numpy(pos).cuda(), torch.from_numpy(q).cuda())
+    e1 = oracle.rel_l2(p1.cpu().numpy()[t], dphi)
+    alphas = []
+    for _ in range(8):
+        out = D.solve(P_in, Q_in, [int(c) for c in cuts[:-1]], reuse_weights=True)
+        alphas.append(D.alpha)
+        phi = np.concatenate([o[0].cpu().numpy() for o in out])
+        grad = np.concatenate([o[1].cpu().numpy() for o in out])
+        assert oracle.rel_l2(phi[t], dphi) < 10 * e1 + 1e-12
+        assert oracle.rel_l2(grad[t], dgrad) < 1e-3
+    assert len(set(alphas)) >= 2, alphas
+    assert len(tu.history) >= 3
+    D.close()
