@@ -37,7 +37,8 @@ import numpy as np  # noqa: E402
 import synth  # noqa: E402
 
 METRIC = "FMM particles/s at 1/2/4/8 B200 (P=10); P2P+M2L % of FP32 roofline"
-CONFIG_NAMES = {"c1": "configs[0]", "c2": "configs[1]", "c3": "configs[2]", "sph": "Table I case 2 (sphere)"}
+CONFIG_NAMES = {"c1": "configs[0]", "c2": "configs[1]", "c3": "configs[2]", "sph": "Table I case 2 (sphere)",
+                "c4s": "configs[3] (strong-scaling N on 1 GPU)", "c4w": "configs[3] (weak-scaling per-GPU N)"}
 FP32_LANES_PER_SM = 128
 
 

@@ -98,36 +98,36 @@ __global__ void __launch_bounds__(DT_THREADS) k_dtt_step(const uint64_t* __restr
         if (*reinterpret_cast<volatile unsigned long long*>(&cnt[3]) & 6ull) return;
         nf = (int64_t)min(*nf_dev, (unsigned long long)cap_next);
     }
-    for (int64_t tile = (int64_t)blockIdx.x * DT_THREADS * DT_ITEMS; tile < nf;
-         tile += (int64_t)gridDim.x * DT_THREADS * DT_ITEMS) {
-        uint32_t a[DT_ITEMS], b[DT_ITEMS], nch[DT_ITEMS];
-        int o[DT_ITEMS];
-        unsigned long long packed = 0;   // m2l | p2p << 16 | children << 32
-        // thread tid owns frontier entries i0 .. i0+3: the outputs (block scan in thread order)
-        // keep the frontier order, so the children of a split source stay adjacent downstream
+    // thread tid owns frontier entries i0 .. i0+3 of a tile: the outputs (block scan in thread
+    // order) keep the frontier order, so the children of a split source stay adjacent downstream.
+    // The next tile's entries are loaded while this tile is classified (ncu: the frontier load
+    // was the top long-scoreboard stall).
+    auto load_tile = [&](int64_t tile, uint64_t (&pr)[DT_ITEMS]) {
         const int64_t i0 = tile + (int64_t)tid * DT_ITEMS;
         if (i0 + DT_ITEMS <= nf) {
             const ulonglong2 u0 = *reinterpret_cast<const ulonglong2*>(fr + i0);
             const ulonglong2 u1 = *reinterpret_cast<const ulonglong2*>(fr + i0 + 2);
-            const uint64_t pr[4] = {u0.x, u0.y, u1.x, u1.y};
-#pragma unroll
-            for (int k = 0; k < DT_ITEMS; ++k) {
-                o[k] = -1; nch[k] = 0;
-                a[k] = (uint32_t)(pr[k] >> 32);
-                b[k] = (uint32_t)pr[k];
-            }
+            pr[0] = u0.x; pr[1] = u0.y; pr[2] = u1.x; pr[3] = u1.y;
         } else {
 #pragma unroll
-            for (int k = 0; k < DT_ITEMS; ++k) {
-                const int64_t i = i0 + k;
-                o[k] = -1; a[k] = b[k] = nch[k] = 0;
-                if (i < nf) {
-                    const uint64_t pr = fr[i];
-                    a[k] = (uint32_t)(pr >> 32);
-                    b[k] = (uint32_t)pr;
-                }
-            }
+            for (int k = 0; k < DT_ITEMS; ++k) pr[k] = i0 + k < nf ? fr[i0 + k] : 0ull;
         }
+    };
+    const int64_t tstride = (int64_t)gridDim.x * DT_THREADS * DT_ITEMS;
+    uint64_t nxt[DT_ITEMS];
+    if ((int64_t)blockIdx.x * DT_THREADS * DT_ITEMS < nf) load_tile((int64_t)blockIdx.x * DT_THREADS * DT_ITEMS, nxt);
+    for (int64_t tile = (int64_t)blockIdx.x * DT_THREADS * DT_ITEMS; tile < nf; tile += tstride) {
+        uint32_t a[DT_ITEMS], b[DT_ITEMS], nch[DT_ITEMS];
+        int o[DT_ITEMS];
+        unsigned long long packed = 0;   // m2l | p2p << 16 | children << 32
+        const int64_t i0 = tile + (int64_t)tid * DT_ITEMS;
+#pragma unroll
+        for (int k = 0; k < DT_ITEMS; ++k) {
+            o[k] = -1; nch[k] = 0;
+            a[k] = (uint32_t)(nxt[k] >> 32);
+            b[k] = (uint32_t)nxt[k];
+        }
+        if (tile + tstride < nf) load_tile(tile + tstride, nxt);
 #pragma unroll
         for (int k = 0; k < DT_ITEMS; ++k) {
             const int64_t i = i0 + k;

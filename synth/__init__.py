@@ -102,6 +102,10 @@ CONFIGS = {
     "c1": dict(kind="cube", n=4096, P=4, theta=0.5, ncrit=32, prec="f64", seed=1),
     "c2": dict(kind="cube", n=1 << 20, P=10, theta=0.4, ncrit=64, prec="f32", seed=2),
     "c3": dict(kind="plummer", n=10_000_000, P=10, theta=0.4, ncrit=64, prec="f32", seed=3),
+    # configs[3] on one GPU: the strong-scaling problem (N = 2^26, Q24) and the weak-scaling
+    # per-GPU size (2^24); same parameters as c2
+    "c4s": dict(kind="cube", n=1 << 26, P=10, theta=0.4, ncrit=64, prec="f32", seed=4),
+    "c4w": dict(kind="cube", n=1 << 24, P=10, theta=0.4, ncrit=64, prec="f32", seed=4),
     # Table I case 2: sphere surface, P=10, theta=0.4, ncrit=512
     "sph": dict(kind="sphere", n=1 << 22, P=10, theta=0.4, ncrit=512, prec="f32", seed=5),
 }
