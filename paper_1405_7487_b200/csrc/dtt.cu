@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(128) k_segsort_warp(const uint64_t* __restrict
 }
 
 // Warp-per-segment stable LSD radix sort in shared memory for up to MAXN keys: BITS-bit
-// digits; ranking row by row (32 keys) with __match_any_sync and a per-warp running
+// digits; ranking row by row (32 keys) with a ballot multi-split and a per-warp running
 // histogram, exclusive scan of the bins, scatter to the other buffer.  ~25 instr/key/pass.
 // <1024, 8>: 11 KB of shared memory per warp (20 warps/SM); <2048, 10>: 24 KB.
 constexpr int WR_WARPS = 4;
@@ -390,8 +390,8 @@ __global__ void __launch_bounds__(WR_WARPS * 32) k_segsort_wradix(const uint64_t
             for (int r = 0; r < n; r += 32) {
                 const int i = r + lane;
                 const bool ok = i < n;
-                const uint32_t d = ok ? (in[i] >> shift) & (BINS - 1) : 0xFFFFFFFFu;
-                const unsigned peers = __match_any_sync(0xffffffffu, d);
+                const uint32_t d = ok ? (in[i] >> shift) & (BINS - 1) : 0u;
+                const unsigned peers = match_digit<BITS>(d, __ballot_sync(0xffffffffu, ok));
                 uint32_t before = 0;
                 if (ok) before = hist[d];
                 __syncwarp();

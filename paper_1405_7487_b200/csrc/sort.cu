@@ -7,7 +7,7 @@
 //
 // Onesweep form (n < 2^30): ONE read of the keys builds the 256-bin histograms of every
 // digit pass at once; then each 8-bit pass is a single kernel: a tile (4096 keys) takes the
-// next tile number from an atomic counter, ranks its keys (warps: __match_any_sync + per-warp
+// next tile number from an atomic counter, ranks its keys (warps: ballot multi-split + per-warp
 // bin counters, then per-bin prefix over warps -- stable), publishes its per-bin counts and
 // finds the counts of all earlier tiles by decoupled look-back (one 32-bit status word per
 // tile and bin: flag | value), then scatters to digit base + earlier tiles + in-tile rank.
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_scatter(const uint64_t* __restri
         k[i] = ok ? kin[j] : 0ull;
         if (HAS_VAL) v[i] = ok ? vin[j] : 0u;
         uint32_t d = ok ? (uint32_t)((k[i] >> shift) & 0xFF) : 0x100u;
-        unsigned peers = __match_any_sync(0xffffffffu, d);
+        unsigned peers = match_digit<9>(d, 0xffffffffu);
         uint32_t rank = __popc(peers & lt);
         uint32_t cnt = __popc(peers);
         bool leader = (peers & lt) == 0;
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_os_pass(const uint64_t* __restri
         k[i] = ok ? kin[j] : 0ull;
         if (HAS_VAL) v[i] = ok ? vin[j] : 0u;
         const uint32_t d = ok ? (uint32_t)((k[i] >> shift) & 0xFF) : 0x100u;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const unsigned peers = match_digit<9>(d, 0xffffffffu);
         const uint32_t rank = __popc(peers & lt);
         const uint32_t before = (d < 0x100u) ? s_whist[w][d] : 0u;
         __syncwarp();
