@@ -122,6 +122,8 @@ fmm_status fmm_create(int64_t n_max, int p, double theta, int ncrit, int prec, i
         ctx->overlap = !(g4 && g4[0] == '0');
         const char* g5 = getenv("FMM_CANONICAL_M2L");
         ctx->canonical_m2l = !(g5 && g5[0] == '0');
+        const char* g15 = getenv("FMM_DTT");
+        ctx->dtt_mode = (g15 && std::string(g15) == "bfs") ? 1 : 0;
         const char* g7 = getenv("FMM_LIST_SORT");
         ctx->list_sort = g7 ? atoi(g7) : 0;
         const char* g6 = getenv("FMM_M2L_VARIANT");
@@ -159,6 +161,9 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
                       &ctx->run_len64, &ctx->dcount2, &ctx->tcnt, &ctx->cnt64, &ctx->big_off, &ctx->M, &ctx->L, &ctx->Mr, &ctx->Lr, &ctx->near_phi, &ctx->near_grad,
                       &ctx->far, &ctx->h_stage};
     for (DevBuf* b : bufs) buf_free(*b);
+    DevBuf* tbufs[] = {&ctx->tc_cnt, &ctx->tc_scan, &ctx->tc_lb, &ctx->tc_d[0], &ctx->tc_d[1], &ctx->tc_doff[0],
+                       &ctx->tc_doff[1], &ctx->tc_glob};
+    for (DevBuf* b : tbufs) buf_free(*b);
     DevBuf* lbufs[] = {&ctx->let_tmp, &ctx->let_cov, &ctx->c_orig, &ctx->part_tmp, &ctx->seg_lists, &ctx->orb_tmp, &ctx->root_given, &ctx->fold_tab, &ctx->leaf_cls, &ctx->dtt_lvl};
     for (DevBuf* b : lbufs) buf_free(*b);
     for (auto& lp : ctx->let_peers) {
@@ -196,6 +201,7 @@ fmm_status fmm_build_tree(fmm_ctx* ctx, const void* pos, int64_t n, void* stream
     DeviceGuard g(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
     ctx->built = ctx->tree_built = false;
+    ctx->lists_csr = false;
     ctx->evaluated = ctx->upward_done = false;
     ctx->n = n;
     ctx->built_pos = pos;
@@ -238,9 +244,18 @@ fmm_status fmm_dtt(fmm_ctx* ctx, int remote, void* stream) {
     DeviceGuard g(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
     if (!remote) {
+        ctx->lists_csr = false;
+        if (ctx->dtt_mode == 0) {
+            PhaseScope ps(ctx, PH_DTT, s);
+            FMM_TRY(tct_lists(ctx, s));
+            ctx->lists_csr = true;
+            return FMM_OK;
+        }
         const uint64_t root_pair = 0;
         return dtt_pass(ctx, &root_pair, 1, false, s, -1);
     }
+    // remote traversals append packed pairs to the local lists
+    if (ctx->lists_csr) FMM_TRY(lists_csr_to_packed(ctx, s));
     // (local root 0, remote root) of every LET grafted since the last remote traversal
     std::vector<uint64_t> seeds;
     int dmax = 0;

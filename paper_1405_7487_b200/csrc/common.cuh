@@ -136,6 +136,12 @@ struct fmm_ctx {
     int64_t n_m2l = 0, n_p2p = 0, p2p_inter = 0;
     DevBuf fr_a, fr_b, lst_m2l, lst_p2p, lst_tmp, m2l_src, p2p_src, m2l_off, p2p_off, cnt_tmp, cnt_tmp2, dcount;
     DevBuf dtt_lvl;                                          // per-level frontier sizes (dtt.cu fast path)
+    // target-ordered traversal (tct.cu): per-level counts/scans, level_begin, pass-down sets
+    // (ping-pong CSR), global split lists of overflowed targets
+    DevBuf tc_cnt, tc_scan, tc_lb, tc_d[2], tc_doff[2], tc_glob;
+    int64_t tc_est_m2l = 0, tc_est_p2p = 0;
+    bool lists_csr = false;     // lists came from tct (CSR only; no packed pair list)
+    int dtt_mode = 0;           // 0: target-ordered traversal (tct.cu), 1: breadth-first (FMM_DTT=bfs)
     int64_t dtt_est_front = 0, dtt_est_m2l = 0, dtt_est_p2p = 0;   // buffer sizes learnt from the last build
     // P2P source runs: runs[n_runs] = {start body, flat offset}, then rtot[ncell]; run_off[ncell+1]
     int64_t n_runs = 0;
@@ -240,6 +246,12 @@ fmm_status build_tree(fmm_ctx* ctx, cudaStream_t s);
 fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append, cudaStream_t s,
                     int max_depth_src = -1);
 fmm_status lists_pass(fmm_ctx* ctx, cudaStream_t s);
+// tct.cu: target-ordered traversal writing the CSR lists directly (local traversal only)
+fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s);
+// dtt.cu: CSR lists -> packed (target << 32 | source) pairs, so remote traversals can append
+fmm_status lists_csr_to_packed(fmm_ctx* ctx, cudaStream_t s);
+// dtt.cu: P2P interaction count and source runs of the CSR lists (synchronises s)
+fmm_status lists_finish(fmm_ctx* ctx, cudaStream_t s);
 fmm_status build_lists(fmm_ctx* ctx, cudaStream_t s);
 // let.cu
 fmm_status let_cover(fmm_ctx* ctx, double* cover, int* ncover, cudaStream_t s);

@@ -932,13 +932,21 @@ fmm_status lists_pass(fmm_ctx* ctx, cudaStream_t s) {
     // P2P sources are always put in ascending order (the source runs need it); the M2L
     // segments only when canonical device order is requested (fmm_copy_lists sorts on the
     // host otherwise; the set and the grouping by target are the same either way).
-    if (ctx->list_sort == 1 && ctx->canonical_m2l) {
+    if (ctx->lists_csr) {
+        // the target-ordered traversal wrote the CSR lists
+    } else if (ctx->list_sort == 1 && ctx->canonical_m2l) {
         FMM_TRY(canonicalise_sorted(ctx, ctx->lst_m2l, ctx->n_m2l, ctx->m2l_off, ctx->m2l_src, s));
         FMM_TRY(canonicalise_sorted(ctx, ctx->lst_p2p, ctx->n_p2p, ctx->p2p_off, ctx->p2p_src, s));
     } else {
         FMM_TRY(canonicalise(ctx, ctx->lst_m2l, ctx->n_m2l, tcnt_m2l, ctx->m2l_off, ctx->m2l_src, ctx->canonical_m2l, s));
         FMM_TRY(canonicalise(ctx, ctx->lst_p2p, ctx->n_p2p, tcnt_p2p, ctx->p2p_off, ctx->p2p_src, true, s));
     }
+    return lists_finish(ctx, s);
+}
+
+// the target-ordered traversal (tct.cu) already wrote the CSR lists
+fmm_status lists_finish(fmm_ctx* ctx, cudaStream_t s) {
+    const int64_t nc = ctx->ncell;
     unsigned long long* d_inter = P_<unsigned long long>(ctx->dcount2) + 2;
     FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_inter, 0, 8, s));
     k_p2p_inter<<<ctx->num_sms * 4, 256, 0, s>>>(P_<uint64_t>(ctx->p2p_off), nc, P_<uint32_t>(ctx->p2p_src),
@@ -948,6 +956,30 @@ fmm_status lists_pass(fmm_ctx* ctx, cudaStream_t s) {
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&inter, d_inter, 8, cudaMemcpyDeviceToHost, s));
     FMM_TRY(build_runs(ctx, s));   // synchronises s
     ctx->p2p_inter = (int64_t)inter;
+    return FMM_OK;
+}
+
+// CSR lists -> packed (target << 32 | source) words in list order, so that remote (LET)
+// traversals can append to them and lists_pass regroups everything
+__global__ void k_csr_to_packed(const uint64_t* __restrict__ off, int64_t nc, const uint32_t* __restrict__ src,
+                                uint64_t* __restrict__ lst) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nc; t += nw)
+        for (uint64_t p = off[t] + lane; p < off[t + 1]; p += 32) lst[p] = ((uint64_t)t << 32) | src[p];
+}
+
+fmm_status lists_csr_to_packed(fmm_ctx* ctx, cudaStream_t s) {
+    const int64_t nc = ctx->ncell;
+    FMM_TRY(buf_ensure(ctx, ctx->lst_m2l, (size_t)std::max<int64_t>(ctx->n_m2l, 1) * 8));
+    FMM_TRY(buf_ensure(ctx, ctx->lst_p2p, (size_t)std::max<int64_t>(ctx->n_p2p, 1) * 8));
+    const unsigned g = (unsigned)std::max<int64_t>(std::min<int64_t>((nc + 7) / 8, (int64_t)ctx->num_sms * 16), 1);
+    k_csr_to_packed<<<g, 256, 0, s>>>(P_<uint64_t>(ctx->m2l_off), nc, P_<uint32_t>(ctx->m2l_src), P_<uint64_t>(ctx->lst_m2l));
+    FMM_LAUNCH(ctx);
+    k_csr_to_packed<<<g, 256, 0, s>>>(P_<uint64_t>(ctx->p2p_off), nc, P_<uint32_t>(ctx->p2p_src), P_<uint64_t>(ctx->lst_p2p));
+    FMM_LAUNCH(ctx);
+    FMM_CUDA_TRY(ctx, cudaGetLastError());
+    ctx->lists_csr = false;
     return FMM_OK;
 }
 

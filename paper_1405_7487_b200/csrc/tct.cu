@@ -1,0 +1,335 @@
+// tct.cu -- the dual tree traversal (a8, R8-R10) organised by TARGET cell, emitting the CSR
+// M2L and P2P lists directly (no unsorted pair list, no grouping, no segment sorts).
+//
+// R9 visits pair (A, B) iff (A, B) = (root, root), or (parent(A), B) is visited and splits A,
+// or (A, parent(B)) is visited and splits B.  So, for a target T, its visited sources are
+//   * the sources its parent passed down: D(parent(T)) = { B : (parent(T), B) visited, splits A }
+//     (the root's: { root }), and
+//   * the children of every source B whose pair (T, B) splits B,
+// and every visited (T, B) is classified by the same R8/R9 test as the breadth-first
+// traversal (dtt.cu): MAC -> M2L, both leaves -> P2P, split A -> D(T), split B -> B's children.
+// Targets are processed level by level (a warp per target); the pass-down sets D of one level
+// feed the next.  Each level runs twice: a counting pass (list lengths per target, scanned into
+// the CSR offsets) and an emitting pass that writes the entries at those offsets.
+//
+// Order inside a target's list (deterministic; R10 fixes the set, fmm_copy_lists sorts for the
+// canonical order): by source level; within a level, first the sources inherited from the
+// parent (in the parent's order), then the children of the split sources (ascending).  The
+// split-B sources of a level wait in a per-warp shared-memory list; a target whose list
+// outgrows it (Plummer: shallow halo leaves next to the core) is redone by a second kernel
+// with per-warp lists in global memory sized for a whole tree level.
+#include "common.cuh"
+
+namespace {
+
+constexpr int TC_WARPS = 4;
+constexpr int TC_CAP = 512;    // split-B sources per target and level held in shared memory
+constexpr int TC_GWARPS = 32;  // warps of the global-memory kernel (overflowed targets)
+
+struct Cells {
+    const double4* __restrict__ cr;
+    const uint32_t* __restrict__ cb;
+    const uint32_t* __restrict__ cc;
+};
+
+// outcome of (T, s): 0 M2L, 1 P2P, 2 split T (s passed down), 3 split s (its children visited)
+__device__ __forceinline__ int tc_classify(const double4 T, uint32_t nT, const Cells& v, uint32_t s, double theta) {
+    const double4 B = v.cr[s];
+    const uint32_t nB = v.cc[s];   // loaded with the centre (one round trip)
+    const double dx = __dsub_rn(T.x, B.x), dy = __dsub_rn(T.y, B.y), dz = __dsub_rn(T.z, B.z);
+    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    if (__dadd_rn(T.w, B.w) < __dmul_rn(theta, __dsqrt_rn(d2))) return 0;
+    if (nT == 0 && nB == 0) return 1;
+    if (nB == 0 || (nT != 0 && T.w >= B.w)) return 2;
+    return 3;
+}
+
+struct TcOut {   // per-target output cursors (warp-uniform)
+    uint32_t m, p, d;
+};
+
+// EMIT = false: count; true: write at offM/offP/offD + cursor.  GLOB = false: targets [tb, te),
+// split lists in shared memory, a target that overflows them is recorded (ovf flag + list) and
+// skipped; GLOB = true: the recorded targets, split lists in global memory (gcap per list).
+template <bool EMIT, bool GLOB>
+__global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
+    int64_t tb, int64_t te, const int32_t* __restrict__ parent, int64_t pb, const uint64_t* __restrict__ doff_prev,
+    const uint32_t* __restrict__ dsrc_prev, Cells v, const int64_t* __restrict__ lb_dev, int nlb, double theta,
+    uint32_t* __restrict__ cnt_m, uint32_t* __restrict__ cnt_p, uint32_t* __restrict__ cnt_d,
+    const uint64_t* __restrict__ offM, const uint64_t* __restrict__ offP, const uint64_t* __restrict__ offD,
+    uint32_t* __restrict__ srcM, uint32_t* __restrict__ srcP, uint32_t* __restrict__ dsrc,
+    uint8_t* __restrict__ ovf, uint32_t* __restrict__ ovf_list, unsigned* __restrict__ n_ovf,
+    uint32_t* __restrict__ gscratch, int64_t gcap) {
+    __shared__ uint32_t s_sb[GLOB ? 1 : TC_WARPS][2][GLOB ? 1 : TC_CAP];
+    __shared__ int64_t s_lb[FMM_MAXLEVEL + 3];
+    for (int i = threadIdx.x; i < nlb; i += blockDim.x) s_lb[i] = lb_dev[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t nwarps = (int64_t)gridDim.x * TC_WARPS;
+    const int64_t gw = (int64_t)blockIdx.x * TC_WARPS + w;
+    uint32_t* list0;
+    uint32_t* list1;
+    int64_t cap;
+    if (GLOB) {
+        list0 = gscratch + (size_t)gw * 2 * gcap;
+        list1 = list0 + gcap;
+        cap = gcap;
+    } else {
+        list0 = s_sb[w][0];
+        list1 = s_sb[w][GLOB ? 0 : 1];
+        cap = TC_CAP;
+    }
+    const int64_t nitems = GLOB ? (int64_t)*n_ovf : te - tb;
+    for (int64_t it = gw; it < nitems; it += nwarps) {
+        const int64_t t = GLOB ? (int64_t)ovf_list[it] : tb + it;
+        if (!GLOB && EMIT && ovf[t - tb]) continue;   // done by the global-memory kernel
+        const double4 T = v.cr[t];
+        const uint32_t nT = v.cc[t];
+        uint64_t x0 = 0, x1 = 1;   // root: the root is its only source
+        if (doff_prev) {
+            const int64_t pi = (int64_t)parent[t] - pb;
+            x0 = doff_prev[pi];
+            x1 = doff_prev[pi + 1];
+        }
+        uint64_t oM = 0, oP = 0, oD = 0;
+        if (EMIT) {
+            oM = offM[t - tb];
+            oP = offP[t - tb];
+            oD = offD[t - tb];
+        }
+        TcOut o{0u, 0u, 0u};
+        bool over = false;
+        int cur = 0;
+        uint32_t ncur = 0;
+        uint64_t xp = x0;
+        // emit the outcome of this lane's pair; `act` = lanes holding a pair, in emission order
+        auto put = [&](int oc, uint32_t s, bool act, uint32_t* nxt, uint32_t& nnext) {
+            const unsigned bm = __ballot_sync(0xffffffffu, act && oc == 0);
+            const unsigned bp = __ballot_sync(0xffffffffu, act && oc == 1);
+            const unsigned bd = __ballot_sync(0xffffffffu, act && oc == 2);
+            const unsigned bs = __ballot_sync(0xffffffffu, act && oc == 3);
+            if (act) {
+                if (oc == 0) {
+                    if (EMIT) srcM[oM + o.m + __popc(bm & lt)] = s;
+                } else if (oc == 1) {
+                    if (EMIT) srcP[oP + o.p + __popc(bp & lt)] = s;
+                } else if (oc == 2) {
+                    if (EMIT) dsrc[oD + o.d + __popc(bd & lt)] = s;
+                } else {
+                    const uint32_t k = nnext + __popc(bs & lt);
+                    if (k < cap) nxt[k] = s;
+                }
+            }
+            o.m += __popc(bm);
+            o.p += __popc(bp);
+            o.d += __popc(bd);
+            nnext += __popc(bs);
+        };
+        for (int lam = 0; lam <= FMM_MAXLEVEL && (xp < x1 || ncur > 0); ++lam) {
+            const int64_t lend = lam + 1 < nlb ? s_lb[lam + 1] : INT64_MAX;
+            uint32_t* nxt = cur ? list0 : list1;
+            uint32_t nnext = 0;
+            // sources passed down by the parent at this level (a prefix of the rest: D is
+            // ordered by level)
+            while (xp < x1) {
+                const uint64_t i = xp + (uint64_t)lane;
+                const uint32_t s = i < x1 ? (doff_prev ? dsrc_prev[i] : 0u) : 0xffffffffu;
+                const bool act = i < x1 && (int64_t)s < lend;
+                const unsigned am = __ballot_sync(0xffffffffu, act);
+                if (!am) break;
+                const int oc = act ? tc_classify(T, nT, v, s, theta) : -1;
+                put(oc, s, act, nxt, nnext);
+                xp += (uint64_t)__popc(am);
+                if (am != 0xffffffffu) break;   // the level's entries ended inside this chunk
+            }
+            // children of this target's split sources of the previous level, in (source, child)
+            // order, flattened over the lanes: a round of 32 split sources is expanded into its
+            // children (prefix sum of the child counts), and each lane classifies one child per
+            // step -- every step issues 32 independent cell loads
+            const uint32_t* sb = cur ? list1 : list0;
+            for (uint32_t base = 0; base < ncur; base += 32) {
+                const bool has = base + lane < ncur;
+                const uint32_t B = has ? sb[base + lane] : 0u;
+                const uint32_t c0 = has ? v.cb[B] : 0u, nc = has ? v.cc[B] : 0u;
+                uint32_t incl = nc;   // inclusive scan of the child counts
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += y;
+                }
+                const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                for (uint32_t f0 = 0; f0 < total; f0 += 32) {
+                    const uint32_t f = f0 + lane;
+                    const bool act = f < total;
+                    // owner lane: the first lane whose inclusive count exceeds f (binary search)
+                    int lo = 0;
+#pragma unroll
+                    for (int step = 16; step; step >>= 1) {
+                        const uint32_t probe = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+                        if (probe <= f) lo += step;
+                    }
+                    const uint32_t own_incl = __shfl_sync(0xffffffffu, incl, lo);
+                    const uint32_t own_nc = __shfl_sync(0xffffffffu, nc, lo);
+                    const uint32_t own_c0 = __shfl_sync(0xffffffffu, c0, lo);
+                    const uint32_t sc = own_c0 + (f - (own_incl - own_nc));
+                    const int oc = act ? tc_classify(T, nT, v, sc, theta) : -1;
+                    put(oc, sc, act, nxt, nnext);
+                }
+            }
+            if (nnext > cap) {   // (global lists hold a whole level: cannot happen there)
+                over = true;
+                break;
+            }
+            __syncwarp();
+            cur ^= 1;
+            ncur = nnext;
+        }
+        if (!EMIT && lane == 0) {
+            if (over && !GLOB) {
+                ovf[t - tb] = 1;
+                ovf_list[atomicAdd(n_ovf, 1u)] = (uint32_t)t;
+            }
+            cnt_m[t - tb] = o.m;
+            cnt_p[t - tb] = o.p;
+            cnt_d[t - tb] = o.d;
+        }
+        __syncwarp();
+    }
+}
+
+// per-level offsets: out = base + exclusive scan (u64), written for the level's targets; the
+// level totals go to tot[0..2] (device) for the host
+__global__ void k_widen3(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                         const uint32_t* __restrict__ c, int64_t n, uint64_t* __restrict__ wa,
+                         uint64_t* __restrict__ wb, uint64_t* __restrict__ wc) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        wa[i] = a[i];
+        wb[i] = b[i];
+        wc[i] = c[i];
+    }
+}
+
+__global__ void k_add_base(uint64_t* __restrict__ x, int64_t n, uint64_t base) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) x[i] += base;
+}
+
+}  // namespace
+
+// Builds m2l_off/src and p2p_off/src (CSR, deterministic order) for the local traversal.
+fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s) {
+    const int64_t nc = ctx->ncell;
+    const int nlev = (int)ctx->depth + 1;
+    const int nlb = (int)ctx->level_begin.size();
+    const Cells v{P_<double4>(ctx->c_cr), P_<uint32_t>(ctx->c_cb), P_<uint32_t>(ctx->c_cc)};
+    int64_t maxw = 1;
+    for (int l = 0; l < nlev; ++l) maxw = std::max(maxw, ctx->level_begin[l + 1] - ctx->level_begin[l]);
+    FMM_TRY(buf_ensure(ctx, ctx->m2l_off, (size_t)(nc + 1) * 8));
+    FMM_TRY(buf_ensure(ctx, ctx->p2p_off, (size_t)(nc + 1) * 8));
+    // per-level scratch: counts (3 x u32), u64 widened and scanned counts (6 x (maxw + 1)),
+    // overflow flags (u8) and list (u32)
+    FMM_TRY(buf_ensure(ctx, ctx->tc_cnt, (size_t)maxw * 12 + (size_t)maxw * 5 + 256));
+    FMM_TRY(buf_ensure(ctx, ctx->tc_scan, (size_t)(maxw + 1) * 8 * 6 + 64));
+    FMM_TRY(buf_ensure(ctx, ctx->tc_lb, (size_t)nlb * 8 + 64));
+    FMM_TRY(buf_ensure(ctx, ctx->dcount2, 128));
+    uint32_t* cm = P_<uint32_t>(ctx->tc_cnt);
+    uint32_t* cp = cm + maxw;
+    uint32_t* cd = cp + maxw;
+    uint32_t* ovf_list = cd + maxw;
+    uint8_t* ovf = reinterpret_cast<uint8_t*>(ovf_list + maxw);
+    uint64_t* wm = P_<uint64_t>(ctx->tc_scan);
+    uint64_t* wp = wm + (maxw + 1);
+    uint64_t* wd = wp + (maxw + 1);
+    uint64_t* om = wd + (maxw + 1);
+    uint64_t* op = om + (maxw + 1);
+    uint64_t* od = op + (maxw + 1);
+    unsigned* n_ovf = P_<unsigned>(ctx->dcount2) + 24;
+    int64_t* lb = P_<int64_t>(ctx->tc_lb);
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(lb, ctx->level_begin.data(), (size_t)nlb * 8, cudaMemcpyHostToDevice, s));
+    // output capacities from the previous build (grown on demand, keeping what is written)
+    FMM_TRY(buf_ensure(ctx, ctx->m2l_src, (size_t)std::max<int64_t>(ctx->tc_est_m2l, 1024) * 4));
+    FMM_TRY(buf_ensure(ctx, ctx->p2p_src, (size_t)std::max<int64_t>(ctx->tc_est_p2p, 1024) * 4));
+    uint64_t baseM = 0, baseP = 0;
+    DevBuf* dprev = &ctx->tc_d[0];
+    DevBuf* dcur = &ctx->tc_d[1];
+    const uint64_t* doff_prev = nullptr;
+    int64_t pb = 0;
+    const int grid_max = ctx->num_sms * 8;
+    const int32_t* par = P_<int32_t>(ctx->c_parent);
+    for (int l = 0; l < nlev; ++l) {
+        const int64_t tb = ctx->level_begin[l], te = ctx->level_begin[l + 1], nt = te - tb;
+        const unsigned g = (unsigned)std::min<int64_t>((nt + TC_WARPS - 1) / TC_WARPS, grid_max);
+        const uint32_t* dsrc_prev = doff_prev ? P_<uint32_t>(*dprev) : nullptr;
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(ovf, 0, (size_t)nt, s));
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(n_ovf, 0, 4, s));
+        k_tct_level<false, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, lb, nlb,
+                                                              ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr, nullptr,
+                                                              nullptr, nullptr, ovf, ovf_list, n_ovf, nullptr, 0);
+        FMM_LAUNCH(ctx);
+        unsigned novf = 0;
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&novf, n_ovf, 4, cudaMemcpyDeviceToHost, s));
+        FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+        const int64_t gcap = maxw;   // a split list never exceeds one tree level
+        if (novf) {
+            FMM_TRY(buf_ensure(ctx, ctx->tc_glob, (size_t)TC_GWARPS * 2 * gcap * 4));
+            k_tct_level<false, true><<<TC_GWARPS / TC_WARPS, TC_WARPS * 32, 0, s>>>(
+                tb, te, par, pb, doff_prev, dsrc_prev, v, lb, nlb, ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr,
+                nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, P_<uint32_t>(ctx->tc_glob), gcap);
+            FMM_LAUNCH(ctx);
+        }
+        const unsigned gw = (unsigned)std::min<int64_t>((nt + 255) / 256, grid_max);
+        k_widen3<<<gw, 256, 0, s>>>(cm, cp, cd, nt, wm, wp, wd);
+        FMM_LAUNCH(ctx);
+        FMM_TRY(scan_exclusive_u64(ctx, wm, om, nt, om + nt, s));
+        FMM_TRY(scan_exclusive_u64(ctx, wp, op, nt, op + nt, s));
+        FMM_TRY(scan_exclusive_u64(ctx, wd, od, nt, od + nt, s));
+        uint64_t tot[3];
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&tot[0], om + nt, 8, cudaMemcpyDeviceToHost, s));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&tot[1], op + nt, 8, cudaMemcpyDeviceToHost, s));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&tot[2], od + nt, 8, cudaMemcpyDeviceToHost, s));
+        FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+        // CSR offsets of this level's targets (cells are level-major: previous levels come first)
+        k_add_base<<<gw, 256, 0, s>>>(om, nt, baseM);
+        FMM_LAUNCH(ctx);
+        k_add_base<<<gw, 256, 0, s>>>(op, nt, baseP);
+        FMM_LAUNCH(ctx);
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<uint64_t>(ctx->m2l_off) + tb, om, (size_t)nt * 8, cudaMemcpyDeviceToDevice, s));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<uint64_t>(ctx->p2p_off) + tb, op, (size_t)nt * 8, cudaMemcpyDeviceToDevice, s));
+        const uint64_t needM = baseM + tot[0], needP = baseP + tot[1];
+        if (needM * 4 > ctx->m2l_src.bytes) FMM_TRY(buf_ensure(ctx, ctx->m2l_src, (size_t)(needM + needM / 4) * 4, true, s));
+        if (needP * 4 > ctx->p2p_src.bytes) FMM_TRY(buf_ensure(ctx, ctx->p2p_src, (size_t)(needP + needP / 4) * 4, true, s));
+        FMM_TRY(buf_ensure(ctx, *dcur, (size_t)std::max<uint64_t>(tot[2], 1) * 4));
+        k_tct_level<true, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, lb, nlb,
+                                                             ctx->theta, nullptr, nullptr, nullptr, om, op, od,
+                                                             P_<uint32_t>(ctx->m2l_src), P_<uint32_t>(ctx->p2p_src),
+                                                             P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf, nullptr, 0);
+        FMM_LAUNCH(ctx);
+        if (novf) {
+            k_tct_level<true, true><<<TC_GWARPS / TC_WARPS, TC_WARPS * 32, 0, s>>>(
+                tb, te, par, pb, doff_prev, dsrc_prev, v, lb, nlb, ctx->theta, nullptr, nullptr, nullptr, om, op, od,
+                P_<uint32_t>(ctx->m2l_src), P_<uint32_t>(ctx->p2p_src), P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf,
+                P_<uint32_t>(ctx->tc_glob), gcap);
+            FMM_LAUNCH(ctx);
+        }
+        baseM = needM;
+        baseP = needP;
+        // this level's pass-down offsets become the next level's input (od holds nt + 1 entries)
+        FMM_TRY(buf_ensure(ctx, ctx->tc_doff[l & 1], (size_t)(nt + 1) * 8));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->tc_doff[l & 1].p, od, (size_t)(nt + 1) * 8, cudaMemcpyDeviceToDevice, s));
+        doff_prev = P_<uint64_t>(ctx->tc_doff[l & 1]);
+        pb = tb;
+        std::swap(dprev, dcur);
+    }
+    const uint64_t ends[2] = {baseM, baseP};
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<uint64_t>(ctx->m2l_off) + nc, &ends[0], 8, cudaMemcpyHostToDevice, s));
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<uint64_t>(ctx->p2p_off) + nc, &ends[1], 8, cudaMemcpyHostToDevice, s));
+    FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));   // ends[] lives on this stack frame
+    FMM_CUDA_TRY(ctx, cudaGetLastError());
+    ctx->n_m2l = (int64_t)baseM;
+    ctx->n_p2p = (int64_t)baseP;
+    ctx->tc_est_m2l = (int64_t)(baseM + baseM / 8 + 1024);
+    ctx->tc_est_p2p = (int64_t)(baseP + baseP / 8 + 1024);
+    return FMM_OK;
+}

@@ -196,6 +196,33 @@ def test_solve_equals_build_evaluate(torch_cuda, prec, kind, monkeypatch):
         np.testing.assert_array_equal(a, b)
 
 
+@pytest.mark.parametrize("prec,kind,n", [("f32", "cube", 40000), ("f64", "plummer", 30000), ("f32", "sphere", 30000)])
+def test_target_traversal_equals_bfs(torch_cuda, prec, kind, n, monkeypatch):
+    """The target-ordered traversal (default) and the breadth-first one (FMM_DTT=bfs) give the same
+    M2L and P2P lists (canonical order) and the same fields to the precision's tolerance; the
+    target-ordered lists are bit-reproducible between runs."""
+    torch = torch_cuda
+    from paper_1405_7487_b200 import FMM
+    dt = np.float32 if prec == "f32" else np.float64
+    pos, q = synth.generate(kind, n, 17, dt)
+    tp, tq = torch.from_numpy(pos).cuda(), torch.from_numpy(q).cuda()
+    P, ncrit = (10, 64) if prec == "f32" else (6, 16)
+    f = FMM(n, P, 0.4, ncrit, prec)
+    phi_t, grad_t = f.solve(tp, tq)
+    phi_t2, grad_t2 = f.solve(tp, tq)
+    monkeypatch.setenv("FMM_DTT", "bfs")
+    g = FMM(n, P, 0.4, ncrit, prec)
+    phi_b, grad_b = g.solve(tp, tq)
+    torch.cuda.synchronize()
+    for a, b in zip(f.lists(), g.lists()):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(phi_t.cpu().numpy(), phi_t2.cpu().numpy())
+    np.testing.assert_array_equal(grad_t.cpu().numpy(), grad_t2.cpu().numpy())
+    tol = TOL[prec]
+    assert oracle.rel_l2(phi_t.cpu().numpy().astype(np.float64), phi_b.cpu().numpy().astype(np.float64)) <= tol
+    assert oracle.rel_l2(grad_t.cpu().numpy().astype(np.float64), grad_b.cpu().numpy().astype(np.float64)) <= tol
+
+
 def test_repeat_builds_reuse_context(torch_cuda):
     # ONE context across sizes and distributions: workspace growth, and the back-to-back
     # traversal sized from the previous build (smaller, larger -> overflow fallback, deeper)
