@@ -122,6 +122,8 @@ fmm_status fmm_create(int64_t n_max, int p, double theta, int ncrit, int prec, i
         ctx->overlap = !(g4 && g4[0] == '0');
         const char* g5 = getenv("FMM_CANONICAL_M2L");
         ctx->canonical_m2l = !(g5 && g5[0] == '0');
+        const char* g16 = getenv("FMM_TCT_SINGLE");
+        ctx->tc_single = !(g16 && g16[0] == '0');
         const char* g15 = getenv("FMM_DTT");
         ctx->dtt_mode = (g15 && std::string(g15) == "bfs") ? 1 : 0;
         const char* g7 = getenv("FMM_LIST_SORT");
@@ -161,8 +163,8 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
                       &ctx->run_len64, &ctx->dcount2, &ctx->tcnt, &ctx->cnt64, &ctx->big_off, &ctx->M, &ctx->L, &ctx->Mr, &ctx->Lr, &ctx->near_phi, &ctx->near_grad,
                       &ctx->far, &ctx->h_stage};
     for (DevBuf* b : bufs) buf_free(*b);
-    DevBuf* tbufs[] = {&ctx->tc_cnt, &ctx->tc_scan, &ctx->tc_lb, &ctx->tc_d[0], &ctx->tc_d[1], &ctx->tc_doff[0],
-                       &ctx->tc_doff[1], &ctx->tc_glob};
+    DevBuf* tbufs[] = {&ctx->tc_cnt, &ctx->tc_lb, &ctx->tc_d[0], &ctx->tc_d[1], &ctx->tc_doff[0],
+                       &ctx->tc_doff[1], &ctx->tc_glob, &ctx->tc_slab, &ctx->tc_bsum};
     for (DevBuf* b : tbufs) buf_free(*b);
     DevBuf* lbufs[] = {&ctx->let_tmp, &ctx->let_cov, &ctx->c_orig, &ctx->part_tmp, &ctx->seg_lists, &ctx->orb_tmp, &ctx->root_given, &ctx->fold_tab, &ctx->leaf_cls, &ctx->dtt_lvl};
     for (DevBuf* b : lbufs) buf_free(*b);

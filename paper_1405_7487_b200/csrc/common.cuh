@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <array>
 #include <string>
 #include <utility>
 #include <vector>
@@ -138,7 +139,9 @@ struct fmm_ctx {
     DevBuf dtt_lvl;                                          // per-level frontier sizes (dtt.cu fast path)
     // target-ordered traversal (tct.cu): per-level counts/scans, level_begin, pass-down sets
     // (ping-pong CSR), global split lists of overflowed targets
-    DevBuf tc_cnt, tc_scan, tc_lb, tc_d[2], tc_doff[2], tc_glob;
+    DevBuf tc_cnt, tc_lb, tc_d[2], tc_doff[2], tc_glob, tc_slab, tc_bsum;
+    std::vector<std::array<uint32_t, 3>> tc_max;   // per-level max list lengths of the last build
+    bool tc_single = true;      // single pass into slots sized from tc_max (FMM_TCT_SINGLE=0: count + emit)
     int64_t tc_est_m2l = 0, tc_est_p2p = 0;
     bool lists_csr = false;     // lists came from tct (CSR only; no packed pair list)
     int dtt_mode = 0;           // 0: target-ordered traversal (tct.cu), 1: breadth-first (FMM_DTT=bfs)

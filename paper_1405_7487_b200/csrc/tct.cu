@@ -18,6 +18,8 @@
 // split-B sources of a level wait in a per-warp shared-memory list; a target whose list
 // outgrows it (Plummer: shallow halo leaves next to the core) is redone by a second kernel
 // with per-warp lists in global memory sized for a whole tree level.
+#include <array>
+
 #include "common.cuh"
 
 namespace {
@@ -48,10 +50,12 @@ struct TcOut {   // per-target output cursors (warp-uniform)
     uint32_t m, p, d;
 };
 
-// EMIT = false: count; true: write at offM/offP/offD + cursor.  GLOB = false: targets [tb, te),
-// split lists in shared memory, a target that overflows them is recorded (ovf flag + list) and
-// skipped; GLOB = true: the recorded targets, split lists in global memory (gcap per list).
-template <bool EMIT, bool GLOB>
+// MODE 0: count; 1: write at offM/offP/offD + cursor; 2 (single pass): write into per-target slab
+// slots of capM/capP/capD entries (srcM/srcP/dsrc = slabs) and count -- a target whose lists
+// outgrow a slot is recorded like a split-list overflow.  GLOB = false: targets [tb, te), split
+// lists in shared memory, a target that overflows them is recorded (ovf flag + list) and
+// skipped by MODE 1; GLOB = true: the recorded targets, split lists in global memory (gcap).
+template <int MODE, bool GLOB>
 __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
     int64_t tb, int64_t te, const int32_t* __restrict__ parent, int64_t pb, const uint64_t* __restrict__ doff_prev,
     const uint32_t* __restrict__ dsrc_prev, Cells v, const int64_t* __restrict__ lb_dev, int nlb, double theta,
@@ -59,7 +63,8 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
     const uint64_t* __restrict__ offM, const uint64_t* __restrict__ offP, const uint64_t* __restrict__ offD,
     uint32_t* __restrict__ srcM, uint32_t* __restrict__ srcP, uint32_t* __restrict__ dsrc,
     uint8_t* __restrict__ ovf, uint32_t* __restrict__ ovf_list, unsigned* __restrict__ n_ovf,
-    uint32_t* __restrict__ gscratch, int64_t gcap) {
+    uint32_t* __restrict__ gscratch, int64_t gcap, uint32_t capM, uint32_t capP, uint32_t capD) {
+    constexpr bool EMIT = MODE != 0, COUNT = MODE != 1, SLAB = MODE == 2;
     __shared__ uint32_t s_sb[GLOB ? 1 : TC_WARPS][2][GLOB ? 1 : TC_CAP];
     __shared__ int64_t s_lb[FMM_MAXLEVEL + 3];
     for (int i = threadIdx.x; i < nlb; i += blockDim.x) s_lb[i] = lb_dev[i];
@@ -83,7 +88,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
     const int64_t nitems = GLOB ? (int64_t)*n_ovf : te - tb;
     for (int64_t it = gw; it < nitems; it += nwarps) {
         const int64_t t = GLOB ? (int64_t)ovf_list[it] : tb + it;
-        if (!GLOB && EMIT && ovf[t - tb]) continue;   // done by the global-memory kernel
+        if (!GLOB && MODE == 1 && ovf[t - tb]) continue;   // done by the global-memory kernel
         const double4 T = v.cr[t];
         const uint32_t nT = v.cc[t];
         uint64_t x0 = 0, x1 = 1;   // root: the root is its only source
@@ -93,7 +98,11 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
             x1 = doff_prev[pi + 1];
         }
         uint64_t oM = 0, oP = 0, oD = 0;
-        if (EMIT) {
+        if (SLAB) {
+            oM = (uint64_t)(t - tb) * capM;
+            oP = (uint64_t)(t - tb) * capP;
+            oD = (uint64_t)(t - tb) * capD;
+        } else if (EMIT) {
             oM = offM[t - tb];
             oP = offP[t - tb];
             oD = offD[t - tb];
@@ -111,11 +120,14 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
             const unsigned bs = __ballot_sync(0xffffffffu, act && oc == 3);
             if (act) {
                 if (oc == 0) {
-                    if (EMIT) srcM[oM + o.m + __popc(bm & lt)] = s;
+                    const uint32_t k = o.m + __popc(bm & lt);
+                    if (EMIT && (!SLAB || k < capM)) srcM[oM + k] = s;
                 } else if (oc == 1) {
-                    if (EMIT) srcP[oP + o.p + __popc(bp & lt)] = s;
+                    const uint32_t k = o.p + __popc(bp & lt);
+                    if (EMIT && (!SLAB || k < capP)) srcP[oP + k] = s;
                 } else if (oc == 2) {
-                    if (EMIT) dsrc[oD + o.d + __popc(bd & lt)] = s;
+                    const uint32_t k = o.d + __popc(bd & lt);
+                    if (EMIT && (!SLAB || k < capD)) dsrc[oD + k] = s;
                 } else {
                     const uint32_t k = nnext + __popc(bs & lt);
                     if (k < cap) nxt[k] = s;
@@ -185,7 +197,8 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
             cur ^= 1;
             ncur = nnext;
         }
-        if (!EMIT && lane == 0) {
+        if (SLAB) over |= o.m > capM || o.p > capP || o.d > capD;
+        if (COUNT && lane == 0) {
             if (over && !GLOB) {
                 ovf[t - tb] = 1;
                 ovf_list[atomicAdd(n_ovf, 1u)] = (uint32_t)t;
@@ -198,23 +211,140 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
     }
 }
 
-// per-level offsets: out = base + exclusive scan (u64), written for the level's targets; the
-// level totals go to tot[0..2] (device) for the host
-__global__ void k_widen3(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
-                         const uint32_t* __restrict__ c, int64_t n, uint64_t* __restrict__ wa,
-                         uint64_t* __restrict__ wb, uint64_t* __restrict__ wc) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        wa[i] = a[i];
-        wb[i] = b[i];
-        wc[i] = c[i];
+// Per-level offsets of the three lists in three launches: tile scans (+ maxima), a one-block
+// scan of the tile sums (level totals to tot[3] for the host), then base + offsets written
+// straight to the CSR arrays: om/op = m2l_off/p2p_off + tb (base = entries of the previous
+// levels), od = the pass-down offsets (nt + 1 entries).
+constexpr int S3_THREADS = 256, S3_ITEMS = 4, S3_TILE = S3_THREADS * S3_ITEMS;
+
+__device__ __forceinline__ unsigned long long s3_block_excl(unsigned long long v, unsigned long long* s_w,
+                                                            unsigned long long* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned long long x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+    }
+    __syncthreads();
+    if (lane == 31) s_w[w] = x;
+    __syncthreads();
+    unsigned long long pre = 0, tot = 0;
+    for (int i = 0; i < S3_THREADS / 32; ++i) {
+        if (i < w) pre += s_w[i];
+        tot += s_w[i];
+    }
+    *total = tot;
+    return pre + x - v;
+}
+
+__global__ void __launch_bounds__(S3_THREADS) k_scan3_tiles(const uint32_t* __restrict__ c0, const uint32_t* __restrict__ c1,
+                                                           const uint32_t* __restrict__ c2, int64_t n,
+                                                           uint64_t* __restrict__ o0, uint64_t* __restrict__ o1,
+                                                           uint64_t* __restrict__ o2, uint64_t* __restrict__ bsum,
+                                                           int64_t nb, unsigned* __restrict__ mx) {
+    __shared__ unsigned long long s_w[S3_THREADS / 32];
+    const uint32_t* in[3] = {c0, c1, c2};
+    uint64_t* out[3] = {o0, o1, o2};
+    const int64_t base = (int64_t)blockIdx.x * S3_TILE + (int64_t)threadIdx.x * S3_ITEMS;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        uint32_t v[S3_ITEMS];
+        unsigned long long sum = 0;
+        unsigned m = 0;
+#pragma unroll
+        for (int k = 0; k < S3_ITEMS; ++k) {
+            v[k] = base + k < n ? in[a][base + k] : 0u;
+            sum += v[k];
+            m = max(m, v[k]);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if ((threadIdx.x & 31) == 0 && m) atomicMax(&mx[a], m);
+        unsigned long long tot;
+        unsigned long long run = s3_block_excl(sum, s_w, &tot);
+#pragma unroll
+        for (int k = 0; k < S3_ITEMS; ++k) {
+            if (base + k < n) out[a][base + k] = run;
+            run += v[k];
+        }
+        if (threadIdx.x == 0) bsum[(int64_t)a * nb + blockIdx.x] = tot;
     }
 }
 
-__global__ void k_add_base(uint64_t* __restrict__ x, int64_t n, uint64_t base) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) x[i] += base;
+// one block: exclusive scan of the tile sums of each list in place; totals to tot[a]
+__global__ void __launch_bounds__(S3_THREADS) k_scan3_top(uint64_t* __restrict__ bsum, int64_t nb,
+                                                         unsigned long long* __restrict__ tot) {
+    __shared__ unsigned long long s_w[S3_THREADS / 32];
+    for (int a = 0; a < 3; ++a) {
+        uint64_t* b = bsum + (int64_t)a * nb;
+        unsigned long long carry = 0;
+        for (int64_t c0 = 0; c0 < nb; c0 += S3_THREADS) {
+            const int64_t i = c0 + threadIdx.x;
+            const unsigned long long v = i < nb ? b[i] : 0ull;
+            unsigned long long t;
+            const unsigned long long e = s3_block_excl(v, s_w, &t);
+            if (i < nb) b[i] = carry + e;
+            carry += t;
+        }
+        if (threadIdx.x == 0) tot[a] = carry;
+    }
 }
+
+__global__ void k_scan3_add(int64_t n, uint64_t* __restrict__ o0, uint64_t* __restrict__ o1, uint64_t* __restrict__ o2,
+                            const uint64_t* __restrict__ bsum, int64_t nb, uint64_t base0, uint64_t base1,
+                            const unsigned long long* __restrict__ tot) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int64_t b = i / S3_TILE;
+        o0[i] += base0 + bsum[b];
+        o1[i] += base1 + bsum[nb + b];
+        o2[i] += bsum[2 * nb + b];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) o2[n] = tot[2];
+}
+
+// single pass: slab slots -> CSR positions (warp per target; overflowed targets are written
+// by the global-memory kernel instead)
+__global__ void k_slab_gather(int64_t nt, const uint8_t* __restrict__ ovf, const uint32_t* __restrict__ cm,
+                              const uint32_t* __restrict__ cp, const uint32_t* __restrict__ cd,
+                              const uint64_t* __restrict__ om, const uint64_t* __restrict__ op,
+                              const uint64_t* __restrict__ od, const uint32_t* __restrict__ slabM,
+                              const uint32_t* __restrict__ slabP, const uint32_t* __restrict__ slabD, uint32_t capM,
+                              uint32_t capP, uint32_t capD, uint32_t* __restrict__ srcM, uint32_t* __restrict__ srcP,
+                              uint32_t* __restrict__ dsrc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nt; i += nw) {
+        if (ovf[i]) continue;
+        for (uint32_t k = lane; k < cm[i]; k += 32) srcM[om[i] + k] = slabM[(uint64_t)i * capM + k];
+        for (uint32_t k = lane; k < cp[i]; k += 32) srcP[op[i] + k] = slabP[(uint64_t)i * capP + k];
+        for (uint32_t k = lane; k < cd[i]; k += 32) dsrc[od[i] + k] = slabD[(uint64_t)i * capD + k];
+    }
+}
+
+// per-level maxima of the three counts (slot sizes of the next build's single pass)
+__global__ void k_max3(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, const uint32_t* __restrict__ c,
+                       int64_t n, unsigned* __restrict__ mx) {
+    unsigned ma = 0, mb = 0, mc = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        ma = max(ma, a[i]);
+        mb = max(mb, b[i]);
+        mc = max(mc, c[i]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        ma = max(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+        mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+        mc = max(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&mx[0], ma);
+        atomicMax(&mx[1], mb);
+        atomicMax(&mx[2], mc);
+    }
+}
+
 
 }  // namespace
 
@@ -228,10 +358,8 @@ fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s) {
     for (int l = 0; l < nlev; ++l) maxw = std::max(maxw, ctx->level_begin[l + 1] - ctx->level_begin[l]);
     FMM_TRY(buf_ensure(ctx, ctx->m2l_off, (size_t)(nc + 1) * 8));
     FMM_TRY(buf_ensure(ctx, ctx->p2p_off, (size_t)(nc + 1) * 8));
-    // per-level scratch: counts (3 x u32), u64 widened and scanned counts (6 x (maxw + 1)),
-    // overflow flags (u8) and list (u32)
+    // per-level scratch: counts (3 x u32), overflow flags (u8) and list (u32)
     FMM_TRY(buf_ensure(ctx, ctx->tc_cnt, (size_t)maxw * 12 + (size_t)maxw * 5 + 256));
-    FMM_TRY(buf_ensure(ctx, ctx->tc_scan, (size_t)(maxw + 1) * 8 * 6 + 64));
     FMM_TRY(buf_ensure(ctx, ctx->tc_lb, (size_t)nlb * 8 + 64));
     FMM_TRY(buf_ensure(ctx, ctx->dcount2, 128));
     uint32_t* cm = P_<uint32_t>(ctx->tc_cnt);
@@ -239,12 +367,6 @@ fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s) {
     uint32_t* cd = cp + maxw;
     uint32_t* ovf_list = cd + maxw;
     uint8_t* ovf = reinterpret_cast<uint8_t*>(ovf_list + maxw);
-    uint64_t* wm = P_<uint64_t>(ctx->tc_scan);
-    uint64_t* wp = wm + (maxw + 1);
-    uint64_t* wd = wp + (maxw + 1);
-    uint64_t* om = wd + (maxw + 1);
-    uint64_t* op = om + (maxw + 1);
-    uint64_t* od = op + (maxw + 1);
     unsigned* n_ovf = P_<unsigned>(ctx->dcount2) + 24;
     int64_t* lb = P_<int64_t>(ctx->tc_lb);
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(lb, ctx->level_begin.data(), (size_t)nlb * 8, cudaMemcpyHostToDevice, s));
@@ -258,70 +380,102 @@ fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s) {
     int64_t pb = 0;
     const int grid_max = ctx->num_sms * 8;
     const int32_t* par = P_<int32_t>(ctx->c_parent);
+    unsigned* mx = n_ovf + 2;   // 3 per-level maxima
+    unsigned long long* d_tot = P_<unsigned long long>(ctx->dcount2) + 4;   // bytes 32..56
+    FMM_TRY(buf_ensure(ctx, ctx->tc_bsum, (size_t)((maxw + S3_TILE - 1) / S3_TILE) * 3 * 8 + 64));
+    uint64_t* bsum = P_<uint64_t>(ctx->tc_bsum);
+    FMM_TRY(buf_ensure(ctx, ctx->tc_glob, (size_t)TC_GWARPS * 2 * maxw * 4));
+    std::vector<std::array<uint32_t, 3>> maxc(nlev);
     for (int l = 0; l < nlev; ++l) {
         const int64_t tb = ctx->level_begin[l], te = ctx->level_begin[l + 1], nt = te - tb;
         const unsigned g = (unsigned)std::min<int64_t>((nt + TC_WARPS - 1) / TC_WARPS, grid_max);
         const uint32_t* dsrc_prev = doff_prev ? P_<uint32_t>(*dprev) : nullptr;
+        // single pass into per-target slots sized from the previous build's per-level maxima
+        // (first build, or slots over budget: count pass + emit pass)
+        bool slab = ctx->tc_single && l < (int)ctx->tc_max.size();
+        uint32_t capM = 0, capP = 0, capD = 0;
+        if (slab) {
+            auto cap = [](uint32_t m) { return (m + m / 4 + 32 + 31) & ~31u; };
+            capM = cap(ctx->tc_max[l][0]);
+            capP = cap(ctx->tc_max[l][1]);
+            capD = cap(ctx->tc_max[l][2]);
+            const size_t bytes = (size_t)nt * (capM + capP + capD) * 4;
+            if (bytes > ((size_t)4 << 30)) slab = false;
+            else FMM_TRY(buf_ensure(ctx, ctx->tc_slab, bytes + 64));
+        }
+        uint32_t* slabM = P_<uint32_t>(ctx->tc_slab);
+        uint32_t* slabP = slabM + (size_t)nt * capM;
+        uint32_t* slabD = slabP + (size_t)nt * capP;
         FMM_CUDA_TRY(ctx, cudaMemsetAsync(ovf, 0, (size_t)nt, s));
-        FMM_CUDA_TRY(ctx, cudaMemsetAsync(n_ovf, 0, 4, s));
-        k_tct_level<false, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, lb, nlb,
-                                                              ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr, nullptr,
-                                                              nullptr, nullptr, ovf, ovf_list, n_ovf, nullptr, 0);
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(n_ovf, 0, 20, s));
+        if (slab)
+            k_tct_level<2, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, lb, nlb,
+                                                              ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr, slabM,
+                                                              slabP, slabD, ovf, ovf_list, n_ovf, nullptr, 0, capM,
+                                                              capP, capD);
+        else
+            k_tct_level<0, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, lb, nlb,
+                                                              ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr,
+                                                              nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, nullptr,
+                                                              0, 0, 0, 0);
         FMM_LAUNCH(ctx);
-        unsigned novf = 0;
-        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&novf, n_ovf, 4, cudaMemcpyDeviceToHost, s));
-        FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+        // overflowed targets (count read on the device: a no-op launch when there are none)
         const int64_t gcap = maxw;   // a split list never exceeds one tree level
-        if (novf) {
-            FMM_TRY(buf_ensure(ctx, ctx->tc_glob, (size_t)TC_GWARPS * 2 * gcap * 4));
-            k_tct_level<false, true><<<TC_GWARPS / TC_WARPS, TC_WARPS * 32, 0, s>>>(
+        {
+            k_tct_level<0, true><<<TC_GWARPS / TC_WARPS, TC_WARPS * 32, 0, s>>>(
                 tb, te, par, pb, doff_prev, dsrc_prev, v, lb, nlb, ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr,
-                nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, P_<uint32_t>(ctx->tc_glob), gcap);
+                nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0);
             FMM_LAUNCH(ctx);
         }
+        // offsets written straight into m2l_off / p2p_off (+ the entries of earlier levels) and
+        // the pass-down CSR of this level
+        uint64_t* om = P_<uint64_t>(ctx->m2l_off) + tb;
+        uint64_t* op = P_<uint64_t>(ctx->p2p_off) + tb;
+        FMM_TRY(buf_ensure(ctx, ctx->tc_doff[l & 1], (size_t)(nt + 1) * 8));
+        uint64_t* od = P_<uint64_t>(ctx->tc_doff[l & 1]);
+        const int64_t nb = (nt + S3_TILE - 1) / S3_TILE;
+        k_scan3_tiles<<<(unsigned)nb, S3_THREADS, 0, s>>>(cm, cp, cd, nt, om, op, od, bsum, nb, mx);
+        FMM_LAUNCH(ctx);
+        k_scan3_top<<<1, S3_THREADS, 0, s>>>(bsum, nb, d_tot);
+        FMM_LAUNCH(ctx);
         const unsigned gw = (unsigned)std::min<int64_t>((nt + 255) / 256, grid_max);
-        k_widen3<<<gw, 256, 0, s>>>(cm, cp, cd, nt, wm, wp, wd);
+        k_scan3_add<<<gw, 256, 0, s>>>(nt, om, op, od, bsum, nb, baseM, baseP, d_tot);
         FMM_LAUNCH(ctx);
-        FMM_TRY(scan_exclusive_u64(ctx, wm, om, nt, om + nt, s));
-        FMM_TRY(scan_exclusive_u64(ctx, wp, op, nt, op + nt, s));
-        FMM_TRY(scan_exclusive_u64(ctx, wd, od, nt, od + nt, s));
         uint64_t tot[3];
-        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&tot[0], om + nt, 8, cudaMemcpyDeviceToHost, s));
-        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&tot[1], op + nt, 8, cudaMemcpyDeviceToHost, s));
-        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&tot[2], od + nt, 8, cudaMemcpyDeviceToHost, s));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(tot, d_tot, 24, cudaMemcpyDeviceToHost, s));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(maxc[l].data(), mx, 12, cudaMemcpyDeviceToHost, s));
         FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-        // CSR offsets of this level's targets (cells are level-major: previous levels come first)
-        k_add_base<<<gw, 256, 0, s>>>(om, nt, baseM);
-        FMM_LAUNCH(ctx);
-        k_add_base<<<gw, 256, 0, s>>>(op, nt, baseP);
-        FMM_LAUNCH(ctx);
-        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<uint64_t>(ctx->m2l_off) + tb, om, (size_t)nt * 8, cudaMemcpyDeviceToDevice, s));
-        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<uint64_t>(ctx->p2p_off) + tb, op, (size_t)nt * 8, cudaMemcpyDeviceToDevice, s));
         const uint64_t needM = baseM + tot[0], needP = baseP + tot[1];
         if (needM * 4 > ctx->m2l_src.bytes) FMM_TRY(buf_ensure(ctx, ctx->m2l_src, (size_t)(needM + needM / 4) * 4, true, s));
         if (needP * 4 > ctx->p2p_src.bytes) FMM_TRY(buf_ensure(ctx, ctx->p2p_src, (size_t)(needP + needP / 4) * 4, true, s));
         FMM_TRY(buf_ensure(ctx, *dcur, (size_t)std::max<uint64_t>(tot[2], 1) * 4));
-        k_tct_level<true, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, lb, nlb,
-                                                             ctx->theta, nullptr, nullptr, nullptr, om, op, od,
-                                                             P_<uint32_t>(ctx->m2l_src), P_<uint32_t>(ctx->p2p_src),
-                                                             P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf, nullptr, 0);
+        if (slab) {
+            k_slab_gather<<<(unsigned)std::min<int64_t>((nt + 7) / 8, grid_max), 256, 0, s>>>(
+                nt, ovf, cm, cp, cd, om, op, od, slabM, slabP, slabD, capM, capP, capD, P_<uint32_t>(ctx->m2l_src),
+                P_<uint32_t>(ctx->p2p_src), P_<uint32_t>(*dcur));
+        } else {
+            k_tct_level<1, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, lb, nlb,
+                                                              ctx->theta, nullptr, nullptr, nullptr, om, op, od,
+                                                              P_<uint32_t>(ctx->m2l_src), P_<uint32_t>(ctx->p2p_src),
+                                                              P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf, nullptr, 0, 0,
+                                                              0, 0);
+        }
         FMM_LAUNCH(ctx);
-        if (novf) {
-            k_tct_level<true, true><<<TC_GWARPS / TC_WARPS, TC_WARPS * 32, 0, s>>>(
+        {
+            k_tct_level<1, true><<<TC_GWARPS / TC_WARPS, TC_WARPS * 32, 0, s>>>(
                 tb, te, par, pb, doff_prev, dsrc_prev, v, lb, nlb, ctx->theta, nullptr, nullptr, nullptr, om, op, od,
                 P_<uint32_t>(ctx->m2l_src), P_<uint32_t>(ctx->p2p_src), P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf,
-                P_<uint32_t>(ctx->tc_glob), gcap);
+                P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0);
             FMM_LAUNCH(ctx);
         }
         baseM = needM;
         baseP = needP;
-        // this level's pass-down offsets become the next level's input (od holds nt + 1 entries)
-        FMM_TRY(buf_ensure(ctx, ctx->tc_doff[l & 1], (size_t)(nt + 1) * 8));
-        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->tc_doff[l & 1].p, od, (size_t)(nt + 1) * 8, cudaMemcpyDeviceToDevice, s));
-        doff_prev = P_<uint64_t>(ctx->tc_doff[l & 1]);
+        // this level's pass-down offsets (od, nt + 1 entries) are the next level's input
+        doff_prev = od;
         pb = tb;
         std::swap(dprev, dcur);
     }
+    ctx->tc_max = maxc;
     const uint64_t ends[2] = {baseM, baseP};
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<uint64_t>(ctx->m2l_off) + nc, &ends[0], 8, cudaMemcpyHostToDevice, s));
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<uint64_t>(ctx->p2p_off) + nc, &ends[1], 8, cudaMemcpyHostToDevice, s));
