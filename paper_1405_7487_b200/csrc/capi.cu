@@ -390,12 +390,19 @@ fmm_status fmm_solve(fmm_ctx* ctx, const void* pos, const void* q, int64_t n, vo
     FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
     FMM_TRY(gather_bodies_q(ctx, q, ctx->aux));
     FMM_TRY(upward_pass(ctx, ctx->aux));
+    ctx->m2l_part = 1;   // the M2L operand (fp32 folded copy of M) is prepared there too
+    fmm_status st = m2l_pass(ctx, ctx->aux);
+    ctx->m2l_part = 0;
+    FMM_TRY(st);
     FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_up, ctx->aux));
     FMM_TRY(fmm_dtt(ctx, 0, m));
     FMM_TRY(fmm_lists(ctx, m));
     FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(m, ctx->ev_up, 0));
     ctx->upward_done = true;
-    FMM_TRY(fmm_interact(ctx, phi, grad, m));
+    ctx->m2l_part = 2;
+    st = fmm_interact(ctx, phi, grad, m);
+    ctx->m2l_part = 0;
+    FMM_TRY(st);
     if (m != s) {
         FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_done, m));
         FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_done, 0));

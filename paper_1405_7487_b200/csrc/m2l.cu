@@ -109,6 +109,7 @@ fmm_status m2l_pass(fmm_ctx* ctx, cudaStream_t s) {
     PhaseScope ps(ctx, PH_M2L, s);
     FMM_TRY(buf_ensure(ctx, ctx->L, (size_t)ctx->ncell * ctx->ncoef * 8));
     if (ctx->use_fast_m2l && m2l_fast_available(ctx->P, ctx->prec)) return m2l_fast(ctx, s);
+    if (ctx->m2l_part == 1) return FMM_OK;   // the generic kernel has no operand preparation
     // cells without M2L sources still need L = 0 (the generic kernel skips them)
     FMM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->L.p, 0, (size_t)ctx->ncell * ctx->ncoef * 8, s));
     PhaseScope pk(ctx, PH_M2L_KERNEL, s);

@@ -398,7 +398,7 @@ fmm_status m2l_fast_t(fmm_ctx* ctx, cudaStream_t s) {
         ctx->fold_P = P;
         ctx->fold_nt = (int64_t)nt;
     }
-    {
+    if (ctx->m2l_part != 2) {
         char* b = (char*)ctx->fold_tab.p;
         const size_t nt = (size_t)ctx->fold_nt;
         k_m2l_prep_table<R><<<std::max(gp, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
@@ -406,8 +406,9 @@ fmm_status m2l_fast_t(fmm_ctx* ctx, cudaStream_t s) {
             reinterpret_cast<const int*>(b + nt * 8 + (2 * NSP + 1) * 4), reinterpret_cast<const double*>(b),
             reinterpret_cast<const int*>(b + nt * 8 + (NSP + 1) * 4), P_<double>(ctx->M), P_<int32_t>(ctx->c_level),
             P_<double>(ctx->root), sexp, Sv);
+        FMM_LAUNCH(ctx);
     }
-    FMM_LAUNCH(ctx);
+    if (ctx->m2l_part == 1) return FMM_OK;
     unsigned long long* counter = P_<unsigned long long>(ctx->cnt_tmp);
     FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 8, s));
     {
@@ -829,7 +830,7 @@ fmm_status m2l_mir_t(fmm_ctx* ctx, cudaStream_t s) {
         ctx->fold_P = 1000 + P;
         ctx->fold_nt = (int64_t)nt;
     }
-    {
+    if (ctx->m2l_part != 2) {
         char* b = (char*)ctx->fold_tab.p;
         const size_t nt = (size_t)ctx->fold_nt;
         k_m2l_prep_table<float><<<std::max(gp, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
@@ -839,6 +840,7 @@ fmm_status m2l_mir_t(fmm_ctx* ctx, cudaStream_t s) {
             P_<double>(ctx->root), sexp, Sv);
         FMM_LAUNCH(ctx);
     }
+    if (ctx->m2l_part == 1) return FMM_OK;   // operand preparation only (fmm_solve: aux stream)
     unsigned long long* counter = P_<unsigned long long>(ctx->cnt_tmp);
     FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 8, s));
     {
