@@ -164,7 +164,12 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
                       &ctx->far, &ctx->h_stage};
     for (DevBuf* b : bufs) buf_free(*b);
     DevBuf* tbufs[] = {&ctx->tc_cnt, &ctx->tc_lb, &ctx->tc_d[0], &ctx->tc_d[1], &ctx->tc_doff[0],
-                       &ctx->tc_doff[1], &ctx->tc_glob, &ctx->tc_slab, &ctx->tc_bsum};
+                       &ctx->tc_doff[1], &ctx->tc_glob, &ctx->tc_slab, &ctx->tc_bsum, &ctx->tc_cat_off,
+                       &ctx->tc_cat_src};
+    for (auto& pt : ctx->tc_rem) {
+        DevBuf* pb[] = {&pt.off_m, &pt.src_m, &pt.off_p, &pt.src_p};
+        for (DevBuf* b : pb) buf_free(*b);
+    }
     for (DevBuf* b : tbufs) buf_free(*b);
     DevBuf* lbufs[] = {&ctx->let_tmp, &ctx->let_cov, &ctx->c_orig, &ctx->part_tmp, &ctx->seg_lists, &ctx->orb_tmp, &ctx->root_given, &ctx->fold_tab, &ctx->leaf_cls, &ctx->dtt_lvl};
     for (DevBuf* b : lbufs) buf_free(*b);
@@ -204,6 +209,7 @@ fmm_status fmm_build_tree(fmm_ctx* ctx, const void* pos, int64_t n, void* stream
     cudaStream_t s = (cudaStream_t)stream;
     ctx->built = ctx->tree_built = false;
     ctx->lists_csr = false;
+    ctx->tc_nrem = 0;
     ctx->evaluated = ctx->upward_done = false;
     ctx->n = n;
     ctx->built_pos = pos;
@@ -256,8 +262,16 @@ fmm_status fmm_dtt(fmm_ctx* ctx, int remote, void* stream) {
         const uint64_t root_pair = 0;
         return dtt_pass(ctx, &root_pair, 1, false, s, -1);
     }
-    // remote traversals append packed pairs to the local lists
-    if (ctx->lists_csr) FMM_TRY(lists_csr_to_packed(ctx, s));
+    if (ctx->lists_csr) {
+        // target-ordered: one more CSR part per batch of grafted LETs (concatenated by fmm_lists)
+        std::vector<uint32_t> roots;
+        for (size_t k = ctx->let_traversed; k < ctx->let_remote.size(); ++k)
+            if (ctx->let_remote[k].ncell > 0) roots.push_back((uint32_t)ctx->let_remote[k].base);
+        ctx->let_traversed = ctx->let_remote.size();
+        if (roots.empty()) return FMM_OK;
+        PhaseScope ps(ctx, PH_DTT, s);
+        return tct_remote(ctx, roots, s);
+    }
     // (local root 0, remote root) of every LET grafted since the last remote traversal
     std::vector<uint64_t> seeds;
     int dmax = 0;

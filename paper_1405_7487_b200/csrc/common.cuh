@@ -69,6 +69,23 @@ struct LetRemote {
     int depth;   // deepest level of the sender's tree (bounds the traversal's level count)
 };
 
+// CSR lists written by the target-ordered traversal (tct.cu)
+struct TcLists {
+    DevBuf* off_m;
+    DevBuf* src_m;
+    DevBuf* off_p;
+    DevBuf* src_p;
+    int64_t* n_m;
+    int64_t* n_p;
+    int64_t* est_m;   // capacity estimates for the next run
+    int64_t* est_p;
+};
+// one remote (LET) traversal's lists, concatenated after the local ones by tct_concat
+struct TcPart {
+    DevBuf off_m, src_m, off_p, src_p;
+    int64_t n_m = 0, n_p = 0, est_m = 0, est_p = 0;
+};
+
 struct TimedEvent {
     int phase;
     cudaEvent_t a, b;
@@ -142,6 +159,9 @@ struct fmm_ctx {
     // (ping-pong CSR), global split lists of overflowed targets
     DevBuf tc_cnt, tc_lb, tc_d[2], tc_doff[2], tc_glob, tc_slab, tc_bsum;
     std::vector<std::array<uint32_t, 3>> tc_max;   // per-level max list lengths of the last build
+    std::vector<TcPart> tc_rem;                     // remote traversal parts (buffers reused)
+    int tc_nrem = 0;                                // parts written since the last fmm_lists
+    DevBuf tc_cat_off, tc_cat_src;                  // concatenation output (swapped with the lists)
     bool tc_single = true;      // single pass into slots sized from tc_max (FMM_TCT_SINGLE=0: count + emit)
     int64_t tc_est_m2l = 0, tc_est_p2p = 0;
     bool lists_csr = false;     // lists came from tct (CSR only; no packed pair list)
@@ -250,8 +270,12 @@ fmm_status build_tree(fmm_ctx* ctx, cudaStream_t s);
 fmm_status dtt_pass(fmm_ctx* ctx, const uint64_t* seeds, int nseeds, bool append, cudaStream_t s,
                     int max_depth_src = -1);
 fmm_status lists_pass(fmm_ctx* ctx, cudaStream_t s);
-// tct.cu: target-ordered traversal writing the CSR lists directly (local traversal only)
+// tct.cu: target-ordered traversal writing the CSR lists directly: the local traversal, a
+// remote one from the given grafted LET roots (one more part), and the per-target concatenation
+// of the local lists with the remote parts
 fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s);
+fmm_status tct_remote(fmm_ctx* ctx, const std::vector<uint32_t>& roots, cudaStream_t s);
+fmm_status tct_concat(fmm_ctx* ctx, cudaStream_t s);
 // dtt.cu: CSR lists -> packed (target << 32 | source) pairs, so remote traversals can append
 fmm_status lists_csr_to_packed(fmm_ctx* ctx, cudaStream_t s);
 // dtt.cu: P2P interaction count and source runs of the CSR lists (synchronises s)

@@ -933,7 +933,8 @@ fmm_status lists_pass(fmm_ctx* ctx, cudaStream_t s) {
     // segments only when canonical device order is requested (fmm_copy_lists sorts on the
     // host otherwise; the set and the grouping by target are the same either way).
     if (ctx->lists_csr) {
-        // the target-ordered traversal wrote the CSR lists
+        // the target-ordered traversal wrote the CSR lists (+ remote parts to concatenate)
+        if (ctx->tc_nrem > 0) FMM_TRY(tct_concat(ctx, s));
     } else if (ctx->list_sort == 1 && ctx->canonical_m2l) {
         FMM_TRY(canonicalise_sorted(ctx, ctx->lst_m2l, ctx->n_m2l, ctx->m2l_off, ctx->m2l_src, s));
         FMM_TRY(canonicalise_sorted(ctx, ctx->lst_p2p, ctx->n_p2p, ctx->p2p_off, ctx->p2p_src, s));

@@ -46,6 +46,11 @@ __device__ __forceinline__ int tc_classify(const double4 T, uint32_t nT, const C
     return 3;
 }
 
+__global__ void k_widen_u32_tc(const uint32_t* __restrict__ in, int64_t n, uint64_t* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = in[i];
+}
+
 struct TcOut {   // per-target output cursors (warp-uniform)
     uint32_t m, p, d;
 };
@@ -58,17 +63,15 @@ struct TcOut {   // per-target output cursors (warp-uniform)
 template <int MODE, bool GLOB>
 __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
     int64_t tb, int64_t te, const int32_t* __restrict__ parent, int64_t pb, const uint64_t* __restrict__ doff_prev,
-    const uint32_t* __restrict__ dsrc_prev, Cells v, const int64_t* __restrict__ lb_dev, int nlb, double theta,
+    const uint32_t* __restrict__ dsrc_prev, Cells v, const uint32_t* __restrict__ seeds, int nseeds, double theta,
     uint32_t* __restrict__ cnt_m, uint32_t* __restrict__ cnt_p, uint32_t* __restrict__ cnt_d,
     const uint64_t* __restrict__ offM, const uint64_t* __restrict__ offP, const uint64_t* __restrict__ offD,
     uint32_t* __restrict__ srcM, uint32_t* __restrict__ srcP, uint32_t* __restrict__ dsrc,
     uint8_t* __restrict__ ovf, uint32_t* __restrict__ ovf_list, unsigned* __restrict__ n_ovf,
-    uint32_t* __restrict__ gscratch, int64_t gcap, uint32_t capM, uint32_t capP, uint32_t capD) {
+    uint32_t* __restrict__ gscratch, int64_t gcap, uint32_t capM, uint32_t capP, uint32_t capD,
+    unsigned* __restrict__ err) {
     constexpr bool EMIT = MODE != 0, COUNT = MODE != 1, SLAB = MODE == 2;
     __shared__ uint32_t s_sb[GLOB ? 1 : TC_WARPS][2][GLOB ? 1 : TC_CAP];
-    __shared__ int64_t s_lb[FMM_MAXLEVEL + 3];
-    for (int i = threadIdx.x; i < nlb; i += blockDim.x) s_lb[i] = lb_dev[i];
-    __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const int64_t nwarps = (int64_t)gridDim.x * TC_WARPS;
@@ -91,7 +94,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
         if (!GLOB && MODE == 1 && ovf[t - tb]) continue;   // done by the global-memory kernel
         const double4 T = v.cr[t];
         const uint32_t nT = v.cc[t];
-        uint64_t x0 = 0, x1 = 1;   // root: the root is its only source
+        uint64_t x0 = 0, x1 = (uint64_t)nseeds;   // root targets: the seed sources
         if (doff_prev) {
             const int64_t pi = (int64_t)parent[t] - pb;
             x0 = doff_prev[pi];
@@ -138,32 +141,31 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
             o.d += __popc(bd);
             nnext += __popc(bs);
         };
-        for (int lam = 0; lam <= FMM_MAXLEVEL && (xp < x1 || ncur > 0); ++lam) {
-            const int64_t lend = lam + 1 < nlb ? s_lb[lam + 1] : INT64_MAX;
+        // generation 0: the sources the parent passed down (the root: the seeds), in order
+        for (int gen = 0; gen == 0 || ncur > 0; ++gen) {
             uint32_t* nxt = cur ? list0 : list1;
             uint32_t nnext = 0;
-            // sources passed down by the parent at this level (a prefix of the rest: D is
-            // ordered by level)
-            while (xp < x1) {
+            for (; gen == 0 && xp < x1; xp += 32) {
                 const uint64_t i = xp + (uint64_t)lane;
-                const uint32_t s = i < x1 ? (doff_prev ? dsrc_prev[i] : 0u) : 0xffffffffu;
-                const bool act = i < x1 && (int64_t)s < lend;
-                const unsigned am = __ballot_sync(0xffffffffu, act);
-                if (!am) break;
+                const bool act = i < x1;
+                const uint32_t s = act ? (doff_prev ? dsrc_prev[i] : seeds[i]) : 0u;
                 const int oc = act ? tc_classify(T, nT, v, s, theta) : -1;
                 put(oc, s, act, nxt, nnext);
-                xp += (uint64_t)__popc(am);
-                if (am != 0xffffffffu) break;   // the level's entries ended inside this chunk
             }
-            // children of this target's split sources of the previous level, in (source, child)
-            // order, flattened over the lanes: a round of 32 split sources is expanded into its
+            // generation g >= 1: the children of the sources generation g-1 split, in (source,
+            // child) order, flattened over the lanes: a round of 32 split sources is expanded into its
             // children (prefix sum of the child counts), and each lane classifies one child per
             // step -- every step issues 32 independent cell loads
             const uint32_t* sb = cur ? list1 : list0;
             for (uint32_t base = 0; base < ncur; base += 32) {
                 const bool has = base + lane < ncur;
                 const uint32_t B = has ? sb[base + lane] : 0u;
-                const uint32_t c0 = has ? v.cb[B] : 0u, nc = has ? v.cc[B] : 0u;
+                uint32_t c0 = has ? v.cb[B] : 0u, nc = has ? v.cc[B] : 0u;
+                if (c0 == FMM_LET_ABSENT) {   // a grafted LET cell whose children were not exported
+                    atomicOr(err, 1u);
+                    c0 = 0u;
+                    nc = 0u;
+                }
                 uint32_t incl = nc;   // inclusive scan of the child counts
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {
@@ -348,19 +350,20 @@ __global__ void k_max3(const uint32_t* __restrict__ a, const uint32_t* __restric
 
 }  // namespace
 
-// Builds m2l_off/src and p2p_off/src (CSR, deterministic order) for the local traversal.
-fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s) {
+// One target-ordered traversal of the local target tree from the given seed sources at the root
+// (local: the root itself; remote: the roots of grafted LETs) into the CSR lists `o`.
+fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& seeds, TcLists& o, bool single,
+                   std::vector<std::array<uint32_t, 3>>& tc_max) {
     const int64_t nc = ctx->ncell;
     const int nlev = (int)ctx->depth + 1;
-    const int nlb = (int)ctx->level_begin.size();
     const Cells v{P_<double4>(ctx->c_cr), P_<uint32_t>(ctx->c_cb), P_<uint32_t>(ctx->c_cc)};
     int64_t maxw = 1;
     for (int l = 0; l < nlev; ++l) maxw = std::max(maxw, ctx->level_begin[l + 1] - ctx->level_begin[l]);
-    FMM_TRY(buf_ensure(ctx, ctx->m2l_off, (size_t)(nc + 1) * 8));
-    FMM_TRY(buf_ensure(ctx, ctx->p2p_off, (size_t)(nc + 1) * 8));
+    FMM_TRY(buf_ensure(ctx, *o.off_m, (size_t)(nc + 1) * 8));
+    FMM_TRY(buf_ensure(ctx, *o.off_p, (size_t)(nc + 1) * 8));
     // per-level scratch: counts (3 x u32), overflow flags (u8) and list (u32)
     FMM_TRY(buf_ensure(ctx, ctx->tc_cnt, (size_t)maxw * 12 + (size_t)maxw * 5 + 256));
-    FMM_TRY(buf_ensure(ctx, ctx->tc_lb, (size_t)nlb * 8 + 64));
+    FMM_TRY(buf_ensure(ctx, ctx->tc_lb, seeds.size() * 4 + 64));
     FMM_TRY(buf_ensure(ctx, ctx->dcount2, 128));
     uint32_t* cm = P_<uint32_t>(ctx->tc_cnt);
     uint32_t* cp = cm + maxw;
@@ -368,11 +371,14 @@ fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s) {
     uint32_t* ovf_list = cd + maxw;
     uint8_t* ovf = reinterpret_cast<uint8_t*>(ovf_list + maxw);
     unsigned* n_ovf = P_<unsigned>(ctx->dcount2) + 24;
-    int64_t* lb = P_<int64_t>(ctx->tc_lb);
-    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(lb, ctx->level_begin.data(), (size_t)nlb * 8, cudaMemcpyHostToDevice, s));
+    uint32_t* d_seeds = P_<uint32_t>(ctx->tc_lb);
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(d_seeds, seeds.data(), seeds.size() * 4, cudaMemcpyHostToDevice, s));
+    const int nseeds = (int)seeds.size();
+    unsigned* d_err = P_<unsigned>(ctx->dcount2) + 30;
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_err, 0, 4, s));
     // output capacities from the previous build (grown on demand, keeping what is written)
-    FMM_TRY(buf_ensure(ctx, ctx->m2l_src, (size_t)std::max<int64_t>(ctx->tc_est_m2l, 1024) * 4));
-    FMM_TRY(buf_ensure(ctx, ctx->p2p_src, (size_t)std::max<int64_t>(ctx->tc_est_p2p, 1024) * 4));
+    FMM_TRY(buf_ensure(ctx, *o.src_m, (size_t)std::max<int64_t>(*o.est_m, 1024) * 4));
+    FMM_TRY(buf_ensure(ctx, *o.src_p, (size_t)std::max<int64_t>(*o.est_p, 1024) * 4));
     uint64_t baseM = 0, baseP = 0;
     DevBuf* dprev = &ctx->tc_d[0];
     DevBuf* dcur = &ctx->tc_d[1];
@@ -392,13 +398,13 @@ fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s) {
         const uint32_t* dsrc_prev = doff_prev ? P_<uint32_t>(*dprev) : nullptr;
         // single pass into per-target slots sized from the previous build's per-level maxima
         // (first build, or slots over budget: count pass + emit pass)
-        bool slab = ctx->tc_single && l < (int)ctx->tc_max.size();
+        bool slab = single && l < (int)tc_max.size();
         uint32_t capM = 0, capP = 0, capD = 0;
         if (slab) {
             auto cap = [](uint32_t m) { return (m + m / 4 + 32 + 31) & ~31u; };
-            capM = cap(ctx->tc_max[l][0]);
-            capP = cap(ctx->tc_max[l][1]);
-            capD = cap(ctx->tc_max[l][2]);
+            capM = cap(tc_max[l][0]);
+            capP = cap(tc_max[l][1]);
+            capD = cap(tc_max[l][2]);
             const size_t bytes = (size_t)nt * (capM + capP + capD) * 4;
             if (bytes > ((size_t)4 << 30)) slab = false;
             else FMM_TRY(buf_ensure(ctx, ctx->tc_slab, bytes + 64));
@@ -409,28 +415,28 @@ fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s) {
         FMM_CUDA_TRY(ctx, cudaMemsetAsync(ovf, 0, (size_t)nt, s));
         FMM_CUDA_TRY(ctx, cudaMemsetAsync(n_ovf, 0, 20, s));
         if (slab)
-            k_tct_level<2, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, lb, nlb,
+            k_tct_level<2, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds,
                                                               ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr, slabM,
                                                               slabP, slabD, ovf, ovf_list, n_ovf, nullptr, 0, capM,
-                                                              capP, capD);
+                                                              capP, capD, d_err);
         else
-            k_tct_level<0, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, lb, nlb,
+            k_tct_level<0, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds,
                                                               ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr,
                                                               nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, nullptr,
-                                                              0, 0, 0, 0);
+                                                              0, 0, 0, 0, d_err);
         FMM_LAUNCH(ctx);
         // overflowed targets (count read on the device: a no-op launch when there are none)
         const int64_t gcap = maxw;   // a split list never exceeds one tree level
         {
             k_tct_level<0, true><<<TC_GWARPS / TC_WARPS, TC_WARPS * 32, 0, s>>>(
-                tb, te, par, pb, doff_prev, dsrc_prev, v, lb, nlb, ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr,
-                nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0);
+                tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds, ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr,
+                nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err);
             FMM_LAUNCH(ctx);
         }
         // offsets written straight into m2l_off / p2p_off (+ the entries of earlier levels) and
         // the pass-down CSR of this level
-        uint64_t* om = P_<uint64_t>(ctx->m2l_off) + tb;
-        uint64_t* op = P_<uint64_t>(ctx->p2p_off) + tb;
+        uint64_t* om = P_<uint64_t>(*o.off_m) + tb;
+        uint64_t* op = P_<uint64_t>(*o.off_p) + tb;
         FMM_TRY(buf_ensure(ctx, ctx->tc_doff[l & 1], (size_t)(nt + 1) * 8));
         uint64_t* od = P_<uint64_t>(ctx->tc_doff[l & 1]);
         const int64_t nb = (nt + S3_TILE - 1) / S3_TILE;
@@ -446,26 +452,26 @@ fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s) {
         FMM_CUDA_TRY(ctx, cudaMemcpyAsync(maxc[l].data(), mx, 12, cudaMemcpyDeviceToHost, s));
         FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
         const uint64_t needM = baseM + tot[0], needP = baseP + tot[1];
-        if (needM * 4 > ctx->m2l_src.bytes) FMM_TRY(buf_ensure(ctx, ctx->m2l_src, (size_t)(needM + needM / 4) * 4, true, s));
-        if (needP * 4 > ctx->p2p_src.bytes) FMM_TRY(buf_ensure(ctx, ctx->p2p_src, (size_t)(needP + needP / 4) * 4, true, s));
+        if (needM * 4 > o.src_m->bytes) FMM_TRY(buf_ensure(ctx, *o.src_m, (size_t)(needM + needM / 4) * 4, true, s));
+        if (needP * 4 > o.src_p->bytes) FMM_TRY(buf_ensure(ctx, *o.src_p, (size_t)(needP + needP / 4) * 4, true, s));
         FMM_TRY(buf_ensure(ctx, *dcur, (size_t)std::max<uint64_t>(tot[2], 1) * 4));
         if (slab) {
             k_slab_gather<<<(unsigned)std::min<int64_t>((nt + 7) / 8, grid_max), 256, 0, s>>>(
-                nt, ovf, cm, cp, cd, om, op, od, slabM, slabP, slabD, capM, capP, capD, P_<uint32_t>(ctx->m2l_src),
-                P_<uint32_t>(ctx->p2p_src), P_<uint32_t>(*dcur));
+                nt, ovf, cm, cp, cd, om, op, od, slabM, slabP, slabD, capM, capP, capD, P_<uint32_t>(*o.src_m),
+                P_<uint32_t>(*o.src_p), P_<uint32_t>(*dcur));
         } else {
-            k_tct_level<1, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, lb, nlb,
+            k_tct_level<1, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds,
                                                               ctx->theta, nullptr, nullptr, nullptr, om, op, od,
-                                                              P_<uint32_t>(ctx->m2l_src), P_<uint32_t>(ctx->p2p_src),
+                                                              P_<uint32_t>(*o.src_m), P_<uint32_t>(*o.src_p),
                                                               P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf, nullptr, 0, 0,
-                                                              0, 0);
+                                                              0, 0, d_err);
         }
         FMM_LAUNCH(ctx);
         {
             k_tct_level<1, true><<<TC_GWARPS / TC_WARPS, TC_WARPS * 32, 0, s>>>(
-                tb, te, par, pb, doff_prev, dsrc_prev, v, lb, nlb, ctx->theta, nullptr, nullptr, nullptr, om, op, od,
-                P_<uint32_t>(ctx->m2l_src), P_<uint32_t>(ctx->p2p_src), P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf,
-                P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0);
+                tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds, ctx->theta, nullptr, nullptr, nullptr, om, op, od,
+                P_<uint32_t>(*o.src_m), P_<uint32_t>(*o.src_p), P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf,
+                P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err);
             FMM_LAUNCH(ctx);
         }
         baseM = needM;
@@ -475,15 +481,122 @@ fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s) {
         pb = tb;
         std::swap(dprev, dcur);
     }
-    ctx->tc_max = maxc;
+    tc_max = maxc;
     const uint64_t ends[2] = {baseM, baseP};
-    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<uint64_t>(ctx->m2l_off) + nc, &ends[0], 8, cudaMemcpyHostToDevice, s));
-    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<uint64_t>(ctx->p2p_off) + nc, &ends[1], 8, cudaMemcpyHostToDevice, s));
+    unsigned herr = 0;
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<uint64_t>(*o.off_m) + nc, &ends[0], 8, cudaMemcpyHostToDevice, s));
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<uint64_t>(*o.off_p) + nc, &ends[1], 8, cudaMemcpyHostToDevice, s));
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, s));
     FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));   // ends[] lives on this stack frame
     FMM_CUDA_TRY(ctx, cudaGetLastError());
-    ctx->n_m2l = (int64_t)baseM;
-    ctx->n_p2p = (int64_t)baseP;
-    ctx->tc_est_m2l = (int64_t)(baseM + baseM / 8 + 1024);
-    ctx->tc_est_p2p = (int64_t)(baseP + baseP / 8 + 1024);
+    if (herr) {
+        ctx->err = "dual tree traversal needed children of a remote LET cell that were not exported";
+        return FMM_ERR_STATE;
+    }
+    *o.n_m = (int64_t)baseM;
+    *o.n_p = (int64_t)baseP;
+    *o.est_m = (int64_t)(baseM + baseM / 8 + 1024);
+    *o.est_p = (int64_t)(baseP + baseP / 8 + 1024);
+    return FMM_OK;
+}
+
+// local traversal: the root is the only seed; the lists land in the context's CSR arrays
+fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s) {
+    TcLists o{&ctx->m2l_off, &ctx->m2l_src, &ctx->p2p_off, &ctx->p2p_src, &ctx->n_m2l, &ctx->n_p2p,
+              &ctx->tc_est_m2l, &ctx->tc_est_p2p};
+    const std::vector<uint32_t> seeds{0u};
+    return tct_run(ctx, s, seeds, o, ctx->tc_single, ctx->tc_max);
+}
+
+// remote traversal of the LET roots grafted since the last one: one more CSR part
+fmm_status tct_remote(fmm_ctx* ctx, const std::vector<uint32_t>& roots, cudaStream_t s) {
+    if ((int)ctx->tc_rem.size() <= ctx->tc_nrem) ctx->tc_rem.emplace_back();   // buffers kept for reuse
+    TcPart& pt = ctx->tc_rem[ctx->tc_nrem++];
+    TcLists o{&pt.off_m, &pt.src_m, &pt.off_p, &pt.src_p, &pt.n_m, &pt.n_p, &pt.est_m, &pt.est_p};
+    std::vector<std::array<uint32_t, 3>> none;   // count + emit passes (no slot history)
+    return tct_run(ctx, s, roots, o, false, none);
+}
+
+namespace {
+constexpr int CAT_MAX = 8;   // CSR parts concatenated per pass
+struct CatParts {
+    const uint64_t* off[CAT_MAX];
+    const uint32_t* src[CAT_MAX];
+    int n;
+};
+
+__global__ void k_cat_count(int64_t nc, CatParts pa, uint32_t* __restrict__ cnt) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nc; t += stride) {
+        uint64_t c = 0;
+        for (int k = 0; k < pa.n; ++k) c += pa.off[k][t + 1] - pa.off[k][t];
+        cnt[t] = (uint32_t)c;
+    }
+}
+
+__global__ void k_cat_copy(int64_t nc, CatParts pa, const uint64_t* __restrict__ off, uint32_t* __restrict__ src) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nc; t += nw) {
+        uint64_t o = off[t];
+        for (int k = 0; k < pa.n; ++k) {
+            const uint64_t b = pa.off[k][t], e = pa.off[k][t + 1];
+            for (uint64_t p = b + lane; p < e; p += 32) src[o + (p - b)] = pa.src[k][p];
+            o += e - b;
+        }
+    }
+}
+}  // namespace
+
+// lists of the local traversal followed, per target, by each remote part in graft order
+fmm_status tct_concat(fmm_ctx* ctx, cudaStream_t s) {
+    const int64_t nc = ctx->ncell;
+    struct L {
+        DevBuf* off;
+        DevBuf* src;
+        int64_t* n;
+        bool m2l;
+    } lists[2] = {{&ctx->m2l_off, &ctx->m2l_src, &ctx->n_m2l, true}, {&ctx->p2p_off, &ctx->p2p_src, &ctx->n_p2p, false}};
+    FMM_TRY(buf_ensure(ctx, ctx->tc_cnt, (size_t)(nc + 1) * 12 + 256));
+    uint32_t* cnt = P_<uint32_t>(ctx->tc_cnt);
+    FMM_TRY(buf_ensure(ctx, ctx->cnt64, (size_t)(nc + 1) * 8));
+    uint64_t* c64 = P_<uint64_t>(ctx->cnt64);
+    const unsigned g = (unsigned)std::min<int64_t>((nc + 255) / 256, (int64_t)ctx->num_sms * 8);
+    const unsigned gw = (unsigned)std::min<int64_t>((nc + 7) / 8, (int64_t)ctx->num_sms * 8);
+    size_t done = 0;
+    const size_t nparts = (size_t)ctx->tc_nrem;
+    while (done < nparts) {
+        const size_t take = std::min<size_t>(CAT_MAX - 1, nparts - done);
+        for (auto& li : lists) {
+            CatParts pa{};
+            pa.off[0] = P_<uint64_t>(*li.off);
+            pa.src[0] = P_<uint32_t>(*li.src);
+            int64_t total = *li.n;
+            for (size_t k = 0; k < take; ++k) {
+                TcPart& pt = ctx->tc_rem[done + k];
+                pa.off[k + 1] = P_<uint64_t>(li.m2l ? pt.off_m : pt.off_p);
+                pa.src[k + 1] = P_<uint32_t>(li.m2l ? pt.src_m : pt.src_p);
+                total += li.m2l ? pt.n_m : pt.n_p;
+            }
+            pa.n = (int)take + 1;
+            k_cat_count<<<g, 256, 0, s>>>(nc, pa, cnt);
+            FMM_LAUNCH(ctx);
+            DevBuf& noff = ctx->tc_cat_off;
+            DevBuf& nsrc = ctx->tc_cat_src;
+            FMM_TRY(buf_ensure(ctx, noff, (size_t)(nc + 1) * 8));
+            FMM_TRY(buf_ensure(ctx, nsrc, (size_t)std::max<int64_t>(total, 1) * 4));
+            k_widen_u32_tc<<<g, 256, 0, s>>>(cnt, nc, c64);
+            FMM_LAUNCH(ctx);
+            FMM_TRY(scan_exclusive_u64(ctx, c64, P_<uint64_t>(noff), nc, P_<uint64_t>(noff) + nc, s));
+            k_cat_copy<<<gw, 256, 0, s>>>(nc, pa, P_<uint64_t>(noff), P_<uint32_t>(nsrc));
+            FMM_LAUNCH(ctx);
+            std::swap(*li.off, noff);
+            std::swap(*li.src, nsrc);
+            *li.n = total;
+        }
+        done += take;
+    }
+    FMM_CUDA_TRY(ctx, cudaGetLastError());
+    ctx->tc_nrem = 0;
     return FMM_OK;
 }
