@@ -124,6 +124,8 @@ fmm_status fmm_create(int64_t n_max, int p, double theta, int ncrit, int prec, i
         ctx->canonical_m2l = !(g5 && g5[0] == '0');
         const char* g16 = getenv("FMM_TCT_SINGLE");
         ctx->tc_single = !(g16 && g16[0] == '0');
+        const char* g17 = getenv("FMM_TCT_CAP");
+        ctx->tc_scap = g17 ? atoi(g17) : 0;
         const char* g15 = getenv("FMM_DTT");
         ctx->dtt_mode = (g15 && std::string(g15) == "bfs") ? 1 : 0;
         const char* g7 = getenv("FMM_LIST_SORT");

@@ -161,6 +161,7 @@ struct fmm_ctx {
     std::vector<std::array<uint32_t, 3>> tc_max;   // per-level max list lengths of the last build
     std::vector<TcPart> tc_rem;                     // remote traversal parts (buffers reused)
     int tc_nrem = 0;                                // parts written since the last fmm_lists
+    int tc_scap = 0;                                // shared split-list capacity override (FMM_TCT_CAP, tests)
     DevBuf tc_cat_off, tc_cat_src;                  // concatenation output (swapped with the lists)
     bool tc_single = true;      // single pass into slots sized from tc_max (FMM_TCT_SINGLE=0: count + emit)
     int64_t tc_est_m2l = 0, tc_est_p2p = 0;

@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
     } else {
         list0 = s_sb[w][0];
         list1 = s_sb[w][GLOB ? 0 : 1];
-        cap = TC_CAP;
+        cap = min((int64_t)TC_CAP, gcap);   // gcap: shared-list cap (tests force overflows with it)
     }
     const int64_t nitems = GLOB ? (int64_t)*n_ovf : te - tb;
     for (int64_t it = gw; it < nitems; it += nwarps) {
@@ -374,6 +374,7 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
     uint32_t* d_seeds = P_<uint32_t>(ctx->tc_lb);
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(d_seeds, seeds.data(), seeds.size() * 4, cudaMemcpyHostToDevice, s));
     const int nseeds = (int)seeds.size();
+    const int64_t scap = ctx->tc_scap > 0 ? ctx->tc_scap : TC_CAP;   // shared split-list capacity
     unsigned* d_err = P_<unsigned>(ctx->dcount2) + 30;
     FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_err, 0, 4, s));
     // output capacities from the previous build (grown on demand, keeping what is written)
@@ -417,13 +418,13 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
         if (slab)
             k_tct_level<2, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds,
                                                               ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr, slabM,
-                                                              slabP, slabD, ovf, ovf_list, n_ovf, nullptr, 0, capM,
+                                                              slabP, slabD, ovf, ovf_list, n_ovf, nullptr, scap, capM,
                                                               capP, capD, d_err);
         else
             k_tct_level<0, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds,
                                                               ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr,
                                                               nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, nullptr,
-                                                              0, 0, 0, 0, d_err);
+                                                              scap, 0, 0, 0, d_err);
         FMM_LAUNCH(ctx);
         // overflowed targets (count read on the device: a no-op launch when there are none)
         const int64_t gcap = maxw;   // a split list never exceeds one tree level
@@ -463,8 +464,8 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
             k_tct_level<1, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds,
                                                               ctx->theta, nullptr, nullptr, nullptr, om, op, od,
                                                               P_<uint32_t>(*o.src_m), P_<uint32_t>(*o.src_p),
-                                                              P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf, nullptr, 0, 0,
-                                                              0, 0, d_err);
+                                                              P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf, nullptr, scap,
+                                                              0, 0, 0, d_err);
         }
         FMM_LAUNCH(ctx);
         {

@@ -223,6 +223,28 @@ def test_target_traversal_equals_bfs(torch_cuda, prec, kind, n, monkeypatch):
     assert oracle.rel_l2(grad_t.cpu().numpy().astype(np.float64), grad_b.cpu().numpy().astype(np.float64)) <= tol
 
 
+@pytest.mark.parametrize("kind", ["plummer", "cube"])
+def test_target_traversal_overflow_paths(torch_cuda, kind, monkeypatch):
+    """Split lists forced over a 4-entry shared capacity (FMM_TCT_CAP=4): most targets take the
+    global-memory overflow kernels, in both the count/emit and the single-pass (slot) modes; the
+    lists and fields are bit-identical to the normal path."""
+    torch = torch_cuda
+    from paper_1405_7487_b200 import FMM
+    pos, q = synth.generate(kind, 20000, 23, np.float64)
+    tp, tq = torch.from_numpy(pos).cuda(), torch.from_numpy(q).cuda()
+    f = FMM(20000, 5, 0.5, 16, "f64")
+    phi_a, grad_a = f.solve(tp, tq)
+    monkeypatch.setenv("FMM_TCT_CAP", "4")
+    g = FMM(20000, 5, 0.5, 16, "f64")
+    for _ in range(2):   # first build: count + emit passes; second: single pass into slots
+        phi_b, grad_b = g.solve(tp, tq)
+        torch.cuda.synchronize()
+        for a, b in zip(f.lists(), g.lists()):
+            np.testing.assert_array_equal(a, b)
+        np.testing.assert_array_equal(phi_a.cpu().numpy(), phi_b.cpu().numpy())
+        np.testing.assert_array_equal(grad_a.cpu().numpy(), grad_b.cpu().numpy())
+
+
 def test_repeat_builds_reuse_context(torch_cuda):
     # ONE context across sizes and distributions: workspace growth, and the back-to-back
     # traversal sized from the previous build (smaller, larger -> overflow fallback, deeper)
