@@ -525,6 +525,98 @@ class DistFMM:
         self.stats["let_data_bytes"] = sum(int(t.numel()) for row in sends for t in row)
         return out
 
+    # 4-6 in one pass (solve): the upward pass runs on a side stream while the covers are
+    # exchanged and the LET structures planned, so each ring message carries structure AND data
+    # (one exchange instead of two) and every fragment is grafted, unpacked and traversed as it
+    # lands; the local traversal overlaps the first ring round
+    def build_evaluate(self, lpos, lq):
+        cm, K, F = self.comm, self.K, self.fmm
+        nl = len(F)
+        dev = lpos[0].device
+        main = torch.cuda.current_stream(dev)
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(dev)
+        side = self._side
+        for f, p in zip(F, lpos):
+            f.set_root_bounds(self.global_bounds if self.partitioner == "morton" else None)
+            f.build_tree(p)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            for i, f in enumerate(F):
+                f.upward(lpos[i], lq[i], stream=side)
+        up_done = side.record_event()
+        cov = []
+        for f in F:
+            c = f.let_cover()
+            t = torch.zeros(1 + 8 * 73, dtype=torch.float64)
+            t[0] = len(c)
+            t[1:1 + c.size] = torch.from_numpy(c.reshape(-1))
+            cov.append(t.to(dev))
+        allcov = cm.allgather(cov)
+        plans, sends = [], []
+        for i, f in enumerate(F):
+            me = cm.ranks[i]
+            row, pl = [], []
+            for j in range(K):
+                if j == me:
+                    row.append(torch.empty(0, dtype=torch.uint8, device=dev))
+                    pl.append((0, 0))
+                    continue
+                cj = allcov[i][j].cpu().numpy()
+                sb, d = f.let_plan(j, cj[1:1 + 8 * int(cj[0])].reshape(-1, 8))
+                buf = torch.empty(sb + d, dtype=torch.uint8, device=dev)   # [structure | data]
+                if sb:
+                    f.let_pack_struct(j, buf[:sb])
+                row.append(buf)
+                pl.append((sb, d))
+            sends.append(row)
+            plans.append(pl)
+        main.wait_event(up_done)
+        for i, f in enumerate(F):
+            me = cm.ranks[i]
+            for j in range(K):
+                sb, d = plans[i][j]
+                if d and j != me:
+                    f.let_pack_data(j, sends[i][j][sb:])
+        szs = cm.alltoallv([[torch.tensor(list(plans[i][j]), dtype=torch.int64, device=dev) for j in range(K)]
+                            for i in range(nl)])
+        rsz = [[tuple(int(x) for x in t.tolist()) for t in szs[i]] for i in range(nl)]
+        me = cm.ranks
+
+        def start(sr):
+            dst = [(me[i] + sr) % K for i in range(nl)]
+            src = [(me[i] - sr) % K for i in range(nl)]
+            return cm.sendrecv([sends[i][dst[i]] for i in range(nl)], dst, src,
+                               [sum(rsz[i][src[i]]) for i in range(nl)], async_op=True), src
+
+        self._peers = [[] for _ in range(nl)]
+        h = start(1) if K > 1 else None
+        for f in F:                       # local traversal overlaps the first ring round
+            f.dtt(remote=False)
+        for sr in range(1, K):
+            hh, src = h
+            recv = hh.wait()
+            if sr + 1 < K:
+                h = start(sr + 1)
+            for i, f in enumerate(F):
+                rsb, _ = rsz[i][src[i]]
+                if rsb > 0:
+                    f.let_graft([recv[i][:rsb]])
+                    f.let_unpack([recv[i][rsb:]], first=len(self._peers[i]))
+                    f.dtt(remote=True)    # traverses only the fragment just grafted
+                    self._peers[i].append(src[i])
+        out = []
+        for i, f in enumerate(F):
+            f.make_lists()
+            n = lpos[i].shape[0]
+            phi = torch.empty(n, dtype=f.dtype, device=dev)
+            grad = torch.empty((n, 3), dtype=f.dtype, device=dev)
+            f.interact(phi, grad)
+            out.append((phi, grad))
+        self.stats["let_struct_bytes"] = sum(p[0] for pl in plans for p in pl)
+        self.stats["let_data_bytes"] = sum(p[1] for pl in plans for p in pl)
+        return out
+
     # 7: results (and the Eq. (1) weights of this step) back to the owners, original order
     def gather_back(self, res, wts, back, packed, cnt, gid_base, n_in):
         cm = self.comm
@@ -557,8 +649,7 @@ class DistFMM:
             t0 = time.perf_counter()
             self.alpha = self.tuner.next_alpha()                 # for this step's weights
         lpos, lq, lgid, back, packed, cnt = self.partition(pos, q, gid_base, w)
-        self.build(lpos)
-        res = self.evaluate(lpos, lq)
+        res = self.build_evaluate(lpos, lq)
         wts = []
         lr = np.zeros(2)
         for f in self.fmm:

@@ -21,9 +21,13 @@ for it in range(3):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     lpos, lq, lgid, back, packed, cnt = D.partition(P_in, Q_in, gb, D.weights)
     torch.cuda.synchronize(); t1 = time.perf_counter()
-    D.build(lpos)
-    torch.cuda.synchronize(); t2 = time.perf_counter()
-    res = D.evaluate(lpos, lq)
+    if len(sys.argv) > 3 and sys.argv[3] == "split":   # the two-exchange flow (build, then evaluate)
+        D.build(lpos)
+        torch.cuda.synchronize(); t2 = time.perf_counter()
+        res = D.evaluate(lpos, lq)
+    else:                                              # solve's flow: one exchange, upward overlapped
+        res = D.build_evaluate(lpos, lq)
+        torch.cuda.synchronize(); t2 = time.perf_counter()
     torch.cuda.synchronize(); t3 = time.perf_counter()
     wts = [f.work(D.c_m2l, D.alpha)[0] for f in D.fmm]
     torch.cuda.synchronize(); t4 = time.perf_counter()
