@@ -527,7 +527,15 @@ fmm_status fmm_solve_host(fmm_ctx* ctx, const void* pos_h, const void* q_h, int6
     {
         PhaseScope ps(ctx, PH_COPY, s);
         if (n) FMM_CUDA_TRY(ctx, cudaMemcpyAsync(dpos, pos_h, bpos, cudaMemcpyHostToDevice, s));
-        if (n) FMM_CUDA_TRY(ctx, cudaMemcpyAsync(dq, q_h, bq, cudaMemcpyHostToDevice, s));
+        if (n && ctx->overlap) {
+            // q is first needed by P2M on the aux stream: copy it there, behind the caller's
+            // earlier work, while the tree is built from the positions
+            FMM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
+            FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+            FMM_CUDA_TRY(ctx, cudaMemcpyAsync(dq, q_h, bq, cudaMemcpyHostToDevice, ctx->aux));
+        } else if (n) {
+            FMM_CUDA_TRY(ctx, cudaMemcpyAsync(dq, q_h, bq, cudaMemcpyHostToDevice, s));
+        }
     }
     FMM_TRY(fmm_solve(ctx, dpos, dq, n, dphi, dgrad, stream));
     {
