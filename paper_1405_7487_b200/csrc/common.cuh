@@ -159,9 +159,12 @@ struct fmm_ctx {
     // (ping-pong CSR), global split lists of overflowed targets
     DevBuf tc_cnt, tc_lb, tc_d[2], tc_doff[2], tc_glob, tc_slab, tc_bsum;
     std::vector<std::array<uint32_t, 3>> tc_max;   // per-level max list lengths of the last build
+    std::vector<std::array<uint64_t, 3>> tc_tot;   // per-level list totals of the last build
+    DevBuf tc_rec;                                  // per-level device records (bases, totals, maxima)
     std::vector<TcPart> tc_rem;                     // remote traversal parts (buffers reused)
     int tc_nrem = 0;                                // parts written since the last fmm_lists
     int tc_scap = 0;                                // shared split-list capacity override (FMM_TCT_CAP, tests)
+    bool tc_tight = false;                          // fast mode treats outputs as 16 entries (FMM_TCT_TIGHT, tests)
     DevBuf tc_cat_off, tc_cat_src;                  // concatenation output (swapped with the lists)
     bool tc_single = true;      // single pass into slots sized from tc_max (FMM_TCT_SINGLE=0: count + emit)
     int64_t tc_est_m2l = 0, tc_est_p2p = 0;

@@ -69,8 +69,11 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
     uint32_t* __restrict__ srcM, uint32_t* __restrict__ srcP, uint32_t* __restrict__ dsrc,
     uint8_t* __restrict__ ovf, uint32_t* __restrict__ ovf_list, unsigned* __restrict__ n_ovf,
     uint32_t* __restrict__ gscratch, int64_t gcap, uint32_t capM, uint32_t capP, uint32_t capD,
-    unsigned* __restrict__ err) {
+    unsigned* __restrict__ err, uint64_t lenM = ~0ull, uint64_t lenP = ~0ull, uint64_t lenD = ~0ull) {
     constexpr bool EMIT = MODE != 0, COUNT = MODE != 1, SLAB = MODE == 2;
+    // an earlier level outgrew the buffers sized from the previous build: the traversal is
+    // redone, so stop here instead of reading incomplete pass-down sets
+    if (*reinterpret_cast<volatile unsigned*>(err) & 2u) return;
     __shared__ uint32_t s_sb[GLOB ? 1 : TC_WARPS][2][GLOB ? 1 : TC_CAP];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
@@ -101,6 +104,11 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
             x1 = doff_prev[pi + 1];
         }
         uint64_t oM = 0, oP = 0, oD = 0;
+        if (MODE == 1 && (offM[t - tb] + cnt_m[t - tb] > lenM || offP[t - tb] + cnt_p[t - tb] > lenP ||
+                          offD[t - tb] + cnt_d[t - tb] > lenD)) {   // outputs sized from the previous build
+            if (lane == 0) atomicOr(err, 2u);
+            continue;
+        }
         if (SLAB) {
             oM = (uint64_t)(t - tb) * capM;
             oP = (uint64_t)(t - tb) * capP;
@@ -276,7 +284,9 @@ __global__ void __launch_bounds__(S3_THREADS) k_scan3_tiles(const uint32_t* __re
 
 // one block: exclusive scan of the tile sums of each list in place; totals to tot[a]
 __global__ void __launch_bounds__(S3_THREADS) k_scan3_top(uint64_t* __restrict__ bsum, int64_t nb,
-                                                         unsigned long long* __restrict__ tot) {
+                                                         unsigned long long* __restrict__ tot,
+                                                         const uint64_t* __restrict__ base_in,
+                                                         uint64_t* __restrict__ base_out) {
     __shared__ unsigned long long s_w[S3_THREADS / 32];
     for (int a = 0; a < 3; ++a) {
         uint64_t* b = bsum + (int64_t)a * nb;
@@ -289,13 +299,17 @@ __global__ void __launch_bounds__(S3_THREADS) k_scan3_top(uint64_t* __restrict__
             if (i < nb) b[i] = carry + e;
             carry += t;
         }
-        if (threadIdx.x == 0) tot[a] = carry;
+        if (threadIdx.x == 0) {
+            tot[a] = carry;
+            if (a < 2) base_out[a] = base_in[a] + carry;   // entries up to the end of this level
+        }
     }
 }
 
 __global__ void k_scan3_add(int64_t n, uint64_t* __restrict__ o0, uint64_t* __restrict__ o1, uint64_t* __restrict__ o2,
-                            const uint64_t* __restrict__ bsum, int64_t nb, uint64_t base0, uint64_t base1,
+                            const uint64_t* __restrict__ bsum, int64_t nb, const uint64_t* __restrict__ base,
                             const unsigned long long* __restrict__ tot) {
+    const uint64_t base0 = base[0], base1 = base[1];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const int64_t b = i / S3_TILE;
@@ -314,11 +328,17 @@ __global__ void k_slab_gather(int64_t nt, const uint8_t* __restrict__ ovf, const
                               const uint64_t* __restrict__ od, const uint32_t* __restrict__ slabM,
                               const uint32_t* __restrict__ slabP, const uint32_t* __restrict__ slabD, uint32_t capM,
                               uint32_t capP, uint32_t capD, uint32_t* __restrict__ srcM, uint32_t* __restrict__ srcP,
-                              uint32_t* __restrict__ dsrc) {
+                              uint32_t* __restrict__ dsrc, uint64_t lenM, uint64_t lenP, uint64_t lenD,
+                              unsigned* __restrict__ err) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    if (*reinterpret_cast<volatile unsigned*>(err) & 2u) return;   // being redone (see k_tct_level)
     for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nt; i += nw) {
         if (ovf[i]) continue;
+        if (om[i] + cm[i] > lenM || op[i] + cp[i] > lenP || od[i] + cd[i] > lenD) {   // outputs sized from
+            if (lane == 0) atomicOr(err, 2u);                                           // the previous build
+            continue;
+        }
         for (uint32_t k = lane; k < cm[i]; k += 32) srcM[om[i] + k] = slabM[(uint64_t)i * capM + k];
         for (uint32_t k = lane; k < cp[i]; k += 32) srcP[op[i] + k] = slabP[(uint64_t)i * capP + k];
         for (uint32_t k = lane; k < cd[i]; k += 32) dsrc[od[i] + k] = slabD[(uint64_t)i * capD + k];
@@ -353,7 +373,8 @@ __global__ void k_max3(const uint32_t* __restrict__ a, const uint32_t* __restric
 // One target-ordered traversal of the local target tree from the given seed sources at the root
 // (local: the root itself; remote: the roots of grafted LETs) into the CSR lists `o`.
 fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& seeds, TcLists& o, bool single,
-                   std::vector<std::array<uint32_t, 3>>& tc_max) {
+                   std::vector<std::array<uint32_t, 3>>& tc_max, std::vector<std::array<uint64_t, 3>>& tc_tot,
+                   bool allow_fast) {
     const int64_t nc = ctx->ncell;
     const int nlev = (int)ctx->depth + 1;
     const Cells v{P_<double4>(ctx->c_cr), P_<uint32_t>(ctx->c_cb), P_<uint32_t>(ctx->c_cc)};
@@ -370,51 +391,76 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
     uint32_t* cd = cp + maxw;
     uint32_t* ovf_list = cd + maxw;
     uint8_t* ovf = reinterpret_cast<uint8_t*>(ovf_list + maxw);
-    unsigned* n_ovf = P_<unsigned>(ctx->dcount2) + 24;
     uint32_t* d_seeds = P_<uint32_t>(ctx->tc_lb);
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(d_seeds, seeds.data(), seeds.size() * 4, cudaMemcpyHostToDevice, s));
     const int nseeds = (int)seeds.size();
     const int64_t scap = ctx->tc_scap > 0 ? ctx->tc_scap : TC_CAP;   // shared split-list capacity
-    unsigned* d_err = P_<unsigned>(ctx->dcount2) + 30;
-    FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_err, 0, 4, s));
-    // output capacities from the previous build (grown on demand, keeping what is written)
+    // per-level device records, zeroed once: bases (entries before each level) [nlev+1][2],
+    // totals [nlev][3], overflow counts [nlev], maxima [nlev][3], error flags
+    const size_t rec_bytes = (size_t)(nlev + 1) * 16 + (size_t)nlev * 24 + (size_t)nlev * 4 + (size_t)nlev * 12 + 64;
+    FMM_TRY(buf_ensure(ctx, ctx->tc_rec, rec_bytes));
+    uint64_t* d_base = P_<uint64_t>(ctx->tc_rec);
+    unsigned long long* d_tot = reinterpret_cast<unsigned long long*>(d_base + 2 * (nlev + 1));
+    unsigned* d_novf = reinterpret_cast<unsigned*>(d_tot + 3 * nlev);
+    unsigned* d_mx = d_novf + nlev;
+    unsigned* d_err = d_mx + 3 * nlev;
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->tc_rec.p, 0, rec_bytes, s));
+    const int grid_max = ctx->num_sms * 8;
+    const int32_t* par = P_<int32_t>(ctx->c_parent);
+    FMM_TRY(buf_ensure(ctx, ctx->tc_bsum, (size_t)((maxw + S3_TILE - 1) / S3_TILE) * 3 * 8 + 64));
+    uint64_t* bsum = P_<uint64_t>(ctx->tc_bsum);
+    FMM_TRY(buf_ensure(ctx, ctx->tc_glob, (size_t)TC_GWARPS * 2 * maxw * 4));
+    FMM_TRY(buf_ensure(ctx, ctx->tc_doff[0], (size_t)(maxw + 1) * 8));
+    FMM_TRY(buf_ensure(ctx, ctx->tc_doff[1], (size_t)(maxw + 1) * 8));
+    // slot sizes per level from the previous build's maxima (single pass); with the previous
+    // build's per-level totals too, every buffer is sized up front and the levels run without
+    // host round trips (fast), a capacity overflow being detected at the end (then: redone)
+    auto slot = [](uint32_t m) { return (m + m / 4 + 32 + 31) & ~31u; };
+    std::vector<char> use_slab(nlev, 0);
+    size_t slab_bytes = 64;
+    for (int l = 0; l < nlev && single && (int)tc_max.size() == nlev; ++l) {
+        const int64_t nt = ctx->level_begin[l + 1] - ctx->level_begin[l];
+        const size_t b = (size_t)nt * (slot(tc_max[l][0]) + slot(tc_max[l][1]) + slot(tc_max[l][2])) * 4;
+        use_slab[l] = b <= ((size_t)4 << 30);
+        if (use_slab[l]) slab_bytes = std::max(slab_bytes, b + 64);
+    }
+    FMM_TRY(buf_ensure(ctx, ctx->tc_slab, slab_bytes));
+    bool fast = allow_fast && single && (int)tc_max.size() == nlev && (int)tc_tot.size() == nlev;
+    uint64_t maxd = 1;
+    for (int l = 0; l < nlev && fast; ++l) {
+        fast = fast && use_slab[l];
+        maxd = std::max<uint64_t>(maxd, tc_tot[l][2]);
+    }
+    maxd += maxd / 8 + 1024;
     FMM_TRY(buf_ensure(ctx, *o.src_m, (size_t)std::max<int64_t>(*o.est_m, 1024) * 4));
     FMM_TRY(buf_ensure(ctx, *o.src_p, (size_t)std::max<int64_t>(*o.est_p, 1024) * 4));
-    uint64_t baseM = 0, baseP = 0;
+    if (fast) {
+        FMM_TRY(buf_ensure(ctx, ctx->tc_d[0], (size_t)maxd * 4));
+        FMM_TRY(buf_ensure(ctx, ctx->tc_d[1], (size_t)maxd * 4));
+    }
+    uint64_t baseM = 0, baseP = 0;   // host copies (synchronous levels only)
     DevBuf* dprev = &ctx->tc_d[0];
     DevBuf* dcur = &ctx->tc_d[1];
     const uint64_t* doff_prev = nullptr;
     int64_t pb = 0;
-    const int grid_max = ctx->num_sms * 8;
-    const int32_t* par = P_<int32_t>(ctx->c_parent);
-    unsigned* mx = n_ovf + 2;   // 3 per-level maxima
-    unsigned long long* d_tot = P_<unsigned long long>(ctx->dcount2) + 4;   // bytes 32..56
-    FMM_TRY(buf_ensure(ctx, ctx->tc_bsum, (size_t)((maxw + S3_TILE - 1) / S3_TILE) * 3 * 8 + 64));
-    uint64_t* bsum = P_<uint64_t>(ctx->tc_bsum);
-    FMM_TRY(buf_ensure(ctx, ctx->tc_glob, (size_t)TC_GWARPS * 2 * maxw * 4));
-    std::vector<std::array<uint32_t, 3>> maxc(nlev);
+    const int64_t gcap = maxw;   // a split list never exceeds one tree level
     for (int l = 0; l < nlev; ++l) {
         const int64_t tb = ctx->level_begin[l], te = ctx->level_begin[l + 1], nt = te - tb;
         const unsigned g = (unsigned)std::min<int64_t>((nt + TC_WARPS - 1) / TC_WARPS, grid_max);
         const uint32_t* dsrc_prev = doff_prev ? P_<uint32_t>(*dprev) : nullptr;
-        // single pass into per-target slots sized from the previous build's per-level maxima
-        // (first build, or slots over budget: count pass + emit pass)
-        bool slab = single && l < (int)tc_max.size();
+        const bool slab = use_slab[l];
         uint32_t capM = 0, capP = 0, capD = 0;
         if (slab) {
-            auto cap = [](uint32_t m) { return (m + m / 4 + 32 + 31) & ~31u; };
-            capM = cap(tc_max[l][0]);
-            capP = cap(tc_max[l][1]);
-            capD = cap(tc_max[l][2]);
-            const size_t bytes = (size_t)nt * (capM + capP + capD) * 4;
-            if (bytes > ((size_t)4 << 30)) slab = false;
-            else FMM_TRY(buf_ensure(ctx, ctx->tc_slab, bytes + 64));
+            capM = slot(tc_max[l][0]);
+            capP = slot(tc_max[l][1]);
+            capD = slot(tc_max[l][2]);
         }
         uint32_t* slabM = P_<uint32_t>(ctx->tc_slab);
         uint32_t* slabP = slabM + (size_t)nt * capM;
         uint32_t* slabD = slabP + (size_t)nt * capP;
+        unsigned* n_ovf = d_novf + l;
+        unsigned* mx = d_mx + 3 * l;
         FMM_CUDA_TRY(ctx, cudaMemsetAsync(ovf, 0, (size_t)nt, s));
-        FMM_CUDA_TRY(ctx, cudaMemsetAsync(n_ovf, 0, 20, s));
         if (slab)
             k_tct_level<2, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds,
                                                               ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr, slabM,
@@ -427,77 +473,89 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
                                                               scap, 0, 0, 0, d_err);
         FMM_LAUNCH(ctx);
         // overflowed targets (count read on the device: a no-op launch when there are none)
-        const int64_t gcap = maxw;   // a split list never exceeds one tree level
-        {
-            k_tct_level<0, true><<<TC_GWARPS / TC_WARPS, TC_WARPS * 32, 0, s>>>(
-                tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds, ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr,
-                nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err);
-            FMM_LAUNCH(ctx);
-        }
-        // offsets written straight into m2l_off / p2p_off (+ the entries of earlier levels) and
-        // the pass-down CSR of this level
+        k_tct_level<0, true><<<TC_GWARPS / TC_WARPS, TC_WARPS * 32, 0, s>>>(
+            tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds, ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr,
+            nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err);
+        FMM_LAUNCH(ctx);
+        // offsets written straight into m2l_off / p2p_off (+ the entries of earlier levels, a
+        // device value) and the pass-down CSR of this level
         uint64_t* om = P_<uint64_t>(*o.off_m) + tb;
         uint64_t* op = P_<uint64_t>(*o.off_p) + tb;
-        FMM_TRY(buf_ensure(ctx, ctx->tc_doff[l & 1], (size_t)(nt + 1) * 8));
         uint64_t* od = P_<uint64_t>(ctx->tc_doff[l & 1]);
         const int64_t nb = (nt + S3_TILE - 1) / S3_TILE;
         k_scan3_tiles<<<(unsigned)nb, S3_THREADS, 0, s>>>(cm, cp, cd, nt, om, op, od, bsum, nb, mx);
         FMM_LAUNCH(ctx);
-        k_scan3_top<<<1, S3_THREADS, 0, s>>>(bsum, nb, d_tot);
+        k_scan3_top<<<1, S3_THREADS, 0, s>>>(bsum, nb, d_tot + 3 * l, d_base + 2 * l, d_base + 2 * (l + 1));
         FMM_LAUNCH(ctx);
         const unsigned gw = (unsigned)std::min<int64_t>((nt + 255) / 256, grid_max);
-        k_scan3_add<<<gw, 256, 0, s>>>(nt, om, op, od, bsum, nb, baseM, baseP, d_tot);
+        k_scan3_add<<<gw, 256, 0, s>>>(nt, om, op, od, bsum, nb, d_base + 2 * l, d_tot + 3 * l);
         FMM_LAUNCH(ctx);
-        uint64_t tot[3];
-        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(tot, d_tot, 24, cudaMemcpyDeviceToHost, s));
-        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(maxc[l].data(), mx, 12, cudaMemcpyDeviceToHost, s));
-        FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-        const uint64_t needM = baseM + tot[0], needP = baseP + tot[1];
-        if (needM * 4 > o.src_m->bytes) FMM_TRY(buf_ensure(ctx, *o.src_m, (size_t)(needM + needM / 4) * 4, true, s));
-        if (needP * 4 > o.src_p->bytes) FMM_TRY(buf_ensure(ctx, *o.src_p, (size_t)(needP + needP / 4) * 4, true, s));
-        FMM_TRY(buf_ensure(ctx, *dcur, (size_t)std::max<uint64_t>(tot[2], 1) * 4));
+        if (!fast) {   // sizes now: grow the outputs (keeping the earlier levels' entries)
+            uint64_t tot[3];
+            FMM_CUDA_TRY(ctx, cudaMemcpyAsync(tot, d_tot + 3 * l, 24, cudaMemcpyDeviceToHost, s));
+            FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+            const uint64_t needM = baseM + tot[0], needP = baseP + tot[1];
+            if (needM * 4 > o.src_m->bytes) FMM_TRY(buf_ensure(ctx, *o.src_m, (size_t)(needM + needM / 4) * 4, true, s));
+            if (needP * 4 > o.src_p->bytes) FMM_TRY(buf_ensure(ctx, *o.src_p, (size_t)(needP + needP / 4) * 4, true, s));
+            FMM_TRY(buf_ensure(ctx, *dcur, (size_t)std::max<uint64_t>(tot[2], 1) * 4));
+            baseM = needM;
+            baseP = needP;
+        }
+        uint64_t lenM = o.src_m->bytes / 4, lenP = o.src_p->bytes / 4, lenD = dcur->bytes / 4;
+        if (fast && ctx->tc_tight) lenM = lenP = lenD = 16;   // tests: force the capacity-overflow redo
         if (slab) {
             k_slab_gather<<<(unsigned)std::min<int64_t>((nt + 7) / 8, grid_max), 256, 0, s>>>(
                 nt, ovf, cm, cp, cd, om, op, od, slabM, slabP, slabD, capM, capP, capD, P_<uint32_t>(*o.src_m),
-                P_<uint32_t>(*o.src_p), P_<uint32_t>(*dcur));
+                P_<uint32_t>(*o.src_p), P_<uint32_t>(*dcur), lenM, lenP, lenD, d_err);
         } else {
             k_tct_level<1, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds,
-                                                              ctx->theta, nullptr, nullptr, nullptr, om, op, od,
+                                                              ctx->theta, cm, cp, cd, om, op, od,
                                                               P_<uint32_t>(*o.src_m), P_<uint32_t>(*o.src_p),
                                                               P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf, nullptr, scap,
-                                                              0, 0, 0, d_err);
+                                                              0, 0, 0, d_err, lenM, lenP, lenD);
         }
         FMM_LAUNCH(ctx);
-        {
-            k_tct_level<1, true><<<TC_GWARPS / TC_WARPS, TC_WARPS * 32, 0, s>>>(
-                tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds, ctx->theta, nullptr, nullptr, nullptr, om, op, od,
-                P_<uint32_t>(*o.src_m), P_<uint32_t>(*o.src_p), P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf,
-                P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err);
-            FMM_LAUNCH(ctx);
-        }
-        baseM = needM;
-        baseP = needP;
+        k_tct_level<1, true><<<TC_GWARPS / TC_WARPS, TC_WARPS * 32, 0, s>>>(
+            tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds, ctx->theta, cm, cp, cd, om, op, od,
+            P_<uint32_t>(*o.src_m), P_<uint32_t>(*o.src_p), P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf,
+            P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err, lenM, lenP, lenD);
+        FMM_LAUNCH(ctx);
         // this level's pass-down offsets (od, nt + 1 entries) are the next level's input
         doff_prev = od;
         pb = tb;
         std::swap(dprev, dcur);
     }
-    tc_max = maxc;
-    const uint64_t ends[2] = {baseM, baseP};
+    // the list ends (device bases after the last level), the records for the next build
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<uint64_t>(*o.off_m) + nc, d_base + 2 * nlev, 8, cudaMemcpyDeviceToDevice, s));
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<uint64_t>(*o.off_p) + nc, d_base + 2 * nlev + 1, 8, cudaMemcpyDeviceToDevice, s));
+    std::vector<uint64_t> hbase(2 * (nlev + 1)), htot(3 * (size_t)nlev);
+    std::vector<unsigned> hmx(3 * (size_t)nlev);
     unsigned herr = 0;
-    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<uint64_t>(*o.off_m) + nc, &ends[0], 8, cudaMemcpyHostToDevice, s));
-    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<uint64_t>(*o.off_p) + nc, &ends[1], 8, cudaMemcpyHostToDevice, s));
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(hbase.data(), d_base, hbase.size() * 8, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(htot.data(), d_tot, htot.size() * 8, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(hmx.data(), d_mx, hmx.size() * 4, cudaMemcpyDeviceToHost, s));
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, s));
-    FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));   // ends[] lives on this stack frame
+    FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
     FMM_CUDA_TRY(ctx, cudaGetLastError());
-    if (herr) {
+    if (herr & 1u) {
         ctx->err = "dual tree traversal needed children of a remote LET cell that were not exported";
         return FMM_ERR_STATE;
     }
-    *o.n_m = (int64_t)baseM;
-    *o.n_p = (int64_t)baseP;
-    *o.est_m = (int64_t)(baseM + baseM / 8 + 1024);
-    *o.est_p = (int64_t)(baseP + baseP / 8 + 1024);
+    std::vector<std::array<uint32_t, 3>> maxc(nlev);
+    std::vector<std::array<uint64_t, 3>> totc(nlev);
+    for (int l = 0; l < nlev; ++l)
+        for (int a = 0; a < 3; ++a) {
+            maxc[l][a] = hmx[3 * l + a];
+            totc[l][a] = htot[3 * l + a];
+        }
+    tc_max = maxc;
+    tc_tot = totc;
+    const uint64_t endM = hbase[2 * nlev], endP = hbase[2 * nlev + 1];
+    *o.est_m = (int64_t)(endM + endM / 8 + 1024);
+    *o.est_p = (int64_t)(endP + endP / 8 + 1024);
+    if (herr & 2u) return FMM_ERR_OOM;   // outputs sized from the previous build were too small: redo
+    *o.n_m = (int64_t)endM;
+    *o.n_p = (int64_t)endP;
     return FMM_OK;
 }
 
@@ -506,7 +564,10 @@ fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s) {
     TcLists o{&ctx->m2l_off, &ctx->m2l_src, &ctx->p2p_off, &ctx->p2p_src, &ctx->n_m2l, &ctx->n_p2p,
               &ctx->tc_est_m2l, &ctx->tc_est_p2p};
     const std::vector<uint32_t> seeds{0u};
-    return tct_run(ctx, s, seeds, o, ctx->tc_single, ctx->tc_max);
+    fmm_status st = tct_run(ctx, s, seeds, o, ctx->tc_single, ctx->tc_max, ctx->tc_tot, true);
+    if (st == FMM_ERR_OOM && ctx->err.empty())   // a capacity guess was short: sizes are known now
+        st = tct_run(ctx, s, seeds, o, ctx->tc_single, ctx->tc_max, ctx->tc_tot, false);
+    return st;
 }
 
 // remote traversal of the LET roots grafted since the last one: one more CSR part
@@ -515,7 +576,8 @@ fmm_status tct_remote(fmm_ctx* ctx, const std::vector<uint32_t>& roots, cudaStre
     TcPart& pt = ctx->tc_rem[ctx->tc_nrem++];
     TcLists o{&pt.off_m, &pt.src_m, &pt.off_p, &pt.src_p, &pt.n_m, &pt.n_p, &pt.est_m, &pt.est_p};
     std::vector<std::array<uint32_t, 3>> none;   // count + emit passes (no slot history)
-    return tct_run(ctx, s, roots, o, false, none);
+    std::vector<std::array<uint64_t, 3>> none_t;
+    return tct_run(ctx, s, roots, o, false, none, none_t, false);
 }
 
 namespace {

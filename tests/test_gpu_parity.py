@@ -235,8 +235,9 @@ def test_target_traversal_overflow_paths(torch_cuda, kind, monkeypatch):
     f = FMM(20000, 5, 0.5, 16, "f64")
     phi_a, grad_a = f.solve(tp, tq)
     monkeypatch.setenv("FMM_TCT_CAP", "4")
+    monkeypatch.setenv("FMM_TCT_TIGHT", "1")   # and the sync-free pass redone after a capacity overflow
     g = FMM(20000, 5, 0.5, 16, "f64")
-    for _ in range(2):   # first build: count + emit passes; second: single pass into slots
+    for _ in range(3):   # first build: count + emit passes; then single pass into slots (sync-free)
         phi_b, grad_b = g.solve(tp, tq)
         torch.cuda.synchronize()
         for a, b in zip(f.lists(), g.lists()):
