@@ -558,6 +558,14 @@ fmm_status fmm_get_counts(const fmm_ctx* ctx, fmm_counts* out) {
     out->depth = ctx->depth;
     out->n_m2l = ctx->n_m2l;
     out->n_p2p = ctx->n_p2p;
+    if (ctx->p2p_inter < 0) {   // counted by the P2P run builder on the device; read once
+        fmm_ctx* c = const_cast<fmm_ctx*>(ctx);
+        DeviceGuard g(c->device);
+        unsigned long long v = 0;
+        FMM_CUDA_TRY(c, cudaDeviceSynchronize());
+        FMM_CUDA_TRY(c, cudaMemcpy(&v, P_<unsigned long long>(c->dcount2) + 2, 8, cudaMemcpyDeviceToHost));
+        c->p2p_inter = (int64_t)v;
+    }
     out->p2p_interactions = ctx->p2p_inter;
     return FMM_OK;
 }

@@ -471,19 +471,6 @@ __global__ void k_unpack_src(const uint64_t* __restrict__ lst, int64_t n, uint32
     if (i < n) src[i] = (uint32_t)lst[i];
 }
 
-__global__ void k_p2p_inter(const uint64_t* __restrict__ off, int64_t ncell, const uint32_t* __restrict__ src,
-                            const uint32_t* __restrict__ bc, unsigned long long* out) {
-    unsigned long long s = 0;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ncell; t += (int64_t)gridDim.x * blockDim.x) {
-        unsigned long long st = 0;
-        for (uint64_t p = off[t]; p < off[t + 1]; ++p) st += bc[src[p]];
-        s += st * bc[t];
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
-}
-
 // segments longer than SEG_MAX: gather them as packed (target, source) keys, radix-sort that
 // (small) array, write the sources back in place
 __global__ void k_big_flags(const uint64_t* __restrict__ off, int64_t ncell, uint64_t* __restrict__ sz) {
@@ -686,8 +673,10 @@ __global__ void k_run_flags(const uint64_t* __restrict__ off, const uint32_t* __
 __global__ void k_run_emit(const uint64_t* __restrict__ off, const uint32_t* __restrict__ src, int64_t ncell,
                            const uint32_t* __restrict__ bb, const uint32_t* __restrict__ bc,
                            const uint32_t* __restrict__ flag, const uint32_t* __restrict__ rid,
-                           uint2* __restrict__ runs, uint32_t* __restrict__ roff, uint32_t* __restrict__ rtot) {
+                           uint2* __restrict__ runs, uint32_t* __restrict__ roff, uint32_t* __restrict__ rtot,
+                           unsigned long long* __restrict__ inter) {
     const int lane = threadIdx.x & 31;
+    unsigned long long my_inter = 0;   // lane 0: sum over this warp's targets of |T| * sources(T)
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t t = w0; t < ncell; t += nw) {
         const uint64_t p0 = off[t], p1 = off[t + 1];
@@ -707,8 +696,12 @@ __global__ void k_run_emit(const uint64_t* __restrict__ off, const uint32_t* __r
             if (ok && flag[p]) runs[rid[p]] = make_uint2(bb[sc], carry + x - c);
             carry += __shfl_sync(0xffffffffu, x, 31);
         }
-        if (lane == 0) rtot[t] = carry;
+        if (lane == 0) {
+            rtot[t] = carry;
+            my_inter += (unsigned long long)carry * bc[t];
+        }
     }
+    if (lane == 0 && my_inter) atomicAdd(inter, my_inter);
 }
 
 __global__ void k_run_last(int64_t ncell, uint32_t nr, uint32_t* __restrict__ roff) { roff[ncell] = nr; }
@@ -782,8 +775,10 @@ fmm_status build_runs(fmm_ctx* ctx, cudaStream_t s) {
     FMM_TRY(buf_ensure(ctx, ctx->runs, (size_t)std::max<uint32_t>(nr, 1) * 8 + (size_t)(nc + 1) * 4 + 64));
     uint2* runs = P_<uint2>(ctx->runs);
     uint32_t* rtot = reinterpret_cast<uint32_t*>(runs + std::max<uint32_t>(nr, 1));
+    unsigned long long* d_inter = P_<unsigned long long>(ctx->dcount2) + 2;   // read lazily (fmm_get_counts)
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_inter, 0, 8, s));
     k_run_emit<<<std::max(g, 1), 128, 0, s>>>(off, src, nc, P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), flag, rid,
-                                             runs, P_<uint32_t>(ctx->run_off), rtot);
+                                             runs, P_<uint32_t>(ctx->run_off), rtot, d_inter);
     FMM_LAUNCH(ctx);
     k_run_last<<<1, 1, 0, s>>>(nc, nr, P_<uint32_t>(ctx->run_off));
     FMM_LAUNCH(ctx);
@@ -947,16 +942,8 @@ fmm_status lists_pass(fmm_ctx* ctx, cudaStream_t s) {
 
 // the target-ordered traversal (tct.cu) already wrote the CSR lists
 fmm_status lists_finish(fmm_ctx* ctx, cudaStream_t s) {
-    const int64_t nc = ctx->ncell;
-    unsigned long long* d_inter = P_<unsigned long long>(ctx->dcount2) + 2;
-    FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_inter, 0, 8, s));
-    k_p2p_inter<<<ctx->num_sms * 4, 256, 0, s>>>(P_<uint64_t>(ctx->p2p_off), nc, P_<uint32_t>(ctx->p2p_src),
-                                                  P_<uint32_t>(ctx->c_bc), d_inter);
-    FMM_LAUNCH(ctx);
-    unsigned long long inter = 0;
-    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&inter, d_inter, 8, cudaMemcpyDeviceToHost, s));
-    FMM_TRY(build_runs(ctx, s));   // synchronises s
-    ctx->p2p_inter = (int64_t)inter;
+    FMM_TRY(build_runs(ctx, s));   // synchronises s; the interaction count stays on the device
+    ctx->p2p_inter = -1;
     return FMM_OK;
 }
 
