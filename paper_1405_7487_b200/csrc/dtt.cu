@@ -1,4 +1,6 @@
-// dtt.cu -- dual tree traversal producing explicit M2L and P2P lists (a8).
+// dtt.cu -- breadth-first dual tree traversal producing explicit M2L and P2P lists (a8), used
+// with FMM_DTT=bfs; the default traversal is target-ordered (tct.cu).  The P2P source runs
+// (build_runs) and the list finishing below serve both.
 //
 // PAPER.md:151 §II-C: "the M2L and P2P kernels are processed ... by using the dual tree
 // traversal [Dehnen]"; north_star asks for the traversal to emit explicit lists.
