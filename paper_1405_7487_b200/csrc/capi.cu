@@ -128,6 +128,8 @@ fmm_status fmm_create(int64_t n_max, int p, double theta, int ncrit, int prec, i
         ctx->tc_scap = g17 ? atoi(g17) : 0;
         const char* g18 = getenv("FMM_TCT_TIGHT");
         ctx->tc_tight = g18 && g18[0] == '1';
+        const char* g21 = getenv("FMM_TREE_FAST");
+        ctx->tree_fast = !(g21 && g21[0] == '0');
         const char* g15 = getenv("FMM_DTT");
         ctx->dtt_mode = (g15 && std::string(g15) == "bfs") ? 1 : 0;
         const char* g7 = getenv("FMM_LIST_SORT");
@@ -169,7 +171,7 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
     for (DevBuf* b : bufs) buf_free(*b);
     DevBuf* tbufs[] = {&ctx->tc_cnt, &ctx->tc_lb, &ctx->tc_d[0], &ctx->tc_d[1], &ctx->tc_doff[0],
                        &ctx->tc_doff[1], &ctx->tc_glob, &ctx->tc_slab, &ctx->tc_bsum, &ctx->tc_cat_off,
-                       &ctx->tc_cat_src, &ctx->tc_rec};
+                       &ctx->tc_cat_src, &ctx->tc_rec, &ctx->tree_lb};
     for (auto& pt : ctx->tc_rem) {
         DevBuf* pb[] = {&pt.off_m, &pt.src_m, &pt.off_p, &pt.src_p};
         for (DevBuf* b : pb) buf_free(*b);

@@ -148,6 +148,9 @@ struct fmm_ctx {
     std::vector<int64_t> level_begin;  // host: first cell of each level, size depth+2
     DevBuf c_key, c_level, c_bb, c_bc, c_cb, c_cc, c_parent, c_bmin, c_bmax, c_cr;  // c_cr: double4 (cx,cy,cz,R)
     DevBuf split_tmp, split_cnt;       // per-level temporaries
+    DevBuf tree_lb;                    // sync-free build: level starts + overflow flag (device)
+    bool tree_fast = true;             // levels from the previous build's sizes (FMM_TREE_FAST=0: off)
+    int64_t tree_prev_depth = -1, tree_prev_ncell = 0, tree_prev_maxw = 0;
     DevBuf leaf_ids;                   // u32 list of leaf cells
 
     // lists (CSR by target, canonical order): m2l_off[ncell+1] (u64), m2l_src[n_m2l] (u32); p2p likewise.
