@@ -80,8 +80,12 @@ fmm_status fmm_build(fmm_ctx* ctx, const void* pos, int64_t n, void* stream);
  *   root), replacing earlier lists; remote != 0: from (root, r) for the root r of every LET
  *   grafted by fmm_let_graft, appended to the lists of the last fmm_dtt.  Synchronises.
  *   FMM_ERR_STATE if the traversal needs children of a remote cell that were not exported.
- * fmm_lists: groups the traversal's pairs into canonical CSR lists (R10; sources of a
- *   target ascending: local cells, then LET 0, LET 1, ... in their sender's order).
+ *   The traversal is organised by target cell (default): each target's lists come out
+ *   grouped, in a deterministic order (by traversal generation; R10 fixes the set, and
+ *   fmm_copy_lists returns the canonical ascending order); FMM_DTT=bfs selects the
+ *   breadth-first traversal whose lists fmm_lists sorts into ascending order.
+ * fmm_lists: finishes the lists (CSR by target): the local ones followed, per target, by the
+ *   sources found in each remote traversal (graft order), and the P2P source runs.
  * fmm_build(pos, n) == fmm_build_tree + fmm_dtt(0) + fmm_lists. */
 fmm_status fmm_build_tree(fmm_ctx* ctx, const void* pos, int64_t n, void* stream);
 /* fmm_set_root_bounds: later builds take the R2 root cube from these bounds (HOST [6]: lo xyz,
