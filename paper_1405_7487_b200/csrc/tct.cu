@@ -26,7 +26,7 @@ namespace {
 
 constexpr int TC_WARPS = 4;
 constexpr int TC_CAP = 512;    // split-B sources per target and level held in shared memory
-constexpr int TC_GWARPS = 32;  // warps of the global-memory kernel (overflowed targets)
+constexpr int TC_GWARPS_MAX = 1024;   // warps of the global-memory kernel (overflowed targets), at most
 
 struct Cells {
     const double4* __restrict__ cr;
@@ -409,7 +409,10 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
     const int32_t* par = P_<int32_t>(ctx->c_parent);
     FMM_TRY(buf_ensure(ctx, ctx->tc_bsum, (size_t)((maxw + S3_TILE - 1) / S3_TILE) * 3 * 8 + 64));
     uint64_t* bsum = P_<uint64_t>(ctx->tc_bsum);
-    FMM_TRY(buf_ensure(ctx, ctx->tc_glob, (size_t)TC_GWARPS * 2 * maxw * 4));
+    // overflow kernel: two level-sized split lists per warp, as many warps as 1 GB allows
+    const int gwarps = (int)std::max<int64_t>(TC_WARPS, std::min<int64_t>(TC_GWARPS_MAX,
+                                                                   ((int64_t)1 << 30) / (2 * maxw * 4)) / TC_WARPS * TC_WARPS);
+    FMM_TRY(buf_ensure(ctx, ctx->tc_glob, (size_t)gwarps * 2 * maxw * 4));
     FMM_TRY(buf_ensure(ctx, ctx->tc_doff[0], (size_t)(maxw + 1) * 8));
     FMM_TRY(buf_ensure(ctx, ctx->tc_doff[1], (size_t)(maxw + 1) * 8));
     // slot sizes per level from the previous build's maxima (single pass); with the previous
@@ -421,7 +424,7 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
     for (int l = 0; l < nlev && single && (int)tc_max.size() == nlev; ++l) {
         const int64_t nt = ctx->level_begin[l + 1] - ctx->level_begin[l];
         const size_t b = (size_t)nt * (slot(tc_max[l][0]) + slot(tc_max[l][1]) + slot(tc_max[l][2])) * 4;
-        use_slab[l] = b <= ((size_t)4 << 30);
+        use_slab[l] = b <= ((size_t)16 << 30);
         if (use_slab[l]) slab_bytes = std::max(slab_bytes, b + 64);
     }
     FMM_TRY(buf_ensure(ctx, ctx->tc_slab, slab_bytes));
@@ -473,7 +476,7 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
                                                               scap, 0, 0, 0, d_err);
         FMM_LAUNCH(ctx);
         // overflowed targets (count read on the device: a no-op launch when there are none)
-        k_tct_level<0, true><<<TC_GWARPS / TC_WARPS, TC_WARPS * 32, 0, s>>>(
+        k_tct_level<0, true><<<gwarps / TC_WARPS, TC_WARPS * 32, 0, s>>>(
             tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds, ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr,
             nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err);
         FMM_LAUNCH(ctx);
@@ -515,7 +518,7 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
                                                               0, 0, 0, d_err, lenM, lenP, lenD);
         }
         FMM_LAUNCH(ctx);
-        k_tct_level<1, true><<<TC_GWARPS / TC_WARPS, TC_WARPS * 32, 0, s>>>(
+        k_tct_level<1, true><<<gwarps / TC_WARPS, TC_WARPS * 32, 0, s>>>(
             tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds, ctx->theta, cm, cp, cd, om, op, od,
             P_<uint32_t>(*o.src_m), P_<uint32_t>(*o.src_p), P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf,
             P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err, lenM, lenP, lenD);
