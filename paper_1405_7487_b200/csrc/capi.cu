@@ -169,7 +169,7 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
                       &ctx->run_len64, &ctx->dcount2, &ctx->tcnt, &ctx->cnt64, &ctx->big_off, &ctx->M, &ctx->L, &ctx->Mr, &ctx->Lr, &ctx->near_phi, &ctx->near_grad,
                       &ctx->far, &ctx->h_stage};
     for (DevBuf* b : bufs) buf_free(*b);
-    DevBuf* tbufs[] = {&ctx->tc_cnt, &ctx->tc_lb, &ctx->tc_d[0], &ctx->tc_d[1], &ctx->tc_doff[0],
+    DevBuf* tbufs[] = {&ctx->tc_cnt, &ctx->tc_voff, &ctx->tc_lb, &ctx->tc_d[0], &ctx->tc_d[1], &ctx->tc_doff[0],
                        &ctx->tc_doff[1], &ctx->tc_glob, &ctx->tc_slab, &ctx->tc_bsum, &ctx->tc_cat_off,
                        &ctx->tc_cat_src, &ctx->tc_rec, &ctx->tree_lb};
     for (auto& pt : ctx->tc_rem) {

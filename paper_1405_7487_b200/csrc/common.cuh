@@ -160,7 +160,7 @@ struct fmm_ctx {
     DevBuf dtt_lvl;                                          // per-level frontier sizes (dtt.cu fast path)
     // target-ordered traversal (tct.cu): per-level counts/scans, level_begin, pass-down sets
     // (ping-pong CSR), global split lists of overflowed targets
-    DevBuf tc_cnt, tc_lb, tc_d[2], tc_doff[2], tc_glob, tc_slab, tc_bsum;
+    DevBuf tc_cnt, tc_voff, tc_lb, tc_d[2], tc_doff[2], tc_glob, tc_slab, tc_bsum;
     std::vector<std::array<uint32_t, 3>> tc_max;   // per-level max list lengths of the last build
     std::vector<std::array<uint64_t, 3>> tc_tot;   // per-level list totals of the last build
     DevBuf tc_rec;                                  // per-level device records (bases, totals, maxima)

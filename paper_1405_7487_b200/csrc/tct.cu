@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
     uint32_t* __restrict__ srcM, uint32_t* __restrict__ srcP, uint32_t* __restrict__ dsrc,
     uint8_t* __restrict__ ovf, uint32_t* __restrict__ ovf_list, unsigned* __restrict__ n_ovf,
     uint32_t* __restrict__ gscratch, int64_t gcap, uint32_t capM, uint32_t capP, uint32_t capD,
-    unsigned* __restrict__ err, uint64_t lenM = ~0ull, uint64_t lenP = ~0ull, uint64_t lenD = ~0ull) {
+    unsigned* __restrict__ err, int S, uint64_t lenM = ~0ull, uint64_t lenP = ~0ull, uint64_t lenD = ~0ull) {
     constexpr bool EMIT = MODE != 0, COUNT = MODE != 1, SLAB = MODE == 2;
     // an earlier level outgrew the buffers sized from the previous build: the traversal is
     // redone, so stop here instead of reading incomplete pass-down sets
@@ -91,10 +91,14 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
         list1 = s_sb[w][GLOB ? 0 : 1];
         cap = min((int64_t)TC_CAP, gcap);   // gcap: shared-list cap (tests force overflows with it)
     }
-    const int64_t nitems = GLOB ? (int64_t)*n_ovf : te - tb;
+    // work items are (target, slice) pairs, slice k of S taking the k-th part of the target's
+    // pass-down set (and everything it generates): more warps for the wide upper levels
+    const int64_t nitems = GLOB ? (int64_t)*n_ovf : (te - tb) * S;
     for (int64_t it = gw; it < nitems; it += nwarps) {
-        const int64_t t = GLOB ? (int64_t)ovf_list[it] : tb + it;
-        if (!GLOB && MODE == 1 && ovf[t - tb]) continue;   // done by the global-memory kernel
+        const int64_t vi = GLOB ? (int64_t)ovf_list[it] : it;   // virtual target index
+        const int64_t t = tb + vi / S;
+        const int64_t slice = vi % S;
+        if (!GLOB && MODE == 1 && ovf[vi]) continue;   // done by the global-memory kernel
         const double4 T = v.cr[t];
         const uint32_t nT = v.cc[t];
         uint64_t x0 = 0, x1 = (uint64_t)nseeds;   // root targets: the seed sources
@@ -103,20 +107,25 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
             x0 = doff_prev[pi];
             x1 = doff_prev[pi + 1];
         }
+        {
+            const uint64_t len = x1 - x0;
+            x1 = x0 + len * (uint64_t)(slice + 1) / (uint64_t)S;
+            x0 = x0 + len * (uint64_t)slice / (uint64_t)S;
+        }
         uint64_t oM = 0, oP = 0, oD = 0;
-        if (MODE == 1 && (offM[t - tb] + cnt_m[t - tb] > lenM || offP[t - tb] + cnt_p[t - tb] > lenP ||
-                          offD[t - tb] + cnt_d[t - tb] > lenD)) {   // outputs sized from the previous build
+        if (MODE == 1 && (offM[vi] + cnt_m[vi] > lenM || offP[vi] + cnt_p[vi] > lenP ||
+                          offD[vi] + cnt_d[vi] > lenD)) {   // outputs sized from the previous build
             if (lane == 0) atomicOr(err, 2u);
             continue;
         }
         if (SLAB) {
-            oM = (uint64_t)(t - tb) * capM;
-            oP = (uint64_t)(t - tb) * capP;
-            oD = (uint64_t)(t - tb) * capD;
+            oM = (uint64_t)vi * capM;
+            oP = (uint64_t)vi * capP;
+            oD = (uint64_t)vi * capD;
         } else if (EMIT) {
-            oM = offM[t - tb];
-            oP = offP[t - tb];
-            oD = offD[t - tb];
+            oM = offM[vi];
+            oP = offP[vi];
+            oD = offD[vi];
         }
         TcOut o{0u, 0u, 0u};
         bool over = false;
@@ -210,12 +219,12 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
         if (SLAB) over |= o.m > capM || o.p > capP || o.d > capD;
         if (COUNT && lane == 0) {
             if (over && !GLOB) {
-                ovf[t - tb] = 1;
-                ovf_list[atomicAdd(n_ovf, 1u)] = (uint32_t)t;
+                ovf[vi] = 1;
+                ovf_list[atomicAdd(n_ovf, 1u)] = (uint32_t)vi;
             }
-            cnt_m[t - tb] = o.m;
-            cnt_p[t - tb] = o.p;
-            cnt_d[t - tb] = o.d;
+            cnt_m[vi] = o.m;
+            cnt_p[vi] = o.p;
+            cnt_d[vi] = o.d;
         }
         __syncwarp();
     }
@@ -317,7 +326,25 @@ __global__ void k_scan3_add(int64_t n, uint64_t* __restrict__ o0, uint64_t* __re
         o1[i] += base1 + bsum[nb + b];
         o2[i] += bsum[2 * nb + b];
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) o2[n] = tot[2];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        o0[n] = base0 + tot[0];
+        o1[n] = base1 + tot[1];
+        o2[n] = tot[2];
+    }
+}
+
+// per-target CSR offsets from the (target, slice) offsets: the target's first slice
+__global__ void k_target_offsets(int64_t nt, int S, const uint64_t* __restrict__ vm, const uint64_t* __restrict__ vp,
+                                 const uint64_t* __restrict__ vd, uint64_t* __restrict__ om, uint64_t* __restrict__ op,
+                                 uint64_t* __restrict__ od) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t <= nt; t += stride) {
+        if (t < nt) {
+            om[t] = vm[t * S];
+            op[t] = vp[t * S];
+        }
+        od[t] = vd[t * S];
+    }
 }
 
 // single pass: slab slots -> CSR positions (warp per target; overflowed targets are written
@@ -380,17 +407,32 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
     const Cells v{P_<double4>(ctx->c_cr), P_<uint32_t>(ctx->c_cb), P_<uint32_t>(ctx->c_cc)};
     int64_t maxw = 1;
     for (int l = 0; l < nlev; ++l) maxw = std::max(maxw, ctx->level_begin[l + 1] - ctx->level_begin[l]);
+    // slices per target: levels with fewer targets than ~32 warps per SM split each target's
+    // pass-down set over up to 32 warps
+    const int64_t want = (int64_t)ctx->num_sms * 32;
+    std::vector<int> S(nlev, 1);
+    int64_t maxv = maxw;   // (target, slice) items of the widest level
+    for (int l = 0; l < nlev; ++l) {
+        const int64_t nt = ctx->level_begin[l + 1] - ctx->level_begin[l];
+        S[l] = (int)std::min<int64_t>(32, std::max<int64_t>(1, want / std::max<int64_t>(nt, 1)));
+        maxv = std::max(maxv, nt * S[l]);
+    }
     FMM_TRY(buf_ensure(ctx, *o.off_m, (size_t)(nc + 1) * 8));
     FMM_TRY(buf_ensure(ctx, *o.off_p, (size_t)(nc + 1) * 8));
-    // per-level scratch: counts (3 x u32), overflow flags (u8) and list (u32)
-    FMM_TRY(buf_ensure(ctx, ctx->tc_cnt, (size_t)maxw * 12 + (size_t)maxw * 5 + 256));
+    // per-level scratch over (target, slice) items: counts (3 x u32), overflow flags (u8) and
+    // list (u32), item offsets (3 x u64)
+    FMM_TRY(buf_ensure(ctx, ctx->tc_cnt, (size_t)maxv * 12 + (size_t)maxv * 5 + 256));
+    FMM_TRY(buf_ensure(ctx, ctx->tc_voff, (size_t)(maxv + 1) * 8 * 3 + 64));
+    uint64_t* vm = P_<uint64_t>(ctx->tc_voff);
+    uint64_t* vp = vm + (maxv + 1);
+    uint64_t* vd = vp + (maxv + 1);
     FMM_TRY(buf_ensure(ctx, ctx->tc_lb, seeds.size() * 4 + 64));
     FMM_TRY(buf_ensure(ctx, ctx->dcount2, 128));
     uint32_t* cm = P_<uint32_t>(ctx->tc_cnt);
-    uint32_t* cp = cm + maxw;
-    uint32_t* cd = cp + maxw;
-    uint32_t* ovf_list = cd + maxw;
-    uint8_t* ovf = reinterpret_cast<uint8_t*>(ovf_list + maxw);
+    uint32_t* cp = cm + maxv;
+    uint32_t* cd = cp + maxv;
+    uint32_t* ovf_list = cd + maxv;
+    uint8_t* ovf = reinterpret_cast<uint8_t*>(ovf_list + maxv);
     uint32_t* d_seeds = P_<uint32_t>(ctx->tc_lb);
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(d_seeds, seeds.data(), seeds.size() * 4, cudaMemcpyHostToDevice, s));
     const int nseeds = (int)seeds.size();
@@ -407,7 +449,7 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
     FMM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->tc_rec.p, 0, rec_bytes, s));
     const int grid_max = ctx->num_sms * 8;
     const int32_t* par = P_<int32_t>(ctx->c_parent);
-    FMM_TRY(buf_ensure(ctx, ctx->tc_bsum, (size_t)((maxw + S3_TILE - 1) / S3_TILE) * 3 * 8 + 64));
+    FMM_TRY(buf_ensure(ctx, ctx->tc_bsum, (size_t)((maxv + S3_TILE - 1) / S3_TILE) * 3 * 8 + 64));
     uint64_t* bsum = P_<uint64_t>(ctx->tc_bsum);
     // overflow kernel: two level-sized split lists per warp, as many warps as 1 GB allows
     const int gwarps = (int)std::max<int64_t>(TC_WARPS, std::min<int64_t>(TC_GWARPS_MAX,
@@ -422,8 +464,8 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
     std::vector<char> use_slab(nlev, 0);
     size_t slab_bytes = 64;
     for (int l = 0; l < nlev && single && (int)tc_max.size() == nlev; ++l) {
-        const int64_t nt = ctx->level_begin[l + 1] - ctx->level_begin[l];
-        const size_t b = (size_t)nt * (slot(tc_max[l][0]) + slot(tc_max[l][1]) + slot(tc_max[l][2])) * 4;
+        const int64_t nv = (ctx->level_begin[l + 1] - ctx->level_begin[l]) * S[l];
+        const size_t b = (size_t)nv * (slot(tc_max[l][0]) + slot(tc_max[l][1]) + slot(tc_max[l][2])) * 4;
         use_slab[l] = b <= ((size_t)16 << 30);
         if (use_slab[l]) slab_bytes = std::max(slab_bytes, b + 64);
     }
@@ -449,7 +491,9 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
     const int64_t gcap = maxw;   // a split list never exceeds one tree level
     for (int l = 0; l < nlev; ++l) {
         const int64_t tb = ctx->level_begin[l], te = ctx->level_begin[l + 1], nt = te - tb;
-        const unsigned g = (unsigned)std::min<int64_t>((nt + TC_WARPS - 1) / TC_WARPS, grid_max);
+        const int Sl = S[l];
+        const int64_t nv = nt * Sl;
+        const unsigned g = (unsigned)std::min<int64_t>((nv + TC_WARPS - 1) / TC_WARPS, grid_max);
         const uint32_t* dsrc_prev = doff_prev ? P_<uint32_t>(*dprev) : nullptr;
         const bool slab = use_slab[l];
         uint32_t capM = 0, capP = 0, capD = 0;
@@ -459,39 +503,44 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
             capD = slot(tc_max[l][2]);
         }
         uint32_t* slabM = P_<uint32_t>(ctx->tc_slab);
-        uint32_t* slabP = slabM + (size_t)nt * capM;
-        uint32_t* slabD = slabP + (size_t)nt * capP;
+        uint32_t* slabP = slabM + (size_t)nv * capM;
+        uint32_t* slabD = slabP + (size_t)nv * capP;
         unsigned* n_ovf = d_novf + l;
         unsigned* mx = d_mx + 3 * l;
-        FMM_CUDA_TRY(ctx, cudaMemsetAsync(ovf, 0, (size_t)nt, s));
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(ovf, 0, (size_t)nv, s));
         if (slab)
             k_tct_level<2, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds,
                                                               ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr, slabM,
                                                               slabP, slabD, ovf, ovf_list, n_ovf, nullptr, scap, capM,
-                                                              capP, capD, d_err);
+                                                              capP, capD, d_err, Sl);
         else
             k_tct_level<0, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds,
                                                               ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr,
                                                               nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, nullptr,
-                                                              scap, 0, 0, 0, d_err);
+                                                              scap, 0, 0, 0, d_err, Sl);
         FMM_LAUNCH(ctx);
         // overflowed targets (count read on the device: a no-op launch when there are none)
         k_tct_level<0, true><<<gwarps / TC_WARPS, TC_WARPS * 32, 0, s>>>(
             tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds, ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr,
-            nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err);
+            nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err, Sl);
         FMM_LAUNCH(ctx);
         // offsets written straight into m2l_off / p2p_off (+ the entries of earlier levels, a
         // device value) and the pass-down CSR of this level
         uint64_t* om = P_<uint64_t>(*o.off_m) + tb;
         uint64_t* op = P_<uint64_t>(*o.off_p) + tb;
         uint64_t* od = P_<uint64_t>(ctx->tc_doff[l & 1]);
-        const int64_t nb = (nt + S3_TILE - 1) / S3_TILE;
-        k_scan3_tiles<<<(unsigned)nb, S3_THREADS, 0, s>>>(cm, cp, cd, nt, om, op, od, bsum, nb, mx);
+        // offsets per (target, slice) item (M2L/P2P absolute, pass-down level-local), then the
+        // targets' CSR offsets (their first slice)
+        const int64_t nb = (nv + S3_TILE - 1) / S3_TILE;
+        k_scan3_tiles<<<(unsigned)nb, S3_THREADS, 0, s>>>(cm, cp, cd, nv, vm, vp, vd, bsum, nb, mx);
         FMM_LAUNCH(ctx);
         k_scan3_top<<<1, S3_THREADS, 0, s>>>(bsum, nb, d_tot + 3 * l, d_base + 2 * l, d_base + 2 * (l + 1));
         FMM_LAUNCH(ctx);
-        const unsigned gw = (unsigned)std::min<int64_t>((nt + 255) / 256, grid_max);
-        k_scan3_add<<<gw, 256, 0, s>>>(nt, om, op, od, bsum, nb, d_base + 2 * l, d_tot + 3 * l);
+        const unsigned gw = (unsigned)std::min<int64_t>((nv + 255) / 256, grid_max);
+        k_scan3_add<<<gw, 256, 0, s>>>(nv, vm, vp, vd, bsum, nb, d_base + 2 * l, d_tot + 3 * l);
+        FMM_LAUNCH(ctx);
+        k_target_offsets<<<(unsigned)std::min<int64_t>((nt + 256) / 256, grid_max), 256, 0, s>>>(nt, Sl, vm, vp, vd,
+                                                                                               om, op, od);
         FMM_LAUNCH(ctx);
         if (!fast) {   // sizes now: grow the outputs (keeping the earlier levels' entries)
             uint64_t tot[3];
@@ -507,21 +556,21 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
         uint64_t lenM = o.src_m->bytes / 4, lenP = o.src_p->bytes / 4, lenD = dcur->bytes / 4;
         if (fast && ctx->tc_tight) lenM = lenP = lenD = 16;   // tests: force the capacity-overflow redo
         if (slab) {
-            k_slab_gather<<<(unsigned)std::min<int64_t>((nt + 7) / 8, grid_max), 256, 0, s>>>(
-                nt, ovf, cm, cp, cd, om, op, od, slabM, slabP, slabD, capM, capP, capD, P_<uint32_t>(*o.src_m),
+            k_slab_gather<<<(unsigned)std::min<int64_t>((nv + 7) / 8, grid_max), 256, 0, s>>>(
+                nv, ovf, cm, cp, cd, vm, vp, vd, slabM, slabP, slabD, capM, capP, capD, P_<uint32_t>(*o.src_m),
                 P_<uint32_t>(*o.src_p), P_<uint32_t>(*dcur), lenM, lenP, lenD, d_err);
         } else {
             k_tct_level<1, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds,
-                                                              ctx->theta, cm, cp, cd, om, op, od,
+                                                              ctx->theta, cm, cp, cd, vm, vp, vd,
                                                               P_<uint32_t>(*o.src_m), P_<uint32_t>(*o.src_p),
                                                               P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf, nullptr, scap,
-                                                              0, 0, 0, d_err, lenM, lenP, lenD);
+                                                              0, 0, 0, d_err, Sl, lenM, lenP, lenD);
         }
         FMM_LAUNCH(ctx);
         k_tct_level<1, true><<<gwarps / TC_WARPS, TC_WARPS * 32, 0, s>>>(
-            tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds, ctx->theta, cm, cp, cd, om, op, od,
+            tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds, ctx->theta, cm, cp, cd, vm, vp, vd,
             P_<uint32_t>(*o.src_m), P_<uint32_t>(*o.src_p), P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf,
-            P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err, lenM, lenP, lenD);
+            P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err, Sl, lenM, lenP, lenD);
         FMM_LAUNCH(ctx);
         // this level's pass-down offsets (od, nt + 1 entries) are the next level's input
         doff_prev = od;
