@@ -526,9 +526,9 @@ class DistFMM:
         return out
 
     # 4-6 in one pass (solve): the upward pass runs on a side stream while the covers are
-    # exchanged and the LET structures planned, so each ring message carries structure AND data
-    # (one exchange instead of two) and every fragment is grafted, unpacked and traversed as it
-    # lands; the local traversal overlaps the first ring round
+    # exchanged, the LET structures planned and the local tree traversed, so each ring message
+    # carries structure AND data (one exchange instead of two) and every fragment is grafted,
+    # unpacked and traversed as it lands (round s+1 in flight meanwhile)
     def build_evaluate(self, lpos, lq):
         cm, K, F = self.comm, self.K, self.fmm
         nl = len(F)
@@ -571,6 +571,8 @@ class DistFMM:
                 pl.append((sb, d))
             sends.append(row)
             plans.append(pl)
+        for f in F:                       # local traversal overlaps the side-stream upward pass
+            f.dtt(remote=False)
         main.wait_event(up_done)
         for i, f in enumerate(F):
             me = cm.ranks[i]
@@ -591,8 +593,6 @@ class DistFMM:
 
         self._peers = [[] for _ in range(nl)]
         h = start(1) if K > 1 else None
-        for f in F:                       # local traversal overlaps the first ring round
-            f.dtt(remote=False)
         for sr in range(1, K):
             hh, src = h
             recv = hh.wait()
