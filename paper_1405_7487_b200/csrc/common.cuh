@@ -283,8 +283,6 @@ fmm_status lists_pass(fmm_ctx* ctx, cudaStream_t s);
 fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s);
 fmm_status tct_remote(fmm_ctx* ctx, const std::vector<uint32_t>& roots, cudaStream_t s);
 fmm_status tct_concat(fmm_ctx* ctx, cudaStream_t s);
-// dtt.cu: CSR lists -> packed (target << 32 | source) pairs, so remote traversals can append
-fmm_status lists_csr_to_packed(fmm_ctx* ctx, cudaStream_t s);
 // dtt.cu: P2P interaction count and source runs of the CSR lists (synchronises s)
 fmm_status lists_finish(fmm_ctx* ctx, cudaStream_t s);
 fmm_status build_lists(fmm_ctx* ctx, cudaStream_t s);

@@ -949,30 +949,6 @@ fmm_status lists_finish(fmm_ctx* ctx, cudaStream_t s) {
     return FMM_OK;
 }
 
-// CSR lists -> packed (target << 32 | source) words in list order, so that remote (LET)
-// traversals can append to them and lists_pass regroups everything
-__global__ void k_csr_to_packed(const uint64_t* __restrict__ off, int64_t nc, const uint32_t* __restrict__ src,
-                                uint64_t* __restrict__ lst) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nc; t += nw)
-        for (uint64_t p = off[t] + lane; p < off[t + 1]; p += 32) lst[p] = ((uint64_t)t << 32) | src[p];
-}
-
-fmm_status lists_csr_to_packed(fmm_ctx* ctx, cudaStream_t s) {
-    const int64_t nc = ctx->ncell;
-    FMM_TRY(buf_ensure(ctx, ctx->lst_m2l, (size_t)std::max<int64_t>(ctx->n_m2l, 1) * 8));
-    FMM_TRY(buf_ensure(ctx, ctx->lst_p2p, (size_t)std::max<int64_t>(ctx->n_p2p, 1) * 8));
-    const unsigned g = (unsigned)std::max<int64_t>(std::min<int64_t>((nc + 7) / 8, (int64_t)ctx->num_sms * 16), 1);
-    k_csr_to_packed<<<g, 256, 0, s>>>(P_<uint64_t>(ctx->m2l_off), nc, P_<uint32_t>(ctx->m2l_src), P_<uint64_t>(ctx->lst_m2l));
-    FMM_LAUNCH(ctx);
-    k_csr_to_packed<<<g, 256, 0, s>>>(P_<uint64_t>(ctx->p2p_off), nc, P_<uint32_t>(ctx->p2p_src), P_<uint64_t>(ctx->lst_p2p));
-    FMM_LAUNCH(ctx);
-    FMM_CUDA_TRY(ctx, cudaGetLastError());
-    ctx->lists_csr = false;
-    return FMM_OK;
-}
-
 fmm_status build_lists(fmm_ctx* ctx, cudaStream_t s) {
     const uint64_t root_pair = 0;
     FMM_TRY(dtt_pass(ctx, &root_pair, 1, false, s, -1));
