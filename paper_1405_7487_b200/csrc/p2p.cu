@@ -604,9 +604,10 @@ fmm_status p2p_t(fmm_ctx* ctx, cudaStream_t s) {
             return FMM_OK;
         };
         FMM_TRY(launch(k_p2p_cta<32, 64, 1>, lists, ctx->n_leaf_cls[0], counter));
-        // mid leaves: TMA bulk-copy staging (measured 3% faster at c2/c3); big leaves: cp.async
-        // (bulk copies measured 3% slower for the sphere's ~234-body leaves)
-        FMM_TRY(launch(k_p2p_tma<256, 2>, lists + ctx->nleaf, ctx->n_leaf_cls[1], counter + 1));
+        // mid leaves: TMA bulk-copy staging (measured 3% faster at c2/c3) of 512-body chunks
+        // (1.5% faster than 256, 1024 and 3 stages slower); big leaves: cp.async (bulk copies,
+        // also of 512-body chunks, measured 3-5% slower for the sphere's ~234-body leaves)
+        FMM_TRY(launch(k_p2p_tma<512, 2>, lists + ctx->nleaf, ctx->n_leaf_cls[1], counter + 1));
         FMM_TRY(launch(k_p2p_cta<128, 256, 4>, lists + 2 * ctx->nleaf, ctx->n_leaf_cls[2], counter + 2));
         FMM_CUDA_TRY(ctx, cudaGetLastError());
         return FMM_OK;
