@@ -249,6 +249,27 @@ def test_target_traversal_overflow_paths(torch_cuda, kind, monkeypatch):
         np.testing.assert_array_equal(grad_a.cpu().numpy(), grad_b.cpu().numpy())
 
 
+def test_random_rebuilds_one_context(torch_cuda):
+    """20 builds of random sizes and distributions on ONE context, in an order that makes the
+    size-learning fast paths (tree levels, traversal slots and buffers sized from the previous
+    build) meet both repeats and surprises (deeper trees, longer lists, wider levels): structure
+    bit-exact and fields at tolerance every time."""
+    from paper_1405_7487_b200 import FMM
+    rng = np.random.default_rng(2024)
+    f = FMM(16000, 4, 0.5, 16, "f64")
+    for it in range(20):
+        kind = ["cube", "plummer", "sphere"][int(rng.integers(3))]
+        n = int(rng.integers(1, 16001)) if it % 4 else 12000   # repeats of one size too
+        pos, q = synth.generate(kind, n, 100 + it if it % 4 else 7)
+        tp = torch_cuda.from_numpy(pos).cuda()
+        phi, grad = f.solve(tp, torch_cuda.from_numpy(q).cuda())
+        o = oracle.FMM(pos, q, 4, 0.5, 16).traverse()
+        check_structure(f, o)
+        ophi, ograd = o.evaluate()
+        assert oracle.rel_l2(phi.cpu().numpy(), ophi) <= 1e-12, (it, kind, n)
+        assert oracle.rel_l2(grad.cpu().numpy(), ograd) <= 1e-12, (it, kind, n)
+
+
 def test_repeat_builds_reuse_context(torch_cuda):
     # ONE context across sizes and distributions: workspace growth, and the back-to-back
     # traversal sized from the previous build (smaller, larger -> overflow fallback, deeper)
