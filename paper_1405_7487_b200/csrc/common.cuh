@@ -238,6 +238,17 @@ struct PhaseScope {
 // launch accounting
 #define FMM_LAUNCH(ctx) ((ctx)->launches++)
 
+// function attributes are per device: set once per (call site, device)
+#define FMM_FUNC_ATTR_ONCE(ctx, attr, value, ...)                                                   \
+    do {                                                                                           \
+        static unsigned long long done_mask_ = 0ull;                                               \
+        const unsigned long long bit_ = 1ull << ((ctx)->device & 63);                              \
+        if (!(done_mask_ & bit_)) {                                                                \
+            FMM_CUDA_TRY(ctx, cudaFuncSetAttribute(__VA_ARGS__, attr, value));                     \
+            done_mask_ |= bit_;                                                                    \
+        }                                                                                          \
+    } while (0)
+
 // Lanes whose BITS-bit digit d equals this lane's, among the lanes in `valid` (a ballot-based
 // multi-split: one vote per digit bit).  Same result as __match_any_sync restricted to `valid`;
 // MATCH.ANY measured far slower on sm_100 (top stall of the list and sort kernels).

@@ -589,24 +589,14 @@ fmm_status canonicalise(fmm_ctx* ctx, DevBuf& lst, int64_t n, uint32_t* tcnt, De
         }
         if (cc[1]) {
             constexpr size_t sm = wradix_smem<1024, 8>();
-            static bool attr1 = false;
-            if (!attr1) {
-                FMM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_segsort_wradix<1024, 8>,
-                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-                attr1 = true;
-            }
+            FMM_FUNC_ATTR_ONCE(ctx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm, k_segsort_wradix<1024, 8>);
             k_segsort_wradix<1024, 8><<<gwarps(cc[1], WR_WARPS), WR_WARPS * 32, sm, s>>>(
                 P_<uint64_t>(off), lists + (size_t)nc, cc[1], P_<uint32_t>(src), nbits);
             FMM_LAUNCH(ctx);
         }
         if (cc[2]) {
             constexpr size_t sm = wradix_smem<2048, 10>();
-            static bool attr2 = false;
-            if (!attr2) {
-                FMM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_segsort_wradix<2048, 10>,
-                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-                attr2 = true;
-            }
+            FMM_FUNC_ATTR_ONCE(ctx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm, k_segsort_wradix<2048, 10>);
             k_segsort_wradix<2048, 10><<<gwarps(cc[2], WR_WARPS), WR_WARPS * 32, sm, s>>>(
                 P_<uint64_t>(off), lists + 2 * (size_t)nc, cc[2], P_<uint32_t>(src), nbits);
             FMM_LAUNCH(ctx);

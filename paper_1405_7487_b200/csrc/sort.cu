@@ -339,11 +339,7 @@ fmm_status radix_sort_impl(fmm_ctx* ctx, uint64_t* k0, uint64_t* k1, uint32_t* v
         k_os_base<<<sh.n, RS_BINS, 0, s>>>(hist);
         FMM_LAUNCH(ctx);
         constexpr int smem = RS_TILE * (8 + (HAS_VAL ? 4 : 0));
-        static bool attr = false;
-        if (!attr) {
-            FMM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_os_pass<HAS_VAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            attr = true;
-        }
+        FMM_FUNC_ATTR_ONCE(ctx, cudaFuncAttributeMaxDynamicSharedMemorySize, smem, k_os_pass<HAS_VAL>);
         for (int p = 0; p < sh.n; ++p) {
             k_os_pass<HAS_VAL><<<(unsigned)ntiles, RS_THREADS, smem, s>>>(kin, kb, vin, vb, n, sh.s[p],
                                                                       hist + p * RS_BINS,
