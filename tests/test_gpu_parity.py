@@ -154,6 +154,23 @@ def test_errors(torch_cuda):
     with pytest.raises(FMMError) as ei:
         f.evaluate(p.clone(), q)   # not the built positions
     assert ei.value.status == FMM_ERR_STATE
+    # fmm_solve: the same argument checks; NaN positions fail before any work
+    with pytest.raises(FMMError) as ei:
+        f.solve(torch.rand((101, 3), dtype=torch.float64, device="cuda"), torch.rand(101, dtype=torch.float64,
+                                                                                      device="cuda"))
+    assert ei.value.status == FMM_ERR_ARG
+    with pytest.raises(FMMError) as ei:
+        f.solve(bad, q)
+    assert ei.value.status == FMM_ERR_NONFINITE
+    from paper_1405_7487_b200.fmm import lib
+    import ctypes as C
+    assert lib().fmm_solve(f._h, C.c_void_p(p.data_ptr()), None, 10, C.c_void_p(q.data_ptr()),
+                           C.c_void_p(q.data_ptr()), None) == FMM_ERR_ARG   # null q
+    phi0, grad0 = f.solve(p[:0].contiguous(), q[:0].contiguous())   # n = 0: a no-op
+    assert phi0.numel() == 0 and grad0.numel() == 0
+    phi, grad = f.solve(p, q)   # and the context still works
+    o = oracle.FMM(p.cpu().numpy(), q.cpu().numpy(), 4, 0.5, 8).traverse()
+    assert oracle.rel_l2(phi.cpu().numpy(), o.evaluate()[0]) <= 1e-12
 
 
 def test_solve_host_matches_device(torch_cuda):
