@@ -174,7 +174,7 @@ struct fmm_ctx {
     bool lists_csr = false;     // lists came from tct (CSR only; no packed pair list)
     int dtt_mode = 0;           // 0: target-ordered traversal (tct.cu), 1: breadth-first (FMM_DTT=bfs)
     int64_t dtt_est_front = 0, dtt_est_m2l = 0, dtt_est_p2p = 0;   // buffer sizes learnt from the last build
-    // P2P source runs: runs[n_runs] = {start body, flat offset}, then rtot[ncell]; run_off[ncell+1]
+    // P2P source runs: runs[n_runs] = {start body, flat offset}; run_off[ncell+1] (+1 spare), then rtot[ncell]
     int64_t n_runs = 0;
     DevBuf runs, run_off, run_tmp, run_pre, run_len64, dcount2, tcnt, cnt64, big_off, seg_lists;
     DevBuf leaf_cls;                    // leaves by P2P size class c at [c nleaf, (c+1) nleaf): tiny, mid, big

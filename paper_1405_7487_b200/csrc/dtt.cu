@@ -641,43 +641,63 @@ fmm_status canonicalise(fmm_ctx* ctx, DevBuf& lst, int64_t n, uint32_t* tcnt, De
 // target's source stream}; rtot[t] = total sources of target t.  Used by the P2P kernel to
 // stream a target's sources as full fixed-size chunks.
 // warp per target: a list entry starts a new run unless its body range begins where the
-// previous entry's ends
-__global__ void k_run_flags(const uint64_t* __restrict__ off, const uint32_t* __restrict__ src, int64_t ncell,
-                            const uint32_t* __restrict__ bb, const uint32_t* __restrict__ bc,
-                            uint32_t* __restrict__ flag) {
-    const int lane = threadIdx.x & 31;
-    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t t = w0; t < ncell; t += nw) {
-        const uint64_t p0 = off[t], p1 = off[t + 1];
-        for (uint64_t p = p0 + lane; p < p1; p += 32) {
-            const uint32_t sc = src[p];
-            uint32_t f = 1;
-            if (p > p0) {
-                const uint32_t pv = src[p - 1];
-                f = bb[pv] + bc[pv] != bb[sc];
-            }
-            flag[p] = f;
-        }
-    }
+// previous entry's ends.  Two passes over the lists: count the runs of every target (and its
+// source total), scan the per-target counts into run_off, then emit the runs at those offsets.
+__device__ __forceinline__ unsigned run_starts(const uint32_t* __restrict__ bb, const uint32_t* __restrict__ bc,
+                                               uint32_t sc, bool ok, uint32_t& prev_end, int lane) {
+    // body range end of the previous entry: the lane before, or the last entry of the previous round
+    const uint32_t b = ok ? bb[sc] : 0u, e = ok ? b + bc[sc] : 0u;
+    uint32_t pe = __shfl_up_sync(0xffffffffu, e, 1);
+    if (lane == 0) pe = prev_end;
+    prev_end = __shfl_sync(0xffffffffu, e, 31);
+    return __ballot_sync(0xffffffffu, ok && pe != b);
 }
 
-// warp per target: flat source offsets are a warp scan of the body counts
-__global__ void k_run_emit(const uint64_t* __restrict__ off, const uint32_t* __restrict__ src, int64_t ncell,
-                           const uint32_t* __restrict__ bb, const uint32_t* __restrict__ bc,
-                           const uint32_t* __restrict__ flag, const uint32_t* __restrict__ rid,
-                           uint2* __restrict__ runs, uint32_t* __restrict__ roff, uint32_t* __restrict__ rtot,
-                           unsigned long long* __restrict__ inter) {
+__global__ void k_run_count(const uint64_t* __restrict__ off, const uint32_t* __restrict__ src, int64_t ncell,
+                            const uint32_t* __restrict__ bb, const uint32_t* __restrict__ bc,
+                            uint32_t* __restrict__ nrun, uint32_t* __restrict__ rtot,
+                            unsigned long long* __restrict__ inter) {
     const int lane = threadIdx.x & 31;
     unsigned long long my_inter = 0;   // lane 0: sum over this warp's targets of |T| * sources(T)
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t t = w0; t < ncell; t += nw) {
         const uint64_t p0 = off[t], p1 = off[t + 1];
-        if (lane == 0) roff[t] = p0 < p1 ? rid[p0] : (p0 > 0 ? rid[p0 - 1] + flag[p0 - 1] : 0u);
-        uint32_t carry = 0;
+        uint32_t prev_end = ~0u, runs = 0, tot = 0;
         for (uint64_t q0 = p0; q0 < p1; q0 += 32) {
             const uint64_t p = q0 + lane;
             const bool ok = p < p1;
             const uint32_t sc = ok ? src[p] : 0u;
+            runs += __popc(run_starts(bb, bc, sc, ok, prev_end, lane));
+            uint32_t c = ok ? bc[sc] : 0u;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            tot += c;
+        }
+        if (lane == 0) {
+            nrun[t] = runs;
+            rtot[t] = tot;
+            my_inter += (unsigned long long)tot * bc[t];
+        }
+    }
+    if (lane == 0 && my_inter) atomicAdd(inter, my_inter);
+}
+
+// warp per target: runs at roff[t] + (rank among the round's run starts); flat source offsets
+// are a warp scan of the body counts
+__global__ void k_run_emit(const uint64_t* __restrict__ off, const uint32_t* __restrict__ src, int64_t ncell,
+                           const uint32_t* __restrict__ bb, const uint32_t* __restrict__ bc,
+                           const uint32_t* __restrict__ roff, uint2* __restrict__ runs) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = w0; t < ncell; t += nw) {
+        const uint64_t p0 = off[t], p1 = off[t + 1];
+        uint32_t prev_end = ~0u, carry = 0, r = roff[t];
+        for (uint64_t q0 = p0; q0 < p1; q0 += 32) {
+            const uint64_t p = q0 + lane;
+            const bool ok = p < p1;
+            const uint32_t sc = ok ? src[p] : 0u;
+            const unsigned st = run_starts(bb, bc, sc, ok, prev_end, lane);
             const uint32_t c = ok ? bc[sc] : 0u;
             uint32_t x = c;
 #pragma unroll
@@ -685,18 +705,13 @@ __global__ void k_run_emit(const uint64_t* __restrict__ off, const uint32_t* __r
                 const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
                 if (lane >= o) x += y;
             }
-            if (ok && flag[p]) runs[rid[p]] = make_uint2(bb[sc], carry + x - c);
+            if ((st >> lane) & 1u) runs[r + __popc(st & lt)] = make_uint2(bb[sc], carry + x - c);
+            r += __popc(st);
             carry += __shfl_sync(0xffffffffu, x, 31);
         }
-        if (lane == 0) {
-            rtot[t] = carry;
-            my_inter += (unsigned long long)carry * bc[t];
-        }
     }
-    if (lane == 0 && my_inter) atomicAdd(inter, my_inter);
 }
 
-__global__ void k_run_last(int64_t ncell, uint32_t nr, uint32_t* __restrict__ roff) { roff[ncell] = nr; }
 
 // leaves split by size for the P2P kernel: tiny leaves (<= P2P_TINY_LEAF bodies) to a warp per
 // leaf, mid-size to a 128-thread CTA with 2 target pairs per thread, big leaves
@@ -734,17 +749,21 @@ __global__ void k_leaf_split(const uint32_t* __restrict__ leaf_ids, int64_t nlea
 }
 
 fmm_status build_runs(fmm_ctx* ctx, cudaStream_t s) {
-    const int64_t n = ctx->n_p2p, nc = ctx->ncell;
-    FMM_TRY(buf_ensure(ctx, ctx->run_tmp, (size_t)std::max<int64_t>(n, 1) * 4 * 2 + 64));
-    uint32_t* flag = P_<uint32_t>(ctx->run_tmp);
-    uint32_t* rid = flag + n;
-    uint32_t* d_nr = P_<uint32_t>(ctx->dcount2);
+    const int64_t nc = ctx->ncell;
+    FMM_TRY(buf_ensure(ctx, ctx->run_tmp, (size_t)(nc + 1) * 4 + 64));
+    FMM_TRY(buf_ensure(ctx, ctx->run_off, (size_t)(2 * nc + 3) * 4));
+    uint32_t* nrun = P_<uint32_t>(ctx->run_tmp);
+    uint32_t* roff = P_<uint32_t>(ctx->run_off);
+    uint32_t* rtot = roff + nc + 2;   // see common.cuh
     const uint64_t* off = P_<uint64_t>(ctx->p2p_off);
     const uint32_t* src = P_<uint32_t>(ctx->p2p_src);
     const int g = (int)std::min<int64_t>((nc + 3) / 4, (int64_t)ctx->num_sms * 16);
-    k_run_flags<<<std::max(g, 1), 128, 0, s>>>(off, src, nc, P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), flag);
+    unsigned long long* d_inter = P_<unsigned long long>(ctx->dcount2) + 2;   // read lazily (fmm_get_counts)
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_inter, 0, 8, s));
+    k_run_count<<<std::max(g, 1), 128, 0, s>>>(off, src, nc, P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), nrun,
+                                              rtot, d_inter);
     FMM_LAUNCH(ctx);
-    FMM_TRY(scan_exclusive_u32(ctx, flag, rid, n, d_nr, s));
+    FMM_TRY(scan_exclusive_u32(ctx, nrun, roff, nc, roff + nc, s));
     // P2P leaf classes (see k_leaf_split); the counts ride on the same host round trip
     FMM_TRY(buf_ensure(ctx, ctx->leaf_cls, (size_t)3 * std::max<int64_t>(ctx->nleaf, 1) * 4));
     unsigned* d_lc = P_<unsigned>(ctx->dcount2) + 16;   // u32 16..19 (0: runs, 4..5: inter, 8..12: classes)
@@ -757,22 +776,15 @@ fmm_status build_runs(fmm_ctx* ctx, cudaStream_t s) {
         ctx->launches += 2;
     }
     uint32_t hr[4] = {0, 0, 0, 0};
-    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&hr[0], d_nr, 4, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&hr[0], roff + nc, 4, cudaMemcpyDeviceToHost, s));
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(&hr[1], d_lc, 12, cudaMemcpyDeviceToHost, s));
     FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
     const uint32_t nr = hr[0];
     for (int c = 0; c < 3; ++c) ctx->n_leaf_cls[c] = hr[1 + c];
     ctx->n_runs = nr;
-    FMM_TRY(buf_ensure(ctx, ctx->run_off, (size_t)(nc + 2) * 4));
-    FMM_TRY(buf_ensure(ctx, ctx->runs, (size_t)std::max<uint32_t>(nr, 1) * 8 + (size_t)(nc + 1) * 4 + 64));
-    uint2* runs = P_<uint2>(ctx->runs);
-    uint32_t* rtot = reinterpret_cast<uint32_t*>(runs + std::max<uint32_t>(nr, 1));
-    unsigned long long* d_inter = P_<unsigned long long>(ctx->dcount2) + 2;   // read lazily (fmm_get_counts)
-    FMM_CUDA_TRY(ctx, cudaMemsetAsync(d_inter, 0, 8, s));
-    k_run_emit<<<std::max(g, 1), 128, 0, s>>>(off, src, nc, P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), flag, rid,
-                                             runs, P_<uint32_t>(ctx->run_off), rtot, d_inter);
-    FMM_LAUNCH(ctx);
-    k_run_last<<<1, 1, 0, s>>>(nc, nr, P_<uint32_t>(ctx->run_off));
+    FMM_TRY(buf_ensure(ctx, ctx->runs, (size_t)std::max<uint32_t>(nr, 1) * 8 + 64));
+    k_run_emit<<<std::max(g, 1), 128, 0, s>>>(off, src, nc, P_<uint32_t>(ctx->c_bb), P_<uint32_t>(ctx->c_bc), roff,
+                                             P_<uint2>(ctx->runs));
     FMM_LAUNCH(ctx);
     FMM_CUDA_TRY(ctx, cudaGetLastError());
     return FMM_OK;

@@ -590,7 +590,7 @@ fmm_status p2p_t(fmm_ctx* ctx, cudaStream_t s) {
         unsigned long long* counter = P_<unsigned long long>(ctx->cnt_tmp2);
         FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 24, s));
         const uint2* runs = P_<uint2>(ctx->runs);
-        const uint32_t* rtot = reinterpret_cast<const uint32_t*>(runs + std::max<int64_t>(ctx->n_runs, 1));
+        const uint32_t* rtot = P_<uint32_t>(ctx->run_off) + ctx->ncell + 2;
         const uint32_t* lists = P_<uint32_t>(ctx->leaf_cls);
         auto launch = [&](auto kern, const uint32_t* ids, int64_t cnt, unsigned long long* ctr) -> fmm_status {
             if (cnt == 0) return FMM_OK;
