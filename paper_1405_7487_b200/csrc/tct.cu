@@ -35,9 +35,18 @@ struct Cells {
 };
 
 // outcome of (T, s): 0 M2L, 1 P2P, 2 split T (s passed down), 3 split s (its children visited)
+// the child count is loaded with the centre, before the MAC test needs neither (one round trip;
+// a plain load is sunk into the non-MAC branch by the compiler, a second round trip for ~80% of
+// the candidates)
+__device__ __forceinline__ uint32_t ld_early_u32(const uint32_t* p) {
+    uint32_t r;
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+
 __device__ __forceinline__ int tc_classify(const double4 T, uint32_t nT, const Cells& v, uint32_t s, double theta) {
+    const uint32_t nB = ld_early_u32(v.cc + s);
     const double4 B = v.cr[s];
-    const uint32_t nB = v.cc[s];   // loaded with the centre (one round trip)
     const double dx = __dsub_rn(T.x, B.x), dy = __dsub_rn(T.y, B.y), dz = __dsub_rn(T.z, B.z);
     const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
     if (__dadd_rn(T.w, B.w) < __dmul_rn(theta, __dsqrt_rn(d2))) return 0;
@@ -162,12 +171,18 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
         for (int gen = 0; gen == 0 || ncur > 0; ++gen) {
             uint32_t* nxt = cur ? list0 : list1;
             uint32_t nnext = 0;
-            for (; gen == 0 && xp < x1; xp += 32) {
-                const uint64_t i = xp + (uint64_t)lane;
-                const bool act = i < x1;
-                const uint32_t s = act ? (doff_prev ? dsrc_prev[i] : seeds[i]) : 0u;
-                const int oc = act ? tc_classify(T, nT, v, s, theta) : -1;
-                put(oc, s, act, nxt, nnext);
+            if (gen == 0 && xp < x1) {
+                // the next round's source ids are loaded before this round is classified
+                const uint32_t* ids = doff_prev ? dsrc_prev : seeds;
+                uint32_t s_next = xp + lane < x1 ? ids[xp + lane] : 0u;
+                for (; xp < x1; xp += 32) {
+                    const uint64_t i = xp + (uint64_t)lane;
+                    const bool act = i < x1;
+                    const uint32_t s = s_next;
+                    if (i + 32 < x1) s_next = ids[i + 32];
+                    const int oc = act ? tc_classify(T, nT, v, s, theta) : -1;
+                    put(oc, s, act, nxt, nnext);
+                }
             }
             // generation g >= 1: the children of the sources generation g-1 split, in (source,
             // child) order, flattened over the lanes: a round of 32 split sources is expanded into its
