@@ -15,7 +15,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", "-DNDEBUG"]
 # per-file extra flags (P2P: flush denormals so rsqrt is a single MUFU.RSQ)
-EXTRA = {"p2p.cu": ["-ftz=true"], "m2l.cu": ["-ftz=true"]}
+EXTRA = {"p2p.cu": ["-ftz=true"], "p2p_mutual.cu": ["-ftz=true"], "m2l.cu": ["-ftz=true"]}
 
 
 def sources():

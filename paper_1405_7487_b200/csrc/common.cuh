@@ -101,6 +101,9 @@ struct fmm_ctx {
     bool use_fast_m2l = true;
     bool use_fast_p2p = true;   // fp32 grouped P2P (FMM_P2P_GENERIC=1 disables)
     int p2p_variant = 0;
+    int p2p_mutual = 0;         // mutual P2P (p2p_mutual.cu): 0 off, 1 on, 2 auto (mean leaf >= P2P_BIG_LEAF)
+    bool mut_ready = false;     // this build's mirror indices / reaction slots are prepared
+    DevBuf mut_mir, mut_w, mut_so, mut_slot;
     int m2l_variant = 0;        // fp32 register M2L: 0 mirror-paired f32x2, 1 scalar (FMM_M2L_VARIANT)
     int p2p_np = 2;             // CTA P2P: target pairs per thread (FMM_P2P_NP = 1, 2, 4)        // 0: CTA per leaf over source runs, 1: warp per leaf (FMM_P2P_VARIANT)
     int m2l_part = 0;            // m2l_pass: 0 all, 1 operand preparation only, 2 without it (fmm_solve split)
@@ -296,6 +299,8 @@ fmm_status tct_remote(fmm_ctx* ctx, const std::vector<uint32_t>& roots, cudaStre
 fmm_status tct_concat(fmm_ctx* ctx, cudaStream_t s);
 // dtt.cu: P2P interaction count and source runs of the CSR lists (synchronises s)
 fmm_status lists_finish(fmm_ctx* ctx, cudaStream_t s);
+fmm_status p2p_mutual_prep(fmm_ctx* ctx, cudaStream_t s);
+fmm_status p2p_mutual(fmm_ctx* ctx, cudaStream_t s);
 fmm_status build_lists(fmm_ctx* ctx, cudaStream_t s);
 // let.cu
 fmm_status let_cover(fmm_ctx* ctx, double* cover, int* ncover, cudaStream_t s);

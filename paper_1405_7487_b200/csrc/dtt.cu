@@ -948,6 +948,11 @@ fmm_status lists_pass(fmm_ctx* ctx, cudaStream_t s) {
 fmm_status lists_finish(fmm_ctx* ctx, cudaStream_t s) {
     FMM_TRY(build_runs(ctx, s));   // synchronises s; the interaction count stays on the device
     ctx->p2p_inter = -1;
+    // mutual P2P (p2p_mutual.cu): on request, or (auto) for large leaves
+    const bool mut = ctx->p2p_mutual == 1 ||
+                     (ctx->p2p_mutual == 2 && ctx->nleaf > 0 && ctx->n >= (int64_t)P2P_BIG_LEAF * ctx->nleaf);
+    ctx->mut_ready = false;
+    if (mut) FMM_TRY(p2p_mutual_prep(ctx, s));
     return FMM_OK;
 }
 

@@ -582,6 +582,7 @@ fmm_status p2p_t(fmm_ctx* ctx, cudaStream_t s) {
     FMM_TRY(buf_ensure(ctx, ctx->near_phi, (size_t)ctx->n * sizeof(Real)));
     FMM_TRY(buf_ensure(ctx, ctx->near_grad, (size_t)ctx->n * 3 * sizeof(Real)));
     PhaseScope pk(ctx, PH_P2P_KERNEL, s);
+    if (std::is_same<Real, float>::value && ctx->mut_ready) return p2p_mutual(ctx, s);
     if (std::is_same<Real, float>::value && ctx->use_fast_p2p && ctx->p2p_variant == 0) {
         // three leaf classes (k_leaf_split): tiny (<= P2P_TINY_LEAF) a warp per leaf, mid a CTA with
         // 2 target pairs per thread, big (>= P2P_BIG_LEAF) a CTA with 4 (measured: mean-8 leaves
