@@ -16,6 +16,8 @@
 // |S| over the entries with S > A) and added by k_mut_react to S's near field, in S's list
 // order: every sum has a fixed order, results are bit-reproducible.  The self pair (A, A) takes
 // the one-sided form with the r^2 > 0 test (R17: coincident points share a leaf).
+// Opt-in (FMM_P2P_MUTUAL): the mirror search scans the source's list per entry (fine for the
+// sphere's ~45-entry lists, slow for c3's ~230) and slots over 8 GB fall back to one-sided P2P.
 #include "common.cuh"
 
 namespace {
