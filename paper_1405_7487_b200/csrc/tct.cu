@@ -330,35 +330,32 @@ __global__ void __launch_bounds__(S3_THREADS) k_scan3_top(uint64_t* __restrict__
     }
 }
 
+// adds the tile bases; the first slice of every target also lands in the targets' CSR offsets
+// (om/op: m2l_off/p2p_off + tb; od: the level's pass-down offsets, nt + 1 entries)
 __global__ void k_scan3_add(int64_t n, uint64_t* __restrict__ o0, uint64_t* __restrict__ o1, uint64_t* __restrict__ o2,
                             const uint64_t* __restrict__ bsum, int64_t nb, const uint64_t* __restrict__ base,
-                            const unsigned long long* __restrict__ tot) {
+                            const unsigned long long* __restrict__ tot, int S, int64_t nt, uint64_t* __restrict__ om,
+                            uint64_t* __restrict__ op, uint64_t* __restrict__ od) {
     const uint64_t base0 = base[0], base1 = base[1];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const int64_t b = i / S3_TILE;
-        o0[i] += base0 + bsum[b];
-        o1[i] += base1 + bsum[nb + b];
-        o2[i] += bsum[2 * nb + b];
+        const uint64_t v0 = o0[i] + base0 + bsum[b], v1 = o1[i] + base1 + bsum[nb + b], v2 = o2[i] + bsum[2 * nb + b];
+        o0[i] = v0;
+        o1[i] = v1;
+        o2[i] = v2;
+        if (i % S == 0) {
+            const int64_t t = i / S;
+            om[t] = v0;
+            op[t] = v1;
+            od[t] = v2;
+        }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         o0[n] = base0 + tot[0];
         o1[n] = base1 + tot[1];
         o2[n] = tot[2];
-    }
-}
-
-// per-target CSR offsets from the (target, slice) offsets: the target's first slice
-__global__ void k_target_offsets(int64_t nt, int S, const uint64_t* __restrict__ vm, const uint64_t* __restrict__ vp,
-                                 const uint64_t* __restrict__ vd, uint64_t* __restrict__ om, uint64_t* __restrict__ op,
-                                 uint64_t* __restrict__ od) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t <= nt; t += stride) {
-        if (t < nt) {
-            om[t] = vm[t * S];
-            op[t] = vp[t * S];
-        }
-        od[t] = vd[t * S];
+        od[nt] = tot[2];
     }
 }
 
@@ -552,10 +549,7 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
         k_scan3_top<<<1, S3_THREADS, 0, s>>>(bsum, nb, d_tot + 3 * l, d_base + 2 * l, d_base + 2 * (l + 1));
         FMM_LAUNCH(ctx);
         const unsigned gw = (unsigned)std::min<int64_t>((nv + 255) / 256, grid_max);
-        k_scan3_add<<<gw, 256, 0, s>>>(nv, vm, vp, vd, bsum, nb, d_base + 2 * l, d_tot + 3 * l);
-        FMM_LAUNCH(ctx);
-        k_target_offsets<<<(unsigned)std::min<int64_t>((nt + 256) / 256, grid_max), 256, 0, s>>>(nt, Sl, vm, vp, vd,
-                                                                                               om, op, od);
+        k_scan3_add<<<gw, 256, 0, s>>>(nv, vm, vp, vd, bsum, nb, d_base + 2 * l, d_tot + 3 * l, Sl, nt, om, op, od);
         FMM_LAUNCH(ctx);
         if (!fast) {   // sizes now: grow the outputs (keeping the earlier levels' entries)
             uint64_t tot[3];
