@@ -159,18 +159,23 @@ __global__ void __launch_bounds__(LP_WARPS * 32) k_l2p_t(const Body* __restrict_
                                                           const Real* __restrict__ near_grad, Real* __restrict__ phi,
                                                           Real* __restrict__ grad, double4* __restrict__ far) {
     constexpr int NC = P * (P + 1) * (P + 2) / 6;
-    __shared__ double s_L[LP_WARPS][NC];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int64_t li = (int64_t)blockIdx.x * LP_WARPS + w; li < nleaf; li += (int64_t)gridDim.x * LP_WARPS) {
-        const uint32_t c = leaf_ids[li];
+    // two leaves per warp, a half-warp each (small Plummer leaves fill a half-warp; the halves'
+    // broadcast reads of their own L copies fall in different banks, one wavefront)
+    __shared__ double s_L[LP_WARPS][2][NC];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, half = lane >> 4, hl = lane & 15;
+    for (int64_t lp = (int64_t)blockIdx.x * LP_WARPS + w; 2 * lp < nleaf; lp += (int64_t)gridDim.x * LP_WARPS) {
+        const int64_t li = 2 * lp + half;
+        const bool has = li < nleaf;
+        const uint32_t c = has ? leaf_ids[li] : leaf_ids[2 * lp];
         const double4 ctr = cr[c];
         __syncwarp();
-        for (int k = lane; k < NC; k += 32) s_L[w][k] = L[(int64_t)c * NC + k];
+        if (has)
+            for (int k = hl; k < NC; k += 16) s_L[w][half][k] = L[(int64_t)c * NC + k];
         __syncwarp();
-        const double* Ls = s_L[w];
-        const uint32_t b0 = bb[c], nb = bc[c];
-        for (uint32_t j0 = 0; j0 < nb; j0 += 32) {
-            const uint32_t j = j0 + lane;
+        const double* Ls = s_L[w][half];
+        const uint32_t b0 = bb[c], nb = has ? bc[c] : 0u;
+        for (uint32_t j0 = 0; j0 < nb; j0 += 16) {
+            const uint32_t j = j0 + hl;
             if (j >= nb) continue;
             const Body p = body[b0 + j];
             const double z[3] = {(double)p.x - ctr.x, (double)p.y - ctr.y, (double)p.z - ctr.z};
