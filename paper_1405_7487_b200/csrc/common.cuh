@@ -144,6 +144,7 @@ struct fmm_ctx {
     DevBuf key_a, key_b, idx_a, idx_b, sort_counts, scan_tmp, red_tmp;
     uint64_t* d_keys = nullptr;   // sorted keys (points into key_a or key_b)
     uint32_t* d_perm = nullptr;   // perm (points into idx_a or idx_b)
+    DevBuf iperm;                 // inverse of d_perm (gather_bodies_q), for the output merge
     DevBuf body;                  // sorted (x,y,z,q): float4 (F32) or double4-like (F64)
 
     // cells (SoA, BFS order)

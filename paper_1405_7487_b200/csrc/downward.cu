@@ -228,19 +228,20 @@ __global__ void __launch_bounds__(LP_WARPS * 32) k_l2p_t(const Body* __restrict_
 }
 
 // R18 with the far field kept separately (L2P ran concurrently with P2P): the same sums as the
-// fused L2P epilogue, (Real)(far + (double)near), scattered to the caller's order
+// fused L2P epilogue, (Real)(far + (double)near), in the caller's order
 template <typename Real>
-__global__ void k_merge_nearfar(int64_t n, const uint32_t* __restrict__ perm, const double4* __restrict__ far,
+__global__ void k_merge_nearfar(int64_t n, const uint32_t* __restrict__ iperm, const double4* __restrict__ far,
                                 const Real* __restrict__ near_phi, const Real* __restrict__ near_grad,
                                 Real* __restrict__ phi, Real* __restrict__ grad) {
+    // caller order o, sorted index i = iperm[o]: gathered reads, coalesced writes
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n; o += stride) {
+        const int64_t i = iperm[o];
         const double4 f = far[i];
-        const uint32_t o = perm[i];
         phi[o] = (Real)(f.x + (double)near_phi[i]);
-        grad[3 * (int64_t)o + 0] = (Real)(f.y + (double)near_grad[3 * i + 0]);
-        grad[3 * (int64_t)o + 1] = (Real)(f.z + (double)near_grad[3 * i + 1]);
-        grad[3 * (int64_t)o + 2] = (Real)(f.w + (double)near_grad[3 * i + 2]);
+        grad[3 * o + 0] = (Real)(f.y + (double)near_grad[3 * i + 0]);
+        grad[3 * o + 1] = (Real)(f.z + (double)near_grad[3 * i + 1]);
+        grad[3 * o + 2] = (Real)(f.w + (double)near_grad[3 * i + 2]);
     }
 }
 
@@ -287,7 +288,7 @@ template <typename Real>
 fmm_status merge_t(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s) {
     PhaseScope ps(ctx, PH_DOWN, s);
     const int g = (int)std::min<int64_t>((ctx->n + 255) / 256, (int64_t)ctx->num_sms * 8);
-    k_merge_nearfar<Real><<<std::max(g, 1), 256, 0, s>>>(ctx->n, ctx->d_perm, P_<double4>(ctx->far),
+    k_merge_nearfar<Real><<<std::max(g, 1), 256, 0, s>>>(ctx->n, P_<uint32_t>(ctx->iperm), P_<double4>(ctx->far),
                                                          P_<Real>(ctx->near_phi), P_<Real>(ctx->near_grad),
                                                          (Real*)phi, (Real*)grad);
     FMM_LAUNCH(ctx);

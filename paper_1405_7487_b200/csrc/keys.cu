@@ -196,6 +196,14 @@ fmm_status build_keys(fmm_ctx* ctx, const void* pos, int64_t n, cudaStream_t s) 
     return build_keys_t<double>(ctx, (const double*)pos, n, s);
 }
 
+namespace {
+// iperm[perm[i]] = i: the output merge gathers in the caller's order (coalesced writes)
+__global__ void k_invert_perm(const uint32_t* __restrict__ perm, int64_t n, uint32_t* __restrict__ iperm) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) iperm[perm[i]] = (uint32_t)i;
+}
+}  // namespace
+
 fmm_status gather_bodies_q(fmm_ctx* ctx, const void* q, cudaStream_t s) {
     int64_t n = ctx->n;
     const int gblk = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8);
@@ -203,6 +211,9 @@ fmm_status gather_bodies_q(fmm_ctx* ctx, const void* q, cudaStream_t s) {
         k_gather_q<float><<<gblk, 256, 0, s>>>((const float*)q, ctx->d_perm, n, P_<float4>(ctx->body));
     else
         k_gather_q<double><<<gblk, 256, 0, s>>>((const double*)q, ctx->d_perm, n, P_<dbody>(ctx->body));
+    FMM_LAUNCH(ctx);
+    FMM_TRY(buf_ensure(ctx, ctx->iperm, (size_t)std::max<int64_t>(n, 1) * 4));
+    k_invert_perm<<<gblk, 256, 0, s>>>(ctx->d_perm, n, P_<uint32_t>(ctx->iperm));
     FMM_LAUNCH(ctx);
     FMM_CUDA_TRY(ctx, cudaGetLastError());
     return FMM_OK;
