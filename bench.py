@@ -43,11 +43,7 @@ FP32_LANES_PER_SM = 128
 
 
 # ----------------------------------------------------------- algorithmic work
-from paper_1405_7487_b200.costs import m2l_flops_per_pair, t2n  # noqa: E402,F401
-
-
-P2P_FLOPS = 20      # 3 sub, |r|^2 (3 mul 2 add), rsqrt, q/r, q/r^3 (2 mul), phi add, 3 fma grad
-P2P_INSTR = 13      # FP32-pipe instructions per interaction (SASS, -ftz)
+from paper_1405_7487_b200.costs import P2P_FLOPS, P2P_INSTR, m2l_flops_per_pair, t2n  # noqa: E402,F401
 
 
 def peaks():
@@ -118,10 +114,24 @@ def oracle_rate(cfg: dict, n_sample: int, reps: int = 1):
     return n_sample, times
 
 
+def host_cpu():
+    """Host CPU model and logical core count (lscpu / os.cpu_count) for the oracle's baseline."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except (OSError, subprocess.TimeoutExpired):
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
+
+
 def cpu_baseline(cfg):
     n_s = 1 << 14
     n, times = oracle_rate(cfg, n_s)
-    return {"value": n / times[0], "unit": "particles/s", "cores": 1, "kind": "oracle",
+    return {"value": n / times[0], "unit": "particles/s", "cores": 1, "kind": "oracle", "host": host_cpu(),
             "sample": f"full oracle FMM (keys..L2P) on {n} particles of the {cfg['kind']} distribution with the "
                       f"workload's P={cfg['P']}, theta={cfg['theta']}, ncrit={cfg['ncrit']}; single-threaded fp64 "
                       f"C, {times[0]:.1f} s"}
@@ -139,7 +149,7 @@ def run_reference(args, cfg, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(cfg, args, world),
-            "cpu_baseline": {"value": n / t, "unit": "particles/s", "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": n / t, "unit": "particles/s", "cores": 1, "kind": "oracle", "host": host_cpu(),
                              "sample": f"full oracle FMM on {n} particles of the workload's distribution and "
                                        f"parameters per step"},
             "e2e": {"value": n / t, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -165,34 +175,46 @@ def workload_config(cfg, args, world=1):
 
 
 def roofline_block(args, cfg, counts, ph):
+    """Dominant kernel against the FP32 ALU peak.  `achieved` counts
+    algorithmic flops (P2P: 18 per interaction, FFMA = 2; M2L: the harmonic form's FMA + recurrence
+    ops, costs.py); P2P's primary figure, the FP32 issue-slot fraction (13 lane-ops per interaction),
+    is reported beside it as `fp32_issue_frac`."""
     pk = peaks()
     sm_mhz = pk["sm_max_mhz"]
     fp32_peak_tflops = 148 * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12     # FFMA = 2 flops
+    lane_peak = 148 * FP32_LANES_PER_SM * sm_mhz * 1e6                         # lane-ops/s
     m2l = m2l_flops_per_pair(cfg["P"])
     m2l_ms = ph.get("m2l_kernel", 0.0) / args.steps
     p2p_ms = ph.get("p2p_kernel", 0.0) / args.steps
     m2l_tf = counts["n_m2l"] * m2l["flops"] / (m2l_ms * 1e-3) / 1e12 if m2l_ms else 0.0
     p2p_tf = counts["p2p_interactions"] * P2P_FLOPS / (p2p_ms * 1e-3) / 1e12 if p2p_ms else 0.0
+    p2p_issue = counts["p2p_interactions"] * P2P_INSTR / (p2p_ms * 1e-3) / lane_peak if p2p_ms else None
+    m2l_issue = counts["n_m2l"] * m2l["instr"] / (m2l_ms * 1e-3) / lane_peak if m2l_ms else None
     dom = "m2l" if m2l_ms >= p2p_ms else "p2p"
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(f"{args.config}:{dom}")
-    return {"kernel": f"{dom} ({'k_m2l_mir' if dom == 'm2l' else 'k_p2p_tma + k_p2p_cta (leaf classes)'})", "bound": "alu",
-            "achieved": round(m2l_tf if dom == "m2l" else p2p_tf, 3), "peak": round(fp32_peak_tflops, 2),
-            "unit": "TFLOP/s", "frac": round((m2l_tf if dom == "m2l" else p2p_tf) / fp32_peak_tflops, 4),
-            "traffic": traffic,
+    ach = m2l_tf if dom == "m2l" else p2p_tf
+    return {"kernel": f"{dom} ({'k_m2l_mir' if dom == 'm2l' else 'k_p2p_tma + k_p2p_cta (leaf classes)'})",
+            "bound": "alu", "achieved": round(ach, 3), "peak": round(fp32_peak_tflops, 2),
+            "unit": "TFLOP/s", "frac": round(ach / fp32_peak_tflops, 4), "traffic": traffic,
+            "fp32_issue_frac": round((m2l_issue if dom == "m2l" else p2p_issue) or 0.0, 4),
+            "flops_per_unit": m2l["flops"] if dom == "m2l" else P2P_FLOPS,
+            "units_per_launch": counts["n_m2l"] if dom == "m2l" else counts["p2p_interactions"],
             "peak_note": "FP32 FFMA peak = 148 SMs x 128 lanes x 2 flop x sm_max_mhz (MEASURED_PEAKS.json); "
-                         "DESIGN.md §6",
+                         "fp32_issue_frac = lane-ops per unit (P2P 13, SURVEY §8(d) item 1) x units/s / "
+                         "(148 x 128 x sm_max_mhz); DESIGN.md §6",
             "per_kernel": {
                 "m2l": {"ms": round(m2l_ms, 4), "pairs": counts["n_m2l"], "flops_per_pair": m2l["flops"],
-                        "TFLOP/s": round(m2l_tf, 3), "frac": round(m2l_tf / fp32_peak_tflops, 4),
+                        "instr_per_pair": m2l["instr"], "TFLOP/s": round(m2l_tf, 3),
+                        "frac": round(m2l_tf / fp32_peak_tflops, 4),
+                        "fp32_issue_frac": round(m2l_issue, 4) if m2l_issue else None,
                         "pairs_per_s": counts["n_m2l"] / (m2l_ms * 1e-3) if m2l_ms else None},
                 "p2p": {"ms": round(p2p_ms, 4), "interactions": counts["p2p_interactions"],
-                        "flops_per_interaction": P2P_FLOPS, "TFLOP/s": round(p2p_tf, 3),
-                        "frac": round(p2p_tf / fp32_peak_tflops, 4),
-                        "fp32_issue_frac": round(counts["p2p_interactions"] * P2P_INSTR / (p2p_ms * 1e-3) /
-                                                 (148 * FP32_LANES_PER_SM * sm_mhz * 1e6), 4) if p2p_ms else None,
+                        "flops_per_interaction": P2P_FLOPS, "instr_per_interaction": P2P_INSTR,
+                        "TFLOP/s": round(p2p_tf, 3), "frac": round(p2p_tf / fp32_peak_tflops, 4),
+                        "fp32_issue_frac": round(p2p_issue, 4) if p2p_issue else None,
                         "interactions_per_s": counts["p2p_interactions"] / (p2p_ms * 1e-3) if p2p_ms else None}},
             "measured": "CUDA events recorded by libfmm around each kernel on the stream it runs on (P2P then "
                         "M2L, back to back on the caller's stream); per-launch average over the timed steps",

@@ -1,7 +1,9 @@
 """Algorithmic work counts of the two hot kernels (bench roofline, Eq. (1) cost ratio)."""
 from __future__ import annotations
 
-P2P_FLOPS = 20      # 3 sub, |r|^2 (3 mul 2 add), rsqrt, q/r, q/r^3 (2 mul), phi add, 3 fma grad
+# 18 FP32 flops (FFMA = 2) + 1 MUFU rsqrt per interaction:
+# 3 sub, |r|^2 (1 mul + 2 fma = 5), q/r (1 mul), phi add (1), 1/r^2 and q/r^3 (2 mul), grad (3 fma = 6)
+P2P_FLOPS = 18
 P2P_INSTR = 13      # FP32-pipe lane-ops per interaction (SASS, -ftz)
 
 

@@ -17,18 +17,6 @@ const char* kPhaseNames[PH_COUNT] = {"bounds", "sort", "tree", "geometry", "dtt"
 
 fmm_status check_ctx(const fmm_ctx* ctx) { return ctx ? FMM_OK : FMM_ERR_ARG; }
 
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        cudaGetDevice(&prev);
-        if (prev != dev) cudaSetDevice(dev);
-    }
-    ~DeviceGuard() {
-        int cur = -1;
-        cudaGetDevice(&cur);
-        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-    }
-};
 }  // namespace
 
 fmm_status buf_ensure(fmm_ctx* ctx, DevBuf& b, size_t bytes, bool keep, cudaStream_t s) {

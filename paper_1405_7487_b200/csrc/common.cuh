@@ -219,6 +219,20 @@ struct fmm_ctx {
     } while (0)
 
 // grow a device buffer to at least `bytes` (contents discarded unless keep)
+// makes `dev` current for the scope of an ABI call and restores the caller's device after it
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
 fmm_status buf_ensure(fmm_ctx* ctx, DevBuf& b, size_t bytes, bool keep = false, cudaStream_t s = 0);
 void buf_free(DevBuf& b);
 

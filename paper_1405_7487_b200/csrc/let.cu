@@ -529,7 +529,7 @@ extern "C" fmm_status fmm_work(fmm_ctx* ctx, double c_m2l, float alpha, float* w
     }
     if (lr_sums) lr_sums[0] = lr_sums[1] = 0.0;
     if (ctx->n == 0) return FMM_OK;
-    cudaSetDevice(ctx->device);
+    DeviceGuard guard(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t nc = ctx->ncell;
     FMM_TRY(buf_ensure(ctx, ctx->let_tmp, (size_t)nc * 16 + 64));

@@ -391,10 +391,11 @@ fmm_status m2l_fast_t(fmm_ctx* ctx, cudaStream_t s) {
         const size_t nt = t.k.size();
         FMM_TRY(buf_ensure(ctx, ctx->fold_tab, (NSP + 1) * 4 + NSP * 4 + nt * 4 + nt * 8 + 64));
         char* b = (char*)ctx->fold_tab.p;
-        FMM_CUDA_TRY(ctx, cudaMemcpy(b, t.w.data(), nt * 8, cudaMemcpyHostToDevice));
-        FMM_CUDA_TRY(ctx, cudaMemcpy(b + nt * 8, t.off.data(), (NSP + 1) * 4, cudaMemcpyHostToDevice));
-        FMM_CUDA_TRY(ctx, cudaMemcpy(b + nt * 8 + (NSP + 1) * 4, t.dg.data(), NSP * 4, cudaMemcpyHostToDevice));
-        FMM_CUDA_TRY(ctx, cudaMemcpy(b + nt * 8 + (2 * NSP + 1) * 4, t.k.data(), nt * 4, cudaMemcpyHostToDevice));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(b, t.w.data(), nt * 8, cudaMemcpyHostToDevice, s));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(b + nt * 8, t.off.data(), (NSP + 1) * 4, cudaMemcpyHostToDevice, s));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(b + nt * 8 + (NSP + 1) * 4, t.dg.data(), NSP * 4, cudaMemcpyHostToDevice, s));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(b + nt * 8 + (2 * NSP + 1) * 4, t.k.data(), nt * 4, cudaMemcpyHostToDevice, s));
+        FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));   // pageable sources: complete before reuse
         ctx->fold_P = P;
         ctx->fold_nt = (int64_t)nt;
     }
@@ -685,7 +686,8 @@ __global__ void __launch_bounds__(128, 2)
             if (p + 32 < p1) fetch_cb(bnext);   // after the recurrence: bnext has landed
             // (rho_B/rho_A)^n: only in warps where some lane needs it (uniform trees: never)
             const bool need = __any_sync(__activemask(), de != 0);
-            auto pw = [&](int n) { return __int_as_float((127 + de * n) << 23); };
+            // 2^(de*n) from exponent bits, saturated like exp2f (0 / inf) when |de*n| leaves the range
+            auto pw = [&](int n) { return __int_as_float(min(max(127 + de * n, 0), 255) << 23); };
             const float4* sv = Sv + (size_t)b * NCH;
             sfor<0, NCH>([&](auto cc) {
                 constexpr int C = decltype(cc)::value;
@@ -823,10 +825,11 @@ fmm_status m2l_mir_t(fmm_ctx* ctx, cudaStream_t s) {
         const size_t nt = t.k.size();
         FMM_TRY(buf_ensure(ctx, ctx->fold_tab, (NSP + 1) * 4 + NSP * 4 + nt * 4 + nt * 8 + 64));
         char* b = (char*)ctx->fold_tab.p;
-        FMM_CUDA_TRY(ctx, cudaMemcpy(b, t.w.data(), nt * 8, cudaMemcpyHostToDevice));
-        FMM_CUDA_TRY(ctx, cudaMemcpy(b + nt * 8, t.off.data(), (NSP + 1) * 4, cudaMemcpyHostToDevice));
-        FMM_CUDA_TRY(ctx, cudaMemcpy(b + nt * 8 + (NSP + 1) * 4, t.dg.data(), NSP * 4, cudaMemcpyHostToDevice));
-        FMM_CUDA_TRY(ctx, cudaMemcpy(b + nt * 8 + (2 * NSP + 1) * 4, t.k.data(), nt * 4, cudaMemcpyHostToDevice));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(b, t.w.data(), nt * 8, cudaMemcpyHostToDevice, s));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(b + nt * 8, t.off.data(), (NSP + 1) * 4, cudaMemcpyHostToDevice, s));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(b + nt * 8 + (NSP + 1) * 4, t.dg.data(), NSP * 4, cudaMemcpyHostToDevice, s));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(b + nt * 8 + (2 * NSP + 1) * 4, t.k.data(), nt * 4, cudaMemcpyHostToDevice, s));
+        FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));   // pageable sources: complete before reuse
         ctx->fold_P = 1000 + P;
         ctx->fold_nt = (int64_t)nt;
     }

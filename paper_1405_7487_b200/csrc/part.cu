@@ -137,7 +137,7 @@ extern "C" {
 
 fmm_status fmm_bounds(fmm_ctx* ctx, const void* pos, int64_t n, double* out, void* stream) {
     if (!ctx || !out || n < 0 || (n > 0 && !pos)) return FMM_ERR_ARG;
-    cudaSetDevice(ctx->device);
+    DeviceGuard guard(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
     for (int d = 0; d < 3; ++d) {
         out[d] = INFINITY;
@@ -167,7 +167,7 @@ fmm_status fmm_bounds(fmm_ctx* ctx, const void* pos, int64_t n, double* out, voi
 fmm_status fmm_part_keys(fmm_ctx* ctx, const void* pos, int64_t n, const double* bounds, uint64_t* keys, void* stream) {
     if (!ctx || !bounds || n < 0 || (n > 0 && (!pos || !keys))) return FMM_ERR_ARG;
     if (n == 0) return FMM_OK;
-    cudaSetDevice(ctx->device);
+    DeviceGuard guard(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
     const unsigned g = grid_for(ctx, n);
     if (ctx->prec == FMM_F32)
@@ -186,7 +186,7 @@ fmm_status fmm_part_histogram(fmm_ctx* ctx, const uint64_t* keys, const float* w
     if (!ctx || bits < 1 || bits > 24 || prefix_bits < 0 || prefix_bits + bits > 63 || !hist || n < 0 ||
         (n > 0 && !keys))
         return FMM_ERR_ARG;
-    cudaSetDevice(ctx->device);
+    DeviceGuard guard(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
     FMM_CUDA_TRY(ctx, cudaMemsetAsync(hist, 0, ((size_t)1 << bits) * 8, s));
     if (n == 0) return FMM_OK;
@@ -204,7 +204,7 @@ fmm_status fmm_part_pack(fmm_ctx* ctx, const void* pos, const void* q, const uin
         return FMM_ERR_ARG;
     for (int r = 0; r < nranks; ++r) counts[r] = 0;
     if (n == 0) return FMM_OK;
-    cudaSetDevice(ctx->device);
+    DeviceGuard guard(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
     // scratch: dkey[2n] u64 | idx[2n] u32 | splitters | counts
     const size_t need = (size_t)n * 16 + (size_t)n * 8 + 256 * 8 + 256 * 8 + 64;
@@ -313,7 +313,7 @@ fmm_status fmm_orb_histogram(fmm_ctx* ctx, const uint64_t* keys, const float* w,
     if (!ctx || ngroups < 1 || ngroups > 256 || !axis || !prefix || !hist || bits < 1 || bits > 16 ||
         prefix_bits < 0 || prefix_bits + bits > 21 || n < 0 || (n > 0 && (!keys || !group)))
         return FMM_ERR_ARG;
-    cudaSetDevice(ctx->device);
+    DeviceGuard guard(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
     FMM_TRY(buf_ensure(ctx, ctx->orb_tmp, (size_t)256 * 12 + 64));
     int32_t* dax = P_<int32_t>(ctx->orb_tmp);
@@ -334,7 +334,7 @@ fmm_status fmm_orb_split(fmm_ctx* ctx, const uint64_t* keys, int32_t* group, int
     if (!ctx || ngroups < 1 || ngroups > 256 || !axis || !cut || !right || n < 0 || (n > 0 && (!keys || !group)))
         return FMM_ERR_ARG;
     if (n == 0) return FMM_OK;
-    cudaSetDevice(ctx->device);
+    DeviceGuard guard(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
     FMM_TRY(buf_ensure(ctx, ctx->orb_tmp, (size_t)256 * 12 + 64));
     int32_t* dax = P_<int32_t>(ctx->orb_tmp);
@@ -357,7 +357,7 @@ fmm_status fmm_part_pack_dest(fmm_ctx* ctx, const void* pos, const void* q, cons
         return FMM_ERR_ARG;
     for (int r = 0; r < nranks; ++r) counts[r] = 0;
     if (n == 0) return FMM_OK;
-    cudaSetDevice(ctx->device);
+    DeviceGuard guard(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
     const size_t need = (size_t)n * 24 + 256 * 8 + 64;
     FMM_TRY(buf_ensure(ctx, ctx->part_tmp, need));

@@ -128,10 +128,10 @@ class FMM:
         import torch
         return torch.float32 if self.prec == F32 else torch.float64
 
-    @staticmethod
-    def _stream(stream):
+    def _stream(self, stream):
+        """cudaStream_t of `stream`, default: the current stream of the CONTEXT's device."""
         import torch
-        return (stream if stream is not None else torch.cuda.current_stream()).cuda_stream
+        return (stream if stream is not None else torch.cuda.current_stream(self.device)).cuda_stream
 
     def _check_tensor(self, t, shape, name):
         import torch
@@ -192,9 +192,19 @@ class FMM:
         dt = np.float32 if self.prec == F32 else np.float64
         pos = np.ascontiguousarray(pos, dtype=dt)
         q = np.ascontiguousarray(q, dtype=dt)
+        if pos.ndim != 2 or pos.shape[1] != 3:
+            raise FMMError(FMM_ERR_ARG, f"pos must have shape (n, 3), got {pos.shape}")
         n = pos.shape[0]
+        if q.shape != (n,):
+            raise FMMError(FMM_ERR_ARG, f"q must have shape ({n},), got {q.shape}")
         phi = np.empty(n, dt) if phi is None else phi
         grad = np.empty((n, 3), dt) if grad is None else grad
+        for a, shape, name in ((phi, (n,), "phi"), (grad, (n, 3), "grad")):
+            # the library writes n*es / 3n*es bytes straight into these buffers
+            if not isinstance(a, np.ndarray) or a.dtype != dt or a.shape != shape:
+                raise FMMError(FMM_ERR_ARG, f"{name} must be a numpy {np.dtype(dt).name} array of shape {shape}")
+            if not a.flags.c_contiguous or not a.flags.writeable:
+                raise FMMError(FMM_ERR_ARG, f"{name} must be C-contiguous and writeable")
         s = None if stream is None else C.c_void_p(stream.cuda_stream)
         self._check(lib().fmm_solve_host(self._h, _np_ptr(pos), _np_ptr(q), n, _np_ptr(phi), _np_ptr(grad), s),
                     "fmm_solve_host")
@@ -367,7 +377,7 @@ class FMM:
     def work(self, c_m2l: float, alpha: float = 1.0, out=None, stream=None):
         """Eq. (1) weights of the last build (caller order) and the sums of l and r."""
         import torch
-        w = torch.empty(self.n, dtype=torch.float32, device="cuda") if out is None else out
+        w = torch.empty(self.n, dtype=torch.float32, device=torch.device("cuda", self.device)) if out is None else out
         lr = np.zeros(2)
         self._check(lib().fmm_work(self._h, float(c_m2l), float(alpha), C.c_void_p(w.data_ptr()), _np_ptr(lr),
                                    C.c_void_p(self._stream(stream))), "fmm_work")
