@@ -156,21 +156,24 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(cfg, args, world=1):
-    n = cfg["n"] * world
+def workload_config(cfg, args, world=1, N=None):
+    n = cfg["n"] * world if N is None else N
     d = {"workload": f"BASELINE.json {CONFIG_NAMES[args.config]}: 3D Laplace FMM, N={n} {cfg['kind']}, "
                      f"{cfg['prec']}, P={cfg['P']}, theta={cfg['theta']}, ncrit={cfg['ncrit']}",
          "N": n, "distribution": cfg["kind"], "P": cfg["P"], "theta": cfg["theta"], "ncrit": cfg["ncrit"],
          "precision": cfg["prec"], "seed": cfg["seed"], "l2": "flushed (256 MB write) before every timed step",
          "parallelism": "1 GPU"}
-    if world > 1:
+    if world > 1 or getattr(args, "dist", False):
         part = "ORB multisection" if getattr(args, "partitioner", "morton") == "orb" else "Morton-range"
-        d["parallelism"] = (f"{world} GPUs, one FMM: {part} partition with Eq. (1) weights + LET exchange over "
-                            f"NCCL (weak scaling at constant density, {cfg['n']} particles per GPU, rank r's "
-                            f"slice in unit cube r of a 2x2x2 Morton block pattern)")
-        d["workload"] = ("BASELINE.json configs[3] (weak scaling, per-GPU size of " + CONFIG_NAMES[args.config] +
+        how = (f"weak scaling at constant density, {cfg['n']} particles per GPU, rank r's particles in unit cube r "
+               f"of a 2x2x2 Morton block pattern" if args.scaling == "weak" else
+               f"strong scaling, one {cfg['n']}-particle set split into {world} index slices")
+        d["parallelism"] = (f"{world} GPU(s), one FMM through fmm_dist_solve: {part} partition with Eq. (1) weights + "
+                            f"LET exchange over NCCL ({how})")
+        d["workload"] = (f"BASELINE.json configs[3] ({args.scaling} scaling, " + CONFIG_NAMES[args.config] +
                          f"): 3D Laplace FMM, N={n} {cfg['kind']}, {cfg['prec']}, P={cfg['P']}, theta={cfg['theta']}, "
                          f"ncrit={cfg['ncrit']}")
+        d["scaling"] = args.scaling
     return d
 
 
@@ -222,51 +225,67 @@ def roofline_block(args, cfg, counts, ph):
 
 
 def weak_offset(r: int) -> np.ndarray:
-    """Weak scaling at constant density: rank r's 2^20 particles fill unit cube r of a block
-    pattern in Morton order (r bits -> x, y, z, x, ...; 2 GPUs: 2x1x1, 4: 2x2x1, 8: 2x2x2), so
-    every GPU's particles have the same spacing and its tree the same leaf occupancy as c2."""
+    """Weak scaling at constant density: rank r's particles fill unit cube r of a block pattern in
+    Morton order (r bits -> x, y, z, x, ...; 2 GPUs: 2x1x1, 4: 2x2x1, 8: 2x2x2), so every GPU's
+    particles have the same spacing and its tree the same leaf occupancy as the 1-GPU case."""
     o = np.zeros(3)
     for b in range(max(r.bit_length(), 1)):
         o[b % 3] += ((r >> b) & 1) << (b // 3)
     return o
 
 
+def dist_input(cfg, scaling, rank, world):
+    """(pos, q, gid_base, N_total) of this rank.  weak: cfg['n'] particles per rank in rank r's unit
+    cube (constant density); strong: rank r's contiguous slice of ONE cfg['n']-particle set."""
+    dt_np = np.float32 if cfg["prec"] == "f32" else np.float64
+    if scaling == "weak":
+        n = cfg["n"]
+        pos, q = synth.generate(cfg["kind"], n, cfg["seed"], dt_np, start=rank * n, n_total=n * world)
+        return (pos + weak_offset(rank)).astype(dt_np), q, rank * n, n * world
+    N = cfg["n"]
+    lo, hi = rank * N // world, (rank + 1) * N // world
+    pos, q = synth.generate(cfg["kind"], hi - lo, cfg["seed"], dt_np, start=lo, n_total=N)
+    return pos, q, lo, N
+
+
 def run_dist(args, cfg, rank, world, local):
-    """--gpus N > 1 under torchrun: the distributed FMM (dist.py) over NCCL."""
+    """--gpus N > 1 under torchrun (or --dist on one GPU): the library's distributed driver
+    (fmm_create_dist / fmm_dist_solve over NCCL; the process group only broadcasts the NCCL id and
+    times the step as the max over ranks)."""
     import torch
     import torch.distributed as tdist
-    from paper_1405_7487_b200.dist import DistFMM, TorchComm
-    dt_np = np.float32 if cfg["prec"] == "f32" else np.float64
+    from paper_1405_7487_b200.dist import DistFMM, nccl_unique_id
     dt_t = torch.float32 if cfg["prec"] == "f32" else torch.float64
-    n = cfg["n"]
-    N = n * world
-    pos, q = synth.generate(cfg["kind"], n, cfg["seed"], dt_np, start=rank * n, n_total=N)
-    pos = (pos + weak_offset(rank)).astype(dt_np)      # constant density: rank r's unit cube
+    pos, q, gid_base, N = dist_input(cfg, args.scaling, rank, world)
+    n = len(pos)
     dpos = torch.from_numpy(pos).cuda()
     dq = torch.from_numpy(q).cuda()
-    D = DistFMM(TorchComm(), N, cfg["P"], cfg["theta"], cfg["ncrit"], cfg["prec"], local,
-                partitioner=args.partitioner)
-    f = D.fmm[0]
+    uid = [nccl_unique_id() if rank == 0 else None]
+    tdist.broadcast_object_list(uid, src=0)
+    # a rank may own up to twice its share after an Eq. (1)-weighted partition
+    D = DistFMM(max(2 * N // world, n) + 1024, cfg["P"], cfg["theta"], cfg["ncrit"], cfg["prec"], local, world, rank,
+                unique_id=uid[0], partitioner=args.partitioner)
     stream = torch.cuda.current_stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    phi = torch.empty(n, dtype=dt_t, device="cuda")
+    grad = torch.empty((n, 3), dtype=dt_t, device="cuda")
 
     def step():
         # every step after the first partitions with the previous step's Eq. (1) weights
-        return D.solve([dpos], [dq], [rank * n], reuse_weights=True)
+        D.solve(dpos, dq, gid_base, reuse_weights=True, phi=phi, grad=grad, stream=stream)
 
     if args.tune_alpha > 0:
         # Eq. (1) alpha optimised over time steps (PAPER.md:113) before the measured run, then frozen
-        D.enable_alpha_tuning()
+        D.tune_alpha()
         for _ in range(args.tune_alpha):
             step()
-        D.alpha = D.tuner.best
-        D.tuner = None
+        D.tune_alpha(0.0, 0.0, 0.0)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    f.set_timing(True)
-    f.phase_times(reset=True)
-    f.launch_count(reset=True)
+    D.set_timing(True)
+    D.phase_times(reset=True)
+    D.launch_count(reset=True)
     tdist.barrier()
     torch.cuda.synchronize()
     ms = 0.0
@@ -281,9 +300,10 @@ def run_dist(args, cfg, rank, world, local):
             ms += a.elapsed_time(b)
         tdist.barrier()
         torch.cuda.synchronize()
-    launches = f.launch_count(reset=True)
-    ph = f.phase_times(reset=True)
-    f.set_timing(False)
+    launches = D.launch_count(reset=True)
+    ph = D.phase_times(reset=True)
+    timeline = D.timeline()
+    D.set_timing(False)
     t = torch.tensor([ms], device="cuda", dtype=torch.float64)
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms_step = float(t.item()) / args.steps
@@ -298,33 +318,35 @@ def run_dist(args, cfg, rank, world, local):
     for _ in range(e2e_steps):
         gp = hpos.to("cuda", non_blocking=True)
         gq = hq.to("cuda", non_blocking=True)
-        (phi, grad), = D.solve([gp], [gq], [rank * n], reuse_weights=True)
-        hphi.copy_(phi, non_blocking=True)
-        hgrad.copy_(grad, non_blocking=True)
+        p_, g_ = D.solve(gp, gq, gid_base, reuse_weights=True, stream=stream)
+        hphi.copy_(p_, non_blocking=True)
+        hgrad.copy_(g_, non_blocking=True)
         torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     e2e_s = float(t.item())
-    counts = f.counts()
+    counts = D.counts()
+    st = D.stats()
     es = 4 if cfg["prec"] == "f32" else 8
     if rank == 0:
         line = {"metric": METRIC, "value": N / (ms_step * 1e-3), "unit": "particles/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32" if cfg["prec"] == "f32" else "f64",
+                "scaling": args.scaling, "vs_baseline": None, "dtype": "f32" if cfg["prec"] == "f32" else "f64",
                 "data": "synthetic (seeded SplitMix64 generator, synth/; each rank draws its slice)",
-                "config": workload_config(cfg, args, world),
+                "config": workload_config(cfg, args, world, N),
                 "e2e": {"value": N / e2e_s, "unit": "particles/s", "h2d_bytes_per_step": n * 4 * es,
-                        "d2h_bytes_per_step": n * 4 * es, "api": "DistFMM.solve (pinned host buffers, per rank)"},
+                        "d2h_bytes_per_step": n * 4 * es, "api": "fmm_dist_solve (pinned host buffers, per rank)"},
                 "gpu_launches": launches,
                 "roofline": roofline_block(args, cfg, counts, ph),
                 "clocks": clk.summary(),
                 "phases_ms": {k: round(v / args.steps, 4) for k, v in ph.items()},
+                "timeline_ms_rank0": {k: [round(x, 3) for x in v] for k, v in timeline.items()},
                 "phases_note": "per-phase CUDA-event spans; upward overlaps dtt/lists and downward overlaps p2p "
                                "(aux stream), so the spans sum to more than ms_per_step",
                 "counts_rank0": counts,
-                "let_bytes_rank0": dict(D.stats),
-                "alpha": D.alpha, "alpha_tuned_steps": args.tune_alpha}
+                "dist_rank0": {k: (v.tolist() if hasattr(v, "tolist") else v) for k, v in st.items()},
+                "alpha_tuned_steps": args.tune_alpha}
         print(json.dumps(line), flush=True)
     tdist.barrier()
     D.close()
@@ -336,7 +358,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIG_NAMES))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIG_NAMES),
+                    help="default: c2 on 1 GPU; with --gpus N > 1 (or --dist): c4w (weak) / c4s (strong)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="multi-GPU: weak = the config's N per GPU (BASELINE configs[3]: 2^24), strong = the "
+                         "config's N in total (configs[3]: 2^26)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist", action="store_true", help="use the distributed path even on 1 GPU")
@@ -346,11 +372,12 @@ def main():
                     help="multi-GPU partition: Morton ranges (north_star) or ORB multisection (SURVEY 8f f3)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    cfg = synth.CONFIGS[args.config]
-
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config is None:
+        args.config = "c2" if world == 1 and not args.dist else ("c4w" if args.scaling == "weak" else "c4s")
+    cfg = synth.CONFIGS[args.config]
 
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)

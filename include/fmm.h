@@ -35,7 +35,7 @@ typedef enum {
     FMM_ERR_NONFINITE = 3, /* a position is NaN or Inf */
     FMM_ERR_OOM = 4,       /* device allocation failed */
     FMM_ERR_CUDA = 5,      /* a CUDA runtime error; see fmm_last_error */
-    FMM_ERR_NCCL = 6       /* reserved for the multi-GPU layer */
+    FMM_ERR_NCCL = 6       /* an NCCL call of the multi-GPU driver failed (or libnccl is missing) */
 } fmm_status;
 
 typedef enum { FMM_F32 = 0, FMM_F64 = 1 } fmm_prec;
@@ -144,6 +144,53 @@ fmm_status fmm_copy_lists(const fmm_ctx* ctx, uint32_t* m2l, uint32_t* p2p);
 /* fp64 expansions [ncell][ncoef] after fmm_evaluate (R11 order); either may be NULL */
 fmm_status fmm_copy_expansions(const fmm_ctx* ctx, double* M, double* L);
 
+/* ---- debug stage entry points: the hot kernels on a CALLER-SUPPLIED tree and
+ * interaction list, so each stage can be checked against an independent implementation (the
+ * parity tests feed the oracle's tree and lists).  Every pointer in the view is DEVICE memory;
+ * cells are indexed 0..ncell-1 in the caller's order; bodies are in the caller's (sorted) order,
+ * cell c owning bodies [body_begin[c], body_begin[c] + body_count[c]).
+ *   n, ncell          bodies and cells (n <= the context's n_max)
+ *   pos, q            [n][3], [n] in the context precision (P2P)
+ *   body_begin, body_count, child_count   u32 [ncell] (P2P; leaves = child_count 0, their body
+ *                     ranges disjoint)
+ *   center            fp64 [ncell][3] expansion centres (M2L)
+ *   level             int32 [ncell] tree level of each cell (M2L; sets the power-of-two operand
+ *                     scale rho = 2^(E - level), 2^E >= 2 root_half_width; exact)
+ *   M                 fp64 [ncell][ncoef] multipoles, R11 order (M2L)
+ *   root_half_width   the root cube's half-width h (M2L)
+ * Pair lists are DEVICE u32 [n_pairs][2] (target, source) cell pairs in ascending order (R10);
+ * FMM_ERR_ARG if out of order or naming a cell >= ncell.  Both calls synchronise `stream` and
+ * leave the context without a build (fmm_evaluate then returns FMM_ERR_STATE).
+ * fmm_debug_p2p: phi [n], grad [n][3] (device, context precision, the view's body order) = the
+ *   near field of R17 over the P2P pairs (§II-A "P2P"); bodies of leaves without
+ *   pairs get 0.
+ * fmm_debug_m2l: L (device fp64 [ncell][ncoef], overwritten) = sum over the M2L pairs (A <- B)
+ *   of R14 ("M2L"); cells without pairs get 0. */
+typedef struct {
+    int64_t n, ncell;
+    const void* pos;
+    const void* q;
+    const uint32_t* body_begin;
+    const uint32_t* body_count;
+    const uint32_t* child_count;
+    const double* center;
+    const int32_t* level;
+    const double* M;
+    double root_half_width;
+} fmm_tree_view;
+fmm_status fmm_debug_p2p(fmm_ctx* ctx, const fmm_tree_view* view, const uint32_t* p2p, int64_t n_pairs, void* phi,
+                         void* grad, void* stream);
+fmm_status fmm_debug_m2l(fmm_ctx* ctx, const fmm_tree_view* view, const uint32_t* m2l, int64_t n_pairs, double* L,
+                         void* stream);
+
+/* fmm_debug_check: memory checking without compute-sanitizer.  In a context created with the
+ * environment variable FMM_GUARD=1 every device buffer has a 4 KiB guard zone after its usable
+ * bytes; this call synchronises the device and verifies every live guard zone of the context's
+ * device: FMM_ERR_STATE (and *nbad > 0, HOST, may be NULL) if any was overwritten.  FMM_POISON=1
+ * fills fresh allocations with 0xFF bytes (NaN / huge values) so reads of unwritten memory
+ * surface in the results. */
+fmm_status fmm_debug_check(fmm_ctx* ctx, int64_t* nbad);
+
 /* ---- multi-GPU: Morton-range partition (§II-B,
  * Eq. (1)).  The collectives between these calls are the caller's (the
  * Python layer uses torch.distributed over NCCL); every step on the data runs here.
@@ -230,6 +277,100 @@ fmm_status fmm_let_remote(const fmm_ctx* ctx, int k, int64_t* base, int64_t* nce
  *   one M2L pair in P2P interactions).  lr_sums (HOST [2], may be NULL): sum of l and of r;
  *   synchronises when given.  Needs fmm_lists. */
 fmm_status fmm_work(fmm_ctx* ctx, double c_m2l, float alpha, float* w, double* lr_sums, void* stream);
+
+/* ---- multi-GPU driver (SURVEY §8(b) fmm_create_dist / fmm_set_weights, §8(e), §8(f) f1, f3, f4).
+ * One context per rank; the LIBRARY owns the communicator, the partition arithmetic and every
+ * exchange of a distributed step (dist.cu states the step with its PAPER.md passages).
+ * Transports: NCCL (one rank per process or thread; libnccl is dlopen'ed -- the copy the process
+ * already loaded, e.g. torch's, else libnccl.so.2 -- so this library has no link-time NCCL
+ * dependency; failures return FMM_ERR_NCCL), or an in-process group of K ranks, one host thread
+ * per rank, for several GPUs of one process or K ranks sharing one GPU in the parity tests
+ * (host barriers swap device pointers and events; no kernel ever waits for another rank's).
+ * fmm_group_create / destroy: the in-process group (destroy after every member context).
+ * fmm_dist_unique_id: a fresh 128-byte ncclUniqueId (rank 0 makes it, the caller broadcasts it).
+ * fmm_create_dist: as fmm_create, plus nranks, rank, and EXACTLY ONE of nccl_unique_id (HOST
+ *   128 B) / group; partitioner FMM_PART_MORTON (Morton-curve ranges weighted by Eq. (1),
+ *   north_star) or FMM_PART_ORB (multisection).  n_local_max bounds the
+ *   particles a rank may own after the partition (FMM_ERR_ARG from fmm_dist_solve otherwise).
+ *   Every rank must call the same sequence of fmm_dist_* calls.
+ * fmm_set_weights: partition weights (DEVICE fp32 [n], caller order; NULL clears) for the next
+ *   fmm_dist_solve with the same n; default 1 (Eq. (1) at the first step).
+ * fmm_dist_set_alpha: Eq. (1) w = l + alpha r for the weights this rank computes;
+ *   c_m2l > 0 overrides the cost of one M2L pair in P2P interactions (default: the kernel's
+ *   FP32 lane-op ratio).  fmm_dist_tune_alpha: golden-section search of log alpha over [lo, hi]
+ *   by the measured step runtime ("optimized over the time steps"); lo = hi = 0 stops
+ *   it (alpha stays at the best probe).
+ * fmm_dist_solve: ONE distributed step on this rank's particles pos [n][3], q [n] (DEVICE, context
+ *   precision; their global ids are gid_base + i): partition (weights: with reuse_weights the
+ *   Eq. (1) weights this context computed in its previous step if n is unchanged, else those of
+ *   fmm_set_weights, else 1), particle exchange, local tree, LET exchange overlapped with the
+ *   traversal, interactions, results back.  phi [n], grad [n][3] (DEVICE) in the caller's order.
+ *   Synchronises `stream`; every stream the step used is joined into it before return.
+ * fmm_dist_get_stats: the last step's bounds, alpha, byte counts, local size, work sums.
+ * fmm_dist_local: the last step's local particles' global ids (HOST int64 [n_local], may be NULL)
+ *   and the peers whose LETs were grafted, in graft order (HOST int32 [nranks], -1 padded).
+ *   fmm_get_counts / fmm_copy_* / fmm_let_remote on the same context describe the local tree.
+ * fmm_dist_weights: the Eq. (1) weights of the last step for the caller's particles (HOST fp32 [n]).
+ * fmm_dist_orb_boxes: ORB boxes of the last step (HOST int32 [nranks][6], quantised lo xyz, hi xyz).
+ * fmm_dist_timeline: with fmm_set_timing on, per span of the last step (names by
+ *   fmm_dist_timeline_name) its start and end in ms after the step began (CUDA events on the
+ *   stream the span ran on; -1 if the span did not run); ms HOST [cap][2]. */
+typedef struct fmm_group fmm_group;
+typedef struct {
+    double bounds[6];
+    double alpha, c_m2l;
+    int64_t n_local;
+    int32_t npeers;
+    int32_t tuner_probes;
+    int64_t let_struct_bytes, let_data_bytes, part_bytes;
+    double work_local, work_remote;
+    int32_t tuner_converged, pad;
+    double tuner_best;
+} fmm_dist_stats;
+#define FMM_PART_MORTON 0
+#define FMM_PART_ORB 1
+fmm_status fmm_group_create(int nranks, fmm_group** out);
+fmm_status fmm_group_destroy(fmm_group* group);
+fmm_status fmm_dist_unique_id(void* out);
+fmm_status fmm_create_dist(int64_t n_local_max, int p, double theta, int ncrit, int prec, int device, int nranks,
+                           int rank, const void* nccl_unique_id, fmm_group* group, int partitioner, fmm_ctx** out);
+fmm_status fmm_set_weights(fmm_ctx* ctx, const float* w, int64_t n);
+fmm_status fmm_dist_set_alpha(fmm_ctx* ctx, double alpha, double c_m2l);
+fmm_status fmm_dist_tune_alpha(fmm_ctx* ctx, double lo, double hi, double tol);
+fmm_status fmm_dist_solve(fmm_ctx* ctx, const void* pos, const void* q, int64_t n, int64_t gid_base,
+                          int reuse_weights, void* phi, void* grad, void* stream);
+fmm_status fmm_dist_get_stats(const fmm_ctx* ctx, fmm_dist_stats* out);
+fmm_status fmm_dist_local(const fmm_ctx* ctx, int64_t* gid, int32_t* peers);
+fmm_status fmm_dist_weights(const fmm_ctx* ctx, float* w);
+fmm_status fmm_dist_orb_boxes(const fmm_ctx* ctx, int32_t* boxes);
+fmm_status fmm_dist_timeline(const fmm_ctx* ctx, double* ms, int cap, int* n);
+const char* fmm_dist_timeline_name(int i);
+
+/* ---- the driver's host logic, callable without a device (CPU tests of the partition rules):
+ * fmm_splitters: the K-1 Morton splitters (rank j takes keys >= splitter j) by histogram
+ *   refinement ("each bit of the key is examined at each step"): `bits` key bits per
+ *   round until the bin holding the j/K weight quantile carries <= tol/K of the total.  fn returns
+ *   the GLOBAL weights of the keys under each of nprefix prefixes (top prefix_bits bits) binned by
+ *   their next `bits` bits, into hist [nprefix][2^bits]; nonzero return = failure.
+ * fmm_orb_plan: ORB multisection through the two callbacks (histogram of the
+ *   quantised coordinate along axis[g] for every group g with axis[g] >= 0, and the split of the
+ *   groups at cut[g] into right[g]); boxes HOST int32 [nranks][6].
+ * fmm_alpha_tuner_*: the golden-section alpha search fmm_dist_tune_alpha runs (next() before a
+ *   step's weights, report(runtime) after the step). */
+typedef int (*fmm_hist_fn)(void* user, const uint64_t* prefixes, int nprefix, int prefix_bits, int bits, double* hist);
+typedef int (*fmm_orb_hist_fn)(void* user, const int32_t* axis, const uint32_t* prefix, int prefix_bits, int bits,
+                               double* hist);
+typedef int (*fmm_orb_split_fn)(void* user, const int32_t* axis, const uint32_t* cut, const int32_t* right);
+fmm_status fmm_splitters(int nranks, int bits, double tol, fmm_hist_fn fn, void* user, uint64_t* splitters);
+fmm_status fmm_orb_plan(int nranks, int bits, fmm_orb_hist_fn hist, fmm_orb_split_fn split, void* user,
+                        int32_t* boxes);
+typedef struct fmm_alpha_tuner fmm_alpha_tuner;
+fmm_status fmm_alpha_tuner_create(double lo, double hi, double tol, fmm_alpha_tuner** out);
+double fmm_alpha_tuner_next(const fmm_alpha_tuner* t);
+fmm_status fmm_alpha_tuner_report(fmm_alpha_tuner* t, double runtime);
+fmm_status fmm_alpha_tuner_state(const fmm_alpha_tuner* t, int* converged, double* best, int* nhist, double* hist,
+                                 int cap);
+fmm_status fmm_alpha_tuner_destroy(fmm_alpha_tuner* t);
 
 /* ---- timing (bench): per-phase device time from CUDA events recorded on the stream
  * each phase runs on.  enable != 0 turns recording on (small overhead).

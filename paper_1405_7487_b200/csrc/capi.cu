@@ -6,6 +6,8 @@
 #include <cstring>
 
 #include <cmath>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -19,28 +21,54 @@ fmm_status check_ctx(const fmm_ctx* ctx) { return ctx ? FMM_OK : FMM_ERR_ARG; }
 
 }  // namespace
 
+// ---- memory checking without compute-sanitizer (closed on this pool): with FMM_GUARD=1 every
+// buffer a context allocates gets a 4 KiB guard zone after its usable bytes, filled with a
+// pattern that fmm_debug_check verifies (out-of-bounds writes past any buffer end); with
+// FMM_POISON=1 fresh allocations are filled with 0xFF bytes (NaN floats, huge indices), so a
+// kernel reading memory no kernel wrote shows up as NaN / wrong structure in the parity tests.
+constexpr size_t kGuardBytes = 4096;
+constexpr unsigned char kGuardByte = 0xA5;
+std::mutex g_guard_mu;
+std::map<void*, size_t>& guard_registry() {   // device pointer -> usable bytes
+    static std::map<void*, size_t> m;
+    return m;
+}
+
 fmm_status buf_ensure(fmm_ctx* ctx, DevBuf& b, size_t bytes, bool keep, cudaStream_t s) {
     if (bytes <= b.bytes) return FMM_OK;
     void* p = nullptr;
     size_t nb = std::max(bytes, (size_t)256);
-    cudaError_t e = cudaMalloc(&p, nb);
+    cudaError_t e = cudaMalloc(&p, nb + (ctx->guard ? kGuardBytes : 0));
     if (e != cudaSuccess) {
         cudaGetLastError();
         ctx->err = "cudaMalloc(" + std::to_string(nb) + " B) failed: " + cudaGetErrorString(e);
         return FMM_ERR_OOM;
     }
+    if (ctx->poison) FMM_CUDA_TRY(ctx, cudaMemsetAsync(p, 0xFF, nb, s));
+    if (ctx->guard) {
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync((char*)p + nb, kGuardByte, kGuardBytes, s));
+        std::lock_guard<std::mutex> lk(g_guard_mu);
+        guard_registry()[p] = nb;
+    }
     if (keep && b.p && b.bytes) {
         FMM_CUDA_TRY(ctx, cudaMemcpyAsync(p, b.p, b.bytes, cudaMemcpyDeviceToDevice, s));
         FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
     }
-    if (b.p) cudaFree(b.p);
+    if (ctx->poison || ctx->guard) FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    buf_free(b);
     b.p = p;
     b.bytes = nb;
     return FMM_OK;
 }
 
 void buf_free(DevBuf& b) {
-    if (b.p) cudaFree(b.p);
+    if (b.p) {
+        {
+            std::lock_guard<std::mutex> lk(g_guard_mu);
+            guard_registry().erase(b.p);
+        }
+        cudaFree(b.p);
+    }
     b.p = nullptr;
     b.bytes = 0;
 }
@@ -126,6 +154,10 @@ fmm_status fmm_create(int64_t n_max, int p, double theta, int ncrit, int prec, i
         ctx->list_sort = g7 ? atoi(g7) : 0;
         const char* g6 = getenv("FMM_M2L_VARIANT");
         ctx->m2l_variant = g6 ? atoi(g6) : 0;
+        const char* gg = getenv("FMM_GUARD");
+        ctx->guard = gg && gg[0] == '1';
+        const char* gp = getenv("FMM_POISON");
+        ctx->poison = gp && gp[0] == '1';
     }
     if (cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -150,6 +182,8 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
     if (!ctx) return FMM_ERR_ARG;
     DeviceGuard g(ctx->device);
     cudaDeviceSynchronize();
+    if (ctx->dist) dist_destroy(ctx->dist);
+    ctx->dist = nullptr;
     DevBuf* bufs[] = {&ctx->root, &ctx->key_a, &ctx->key_b, &ctx->idx_a, &ctx->idx_b, &ctx->sort_counts,
                       &ctx->scan_tmp, &ctx->red_tmp, &ctx->body, &ctx->c_key, &ctx->c_level, &ctx->c_bb,
                       &ctx->c_bc, &ctx->c_cb, &ctx->c_cc, &ctx->c_parent, &ctx->c_bmin, &ctx->c_bmax, &ctx->c_cr,
@@ -643,6 +677,36 @@ fmm_status fmm_copy_expansions(const fmm_ctx* ctx_c, double* M, double* L) {
     size_t sz = (size_t)ctx->ncell * ctx->ncoef * 8;
     if (M && sz) FMM_CUDA_TRY(ctx, cudaMemcpy(M, ctx->M.p, sz, cudaMemcpyDeviceToHost));
     if (L && sz) FMM_CUDA_TRY(ctx, cudaMemcpy(L, ctx->L.p, sz, cudaMemcpyDeviceToHost));
+    return FMM_OK;
+}
+
+fmm_status fmm_debug_check(fmm_ctx* ctx, int64_t* nbad) {
+    FMM_TRY(check_ctx(ctx));
+    DeviceGuard g(ctx->device);
+    FMM_CUDA_TRY(ctx, cudaDeviceSynchronize());
+    int64_t bad = 0, checked = 0;
+    std::vector<unsigned char> h(kGuardBytes);
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    for (const auto& kv : guard_registry()) {
+        cudaPointerAttributes a;
+        if (cudaPointerGetAttributes(&a, kv.first) != cudaSuccess || a.device != ctx->device) {
+            cudaGetLastError();
+            continue;
+        }
+        FMM_CUDA_TRY(ctx, cudaMemcpy(h.data(), (char*)kv.first + kv.second, kGuardBytes, cudaMemcpyDeviceToHost));
+        ++checked;
+        for (unsigned char c : h)
+            if (c != kGuardByte) {
+                ++bad;
+                break;
+            }
+    }
+    if (nbad) *nbad = bad;
+    if (bad) {
+        ctx->err = "fmm_debug_check: " + std::to_string(bad) + " of " + std::to_string(checked) +
+                   " guarded buffers written past their end";
+        return FMM_ERR_STATE;
+    }
     return FMM_OK;
 }
 

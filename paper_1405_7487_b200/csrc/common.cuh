@@ -86,6 +86,9 @@ struct TcPart {
     int64_t n_m = 0, n_p = 0, est_m = 0, est_p = 0;
 };
 
+struct DistState;   // dist.cu: multi-GPU driver state of a context made by fmm_create_dist
+void dist_destroy(DistState* d);
+
 struct TimedEvent {
     int phase;
     cudaEvent_t a, b;
@@ -200,6 +203,11 @@ struct fmm_ctx {
     size_t let_traversed = 0;   // grafted LETs already seeded into the traversal
     DevBuf let_tmp, let_cov, c_orig, part_tmp, orb_tmp;
     DevBuf h_stage;              // device staging for fmm_solve_host
+    // dist.cu: the partition's keys were sorted by the driver (key_a / idx_a hold the sorted keys
+    // and permutation of this build's positions): build_keys only derives the root cube and gathers
+    bool presorted = false;
+    bool guard = false, poison = false;   // FMM_GUARD / FMM_POISON (capi.cu buf_ensure, fmm_debug_check)
+    DistState* dist = nullptr;   // fmm_create_dist contexts only
 };
 
 // ---- error helpers

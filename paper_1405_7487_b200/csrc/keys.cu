@@ -173,16 +173,24 @@ fmm_status build_keys_t(fmm_ctx* ctx, const Real* pos, int64_t n, cudaStream_t s
         }
     }
     PhaseScope ps(ctx, PH_SORT, s);
-    FMM_TRY(buf_ensure(ctx, ctx->key_a, (size_t)n * 8));
+    FMM_TRY(buf_ensure(ctx, ctx->key_a, (size_t)n * 8, ctx->presorted, s));
     FMM_TRY(buf_ensure(ctx, ctx->key_b, (size_t)n * 8));
-    FMM_TRY(buf_ensure(ctx, ctx->idx_a, (size_t)n * 4));
+    FMM_TRY(buf_ensure(ctx, ctx->idx_a, (size_t)n * 4, ctx->presorted, s));
     FMM_TRY(buf_ensure(ctx, ctx->idx_b, (size_t)n * 4));
     const int gblk = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8);
-    k_keys<Real><<<gblk, 256, 0, s>>>(pos, n, P_<double>(ctx->root), P_<uint64_t>(ctx->key_a), P_<uint32_t>(ctx->idx_a));
-    FMM_LAUNCH(ctx);
-    FMM_CUDA_TRY(ctx, cudaGetLastError());
-    FMM_TRY(radix_sort_pairs(ctx, P_<uint64_t>(ctx->key_a), P_<uint64_t>(ctx->key_b), P_<uint32_t>(ctx->idx_a),
-                             P_<uint32_t>(ctx->idx_b), n, 0, 64, &ctx->d_keys, &ctx->d_perm, s, ~0ull));
+    if (ctx->presorted) {
+        // the multi-GPU driver sorted this build's keys already (dist.cu: staying particles while
+        // the partition exchange flew, arrivals after, merged) -- the same (key, index) order
+        ctx->d_keys = P_<uint64_t>(ctx->key_a);
+        ctx->d_perm = P_<uint32_t>(ctx->idx_a);
+    } else {
+        k_keys<Real><<<gblk, 256, 0, s>>>(pos, n, P_<double>(ctx->root), P_<uint64_t>(ctx->key_a),
+                                          P_<uint32_t>(ctx->idx_a));
+        FMM_LAUNCH(ctx);
+        FMM_CUDA_TRY(ctx, cudaGetLastError());
+        FMM_TRY(radix_sort_pairs(ctx, P_<uint64_t>(ctx->key_a), P_<uint64_t>(ctx->key_b), P_<uint32_t>(ctx->idx_a),
+                                 P_<uint32_t>(ctx->idx_b), n, 0, 64, &ctx->d_keys, &ctx->d_perm, s, ~0ull));
+    }
     FMM_TRY(buf_ensure(ctx, ctx->body, (size_t)n * sizeof(typename BodyT<Real>::type)));
     k_gather_pos<Real><<<gblk, 256, 0, s>>>(pos, ctx->d_perm, n, P_<typename BodyT<Real>::type>(ctx->body));
     FMM_LAUNCH(ctx);

@@ -22,6 +22,11 @@ F32, F64 = 0, 1
 
 # every symbol include/fmm.h declares: (restype, argtypes)
 _p, _i, _i64, _d = C.c_void_p, C.c_int, C.c_int64, C.c_double
+# host-logic callbacks of the distributed driver (fmm_hist_fn, fmm_orb_hist_fn, fmm_orb_split_fn)
+HIST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double))
+ORB_HIST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_uint32), C.c_int, C.c_int,
+                          C.POINTER(C.c_double))
+ORB_SPLIT_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_uint32), C.POINTER(C.c_int32))
 SYMBOLS = {
     "fmm_version": (_i, []),
     "fmm_create": (_i, [_i64, _i, _d, _i, _i, _i, C.POINTER(_p)]),
@@ -61,6 +66,30 @@ SYMBOLS = {
     "fmm_orb_histogram": (_i, [_p, _p, _p, _p, _i64, _i, _p, _p, _i, _i, _p, _p]),
     "fmm_orb_split": (_i, [_p, _p, _p, _i64, _i, _p, _p, _p, _p]),
     "fmm_part_pack_dest": (_i, [_p, _p, _p, _p, _i64, _i, _i64, _p, _p, _p, _p, _p]),
+    "fmm_debug_p2p": (_i, [_p, _p, _p, _i64, _p, _p, _p]),
+    "fmm_debug_m2l": (_i, [_p, _p, _p, _i64, _p, _p]),
+    "fmm_debug_check": (_i, [_p, _p]),
+    "fmm_group_create": (_i, [_i, _p]),
+    "fmm_group_destroy": (_i, [_p]),
+    "fmm_dist_unique_id": (_i, [_p]),
+    "fmm_create_dist": (_i, [_i64, _i, _d, _i, _i, _i, _i, _i, _p, _p, _i, _p]),
+    "fmm_set_weights": (_i, [_p, _p, _i64]),
+    "fmm_dist_set_alpha": (_i, [_p, _d, _d]),
+    "fmm_dist_tune_alpha": (_i, [_p, _d, _d, _d]),
+    "fmm_dist_solve": (_i, [_p, _p, _p, _i64, _i64, _i, _p, _p, _p]),
+    "fmm_dist_get_stats": (_i, [_p, _p]),
+    "fmm_dist_local": (_i, [_p, _p, _p]),
+    "fmm_dist_weights": (_i, [_p, _p]),
+    "fmm_dist_orb_boxes": (_i, [_p, _p]),
+    "fmm_dist_timeline": (_i, [_p, _p, _i, _p]),
+    "fmm_dist_timeline_name": (C.c_char_p, [_i]),
+    "fmm_splitters": (_i, [_i, _i, _d, HIST_FN, _p, _p]),
+    "fmm_orb_plan": (_i, [_i, _i, ORB_HIST_FN, ORB_SPLIT_FN, _p, _p]),
+    "fmm_alpha_tuner_create": (_i, [_d, _d, _d, _p]),
+    "fmm_alpha_tuner_next": (_d, [_p]),
+    "fmm_alpha_tuner_report": (_i, [_p, _d]),
+    "fmm_alpha_tuner_state": (_i, [_p, _p, _p, _p, _p, _i]),
+    "fmm_alpha_tuner_destroy": (_i, [_p]),
 }
 LET_MAX_COVER = 73
 
@@ -90,6 +119,17 @@ def lib():
 
 class _Counts(C.Structure):
     _fields_ = [(k, C.c_int64) for k in ("n", "ncell", "nleaf", "depth", "n_m2l", "n_p2p", "p2p_interactions")]
+
+
+class _TreeView(C.Structure):
+    """fmm_tree_view (include/fmm.h): device pointers of a caller-supplied tree."""
+    _fields_ = [("n", C.c_int64), ("ncell", C.c_int64), ("pos", C.c_void_p), ("q", C.c_void_p),
+                ("body_begin", C.c_void_p), ("body_count", C.c_void_p), ("child_count", C.c_void_p),
+                ("center", C.c_void_p), ("level", C.c_void_p), ("M", C.c_void_p), ("root_half_width", C.c_double)]
+
+
+def _tp(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
 
 
 def _np_ptr(a):
@@ -382,6 +422,53 @@ class FMM:
         self._check(lib().fmm_work(self._h, float(c_m2l), float(alpha), C.c_void_p(w.data_ptr()), _np_ptr(lr),
                                    C.c_void_p(self._stream(stream))), "fmm_work")
         return w, lr
+
+    # -- debug stage entry points (caller-supplied tree and lists) ------------
+    def _pairs(self, pairs):
+        import torch
+        if pairs.dtype not in (torch.int32, torch.uint32) or not pairs.is_cuda or not pairs.is_contiguous() \
+                or pairs.dim() != 2 or pairs.shape[1] != 2:
+            raise FMMError(FMM_ERR_ARG, "pairs must be a contiguous CUDA (n, 2) int32/uint32 tensor")
+        return pairs
+
+    def debug_p2p(self, pos, q, body_begin, body_count, child_count, pairs, stream=None):
+        """fmm_debug_p2p: near field (R17) of the given P2P cell pairs on the given sorted bodies
+        and cells; phi [n], grad [n][3] in the bodies' order."""
+        import torch
+        n = pos.shape[0]
+        self._check_tensor(pos, (n, 3), "pos")
+        self._check_tensor(q, (n,), "q")
+        pairs = self._pairs(pairs)
+        v = _TreeView(n=n, ncell=body_begin.shape[0], pos=pos.data_ptr(), q=q.data_ptr(),
+                      body_begin=body_begin.data_ptr(), body_count=body_count.data_ptr(),
+                      child_count=child_count.data_ptr(), root_half_width=0.0)
+        phi = torch.empty(n, dtype=self.dtype, device=pos.device)
+        grad = torch.empty((n, 3), dtype=self.dtype, device=pos.device)
+        self._check(lib().fmm_debug_p2p(self._h, C.byref(v), _tp(pairs), pairs.shape[0], _tp(phi), _tp(grad),
+                                        C.c_void_p(self._stream(stream))), "fmm_debug_p2p")
+        self._pos = None
+        return phi, grad
+
+    def debug_m2l(self, center, level, M, root_half_width, pairs, stream=None):
+        """fmm_debug_m2l: L [ncell][ncoef] (fp64) = R14 summed over the given M2L cell pairs."""
+        import torch
+        nc = center.shape[0]
+        pairs = self._pairs(pairs)
+        L = torch.empty_like(M)
+        v = _TreeView(n=0, ncell=nc, center=center.data_ptr(), level=level.data_ptr(), M=M.data_ptr(),
+                      root_half_width=float(root_half_width))
+        self._check(lib().fmm_debug_m2l(self._h, C.byref(v), _tp(pairs), pairs.shape[0], _tp(L),
+                                        C.c_void_p(self._stream(stream))), "fmm_debug_m2l")
+        self._pos = None
+        return L
+
+    def debug_check(self) -> int:
+        """fmm_debug_check: number of guarded buffers written past their end (FMM_GUARD=1)."""
+        nb = C.c_int64()
+        st = lib().fmm_debug_check(self._h, C.byref(nb))
+        if st not in (FMM_OK, FMM_ERR_STATE):
+            self._check(st, "fmm_debug_check")
+        return int(nb.value)
 
     # -- introspection -----------------------------------------------------
     def counts(self) -> dict:

@@ -19,7 +19,7 @@ def libpath():
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "fmm.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(fmm_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(fmm_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_symbols_exported(libpath):

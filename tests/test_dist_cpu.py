@@ -1,7 +1,8 @@
-"""Host-side logic of the multi-GPU path on CPU (no GPU): the splitter rule, and the
-TorchComm collectives over a world_size-2 gloo group -- the same calls the NCCL run makes
-(all_reduce, all_gather, all_to_all_single with uneven splits) -- checked against the
-in-process LoopbackComm the single-GPU tests use.
+"""Host-side logic of the multi-GPU driver on CPU (no GPU): the library's partition rules
+(fmm_splitters, fmm_orb_plan, fmm_alpha_tuner_*; csrc/dist.cu) driven through their callback
+entry points, and the same rules over a world_size-2 gloo process group: each process holds half
+of the particles, its histogram callback all-reduces over gloo -- the N>1 partition step the
+driver runs over NCCL -- and both ranks must agree on the splitters and the ORB boxes.
 """
 import os
 import socket
@@ -13,7 +14,7 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
-from paper_1405_7487_b200.dist import LoopbackComm, TorchComm, choose_bins, partition_splitters
+from paper_1405_7487_b200.dist import partition_splitters
 
 
 def _free_port():
@@ -37,12 +38,6 @@ def _host_hist_fn(keys, w=None):
             out[r] = np.bincount(b, weights=w[sel], minlength=1 << bits)
         return out
     return fn
-
-
-def test_choose_bins():
-    b, r = choose_bins(np.array([1.0, 0.0, 3.0, 2.0]), np.array([0.5, 1.0, 2.5, 6.0]))
-    np.testing.assert_array_equal(b, [0, 0, 2, 3])
-    np.testing.assert_array_equal(r, [0.5, 1.0, 1.5, 2.0])
 
 
 @pytest.mark.parametrize("kind", ["cube", "plummer"])
@@ -80,30 +75,53 @@ def test_partition_degenerate():
 
 def _worker(rank, world, port, q):
     import torch.distributed as dist
+    from paper_1405_7487_b200.dist import orb_plan
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        cm = TorchComm()
-        x = torch.tensor([1.0 + rank, -2.0 * rank, 5.0])
-        s = cm.allreduce([x], "sum")[0].tolist()
-        mn = cm.allreduce([x], "min")[0].tolist()
-        mx = cm.allreduce([x], "max")[0].tolist()
-        g = [t.tolist() for t in cm.allgather([torch.arange(3, dtype=torch.float64) + 10 * rank])[0]]
-        # uneven byte messages: rank r sends r*3 + j + 1 bytes to rank j, valued 16*r + j
-        sends = [torch.full((rank * 3 + j + 1,), 16 * rank + j, dtype=torch.uint8) for j in range(world)]
-        recv = [t.tolist() for t in cm.alltoallv([sends])[0]]
-        h = cm.alltoallv([sends], async_op=True)
-        recv2 = [t.tolist() for t in h.wait()[0]]
-        # ring round 1: send to rank+1, receive from rank-1 (sizes known in advance)
-        dst, src = (rank + 1) % world, (rank - 1) % world
-        msg = torch.full((3 + rank,), 7 * rank + 1, dtype=torch.uint8)
-        ring = cm.sendrecv([msg], [dst], [src], [3 + src], async_op=True).wait()[0].tolist()
-        q.put((rank, s, mn, mx, g, recv, recv2, ring))
+        pos, _ = synth.generate("plummer", 20000, 5)
+        mine = slice(rank * 10000, (rank + 1) * 10000)           # this process's particles
+        k = oracle.keys(pos)[mine]
+        local = _host_hist_fn(k)
+
+        def global_hist(prefixes, pbits, bits):               # the all-reduce the driver does
+            h = torch.from_numpy(np.ascontiguousarray(local(prefixes, pbits, bits)))
+            dist.all_reduce(h)
+            return h.numpy()
+        spl = partition_splitters(global_hist, 4)
+        xyz = _coords(k)
+        grp = np.zeros(len(k), dtype=np.int64)
+
+        def orb_hist(axis, prefix, pbits, bits):
+            out = np.zeros((4, 1 << bits))
+            for g in range(4):
+                if axis[g] < 0:
+                    continue
+                c = xyz[:, axis[g]]
+                sel = grp == g
+                if pbits:
+                    sel &= (c >> (21 - pbits)) == prefix[g]
+                out[g] = np.bincount((c[sel] >> (21 - pbits - bits)) & ((1 << bits) - 1), minlength=1 << bits)
+            h = torch.from_numpy(out)
+            dist.all_reduce(h)
+            return h.numpy()
+
+        def orb_split(axis, cut, right):
+            for g in range(4):
+                if axis[g] >= 0:
+                    grp[(grp == g) & (xyz[:, axis[g]] >= cut[g])] = right[g]
+        boxes = orb_plan(orb_hist, orb_split, 4)
+        q.put((rank, spl.tolist(), {r: (b["lo"], b["hi"]) for r, b in boxes.items()},
+               np.bincount(np.searchsorted(spl, k, side="right"), minlength=4).tolist(),
+               np.bincount(grp, minlength=4).tolist()))
     finally:
         dist.destroy_process_group()
 
 
-def test_torchcomm_gloo_matches_loopback():
+def test_partition_rules_over_gloo():
+    """world_size 2 (gloo): the driver's splitter and ORB rules with globally all-reduced
+    histograms give both ranks the same splitters and boxes, equal to the single-process rules
+    on all particles, and balanced global shares."""
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -113,28 +131,19 @@ def test_torchcomm_gloo_matches_loopback():
         p.start()
     res = {}
     for _ in range(world):
-        r = q.get(timeout=120)
+        r = q.get(timeout=180)
         res[r[0]] = r
     for p in ps:
         p.join(timeout=60)
         assert p.exitcode == 0
-    # the same collectives in-process
-    lb = LoopbackComm(world)
-    xs = [torch.tensor([1.0 + r, -2.0 * r, 5.0]) for r in range(world)]
-    sends = [[torch.full((r * 3 + j + 1,), 16 * r + j, dtype=torch.uint8) for j in range(world)] for r in range(world)]
-    ls = lb.allreduce(xs, "sum"); lmn = lb.allreduce(xs, "min"); lmx = lb.allreduce(xs, "max")
-    lg = lb.allgather([torch.arange(3, dtype=torch.float64) + 10 * r for r in range(world)])
-    lr = lb.alltoallv(sends)
-    lring = lb.sendrecv([torch.full((3 + r,), 7 * r + 1, dtype=torch.uint8) for r in range(world)],
-                        [(r + 1) % world for r in range(world)], [(r - 1) % world for r in range(world)],
-                        [3 + (r - 1) % world for r in range(world)])
-    for r in range(world):
-        _, s, mn, mx, g, recv, recv2, ring = res[r]
-        assert ring == lring[r].tolist() == [7 * ((r - 1) % world) + 1] * (3 + (r - 1) % world)
-        assert s == ls[r].tolist() and mn == lmn[r].tolist() and mx == lmx[r].tolist()
-        assert g == [t.tolist() for t in lg[r]]
-        assert recv == [t.tolist() for t in lr[r]] == recv2
-        assert recv[1 - r] == [16 * (1 - r) + r] * ((1 - r) * 3 + r + 1)
+    assert res[0][1] == res[1][1] and res[0][2] == res[1][2]
+    pos, _ = synth.generate("plummer", 20000, 5)
+    k = oracle.keys(pos)
+    assert res[0][1] == partition_splitters(_host_hist_fn(k), 4).tolist()
+    cnt = np.array(res[0][3]) + np.array(res[1][3])
+    assert np.abs(cnt - 5000).max() <= 0.01 * 5000 + 1, cnt
+    ocnt = np.array(res[0][4]) + np.array(res[1][4])
+    assert np.abs(ocnt - 5000).max() <= 0.01 * 5000 + 1, ocnt
 
 
 def _coords(keys):
@@ -186,8 +195,8 @@ def test_orb_plan_balanced_boxes(K, kind):
 
 
 def _run_tuner(cost, steps, **kw):
-    """Drive AlphaTuner the way DistFMM.solve does: alpha_k is set before step k's weights, and
-    step k's runtime reflects the partition made with alpha_{k-1}."""
+    """Drive the library's alpha tuner the way fmm_dist_solve does: alpha_k is set before step k's
+    weights, and step k's runtime reflects the partition made with alpha_{k-1}."""
     from paper_1405_7487_b200.dist import AlphaTuner
     tu = AlphaTuner(**kw)
     prev = None

@@ -1,10 +1,12 @@
-"""Multi-GPU path on ONE GPU: K ranks driven by one process (LoopbackComm),
-checked against the oracle's per-partition mode (oracle.traverse_pair / evaluate_multi).
+"""Multi-GPU path on ONE GPU: K ranks of the library's distributed driver
+(fmm_create_dist + fmm_dist_solve, csrc/dist.cu) in one process -- an in-process group (fmm_group),
+one host thread per rank -- checked against the oracle's per-partition mode
+(oracle.traverse_pair / evaluate_multi).
 
 Bar: rank i's lists over (local tree + grafted LETs) equal the oracle's
 lists of T_i against every full local tree S_j, bit-exact (remote sources mapped back to the
 sender's cell ids); phi / grad against evaluate_multi at the §8(c) tolerances.  The ranks
-run one after another: no kernel waits on another rank's kernel.
+meet at host barriers; no kernel waits on another rank's kernel.
 """
 import numpy as np
 import pytest
@@ -28,17 +30,54 @@ def torch_cuda():
     return torch
 
 
-def run_dist(torch, kind, n, K, P, theta, ncrit, prec, seed, part="morton"):
-    from paper_1405_7487_b200.dist import DistFMM, LoopbackComm
-    dt = np.float32 if prec == "f32" else np.float64
-    tdt = torch.float32 if prec == "f32" else torch.float64
-    pos, q = synth.generate(kind, n, seed, dt)
+class Ranks:
+    """K DistFMM contexts of one LocalGroup and their last step's results."""
+
+    def __init__(self, torch, K, n_max, P, theta, ncrit, prec, part="morton"):
+        from paper_1405_7487_b200.dist import DistFMM, LocalGroup
+        self.torch, self.K = torch, K
+        self.group = LocalGroup(K)
+        self.fmm = [DistFMM(n_max, P, theta, ncrit, prec, 0, K, r, group=self.group, partitioner=part)
+                    for r in range(K)]
+        self.streams = [torch.cuda.Stream() for _ in range(K)]
+
+    def solve(self, P_in, Q_in, bases, reuse_weights=False):
+        from paper_1405_7487_b200.dist import run_ranks
+
+        def body(r):
+            st = self.streams[r]
+            out = self.fmm[r].solve(P_in[r], Q_in[r], bases[r], reuse_weights=reuse_weights, stream=st)
+            st.synchronize()
+            return out
+        out = run_ranks(body, self.K)
+        self.local = [f.local() for f in self.fmm]             # (gids, peers) per rank
+        return out
+
+    @property
+    def global_bounds(self):
+        return self.fmm[0].stats()["bounds"]
+
+    def close(self):
+        for f in self.fmm:
+            f.close()
+        self.group.close()
+
+
+def split_input(torch, pos, q, K):
     # initial ownership: contiguous index slices (not spatial), as a user would hold them
+    n = len(pos)
     cuts = np.linspace(0, n, K + 1).astype(int)
-    P_in = [torch.from_numpy(pos[cuts[r]:cuts[r + 1]]).cuda() for r in range(K)]
-    Q_in = [torch.from_numpy(q[cuts[r]:cuts[r + 1]]).cuda() for r in range(K)]
-    D = DistFMM(LoopbackComm(K), n, P, theta, ncrit, prec, partitioner=part)
-    out = D.solve(P_in, Q_in, [int(c) for c in cuts[:-1]])
+    P_in = [torch.from_numpy(np.ascontiguousarray(pos[cuts[r]:cuts[r + 1]])).cuda() for r in range(K)]
+    Q_in = [torch.from_numpy(np.ascontiguousarray(q[cuts[r]:cuts[r + 1]])).cuda() for r in range(K)]
+    return P_in, Q_in, [int(c) for c in cuts[:-1]]
+
+
+def run_dist(torch, kind, n, K, P, theta, ncrit, prec, seed, part="morton"):
+    dt = np.float32 if prec == "f32" else np.float64
+    pos, q = synth.generate(kind, n, seed, dt)
+    P_in, Q_in, bases = split_input(torch, pos, q, K)
+    D = Ranks(torch, K, n, P, theta, ncrit, prec, part)
+    out = D.solve(P_in, Q_in, bases)
     torch.cuda.synchronize()
     phi = np.concatenate([o[0].cpu().numpy() for o in out]).astype(np.float64)
     grad = np.concatenate([o[1].cpu().numpy() for o in out]).astype(np.float64)
@@ -63,8 +102,7 @@ CASES = [
 @pytest.mark.parametrize("kind,n,K,P,theta,ncrit,prec,part", CASES)
 def test_dist_lists_and_fields(torch_cuda, kind, n, K, P, theta, ncrit, prec, part):
     D, pos, q, phi, grad = run_dist(torch_cuda, kind, n, K, P, theta, ncrit, prec, 500 + n + K, part)
-    lpos, lq, lgid = D.local
-    gids = [g.cpu().numpy() for g in lgid]
+    gids = [g for g, _ in D.local]
     # every particle lands on exactly one rank, and the ranks are Morton ranges of similar size
     allg = np.sort(np.concatenate(gids))
     np.testing.assert_array_equal(allg, np.arange(n))
@@ -73,13 +111,15 @@ def test_dist_lists_and_fields(torch_cuda, kind, n, K, P, theta, ncrit, prec, pa
     if part == "orb":   # ORB boxes are axis-aligned and disjoint: each rank's particles lie in its box
         from oracle import keys as okeys
         k = okeys(pos.astype(np.float64))
-        for r, g in D.orb_groups.items():
+        boxes = D.fmm[0].orb_boxes()
+        for r in range(K):
+            assert np.array_equal(D.fmm[r].orb_boxes(), boxes)      # every rank made the same plan
             kk = k[gids[r]]
             for a in range(3):
                 c = np.zeros(len(kk), dtype=np.int64)
                 for l in range(21):
                     c |= (((kk >> np.uint64(3 * l + a)) & np.uint64(1)).astype(np.int64)) << l
-                assert np.all((c >= g["lo"][a]) & (c < g["hi"][a]))
+                assert np.all((c >= boxes[r, a]) & (c < boxes[r, 3 + a]))
     # oracle trees of every rank, built from the rank's particles in the order the rank holds them
     rb = D.global_bounds if part == "morton" else None   # the root cube the ranks built on
     O = [oracle.FMM(pos[g].astype(np.float64), q[g].astype(np.float64), P, theta, ncrit, bounds=rb) for g in gids]
@@ -87,7 +127,7 @@ def test_dist_lists_and_fields(torch_cuda, kind, n, K, P, theta, ncrit, prec, pa
         f = D.fmm[i]
         m2l, p2p = f.lists()
         nci = f.counts()["ncell"]
-        peers = D._peers[i]
+        peers = D.local[i][1]
         regions = [f.let_remote(k) for k in range(len(peers))]
 
         def split(lst):
@@ -118,6 +158,9 @@ def test_dist_lists_and_fields(torch_cuda, kind, n, K, P, theta, ncrit, prec, pa
     # fields: rank-local results against the oracle's multi-tree evaluation, and the gathered
     # (original-order) results against the same numbers
     ref_phi = np.zeros(n); ref_grad = np.zeros((n, 3))
+    st = [f.stats() for f in D.fmm]
+    assert all(np.array_equal(x["bounds"], st[0]["bounds"]) for x in st)
+    assert sum(x["n_local"] for x in st) == n
     for i in range(K):
         o_phi, o_grad = oracle.evaluate_multi(O[i], [O[j] for j in range(K) if j != i])
         ref_phi[gids[i]] = o_phi
@@ -127,6 +170,7 @@ def test_dist_lists_and_fields(torch_cuda, kind, n, K, P, theta, ncrit, prec, pa
     t = synth.sample_targets(n, 200, 7)
     dp, dg = oracle.direct(pos.astype(np.float64), q.astype(np.float64), t)
     assert oracle.rel_l2(phi[t], dp) <= 1e-2 and oracle.rel_l2(grad[t], dg) <= 5e-2
+    D.close()
 
 
 def test_dist_single_rank_equals_single_gpu(torch_cuda):
@@ -145,7 +189,7 @@ def test_let_needs_subset_of_remote_tree(torch_cuda):
     D, pos, q, phi, grad = run_dist(torch_cuda, "cube", 30000, 4, 4, 0.5, 16, "f64", 21)
     for i in range(4):
         f = D.fmm[i]
-        for k, j in enumerate(D._peers[i]):
+        for k, j in enumerate(D.local[i][1]):
             _, ncl, nbd, orig = f.let_remote(k)
             assert ncl < D.fmm[j].counts()["ncell"]
             assert nbd < D.fmm[j].counts()["n"]
@@ -161,7 +205,7 @@ def _host_work(D, i, c, alpha):
     m2l, p2p = f.lists()
     # body counts of every source index (local cells, then each grafted LET)
     src_bc = {}
-    for k, j in enumerate(D._peers[i]):
+    for k, j in enumerate(D.local[i][1]):
         base, ncl, _, orig = f.let_remote(k)
         rb = D.fmm[j].cells()["body_count"].astype(np.float64)[orig]
         for t in range(ncl):
@@ -209,40 +253,41 @@ def test_work_weights_eq1(torch_cuda, K):
 def test_weighted_partition_balances_work(torch_cuda):
     """Second step partitions with the first step's Eq. (1) weights: the ranks' shares of the
     (first-step) work are balanced, where the unweighted split by particle count is not."""
-    import torch
-    from paper_1405_7487_b200.dist import DistFMM, LoopbackComm
+    torch = torch_cuda
     n, K = 20000, 4
     pos, q = synth.generate("plummer", n, 77, np.float64)
-    cuts = np.linspace(0, n, K + 1).astype(int)
-    P_in = [torch.from_numpy(pos[cuts[r]:cuts[r + 1]]).cuda() for r in range(K)]
-    Q_in = [torch.from_numpy(q[cuts[r]:cuts[r + 1]]).cuda() for r in range(K)]
-    D = DistFMM(LoopbackComm(K), n, 4, 0.5, 16, "f64")
-    D.solve(P_in, Q_in, [int(c) for c in cuts[:-1]])
-    w1 = np.concatenate([w.cpu().numpy() for w in D.weights]).astype(np.float64)   # owner order = global order
-    g1 = [g.cpu().numpy() for g in D.local[2]]
+    P_in, Q_in, bases = split_input(torch, pos, q, K)
+    D = Ranks(torch, K, n, 4, 0.5, 16, "f64")
+    D.solve(P_in, Q_in, bases)
+    w1 = np.concatenate([D.fmm[r].weights(len(P_in[r])) for r in range(K)]).astype(np.float64)  # owner order
+    g1 = [g for g, _ in D.local]
     share1 = np.array([w1[g].sum() for g in g1]) / w1.sum()
-    D.solve(P_in, Q_in, [int(c) for c in cuts[:-1]], reuse_weights=True)
-    g2 = [g.cpu().numpy() for g in D.local[2]]
+    D.solve(P_in, Q_in, bases, reuse_weights=True)
+    g2 = [g for g, _ in D.local]
     share2 = np.array([w1[g].sum() for g in g2]) / w1.sum()
     assert np.abs(share2 - 1.0 / K).max() < 0.01, share2
     assert np.abs(share1 - 1.0 / K).max() > np.abs(share2 - 1.0 / K).max(), (share1, share2)
+    # the same weights given explicitly (fmm_set_weights) make the same partition
+    for r in range(K):
+        D.fmm[r].set_weights(torch.from_numpy(w1[bases[r]:bases[r] + len(P_in[r])].astype(np.float32)).cuda())
+    D.solve(P_in, Q_in, bases)
+    for a, b in zip(g2, [g for g, _ in D.local]):
+        np.testing.assert_array_equal(a, b)
+    D.close()
 
 
 @pytest.mark.parametrize("part", ["morton", "orb"])
 def test_dist_degenerate(torch_cuda, part):
     """Ranks left empty by the partition (3 particles on 4 ranks; all particles coincident):
     the distributed path still returns the direct sum."""
-    import torch
-    from paper_1405_7487_b200.dist import DistFMM, LoopbackComm
+    torch = torch_cuda
     for pos in (np.array([[0.1, 0.2, 0.3], [0.9, 0.8, 0.7], [0.5, 0.5, 0.1]]),
                 np.tile(np.array([[0.25, 0.5, 0.75]]), (40, 1))):
         n, K = len(pos), 4
         q = np.linspace(-1.0, 1.0, n)
-        cuts = np.linspace(0, n, K + 1).astype(int)
-        P_in = [torch.from_numpy(np.ascontiguousarray(pos[cuts[r]:cuts[r + 1]])).cuda() for r in range(K)]
-        Q_in = [torch.from_numpy(np.ascontiguousarray(q[cuts[r]:cuts[r + 1]])).cuda() for r in range(K)]
-        D = DistFMM(LoopbackComm(K), n, 4, 0.5, 2, "f64", partitioner=part)
-        out = D.solve(P_in, Q_in, [int(c) for c in cuts[:-1]])
+        P_in, Q_in, bases = split_input(torch, pos, q, K)
+        D = Ranks(torch, K, n, 4, 0.5, 2, "f64", part)
+        out = D.solve(P_in, Q_in, bases)
         phi = np.concatenate([o[0].cpu().numpy() for o in out])
         grad = np.concatenate([o[1].cpu().numpy() for o in out])
         dp, dg = oracle.direct(pos, q)
@@ -252,19 +297,18 @@ def test_dist_degenerate(torch_cuda, part):
 
 
 def test_alpha_tuning_steps(torch_cuda):
-    """Eq. (1) alpha optimised over time steps: a tuned multi-step run changes
-    alpha between steps (probes of the golden-section search), and every step still returns the
-    direct sum within the FMM error of a single-rank solve."""
-    import torch
+    """Eq. (1) alpha optimised over time steps (fmm_dist_tune_alpha): a tuned
+    multi-step run changes alpha between steps (probes of the golden-section search), every rank
+    uses the same alpha, and every step still returns the direct sum within the FMM error of a
+    single-rank solve."""
+    torch = torch_cuda
     from paper_1405_7487_b200 import FMM
-    from paper_1405_7487_b200.dist import DistFMM, LoopbackComm
     n, K = 12000, 3
     pos, q = synth.generate("plummer", n, 5, np.float64)
-    cuts = np.linspace(0, n, K + 1).astype(int)
-    P_in = [torch.from_numpy(pos[cuts[r]:cuts[r + 1]]).cuda() for r in range(K)]
-    Q_in = [torch.from_numpy(q[cuts[r]:cuts[r + 1]]).cuda() for r in range(K)]
-    D = DistFMM(LoopbackComm(K), n, 6, 0.5, 16, "f64")
-    tu = D.enable_alpha_tuning(lo=0.25, hi=4.0, tol=0.2)
+    P_in, Q_in, bases = split_input(torch, pos, q, K)
+    D = Ranks(torch, K, n, 6, 0.5, 16, "f64")
+    for f in D.fmm:
+        f.tune_alpha(0.25, 4.0, 0.2)
     t = synth.sample_targets(n, 300, 5)
     dphi, dgrad = oracle.direct(pos, q, t)
     f1 = FMM(n, 6, 0.5, 16, "f64")
@@ -272,12 +316,63 @@ def test_alpha_tuning_steps(torch_cuda):
     e1 = oracle.rel_l2(p1.cpu().numpy()[t], dphi)
     alphas = []
     for _ in range(8):
-        out = D.solve(P_in, Q_in, [int(c) for c in cuts[:-1]], reuse_weights=True)
-        alphas.append(D.alpha)
+        out = D.solve(P_in, Q_in, bases, reuse_weights=True)
+        al = [f.alpha for f in D.fmm]
+        assert len(set(al)) == 1, al
+        alphas.append(al[0])
         phi = np.concatenate([o[0].cpu().numpy() for o in out])
         grad = np.concatenate([o[1].cpu().numpy() for o in out])
         assert oracle.rel_l2(phi[t], dphi) < 10 * e1 + 1e-12
         assert oracle.rel_l2(grad[t], dgrad) < 1e-3
     assert len(set(alphas)) >= 2, alphas
-    assert len(tu.history) >= 3
+    assert D.fmm[0].stats()["tuner_probes"] >= 3
+    D.close()
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_partition_overlap_bit_identical(torch_cuda, prec, monkeypatch):
+    """f1: the staying particles sorted while the partition exchange flies and the
+    arrivals merged in (default) give bit-identical keys, permutation, cells, lists and fields to a
+    full sort after the exchange (FMM_DIST_SORT=0), over two steps with reused Eq. (1) weights."""
+    torch = torch_cuda
+    n, K = 30000, 3
+    dt = np.float32 if prec == "f32" else np.float64
+    pos, q = synth.generate("plummer", n, 12, dt)
+    P_in, Q_in, bases = split_input(torch, pos, q, K)
+    A = Ranks(torch, K, n, 6, 0.5, 32, prec)
+    monkeypatch.setenv("FMM_DIST_SORT", "0")
+    B = Ranks(torch, K, n, 6, 0.5, 32, prec)
+    for reuse in (False, True):
+        oa = A.solve(P_in, Q_in, bases, reuse_weights=reuse)
+        ob = B.solve(P_in, Q_in, bases, reuse_weights=reuse)
+        for r in range(K):
+            np.testing.assert_array_equal(oa[r][0].cpu().numpy(), ob[r][0].cpu().numpy())
+            np.testing.assert_array_equal(oa[r][1].cpu().numpy(), ob[r][1].cpu().numpy())
+            fa, fb = A.fmm[r], B.fmm[r]
+            for x, y in zip(fa.sorted(), fb.sorted()):
+                np.testing.assert_array_equal(x, y)
+            for x, y in zip(fa.lists(), fb.lists()):
+                np.testing.assert_array_equal(x, y)
+    A.close()
+    B.close()
+
+
+def test_dist_timeline_overlap(torch_cuda):
+    """fmm_dist_timeline: the LET structure exchange is posted before the local traversal (their
+    spans overlap or the exchange ends first), the data exchange starts after the upward pass, and
+    the staying-particle sort starts before the particle exchange ends."""
+    torch = torch_cuda
+    n, K = 60000, 2
+    pos, q = synth.generate("cube", n, 3, np.float32)
+    P_in, Q_in, bases = split_input(torch, pos, q, K)
+    D = Ranks(torch, K, n, 10, 0.4, 64, "f32")
+    for f in D.fmm:
+        f.set_timing(True)
+    D.solve(P_in, Q_in, bases)
+    D.solve(P_in, Q_in, bases, reuse_weights=True)
+    for f in D.fmm:
+        tl = f.timeline()
+        assert tl["let_struct_exchange"][0] <= tl["local_dtt"][0] + 1e-3, tl
+        assert tl["let_data_exchange"][1] >= tl["upward"][1] - 1e-3, tl
+        assert tl["stay_sort"][0] <= tl["particle_exchange"][1] + 1e-3, tl
     D.close()

@@ -410,3 +410,58 @@ def test_switch_alternatives(torch_cuda, env, prec, monkeypatch):
         check_structure(f, o)
         ophi, ograd = o.evaluate()
         assert_fields(phi.cpu().numpy(), ophi, grad.cpu().numpy(), ograd, TOL[prec], f"{env} {kind}")
+
+
+@pytest.mark.parametrize("kind,n,P,theta,ncrit,prec", [("cube", 4096, 4, 0.5, 32, "f64"),
+                                                       ("plummer", 5000, 10, 0.4, 64, "f32"),
+                                                       ("sphere", 3000, 6, 0.5, 16, "f64")])
+def test_debug_stages_on_oracle_tree(torch_cuda, kind, n, P, theta, ncrit, prec):
+    """fmm_debug_p2p / fmm_debug_m2l (SURVEY §8(b) debug entry points) fed the ORACLE's sorted
+    bodies, cells and canonical lists: the product P2P kernels against per-pair oracle.p2p (R17)
+    sums, the product M2L kernels against per-pair oracle.m2l (R14) sums on the oracle's M."""
+    torch = torch_cuda
+    from paper_1405_7487_b200 import FMM
+    dt = np.float32 if prec == "f32" else np.float64
+    tdt = torch.float32 if prec == "f32" else torch.float64
+    pos, q = synth.generate(kind, n, 300 + n, dt)
+    p64, q64 = pos.astype(np.float64), q.astype(np.float64)
+    o = oracle.FMM(p64, q64, P, theta, ncrit).traverse()
+    o.evaluate()
+    _, perm = o.sorted()
+    cells = o.cells()
+    m2l, p2p = o.lists()
+    M, _ = o.expansions()
+    sp, sq = p64[perm], q64[perm]
+    bb, bc = cells["body_begin"], cells["body_count"]
+    # references: per-pair sums of the pinned oracle stage functions
+    rphi = np.zeros(n); rgrad = np.zeros((n, 3))
+    for a, b in p2p:
+        ph, gr = oracle.p2p(sp[bb[a]:bb[a] + bc[a]], sp[bb[b]:bb[b] + bc[b]], sq[bb[b]:bb[b] + bc[b]])
+        rphi[bb[a]:bb[a] + bc[a]] += ph
+        rgrad[bb[a]:bb[a] + bc[a]] += gr
+    rL = np.zeros_like(M)
+    c = cells["center"]
+    for a, b in m2l:
+        oracle.m2l(P, M[b], c[a] - c[b], rL[a])
+    f = FMM(n, P, theta, ncrit, prec)
+    cu = lambda x, d=None: torch.from_numpy(np.ascontiguousarray(x if d is None else x.astype(d))).cuda()  # noqa: E731
+    u32 = lambda x: cu(x.astype(np.int32))  # noqa: E731
+    phi, grad = f.debug_p2p(cu(pos[perm]), cu(q[perm]), u32(bb), u32(bc), u32(cells["child_count"]), u32(p2p))
+    torch.cuda.synchronize()
+    assert phi.dtype == tdt
+    assert_fields(phi.cpu().numpy(), rphi, grad.cpu().numpy(), rgrad, TOL[prec], "debug_p2p")
+    h = 0.5 * float(np.max(cells["bmax"][0] - cells["bmin"][0]))   # R2 half-width (root box = all bodies)
+    L = f.debug_m2l(cu(c), cu(cells["level"]), cu(M), h, u32(m2l)).cpu().numpy()
+    # fp64 kernels: 1e-11 of the largest coefficient; fp32 M2L arithmetic (R19): per degree, the
+    # fp32 operand rounding relative to that degree's largest coefficient
+    tol = 1e-11 if prec == "f64" else 2e-5
+    ex = oracle.multi_indices(P).sum(axis=1)
+    for deg in range(P):
+        k = ex == deg
+        scale = np.abs(rL[:, k]).max()
+        assert np.abs(L[:, k] - rL[:, k]).max() <= tol * scale, (deg, np.abs(L[:, k] - rL[:, k]).max() / scale)
+    # a list out of canonical order is rejected
+    from paper_1405_7487_b200 import FMMError
+    bad = p2p[::-1].copy()
+    with pytest.raises(FMMError):
+        f.debug_p2p(cu(pos[perm]), cu(q[perm]), u32(bb), u32(bc), u32(cells["child_count"]), u32(bad))
