@@ -109,6 +109,7 @@ struct fmm_ctx {
     DevBuf mut_mir, mut_w, mut_so, mut_slot;
     int m2l_variant = 0;        // fp32 register M2L: 0 mirror-paired f32x2, 1 scalar (FMM_M2L_VARIANT)
     int p2p_np = 2;             // CTA P2P: target pairs per thread (FMM_P2P_NP = 1, 2, 4)        // 0: CTA per leaf over source runs, 1: warp per leaf (FMM_P2P_VARIANT)
+    bool m2l_deep = false;       // m2l_pass: tree spans > 14 levels, fp32 mode uses the fp64 kernel
     int m2l_part = 0;            // m2l_pass: 0 all, 1 operand preparation only, 2 without it (fmm_solve split)
     int list_sort = 0;           // list grouping: 0 counting scatter + per-segment sorts, 1 one radix sort of the packed pairs (FMM_LIST_SORT)
     bool canonical_m2l = true;   // sort M2L sources within each target on the device (FMM_CANONICAL_M2L=0: skip)

@@ -515,6 +515,22 @@ static fmm_status dist_step(fmm_ctx* ctx, DistState* D, const void* pos, const v
         FMM_TRY(buf_ensure(ctx, D->si, (size_t)std::max<int64_t>(nstay, 1) * 8));
     }
     FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[1], m));   // packed particles ready
+    // the staying particles' sort is enqueued first, so it runs while the exchange flies
+    if (presort && nstay > 0) {
+        FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(side, D->ev[1], 0));
+        S.tl_begin(TL_STAY_SORT, side);
+        uint64_t* k0 = P_<uint64_t>(D->sk);
+        uint32_t* i0 = P_<uint32_t>(D->si);
+        FMM_TRY(fmm_part_keys(ctx, (char*)D->pk_pos.p + soff[me] * 3 * es, nstay, D->gb, k0, side));
+        k_iota_u32<<<grid1(nstay), 256, 0, side>>>(nstay, (uint32_t)roff[me], i0);
+        FMM_LAUNCH(ctx);
+        uint64_t* ko = nullptr;
+        uint32_t* io = nullptr;
+        FMM_TRY(radix_sort_pairs(ctx, k0, k0 + nstay, i0, i0 + nstay, nstay, 0, 64, &ko, &io, side, ~0ull));
+        D->stay_in_b = ko != k0;
+        S.tl_end(TL_STAY_SORT, side);
+        FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[3], side));
+    }
     FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(cs, D->ev[1], 0));
     S.tl_begin(TL_EXCHANGE, cs);
     {
@@ -541,21 +557,6 @@ static fmm_status dist_step(fmm_ctx* ctx, DistState* D, const void* pos, const v
     }
     S.tl_end(TL_EXCHANGE, cs);
     FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[2], cs));   // local particles landed
-    if (presort && nstay > 0) {
-        FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(side, D->ev[1], 0));
-        S.tl_begin(TL_STAY_SORT, side);
-        uint64_t* k0 = P_<uint64_t>(D->sk);
-        uint32_t* i0 = P_<uint32_t>(D->si);
-        FMM_TRY(fmm_part_keys(ctx, (char*)D->pk_pos.p + soff[me] * 3 * es, nstay, D->gb, k0, side));
-        k_iota_u32<<<grid1(nstay), 256, 0, side>>>(nstay, (uint32_t)roff[me], i0);
-        FMM_LAUNCH(ctx);
-        uint64_t* ko = nullptr;
-        uint32_t* io = nullptr;
-        FMM_TRY(radix_sort_pairs(ctx, k0, k0 + nstay, i0, i0 + nstay, nstay, 0, 64, &ko, &io, side, ~0ull));
-        D->stay_in_b = ko != k0;
-        S.tl_end(TL_STAY_SORT, side);
-        FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[3], side));
-    }
     FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(m, D->ev[2], 0));
     // ---- 4. local tree on the global root cube (Morton) / local box (ORB)
     S.tl_begin(TL_TREE, m);

@@ -44,6 +44,10 @@ static_assert(sizeof(LetHeader) == 64, "LetHeader is 64 B");
 constexpr int64_t LET_MAGIC = 0x4c45543031ll;   // "LET01"
 
 size_t let_body_size(int prec) { return prec == FMM_F32 ? sizeof(float4) : sizeof(dbody); }
+// bytes per shipped multipole coefficient: fp32 contexts ship the fp32 operand precision the M2L
+// reads (R19), scaled by the cell's power-of-two rho^-|beta| (exact, keeps the fp32 range);
+// fp64 contexts ship fp64
+size_t let_m_size(int prec) { return prec == FMM_F32 ? 4 : 8; }
 // data message: header | M [ncell][ncoef] fp64 | q [nbody]; each part padded to 16 B
 size_t let_round16(size_t b) { return (b + 15) / 16 * 16; }
 
@@ -174,6 +178,41 @@ __global__ void k_let_pack_M(int64_t nc, int ncoef, const uint32_t* __restrict__
     }
 }
 
+__device__ __forceinline__ int coef_degree(int k) {
+    int n = 0;
+    while (ncoef_of(n + 1) <= k) ++n;
+    return n;
+}
+
+// fp32 mode: M_beta / rho^|beta| as float, rho = 2^(E - level) of the sender's cell
+__global__ void k_let_pack_M32(int64_t nc, int ncoef, const uint32_t* __restrict__ eflag,
+                               const uint32_t* __restrict__ eidx, const int32_t* __restrict__ level,
+                               const double* __restrict__ root, const double* __restrict__ M, float* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int E;
+    frexp(2.0 * root[10], &E);
+    for (int64_t c = w; c < nc; c += nw) {
+        if (!eflag[c]) continue;
+        const int e = E - level[c];
+        const double* src = M + (size_t)c * ncoef;
+        float* dst = out + (size_t)eidx[c] * ncoef;
+        for (int k = lane; k < ncoef; k += 32) dst[k] = (float)ldexp(src[k], -e * coef_degree(k));
+    }
+}
+
+// receiver: the grafted cell's level' = E_local - e_sender (k_let_graft_cells) gives back e exactly
+__global__ void k_let_unpack_M32(int64_t m, int ncoef, const float* __restrict__ in, const int32_t* __restrict__ level,
+                                 const double* __restrict__ root, double* __restrict__ M) {
+    int E;
+    frexp(2.0 * root[10], &E);
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m * ncoef; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = t / ncoef;
+        const int k = (int)(t - c * ncoef);
+        M[t] = ldexp((double)in[t], (E - level[c]) * coef_degree(k));
+    }
+}
+
 // graft one peer's cells at [base, base + m): indices rebased, scale exponent re-expressed as
 // a level of this tree (E_local - e) so the M2L operand preparation reproduces it exactly
 __global__ void k_let_graft_cells(int64_t m, const LetCell* __restrict__ in, int64_t base, int64_t bbase,
@@ -300,7 +339,7 @@ fmm_status let_plan(fmm_ctx* ctx, int peer, const double* cover, int ncover, int
     lp.planned = true;
     const size_t bs = let_body_size(ctx->prec), rs = ctx->prec == FMM_F32 ? 4 : 8;
     *sbytes = (int64_t)(sizeof(LetHeader) + (size_t)lp.ncell * sizeof(LetCell) + (size_t)lp.nbody * bs);
-    *dbytes = (int64_t)(sizeof(LetHeader) + let_round16((size_t)lp.ncell * ctx->ncoef * 8) +
+    *dbytes = (int64_t)(sizeof(LetHeader) + let_round16((size_t)lp.ncell * ctx->ncoef * let_m_size(ctx->prec)) +
                         let_round16((size_t)lp.nbody * rs));
     return FMM_OK;
 }
@@ -339,9 +378,14 @@ fmm_status let_pack(fmm_ctx* ctx, int peer, int part, void* dst, cudaStream_t s)
             ctx->err = "fmm_let_pack_data: run fmm_upward first";
             return FMM_ERR_STATE;
         }
-        k_let_pack_M<<<gw, 256, 0, s>>>(nc, ctx->ncoef, P_<uint32_t>(lp.eflag), P_<uint32_t>(lp.eidx),
-                                        P_<double>(ctx->M), (double*)p);
-        p += let_round16((size_t)lp.ncell * ctx->ncoef * 8);
+        if (ctx->prec == FMM_F32)
+            k_let_pack_M32<<<gw, 256, 0, s>>>(nc, ctx->ncoef, P_<uint32_t>(lp.eflag), P_<uint32_t>(lp.eidx),
+                                              P_<int32_t>(ctx->c_level), P_<double>(ctx->root), P_<double>(ctx->M),
+                                              (float*)p);
+        else
+            k_let_pack_M<<<gw, 256, 0, s>>>(nc, ctx->ncoef, P_<uint32_t>(lp.eflag), P_<uint32_t>(lp.eidx),
+                                            P_<double>(ctx->M), (double*)p);
+        p += let_round16((size_t)lp.ncell * ctx->ncoef * let_m_size(ctx->prec));
         if (ctx->prec == FMM_F32)
             k_let_pack_q<float, float4><<<gw, 256, 0, s>>>(nc, P_<float4>(ctx->body), P_<uint32_t>(ctx->c_bb),
                                                           P_<uint32_t>(lp.bflag), P_<uint32_t>(lp.boff), (float*)p);
@@ -434,17 +478,22 @@ fmm_status let_unpack(fmm_ctx* ctx, int first, int npeers, const void* const* sr
     FMM_TRY(buf_ensure(ctx, ctx->M, (size_t)ctot * ctx->ncoef * 8, true, s));
     for (int k = 0; k < npeers; ++k) {
         const LetRemote& r = ctx->let_remote[first + k];
-        const size_t need = sizeof(LetHeader) + let_round16((size_t)r.ncell * ctx->ncoef * 8) +
+        const size_t need = sizeof(LetHeader) + let_round16((size_t)r.ncell * ctx->ncoef * let_m_size(ctx->prec)) +
                             (size_t)r.nbody * (ctx->prec == FMM_F32 ? 4 : 8);
         if (!src[k] || bytes[k] < (int64_t)need) {
             ctx->err = "fmm_let_unpack: short buffer";
             return FMM_ERR_ARG;
         }
         const char* p = (const char*)src[k] + sizeof(LetHeader);
-        if (r.ncell)
+        if (r.ncell && ctx->prec == FMM_F32) {
+            k_let_unpack_M32<<<blocks_for(r.ncell * ctx->ncoef, 256), 256, 0, s>>>(
+                r.ncell, ctx->ncoef, (const float*)p, P_<int32_t>(ctx->c_level) + r.base, P_<double>(ctx->root),
+                P_<double>(ctx->M) + (size_t)r.base * ctx->ncoef);
+            FMM_LAUNCH(ctx);
+        } else if (r.ncell)
             FMM_CUDA_TRY(ctx, cudaMemcpyAsync(P_<double>(ctx->M) + (size_t)r.base * ctx->ncoef, p,
                                               (size_t)r.ncell * ctx->ncoef * 8, cudaMemcpyDeviceToDevice, s));
-        p += let_round16((size_t)r.ncell * ctx->ncoef * 8);
+        p += let_round16((size_t)r.ncell * ctx->ncoef * let_m_size(ctx->prec));
         if (r.nbody) {
             if (ctx->prec == FMM_F32)
                 k_let_unpack_q<float, float4><<<blocks_for(r.nbody, 256), 256, 0, s>>>(

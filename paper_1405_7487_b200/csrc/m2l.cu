@@ -11,6 +11,8 @@
 // This file holds the generic kernel (any P <= 16, Real = float or double): warp per
 // target cell over its CSR source range, D table and signed M in shared memory, lanes
 // over alpha, each pair's contribution accumulated into fp64 (R19).
+#include <climits>
+
 #include "common.cuh"
 
 namespace {
@@ -103,11 +105,54 @@ fmm_status m2l_generic(fmm_ctx* ctx, cudaStream_t s) {
     FMM_CUDA_TRY(ctx, cudaGetLastError());
     return FMM_OK;
 }
+__global__ void k_level_span(int64_t n, const int32_t* __restrict__ level, int* __restrict__ mm) {
+    int lo = INT_MAX, hi = INT_MIN;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        lo = min(lo, level[i]);
+        hi = max(hi, level[i]);
+    }
+    atomicMin(mm, lo);
+    atomicMax(mm + 1, hi);
+}
+
+// largest level difference between two cells that may meet in an M2L pair: the local tree spans
+// levels 0..depth; grafted LET cells carry levels rebased to this tree's root (let.cu), so with
+// remote cells the span is measured
+fmm_status level_span(fmm_ctx* ctx, cudaStream_t s, int* span) {
+    if (ctx->nrem == 0) {
+        *span = (int)ctx->depth;
+        return FMM_OK;
+    }
+    const int64_t nct = ctx->ncell + ctx->nrem;
+    FMM_TRY(buf_ensure(ctx, ctx->cnt_tmp, 64));
+    int* mm = P_<int>(ctx->cnt_tmp);
+    const int init[2] = {INT_MAX, INT_MIN};
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(mm, init, 8, cudaMemcpyHostToDevice, s));
+    k_level_span<<<(unsigned)std::min<int64_t>((nct + 255) / 256, 1024), 256, 0, s>>>(nct, P_<int32_t>(ctx->c_level), mm);
+    FMM_LAUNCH(ctx);
+    int h[2];
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(h, mm, 8, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    *span = h[1] - h[0];
+    return FMM_OK;
+}
 }  // namespace
 
 fmm_status m2l_pass(fmm_ctx* ctx, cudaStream_t s) {
     PhaseScope ps(ctx, PH_M2L, s);
     FMM_TRY(buf_ensure(ctx, ctx->L, (size_t)ctx->ncell * ctx->ncoef * 8));
+    // fp32 kernels scale operands by 2^(de n) with de = the pair's level difference, n <= P-1: in
+    // range for |de| <= 14 (P <= 10).  Trees spanning more levels (coincident clusters, extreme
+    // adaptivity) take the fp64 generic kernel, exact in range at any level difference.
+    int span = 0;
+    if (ctx->prec == FMM_F32 && ctx->m2l_part != 2) FMM_TRY(level_span(ctx, s, &span));
+    if (ctx->prec == FMM_F32 && ctx->m2l_part != 2) ctx->m2l_deep = span > 14;
+    if (ctx->prec == FMM_F32 && ctx->m2l_deep) {
+        if (ctx->m2l_part == 1) return FMM_OK;
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->L.p, 0, (size_t)ctx->ncell * ctx->ncoef * 8, s));
+        PhaseScope pk(ctx, PH_M2L_KERNEL, s);
+        return m2l_generic<double>(ctx, s);
+    }
     if (ctx->use_fast_m2l && m2l_fast_available(ctx->P, ctx->prec)) return m2l_fast(ctx, s);
     if (ctx->m2l_part == 1) return FMM_OK;   // the generic kernel has no operand preparation
     // cells without M2L sources still need L = 0 (the generic kernel skips them)

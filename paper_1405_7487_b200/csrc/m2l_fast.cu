@@ -686,8 +686,9 @@ __global__ void __launch_bounds__(128, 2)
             if (p + 32 < p1) fetch_cb(bnext);   // after the recurrence: bnext has landed
             // (rho_B/rho_A)^n: only in warps where some lane needs it (uniform trees: never)
             const bool need = __any_sync(__activemask(), de != 0);
-            // 2^(de*n) from exponent bits, saturated like exp2f (0 / inf) when |de*n| leaves the range
-            auto pw = [&](int n) { return __int_as_float(min(max(127 + de * n, 0), 255) << 23); };
+            // 2^(de*n) from exponent bits: |de| <= 14 is guaranteed by m2l_pass, which routes trees
+            // spanning more than 14 levels to the fp64 kernel (|de * n| <= 126 for n <= 9)
+            auto pw = [&](int n) { return __int_as_float((127 + de * n) << 23); };
             const float4* sv = Sv + (size_t)b * NCH;
             sfor<0, NCH>([&](auto cc) {
                 constexpr int C = decltype(cc)::value;
