@@ -12,17 +12,27 @@
 // target cell over its CSR source range, D table and signed M in shared memory, lanes
 // over alpha, each pair's contribution accumulated into fp64 (R19).
 #include <climits>
+#include <type_traits>
 
 #include "common.cuh"
 
 namespace {
 constexpr int ML_WARPS = 2;
 
+// Real = float: every pair is evaluated in the target's power-of-two units (rho_A = 2^(E - level),
+// 2^E >= 2 h): u = d / rho_A, M_beta / rho_A^|beta|, and L_alpha = Lhat_alpha / rho_A^(|alpha|+1) --
+// exact rescalings that keep D up to order 2P-2 and the multipoles inside the fp32 range at any P
+// and any level (DESIGN.md §2 reading 5); Real = double evaluates R14 as written.
 template <typename Real>
 __global__ void __launch_bounds__(ML_WARPS * 32) k_m2l_generic(int64_t ncell, const uint32_t* __restrict__ src,
                                                                 const uint64_t* __restrict__ off,
                                                                 const double4* __restrict__ cr, int P, int ncoef,
-                                                                const double* __restrict__ M, double* __restrict__ L) {
+                                                                const double* __restrict__ M, double* __restrict__ L,
+                                                                const int32_t* __restrict__ level,
+                                                                const double* __restrict__ root) {
+    constexpr bool kScaled = std::is_same<Real, float>::value;
+    int E = 0;
+    if (kScaled) frexp(2.0 * root[10], &E);
     // dynamic shared memory: ex[ncoef] | per warp: L (double) [ncoef], D [ncoef], M [ncoef]
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -38,17 +48,18 @@ __global__ void __launch_bounds__(ML_WARPS * 32) k_m2l_generic(int64_t ncell, co
         uint64_t p0 = off[a], p1 = off[a + 1];
         if (p0 == p1) continue;
         double4 ca = cr[a];
+        const int ea = kScaled ? E - level[a] : 0;
         for (int k = lane; k < ncoef; k += 32) sLw[k] = 0.0;
         for (uint64_t p = p0; p < p1; ++p) {
             uint32_t b = src[p];
             double4 cb = cr[b];
-            Real d[3] = {(Real)(ca.x - cb.x), (Real)(ca.y - cb.y), (Real)(ca.z - cb.z)};
+            Real d[3] = {(Real)ldexp(ca.x - cb.x, -ea), (Real)ldexp(ca.y - cb.y, -ea), (Real)ldexp(ca.z - cb.z, -ea)};
             Real r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
             Real inv_r2 = Real(1) / r2;
             __syncwarp();
             if (lane == 0) sDw[0] = Real(1) / sqrt(r2);
             for (int k = lane; k < ncoef; k += 32) {
-                Real m = (Real)M[(int64_t)b * ncoef + k];
+                Real m = (Real)ldexp(M[(int64_t)b * ncoef + k], -ea * (int)ex[k].w);
                 sMw[k] = (ex[k].w & 1) ? -m : m;
             }
             __syncwarp();
@@ -87,7 +98,7 @@ __global__ void __launch_bounds__(ML_WARPS * 32) k_m2l_generic(int64_t ncell, co
             }
         }
         __syncwarp();
-        for (int k = lane; k < ncoef; k += 32) L[a * ncoef + k] = sLw[k];
+        for (int k = lane; k < ncoef; k += 32) L[a * ncoef + k] = ldexp(sLw[k], -ea * ((int)ex[k].w + 1));
         __syncwarp();
     }
 }
@@ -100,7 +111,8 @@ fmm_status m2l_generic(fmm_ctx* ctx, cudaStream_t s) {
     k_m2l_generic<Real><<<std::max(g, 1), ML_WARPS * 32, smem, s>>>(ctx->ncell, P_<uint32_t>(ctx->m2l_src),
                                                                   P_<uint64_t>(ctx->m2l_off), P_<double4>(ctx->c_cr),
                                                                   ctx->P, ctx->ncoef, P_<double>(ctx->M),
-                                                                  P_<double>(ctx->L));
+                                                                  P_<double>(ctx->L), P_<int32_t>(ctx->c_level),
+                                                                  P_<double>(ctx->root));
     FMM_LAUNCH(ctx);
     FMM_CUDA_TRY(ctx, cudaGetLastError());
     return FMM_OK;
