@@ -42,6 +42,7 @@ struct Problem {
     cublasHandle_t h = nullptr;
 };
 Problem g_pb;
+bool g_grouped = true;   // the last run used grouped calls
 
 __host__ __device__ int cidx(int a, int b, int c) {
     int n = a + b + c, m = b + c;
@@ -237,10 +238,20 @@ int m2ltc_run(int mode, int reps, float* ms) {
             }
         }
     }
+    // pointer arrays of the grouped calls live in device memory
+    std::vector<void**> dA(nv), dB(nv), dC(nv);
+    for (int i = 0; i < nv; ++i) {
+        const size_t ng = A[i].size();
+        cudaMalloc(&dA[i], ng * 8); cudaMalloc(&dB[i], ng * 8); cudaMalloc(&dC[i], ng * 8);
+        cudaMemcpy(dA[i], A[i].data(), ng * 8, cudaMemcpyHostToDevice);
+        cudaMemcpy(dB[i], B[i].data(), ng * 8, cudaMemcpyHostToDevice);
+        cudaMemcpy(dC[i], C[i].data(), ng * 8, cudaMemcpyHostToDevice);
+    }
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     float total = 0.f;
+    bool grouped = true;
     for (int r = 0; r < reps + 1; ++r) {
         cudaMemset(pb.Lp, 0, 8 * NPAD * nco * 4);
         cudaEventRecord(e0);
@@ -249,12 +260,24 @@ int m2ltc_run(int mode, int reps, float* ms) {
             std::vector<cublasOperation_t> tn(ng, CUBLAS_OP_N);
             std::vector<int> nn(ng, (int)ncol), ld(ng, nco), one(ng, 1);
             std::vector<float> al(ng, 1.0f), be(ng, 1.0f);
-            const cublasStatus_t st = cublasGemmGroupedBatchedEx(
-                pb.h, tn.data(), tn.data(), m[i].data(), nn.data(), k[i].data(), al.data(), A[i].data(), CUDA_R_32F,
-                ld.data(), B[i].data(), CUDA_R_32F, ld.data(), be.data(), C[i].data(), CUDA_R_32F, ld.data(), ng,
-                one.data(), ct);
+            cublasStatus_t st = CUBLAS_STATUS_NOT_SUPPORTED;
+            if (grouped)
+                st = cublasGemmGroupedBatchedEx(pb.h, tn.data(), tn.data(), m[i].data(), nn.data(), k[i].data(),
+                                                al.data(), (const void* const*)dA[i], CUDA_R_32F, ld.data(),
+                                                (const void* const*)dB[i], CUDA_R_32F, ld.data(), be.data(),
+                                                (void* const*)dC[i], CUDA_R_32F, ld.data(), ng, one.data(), ct);
+            if (st == CUBLAS_STATUS_NOT_SUPPORTED) {   // e.g. emulated FP32: one GEMM per (p, degree)
+                grouped = false;
+                const float one_f = 1.0f;
+                for (int g = 0; g < ng; ++g) {
+                    st = cublasGemmEx(pb.h, CUBLAS_OP_N, CUBLAS_OP_N, m[i][g], (int)ncol, k[i][g], &one_f, A[i][g],
+                                      CUDA_R_32F, nco, B[i][g], CUDA_R_32F, nco, &one_f, C[i][g], CUDA_R_32F, nco, ct,
+                                      CUBLAS_GEMM_DEFAULT);
+                    if (st != CUBLAS_STATUS_SUCCESS) break;
+                }
+            }
             if (st != CUBLAS_STATUS_SUCCESS) {
-                fprintf(stderr, "cublasGemmGroupedBatchedEx failed: %d\n", (int)st);
+                fprintf(stderr, "cuBLAS GEMM failed: %d (mode %d)\n", (int)st, mode);
                 return 10 + (int)st;
             }
         }
@@ -264,6 +287,10 @@ int m2ltc_run(int mode, int reps, float* ms) {
         cudaEventElapsedTime(&t, e0, e1);
         if (r > 0) total += t;   // the first run is a warm-up
     }
+    for (int i = 0; i < nv; ++i) {
+        cudaFree(dA[i]); cudaFree(dB[i]); cudaFree(dC[i]);
+    }
+    g_grouped = grouped;
     *ms = total / reps;
     // back to Morton order, unscaled
     std::vector<int> deg(nco);
@@ -276,6 +303,8 @@ int m2ltc_run(int mode, int reps, float* ms) {
     cudaFree(ddeg);
     return cudaDeviceSynchronize() == cudaSuccess ? 0 : 5;
 }
+
+int m2ltc_grouped() { return g_grouped ? 1 : 0; }
 
 // fp64 M or L rows of the given Morton cell ids into out [n][ncoef]
 int m2ltc_rows(int which, int n, const int64_t* ids, double* out) {
