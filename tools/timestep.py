@@ -1,21 +1,21 @@
 """Multi-step use of the distributed FMM: a leapfrog N-body integration where every
 step re-partitions with the previous step's Eq. (1) weights and Eq. (1)'s alpha is optimised over
-the steps by measured runtime (AlphaTuner).  Gravity with G = 1: masses are the charges, the
-acceleration is +grad(phi) of phi = sum m_j / r (the library's sign), and the energy
+the steps by measured runtime (fmm_dist_tune_alpha).  Gravity with G = 1: masses are the charges,
+the acceleration is +grad(phi) of phi = sum m_j / r (the library's sign), and the energy
 E = sum m v^2 / 2 - sum m phi / 2 is printed so the drift can be checked.
 
-    python tools/timestep.py [K ranks (LoopbackComm on one GPU)] [N] [steps]
+    python tools/timestep.py [K ranks (an in-process group on one GPU)] [N] [steps]
 """
 import os
 import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
-import torch
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
 
-import synth
-from paper_1405_7487_b200.dist import DistFMM, LoopbackComm
+import synth  # noqa: E402
+from paper_1405_7487_b200.dist import DistFMM, LocalGroup, run_ranks  # noqa: E402
 
 
 def main():
@@ -28,9 +28,11 @@ def main():
     vel = rng.normal(scale=0.3, size=(n, 3))          # a warm start; any velocities do
     vel -= vel.mean(0)
     cuts = np.linspace(0, n, K + 1).astype(int)
-    gb = [int(c) for c in cuts[:-1]]
-    D = DistFMM(LoopbackComm(K), n, 6, 0.5, 32, "f64")
-    tuner = D.enable_alpha_tuning(lo=0.25, hi=4.0, tol=0.3)
+    G = LocalGroup(K)
+    D = [DistFMM(n, 6, 0.5, 32, "f64", 0, K, r, group=G) for r in range(K)]
+    for f in D:
+        f.tune_alpha(0.25, 4.0, 0.3)
+    streams = [torch.cuda.Stream() for _ in range(K)]
     dt = 1e-3
 
     def forces(p):
@@ -38,7 +40,8 @@ def main():
         M_in = [torch.from_numpy(np.ascontiguousarray(m[cuts[r]:cuts[r + 1]])).cuda() for r in range(K)]
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        out = D.solve(P_in, M_in, gb, reuse_weights=True)
+        out = run_ranks(lambda r: D[r].solve(P_in[r], M_in[r], int(cuts[r]), reuse_weights=True,
+                                             stream=streams[r]), K)
         torch.cuda.synchronize()
         t = time.perf_counter() - t0
         phi = np.concatenate([o[0].cpu().numpy() for o in out])
@@ -53,11 +56,14 @@ def main():
         phi, acc, t = forces(pos)
         vel += 0.5 * dt * acc
         e = 0.5 * np.sum(m * np.sum(vel ** 2, 1)) - 0.5 * np.sum(m * phi)
-        print(f"step {k:3d}  {1e3 * t:7.2f} ms  alpha {D.alpha:6.3f}  work l/r {D.stats['work_local']:.3e}/"
-              f"{D.stats['work_remote']:.3e}  dE/E {abs(e - e0) / abs(e0):.2e}", flush=True)
-    print("alpha probes (alpha, runtime s):", [(round(a, 3), round(t, 4)) for a, t in tuner.history],
-          "best", round(tuner.best, 3))
-    D.close()
+        st = D[0].stats()
+        print(f"step {k:3d}  {1e3 * t:7.2f} ms  alpha {st['alpha']:6.3f}  work l/r {st['work_local']:.3e}/"
+              f"{st['work_remote']:.3e}  dE/E {abs(e - e0) / abs(e0):.2e}", flush=True)
+    st = D[0].stats()
+    print("alpha probes", st["tuner_probes"], "best", round(st["tuner_best"], 3), "converged", st["tuner_converged"])
+    for f in D:
+        f.close()
+    G.close()
 
 
 if __name__ == "__main__":
