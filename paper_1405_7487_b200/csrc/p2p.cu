@@ -459,6 +459,11 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_tma(const float4* __restrict
     __shared__ __align__(8) uint64_t full[NS], empty[NS];
     __shared__ unsigned long long s_leaf;
     __shared__ uint32_t s_self;
+    // the leaf's source runs, loaded coalesced once per leaf: the issuing thread walks them from
+    // shared memory instead of with dependent global loads (ncu: warp 0 -- the producer -- was the
+    // straggler every other warp waited for at the chunk barriers)
+    constexpr int RUN_CAP = 256;
+    __shared__ uint2 s_runs[RUN_CAP];
     const int tid = threadIdx.x, lane = tid & 31;
     if (tid == 0) {
         for (int i = 0; i < NS; ++i) {
@@ -478,13 +483,16 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_tma(const float4* __restrict
         const uint32_t a = leaf_ids[li];
         const uint32_t tb = bb[a], nt_all = bc[a];
         const uint32_t r0 = roff[a], r1 = roff[a + 1], ns = rtot[a];
+        const bool runs_in_smem = r1 - r0 <= (uint32_t)RUN_CAP;
         for (uint32_t r = r0 + tid; r < r1; r += PC_THREADS) {
             const uint2 ru = runs[r];
             const uint32_t end = (r + 1 < r1) ? runs[r + 1].y : ns;
             if (ru.x <= tb && tb < ru.x + (end - ru.y)) s_self = ru.y + (tb - ru.x);
+            if (runs_in_smem) s_runs[r - r0] = ru;
         }
         __syncthreads();
         const uint32_t selfF = s_self;
+        const uint2* lruns = runs_in_smem ? s_runs - r0 : runs;   // indexed by the global run number
         for (uint32_t t0 = 0; t0 < nt_all; t0 += PC_THREADS * (2 * NP)) {
             const uint32_t nt = min(nt_all - t0, (uint32_t)(PC_THREADS * (2 * NP)));
             const int lpg = (int)((nt + (2 * NP) - 1) / (2 * NP));
@@ -517,9 +525,9 @@ __global__ void __launch_bounds__(PC_THREADS) k_p2p_tma(const float4* __restrict
                 mbar_expect_tx(&full[buf], len * 16u);
                 uint32_t fl = f0, dst = 0;
                 while (dst < len) {
-                    while (cur + 1 < r1 && runs[cur + 1].y <= fl) ++cur;
-                    const uint2 ru = runs[cur];
-                    const uint32_t end = (cur + 1 < r1) ? runs[cur + 1].y : ns;
+                    while (cur + 1 < r1 && lruns[cur + 1].y <= fl) ++cur;
+                    const uint2 ru = lruns[cur];
+                    const uint32_t end = (cur + 1 < r1) ? lruns[cur + 1].y : ns;
                     const uint32_t m = min(end - fl, len - dst);
                     bulk_g2s(&s_tile[buf][dst], body + ru.x + (fl - ru.y), m * 16u, &full[buf]);
                     fl += m;
