@@ -108,4 +108,6 @@ CONFIGS = {
     "c4w": dict(kind="cube", n=1 << 24, P=10, theta=0.4, ncrit=64, prec="f32", seed=4),
     # Table I case 2: sphere surface, P=10, theta=0.4, ncrit=512
     "sph": dict(kind="sphere", n=1 << 22, P=10, theta=0.4, ncrit=512, prec="f32", seed=5),
+    # configs[4] P2P microbench leaf sizes at a smaller N (ncrit 32: mean leaf 8), for A/B runs
+    "c5n32": dict(kind="cube", n=1 << 22, P=4, theta=0.4, ncrit=32, prec="f32", seed=4),
 }
