@@ -26,17 +26,20 @@
 // accumulate their pairs (same target) in Real, then the warp reduces in fp64 and stores
 // the reduced L_hat (no atomics).  Targets are handed to warps through an atomic counter.
 #include <type_traits>
+#include <utility>
 
 #include "common.cuh"
 
 namespace {
 
+// compile-time loop B..E-1 in order (a fold over an index sequence: no recursion-depth limit)
+template <int B, typename F, int... I>
+__device__ __forceinline__ void sfor_seq(F&& f, std::integer_sequence<int, I...>) {
+    (f(std::integral_constant<int, B + I>{}), ...);
+}
 template <int B, int E, typename F>
 __device__ __forceinline__ void sfor(F&& f) {
-    if constexpr (B < E) {
-        f(std::integral_constant<int, B>{});
-        sfor<B + 1, E>(f);
-    }
+    if constexpr (B < E) sfor_seq<B>(f, std::make_integer_sequence<int, E - B>{});
 }
 
 __host__ __device__ constexpr int t2(int y, int z) { return (y + z) * (y + z + 1) / 2 + z; }
@@ -872,6 +875,8 @@ fmm_status m2l_fast(fmm_ctx* ctx, cudaStream_t s) {
                 case 6: return m2l_mir_t<6>(ctx, s);
                 case 8: return m2l_mir_t<8>(ctx, s);
                 case 10: return m2l_mir_t<10>(ctx, s);
+                case 12: return m2l_mir_t<12>(ctx, s);
+                case 16: return m2l_mir_t<16>(ctx, s);
                 default: break;
             }
         }
@@ -880,6 +885,8 @@ fmm_status m2l_fast(fmm_ctx* ctx, cudaStream_t s) {
             case 6: return m2l_fast_t<6, float>(ctx, s);
             case 8: return m2l_fast_t<8, float>(ctx, s);
             case 10: return m2l_fast_t<10, float>(ctx, s);
+            case 12: return m2l_mir_t<12>(ctx, s);   // no scalar P = 12, 16 kernels
+            case 16: return m2l_mir_t<16>(ctx, s);
             default: break;
         }
     } else {
@@ -893,5 +900,5 @@ fmm_status m2l_fast(fmm_ctx* ctx, cudaStream_t s) {
 }
 
 bool m2l_fast_available(int P, int prec) {
-    return prec == FMM_F32 ? (P == 4 || P == 6 || P == 8 || P == 10) : (P == 4 || P == 6);
+    return prec == FMM_F32 ? (P == 4 || P == 6 || P == 8 || P == 10 || P == 12 || P == 16) : (P == 4 || P == 6);
 }

@@ -64,6 +64,8 @@ CASES = [
     ("cube", 1000, 1, 0.3, 8, "f64"),        # P = 1: monopole only, no far gradient
     ("cube", 1000, 2, 0.7, 1, "f64"),        # ncrit = 1
     ("cube", 700, 16, 0.5, 32, "f64"),       # maximum P
+    ("plummer", 3000, 12, 0.5, 32, "f32"),   # fp32 register M2L past P = 10 (configs[4] P sweep)
+    ("cube", 2500, 16, 0.5, 32, "f32"),
     ("plummer", 64, 3, 0.5, 64, "f32"),      # single leaf = direct sum
     ("cube", 7, 4, 0.5, 2, "f64"),
     ("sphere", 30000, 10, 0.4, 512, "f32"),  # Table I case 2 parameters (ncrit 512 leaves)

@@ -7,8 +7,8 @@
        parent's neighbours that are not adjacent: <= 189 sources per cell, 383,233,032 pairs with
        an open boundary), multipoles random with |M_beta| ~ w^|beta| / beta! in cell-width units
        (w = 1/128), fp32 arithmetic, P in {4, 8, 12, 16} -- fed to the product M2L kernels through
-       fmm_debug_m2l (P <= 10: the register kernel k_m2l_mir<P>; P = 12, 16: the scaled generic
-       kernel).  Checked on sampled targets against per-pair oracle.m2l sums (R14).
+       fmm_debug_m2l (the register kernel k_m2l_mir<P>; at P = 12 and 16 its D and L tables exceed the
+       register file and spill to local memory).  Checked on sampled targets against per-pair oracle.m2l sums (R14).
 
 Kernel times are the CUDA events libfmm records around each kernel on its stream, averaged over
 `--reps` launches after a warm-up.  python tools/microbench.py [--only p2p|m2l] [--reps R] [--P 4,8]
@@ -180,7 +180,7 @@ def main():
             npairs, ms, err = run_m2l_uniform(P, a.reps)
             h = m2l_flops_per_pair(P)
             pps = npairs / (ms * 1e-3)
-            kern = f"k_m2l_mir<{P}>" if P in (4, 6, 8, 10) else "k_m2l_generic<float> (scaled)"
+            kern = f"k_m2l_mir<{P}>" if P in (4, 6, 8, 10, 12, 16) else "k_m2l_generic<float> (scaled)"
             print(json.dumps({"micro": "m2l", "grid": "uniform level 7, 2^21 cells, classic list", "kernel": kern,
                               "P": P, "pairs": npairs, "pairs_per_cell": npairs / G ** 3, "ms": round(ms, 4),
                               "pairs_per_s": pps, "harmonic_flops_per_pair": h["flops"],
