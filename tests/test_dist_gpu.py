@@ -376,3 +376,24 @@ def test_dist_timeline_overlap(torch_cuda):
         assert tl["let_data_exchange"][1] >= tl["upward"][1] - 1e-3, tl
         assert tl["stay_sort"][0] <= tl["particle_exchange"][1] + 1e-3, tl
     D.close()
+
+
+def test_nccl_transport_single_rank(torch_cuda):
+    """The NCCL transport (libnccl dlopen'ed by the library, communicator from a unique id) with one
+    rank: fmm_dist_solve returns the single-GPU result bit for bit, twice (the second step with the
+    Eq. (1) weights of the first)."""
+    torch = torch_cuda
+    from paper_1405_7487_b200 import FMM
+    from paper_1405_7487_b200.dist import DistFMM, nccl_unique_id
+    pos, q = synth.generate("plummer", 20000, 13, np.float32)
+    tp, tq = torch.from_numpy(pos).cuda(), torch.from_numpy(q).cuda()
+    D = DistFMM(20000, 10, 0.4, 64, "f32", 0, 1, 0, unique_id=nccl_unique_id())
+    f = FMM(20000, 10, 0.4, 64, "f32")
+    p1, g1 = f.solve(tp, tq)
+    for reuse in (False, True):
+        p, g = D.solve(tp, tq, 0, reuse_weights=reuse)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(p.cpu().numpy(), p1.cpu().numpy())
+        np.testing.assert_array_equal(g.cpu().numpy(), g1.cpu().numpy())
+    assert D.stats()["n_local"] == 20000 and D.stats()["npeers"] == 0
+    D.close()
