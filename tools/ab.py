@@ -29,11 +29,6 @@ for setting in sys.argv[3:]:
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     f = FMM(cfg["n"], cfg["P"], cfg["theta"], cfg["ncrit"], cfg["prec"])
-    for k, v in old.items():
-        if v is None:
-            del os.environ[k]
-        else:
-            os.environ[k] = v
     for _ in range(3):
         phi, grad = f.solve(tp, tq)
     torch.cuda.synchronize()
@@ -54,6 +49,11 @@ for setting in sys.argv[3:]:
     if ref is None:
         ref = out
     rel = float(np.linalg.norm(out - ref) / np.linalg.norm(ref))
+    for k, v in old.items():   # the setting stays in the environment while its context runs
+        if v is None:
+            del os.environ[k]
+        else:
+            os.environ[k] = v
     print(json.dumps({"setting": setting, "ms_step": round(ms / reps, 4),
                       "phases": {k: round(v / reps, 4) for k, v in ph.items() if v > 0},
                       "phi_rel_vs_first": rel}), flush=True)
