@@ -109,6 +109,13 @@ struct fmm_ctx {
     DevBuf mut_mir, mut_w, mut_so, mut_slot;
     int m2l_variant = 0;        // fp32 register M2L: 0 mirror-paired f32x2, 1 scalar (FMM_M2L_VARIANT)
     int p2p_np = 2;             // CTA P2P: target pairs per thread (FMM_P2P_NP = 1, 2, 4)        // 0: CTA per leaf over source runs, 1: warp per leaf (FMM_P2P_VARIANT)
+    // split multi-GPU interactions (dist.cu): operand layout capacity, first cell to prepare, skip
+    // the reduced -> full L expansion, and the remote lists' offsets for the expansion's "no list"
+    int64_t m2l_cap = 0, m2l_prep_c0 = 0;
+    bool m2l_no_expand = false;
+    bool m2l_span_fixed = false;   // m2l_pass keeps m2l_deep as set by the caller (no span reduction)
+    const uint64_t* m2l_off2 = nullptr;
+    int* m2l_sexp = nullptr;     // per-cell scale exponents of the last register-kernel operand preparation
     bool m2l_deep = false;       // m2l_pass: tree spans > 14 levels, fp32 mode uses the fp64 kernel
     int m2l_part = 0;            // m2l_pass: 0 all, 1 operand preparation only, 2 without it (fmm_solve split)
     int list_sort = 0;           // list grouping: 0 counting scatter + per-segment sorts, 1 one radix sort of the packed pairs (FMM_LIST_SORT)
@@ -339,6 +346,7 @@ fmm_status upward_pass(fmm_ctx* ctx, cudaStream_t s);
 fmm_status m2l_pass(fmm_ctx* ctx, cudaStream_t s);
 fmm_status m2l_fast(fmm_ctx* ctx, cudaStream_t s);
 bool m2l_fast_available(int P, int prec);
+fmm_status m2l_expand(fmm_ctx* ctx, const uint64_t* off2, cudaStream_t s);
 fmm_status p2p_pass(fmm_ctx* ctx, cudaStream_t s);
 fmm_status downward_pass(fmm_ctx* ctx, void* phi, void* grad, cudaStream_t s);
 // L2L + L2P writing the far field to ctx->far (sorted order); merge_nearfar adds P2P and un-permutes

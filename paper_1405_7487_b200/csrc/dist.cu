@@ -24,6 +24,7 @@
 //   6. lists, unpack, M2L/P2P/L2L/L2P; Eq. (1) weights of this step (fmm_work);
 //   7. phi, grad and the weights back to the particles' owners, in the caller's order.
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 
@@ -244,10 +245,11 @@ struct fmm_group {
 
 // ------------------------------------------------------------------------------- the driver
 enum { TL_PARTITION, TL_EXCHANGE, TL_STAY_SORT, TL_TREE, TL_UPWARD, TL_COVER, TL_STRUCT_XCHG, TL_LOCAL_DTT,
-       TL_DATA_XCHG, TL_REMOTE_DTT, TL_LISTS, TL_INTERACT, TL_BACK, TL_COUNT };
+       TL_DATA_XCHG, TL_REMOTE_DTT, TL_LISTS, TL_INTERACT, TL_BACK, TL_INTERACT_LOCAL, TL_INTERACT_REMOTE, TL_COUNT };
 static const char* kTlNames[TL_COUNT] = {"partition", "particle_exchange", "stay_sort", "tree", "upward",
                                          "cover_plan", "let_struct_exchange", "local_dtt", "let_data_exchange",
-                                         "remote_dtt", "lists", "interact", "results_back"};
+                                         "remote_dtt", "lists", "interact", "results_back", "interact_local",
+                                         "interact_remote"};
 
 struct DistState {
     Transport* tr = nullptr;
@@ -255,8 +257,17 @@ struct DistState {
     double alpha = 1.0, c_m2l = 0.0;
     fmm_alpha_tuner* tuner = nullptr;
     bool overlap_sort = true;   // f1: staying particles sorted while the particles fly (FMM_DIST_SORT=0: off)
+    // local M2L/P2P started on the compute stream right after the local traversal, while the LET
+    // fragments are grafted and traversed; the remote lists' interactions added after (FMM_DIST_SPLIT=0: off)
+    bool split = true;
+    cudaStream_t cx = nullptr;
+    int64_t nct_cap = 0;
+    // remote-only CSR lists, their P2P source runs, and the second outputs of the remote pass
+    DevBuf r_moff, r_msrc, r_poff, r_psrc, r_runs, r_run_off, r_run_tmp, r_leaf_cls, Lr2, L2, near2_phi, near2_grad,
+        inter_loc, span_tmp;
+    int64_t r_nm = 0, r_np = 0, r_nruns = 0, r_ncls[3] = {0, 0, 0};
     cudaStream_t cs = nullptr, side = nullptr;
-    cudaEvent_t ev[8] = {};
+    cudaEvent_t ev[12] = {};
     std::vector<cudaEvent_t> ev_round;
     // timeline (ctx->timing): start/end events per span, relative to ev_t0
     cudaEvent_t ev_t0 = nullptr;
@@ -277,6 +288,10 @@ struct DistState {
         delete tuner;
         if (cs) cudaStreamDestroy(cs);
         if (side) cudaStreamDestroy(side);
+        if (cx) cudaStreamDestroy(cx);
+        DevBuf* rb[] = {&r_moff, &r_msrc, &r_poff, &r_psrc, &r_runs, &r_run_off, &r_run_tmp, &r_leaf_cls, &Lr2, &L2,
+                        &near2_phi, &near2_grad, &inter_loc, &span_tmp};
+        for (DevBuf* x : rb) buf_free(*x);
         for (auto e : ev)
             if (e) cudaEventDestroy(e);
         for (auto e : ev_round) cudaEventDestroy(e);
@@ -383,6 +398,60 @@ __global__ void k_merge_runs(const uint64_t* __restrict__ ka, const uint32_t* __
         ko[i + lo] = k;
         io[i + lo] = x;
     }
+}
+
+// ---- split interactions (local lists first, remote lists after): buffer swaps and merges
+void swap_m2l_csr(fmm_ctx* ctx, DistState* D) {
+    std::swap(ctx->m2l_off, D->r_moff);
+    std::swap(ctx->m2l_src, D->r_msrc);
+    std::swap(ctx->n_m2l, D->r_nm);
+}
+void swap_p2p_csr(fmm_ctx* ctx, DistState* D) {
+    std::swap(ctx->p2p_off, D->r_poff);
+    std::swap(ctx->p2p_src, D->r_psrc);
+    std::swap(ctx->n_p2p, D->r_np);
+}
+void swap_runs(fmm_ctx* ctx, DistState* D) {
+    std::swap(ctx->runs, D->r_runs);
+    std::swap(ctx->run_off, D->r_run_off);
+    std::swap(ctx->run_tmp, D->r_run_tmp);
+    std::swap(ctx->leaf_cls, D->r_leaf_cls);
+    std::swap(ctx->n_runs, D->r_nruns);
+    for (int k = 0; k < 3; ++k) std::swap(ctx->n_leaf_cls[k], D->r_ncls[k]);
+}
+
+// reduced L_hat: local + remote (each pass wrote only the targets that have a list of its kind)
+__global__ void k_merge_lr(int64_t nc, int NL, const uint64_t* __restrict__ offl, const uint64_t* __restrict__ offr,
+                           double* __restrict__ Lr, const double* __restrict__ Lr2) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nc * NL; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = t / NL;
+        if (offr[c] == offr[c + 1]) continue;
+        Lr[t] = (offl[c] < offl[c + 1] ? Lr[t] : 0.0) + Lr2[t];
+    }
+}
+__global__ void k_add_f64(int64_t n, double* __restrict__ a, const double* __restrict__ b) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] += b[i];
+}
+template <typename Real>
+__global__ void k_add_near(int64_t n, Real* __restrict__ phi, const Real* __restrict__ phi2, Real* __restrict__ grad,
+                           const Real* __restrict__ grad2) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        phi[i] += phi2[i];
+        grad[3 * i] += grad2[3 * i];
+        grad[3 * i + 1] += grad2[3 * i + 1];
+        grad[3 * i + 2] += grad2[3 * i + 2];
+    }
+}
+__global__ void k_add_u64(unsigned long long* a, const unsigned long long* b) { *a += *b; }
+__global__ void k_level_minmax(int64_t n, const int32_t* __restrict__ level, int* __restrict__ mm) {
+    int lo = 1 << 30, hi = -(1 << 30);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        lo = min(lo, level[i]);
+        hi = max(hi, level[i]);
+    }
+    atomicMin(mm, lo);
+    atomicMax(mm + 1, hi);
 }
 
 struct Step {
@@ -592,13 +661,21 @@ static fmm_status dist_step(fmm_ctx* ctx, DistState* D, const void* pos, const v
     ctx->presorted = false;
     FMM_TRY(bst);
     S.tl_end(TL_TREE, m);
-    // ---- upward pass on the aux stream (P2M/M2M need the tree and q only)
-    FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[4], m));
-    FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(aux, D->ev[4], 0));
-    S.tl_begin(TL_UPWARD, aux);
-    FMM_TRY(fmm_upward(ctx, D->l_pos.p, D->l_q.p, aux));
-    S.tl_end(TL_UPWARD, aux);
-    FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[5], aux));   // upward done
+    // ---- upward pass on the aux stream (P2M/M2M need the tree and q only).  The split flow
+    // launches it after the LET capacity is reserved (a reservation may move M and the bodies)
+    // (a rank left without particles takes the unsplit flow: it has no lists; the collective calls
+    // of both flows are the same)
+    const bool split = D->split && K > 1 && nl > 0;
+    auto launch_upward = [&]() -> fmm_status {
+        FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[4], m));
+        FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(aux, D->ev[4], 0));
+        S.tl_begin(TL_UPWARD, aux);
+        FMM_TRY(fmm_upward(ctx, D->l_pos.p, D->l_q.p, aux));
+        S.tl_end(TL_UPWARD, aux);
+        FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[5], aux));   // upward done
+        return FMM_OK;
+    };
+    if (!split) FMM_TRY(launch_upward());
     // ---- 5. covers, plans, LET structure
     S.tl_begin(TL_COVER, m);
     const int CW = 1 + 8 * FMM_LET_MAX_COVER;
@@ -645,6 +722,28 @@ static fmm_status dist_step(fmm_ctx* ctx, DistState* D, const void* pos, const v
     }
     FMM_TRY(buf_ensure(ctx, D->let_recv, (size_t)std::max<int64_t>(ro[K], 256)));
     char* lrecv = (char*)D->let_recv.p;
+    if (split) {
+        // capacity for every incoming fragment now, so grafting never moves an array the local
+        // interactions (compute stream) or the upward pass (aux) are reading: a structure message of
+        // b bytes holds at most (b - 64) / 64 cells and (b - 64) / body-size bodies
+        const int64_t bsz = ctx->prec == FMM_F32 ? 16 : 32;
+        int64_t addc = 0, addb = 0;
+        for (int j = 0; j < K; ++j)
+            if (j != me && rsb[j] > 64) {
+                addc += (rsb[j] - 64) / 64;
+                addb += (rsb[j] - 64) / bsz;
+            }
+        const int64_t ctot = ctx->ncell + addc, btot = nl + addb;
+        DevBuf* u32s[] = {&ctx->c_cb, &ctx->c_cc, &ctx->c_bb, &ctx->c_bc, &ctx->c_level, &ctx->c_parent};
+        for (DevBuf* b : u32s) FMM_TRY(buf_ensure(ctx, *b, (size_t)std::max<int64_t>(ctot, 1) * 4, true, m));
+        FMM_TRY(buf_ensure(ctx, ctx->c_key, (size_t)std::max<int64_t>(ctot, 1) * 8, true, m));
+        FMM_TRY(buf_ensure(ctx, ctx->c_cr, (size_t)std::max<int64_t>(ctot, 1) * 32, true, m));
+        FMM_TRY(buf_ensure(ctx, ctx->c_orig, (size_t)std::max<int64_t>(ctot, 1) * 4, true, m));
+        FMM_TRY(buf_ensure(ctx, ctx->body, (size_t)std::max<int64_t>(btot, 1) * bsz, true, m));
+        FMM_TRY(buf_ensure(ctx, ctx->M, (size_t)std::max<int64_t>(ctot, 1) * ctx->ncoef * 8, true, m));
+        D->nct_cap = std::max<int64_t>(ctot, 1);
+        FMM_TRY(launch_upward());
+    }
     S.tl_end(TL_COVER, m);
     // structure rounds on the comm stream: round r sends to me + r, receives from me - r
     FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[6], m));   // structures packed
@@ -666,6 +765,28 @@ static fmm_status dist_step(fmm_ctx* ctx, DistState* D, const void* pos, const v
     S.tl_begin(TL_LOCAL_DTT, m);
     FMM_TRY(fmm_dtt(ctx, 0, m));
     S.tl_end(TL_LOCAL_DTT, m);
+    bool fast_local = false;
+    if (split) {
+        // local lists -> P2P source runs (synchronises m), then the local M2L and P2P on the compute
+        // stream: they run while the LET fragments are grafted and traversed below
+        FMM_TRY(lists_finish(ctx, m));
+        FMM_TRY(buf_ensure(ctx, D->inter_loc, 64));
+        FMM_CUDA_TRY(ctx, cudaMemcpyAsync(D->inter_loc.p, P_<unsigned long long>(ctx->dcount2) + 2, 8,
+                                          cudaMemcpyDeviceToDevice, m));   // local P2P interaction count
+        FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[8], m));
+        FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(D->cx, D->ev[8], 0));
+        FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(D->cx, D->ev[5], 0));   // M and the bodies' charges
+        S.tl_begin(TL_INTERACT_LOCAL, D->cx);
+        ctx->m2l_cap = D->nct_cap;
+        ctx->m2l_prep_c0 = 0;
+        ctx->m2l_no_expand = true;
+        ctx->m2l_span_fixed = false;
+        ctx->m2l_part = 0;
+        FMM_TRY(m2l_pass(ctx, D->cx));
+        fast_local = ctx->use_fast_m2l && m2l_fast_available(ctx->P, ctx->prec) && !(ctx->prec == FMM_F32 && ctx->m2l_deep);
+        FMM_TRY(p2p_pass(ctx, D->cx));
+        S.tl_end(TL_INTERACT_LOCAL, D->cx);
+    }
     // ---- LET data (multipoles, charges) on the comm stream once the upward pass is done
     FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(cs, D->ev[5], 0));
     S.tl_begin(TL_DATA_XCHG, cs);
@@ -696,30 +817,149 @@ static fmm_status dist_step(fmm_ctx* ctx, DistState* D, const void* pos, const v
         D->peers.push_back(src);
     }
     S.tl_end(TL_REMOTE_DTT, m);
-    S.tl_begin(TL_LISTS, m);
-    FMM_TRY(fmm_lists(ctx, m));
-    S.tl_end(TL_LISTS, m);
-    // ---- 6. data unpacked (graft order), interactions, Eq. (1) weights
-    FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(m, D->ev[7], 0));
-    FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(m, D->ev[5], 0));
-    if (!D->peers.empty()) {
+    FMM_TRY(buf_ensure(ctx, D->phi_loc, (size_t)std::max<int64_t>(nl, 1) * es));
+    FMM_TRY(buf_ensure(ctx, D->grad_loc, (size_t)std::max<int64_t>(nl, 1) * 3 * es));
+    FMM_TRY(buf_ensure(ctx, D->w_loc, (size_t)std::max<int64_t>(nl, 1) * 4));
+    auto unpack = [&]() -> fmm_status {   // LET data (graft order)
+        FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(m, D->ev[7], 0));
+        FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(m, D->ev[5], 0));
+        if (D->peers.empty()) return FMM_OK;
         std::vector<const void*> ptrs;
         std::vector<int64_t> bytes;
         for (int src : D->peers) {
             ptrs.push_back(lrecv + ro[src] + al(rsb[src]));
             bytes.push_back(rdb[src]);
         }
-        FMM_TRY(fmm_let_unpack(ctx, 0, (int)ptrs.size(), ptrs.data(), bytes.data(), m));
+        return fmm_let_unpack(ctx, 0, (int)ptrs.size(), ptrs.data(), bytes.data(), m);
+    };
+    if (!split) {
+        S.tl_begin(TL_LISTS, m);
+        FMM_TRY(fmm_lists(ctx, m));
+        S.tl_end(TL_LISTS, m);
+        // ---- 6. data unpacked (graft order), interactions
+        FMM_TRY(unpack());
+        S.tl_begin(TL_INTERACT, m);
+        FMM_TRY(fmm_interact(ctx, D->phi_loc.p, D->grad_loc.p, m));
+    } else {
+        cudaStream_t cx = D->cx;
+        const int64_t nc = ctx->ncell;
+        S.tl_begin(TL_LISTS, m);
+        // remote-only CSR lists: the remote traversal parts concatenated per target into an empty
+        // list (the local lists stay in place for the kernels reading them on the compute stream)
+        swap_m2l_csr(ctx, D);
+        swap_p2p_csr(ctx, D);
+        FMM_TRY(buf_ensure(ctx, ctx->m2l_off, (size_t)(nc + 1) * 8));
+        FMM_TRY(buf_ensure(ctx, ctx->p2p_off, (size_t)(nc + 1) * 8));
+        FMM_TRY(buf_ensure(ctx, ctx->m2l_src, 64));
+        FMM_TRY(buf_ensure(ctx, ctx->p2p_src, 64));
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->m2l_off.p, 0, (size_t)(nc + 1) * 8, m));
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->p2p_off.p, 0, (size_t)(nc + 1) * 8, m));
+        ctx->n_m2l = ctx->n_p2p = 0;
+        const int parts = ctx->tc_nrem;
+        FMM_TRY(tct_concat(ctx, m));
+        ctx->tc_nrem = parts;   // kept for the full concatenation below
+        // the remote P2P source runs (into the swapped-out run buffers)
+        swap_runs(ctx, D);
+        FMM_TRY(lists_finish(ctx, m));
+        k_add_u64<<<1, 1, 0, m>>>(P_<unsigned long long>(ctx->dcount2) + 2, P_<unsigned long long>(D->inter_loc));
+        FMM_LAUNCH(ctx);
+        swap_runs(ctx, D);
+        swap_p2p_csr(ctx, D);
+        swap_m2l_csr(ctx, D);
+        S.tl_end(TL_LISTS, m);
+        FMM_TRY(unpack());
+        // an fp32 tree spanning more than 14 levels with the LETs grafted: the register kernels'
+        // operand scale leaves the fp32 range (m2l.cu) -- redo M2L with the fp64 kernel on all lists
+        int span = 0;
+        if (ctx->prec == FMM_F32 && fast_local) {
+            FMM_TRY(buf_ensure(ctx, D->span_tmp, 64));
+            int init[2] = {1 << 30, -(1 << 30)}, mm[2];
+            FMM_CUDA_TRY(ctx, cudaMemcpyAsync(D->span_tmp.p, init, 8, cudaMemcpyHostToDevice, m));
+            k_level_minmax<<<grid1(nc + ctx->nrem), 256, 0, m>>>(nc + ctx->nrem, P_<int32_t>(ctx->c_level),
+                                                                 P_<int>(D->span_tmp));
+            FMM_LAUNCH(ctx);
+            FMM_CUDA_TRY(ctx, cudaMemcpyAsync(mm, D->span_tmp.p, 8, cudaMemcpyDeviceToHost, m));
+            FMM_CUDA_TRY(ctx, cudaStreamSynchronize(m));
+            span = mm[1] - mm[0];
+        }
+        const bool redo = fast_local && span > 14;
+        FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[9], m));   // remote lists, runs and data ready
+        FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(cx, D->ev[9], 0));
+        S.tl_begin(TL_INTERACT_REMOTE, cx);
+        ctx->m2l_span_fixed = true;   // keep the local pass's kernel choice
+        ctx->m2l_prep_c0 = nc;        // operands of the grafted cells only
+        if (!redo) {
+            swap_m2l_csr(ctx, D);
+            fmm_status st;
+            if (fast_local) {
+                std::swap(ctx->Lr, D->Lr2);
+                st = m2l_pass(ctx, cx);
+                std::swap(ctx->Lr, D->Lr2);
+            } else {
+                std::swap(ctx->L, D->L2);
+                st = m2l_pass(ctx, cx);
+                std::swap(ctx->L, D->L2);
+            }
+            swap_m2l_csr(ctx, D);
+            FMM_TRY(st);
+            if (fast_local) {
+                const int NL = ctx->P * ctx->P;
+                k_merge_lr<<<grid1(nc * NL), 256, 0, cx>>>(nc, NL, P_<uint64_t>(ctx->m2l_off), P_<uint64_t>(D->r_moff),
+                                                           P_<double>(ctx->Lr), P_<double>(D->Lr2));
+            } else {
+                k_add_f64<<<grid1(nc * ctx->ncoef), 256, 0, cx>>>(nc * ctx->ncoef, P_<double>(ctx->L), P_<double>(D->L2));
+            }
+            FMM_LAUNCH(ctx);
+        }
+        // remote P2P into second partials, added to the local ones
+        swap_p2p_csr(ctx, D);
+        swap_runs(ctx, D);
+        std::swap(ctx->near_phi, D->near2_phi);
+        std::swap(ctx->near_grad, D->near2_grad);
+        fmm_status st = p2p_pass(ctx, cx);
+        std::swap(ctx->near_phi, D->near2_phi);
+        std::swap(ctx->near_grad, D->near2_grad);
+        swap_runs(ctx, D);
+        swap_p2p_csr(ctx, D);
+        FMM_TRY(st);
+        if (ctx->prec == FMM_F32)
+            k_add_near<float><<<grid1(nl), 256, 0, cx>>>(nl, P_<float>(ctx->near_phi), P_<float>(D->near2_phi),
+                                                         P_<float>(ctx->near_grad), P_<float>(D->near2_grad));
+        else
+            k_add_near<double><<<grid1(nl), 256, 0, cx>>>(nl, P_<double>(ctx->near_phi), P_<double>(D->near2_phi),
+                                                          P_<double>(ctx->near_grad), P_<double>(D->near2_grad));
+        FMM_LAUNCH(ctx);
+        if (!redo && fast_local) FMM_TRY(m2l_expand(ctx, P_<uint64_t>(D->r_moff), cx));
+        ctx->m2l_prep_c0 = 0;
+        ctx->m2l_no_expand = false;
+        ctx->m2l_span_fixed = false;
+        // the full concatenated lists (introspection, Eq. (1) weights) on the critical stream, beside
+        // the downward pass: the concatenation rotates the list buffers (tct_concat writes into the
+        // buffers the local and remote lists occupied), so it waits until the compute stream is past
+        // every kernel that reads a list
+        FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[10], cx));
+        FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(m, D->ev[10], 0));
+        FMM_TRY(tct_concat(ctx, m));
+        ctx->built = true;
+        if (redo) {
+            FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[10], m));
+            FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(cx, D->ev[10], 0));
+            ctx->m2l_cap = 0;
+            ctx->m2l_part = 0;
+            FMM_TRY(m2l_pass(ctx, cx));   // all lists, level span measured again: the fp64 kernel
+        }
+        ctx->m2l_cap = 0;
+        FMM_TRY(downward_pass(ctx, D->phi_loc.p, D->grad_loc.p, cx));   // L2L/L2P + near field, local order
+        S.tl_end(TL_INTERACT_REMOTE, cx);
+        FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[11], cx));
+        ctx->evaluated = true;
     }
-    S.tl_begin(TL_INTERACT, m);
-    FMM_TRY(buf_ensure(ctx, D->phi_loc, (size_t)std::max<int64_t>(nl, 1) * es));
-    FMM_TRY(buf_ensure(ctx, D->grad_loc, (size_t)std::max<int64_t>(nl, 1) * 3 * es));
-    FMM_TRY(buf_ensure(ctx, D->w_loc, (size_t)std::max<int64_t>(nl, 1) * 4));
-    FMM_TRY(fmm_interact(ctx, D->phi_loc.p, D->grad_loc.p, m));
+    if (split) S.tl_begin(TL_INTERACT, m);   // (the unsplit flow began the span at its interactions)
     double lr[2] = {0, 0};
     if (nl > 0) FMM_TRY(fmm_work(ctx, D->c_m2l, (float)D->alpha, P_<float>(D->w_loc), lr, m));
     D->st.work_local = lr[0];
     D->st.work_remote = lr[1];
+    if (split) FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(m, D->ev[11], 0));   // phi/grad of the local particles
     S.tl_end(TL_INTERACT, m);
     // ---- 7. results and weights back to the owners
     S.tl_begin(TL_BACK, m);
@@ -758,6 +998,8 @@ static fmm_status dist_step(fmm_ctx* ctx, DistState* D, const void* pos, const v
     FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[0], cs));
     FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(m, D->ev[0], 0));
     FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[0], side));
+    FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(m, D->ev[0], 0));
+    FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[0], D->cx));
     FMM_CUDA_TRY(ctx, cudaStreamWaitEvent(m, D->ev[0], 0));
     if (m != s) {
         FMM_CUDA_TRY(ctx, cudaEventRecord(D->ev[0], m));
@@ -825,6 +1067,9 @@ fmm_status fmm_create_dist(int64_t n_local_max, int p, double theta, int ncrit, 
     D->c_m2l = m2l_cost_ratio(p);
     const char* e = getenv("FMM_DIST_SORT");
     D->overlap_sort = !(e && e[0] == '0');
+    const char* e2 = getenv("FMM_DIST_SPLIT");
+    D->split = !(e2 && e2[0] == '0');
+    ctx->p2p_mutual = 0;   // the split flow runs P2P per list half (one-sided kernels)
     std::string err;
     fmm_status st = nccl_unique_id ? transport_nccl(nranks, rank, nccl_unique_id, device, &D->tr, err)
                                    : transport_local(&group->g, rank, device, &D->tr, err);
@@ -833,6 +1078,7 @@ fmm_status fmm_create_dist(int64_t n_local_max, int p, double theta, int ncrit, 
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         bool ok = cudaStreamCreateWithPriority(&D->cs, cudaStreamNonBlocking, hi) == cudaSuccess &&
                   cudaStreamCreateWithFlags(&D->side, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaStreamCreateWithFlags(&D->cx, cudaStreamNonBlocking) == cudaSuccess &&
                   cudaEventCreate(&D->ev_t0) == cudaSuccess;
         for (auto& ev : D->ev) ok = ok && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
         for (auto& pr : D->tl)
@@ -905,7 +1151,11 @@ fmm_status fmm_dist_solve(fmm_ctx* ctx, const void* pos, const void* q, int64_t 
         D->alpha = D->tuner->next();   // for this step's weights
     }
     fmm_status st = dist_step(ctx, D, pos, q, n, gid_base, w, phi, grad, s);
-    if (st != FMM_OK) return st;
+    if (st != FMM_OK) {
+        // the other ranks must not wait forever in a collective this rank will not reach
+        D->tr->abort();
+        return st;
+    }
     if (D->tuner) {
         FMM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
         double t = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

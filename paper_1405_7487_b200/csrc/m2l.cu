@@ -157,8 +157,10 @@ fmm_status m2l_pass(fmm_ctx* ctx, cudaStream_t s) {
     // range for |de| <= 14 (P <= 10).  Trees spanning more levels (coincident clusters, extreme
     // adaptivity) take the fp64 generic kernel, exact in range at any level difference.
     int span = 0;
-    if (ctx->prec == FMM_F32 && ctx->m2l_part != 2) FMM_TRY(level_span(ctx, s, &span));
-    if (ctx->prec == FMM_F32 && ctx->m2l_part != 2) ctx->m2l_deep = span > 14;
+    if (ctx->prec == FMM_F32 && ctx->m2l_part != 2 && !ctx->m2l_span_fixed) {
+        FMM_TRY(level_span(ctx, s, &span));
+        ctx->m2l_deep = span > 14;
+    }
     if (ctx->prec == FMM_F32 && ctx->m2l_deep) {
         if (ctx->m2l_part == 1) return FMM_OK;
         FMM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->L.p, 0, (size_t)ctx->ncell * ctx->ncoef * 8, s));

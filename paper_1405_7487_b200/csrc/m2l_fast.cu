@@ -314,7 +314,7 @@ FoldTable build_fold_table(int P, int NS, int NSP) {
 }
 
 template <typename R>
-__global__ void k_m2l_prep_table(int64_t ncell, int ncoef, int NSP, const int* __restrict__ toff,
+__global__ void k_m2l_prep_table(int64_t c0, int64_t ncell, int ncoef, int NSP, const int* __restrict__ toff,
                                  const int* __restrict__ tk, const double* __restrict__ tw,
                                  const int* __restrict__ tdg, const double* __restrict__ M,
                                  const int32_t* __restrict__ level, const double* __restrict__ root,
@@ -324,7 +324,7 @@ __global__ void k_m2l_prep_table(int64_t ncell, int ncoef, int NSP, const int* _
     double* Mw = s_M + (size_t)w * ncoef;
     int E;
     frexp(2.0 * root[10], &E);
-    for (int64_t c = (int64_t)blockIdx.x * nw + w; c < ncell; c += (int64_t)gridDim.x * nw) {
+    for (int64_t c = c0 + (int64_t)blockIdx.x * nw + w; c < ncell; c += (int64_t)gridDim.x * nw) {
         const int e = E - level[c];
         for (int k = lane; k < ncoef; k += 32) Mw[k] = M[(size_t)c * ncoef + k];
         if (lane == 0) sexp[c] = e;
@@ -342,14 +342,15 @@ __global__ void k_m2l_prep_table(int64_t ncell, int ncoef, int NSP, const int* _
 
 // reduced, scaled L_hat -> full fp64 L (R11 order) by harmonicity, zero for cells without M2L
 __global__ void k_l_expand(int64_t ncell, int P, int ncoef, const uint64_t* __restrict__ off,
-                           const int* __restrict__ sexp, const double* __restrict__ Lr, double* __restrict__ L) {
+                           const uint64_t* __restrict__ off2, const int* __restrict__ sexp,
+                           const double* __restrict__ Lr, double* __restrict__ L) {
     extern __shared__ double s_L[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double* Lf = s_L + (size_t)w * ncoef;
     const int N0 = P * (P + 1) / 2, NL = P * P;
     for (int64_t c = (int64_t)blockIdx.x * nw + w; c < ncell; c += (int64_t)gridDim.x * nw) {
         double* out = L + (size_t)c * ncoef;
-        if (off[c] == off[c + 1]) {
+        if (off[c] == off[c + 1] && (!off2 || off2[c] == off2[c + 1])) {   // no list (local or remote)
             for (int k = lane; k < ncoef; k += 32) out[k] = 0.0;
             continue;
         }
@@ -381,14 +382,18 @@ fmm_status m2l_fast_t(fmm_ctx* ctx, cudaStream_t s) {
     constexpr int NSP = RF<P>::NSP, NL = RF<P>::NL;
     const int64_t nc = ctx->ncell;
     const int64_t nct = ctx->ncell + ctx->nrem;   // sources include grafted LET cells
-    FMM_TRY(buf_ensure(ctx, ctx->Mr, (size_t)nct * NSP * sizeof(R) + (size_t)nct * 4 + 256));
+    // operand layout capacity (the split multi-GPU flow prepares local and remote cells in two
+    // passes, so the layout must not move between them) and the first cell to prepare
+    const int64_t lay = ctx->m2l_cap > 0 ? ctx->m2l_cap : nct, c0 = ctx->m2l_prep_c0;
+    FMM_TRY(buf_ensure(ctx, ctx->Mr, (size_t)lay * NSP * sizeof(R) + (size_t)lay * 4 + 256));
     FMM_TRY(buf_ensure(ctx, ctx->Lr, (size_t)nc * NL * 8));
     FMM_TRY(buf_ensure(ctx, ctx->cnt_tmp, 64));
     R* Sv = P_<R>(ctx->Mr);
-    int* sexp = reinterpret_cast<int*>(reinterpret_cast<char*>(ctx->Mr.p) + (size_t)nct * NSP * sizeof(R));
+    int* sexp = reinterpret_cast<int*>(reinterpret_cast<char*>(ctx->Mr.p) + (size_t)lay * NSP * sizeof(R));
+    ctx->m2l_sexp = sexp;
     const int nw = 4;
     int g = (int)std::min<int64_t>((nc + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
-    const int gp = (int)std::min<int64_t>((nct + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
+    const int gp = (int)std::min<int64_t>((nct - c0 + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
     if (ctx->fold_P != P) {   // scalar layout table (the mirror kernel keys its own as 1000 + P)
         const FoldTable t = build_fold_table(P, RF<P>::NS, NSP);
         const size_t nt = t.k.size();
@@ -406,7 +411,7 @@ fmm_status m2l_fast_t(fmm_ctx* ctx, cudaStream_t s) {
         char* b = (char*)ctx->fold_tab.p;
         const size_t nt = (size_t)ctx->fold_nt;
         k_m2l_prep_table<R><<<std::max(gp, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
-            nct, ctx->ncoef, NSP, reinterpret_cast<const int*>(b + nt * 8),
+            c0, nct, ctx->ncoef, NSP, reinterpret_cast<const int*>(b + nt * 8),
             reinterpret_cast<const int*>(b + nt * 8 + (2 * NSP + 1) * 4), reinterpret_cast<const double*>(b),
             reinterpret_cast<const int*>(b + nt * 8 + (NSP + 1) * 4), P_<double>(ctx->M), P_<int32_t>(ctx->c_level),
             P_<double>(ctx->root), sexp, Sv);
@@ -423,9 +428,12 @@ fmm_status m2l_fast_t(fmm_ctx* ctx, cudaStream_t s) {
                                                          P_<double>(ctx->Lr), counter);
         FMM_LAUNCH(ctx);
     }
-    k_l_expand<<<std::max(g, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
-        nc, P, ctx->ncoef, P_<uint64_t>(ctx->m2l_off), sexp, P_<double>(ctx->Lr), P_<double>(ctx->L));
-    FMM_LAUNCH(ctx);
+    if (!ctx->m2l_no_expand) {
+        k_l_expand<<<std::max(g, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
+            nc, P, ctx->ncoef, P_<uint64_t>(ctx->m2l_off), ctx->m2l_off2, sexp, P_<double>(ctx->Lr),
+            P_<double>(ctx->L));
+        FMM_LAUNCH(ctx);
+    }
     FMM_CUDA_TRY(ctx, cudaGetLastError());
     return FMM_OK;
 }
@@ -816,14 +824,18 @@ fmm_status m2l_mir_t(fmm_ctx* ctx, cudaStream_t s) {
     constexpr int NSP = K::NSP, NL = K::NL;
     const int64_t nc = ctx->ncell;
     const int64_t nct = ctx->ncell + ctx->nrem;   // sources include grafted LET cells
-    FMM_TRY(buf_ensure(ctx, ctx->Mr, (size_t)nct * NSP * 4 + (size_t)nct * 4 + 256));
+    // operand layout capacity (the split multi-GPU flow prepares local and remote cells in two
+    // passes, so the layout must not move between them) and the first cell to prepare
+    const int64_t lay = ctx->m2l_cap > 0 ? ctx->m2l_cap : nct, c0 = ctx->m2l_prep_c0;
+    FMM_TRY(buf_ensure(ctx, ctx->Mr, (size_t)lay * NSP * 4 + (size_t)lay * 4 + 256));
     FMM_TRY(buf_ensure(ctx, ctx->Lr, (size_t)nc * NL * 8));
     FMM_TRY(buf_ensure(ctx, ctx->cnt_tmp, 64));
     float* Sv = P_<float>(ctx->Mr);
-    int* sexp = reinterpret_cast<int*>(reinterpret_cast<char*>(ctx->Mr.p) + (size_t)nct * NSP * 4);
+    int* sexp = reinterpret_cast<int*>(reinterpret_cast<char*>(ctx->Mr.p) + (size_t)lay * NSP * 4);
+    ctx->m2l_sexp = sexp;
     const int nw = 4;
     const int g = (int)std::min<int64_t>((nc + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
-    const int gp = (int)std::min<int64_t>((nct + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
+    const int gp = (int)std::min<int64_t>((nct - c0 + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
     if (ctx->fold_P != 1000 + P) {
         const FoldTable t = mir::build_fold_table_mir(P, K::NS, NSP);
         const size_t nt = t.k.size();
@@ -841,7 +853,7 @@ fmm_status m2l_mir_t(fmm_ctx* ctx, cudaStream_t s) {
         char* b = (char*)ctx->fold_tab.p;
         const size_t nt = (size_t)ctx->fold_nt;
         k_m2l_prep_table<float><<<std::max(gp, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
-            nct, ctx->ncoef, NSP, reinterpret_cast<const int*>(b + nt * 8),
+            c0, nct, ctx->ncoef, NSP, reinterpret_cast<const int*>(b + nt * 8),
             reinterpret_cast<const int*>(b + nt * 8 + (2 * NSP + 1) * 4), reinterpret_cast<const double*>(b),
             reinterpret_cast<const int*>(b + nt * 8 + (NSP + 1) * 4), P_<double>(ctx->M), P_<int32_t>(ctx->c_level),
             P_<double>(ctx->root), sexp, Sv);
@@ -858,13 +870,30 @@ fmm_status m2l_mir_t(fmm_ctx* ctx, cudaStream_t s) {
                                                           counter);
         FMM_LAUNCH(ctx);
     }
-    k_l_expand<<<std::max(g, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
-        nc, P, ctx->ncoef, P_<uint64_t>(ctx->m2l_off), sexp, P_<double>(ctx->Lr), P_<double>(ctx->L));
-    FMM_LAUNCH(ctx);
+    if (!ctx->m2l_no_expand) {
+        k_l_expand<<<std::max(g, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
+            nc, P, ctx->ncoef, P_<uint64_t>(ctx->m2l_off), ctx->m2l_off2, sexp, P_<double>(ctx->Lr),
+            P_<double>(ctx->L));
+        FMM_LAUNCH(ctx);
+    }
     FMM_CUDA_TRY(ctx, cudaGetLastError());
     return FMM_OK;
 }
 }  // namespace
+
+// the reduced -> full L expansion alone (split multi-GPU flow, dist.cu): after the local and the
+// remote register-kernel passes have left the summed reduced L_hat in ctx->Lr; off2 = the remote
+// lists' offsets (a cell with neither a local nor a remote list gets L = 0)
+fmm_status m2l_expand(fmm_ctx* ctx, const uint64_t* off2, cudaStream_t s) {
+    const int64_t nc = ctx->ncell;
+    const int nw = 4;
+    const int g = (int)std::min<int64_t>((nc + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
+    k_l_expand<<<std::max(g, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
+        nc, ctx->P, ctx->ncoef, P_<uint64_t>(ctx->m2l_off), off2, ctx->m2l_sexp, P_<double>(ctx->Lr), P_<double>(ctx->L));
+    FMM_LAUNCH(ctx);
+    FMM_CUDA_TRY(ctx, cudaGetLastError());
+    return FMM_OK;
+}
 
 // returns FMM_ERR_ARG (without launching) when no register kernel exists for (P, prec)
 fmm_status m2l_fast(fmm_ctx* ctx, cudaStream_t s) {

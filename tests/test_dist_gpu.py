@@ -375,7 +375,38 @@ def test_dist_timeline_overlap(torch_cuda):
         assert tl["let_struct_exchange"][0] <= tl["local_dtt"][0] + 1e-3, tl
         assert tl["let_data_exchange"][1] >= tl["upward"][1] - 1e-3, tl
         assert tl["stay_sort"][0] <= tl["particle_exchange"][1] + 1e-3, tl
+        # split interactions: the local M2L/P2P start before the remote fragments are traversed
+        assert 0 <= tl["interact_local"][0] <= tl["remote_dtt"][0] + 1e-3, tl
+        assert tl["interact_remote"][0] >= tl["interact_local"][0], tl
     D.close()
+
+
+@pytest.mark.parametrize("prec,part", [("f32", "morton"), ("f64", "orb")])
+def test_split_interactions_match_unsplit(torch_cuda, prec, part, monkeypatch):
+    """Local M2L/P2P launched right after the local traversal and the remote lists' interactions
+    added after the fragments (default) against one pass over the concatenated lists
+    (FMM_DIST_SPLIT=0): the same lists bit for bit, the same fields to the precision's tolerance
+    (only the summation order differs)."""
+    torch = torch_cuda
+    n, K = 24000, 3
+    dt = np.float32 if prec == "f32" else np.float64
+    pos, q = synth.generate("plummer", n, 19, dt)
+    P_in, Q_in, bases = split_input(torch, pos, q, K)
+    P, ncrit = (10, 64) if prec == "f32" else (6, 16)
+    A = Ranks(torch, K, n, P, 0.4, ncrit, prec, part)
+    monkeypatch.setenv("FMM_DIST_SPLIT", "0")
+    B = Ranks(torch, K, n, P, 0.4, ncrit, prec, part)
+    oa = A.solve(P_in, Q_in, bases)
+    ob = B.solve(P_in, Q_in, bases)
+    for r in range(K):
+        for x, y in zip(A.fmm[r].lists(), B.fmm[r].lists()):
+            np.testing.assert_array_equal(x, y)
+        assert A.fmm[r].counts() == B.fmm[r].counts()
+    phi_a = np.concatenate([o[0].cpu().numpy() for o in oa]); phi_b = np.concatenate([o[0].cpu().numpy() for o in ob])
+    grad_a = np.concatenate([o[1].cpu().numpy() for o in oa]); grad_b = np.concatenate([o[1].cpu().numpy() for o in ob])
+    assert_fields(phi_a, phi_b, grad_a, grad_b, TOL[prec], "split vs unsplit")
+    A.close()
+    B.close()
 
 
 def test_nccl_transport_single_rank(torch_cuda):
