@@ -257,9 +257,12 @@ struct DistState {
     double alpha = 1.0, c_m2l = 0.0;
     fmm_alpha_tuner* tuner = nullptr;
     bool overlap_sort = true;   // f1: staying particles sorted while the particles fly (FMM_DIST_SORT=0: off)
-    // local M2L/P2P started on the compute stream right after the local traversal, while the LET
-    // fragments are grafted and traversed; the remote lists' interactions added after (FMM_DIST_SPLIT=0: off)
-    bool split = true;
+    // FMM_DIST_SPLIT=1: local M2L/P2P started on the compute stream right after the local traversal,
+    // while the LET fragments are grafted and traversed; the remote lists' interactions added after.
+    // Off by default: the persistent M2L/P2P kernels hold every SM until they finish, so the remote
+    // traversal's kernels queue behind them -- the split reorders the work without overlapping it
+    // (profiles/r02_dist_timeline_1gpu_split.jsonl)
+    bool split = false;
     cudaStream_t cx = nullptr;
     int64_t nct_cap = 0;
     // remote-only CSR lists, their P2P source runs, and the second outputs of the remote pass
@@ -1068,7 +1071,7 @@ fmm_status fmm_create_dist(int64_t n_local_max, int p, double theta, int ncrit, 
     const char* e = getenv("FMM_DIST_SORT");
     D->overlap_sort = !(e && e[0] == '0');
     const char* e2 = getenv("FMM_DIST_SPLIT");
-    D->split = !(e2 && e2[0] == '0');
+    D->split = e2 && e2[0] == '1';
     ctx->p2p_mutual = 0;   // the split flow runs P2P per list half (one-sided kernels)
     std::string err;
     fmm_status st = nccl_unique_id ? transport_nccl(nranks, rank, nccl_unique_id, device, &D->tr, err)

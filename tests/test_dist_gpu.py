@@ -357,11 +357,14 @@ def test_partition_overlap_bit_identical(torch_cuda, prec, monkeypatch):
     B.close()
 
 
-def test_dist_timeline_overlap(torch_cuda):
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_dist_timeline_overlap(torch_cuda, split, monkeypatch):
     """fmm_dist_timeline: the LET structure exchange is posted before the local traversal (their
     spans overlap or the exchange ends first), the data exchange starts after the upward pass, and
-    the staying-particle sort starts before the particle exchange ends."""
+    the staying-particle sort starts before the particle exchange ends; with FMM_DIST_SPLIT=1 the
+    local interactions start before the remote fragments are traversed."""
     torch = torch_cuda
+    monkeypatch.setenv("FMM_DIST_SPLIT", split)
     n, K = 60000, 2
     pos, q = synth.generate("cube", n, 3, np.float32)
     P_in, Q_in, bases = split_input(torch, pos, q, K)
@@ -375,36 +378,39 @@ def test_dist_timeline_overlap(torch_cuda):
         assert tl["let_struct_exchange"][0] <= tl["local_dtt"][0] + 1e-3, tl
         assert tl["let_data_exchange"][1] >= tl["upward"][1] - 1e-3, tl
         assert tl["stay_sort"][0] <= tl["particle_exchange"][1] + 1e-3, tl
-        # split interactions: the local M2L/P2P start before the remote fragments are traversed
-        assert 0 <= tl["interact_local"][0] <= tl["remote_dtt"][0] + 1e-3, tl
-        assert tl["interact_remote"][0] >= tl["interact_local"][0], tl
+        if split == "1":   # split interactions: the local M2L/P2P start before the remote traversal
+            assert 0 <= tl["interact_local"][0] <= tl["remote_dtt"][0] + 1e-3, tl
+            assert tl["interact_remote"][0] >= tl["interact_local"][0], tl
     D.close()
 
 
 @pytest.mark.parametrize("prec,part", [("f32", "morton"), ("f64", "orb")])
 def test_split_interactions_match_unsplit(torch_cuda, prec, part, monkeypatch):
     """Local M2L/P2P launched right after the local traversal and the remote lists' interactions
-    added after the fragments (default) against one pass over the concatenated lists
-    (FMM_DIST_SPLIT=0): the same lists bit for bit, the same fields to the precision's tolerance
-    (only the summation order differs)."""
+    added after the fragments (FMM_DIST_SPLIT=1) against one pass over the concatenated lists
+    (default), over 6 steps with reused Eq. (1) weights (buffer rotations between steps): the same
+    lists bit for bit, the same fields to the precision's tolerance (only the summation order
+    differs)."""
     torch = torch_cuda
     n, K = 24000, 3
     dt = np.float32 if prec == "f32" else np.float64
     pos, q = synth.generate("plummer", n, 19, dt)
     P_in, Q_in, bases = split_input(torch, pos, q, K)
     P, ncrit = (10, 64) if prec == "f32" else (6, 16)
+    monkeypatch.setenv("FMM_DIST_SPLIT", "1")
     A = Ranks(torch, K, n, P, 0.4, ncrit, prec, part)
     monkeypatch.setenv("FMM_DIST_SPLIT", "0")
     B = Ranks(torch, K, n, P, 0.4, ncrit, prec, part)
-    oa = A.solve(P_in, Q_in, bases)
-    ob = B.solve(P_in, Q_in, bases)
-    for r in range(K):
-        for x, y in zip(A.fmm[r].lists(), B.fmm[r].lists()):
-            np.testing.assert_array_equal(x, y)
-        assert A.fmm[r].counts() == B.fmm[r].counts()
-    phi_a = np.concatenate([o[0].cpu().numpy() for o in oa]); phi_b = np.concatenate([o[0].cpu().numpy() for o in ob])
-    grad_a = np.concatenate([o[1].cpu().numpy() for o in oa]); grad_b = np.concatenate([o[1].cpu().numpy() for o in ob])
-    assert_fields(phi_a, phi_b, grad_a, grad_b, TOL[prec], "split vs unsplit")
+    for step in range(6):
+        oa = A.solve(P_in, Q_in, bases, reuse_weights=True)
+        ob = B.solve(P_in, Q_in, bases, reuse_weights=True)
+        for r in range(K):
+            for x, y in zip(A.fmm[r].lists(), B.fmm[r].lists()):
+                np.testing.assert_array_equal(x, y)
+            assert A.fmm[r].counts() == B.fmm[r].counts()
+        phi_a = np.concatenate([o[0].cpu().numpy() for o in oa]); phi_b = np.concatenate([o[0].cpu().numpy() for o in ob])
+        grad_a = np.concatenate([o[1].cpu().numpy() for o in oa]); grad_b = np.concatenate([o[1].cpu().numpy() for o in ob])
+        assert_fields(phi_a, phi_b, grad_a, grad_b, TOL[prec], f"split vs unsplit, step {step}")
     A.close()
     B.close()
 

@@ -69,8 +69,9 @@ def test_guard_and_poison(torch_cuda, monkeypatch, kind, n, P, theta, ncrit, pre
 
 
 def test_guard_dist_and_debug_stages(torch_cuda, monkeypatch):
-    """The distributed driver (in-process group, 3 ranks, both partitioners) and the debug stage
-    entries under guard zones and poisoned allocations."""
+    """The distributed driver (in-process group, 3 ranks, both partitioners; the ORB run with the
+    split interactions of FMM_DIST_SPLIT=1) and the debug stage entries under guard zones and
+    poisoned allocations."""
     torch = torch_cuda
     from paper_1405_7487_b200 import FMM
     from paper_1405_7487_b200.dist import DistFMM, LocalGroup, run_ranks
@@ -82,6 +83,7 @@ def test_guard_dist_and_debug_stages(torch_cuda, monkeypatch):
     P_in = [torch.from_numpy(pos[cuts[r]:cuts[r + 1]]).cuda() for r in range(K)]
     Q_in = [torch.from_numpy(q[cuts[r]:cuts[r + 1]]).cuda() for r in range(K)]
     for part in ("morton", "orb"):
+        monkeypatch.setenv("FMM_DIST_SPLIT", "1" if part == "orb" else "0")
         G = LocalGroup(K)
         Ds = [DistFMM(n, 10, 0.4, 64, "f32", 0, K, r, group=G, partitioner=part) for r in range(K)]
         streams = [torch.cuda.Stream() for _ in range(K)]
