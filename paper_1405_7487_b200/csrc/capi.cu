@@ -191,7 +191,7 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
                       &ctx->lst_p2p, &ctx->lst_tmp, &ctx->m2l_src, &ctx->p2p_src, &ctx->m2l_off, &ctx->p2p_off,
                       &ctx->cnt_tmp, &ctx->cnt_tmp2, &ctx->dcount, &ctx->runs, &ctx->run_off, &ctx->run_tmp, &ctx->run_pre,
                       &ctx->run_len64, &ctx->dcount2, &ctx->tcnt, &ctx->cnt64, &ctx->big_off, &ctx->M, &ctx->L, &ctx->Mr, &ctx->Lr, &ctx->near_phi, &ctx->near_grad,
-                      &ctx->far, &ctx->h_stage, &ctx->mut_mir, &ctx->mut_w, &ctx->mut_so, &ctx->mut_slot, &ctx->iperm};
+                      &ctx->far, &ctx->h_stage, &ctx->mut_mir, &ctx->mut_w, &ctx->mut_so, &ctx->mut_slot, &ctx->iperm, &ctx->m2l_mix};
     for (DevBuf* b : bufs) buf_free(*b);
     DevBuf* tbufs[] = {&ctx->tc_cnt, &ctx->tc_voff, &ctx->tc_lb, &ctx->tc_d[0], &ctx->tc_d[1], &ctx->tc_doff[0],
                        &ctx->tc_doff[1], &ctx->tc_glob, &ctx->tc_slab, &ctx->tc_bsum, &ctx->tc_cat_off,

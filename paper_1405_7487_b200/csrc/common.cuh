@@ -197,6 +197,7 @@ struct fmm_ctx {
 
     // expansions
     DevBuf M, L, Mr, Lr, fold_tab;
+    DevBuf m2l_mix;               // per-target "list mixes levels" flags + level bounds (m2l_fast.cu)
     int fold_P = -1;              // P of the fold table in fold_tab (m2l_fast.cu)
     int64_t fold_nt = 0;   // fp64 [ncell][ncoef]; Mr: packed reduced multipoles for the M2L kernel; Lr: reduced L
     DevBuf near_phi, near_grad;  // P2P partials in sorted order (prec type)

@@ -104,6 +104,8 @@ void drop_build(fmm_ctx* ctx) {
     ctx->lists_csr = false;
     ctx->nrem = ctx->nrem_body = 0;
     ctx->let_remote.clear();
+    ctx->level_begin.clear();   // the caller's cells need not be level-ordered (m2l_fast.cu: all "mixed")
+    ctx->depth = 0;
 }
 
 }  // namespace

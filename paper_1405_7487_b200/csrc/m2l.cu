@@ -131,7 +131,8 @@ __global__ void k_level_span(int64_t n, const int32_t* __restrict__ level, int* 
 // levels 0..depth; grafted LET cells carry levels rebased to this tree's root (let.cu), so with
 // remote cells the span is measured
 fmm_status level_span(fmm_ctx* ctx, cudaStream_t s, int* span) {
-    if (ctx->nrem == 0) {
+    // (a caller-supplied tree -- fmm_debug_m2l -- has no level table: measured too)
+    if (ctx->nrem == 0 && ctx->level_begin.size() >= 2 && ctx->level_begin.back() == ctx->ncell) {
         *span = (int)ctx->depth;
         return FMM_OK;
     }

@@ -318,7 +318,7 @@ __global__ void k_m2l_prep_table(int64_t c0, int64_t ncell, int ncoef, int NSP, 
                                  const int* __restrict__ tk, const double* __restrict__ tw,
                                  const int* __restrict__ tdg, const double* __restrict__ M,
                                  const int32_t* __restrict__ level, const double* __restrict__ root,
-                                 int* __restrict__ sexp, R* __restrict__ Sv) {
+                                 int* __restrict__ sexp, R* __restrict__ Sv, int64_t copy_stride = 0) {
     extern __shared__ double s_M[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double* Mw = s_M + (size_t)w * ncoef;
@@ -335,6 +335,10 @@ __global__ void k_m2l_prep_table(int64_t c0, int64_t ncell, int ncoef, int NSP, 
             for (int t = toff[i]; t < toff[i + 1]; ++t) v += tw[t] * Mw[tk[t]];
             const int dg = tdg[i];
             out[i] = dg < 0 ? R(0) : (R)ldexp(v, -e * dg);
+            if (copy_stride) {   // the operand as the pair scaling 2^(de dg) leaves it, de = -1 and +1
+                out[i - copy_stride] = dg < 0 ? R(0) : (R)ldexp(v, -(e + 1) * dg);
+                out[i + copy_stride] = dg < 0 ? R(0) : (R)ldexp(v, -(e - 1) * dg);
+            }
         }
         __syncwarp();
     }
@@ -638,11 +642,17 @@ __host__ __device__ constexpr int slot_z(int j) {
             if (j-- == 0) return z;
 }
 
-template <int P>
+// SC = false: only the targets whose sources are all within one level of their own
+// (mixed[a] == 0; a uniform tree: every target), reading the operand copy prepared at the pair's
+// scale 2^(de n), de in {-1, 0, 1}, so the kernel has no scaling code at all (~8% fewer
+// instructions per pair); SC = true: the other targets (every target if mixed == nullptr), de = 0
+// copy scaled in registers
+template <int P, bool SC>
 __global__ void __launch_bounds__(128, 2)
     k_m2l_mir(int64_t ncell, const uint32_t* __restrict__ src, const uint64_t* __restrict__ offs,
               const double4* __restrict__ cr, const int* __restrict__ sexp, const float4* __restrict__ Sv,
-              double* __restrict__ Lr, unsigned long long* __restrict__ counter) {
+              double* __restrict__ Lr, unsigned long long* __restrict__ counter,
+              const uint8_t* __restrict__ mixed, int64_t lay) {
     using K = L<P>;
     constexpr int NCH = K::NCH;
     const int lane = threadIdx.x & 31;
@@ -667,6 +677,7 @@ __global__ void __launch_bounds__(128, 2)
         if (a >= ncell) break;
         const uint64_t p0 = offs[a], p1 = offs[a + 1];
         if (p0 == p1) continue;
+        if (mixed && (mixed[a] != 0) != SC) continue;   // the other kernel's target
         const double4 ca = cr[a];
         const int ea = sexp[a];
         const double sa = exp2((double)-ea);   // 1/rho_A, exact
@@ -696,11 +707,13 @@ __global__ void __launch_bounds__(128, 2)
             derivs_mir<P>(ux, uy, uz, R);
             if (p + 32 < p1) fetch_cb(bnext);   // after the recurrence: bnext has landed
             // (rho_B/rho_A)^n: only in warps where some lane needs it (uniform trees: never)
-            const bool need = __any_sync(__activemask(), de != 0);
+            const bool need = SC && __any_sync(__activemask(), de != 0);
             // 2^(de*n) from exponent bits: |de| <= 14 is guaranteed by m2l_pass, which routes trees
             // spanning more than 14 levels to the fp64 kernel (|de * n| <= 126 for n <= 9)
             auto pw = [&](int n) { return __int_as_float((127 + de * n) << 23); };
-            const float4* sv = Sv + (size_t)b * NCH;
+            // SC = false: |de| <= 1 for every pair of this target, and the operand comes from the
+            // copy prepared at that scale (rows -lay .. +lay of the de = 0 copy Sv)
+            const float4* sv = Sv + ((SC ? 0 : (int64_t)de * lay) + (int64_t)b) * NCH;
             sfor<0, NCH>([&](auto cc) {
                 constexpr int C = decltype(cc)::value;
                 const float4 v = sv[C];
@@ -772,6 +785,32 @@ __global__ void __launch_bounds__(128, 2)
     }
 }
 
+// mixed[a] = 1 iff target a's M2L list holds a source more than one level away (no prepared
+// operand copy at that scale).  Local cells are level-ordered, so a local source is within one
+// level of a iff its index lies in lvl[level(a) - 1] .. lvl[level(a) + 2] (no gather); grafted
+// LET cells (index >= nloc) compare their exponents.  Warp per target.
+__global__ void k_m2l_mixed(int64_t ncell, int64_t nloc, const uint32_t* __restrict__ src,
+                            const uint64_t* __restrict__ offs, const int32_t* __restrict__ level,
+                            const int64_t* __restrict__ lvl, int nlvl, const int* __restrict__ sexp,
+                            uint8_t* __restrict__ mixed) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t a = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); a < ncell; a += nw) {
+        const uint64_t p0 = offs[a], p1 = offs[a + 1];
+        const int la = level[a];
+        const bool ok = la + 1 < nlvl;
+        const int64_t lo = ok ? lvl[max(la - 1, 0)] : 0, hi = ok ? lvl[min(la + 2, nlvl - 1)] : -1;
+        const int ea = sexp[a];
+        bool mix = false;
+        for (uint64_t p = p0 + lane; p < p1; p += 32) {
+            const int64_t b = src[p];
+            mix |= b < nloc ? (b < lo || b >= hi) : abs(sexp[b] - ea) > 1;
+        }
+        mix = __any_sync(0xffffffffu, mix);
+        if (lane == 0) mixed[a] = mix ? 1 : 0;
+    }
+}
+
 // operand layout of the mirror kernel as a fold table: output float i -> (kind, 2D index, degree)
 FoldTable build_fold_table_mir(int P, int NS, int NSP) {
     const int O0 = noff(P - 1), O1 = noff(P - 2 < 0 ? 0 : P - 2), G0 = ndia(P - 1), G1 = ndia(P - 2 < 0 ? 0 : P - 2);
@@ -827,11 +866,13 @@ fmm_status m2l_mir_t(fmm_ctx* ctx, cudaStream_t s) {
     // operand layout capacity (the split multi-GPU flow prepares local and remote cells in two
     // passes, so the layout must not move between them) and the first cell to prepare
     const int64_t lay = ctx->m2l_cap > 0 ? ctx->m2l_cap : nct, c0 = ctx->m2l_prep_c0;
-    FMM_TRY(buf_ensure(ctx, ctx->Mr, (size_t)lay * NSP * 4 + (size_t)lay * 4 + 256));
+    // operand: three copies [de = -1 | de = 0 | de = +1] of lay cells each, then the exponents
+    const size_t lstride = (size_t)lay * NSP;   // floats per copy
+    FMM_TRY(buf_ensure(ctx, ctx->Mr, 3 * lstride * 4 + (size_t)lay * 4 + 256));
     FMM_TRY(buf_ensure(ctx, ctx->Lr, (size_t)nc * NL * 8));
     FMM_TRY(buf_ensure(ctx, ctx->cnt_tmp, 64));
-    float* Sv = P_<float>(ctx->Mr);
-    int* sexp = reinterpret_cast<int*>(reinterpret_cast<char*>(ctx->Mr.p) + (size_t)lay * NSP * 4);
+    float* Sv = P_<float>(ctx->Mr) + lstride;   // the de = 0 copy
+    int* sexp = reinterpret_cast<int*>(reinterpret_cast<char*>(ctx->Mr.p) + 3 * lstride * 4);
     ctx->m2l_sexp = sexp;
     const int nw = 4;
     const int g = (int)std::min<int64_t>((nc + nw - 1) / nw, (int64_t)ctx->num_sms * 16);
@@ -856,18 +897,35 @@ fmm_status m2l_mir_t(fmm_ctx* ctx, cudaStream_t s) {
             c0, nct, ctx->ncoef, NSP, reinterpret_cast<const int*>(b + nt * 8),
             reinterpret_cast<const int*>(b + nt * 8 + (2 * NSP + 1) * 4), reinterpret_cast<const double*>(b),
             reinterpret_cast<const int*>(b + nt * 8 + (NSP + 1) * 4), P_<double>(ctx->M), P_<int32_t>(ctx->c_level),
-            P_<double>(ctx->root), sexp, Sv);
+            P_<double>(ctx->root), sexp, Sv, (int64_t)lstride);
         FMM_LAUNCH(ctx);
     }
     if (ctx->m2l_part == 1) return FMM_OK;   // operand preparation only (fmm_solve: aux stream)
     unsigned long long* counter = P_<unsigned long long>(ctx->cnt_tmp);
-    FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 8, s));
     {
         PhaseScope ps(ctx, PH_M2L_KERNEL, s);
-        mir::k_m2l_mir<P><<<ctx->num_sms * 2, 128, 0, s>>>(nc, P_<uint32_t>(ctx->m2l_src), P_<uint64_t>(ctx->m2l_off),
-                                                          P_<double4>(ctx->c_cr), sexp,
-                                                          reinterpret_cast<const float4*>(Sv), P_<double>(ctx->Lr),
-                                                          counter);
+        // split the targets by whether every source is within one level: those run the kernel
+        // without scaling code, the others the scaled kernel (a uniform tree: none of them)
+        // (level ranges only when they describe these cells; else every target counts as mixed)
+        const bool ranges = ctx->level_begin.size() >= 2 && ctx->level_begin.back() == ctx->ncell;
+        const int nlvl = ranges ? (int)ctx->level_begin.size() : 0;
+        FMM_TRY(buf_ensure(ctx, ctx->m2l_mix, (size_t)nlvl * 8 + (size_t)nc + 64));
+        int64_t* lvl = P_<int64_t>(ctx->m2l_mix);
+        uint8_t* mixed = reinterpret_cast<uint8_t*>(lvl + nlvl);
+        if (nlvl > 0)   // pageable source: staged at the call, ordered on s
+            FMM_CUDA_TRY(ctx, cudaMemcpyAsync(lvl, ctx->level_begin.data(), (size_t)nlvl * 8, cudaMemcpyHostToDevice, s));
+        mir::k_m2l_mixed<<<std::max(g, 1), nw * 32, 0, s>>>(nc, ctx->ncell, P_<uint32_t>(ctx->m2l_src),
+                                                            P_<uint64_t>(ctx->m2l_off), P_<int32_t>(ctx->c_level), lvl,
+                                                            nlvl, sexp, mixed);
+        FMM_LAUNCH(ctx);
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 16, s));
+        mir::k_m2l_mir<P, false><<<ctx->num_sms * 2, 128, 0, s>>>(
+            nc, P_<uint32_t>(ctx->m2l_src), P_<uint64_t>(ctx->m2l_off), P_<double4>(ctx->c_cr), sexp,
+            reinterpret_cast<const float4*>(Sv), P_<double>(ctx->Lr), counter, mixed, lay);
+        FMM_LAUNCH(ctx);
+        mir::k_m2l_mir<P, true><<<ctx->num_sms * 2, 128, 0, s>>>(
+            nc, P_<uint32_t>(ctx->m2l_src), P_<uint64_t>(ctx->m2l_off), P_<double4>(ctx->c_cr), sexp,
+            reinterpret_cast<const float4*>(Sv), P_<double>(ctx->Lr), counter + 1, mixed, lay);
         FMM_LAUNCH(ctx);
     }
     if (!ctx->m2l_no_expand) {
