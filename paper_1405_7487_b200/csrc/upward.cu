@@ -15,48 +15,71 @@
 #include "common.cuh"
 
 namespace {
-constexpr int P2M_WARPS = 2;
+constexpr int P2M_WARPS = 4;
 
 __constant__ double c_inv[FMM_MAXP + 1] = {0.0,       1.0,        1.0 / 2,  1.0 / 3,  1.0 / 4,  1.0 / 5,
                                            1.0 / 6,   1.0 / 7,    1.0 / 8,  1.0 / 9,  1.0 / 10, 1.0 / 11,
                                            1.0 / 12,  1.0 / 13,   1.0 / 14, 1.0 / 15, 1.0 / 16};
+
+// M_(a,b,c) = sum_j [q_j x_j^a/a! y_j^b/b!] z_j^c/c!: per batch of 32 bodies, lane j writes its
+// body's products T[(a,b)][j] = q_j x_j^a/a! y_j^b/b! (a+b <= P-1) and Z[c][j] = z_j^c/c! to the
+// warp's shared tables; then every coefficient takes one FMA per body, T x Z, bodies in order
+// (2 shared loads + 1 FMA per body and coefficient instead of 3 loads + 2 multiplies + 1 FMA).
+__host__ __device__ __forceinline__ int p2m_smem_doubles(int P) { return (P * (P + 1) / 2 + P) * 33; }
 
 template <typename Body, int NI>
 __global__ void __launch_bounds__(P2M_WARPS * 32) k_p2m(const Body* __restrict__ body, const uint32_t* __restrict__ leaf_ids,
                                                         int64_t nleaf, const uint32_t* __restrict__ bb,
                                                         const uint32_t* __restrict__ bc, const double4* __restrict__ cr,
                                                         int P, int ncoef, double* __restrict__ M) {
+    extern __shared__ double s_p2m[];
     __shared__ uchar4 ex[816];
-    __shared__ double s_pw[P2M_WARPS][3][FMM_MAXP][33];
-    __shared__ double s_q[P2M_WARPS][32];
     fill_ex_table(ex, ncoef);
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nab = P * (P + 1) / 2;
+    double* T = s_p2m + (size_t)w * p2m_smem_doubles(P);   // T[(a,b)][33]
+    double* Z = T + (size_t)nab * 33;                      // Z[c][33]
+    int tix[NI], zc[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+        const uchar4 e = ex[min(lane + 32 * i, ncoef - 1)];
+        const int s2 = e.x + e.y;
+        tix[i] = (s2 * (s2 + 1) / 2 + e.y) * 33;   // (a,b) row: a+b = s2, then b
+        zc[i] = e.z * 33;
+    }
     for (int64_t li = (int64_t)blockIdx.x * P2M_WARPS + w; li < nleaf; li += (int64_t)gridDim.x * P2M_WARPS) {
         const uint32_t c = leaf_ids[li];
         const double4 ctr = cr[c];
         double acc[NI];
-        uchar4 ek[NI];
 #pragma unroll
-        for (int i = 0; i < NI; ++i) {
-            acc[i] = 0.0;
-            ek[i] = ex[min(lane + 32 * i, ncoef - 1)];
-        }
+        for (int i = 0; i < NI; ++i) acc[i] = 0.0;
         const uint32_t b0 = bb[c], nb = bc[c];
         for (uint32_t j0 = 0; j0 < nb; j0 += 32) {
             const uint32_t m = min(32u, nb - j0);
             __syncwarp();
             if ((uint32_t)lane < m) {
                 const Body p = body[b0 + j0 + lane];
-                const double d[3] = {(double)p.x - ctr.x, (double)p.y - ctr.y, (double)p.z - ctr.z};
-                s_q[w][lane] = (double)p.w;
+                const double dx = (double)p.x - ctr.x, dy = (double)p.y - ctr.y, dz = (double)p.z - ctr.z;
+                double qx[FMM_MAXP], yy[FMM_MAXP];
+                qx[0] = (double)p.w;
+                yy[0] = 1.0;
+                double vz = 1.0;
+                Z[lane] = 1.0;
 #pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    double v = 1.0;
-                    s_pw[w][a][0][lane] = 1.0;
-                    for (int e = 1; e < P; ++e) {
-                        v = v * d[a] * c_inv[e];
-                        s_pw[w][a][e][lane] = v;
+                for (int e = 1; e < FMM_MAXP; ++e) {
+                    if (e < P) {
+                        qx[e] = qx[e - 1] * dx * c_inv[e];
+                        yy[e] = yy[e - 1] * dy * c_inv[e];
+                        vz = vz * dz * c_inv[e];
+                        Z[e * 33 + lane] = vz;
+                    }
+                }
+#pragma unroll
+                for (int s2 = 0; s2 < FMM_MAXP; ++s2) {
+                    if (s2 < P) {
+#pragma unroll
+                        for (int y = 0; y <= s2; ++y) T[(s2 * (s2 + 1) / 2 + y) * 33 + lane] = qx[s2 - y] * yy[y];
                     }
                 }
             }
@@ -64,14 +87,8 @@ __global__ void __launch_bounds__(P2M_WARPS * 32) k_p2m(const Body* __restrict__
             // bodies outer, coefficients inner: the NI accumulators are independent chains
             // (each coefficient still sums its bodies in order)
             for (uint32_t j = 0; j < m; ++j) {
-                const double qj = s_q[w][j];
 #pragma unroll
-                for (int i = 0; i < NI; ++i) {
-                    if (lane + 32 * i < ncoef) {
-                        const uchar4 e = ek[i];
-                        acc[i] += qj * (s_pw[w][0][e.x][j] * s_pw[w][1][e.y][j] * s_pw[w][2][e.z][j]);
-                    }
-                }
+                for (int i = 0; i < NI; ++i) acc[i] = fma(T[tix[i] + j], Z[zc[i] + j], acc[i]);
             }
         }
 #pragma unroll
@@ -83,16 +100,25 @@ __global__ void __launch_bounds__(P2M_WARPS * 32) k_p2m(const Body* __restrict__
 }
 
 // one separable 1D shift pass along axis `ax`: out_alpha = sum_{b <= a_ax} in_{alpha with a_ax -> b} t[a_ax - b]
+// The source index cidx(alpha with a_ax = b) is stepped incrementally in b (cidx = n(n+1)(n+2)/6 +
+// m(m+1)/2 + c, n = |alpha|, m = a_y + a_z: raising a_ax by one adds (n+1)(n+2)/2 to the first
+// term, plus m+1 to the second for the y and z axes, plus 1 for z) -- the same terms in the
+// same order as evaluating cidx per term, without its multiplications and division per term.
 __device__ __forceinline__ void shift_pass_up(const uchar4* __restrict__ ex, int ncoef, int ax, const double* in,
                                               double* out, const double* t, int lane) {
     for (int k = lane; k < ncoef; k += 32) {
         const uchar4 e = ex[k];
         int a[3] = {e.x, e.y, e.z};
         const int top = a[ax];
+        a[ax] = 0;
+        int n = a[0] + a[1] + a[2], m = a[1] + a[2];
+        int idx = cidx(a[0], a[1], a[2]);
         double s = 0.0;
         for (int b = 0; b <= top; ++b) {
-            a[ax] = b;
-            s += in[cidx(a[0], a[1], a[2])] * t[top - b];
+            s += in[idx] * t[top - b];
+            idx += (n + 1) * (n + 2) / 2 + (ax == 0 ? 0 : m + 1) + (ax == 2 ? 1 : 0);
+            ++n;
+            if (ax != 0) ++m;
         }
         out[k] = s;
     }
@@ -158,7 +184,10 @@ fmm_status upward_t(fmm_ctx* ctx, cudaStream_t s) {
     const int ni = (ctx->ncoef + 31) / 32;
     auto p2m = [&](auto tag) {
         constexpr int NI = decltype(tag)::value;
-        k_p2m<Body, NI><<<std::max(g, 1), P2M_WARPS * 32, 0, s>>>(P_<Body>(ctx->body), P_<uint32_t>(ctx->leaf_ids),
+        const size_t sm = (size_t)P2M_WARPS * p2m_smem_doubles(ctx->P) * 8;
+        if (sm > 48 * 1024)
+            cudaFuncSetAttribute(k_p2m<Body, NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_p2m<Body, NI><<<std::max(g, 1), P2M_WARPS * 32, sm, s>>>(P_<Body>(ctx->body), P_<uint32_t>(ctx->leaf_ids),
                                                                  ctx->nleaf, P_<uint32_t>(ctx->c_bb),
                                                                  P_<uint32_t>(ctx->c_bc), P_<double4>(ctx->c_cr),
                                                                  ctx->P, ctx->ncoef, M);
