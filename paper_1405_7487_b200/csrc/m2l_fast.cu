@@ -652,7 +652,8 @@ __global__ void __launch_bounds__(128, 2)
     k_m2l_mir(int64_t ncell, const uint32_t* __restrict__ src, const uint64_t* __restrict__ offs,
               const double4* __restrict__ cr, const int* __restrict__ sexp, const float4* __restrict__ Sv,
               double* __restrict__ Lr, unsigned long long* __restrict__ counter,
-              const uint8_t* __restrict__ mixed, int64_t lay) {
+              const uint8_t* __restrict__ mixed, int64_t lay, const uint32_t* __restrict__ tlist = nullptr,
+              const unsigned long long* __restrict__ tcount = nullptr) {
     using K = L<P>;
     constexpr int NCH = K::NCH;
     const int lane = threadIdx.x & 31;
@@ -670,14 +671,18 @@ __global__ void __launch_bounds__(128, 2)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(se_), "l"(sexp + bn) : "memory");
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
+    // work: every target (skipping the other kernel's), or the listed ones (tlist: the scaled
+    // kernel after k_m2l_mixed)
+    const long long nwork = tlist ? (long long)*tcount : (long long)ncell;
     for (;;) {
         unsigned long long an = 0;
         if (lane == 0) an = atomicAdd(counter, 1ull);
-        const long long a = (long long)__shfl_sync(0xffffffffu, an, 0);
-        if (a >= ncell) break;
+        const long long wi = (long long)__shfl_sync(0xffffffffu, an, 0);
+        if (wi >= nwork) break;
+        const long long a = tlist ? (long long)tlist[wi] : wi;
         const uint64_t p0 = offs[a], p1 = offs[a + 1];
         if (p0 == p1) continue;
-        if (mixed && (mixed[a] != 0) != SC) continue;   // the other kernel's target
+        if (!tlist && mixed && (mixed[a] != 0) != SC) continue;   // the other kernel's target
         const double4 ca = cr[a];
         const int ea = sexp[a];
         const double sa = exp2((double)-ea);   // 1/rho_A, exact
@@ -786,13 +791,14 @@ __global__ void __launch_bounds__(128, 2)
 }
 
 // mixed[a] = 1 iff target a's M2L list holds a source more than one level away (no prepared
-// operand copy at that scale).  Local cells are level-ordered, so a local source is within one
+// operand copy at that scale); those targets are also listed (any order) for the scaled kernel.  Local cells are level-ordered, so a local source is within one
 // level of a iff its index lies in lvl[level(a) - 1] .. lvl[level(a) + 2] (no gather); grafted
 // LET cells (index >= nloc) compare their exponents.  Warp per target.
 __global__ void k_m2l_mixed(int64_t ncell, int64_t nloc, const uint32_t* __restrict__ src,
                             const uint64_t* __restrict__ offs, const int32_t* __restrict__ level,
                             const int64_t* __restrict__ lvl, int nlvl, const int* __restrict__ sexp,
-                            uint8_t* __restrict__ mixed) {
+                            uint8_t* __restrict__ mixed, uint32_t* __restrict__ mlist,
+                            unsigned long long* __restrict__ mcount) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t a = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); a < ncell; a += nw) {
@@ -807,7 +813,10 @@ __global__ void k_m2l_mixed(int64_t ncell, int64_t nloc, const uint32_t* __restr
             mix |= b < nloc ? (b < lo || b >= hi) : abs(sexp[b] - ea) > 1;
         }
         mix = __any_sync(0xffffffffu, mix);
-        if (lane == 0) mixed[a] = mix ? 1 : 0;
+        if (lane == 0) {
+            mixed[a] = mix ? 1 : 0;
+            if (mix) mlist[atomicAdd(mcount, 1ull)] = (uint32_t)a;   // the scaled kernel's work list
+        }
     }
 }
 
@@ -909,23 +918,24 @@ fmm_status m2l_mir_t(fmm_ctx* ctx, cudaStream_t s) {
         // (level ranges only when they describe these cells; else every target counts as mixed)
         const bool ranges = ctx->level_begin.size() >= 2 && ctx->level_begin.back() == ctx->ncell;
         const int nlvl = ranges ? (int)ctx->level_begin.size() : 0;
-        FMM_TRY(buf_ensure(ctx, ctx->m2l_mix, (size_t)nlvl * 8 + (size_t)nc + 64));
+        FMM_TRY(buf_ensure(ctx, ctx->m2l_mix, (size_t)nlvl * 8 + (size_t)nc * 4 + (size_t)nc + 64));
         int64_t* lvl = P_<int64_t>(ctx->m2l_mix);
-        uint8_t* mixed = reinterpret_cast<uint8_t*>(lvl + nlvl);
+        uint32_t* mlist = reinterpret_cast<uint32_t*>(lvl + nlvl);
+        uint8_t* mixed = reinterpret_cast<uint8_t*>(mlist + nc);
         if (nlvl > 0)   // pageable source: staged at the call, ordered on s
             FMM_CUDA_TRY(ctx, cudaMemcpyAsync(lvl, ctx->level_begin.data(), (size_t)nlvl * 8, cudaMemcpyHostToDevice, s));
+        FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 24, s));   // two work counters + the list length
         mir::k_m2l_mixed<<<std::max(g, 1), nw * 32, 0, s>>>(nc, ctx->ncell, P_<uint32_t>(ctx->m2l_src),
                                                             P_<uint64_t>(ctx->m2l_off), P_<int32_t>(ctx->c_level), lvl,
-                                                            nlvl, sexp, mixed);
+                                                            nlvl, sexp, mixed, mlist, counter + 2);
         FMM_LAUNCH(ctx);
-        FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 16, s));
         mir::k_m2l_mir<P, false><<<ctx->num_sms * 2, 128, 0, s>>>(
             nc, P_<uint32_t>(ctx->m2l_src), P_<uint64_t>(ctx->m2l_off), P_<double4>(ctx->c_cr), sexp,
             reinterpret_cast<const float4*>(Sv), P_<double>(ctx->Lr), counter, mixed, lay);
         FMM_LAUNCH(ctx);
         mir::k_m2l_mir<P, true><<<ctx->num_sms * 2, 128, 0, s>>>(
             nc, P_<uint32_t>(ctx->m2l_src), P_<uint64_t>(ctx->m2l_off), P_<double4>(ctx->c_cr), sexp,
-            reinterpret_cast<const float4*>(Sv), P_<double>(ctx->Lr), counter + 1, mixed, lay);
+            reinterpret_cast<const float4*>(Sv), P_<double>(ctx->Lr), counter + 1, mixed, lay, mlist, counter + 2);
         FMM_LAUNCH(ctx);
     }
     if (!ctx->m2l_no_expand) {
