@@ -768,25 +768,65 @@ __global__ void __launch_bounds__(128, 2)
         }
         // warp reduction in fp64; reduced L_hat in (L0 | L1) t2 order for k_l_expand
         constexpr int N0 = P * (P + 1) / 2;
-        sfor<0, K::NL>([&](auto kk) {
+        auto val = [&](auto kk) -> float {   // this lane's partial sum of reduced index k
             constexpr int k = decltype(kk)::value;
             constexpr int x1 = k >= N0, e = x1 ? k - N0 : k;
             constexpr int n = deg2(e), z = zof(e), y = n - z;
-            float f;
             if constexpr (!x1) {
-                if constexpr (y > z) f = R.L0p[off(y, z)].x;
-                else if constexpr (y < z) f = R.L0p[off(z, y)].y;
-                else f = R.L0d[y].x + R.L0d[y].y;
+                if constexpr (y > z) return R.L0p[off(y, z)].x;
+                else if constexpr (y < z) return R.L0p[off(z, y)].y;
+                else return R.L0d[y].x + R.L0d[y].y;
             } else {
-                if constexpr (y > z) f = R.L1p[off(y, z)].x;
-                else if constexpr (y < z) f = R.L1p[off(z, y)].y;
-                else f = R.L1d[y].x + R.L1d[y].y;
+                if constexpr (y > z) return R.L1p[off(y, z)].x;
+                else if constexpr (y < z) return R.L1p[off(z, y)].y;
+                else return R.L1d[y].x + R.L1d[y].y;
             }
-            double v = (double)f;
+        };
+        if constexpr (K::NL <= 128) {
+            // reduce-scatter over the NLP (padded: 32, 64 or 128) values: each xor stage keeps the
+            // half of the block this lane's bit selects and adds the partner's copy of it, so
+            // lane l ends with the totals of k = Q l .. Q l + Q-1, Q = NLP / 32 (~1/5 of the
+            // shuffles of one butterfly per value)
+            constexpr int NLP = K::NL <= 32 ? 32 : (K::NL <= 64 ? 64 : 128), Q = NLP / 32;
+            double v1[NLP / 2], v2[NLP / 4], v3[NLP / 8], v4[NLP / 16], v5[Q];
+            const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
+            sfor<0, NLP / 2>([&](auto jj) {
+                constexpr int j = decltype(jj)::value;
+                double lo = 0.0, hi = 0.0;
+                if constexpr (j < K::NL) lo = (double)val(std::integral_constant<int, j>{});
+                if constexpr (j + NLP / 2 < K::NL) hi = (double)val(std::integral_constant<int, j + NLP / 2>{});
+                v1[j] = (b4 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b4 ? lo : hi, 16);
+            });
+            sfor<0, NLP / 4>([&](auto jj) {
+                constexpr int j = decltype(jj)::value, h = NLP / 4;
+                v2[j] = (b3 ? v1[j + h] : v1[j]) + __shfl_xor_sync(0xffffffffu, b3 ? v1[j] : v1[j + h], 8);
+            });
+            sfor<0, NLP / 8>([&](auto jj) {
+                constexpr int j = decltype(jj)::value, h = NLP / 8;
+                v3[j] = (b2 ? v2[j + h] : v2[j]) + __shfl_xor_sync(0xffffffffu, b2 ? v2[j] : v2[j + h], 4);
+            });
+            sfor<0, NLP / 16>([&](auto jj) {
+                constexpr int j = decltype(jj)::value, h = NLP / 16;
+                v4[j] = (b1 ? v3[j + h] : v3[j]) + __shfl_xor_sync(0xffffffffu, b1 ? v3[j] : v3[j + h], 2);
+            });
+            sfor<0, Q>([&](auto jj) {
+                constexpr int j = decltype(jj)::value;
+                v5[j] = (b0 ? v4[j + Q] : v4[j]) + __shfl_xor_sync(0xffffffffu, b0 ? v4[j] : v4[j + Q], 1);
+            });
 #pragma unroll
-            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == (k & 31)) Lr[(size_t)a * K::NL + k] = v;
-        });
+            for (int j = 0; j < Q; ++j) {
+                const int k = Q * lane + j;
+                if (k < K::NL) Lr[(size_t)a * K::NL + k] = v5[j];
+            }
+        } else {
+            sfor<0, K::NL>([&](auto kk) {
+                constexpr int k = decltype(kk)::value;
+                double v = (double)val(kk);
+#pragma unroll
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == (k & 31)) Lr[(size_t)a * K::NL + k] = v;
+            });
+        }
     }
 }
 
