@@ -831,9 +831,11 @@ __global__ void __launch_bounds__(128, 2)
 }
 
 // mixed[a] = 1 iff target a's M2L list holds a source more than one level away (no prepared
-// operand copy at that scale); those targets are also listed (any order) for the scaled kernel.  Local cells are level-ordered, so a local source is within one
-// level of a iff its index lies in lvl[level(a) - 1] .. lvl[level(a) + 2] (no gather); grafted
-// LET cells (index >= nloc) compare their exponents.  Warp per target.
+// operand copy at that scale); those targets are also listed (any order) for the scaled kernel.
+// Local cells are level-ordered, so a local source is within one level of a iff its index lies
+// in lvl[level(a) - 1] .. lvl[level(a) + 2] (no gather); grafted LET cells (index >= nloc), and
+// every cell of a caller-supplied tree without level ranges (fmm_debug_m2l), compare exponents.
+// Warp per target.
 __global__ void k_m2l_mixed(int64_t ncell, int64_t nloc, const uint32_t* __restrict__ src,
                             const uint64_t* __restrict__ offs, const int32_t* __restrict__ level,
                             const int64_t* __restrict__ lvl, int nlvl, const int* __restrict__ sexp,
@@ -844,13 +846,14 @@ __global__ void k_m2l_mixed(int64_t ncell, int64_t nloc, const uint32_t* __restr
     for (int64_t a = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); a < ncell; a += nw) {
         const uint64_t p0 = offs[a], p1 = offs[a + 1];
         const int la = level[a];
-        const bool ok = la + 1 < nlvl;
-        const int64_t lo = ok ? lvl[max(la - 1, 0)] : 0, hi = ok ? lvl[min(la + 2, nlvl - 1)] : -1;
+        const bool ok = la + 1 < nlvl;   // level ranges describe the local cells
+        const int64_t lo = ok ? lvl[max(la - 1, 0)] : 0, hi = ok ? lvl[min(la + 2, nlvl - 1)] : 0;
+        const int64_t nl = ok ? nloc : 0;
         const int ea = sexp[a];
         bool mix = false;
         for (uint64_t p = p0 + lane; p < p1; p += 32) {
             const int64_t b = src[p];
-            mix |= b < nloc ? (b < lo || b >= hi) : abs(sexp[b] - ea) > 1;
+            mix |= b < nl ? (b < lo || b >= hi) : abs(sexp[b] - ea) > 1;
         }
         mix = __any_sync(0xffffffffu, mix);
         if (lane == 0) {
@@ -955,7 +958,7 @@ fmm_status m2l_mir_t(fmm_ctx* ctx, cudaStream_t s) {
         PhaseScope ps(ctx, PH_M2L_KERNEL, s);
         // split the targets by whether every source is within one level: those run the kernel
         // without scaling code, the others the scaled kernel (a uniform tree: none of them)
-        // (level ranges only when they describe these cells; else every target counts as mixed)
+        // (level ranges only when they describe these cells; else the exponents are compared)
         const bool ranges = ctx->level_begin.size() >= 2 && ctx->level_begin.back() == ctx->ncell;
         const int nlvl = ranges ? (int)ctx->level_begin.size() : 0;
         FMM_TRY(buf_ensure(ctx, ctx->m2l_mix, (size_t)nlvl * 8 + (size_t)nc * 4 + (size_t)nc + 64));
