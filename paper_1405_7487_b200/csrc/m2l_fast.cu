@@ -344,14 +344,46 @@ __global__ void k_m2l_prep_table(int64_t c0, int64_t ncell, int ncoef, int NSP, 
     }
 }
 
-// reduced, scaled L_hat -> full fp64 L (R11 order) by harmonicity, zero for cells without M2L
+// reduced, scaled L_hat -> full fp64 L (R11 order) by harmonicity, zero for cells without M2L.
+// The index maps are decoded once per block into shared tables (per element before: a search
+// loop for the degree and a cidx per term, ~8x the kernel's memory time):
+//   t_red[i] = {cidx of reduced entry i, its scale degree ax+m+1}, i < P^2 (L0 | L1, t2 order);
+//   t_fill[j] = {dst, src1, src2}: L[ax,y,z] = -L[ax-2,y+2,z] - L[ax-2,y,z+2], ax = 2..P-1 in order,
+//   with fill_off[ax] the first entry of level ax.
 __global__ void k_l_expand(int64_t ncell, int P, int ncoef, const uint64_t* __restrict__ off,
                            const uint64_t* __restrict__ off2, const int* __restrict__ sexp,
                            const double* __restrict__ Lr, double* __restrict__ L) {
     extern __shared__ double s_L[];
+    __shared__ ushort2 t_red[FMM_MAXP * FMM_MAXP];
+    __shared__ ushort4 t_fill[816];
+    __shared__ int fill_off[FMM_MAXP + 1];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    double* Lf = s_L + (size_t)w * ncoef;
     const int N0 = P * (P + 1) / 2, NL = P * P;
+    for (int i = threadIdx.x; i < NL; i += blockDim.x) {
+        const int ax = i < N0 ? 0 : 1, ii = i < N0 ? i : i - N0;
+        int m = 0;
+        while ((m + 1) * (m + 2) / 2 <= ii) ++m;
+        const int z = ii - m * (m + 1) / 2, y = m - z;
+        t_red[i] = make_ushort2((unsigned short)cidx(ax, y, z), (unsigned short)(ax + m + 1));
+    }
+    if (threadIdx.x < FMM_MAXP + 1) {   // level ax starts after sum_{a=2}^{ax-1} (P-a)(P-a+1)/2 entries
+        int o = 0;
+        for (int a2 = 2; a2 < (int)threadIdx.x && a2 < P; ++a2) o += (P - a2) * (P - a2 + 1) / 2;
+        fill_off[threadIdx.x] = o;
+    }
+    __syncthreads();
+    for (int ax = 2; ax < P; ++ax) {
+        const int cnt = (P - ax) * (P - ax + 1) / 2, o = fill_off[ax];
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            int m = 0;
+            while ((m + 1) * (m + 2) / 2 <= i) ++m;
+            const int z = i - m * (m + 1) / 2, y = m - z;
+            t_fill[o + i] = make_ushort4((unsigned short)cidx(ax, y, z), (unsigned short)cidx(ax - 2, y + 2, z),
+                                         (unsigned short)cidx(ax - 2, y, z + 2), 0);
+        }
+    }
+    __syncthreads();
+    double* Lf = s_L + (size_t)w * ncoef;
     for (int64_t c = (int64_t)blockIdx.x * nw + w; c < ncell; c += (int64_t)gridDim.x * nw) {
         double* out = L + (size_t)c * ncoef;
         if (off[c] == off[c + 1] && (!off2 || off2[c] == off2[c + 1])) {   // no list (local or remote)
@@ -360,19 +392,15 @@ __global__ void k_l_expand(int64_t ncell, int P, int ncoef, const uint64_t* __re
         }
         const int e = sexp[c];
         for (int i = lane; i < NL; i += 32) {
-            int ax = i < N0 ? 0 : 1, ii = i < N0 ? i : i - N0, m = 0;
-            while ((m + 1) * (m + 2) / 2 <= ii) ++m;
-            int z = ii - m * (m + 1) / 2, y = m - z;
-            Lf[cidx(ax, y, z)] = ldexp(Lr[(size_t)c * NL + i], -e * (ax + m + 1));
+            const ushort2 t = t_red[i];
+            Lf[t.x] = ldexp(Lr[(size_t)c * NL + i], -e * (int)t.y);
         }
         __syncwarp();
         for (int ax = 2; ax < P; ++ax) {
-            int cnt = (P - ax) * (P - ax + 1) / 2;
+            const int o0 = fill_off[ax], cnt = (P - ax) * (P - ax + 1) / 2;
             for (int i = lane; i < cnt; i += 32) {
-                int m = 0;
-                while ((m + 1) * (m + 2) / 2 <= i) ++m;
-                int z = i - m * (m + 1) / 2, y = m - z;
-                Lf[cidx(ax, y, z)] = -Lf[cidx(ax - 2, y + 2, z)] - Lf[cidx(ax - 2, y, z + 2)];
+                const ushort4 t = t_fill[o0 + i];
+                Lf[t.x] = -Lf[t.y] - Lf[t.z];
             }
             __syncwarp();
         }
