@@ -18,16 +18,21 @@ __constant__ double c_inv[FMM_MAXP + 1] = {0.0,       1.0,        1.0 / 2,  1.0 
                                            1.0 / 12,  1.0 / 13,   1.0 / 14, 1.0 / 15, 1.0 / 16};
 
 // separable 1D "down" shift along axis ax: out_alpha = sum_{k <= P-1-|alpha|} in_{alpha + k e_ax} t[k]
+// The source index starts at cidx(alpha) = kk and is stepped as a_ax grows (cidx = n(n+1)(n+2)/6 +
+// m(m+1)/2 + c: +(n+1)(n+2)/2, plus m+1 on the y and z axes, plus 1 on z) -- the same terms in
+// the same order as a cidx per term (upward.cu's shift_pass_up does the same).
 __device__ __forceinline__ void shift_pass_down(const uchar4* __restrict__ ex, int ncoef, int P, int ax,
                                                 const double* in, double* out, const double* t, int lane) {
     for (int kk = lane; kk < ncoef; kk += 32) {
         const uchar4 e = ex[kk];
-        int a[3] = {e.x, e.y, e.z};
-        const int base = a[ax], top = P - 1 - e.w;
+        const int top = P - 1 - e.w;
+        int n = e.w, m = e.y + e.z, idx = kk;
         double s = 0.0;
         for (int k = 0; k <= top; ++k) {
-            a[ax] = base + k;
-            s += in[cidx(a[0], a[1], a[2])] * t[k];
+            s += in[idx] * t[k];
+            idx += (n + 1) * (n + 2) / 2 + (ax == 0 ? 0 : m + 1) + (ax == 2 ? 1 : 0);
+            ++n;
+            if (ax != 0) ++m;
         }
         out[kk] = s;
     }

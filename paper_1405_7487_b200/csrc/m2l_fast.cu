@@ -313,14 +313,32 @@ FoldTable build_fold_table(int P, int NS, int NSP) {
     return t;
 }
 
+// 2^k as a double for |k| <= 1000 (exponent bits), else ldexp's general path
+__device__ __forceinline__ double scale2(double v, int k) {
+    return (k >= -1000 && k <= 1000) ? v * __longlong_as_double((long long)(k + 1023) << 52) : ldexp(v, k);
+}
+
+// the fold table (nt terms) is copied to shared memory once per block: every output entry reads
+// its terms there instead of through L1 per cell
 template <typename R>
 __global__ void k_m2l_prep_table(int64_t c0, int64_t ncell, int ncoef, int NSP, const int* __restrict__ toff,
                                  const int* __restrict__ tk, const double* __restrict__ tw,
                                  const int* __restrict__ tdg, const double* __restrict__ M,
                                  const int32_t* __restrict__ level, const double* __restrict__ root,
-                                 int* __restrict__ sexp, R* __restrict__ Sv, int64_t copy_stride = 0) {
+                                 int* __restrict__ sexp, R* __restrict__ Sv, int64_t copy_stride, int nt) {
     extern __shared__ double s_M[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double* s_tw = s_M + (size_t)nw * ncoef;
+    int* s_tk = reinterpret_cast<int*>(s_tw + nt);
+    int* s_toff = s_tk + nt;
+    int* s_tdg = s_toff + NSP + 1;
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+        s_tw[i] = tw[i];
+        s_tk[i] = tk[i];
+    }
+    for (int i = threadIdx.x; i <= NSP; i += blockDim.x) s_toff[i] = toff[i];
+    for (int i = threadIdx.x; i < NSP; i += blockDim.x) s_tdg[i] = tdg[i];
+    __syncthreads();
     double* Mw = s_M + (size_t)w * ncoef;
     int E;
     frexp(2.0 * root[10], &E);
@@ -332,12 +350,12 @@ __global__ void k_m2l_prep_table(int64_t c0, int64_t ncell, int ncoef, int NSP, 
         R* out = Sv + (size_t)c * NSP;
         for (int i = lane; i < NSP; i += 32) {
             double v = 0.0;
-            for (int t = toff[i]; t < toff[i + 1]; ++t) v += tw[t] * Mw[tk[t]];
-            const int dg = tdg[i];
-            out[i] = dg < 0 ? R(0) : (R)ldexp(v, -e * dg);
+            for (int t = s_toff[i]; t < s_toff[i + 1]; ++t) v += s_tw[t] * Mw[s_tk[t]];
+            const int dg = s_tdg[i];
+            out[i] = dg < 0 ? R(0) : (R)scale2(v, -e * dg);
             if (copy_stride) {   // the operand as the pair scaling 2^(de dg) leaves it, de = -1 and +1
-                out[i - copy_stride] = dg < 0 ? R(0) : (R)ldexp(v, -(e + 1) * dg);
-                out[i + copy_stride] = dg < 0 ? R(0) : (R)ldexp(v, -(e - 1) * dg);
+                out[i - copy_stride] = dg < 0 ? R(0) : (R)scale2(v, -(e + 1) * dg);
+                out[i + copy_stride] = dg < 0 ? R(0) : (R)scale2(v, -(e - 1) * dg);
             }
         }
         __syncwarp();
@@ -442,11 +460,14 @@ fmm_status m2l_fast_t(fmm_ctx* ctx, cudaStream_t s) {
     if (ctx->m2l_part != 2) {
         char* b = (char*)ctx->fold_tab.p;
         const size_t nt = (size_t)ctx->fold_nt;
-        k_m2l_prep_table<R><<<std::max(gp, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
+        const size_t psm = (size_t)nw * ctx->ncoef * 8 + nt * 12 + (size_t)(2 * NSP + 1) * 4;
+        if (psm > 48 * 1024)
+            FMM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_m2l_prep_table<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+        k_m2l_prep_table<R><<<std::max(gp, 1), nw * 32, psm, s>>>(
             c0, nct, ctx->ncoef, NSP, reinterpret_cast<const int*>(b + nt * 8),
             reinterpret_cast<const int*>(b + nt * 8 + (2 * NSP + 1) * 4), reinterpret_cast<const double*>(b),
             reinterpret_cast<const int*>(b + nt * 8 + (NSP + 1) * 4), P_<double>(ctx->M), P_<int32_t>(ctx->c_level),
-            P_<double>(ctx->root), sexp, Sv);
+            P_<double>(ctx->root), sexp, Sv, (int64_t)0, (int)nt);
         FMM_LAUNCH(ctx);
     }
     if (ctx->m2l_part == 1) return FMM_OK;
@@ -973,11 +994,14 @@ fmm_status m2l_mir_t(fmm_ctx* ctx, cudaStream_t s) {
     if (ctx->m2l_part != 2) {
         char* b = (char*)ctx->fold_tab.p;
         const size_t nt = (size_t)ctx->fold_nt;
-        k_m2l_prep_table<float><<<std::max(gp, 1), nw * 32, (size_t)nw * ctx->ncoef * 8, s>>>(
+        const size_t psm = (size_t)nw * ctx->ncoef * 8 + nt * 12 + (size_t)(2 * NSP + 1) * 4;
+        if (psm > 48 * 1024)
+            FMM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_m2l_prep_table<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+        k_m2l_prep_table<float><<<std::max(gp, 1), nw * 32, psm, s>>>(
             c0, nct, ctx->ncoef, NSP, reinterpret_cast<const int*>(b + nt * 8),
             reinterpret_cast<const int*>(b + nt * 8 + (2 * NSP + 1) * 4), reinterpret_cast<const double*>(b),
             reinterpret_cast<const int*>(b + nt * 8 + (NSP + 1) * 4), P_<double>(ctx->M), P_<int32_t>(ctx->c_level),
-            P_<double>(ctx->root), sexp, Sv, (int64_t)lstride);
+            P_<double>(ctx->root), sexp, Sv, (int64_t)lstride, (int)nt);
         FMM_LAUNCH(ctx);
     }
     if (ctx->m2l_part == 1) return FMM_OK;   // operand preparation only (fmm_solve: aux stream)
