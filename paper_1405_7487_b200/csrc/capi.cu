@@ -148,6 +148,8 @@ fmm_status fmm_create(int64_t n_max, int p, double theta, int ncrit, int prec, i
         ctx->tc_tight = g18 && g18[0] == '1';
         const char* g21 = getenv("FMM_TREE_FAST");
         ctx->tree_fast = !(g21 && g21[0] == '0');
+        const char* g22 = getenv("FMM_SORT_STAGED");
+        ctx->sort_staged = g22 ? atoi(g22) : -1;
         const char* g15 = getenv("FMM_DTT");
         ctx->dtt_mode = (g15 && std::string(g15) == "bfs") ? 1 : 0;
         const char* g7 = getenv("FMM_LIST_SORT");

@@ -165,6 +165,7 @@ struct fmm_ctx {
     DevBuf split_tmp, split_cnt;       // per-level temporaries
     DevBuf tree_lb;                    // sync-free build: level starts + overflow flag (device)
     bool tree_fast = true;             // levels from the previous build's sizes (FMM_TREE_FAST=0: off)
+    int sort_staged = -1;              // onesweep pass: -1 staged above one wave of tiles, 0 direct, 1 staged
     int64_t tree_prev_depth = -1, tree_prev_ncell = 0, tree_prev_maxw = 0;
     DevBuf leaf_ids;                   // u32 list of leaf cells
 

@@ -96,6 +96,20 @@ __global__ void __launch_bounds__(RS_THREADS) k_scatter(const uint64_t* __restri
 }
 
 // ---- onesweep
+// Staged pass: the tile is copied into shared memory by cp.async (all of a warp's copies in
+// flight at once) and ranked from there, which frees the registers the direct pass holds its
+// loads in (80 instead of ~120: 3 CTAs per SM instead of 2).  Measured at 2^26 keys: loads alone
+// staged at 2 CTAs per SM were slower than the direct pass (10.8 vs 10.2 ms for 8 passes); the
+// third CTA is what pays (8.3 ms).
+__device__ __forceinline__ void cp_async_8(void* smem, const void* gmem) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(a), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_4(void* smem, const void* gmem) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(a), "l"(gmem) : "memory");
+}
+
 constexpr uint32_t OS_FA = 1u << 30;         // status: tile aggregate published
 constexpr uint32_t OS_FP = 2u << 30;         // status: inclusive prefix published
 constexpr uint32_t OS_VAL = OS_FA - 1u;
@@ -162,7 +176,134 @@ __global__ void __launch_bounds__(RS_BINS) k_os_base(uint32_t* __restrict__ hist
 }
 
 template <bool HAS_VAL>
-__global__ void __launch_bounds__(RS_THREADS) k_os_pass(const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
+__global__ void __launch_bounds__(RS_THREADS, 3) k_os_pass_staged(const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
+                                                        const uint32_t* __restrict__ vin, uint32_t* __restrict__ vout,
+                                                        int64_t n, int shift, const uint32_t* __restrict__ base,
+                                                        uint32_t* __restrict__ status, uint32_t* __restrict__ tile_ctr) {
+    extern __shared__ __align__(16) uint64_t s_k[];   // [RS_TILE] keys, then [RS_TILE] values
+    uint32_t* s_v = reinterpret_cast<uint32_t*>(s_k + RS_TILE);
+    __shared__ uint32_t s_whist[RS_WARPS][RS_BINS];
+    __shared__ uint32_t s_off[RS_BINS], s_lbase[RS_BINS], s_wsum[RS_WARPS];
+    __shared__ uint32_t s_tile;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int b = lane; b < RS_BINS; b += 32) s_whist[w][b] = 0;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    // warp w ranks the contiguous sub-tile [tile*TILE + w*512, +512) in index order (stable)
+    const int64_t b0 = (int64_t)tile * RS_TILE + (int64_t)w * (RS_ITEMS * 32);
+    uint64_t k[RS_ITEMS];
+    uint32_t v[RS_ITEMS];
+    uint32_t pos[RS_ITEMS / 2];   // two 16-bit warp-local ranks per word (0xFFFF: no key)
+    const unsigned lt = (1u << lane) - 1u;
+    // the warp's sub-tile lands in its own slots of s_k / s_v (each lane reads back what it
+    // copied, so waiting for its own copies is enough); the scatter reuses the buffers after the
+    // block barrier that ends the ranking
+    const int sl = w * (RS_ITEMS * 32) + lane;
+#pragma unroll
+    for (int i = 0; i < RS_ITEMS; ++i) {
+        const int64_t j = b0 + i * 32 + lane;
+        if (j < n) {
+            cp_async_8(s_k + sl + i * 32, kin + j);
+            if (HAS_VAL) cp_async_4(s_v + sl + i * 32, vin + j);
+        }
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < RS_ITEMS; ++i) {
+        const int64_t j = b0 + i * 32 + lane;
+        const bool ok = j < n;
+        k[i] = ok ? s_k[sl + i * 32] : 0ull;
+        if (HAS_VAL) v[i] = ok ? s_v[sl + i * 32] : 0u;
+        const uint32_t d = ok ? (uint32_t)((k[i] >> shift) & 0xFF) : 0x100u;
+        const unsigned peers = match_digit<9>(d, 0xffffffffu);
+        const uint32_t rank = __popc(peers & lt);
+        const uint32_t before = (d < 0x100u) ? s_whist[w][d] : 0u;
+        __syncwarp();
+        if ((peers & lt) == 0 && d < 0x100u) s_whist[w][d] = before + __popc(peers);
+        __syncwarp();
+        const uint32_t r16 = ok ? before + rank : 0xFFFFu;
+        if (i & 1) pos[i >> 1] |= r16 << 16;
+        else pos[i >> 1] = r16;
+    }
+    __syncthreads();
+    uint32_t run = 0;   // thread t owns bin t: exclusive prefix over warps, tile total in run
+#pragma unroll
+    for (int ww = 0; ww < RS_WARPS; ++ww) {
+        const uint32_t c = s_whist[ww][threadIdx.x];
+        s_whist[ww][threadIdx.x] = run;
+        run += c;
+    }
+    // decoupled look-back over the earlier tiles' status words of this bin
+    volatile uint32_t* st = status + (size_t)tile * RS_BINS + threadIdx.x;
+    uint32_t excl = 0;
+    if (tile == 0) {
+        *st = OS_FP | run;
+    } else {
+        *st = OS_FA | run;
+        // windows of LB earlier tiles read at once (independent loads), newest first; an
+        // unpublished word restarts the window there
+        constexpr int LB = 16;
+        int64_t j = (int64_t)tile - 1;
+        bool done = false;
+        while (!done) {
+            uint32_t xs[LB];
+#pragma unroll
+            for (int u = 0; u < LB; ++u)
+                xs[u] = j - u >= 0 ? ((volatile uint32_t*)status)[(size_t)(j - u) * RS_BINS + threadIdx.x] : 0x80000000u;   // before tile 0: "prefix 0"
+#pragma unroll
+            for (int u = 0; u < LB; ++u) {
+                if (done) break;
+                const uint32_t x = xs[u];
+                if (!(x & (OS_FA | OS_FP))) break;   // tile j - u not published yet: re-read from it
+                excl += x & OS_VAL;
+                if (x & OS_FP) done = true;
+                --j;
+            }
+        }
+        *st = OS_FP | (excl + run);
+    }
+    // tile-local bin starts (exclusive scan of the tile's bin counts)
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[w] = x;
+    __syncthreads();
+    uint32_t pre = 0;
+    for (int i = 0; i < w; ++i) pre += s_wsum[i];
+    const uint32_t lb = pre + x - run;
+    s_lbase[threadIdx.x] = lb;
+    s_off[threadIdx.x] = base[threadIdx.x] + excl - lb;   // global = s_off[d] + tile-local index
+    __syncthreads();
+    // keys in digit order inside the tile, then written out so that consecutive threads write
+    // consecutive addresses of a bin
+#pragma unroll
+    for (int i = 0; i < RS_ITEMS; ++i) {
+        const uint32_t r16 = (pos[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
+        if (r16 == 0xFFFFu) continue;
+        const uint32_t d = (uint32_t)(k[i] >> shift) & 0xFF;
+        const uint32_t lp = s_lbase[d] + s_whist[w][d] + r16;
+        s_k[lp] = k[i];
+        if (HAS_VAL) s_v[lp] = v[i];
+    }
+    __syncthreads();
+    const int cnt = (int)min((int64_t)RS_TILE, n - (int64_t)tile * RS_TILE);
+    for (int i = threadIdx.x; i < cnt; i += RS_THREADS) {
+        const uint64_t kk = s_k[i];
+        const uint32_t dst = s_off[(uint32_t)(kk >> shift) & 0xFF] + (uint32_t)i;
+        kout[dst] = kk;
+        if (HAS_VAL) vout[dst] = s_v[i];
+    }
+}
+
+// the same pass with the keys loaded straight into registers (loads interleaved with the
+// ranking, ~120 registers, 2 CTAs per SM): lower latency per tile, so it wins while the tiles
+// fit in one wave of the staged kernel's 3 CTAs per SM (c2: 256 tiles, 0.210 vs 0.224 ms)
+template <bool HAS_VAL>
+__global__ void __launch_bounds__(RS_THREADS) k_os_pass_direct(const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
                                                         const uint32_t* __restrict__ vin, uint32_t* __restrict__ vout,
                                                         int64_t n, int shift, const uint32_t* __restrict__ base,
                                                         uint32_t* __restrict__ status, uint32_t* __restrict__ tile_ctr) {
@@ -339,11 +480,18 @@ fmm_status radix_sort_impl(fmm_ctx* ctx, uint64_t* k0, uint64_t* k1, uint32_t* v
         k_os_base<<<sh.n, RS_BINS, 0, s>>>(hist);
         FMM_LAUNCH(ctx);
         constexpr int smem = RS_TILE * (8 + (HAS_VAL ? 4 : 0));
-        FMM_FUNC_ATTR_ONCE(ctx, cudaFuncAttributeMaxDynamicSharedMemorySize, smem, k_os_pass<HAS_VAL>);
+        FMM_FUNC_ATTR_ONCE(ctx, cudaFuncAttributeMaxDynamicSharedMemorySize, smem, k_os_pass_staged<HAS_VAL>);
+        FMM_FUNC_ATTR_ONCE(ctx, cudaFuncAttributeMaxDynamicSharedMemorySize, smem, k_os_pass_direct<HAS_VAL>);
+        // staged tiles (3 CTAs per SM) once there is more than one wave of them (c4s: 8 passes
+        // 10.2 -> 8.3 ms); FMM_SORT_STAGED=0/1 forces either kernel
+        const bool staged = ctx->sort_staged >= 0 ? ctx->sort_staged != 0 : ntiles > (int64_t)ctx->num_sms * 3;
         for (int p = 0; p < sh.n; ++p) {
-            k_os_pass<HAS_VAL><<<(unsigned)ntiles, RS_THREADS, smem, s>>>(kin, kb, vin, vb, n, sh.s[p],
-                                                                      hist + p * RS_BINS,
-                                                                      status + (size_t)p * ntiles * RS_BINS, ctr + p);
+            if (staged)
+                k_os_pass_staged<HAS_VAL><<<(unsigned)ntiles, RS_THREADS, smem, s>>>(
+                    kin, kb, vin, vb, n, sh.s[p], hist + p * RS_BINS, status + (size_t)p * ntiles * RS_BINS, ctr + p);
+            else
+                k_os_pass_direct<HAS_VAL><<<(unsigned)ntiles, RS_THREADS, smem, s>>>(
+                    kin, kb, vin, vb, n, sh.s[p], hist + p * RS_BINS, status + (size_t)p * ntiles * RS_BINS, ctr + p);
             FMM_LAUNCH(ctx);
             std::swap(kin, kb);
             if (HAS_VAL) std::swap(vin, vb);

@@ -395,6 +395,9 @@ SWITCHES = [
     ({"FMM_DTT": "bfs", "FMM_CANONICAL_M2L": "0"}, "f32"),
     ({"FMM_DTT": "bfs", "FMM_LIST_SORT": "1"}, "f64"),
     ({"FMM_OVERLAP": "0", "FMM_P2P_GENERIC": "1", "FMM_M2L_GENERIC": "1"}, "f64"),
+    # the staged onesweep pass (default only above one wave of tiles) for the Morton pairs and,
+    # through the breadth-first lists, the keys-only sort
+    ({"FMM_SORT_STAGED": "1", "FMM_DTT": "bfs", "FMM_LIST_SORT": "1"}, "f32"),
 ]
 
 
