@@ -147,21 +147,14 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
             const unsigned bp = __ballot_sync(0xffffffffu, act && oc == 1);
             const unsigned bd = __ballot_sync(0xffffffffu, act && oc == 2);
             const unsigned bs = __ballot_sync(0xffffffffu, act && oc == 3);
-            if (act) {
-                if (oc == 0) {
-                    const uint32_t k = o.m + __popc(bm & lt);
-                    if (EMIT && (!SLAB || k < capM)) srcM[oM + k] = s;
-                } else if (oc == 1) {
-                    const uint32_t k = o.p + __popc(bp & lt);
-                    if (EMIT && (!SLAB || k < capP)) srcP[oP + k] = s;
-                } else if (oc == 2) {
-                    const uint32_t k = o.d + __popc(bd & lt);
-                    if (EMIT && (!SLAB || k < capD)) dsrc[oD + k] = s;
-                } else {
-                    const uint32_t k = nnext + __popc(bs & lt);
-                    if (k < cap) nxt[k] = s;
-                }
-            }
+            // one select chain and one (generic) store instead of four divergent branches: the
+            // lanes of a round usually hold every outcome, and SIMT ran all four paths
+            const unsigned mine = oc == 0 ? bm : oc == 1 ? bp : oc == 2 ? bd : bs;
+            const uint32_t k = (oc == 0 ? o.m : oc == 1 ? o.p : oc == 2 ? o.d : nnext) + __popc(mine & lt);
+            uint32_t* const dst = oc == 0 ? srcM + oM : oc == 1 ? srcP + oP : oc == 2 ? dsrc + oD : nxt;
+            const uint64_t lim = oc == 3 ? (uint64_t)cap : !EMIT ? 0ull : !SLAB ? ~0ull
+                                 : (uint64_t)(oc == 0 ? capM : oc == 1 ? capP : capD);
+            if (act && k < lim) dst[k] = s;
             o.m += __popc(bm);
             o.p += __popc(bp);
             o.d += __popc(bd);
