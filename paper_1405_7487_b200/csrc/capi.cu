@@ -197,7 +197,7 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
     for (DevBuf* b : bufs) buf_free(*b);
     DevBuf* tbufs[] = {&ctx->tc_cnt, &ctx->tc_voff, &ctx->tc_lb, &ctx->tc_d[0], &ctx->tc_d[1], &ctx->tc_doff[0],
                        &ctx->tc_doff[1], &ctx->tc_glob, &ctx->tc_slab, &ctx->tc_bsum, &ctx->tc_cat_off,
-                       &ctx->tc_cat_src, &ctx->tc_rec, &ctx->tree_lb};
+                       &ctx->tc_cat_src, &ctx->tc_rec, &ctx->tree_lb, &ctx->tc_mixflag};
     for (auto& pt : ctx->tc_rem) {
         DevBuf* pb[] = {&pt.off_m, &pt.src_m, &pt.off_p, &pt.src_p};
         for (DevBuf* b : pb) buf_free(*b);
@@ -241,6 +241,7 @@ fmm_status fmm_build_tree(fmm_ctx* ctx, const void* pos, int64_t n, void* stream
     cudaStream_t s = (cudaStream_t)stream;
     ctx->built = ctx->tree_built = false;
     ctx->lists_csr = false;
+    ctx->tc_mix_ncell = -1;
     ctx->tc_nrem = 0;
     ctx->evaluated = ctx->upward_done = false;
     ctx->n = n;
@@ -285,6 +286,7 @@ fmm_status fmm_dtt(fmm_ctx* ctx, int remote, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (!remote) {
         ctx->lists_csr = false;
+        ctx->tc_mix_ncell = -1;   // set again by the target-ordered traversal
         if (ctx->dtt_mode == 0) {
             PhaseScope ps(ctx, PH_DTT, s);
             FMM_TRY(tct_lists(ctx, s));

@@ -182,6 +182,8 @@ struct fmm_ctx {
     DevBuf tc_rec;                                  // per-level device records (bases, totals, maxima)
     std::vector<TcPart> tc_rem;                     // remote traversal parts (buffers reused)
     int tc_nrem = 0;                                // parts written since the last fmm_lists
+    DevBuf tc_mixflag;                              // per target: an M2L source beyond levels l-1..l+1
+    int64_t tc_mix_ncell = -1;                      // cells the flags describe (-1: none; tct_lists)
     int tc_scap = 0;                                // shared split-list capacity override (FMM_TCT_CAP, tests)
     bool tc_tight = false;                          // fast mode treats outputs as 16 entries (FMM_TCT_TIGHT, tests)
     DevBuf tc_cat_off, tc_cat_src;                  // concatenation output (swapped with the lists)

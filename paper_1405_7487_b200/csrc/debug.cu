@@ -102,6 +102,7 @@ void drop_build(fmm_ctx* ctx) {
     ctx->built = ctx->tree_built = ctx->evaluated = ctx->upward_done = false;
     ctx->built_pos = nullptr;
     ctx->lists_csr = false;
+    ctx->tc_mix_ncell = -1;     // the caller's lists: m2l_fast.cu scans them for mixed levels
     ctx->nrem = ctx->nrem_body = 0;
     ctx->let_remote.clear();
     ctx->level_begin.clear();   // the caller's cells need not be level-ordered (m2l_fast.cu: all "mixed")

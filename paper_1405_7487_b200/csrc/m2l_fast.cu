@@ -912,6 +912,17 @@ __global__ void k_m2l_mixed(int64_t ncell, int64_t nloc, const uint32_t* __restr
     }
 }
 
+// the same split from the traversal's per-target flags (tct.cu: an M2L source outside levels
+// l-1 .. l+1 of a local target) -- a pass over the cells instead of over the M2L list
+__global__ void k_m2l_mixed_flags(int64_t ncell, const uint32_t* __restrict__ flag, uint8_t* __restrict__ mixed,
+                                  uint32_t* __restrict__ mlist, unsigned long long* __restrict__ mcount) {
+    const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= ncell) return;
+    const bool mix = flag[a] != 0;
+    mixed[a] = mix ? 1 : 0;
+    if (mix) mlist[atomicAdd(mcount, 1ull)] = (uint32_t)a;   // the scaled kernel's work list
+}
+
 // operand layout of the mirror kernel as a fold table: output float i -> (kind, 2D index, degree)
 FoldTable build_fold_table_mir(int P, int NS, int NSP) {
     const int O0 = noff(P - 1), O1 = noff(P - 2 < 0 ? 0 : P - 2), G0 = ndia(P - 1), G1 = ndia(P - 2 < 0 ? 0 : P - 2);
@@ -1020,9 +1031,15 @@ fmm_status m2l_mir_t(fmm_ctx* ctx, cudaStream_t s) {
         if (nlvl > 0)   // pageable source: staged at the call, ordered on s
             FMM_CUDA_TRY(ctx, cudaMemcpyAsync(lvl, ctx->level_begin.data(), (size_t)nlvl * 8, cudaMemcpyHostToDevice, s));
         FMM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, 24, s));   // two work counters + the list length
-        mir::k_m2l_mixed<<<std::max(g, 1), nw * 32, 0, s>>>(nc, ctx->ncell, P_<uint32_t>(ctx->m2l_src),
-                                                            P_<uint64_t>(ctx->m2l_off), P_<int32_t>(ctx->c_level), lvl,
-                                                            nlvl, sexp, mixed, mlist, counter + 2);
+        if (ranges && ctx->tc_mix_ncell == nc && ctx->nrem == 0) {   // (no grafted LET sources)
+            // the target-ordered traversal flagged these targets while emitting the lists
+            mir::k_m2l_mixed_flags<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(
+                nc, P_<uint32_t>(ctx->tc_mixflag), mixed, mlist, counter + 2);
+        } else {
+            mir::k_m2l_mixed<<<std::max(g, 1), nw * 32, 0, s>>>(nc, ctx->ncell, P_<uint32_t>(ctx->m2l_src),
+                                                                P_<uint64_t>(ctx->m2l_off), P_<int32_t>(ctx->c_level),
+                                                                lvl, nlvl, sexp, mixed, mlist, counter + 2);
+        }
         FMM_LAUNCH(ctx);
         mir::k_m2l_mir<P, false><<<ctx->num_sms * 2, 128, 0, s>>>(
             nc, P_<uint32_t>(ctx->m2l_src), P_<uint64_t>(ctx->m2l_off), P_<double4>(ctx->c_cr), sexp,

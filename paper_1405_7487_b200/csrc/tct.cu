@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
     uint32_t* __restrict__ srcM, uint32_t* __restrict__ srcP, uint32_t* __restrict__ dsrc,
     uint8_t* __restrict__ ovf, uint32_t* __restrict__ ovf_list, unsigned* __restrict__ n_ovf,
     uint32_t* __restrict__ gscratch, int64_t gcap, uint32_t capM, uint32_t capP, uint32_t capD,
-    unsigned* __restrict__ err, int S, uint64_t lenM = ~0ull, uint64_t lenP = ~0ull, uint64_t lenD = ~0ull) {
+    unsigned* __restrict__ err, int S, uint64_t lenM = ~0ull, uint64_t lenP = ~0ull, uint64_t lenD = ~0ull,
+    uint32_t* __restrict__ mixflag = nullptr, int64_t band_lo = 0, int64_t band_hi = 0) {
     constexpr bool EMIT = MODE != 0, COUNT = MODE != 1, SLAB = MODE == 2;
     // an earlier level outgrew the buffers sized from the previous build: the traversal is
     // redone, so stop here instead of reading incomplete pass-down sets
@@ -138,6 +139,10 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
         }
         TcOut o{0u, 0u, 0u};
         bool over = false;
+        // an M2L source outside the levels l-1 .. l+1 (cells [band_lo, band_hi)): the target needs
+        // the M2L kernel with operand scaling (m2l_fast.cu; noted here instead of a list re-scan)
+        bool mix = false;
+        const uint32_t blo = (uint32_t)band_lo, bw = (uint32_t)(band_hi - band_lo);
         int cur = 0;
         uint32_t ncur = 0;
         uint64_t xp = x0;
@@ -155,6 +160,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
             const uint64_t lim = oc == 3 ? (uint64_t)cap : !EMIT ? 0ull : !SLAB ? ~0ull
                                  : (uint64_t)(oc == 0 ? capM : oc == 1 ? capP : capD);
             if (act && k < lim) dst[k] = s;
+            if (COUNT && mixflag) mix |= act && oc == 0 && s - blo >= bw;   // outside [blo, blo + bw)
             o.m += __popc(bm);
             o.p += __popc(bp);
             o.d += __popc(bd);
@@ -225,6 +231,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
             ncur = nnext;
         }
         if (SLAB) over |= o.m > capM || o.p > capP || o.d > capD;
+        if (COUNT && mixflag && __any_sync(0xffffffffu, mix) && lane == 0) atomicOr(mixflag + t, 1u);
         if (COUNT && lane == 0) {
             if (over && !GLOB) {
                 ovf[vi] = 1;
@@ -406,7 +413,7 @@ __global__ void k_max3(const uint32_t* __restrict__ a, const uint32_t* __restric
 // (local: the root itself; remote: the roots of grafted LETs) into the CSR lists `o`.
 fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& seeds, TcLists& o, bool single,
                    std::vector<std::array<uint32_t, 3>>& tc_max, std::vector<std::array<uint64_t, 3>>& tc_tot,
-                   bool allow_fast) {
+                   bool allow_fast, uint32_t* mixflag = nullptr) {
     const int64_t nc = ctx->ncell;
     const int nlev = (int)ctx->depth + 1;
     const Cells v{P_<double4>(ctx->c_cr), P_<uint32_t>(ctx->c_cb), P_<uint32_t>(ctx->c_cc)};
@@ -512,22 +519,28 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
         uint32_t* slabD = slabP + (size_t)nv * capP;
         unsigned* n_ovf = d_novf + l;
         unsigned* mx = d_mx + 3 * l;
+        // sources of this level's targets that need no operand scaling: levels l-1 .. l+1
+        const int64_t band_lo = ctx->level_begin[std::max(l - 1, 0)];
+        const int64_t band_hi = ctx->level_begin[std::min(l + 2, nlev)];
         FMM_CUDA_TRY(ctx, cudaMemsetAsync(ovf, 0, (size_t)nv, s));
         if (slab)
             k_tct_level<2, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds,
                                                               ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr, slabM,
                                                               slabP, slabD, ovf, ovf_list, n_ovf, nullptr, scap, capM,
-                                                              capP, capD, d_err, Sl);
+                                                              capP, capD, d_err, Sl, ~0ull, ~0ull, ~0ull, mixflag,
+                                                              band_lo, band_hi);
         else
             k_tct_level<0, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds,
                                                               ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr,
                                                               nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, nullptr,
-                                                              scap, 0, 0, 0, d_err, Sl);
+                                                              scap, 0, 0, 0, d_err, Sl, ~0ull, ~0ull, ~0ull, mixflag,
+                                                              band_lo, band_hi);
         FMM_LAUNCH(ctx);
         // overflowed targets (count read on the device: a no-op launch when there are none)
         k_tct_level<0, true><<<gwarps / TC_WARPS, TC_WARPS * 32, 0, s>>>(
             tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds, ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr,
-            nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err, Sl);
+            nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err, Sl,
+            ~0ull, ~0ull, ~0ull, mixflag, band_lo, band_hi);
         FMM_LAUNCH(ctx);
         // offsets written straight into m2l_off / p2p_off (+ the entries of earlier levels, a
         // device value) and the pass-down CSR of this level
@@ -614,13 +627,21 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
 }
 
 // local traversal: the root is the only seed; the lists land in the context's CSR arrays
+// (also flags, per target, an M2L source more than one level away: ctx->tc_mixflag, read by the
+// M2L pass instead of re-scanning the list)
 fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s) {
     TcLists o{&ctx->m2l_off, &ctx->m2l_src, &ctx->p2p_off, &ctx->p2p_src, &ctx->n_m2l, &ctx->n_p2p,
               &ctx->tc_est_m2l, &ctx->tc_est_p2p};
     const std::vector<uint32_t> seeds{0u};
-    fmm_status st = tct_run(ctx, s, seeds, o, ctx->tc_single, ctx->tc_max, ctx->tc_tot, true);
+    ctx->tc_mix_ncell = -1;
+    FMM_TRY(buf_ensure(ctx, ctx->tc_mixflag, (size_t)std::max<int64_t>(ctx->ncell, 1) * 4));
+    uint32_t* mixflag = P_<uint32_t>(ctx->tc_mixflag);
+    // (a redo after a short capacity guess revisits the same pairs: the flags are an OR)
+    FMM_CUDA_TRY(ctx, cudaMemsetAsync(mixflag, 0, (size_t)ctx->ncell * 4, s));
+    fmm_status st = tct_run(ctx, s, seeds, o, ctx->tc_single, ctx->tc_max, ctx->tc_tot, true, mixflag);
     if (st == FMM_ERR_OOM && ctx->err.empty())   // a capacity guess was short: sizes are known now
-        st = tct_run(ctx, s, seeds, o, ctx->tc_single, ctx->tc_max, ctx->tc_tot, false);
+        st = tct_run(ctx, s, seeds, o, ctx->tc_single, ctx->tc_max, ctx->tc_tot, false, mixflag);
+    if (st == FMM_OK) ctx->tc_mix_ncell = ctx->ncell;
     return st;
 }
 
