@@ -147,8 +147,15 @@ __global__ void k_gather_pos_v4(const float4* __restrict__ pos4, const uint32_t*
             if (k < n) {
                 const int64_t e = 3 * (int64_t)perm[k];   // first float of the body
                 off[u] = (int)(e & 3);
-                lo[u] = __ldg(pos4 + (e >> 2));
-                if (off[u] >= 2) hi[u] = __ldg(pos4 + (e >> 2) + 1);
+                const int64_t last4 = (e >> 2) + (off[u] >= 2);   // last float4 read
+                if (4 * last4 + 3 < 3 * n) {
+                    lo[u] = __ldg(pos4 + (e >> 2));
+                    if (off[u] >= 2) hi[u] = __ldg(pos4 + (e >> 2) + 1);
+                } else {   // the array's last floats: no read past its end
+                    const float* p = reinterpret_cast<const float*>(pos4) + e;
+                    lo[u] = make_float4(p[0], p[1], p[2], 0.f);
+                    off[u] = 0;
+                }
             }
         }
 #pragma unroll

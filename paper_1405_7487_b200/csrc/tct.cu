@@ -192,10 +192,10 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
                 const bool has = base + lane < ncur;
                 const uint32_t B = has ? sb[base + lane] : 0u;
                 uint32_t c0 = has ? v.cb[B] : 0u, nc = has ? v.cc[B] : 0u;
-                if (c0 == FMM_LET_ABSENT) {   // a grafted LET cell whose children were not exported
-                    atomicOr(err, 1u);
-                    c0 = 0u;
-                    nc = 0u;
+                if (c0 == FMM_LET_ABSENT) {   // a grafted LET cell whose children were not exported:
+                    atomicOr(err, 1u);        // the traversal fails (FMM_ERR_STATE); the root stands in
+                    c0 = 0u;                  // for the missing child so that every listed source
+                    nc = 1u;                  // owns >= 1 position (the owner arithmetic below)
                 }
                 uint32_t incl = nc;   // inclusive scan of the child counts
 #pragma unroll
@@ -204,20 +204,21 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
                     if (lane >= d) incl += y;
                 }
                 const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                const uint32_t excl = incl - nc;   // first flattened position of this lane's source
                 for (uint32_t f0 = 0; f0 < total; f0 += 32) {
                     const uint32_t f = f0 + lane;
                     const bool act = f < total;
-                    // owner lane: the first lane whose inclusive count exceeds f (binary search)
-                    int lo = 0;
-#pragma unroll
-                    for (int step = 16; step; step >>= 1) {
-                        const uint32_t probe = __shfl_sync(0xffffffffu, incl, lo + step - 1);
-                        if (probe <= f) lo += step;
-                    }
-                    const uint32_t own_incl = __shfl_sync(0xffffffffu, incl, lo);
-                    const uint32_t own_nc = __shfl_sync(0xffffffffu, nc, lo);
-                    const uint32_t own_c0 = __shfl_sync(0xffffffffu, c0, lo);
-                    const uint32_t sc = own_c0 + (f - (own_incl - own_nc));
+                    // owner lane of position f: every listed source (a prefix of the lanes) owns
+                    // >= 1 position, so it is k0 (the owner of f0: the last source starting at or
+                    // before it) plus the number of sources starting in (f0, f] -- one ballot and
+                    // one OR-reduction of start bits instead of a 5-step binary search of shuffles
+                    const int k0 = 31 - __clz(__ballot_sync(0xffffffffu, has && excl <= f0));
+                    const uint32_t rel = excl - f0;
+                    const unsigned starts = __reduce_or_sync(0xffffffffu, has && excl > f0 && rel < 32u ? 1u << rel : 0u);
+                    const int own = (k0 + __popc(starts & ((2u << lane) - 2u))) & 31;
+                    const uint32_t own_excl = __shfl_sync(0xffffffffu, excl, own);
+                    const uint32_t own_c0 = __shfl_sync(0xffffffffu, c0, own);
+                    const uint32_t sc = own_c0 + (f - own_excl);
                     const int oc = act ? tc_classify(T, nT, v, sc, theta) : -1;
                     put(oc, sc, act, nxt, nnext);
                 }

@@ -194,6 +194,26 @@ def test_solve_host_matches_device(torch_cuda):
     np.testing.assert_array_equal(grad_h, grad_d.cpu().numpy())
 
 
+def test_unaligned_positions_same_result(torch_cuda):
+    """fp32 positions that are not 16-B aligned take the scalar gather (keys.cu), aligned ones the
+    float4-pair gather: the sorted bodies, hence every output, are bit-identical."""
+    torch = torch_cuda
+    from paper_1405_7487_b200 import FMM
+    n = 20000
+    pos, q = synth.generate("plummer", n, 93, np.float32)
+    tq = torch.from_numpy(q).cuda()
+    tp = torch.from_numpy(pos).cuda()
+    buf = torch.empty(3 * n + 1, dtype=torch.float32, device="cuda")
+    tpu = buf[1:].view(n, 3)
+    tpu.copy_(tp)
+    assert tp.data_ptr() % 16 == 0 and tpu.data_ptr() % 16 == 4
+    f = FMM(n, 10, 0.4, 64, "f32")
+    phi_a, grad_a = [t.cpu().numpy() for t in f.solve(tp, tq)]
+    phi_u, grad_u = [t.cpu().numpy() for t in f.solve(tpu, tq)]
+    np.testing.assert_array_equal(phi_a, phi_u)
+    np.testing.assert_array_equal(grad_a, grad_u)
+
+
 @pytest.mark.parametrize("prec,kind", [("f32", "cube"), ("f64", "plummer")])
 def test_solve_equals_build_evaluate(torch_cuda, prec, kind, monkeypatch):
     """fmm_solve (P2M/M2M on the aux stream during the traversal, L2L/L2P during P2P, far field
