@@ -146,6 +146,8 @@ fmm_status fmm_create(int64_t n_max, int p, double theta, int ncrit, int prec, i
         ctx->tc_scap = g17 ? atoi(g17) : 0;
         const char* g18 = getenv("FMM_TCT_TIGHT");
         ctx->tc_tight = g18 && g18[0] == '1';
+        const char* g19 = getenv("FMM_TCT_SKIP");
+        ctx->tc_force_skip = g19 && g19[0] == '1';
         const char* g21 = getenv("FMM_TREE_FAST");
         ctx->tree_fast = !(g21 && g21[0] == '0');
         const char* g22 = getenv("FMM_SORT_STAGED");

@@ -178,6 +178,8 @@ struct fmm_ctx {
     // (ping-pong CSR), global split lists of overflowed targets
     DevBuf tc_cnt, tc_voff, tc_lb, tc_d[2], tc_doff[2], tc_glob, tc_slab, tc_bsum;
     std::vector<std::array<uint32_t, 3>> tc_max;   // per-level max list lengths of the last build
+    std::vector<unsigned> tc_novf;                  // per-level overflowed targets of the last local build
+    bool tc_force_skip = false;                     // tests: skip the overflow kernels at every level (FMM_TCT_SKIP=1)
     std::vector<std::array<uint64_t, 3>> tc_tot;   // per-level list totals of the last build
     DevBuf tc_rec;                                  // per-level device records (bases, totals, maxima)
     std::vector<TcPart> tc_rem;                     // remote traversal parts (buffers reused)

@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
     uint8_t* __restrict__ ovf, uint32_t* __restrict__ ovf_list, unsigned* __restrict__ n_ovf,
     uint32_t* __restrict__ gscratch, int64_t gcap, uint32_t capM, uint32_t capP, uint32_t capD,
     unsigned* __restrict__ err, int S, uint64_t lenM = ~0ull, uint64_t lenP = ~0ull, uint64_t lenD = ~0ull,
-    uint32_t* __restrict__ mixflag = nullptr, int64_t band_lo = 0, int64_t band_hi = 0) {
+    uint32_t* __restrict__ mixflag = nullptr, int64_t band_lo = 0, int64_t band_hi = 0, bool ovf_redo = false) {
     constexpr bool EMIT = MODE != 0, COUNT = MODE != 1, SLAB = MODE == 2;
     // an earlier level outgrew the buffers sized from the previous build: the traversal is
     // redone, so stop here instead of reading incomplete pass-down sets
@@ -235,6 +235,9 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 8) k_tct_level(
         if (COUNT && mixflag && __any_sync(0xffffffffu, mix) && lane == 0) atomicOr(mixflag + t, 1u);
         if (COUNT && lane == 0) {
             if (over && !GLOB) {
+                // no overflow kernel follows this level (the previous build had none here): the
+                // traversal stops and is redone with them (tct_lists)
+                if (ovf_redo) atomicOr(err, 2u);
                 ovf[vi] = 1;
                 ovf_list[atomicAdd(n_ovf, 1u)] = (uint32_t)vi;
             }
@@ -414,7 +417,7 @@ __global__ void k_max3(const uint32_t* __restrict__ a, const uint32_t* __restric
 // (local: the root itself; remote: the roots of grafted LETs) into the CSR lists `o`.
 fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& seeds, TcLists& o, bool single,
                    std::vector<std::array<uint32_t, 3>>& tc_max, std::vector<std::array<uint64_t, 3>>& tc_tot,
-                   bool allow_fast, uint32_t* mixflag = nullptr) {
+                   bool allow_fast, uint32_t* mixflag = nullptr, std::vector<unsigned>* novf_hist = nullptr) {
     const int64_t nc = ctx->ncell;
     const int nlev = (int)ctx->depth + 1;
     const Cells v{P_<double4>(ctx->c_cr), P_<uint32_t>(ctx->c_cb), P_<uint32_t>(ctx->c_cc)};
@@ -520,6 +523,11 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
         uint32_t* slabD = slabP + (size_t)nv * capP;
         unsigned* n_ovf = d_novf + l;
         unsigned* mx = d_mx + 3 * l;
+        // the two overflow-kernel launches find nothing to do at a level where the previous build
+        // had no overflowed target (~4 us each at c2): skipped then, and an overflow that does
+        // appear stops the traversal for a redo with them (ovf_redo)
+        const bool skip_glob = fast && novf_hist &&
+                               (ctx->tc_force_skip || (l < (int)novf_hist->size() && (*novf_hist)[l] == 0));
         // sources of this level's targets that need no operand scaling: levels l-1 .. l+1
         const int64_t band_lo = ctx->level_begin[std::max(l - 1, 0)];
         const int64_t band_hi = ctx->level_begin[std::min(l + 2, nlev)];
@@ -529,20 +537,22 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
                                                               ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr, slabM,
                                                               slabP, slabD, ovf, ovf_list, n_ovf, nullptr, scap, capM,
                                                               capP, capD, d_err, Sl, ~0ull, ~0ull, ~0ull, mixflag,
-                                                              band_lo, band_hi);
+                                                              band_lo, band_hi, skip_glob);
         else
             k_tct_level<0, false><<<g, TC_WARPS * 32, 0, s>>>(tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds,
                                                               ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr,
                                                               nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, nullptr,
                                                               scap, 0, 0, 0, d_err, Sl, ~0ull, ~0ull, ~0ull, mixflag,
-                                                              band_lo, band_hi);
+                                                              band_lo, band_hi, skip_glob);
         FMM_LAUNCH(ctx);
         // overflowed targets (count read on the device: a no-op launch when there are none)
-        k_tct_level<0, true><<<gwarps / TC_WARPS, TC_WARPS * 32, 0, s>>>(
-            tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds, ctx->theta, cm, cp, cd, nullptr, nullptr, nullptr,
-            nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err, Sl,
-            ~0ull, ~0ull, ~0ull, mixflag, band_lo, band_hi);
-        FMM_LAUNCH(ctx);
+        if (!skip_glob) {
+            k_tct_level<0, true><<<gwarps / TC_WARPS, TC_WARPS * 32, 0, s>>>(
+                tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds, ctx->theta, cm, cp, cd, nullptr, nullptr,
+                nullptr, nullptr, nullptr, nullptr, ovf, ovf_list, n_ovf, P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err,
+                Sl, ~0ull, ~0ull, ~0ull, mixflag, band_lo, band_hi);
+            FMM_LAUNCH(ctx);
+        }
         // offsets written straight into m2l_off / p2p_off (+ the entries of earlier levels, a
         // device value) and the pass-down CSR of this level
         uint64_t* om = P_<uint64_t>(*o.off_m) + tb;
@@ -583,11 +593,13 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
                                                               0, 0, 0, d_err, Sl, lenM, lenP, lenD);
         }
         FMM_LAUNCH(ctx);
-        k_tct_level<1, true><<<gwarps / TC_WARPS, TC_WARPS * 32, 0, s>>>(
-            tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds, ctx->theta, cm, cp, cd, vm, vp, vd,
-            P_<uint32_t>(*o.src_m), P_<uint32_t>(*o.src_p), P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf,
-            P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err, Sl, lenM, lenP, lenD);
-        FMM_LAUNCH(ctx);
+        if (!skip_glob) {
+            k_tct_level<1, true><<<gwarps / TC_WARPS, TC_WARPS * 32, 0, s>>>(
+                tb, te, par, pb, doff_prev, dsrc_prev, v, d_seeds, nseeds, ctx->theta, cm, cp, cd, vm, vp, vd,
+                P_<uint32_t>(*o.src_m), P_<uint32_t>(*o.src_p), P_<uint32_t>(*dcur), ovf, ovf_list, n_ovf,
+                P_<uint32_t>(ctx->tc_glob), gcap, 0, 0, 0, d_err, Sl, lenM, lenP, lenD);
+            FMM_LAUNCH(ctx);
+        }
         // this level's pass-down offsets (od, nt + 1 entries) are the next level's input
         doff_prev = od;
         pb = tb;
@@ -599,6 +611,8 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
     std::vector<uint64_t> hbase(2 * (nlev + 1)), htot(3 * (size_t)nlev);
     std::vector<unsigned> hmx(3 * (size_t)nlev);
     unsigned herr = 0;
+    std::vector<unsigned> hnovf(nlev);
+    FMM_CUDA_TRY(ctx, cudaMemcpyAsync(hnovf.data(), d_novf, hnovf.size() * 4, cudaMemcpyDeviceToHost, s));
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(hbase.data(), d_base, hbase.size() * 8, cudaMemcpyDeviceToHost, s));
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(htot.data(), d_tot, htot.size() * 8, cudaMemcpyDeviceToHost, s));
     FMM_CUDA_TRY(ctx, cudaMemcpyAsync(hmx.data(), d_mx, hmx.size() * 4, cudaMemcpyDeviceToHost, s));
@@ -618,6 +632,7 @@ fmm_status tct_run(fmm_ctx* ctx, cudaStream_t s, const std::vector<uint32_t>& se
         }
     tc_max = maxc;
     tc_tot = totc;
+    if (novf_hist) *novf_hist = hnovf;   // (a stopped traversal's counts: the redo rewrites them)
     const uint64_t endM = hbase[2 * nlev], endP = hbase[2 * nlev + 1];
     *o.est_m = (int64_t)(endM + endM / 8 + 1024);
     *o.est_p = (int64_t)(endP + endP / 8 + 1024);
@@ -639,9 +654,9 @@ fmm_status tct_lists(fmm_ctx* ctx, cudaStream_t s) {
     uint32_t* mixflag = P_<uint32_t>(ctx->tc_mixflag);
     // (a redo after a short capacity guess revisits the same pairs: the flags are an OR)
     FMM_CUDA_TRY(ctx, cudaMemsetAsync(mixflag, 0, (size_t)ctx->ncell * 4, s));
-    fmm_status st = tct_run(ctx, s, seeds, o, ctx->tc_single, ctx->tc_max, ctx->tc_tot, true, mixflag);
+    fmm_status st = tct_run(ctx, s, seeds, o, ctx->tc_single, ctx->tc_max, ctx->tc_tot, true, mixflag, &ctx->tc_novf);
     if (st == FMM_ERR_OOM && ctx->err.empty())   // a capacity guess was short: sizes are known now
-        st = tct_run(ctx, s, seeds, o, ctx->tc_single, ctx->tc_max, ctx->tc_tot, false, mixflag);
+        st = tct_run(ctx, s, seeds, o, ctx->tc_single, ctx->tc_max, ctx->tc_tot, false, mixflag, &ctx->tc_novf);
     if (st == FMM_OK) ctx->tc_mix_ncell = ctx->ncell;
     return st;
 }

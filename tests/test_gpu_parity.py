@@ -293,6 +293,18 @@ def test_target_traversal_overflow_paths(torch_cuda, kind, monkeypatch):
             np.testing.assert_array_equal(a, b)
         np.testing.assert_array_equal(phi_a.cpu().numpy(), phi_b.cpu().numpy())
         np.testing.assert_array_equal(grad_a.cpu().numpy(), grad_b.cpu().numpy())
+    # the single pass without its overflow kernels (as after a build that had no overflowed target,
+    # FMM_TCT_SKIP=1 at every level): the overflows stop it and the redo gives the same lists
+    monkeypatch.delenv("FMM_TCT_TIGHT")
+    monkeypatch.setenv("FMM_TCT_SKIP", "1")
+    h = FMM(20000, 5, 0.5, 16, "f64")
+    for _ in range(3):
+        phi_c, grad_c = h.solve(tp, tq)
+        torch.cuda.synchronize()
+        for a, b in zip(f.lists(), h.lists()):
+            np.testing.assert_array_equal(a, b)
+        np.testing.assert_array_equal(phi_a.cpu().numpy(), phi_c.cpu().numpy())
+        np.testing.assert_array_equal(grad_a.cpu().numpy(), grad_c.cpu().numpy())
 
 
 def test_random_rebuilds_one_context(torch_cuda):
